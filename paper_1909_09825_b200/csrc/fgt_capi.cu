@@ -1,0 +1,700 @@
+// C ABI of the B200 SOE fast Gauss transform (include/fgt1d_b200.h).
+//
+// Plan / apply orchestration on the device.  Maps to the reference:
+//   fgt_plan_create    <- fgt::plan              proj/src/transform.cpp:200-219
+//   fgt_plan_gap_table <- precompute_gap_table   proj/src/transform.cpp:221-237
+//   fgt_apply_general  <- apply_general          proj/src/transform.cpp:249-253
+//   fgt_apply_same     <- apply_same             proj/src/transform.cpp:239-247
+//   fgt_direct         <- direct                 proj/src/transform.cpp:255-288
+//   fgt_mode_sums      <- detail::mode_sums      proj/src/transform.cpp:310-350
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fgt1d_b200.h"
+#include "fgt_scan.cuh"
+#include "fgt_soe.hpp"
+#include "fgt_sort.cuh"
+
+using namespace fgt_b200;
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+namespace fgt_b200 {
+void set_last_error(const std::string& m) { g_last_error = m; }
+}  // namespace fgt_b200
+
+extern "C" int fgt_gap_table_device(const double* d_sorted_targets, int64_t M, int ne,
+                                    const double* s_re, const double* s_im, double* out_host);
+
+namespace {
+
+struct ApiError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void raise(int code, const std::string& m) { throw ApiError{code, m}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();  // clear sticky-free errors
+    raise(e == cudaErrorMemoryAllocation ? FGT_ERR_NOMEM : FGT_ERR_CUDA,
+          std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return FGT_OK;
+  } catch (const ApiError& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const SoeError& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return FGT_ERR_NOMEM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return FGT_ERR_CUDA;
+  }
+}
+
+// Device context guard: a usable device is mandatory (no CPU fallback).
+void require_device(int device) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    raise(FGT_ERR_CUDA, "no CUDA device available: the B200 transform has no CPU fallback");
+  }
+  if (device >= 0) ck(cudaSetDevice(device), "cudaSetDevice");
+}
+
+template <class T>
+T* dmalloc(size_t n, cudaStream_t st) {
+  if (n == 0) n = 1;
+  void* p = nullptr;
+  ck(cudaMallocAsync(&p, n * sizeof(T), st), "cudaMallocAsync");
+  return static_cast<T*>(p);
+}
+void dfree(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
+Soe soe_from_arrays(const double* t_re, const double* t_im, const double* w_re, const double* w_im,
+                    const uint8_t* sc, int n, int form) {
+  if (n < 0) raise(FGT_ERR_INVALID, "negative SOE size");
+  if (n > 0 && (!t_re || !t_im || !w_re || !w_im))
+    raise(FGT_ERR_INVALID, "SOE arrays must not be NULL");
+  Soe s;
+  s.folded = form == FGT_SOE_FOLDED;
+  for (int k = 0; k < n; ++k) {
+    s.nodes.emplace_back(t_re[k], t_im[k]);
+    s.weights.emplace_back(w_re[k], w_im[k]);
+    if (s.folded) s.self_conj.push_back(sc ? sc[k] : (t_im[k] == 0.0 ? 1 : 0));
+  }
+  return s;
+}
+
+// Taylor degree thresholds: largest r with r^(D+1)/(D+1)! <= 2^-54.
+void fill_rmax(ModeParams& P) {
+  long double fact = 1.0L;
+  for (int D = 0; D <= kMaxDeg; ++D) {
+    fact *= (long double)(D + 1);
+    P.rmax[D] = (double)powl(fact * ldexpl(1.0L, -54), 1.0L / (long double)(D + 1));
+  }
+}
+
+// mode_coefs (transform.cpp:47-56): s_k = t_k * (1/sqrt(delta)) exactly as the
+// reference forms it, mw_k = m_k w_k; plus the Taylor coefficients of
+// exp(-s g) computed in extended precision.
+void build_modes(const Soe& folded, double delta, ModeParams& P, ModeTable& T) {
+  std::memset(&P, 0, sizeof(P));
+  std::memset(&T, 0, sizeof(T));
+  const int ne = (int)folded.nodes.size();
+  if (ne > kMaxModes)
+    raise(FGT_ERR_INVALID, "at most " + std::to_string(kMaxModes) + " folded SOE modes supported");
+  P.ne = ne;
+  const double isq = 1.0 / std::sqrt(delta);
+  double smax = 0.0;
+  for (int k = 0; k < ne; ++k) {
+    const double sre = folded.nodes[k].real() * isq;
+    const double sim = folded.nodes[k].imag() * isq;
+    const std::complex<double> mw = folded.multiplier(k) * folded.weights[k];
+    P.s_re[k] = sre;
+    P.s_im[k] = sim;
+    P.mw_re[k] = mw.real();
+    P.mw_im[k] = mw.imag();
+    T.s[k] = {sre, sim};
+    T.mw[k] = {mw.real(), mw.imag()};
+    smax = std::fmax(smax, std::hypot(sre, sim));
+    std::complex<long double> c(1.0L, 0.0L);
+    const std::complex<long double> ms(-(long double)sre, -(long double)sim);
+    for (int n = 0; n <= kMaxDeg; ++n) {
+      T.coef[k][n] = {(double)c.real(), (double)c.imag()};
+      c = c * ms / (long double)(n + 1);
+    }
+  }
+  P.smax = smax;
+  fill_rmax(P);
+}
+
+bool all_finite_host(const double* v, int64_t n) {
+  for (int64_t i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) return false;
+  return true;
+}
+
+}  // namespace
+
+struct fgt_plan_s {
+  int device = 0;
+  int64_t M = 0, N = 0;
+  double delta = 1.0;
+  Soe soe;  // folded
+  ModeParams P{};
+  ModeTable* d_mt = nullptr;
+  double* d_xs = nullptr;  // sorted targets
+  double* d_ys = nullptr;  // sorted sources
+  bool own_xs = true, own_ys = true;
+  int32_t* d_tperm = nullptr;  // nullptr: identity
+  int32_t* d_sperm = nullptr;
+  bool t_sorted = true, s_sorted = true;
+  bool same_points = false;
+  int64_t ntiles = 0;
+  int64_t* d_tile_ib = nullptr;
+  double zprev0 = 0.0;
+  int* d_flag = nullptr;
+};
+
+namespace {
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Uploads (or borrows) one coordinate set, checks finiteness, and sorts it.
+void prepare_set(const double* src, int64_t n, uint32_t flags, cudaStream_t st, int* d_flag,
+                 const char* what, double** d_sorted, bool* own, int32_t** d_perm,
+                 bool* was_sorted) {
+  *d_sorted = nullptr;
+  *d_perm = nullptr;
+  *own = true;
+  *was_sorted = true;
+  if (n == 0) return;
+  if (n >= ((int64_t)1 << 31)) raise(FGT_ERR_INVALID, std::string(what) + ": at most 2^31-1 points");
+  const bool dev = flags & FGT_DEVICE_PTRS;
+  if (!dev && !all_finite_host(src, n))
+    raise(FGT_ERR_DOMAIN, std::string(what) + " must be finite");
+  if (dev && (flags & FGT_ASSUME_SORTED) && (flags & FGT_BORROW)) {
+    int fin = 1;
+    ck(check_finite(src, n, d_flag, &fin, st), "check_finite");
+    if (!fin) raise(FGT_ERR_DOMAIN, std::string(what) + " must be finite");
+    *d_sorted = const_cast<double*>(src);
+    *own = false;
+    return;
+  }
+  double* d_in = dmalloc<double>(n, st);
+  ck(cudaMemcpyAsync(d_in, src, sizeof(double) * n,
+                     dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
+     "upload points");
+  if (dev) {
+    int fin = 1;
+    ck(check_finite(d_in, n, d_flag, &fin, st), "check_finite");
+    if (!fin) {
+      dfree(d_in, st);
+      raise(FGT_ERR_DOMAIN, std::string(what) + " must be finite");
+    }
+  }
+  int sorted = 1;
+  if (!(flags & FGT_ASSUME_SORTED)) ck(check_sorted(d_in, n, d_flag, &sorted, st), "check_sorted");
+  if (sorted) {
+    *d_sorted = d_in;
+    return;
+  }
+  *was_sorted = false;
+  double* d_out = dmalloc<double>(n, st);
+  int32_t* d_p = dmalloc<int32_t>(n, st);
+  void* ws = dmalloc<char>(radix_sort_workspace_bytes(n), st);
+  ck(radix_sort_with_perm(d_in, n, d_out, d_p, ws, st), "radix sort");
+  dfree(ws, st);
+  dfree(d_in, st);
+  *d_sorted = d_out;
+  *d_perm = d_p;
+}
+
+void finish_plan(fgt_plan_s* p, cudaStream_t st) {
+  const int64_t L = p->M + p->N;
+  p->ntiles = (L + kTile - 1) / kTile;
+  p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
+  ck(launch_partition(p->d_xs, p->M, p->d_ys, p->N, kTile, p->ntiles, p->d_tile_ib, st),
+     "partition");
+  ModeTable T;
+  build_modes(p->soe, p->delta, p->P, T);
+  p->d_mt = dmalloc<ModeTable>(1, st);
+  ck(cudaMemcpyAsync(p->d_mt, &T, sizeof(T), cudaMemcpyHostToDevice, st), "upload modes");
+  ck(cudaStreamSynchronize(st), "plan sync");
+}
+
+void destroy_plan(fgt_plan_s* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  cudaDeviceSynchronize();
+  if (p->own_xs) cudaFree(p->d_xs);
+  if (p->own_ys) cudaFree(p->d_ys);
+  cudaFree(p->d_tperm);
+  cudaFree(p->d_sperm);
+  cudaFree(p->d_tile_ib);
+  cudaFree(p->d_mt);
+  cudaFree(p->d_flag);
+  delete p;
+}
+
+Soe resolve_soe(const double* t_re, const double* t_im, const double* w_re, const double* w_im,
+                const uint8_t* sc, int n_modes, int form) {
+  Soe s = soe_from_arrays(t_re, t_im, w_re, w_im, sc, n_modes, form);
+  soe_validate(s);
+  return soe_fold(s);
+}
+
+void check_delta(double delta) {
+  if (!std::isfinite(delta) || !(delta > 0.0))
+    raise(FGT_ERR_DOMAIN, "delta must be positive and finite");
+}
+
+// Per-apply device workspace, stream ordered.
+struct Work {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  template <class T>
+  T* get(size_t n) {
+    T* p = dmalloc<T>(n, st);
+    ptrs.push_back(p);
+    return p;
+  }
+  ~Work() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
+struct ApplyCtx {
+  StreamArgs sa{};
+  TileState ts{};
+};
+
+// Strength upload + gather into sorted-source order, tile state allocation.
+ApplyCtx prepare_apply(fgt_plan_s* p, const double* strengths, uint32_t flags, Work& w) {
+  ApplyCtx c;
+  const bool dev = flags & FGT_DEVICE_PTRS;
+  const double* alpha = strengths;
+  if (!dev && p->N > 0) {
+    double* d = w.get<double>(p->N);
+    ck(cudaMemcpyAsync(d, strengths, sizeof(double) * p->N, cudaMemcpyHostToDevice, w.st),
+       "upload strengths");
+    alpha = d;
+  }
+  const double* bs = alpha;
+  if (p->d_sperm && p->N > 0) {
+    double* g = w.get<double>(p->N);
+    ck(launch_gather(alpha, p->d_sperm, p->N, g, w.st), "gather strengths");
+    bs = g;
+  }
+  c.sa = StreamArgs{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0};
+  const size_t nt = (size_t)p->ntiles * (size_t)p->P.ne;
+  cplx* block = w.get<cplx>(5 * nt);
+  c.ts = TileState{block, block + nt, block + 2 * nt, block + 3 * nt, block + 4 * nt};
+  return c;
+}
+
+void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint32_t flags,
+               cudaStream_t st, const cplx* carry_in_host, cplx* totals_host, bool finish) {
+  ck(cudaSetDevice(p->device), "cudaSetDevice");
+  const bool dev = flags & FGT_DEVICE_PTRS;
+  if (p->M == 0 && !totals_host) return;
+  Work w{st, {}};
+  double* u = potentials;
+  if (!dev && finish && p->M > 0) u = w.get<double>(p->M);
+  if (p->N == 0 && !totals_host) {
+    ck(cudaMemsetAsync(u, 0, sizeof(double) * p->M, st), "zero potentials");
+  } else {
+    ApplyCtx c = prepare_apply(p, strengths, flags, w);
+    const int ne = p->P.ne;
+    ck(launch_aggregate(c.sa, p->P, p->d_mt, c.ts, st), "tile aggregates");
+    cplx* d_cin = nullptr;
+    if (carry_in_host) {
+      d_cin = w.get<cplx>(2 * ne);
+      ck(cudaMemcpyAsync(d_cin, carry_in_host, sizeof(cplx) * 2 * ne, cudaMemcpyHostToDevice, st),
+         "carry in");
+    }
+    cplx* d_tot = nullptr;
+    if (totals_host) d_tot = w.get<cplx>(3 * ne);
+    ck(launch_carry_scan(c.ts, p->ntiles, ne, d_cin, d_tot, st), "carry scan");
+    if (totals_host) {
+      if (p->ntiles == 0) {
+        for (int k = 0; k < ne; ++k) {
+          totals_host[k] = {1.0, 0.0};
+          totals_host[ne + k] = {0.0, 0.0};
+          totals_host[2 * ne + k] = {0.0, 0.0};
+        }
+      } else {
+        ck(cudaMemcpyAsync(totals_host, d_tot, sizeof(cplx) * 3 * ne, cudaMemcpyDeviceToHost, st),
+           "totals");
+      }
+    }
+    if (finish && p->M > 0) {
+      OutArgs o;
+      o.u = u;
+      o.tperm = p->d_tperm;
+      o.u_offset = 0;
+      ck(launch_main(c.sa, p->P, p->d_mt, c.ts, o, st), "main pass");
+    }
+  }
+  if (!dev && finish && p->M > 0)
+    ck(cudaMemcpyAsync(potentials, u, sizeof(double) * p->M, cudaMemcpyDeviceToHost, st),
+       "download potentials");
+  if (!dev || totals_host) ck(cudaStreamSynchronize(st), "apply sync");
+}
+
+}  // namespace
+
+// ======================================================================= C
+
+extern "C" {
+
+const char* fgt_last_error(void) { return g_last_error.c_str(); }
+
+int fgt_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int fgt_cf_soe(int n, int folded, double* t_re, double* t_im, double* w_re, double* w_im,
+               uint8_t* self_conj) {
+  int count = 0;
+  int rc = guarded([&] {
+    Soe s = soe_cf(n);
+    if (folded) s = soe_fold(s);
+    count = (int)s.nodes.size();
+    for (int k = 0; k < count; ++k) {
+      if (t_re) t_re[k] = s.nodes[k].real();
+      if (t_im) t_im[k] = s.nodes[k].imag();
+      if (w_re) w_re[k] = s.weights[k].real();
+      if (w_im) w_im[k] = s.weights[k].imag();
+      if (self_conj) self_conj[k] = s.folded ? s.self_conj[k] : 0;
+    }
+  });
+  return rc == FGT_OK ? count : -rc;
+}
+
+int fgt_preset_mode_count(int p) {
+  switch (p) {  // transform.cpp:290-302
+    case 0: return 3;
+    case 1: return 4;
+    case 2: return 5;
+    case 3: return 6;
+    default:
+      g_last_error = "unknown precision preset";
+      return -FGT_ERR_DOMAIN;
+  }
+}
+
+int fgt_mode_count_for_tolerance(double tol) {
+  // proj/README.md:184-189 documented transform errors per preset
+  if (!(tol > 0.0) || !std::isfinite(tol)) {
+    g_last_error = "tolerance must be positive and finite";
+    return -FGT_ERR_DOMAIN;
+  }
+  if (tol >= 1e-3) return 3;
+  if (tol >= 1e-6) return 4;
+  if (tol >= 1e-8) return 5;
+  if (tol >= 1e-10) return 6;
+  if (tol >= 1e-11) return 7;
+  g_last_error = "tolerance below the reach of the double-precision CF tables";
+  return -FGT_ERR_DOMAIN;
+}
+
+int fgt_plan_create(const double* targets, int64_t M, const double* sources, int64_t N,
+                    double delta, const double* t_re, const double* t_im, const double* w_re,
+                    const double* w_im, const uint8_t* self_conj, int n_modes, int form,
+                    uint32_t flags, int device, void* stream, fgt_plan_t* out) {
+  return guarded([&] {
+    if (!out) raise(FGT_ERR_INVALID, "out must not be NULL");
+    *out = nullptr;
+    if (M < 0 || N < 0) raise(FGT_ERR_INVALID, "negative point count");
+    check_delta(delta);
+    Soe soe = resolve_soe(t_re, t_im, w_re, w_im, self_conj, n_modes, form);
+    require_device(device);
+    cudaStream_t st = as_stream(stream);
+    fgt_plan_s* p = new fgt_plan_s();
+    try {
+      ck(cudaGetDevice(&p->device), "cudaGetDevice");
+      p->M = M;
+      p->N = N;
+      p->delta = delta;
+      p->soe = soe;
+      ck(cudaMalloc(&p->d_flag, sizeof(int) * 4), "flag");
+      // finiteness of both sets first (the reference checks targets, then sources)
+      if (!(flags & FGT_DEVICE_PTRS)) {
+        if (!all_finite_host(targets, M)) raise(FGT_ERR_DOMAIN, "target coordinates must be finite");
+        if (!all_finite_host(sources, N)) raise(FGT_ERR_DOMAIN, "source coordinates must be finite");
+      }
+      prepare_set(targets, M, flags, st, p->d_flag, "target coordinates", &p->d_xs, &p->own_xs,
+                  &p->d_tperm, &p->t_sorted);
+      prepare_set(sources, N, flags, st, p->d_flag, "source coordinates", &p->d_ys, &p->own_ys,
+                  &p->d_sperm, &p->s_sorted);
+      // same_points: identical vectors as given (transform.cpp:214-216)
+      if (M == N) {
+        int eq = 1;
+        if (M > 0) {
+          if (flags & FGT_DEVICE_PTRS) {
+            ck(check_equal(targets, sources, M, p->d_flag, &eq, st), "same points");
+          } else {
+            for (int64_t i = 0; i < M; ++i)
+              if (!(targets[i] == sources[i])) {
+                eq = 0;
+                break;
+              }
+          }
+        }
+        p->same_points = eq != 0;
+      }
+      // coordinate before the first merged element: the element itself
+      double x0 = 0, y0 = 0;
+      if (M > 0) ck(cudaMemcpyAsync(&x0, p->d_xs, 8, cudaMemcpyDeviceToHost, st), "x0");
+      if (N > 0) ck(cudaMemcpyAsync(&y0, p->d_ys, 8, cudaMemcpyDeviceToHost, st), "y0");
+      ck(cudaStreamSynchronize(st), "sync");
+      p->zprev0 = (M > 0 && N > 0) ? std::fmin(x0, y0) : (M > 0 ? x0 : y0);
+      finish_plan(p, st);
+    } catch (...) {
+      destroy_plan(p);
+      throw;
+    }
+    *out = p;
+  });
+}
+
+int fgt_plan_create_chunk(const double* sorted_targets, int64_t M, const double* sorted_sources,
+                          int64_t N, double z_prev, int has_prev, double delta,
+                          const double* t_re, const double* t_im, const double* w_re,
+                          const double* w_im, const uint8_t* self_conj, int n_modes, int form,
+                          uint32_t flags, int device, void* stream, fgt_plan_t* out) {
+  int rc = fgt_plan_create(sorted_targets, M, sorted_sources, N, delta, t_re, t_im, w_re, w_im,
+                           self_conj, n_modes, form, flags | FGT_ASSUME_SORTED, device, stream,
+                           out);
+  if (rc != FGT_OK) return rc;
+  if (has_prev) (*out)->zprev0 = z_prev;
+  (*out)->same_points = false;
+  return FGT_OK;
+}
+
+void fgt_plan_destroy(fgt_plan_t plan) { destroy_plan(plan); }
+
+int fgt_plan_info(fgt_plan_t p, int64_t* M, int64_t* N, int* n_modes, int* same_points,
+                  int* tsorted, int* ssorted, int64_t* ntiles) {
+  return guarded([&] {
+    if (!p) raise(FGT_ERR_INVALID, "NULL plan");
+    if (M) *M = p->M;
+    if (N) *N = p->N;
+    if (n_modes) *n_modes = p->P.ne;
+    if (same_points) *same_points = p->same_points;
+    if (tsorted) *tsorted = p->t_sorted;
+    if (ssorted) *ssorted = p->s_sorted;
+    if (ntiles) *ntiles = p->ntiles;
+  });
+}
+
+int fgt_plan_copy_sorted(fgt_plan_t p, double* sx, int64_t* tperm, double* sy, int64_t* sperm) {
+  return guarded([&] {
+    if (!p) raise(FGT_ERR_INVALID, "NULL plan");
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    if (sx && p->M) ck(cudaMemcpy(sx, p->d_xs, 8 * p->M, cudaMemcpyDeviceToHost), "copy x");
+    if (sy && p->N) ck(cudaMemcpy(sy, p->d_ys, 8 * p->N, cudaMemcpyDeviceToHost), "copy y");
+    auto perm = [&](int32_t* d, int64_t n, int64_t* out) {
+      if (!out || n == 0) return;
+      if (!d) {
+        for (int64_t i = 0; i < n; ++i) out[i] = i;
+        return;
+      }
+      std::vector<int32_t> h(n);
+      ck(cudaMemcpy(h.data(), d, 4 * n, cudaMemcpyDeviceToHost), "copy perm");
+      for (int64_t i = 0; i < n; ++i) out[i] = h[i];
+    };
+    perm(p->d_tperm, p->M, tperm);
+    perm(p->d_sperm, p->N, sperm);
+  });
+}
+
+int fgt_plan_copy_soe(fgt_plan_t p, double* t_re, double* t_im, double* w_re, double* w_im,
+                      uint8_t* sc) {
+  return guarded([&] {
+    if (!p) raise(FGT_ERR_INVALID, "NULL plan");
+    for (size_t k = 0; k < p->soe.nodes.size(); ++k) {
+      if (t_re) t_re[k] = p->soe.nodes[k].real();
+      if (t_im) t_im[k] = p->soe.nodes[k].imag();
+      if (w_re) w_re[k] = p->soe.weights[k].real();
+      if (w_im) w_im[k] = p->soe.weights[k].imag();
+      if (sc) sc[k] = p->soe.self_conj[k];
+    }
+  });
+}
+
+int fgt_apply_general(fgt_plan_t p, const double* strengths, int64_t n_strengths,
+                      double* potentials, int num_threads, uint32_t flags, void* stream) {
+  (void)num_threads;  // results never depend on it (transform.hpp:60-64)
+  return guarded([&] {
+    if (!p) raise(FGT_ERR_INVALID, "NULL plan");
+    if (n_strengths != p->N)
+      raise(FGT_ERR_INVALID, "strengths length must match the planned source count");
+    run_apply(p, strengths, potentials, flags, as_stream(stream), nullptr, nullptr, true);
+  });
+}
+
+int fgt_apply_same(fgt_plan_t p, const double* strengths, int64_t n_strengths,
+                   double* potentials, int num_threads, uint32_t flags, void* stream) {
+  return guarded([&] {
+    if (!p) raise(FGT_ERR_INVALID, "NULL plan");
+    if (!p->same_points)
+      raise(FGT_ERR_INVALID,
+            "apply_same requires a plan built from identical target and source sets");
+    if (n_strengths != p->N)
+      raise(FGT_ERR_INVALID, "strengths length must match the planned source count");
+    // Same points: the merged stream puts every source before its equal
+    // target, so forward includes self and backward excludes it, exactly the
+    // run_mode_same split (transform.cpp:97-113).
+    (void)num_threads;
+    run_apply(p, strengths, potentials, flags, as_stream(stream), nullptr, nullptr, true);
+  });
+}
+
+int fgt_apply_chunk_aggregate(fgt_plan_t p, const double* strengths, double* agg_out,
+                              uint32_t flags, void* stream) {
+  return guarded([&] {
+    if (!p) raise(FGT_ERR_INVALID, "NULL plan");
+    run_apply(p, strengths, nullptr, flags, as_stream(stream), nullptr,
+              reinterpret_cast<cplx*>(agg_out), false);
+  });
+}
+
+int fgt_apply_chunk_finish(fgt_plan_t p, const double* strengths, const double* carry_in,
+                           double* potentials, uint32_t flags, void* stream) {
+  return guarded([&] {
+    if (!p) raise(FGT_ERR_INVALID, "NULL plan");
+    run_apply(p, strengths, potentials, flags, as_stream(stream),
+              reinterpret_cast<const cplx*>(carry_in), nullptr, true);
+  });
+}
+
+// Chunk g's forward carry is the forward state at its z_prev from all chunks
+// to its left: C+_g = A_{g-1} C+_{g-1} + F_{g-1}; the backward carry is the
+// backward state at its last element from all chunks to its right:
+// C-_g = A_{g+1} C-_{g+1} + G_{g+1}.  Each chunk's A already includes the gap
+// from the previous chunk's last element.
+int fgt_chunk_carries(const double* aggs, int n_chunks, int ne, double* carries_out) {
+  return guarded([&] {
+    if (n_chunks < 0 || ne < 0 || ne > kMaxModes) raise(FGT_ERR_INVALID, "bad sizes");
+    using C = std::complex<double>;
+    const C* a = reinterpret_cast<const C*>(aggs);
+    C* c = reinterpret_cast<C*>(carries_out);
+    for (int k = 0; k < ne; ++k) {
+      C f(0.0, 0.0);
+      for (int g = 0; g < n_chunks; ++g) {
+        c[g * 2 * ne + k] = f;
+        const C A = a[g * 3 * ne + k], F = a[g * 3 * ne + ne + k];
+        f = C(A.real() * f.real() - A.imag() * f.imag() + F.real(),
+              A.real() * f.imag() + A.imag() * f.real() + F.imag());
+      }
+      C b(0.0, 0.0);
+      for (int g = n_chunks - 1; g >= 0; --g) {
+        c[g * 2 * ne + ne + k] = b;
+        const C A = a[g * 3 * ne + k], G = a[g * 3 * ne + 2 * ne + k];
+        b = C(A.real() * b.real() - A.imag() * b.imag() + G.real(),
+              A.real() * b.imag() + A.imag() * b.real() + G.imag());
+      }
+    }
+  });
+}
+
+int fgt_gauss_transform(const double* targets, int64_t M, const double* sources, int64_t N,
+                        const double* strengths, double delta, const double* t_re,
+                        const double* t_im, const double* w_re, const double* w_im,
+                        const uint8_t* self_conj, int n_modes, int form, int ne, int threads,
+                        double* potentials) {
+  // pymodule.cpp:37-60: custom SOE (folded if full) or fold(cf_soe(2*ne)).
+  std::vector<double> tr, ti, wr, wi;
+  std::vector<uint8_t> sc;
+  if (n_modes <= 0) {
+    int cnt = fgt_cf_soe(2 * ne, 1, nullptr, nullptr, nullptr, nullptr, nullptr);
+    if (cnt < 0) return -cnt;
+    tr.resize(cnt), ti.resize(cnt), wr.resize(cnt), wi.resize(cnt), sc.resize(cnt);
+    fgt_cf_soe(2 * ne, 1, tr.data(), ti.data(), wr.data(), wi.data(), sc.data());
+    t_re = tr.data(), t_im = ti.data(), w_re = wr.data(), w_im = wi.data();
+    self_conj = sc.data();
+    n_modes = cnt;
+    form = FGT_SOE_FOLDED;
+  }
+  fgt_plan_t p = nullptr;
+  int rc = fgt_plan_create(targets, M, sources, N, delta, t_re, t_im, w_re, w_im, self_conj,
+                           n_modes, form, 0, -1, nullptr, &p);
+  if (rc != FGT_OK) return rc;
+  rc = p->same_points ? fgt_apply_same(p, strengths, N, potentials, threads, 0, nullptr)
+                      : fgt_apply_general(p, strengths, N, potentials, threads, 0, nullptr);
+  fgt_plan_destroy(p);
+  return rc;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- extras
+
+extern "C" int fgt_plan_gap_table(fgt_plan_t p, double* out) {
+  return guarded([&] {
+    if (!p) raise(FGT_ERR_INVALID, "NULL plan");
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    int rc = fgt_gap_table_device(p->d_xs, p->M, p->P.ne, p->P.s_re, p->P.s_im, out);
+    if (rc != FGT_OK) throw ApiError{rc, g_last_error};
+  });
+}
+
+extern "C" int fgt_mode_sums(fgt_plan_t p, const double* strengths, double* hp, double* hm) {
+  return guarded([&] {
+    if (!p) raise(FGT_ERR_INVALID, "NULL plan");
+    ck(cudaSetDevice(p->device), "cudaSetDevice");
+    cudaStream_t st = nullptr;
+    Work w{st, {}};
+    const int ne = p->P.ne;
+    const size_t cnt = (size_t)ne * (size_t)p->M;
+    cplx* d_hp = w.get<cplx>(cnt);
+    cplx* d_hm = w.get<cplx>(cnt);
+    if (p->N == 0 || p->M == 0) {
+      ck(cudaMemsetAsync(d_hp, 0, sizeof(cplx) * cnt, st), "zero");
+      ck(cudaMemsetAsync(d_hm, 0, sizeof(cplx) * cnt, st), "zero");
+    } else {
+      ApplyCtx c = prepare_apply(p, strengths, 0, w);
+      ck(launch_aggregate(c.sa, p->P, p->d_mt, c.ts, st), "aggregates");
+      ck(launch_carry_scan(c.ts, p->ntiles, ne, nullptr, nullptr, st), "carry scan");
+      OutArgs o;
+      o.hp = d_hp;
+      o.hm = d_hm;
+      ck(launch_mode_sums(c.sa, p->P, p->d_mt, c.ts, o, st), "mode sums");
+    }
+    if (cnt) {
+      ck(cudaMemcpyAsync(hp, d_hp, sizeof(cplx) * cnt, cudaMemcpyDeviceToHost, st), "hp");
+      ck(cudaMemcpyAsync(hm, d_hm, sizeof(cplx) * cnt, cudaMemcpyDeviceToHost, st), "hm");
+    }
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}

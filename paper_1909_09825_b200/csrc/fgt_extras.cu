@@ -1,0 +1,299 @@
+// Device kernels around the hot path:
+//   fgt_direct            <- fgt::direct (proj/src/transform.cpp:255-288): O(|S| N)
+//                            sum; long double in the reference, double-double here
+//   fgt_plan_gap_table    <- precompute_gap_table (transform.cpp:221-237)
+//   fgt_uniform_points_device <- rng::uniform_points (proj/src/rng.cpp:7-29)
+//   fgt_sort_device       <- sort_with_perm (transform.cpp:27-39)
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/fgt1d_b200.h"
+#include "fgt_device.cuh"
+#include "fgt_sort.cuh"
+
+using namespace fgt_b200;
+
+namespace fgt_b200 {
+void set_last_error(const std::string& m);  // fgt_capi.cu
+}
+
+namespace {
+
+struct ErrSink {
+  ErrSink& operator=(const std::string& m) {
+    set_last_error(m);
+    return *this;
+  }
+};
+ErrSink g_err;
+
+int cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();
+  g_err = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? FGT_ERR_NOMEM : FGT_ERR_CUDA;
+}
+
+#define CKR(expr, what)                          \
+  do {                                           \
+    cudaError_t e_ = (expr);                     \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+struct dd {
+  double hi, lo;
+};
+
+__device__ __forceinline__ dd two_sum(double a, double b) {
+  double s = a + b;
+  double bb = s - a;
+  double e = (a - (s - bb)) + (b - bb);
+  return {s, e};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  dd s = two_sum(a.hi, b.hi);
+  double lo = s.lo + a.lo + b.lo;
+  double hi = s.hi + lo;
+  return {hi, lo - (hi - s.hi)};
+}
+
+constexpr int kDirThreads = 256;
+constexpr int kDirPerThread = 32;
+constexpr int64_t kDirChunk = (int64_t)kDirThreads * kDirPerThread;
+
+// One block per (target, source chunk); deterministic in-order reduction.
+__global__ void __launch_bounds__(kDirThreads)
+    direct_partial_kernel(const double* __restrict__ x, const int64_t* __restrict__ subset,
+                          int64_t ntarg, const double* __restrict__ y,
+                          const double* __restrict__ a, int64_t N, double q_hi, double q_lo,
+                          int64_t nchunks, dd* __restrict__ partial) {
+  const int64_t t = blockIdx.x / nchunks;
+  const int64_t ch = blockIdx.x % nchunks;
+  const double xv = x[subset ? subset[t] : t];
+  dd acc = {0.0, 0.0};
+  const int64_t j0 = ch * kDirChunk;
+  for (int r = 0; r < kDirPerThread; ++r) {
+    const int64_t j = j0 + (int64_t)r * kDirThreads + threadIdx.x;
+    if (j >= N) break;
+    const double yv = y[j];
+    // d = x - y exactly (two-diff)
+    dd d = two_sum(xv, -yv);
+    // d^2 (double-double)
+    double p = d.hi * d.hi;
+    double pe = fma(d.hi, d.hi, -p) + 2.0 * d.hi * d.lo;
+    // arg = d^2 / (4 delta)
+    double ah = p * q_hi;
+    double al = fma(p, q_hi, -ah) + (pe * q_hi + p * q_lo);
+    dd arg = two_sum(ah, al);
+    if (arg.hi > 745.5) continue;
+    double eh = exp(-arg.hi);
+    double el = -eh * arg.lo;  // exp(-hi - lo) ~ eh (1 - lo)
+    const double av = a[j];
+    double th = eh * av;
+    double tl = fma(eh, av, -th) + el * av;
+    acc = dd_add(acc, dd{th, tl});
+  }
+  // block reduction (fixed order)
+  __shared__ dd sh[kDirThreads];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kDirThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = dd_add(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void direct_final_kernel(const dd* __restrict__ partial, int64_t ntarg,
+                                    int64_t nchunks, double* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ntarg) return;
+  dd acc = {0.0, 0.0};
+  for (int64_t c = 0; c < nchunks; ++c) acc = dd_add(acc, partial[t * nchunks + c]);
+  out[t] = acc.hi + acc.lo;
+}
+
+__global__ void gap_table_kernel(const double* __restrict__ xs, int64_t M, int ne,
+                                 const double* __restrict__ sre, const double* __restrict__ sim,
+                                 double2* __restrict__ out) {
+  const int64_t n = (M - 1) * ne;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx / (M - 1));
+    const int64_t i = idx % (M - 1);
+    const double d = xs[i + 1] - xs[i];
+    double2 r;
+    if (d == 0.0) {
+      r = make_double2(1.0, 0.0);
+    } else {
+      cplx e = decay_exact(sre[k], sim[k], d);
+      const double n2 = e.re * e.re + e.im * e.im;
+      if (n2 > 1.0) {
+        const double s = sqrt(n2);
+        e.re /= s;
+        e.im /= s;
+      }
+      r = make_double2(e.re, e.im);
+    }
+    out[idx] = r;
+  }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void uniform_kernel(double* __restrict__ out, int64_t n, uint64_t seed, uint64_t stream,
+                               uint64_t offset) {
+  const uint64_t base = mix64(seed ^ stream * 0xA24BAED4963EE407ull);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = mix64(base + ((uint64_t)i + offset) * 0x9E3779B97F4A7C15ull);
+    out[i] = (double)(r >> 11) * 0x1.0p-53;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int fgt_direct(const double* targets, int64_t M, const double* sources, int64_t N,
+               const double* strengths, double delta, const int64_t* subset, int64_t nsub,
+               double* out) {
+  if (!std::isfinite(delta) || !(delta > 0.0)) {
+    g_err = "delta must be positive and finite";
+    return FGT_ERR_DOMAIN;
+  }
+  for (int64_t i = 0; i < M; ++i)
+    if (!std::isfinite(targets[i])) {
+      g_err = "target coordinates must be finite";
+      return FGT_ERR_DOMAIN;
+    }
+  for (int64_t j = 0; j < N; ++j)
+    if (!std::isfinite(sources[j])) {
+      g_err = "source coordinates must be finite";
+      return FGT_ERR_DOMAIN;
+    }
+  const int64_t ntarg = (subset && nsub > 0) ? nsub : M;
+  if (subset && nsub > 0)
+    for (int64_t i = 0; i < nsub; ++i)
+      if (subset[i] < 0 || subset[i] >= M) {
+        g_err = "target subset index out of range";
+        return FGT_ERR_INVALID;
+      }
+  if (ntarg == 0) return FGT_OK;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    g_err = "no CUDA device available: the B200 transform has no CPU fallback";
+    return FGT_ERR_CUDA;
+  }
+  if (N == 0) {
+    for (int64_t i = 0; i < ntarg; ++i) out[i] = 0.0;
+    return FGT_OK;
+  }
+  // 0.25 / delta in double-double (reference: 0.25L / (long double)delta)
+  const long double q = 0.25L / (long double)delta;
+  const double q_hi = (double)q;
+  const double q_lo = (double)(q - (long double)q_hi);
+  const int64_t nchunks = (N + kDirChunk - 1) / kDirChunk;
+  double *dx = nullptr, *dy = nullptr, *da = nullptr, *dout = nullptr;
+  int64_t* ds = nullptr;
+  dd* dpart = nullptr;
+  int rc = FGT_OK;
+  cudaError_t e;
+#define CK2(expr, what)                 \
+  if ((e = (expr)) != cudaSuccess) {    \
+    rc = cuda_fail(e, what);            \
+    goto done;                          \
+  }
+  CK2(cudaMalloc(&dx, 8 * (M > 0 ? M : 1)), "malloc");
+  CK2(cudaMalloc(&dy, 8 * N), "malloc");
+  CK2(cudaMalloc(&da, 8 * N), "malloc");
+  CK2(cudaMalloc(&dout, 8 * ntarg), "malloc");
+  CK2(cudaMalloc(&dpart, sizeof(dd) * ntarg * nchunks), "malloc");
+  CK2(cudaMemcpy(dx, targets, 8 * M, cudaMemcpyHostToDevice), "copy");
+  CK2(cudaMemcpy(dy, sources, 8 * N, cudaMemcpyHostToDevice), "copy");
+  CK2(cudaMemcpy(da, strengths, 8 * N, cudaMemcpyHostToDevice), "copy");
+  if (subset && nsub > 0) {
+    CK2(cudaMalloc(&ds, 8 * nsub), "malloc");
+    CK2(cudaMemcpy(ds, subset, 8 * nsub, cudaMemcpyHostToDevice), "copy");
+  }
+  {
+    // grid.x limit is 2^31-1: process targets in batches
+    const int64_t max_blocks = (int64_t)1 << 30;
+    const int64_t tb = max_blocks / nchunks > 0 ? max_blocks / nchunks : 1;
+    for (int64_t t0 = 0; t0 < ntarg; t0 += tb) {
+      const int64_t nt = ntarg - t0 < tb ? ntarg - t0 : tb;
+      direct_partial_kernel<<<(unsigned)(nt * nchunks), kDirThreads>>>(
+          ds ? dx : dx + t0, ds ? ds + t0 : nullptr, nt, dy, da, N, q_hi, q_lo, nchunks,
+          dpart + t0 * nchunks);
+      CK2(cudaGetLastError(), "direct kernel");
+    }
+    direct_final_kernel<<<(unsigned)((ntarg + 255) / 256), 256>>>(dpart, ntarg, nchunks, dout);
+    CK2(cudaGetLastError(), "direct final");
+    CK2(cudaMemcpy(out, dout, 8 * ntarg, cudaMemcpyDeviceToHost), "copy out");
+  }
+done:
+  cudaFree(dx);
+  cudaFree(dy);
+  cudaFree(da);
+  cudaFree(dout);
+  cudaFree(ds);
+  cudaFree(dpart);
+#undef CK2
+  return rc;
+}
+
+int fgt_uniform_points_device(double* out_device, int64_t count, uint64_t seed, uint64_t stream,
+                              uint64_t offset, void* cuda_stream) {
+  if (count <= 0) return FGT_OK;
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  uniform_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)cuda_stream>>>(out_device, count, seed,
+                                                                         stream, offset);
+  CKR(cudaGetLastError(), "uniform kernel");
+  return FGT_OK;
+}
+
+int fgt_sort_device(const double* x, int64_t n, double* sorted, int32_t* perm, void* stream) {
+  if (n <= 0) return FGT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  void* ws = nullptr;
+  CKR(cudaMallocAsync(&ws, radix_sort_workspace_bytes(n), st), "sort workspace");
+  cudaError_t e = radix_sort_with_perm(x, n, sorted, perm, ws, st);
+  cudaFreeAsync(ws, st);
+  CKR(e, "radix sort");
+  return FGT_OK;
+}
+
+// Gap table of sorted targets, interleaved complex, mode-major:
+// out[(k*(M-1) + i)*2 + {0,1}].
+int fgt_gap_table_device(const double* d_sorted_targets, int64_t M, int ne, const double* s_re,
+                         const double* s_im, double* out_host) {
+  if (M < 2 || ne <= 0) return FGT_OK;
+  double *dsr = nullptr, *dsi = nullptr;
+  double2* dout = nullptr;
+  const int64_t n = (M - 1) * ne;
+  CKR(cudaMalloc(&dsr, 8 * ne), "malloc");
+  CKR(cudaMalloc(&dsi, 8 * ne), "malloc");
+  CKR(cudaMalloc(&dout, sizeof(double2) * n), "malloc");
+  CKR(cudaMemcpy(dsr, s_re, 8 * ne, cudaMemcpyHostToDevice), "copy");
+  CKR(cudaMemcpy(dsi, s_im, 8 * ne, cudaMemcpyHostToDevice), "copy");
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  gap_table_kernel<<<(unsigned)blocks, 256>>>(d_sorted_targets, M, ne, dsr, dsi, dout);
+  CKR(cudaGetLastError(), "gap table");
+  CKR(cudaMemcpy(out_host, dout, sizeof(double2) * n, cudaMemcpyDeviceToHost), "copy");
+  cudaFree(dsr);
+  cudaFree(dsi);
+  cudaFree(dout);
+  return FGT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,437 @@
+// Sort / permutation plumbing of plan(): the device replacement of
+// sort_with_perm (proj/src/transform.cpp:27-39, std::sort of (value, index)
+// pairs => ascending, ties in original order) and of the same-points test
+// (transform.cpp:214-216).
+//
+//   is_sorted       : skip the sort entirely when the input is already ordered
+//   radix sort      : stable LSD, 8-bit digits over order-preserving u64 keys
+//                     with a u32 index payload; passes whose digit is constant
+//                     across all keys are skipped (one global histogram pass)
+//   same_points     : element-wise equality of the two coordinate vectors
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fgt_sort.cuh"
+
+namespace fgt_b200 {
+
+namespace {
+
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kItems = 8;                                   // keys per lane per tile
+constexpr int kSortTile = kSortThreads * kItems;            // 2048 keys per CTA
+constexpr int kRadix = 256;
+
+// -0.0 and +0.0 compare equal in the reference's std::sort; canonicalise so
+// that both map to the same key (the stable index order then decides).
+__device__ __forceinline__ uint64_t key_of(double x) {
+  uint64_t k = (uint64_t)__double_as_longlong(x + 0.0);
+  return (k >> 63) ? ~k : (k | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double value_of(uint64_t k) {
+  k = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)k);
+}
+
+__global__ void make_keys_kernel(const double* __restrict__ x, int64_t n,
+                                 uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = key_of(__ldg(x + i));
+    vals[i] = (uint32_t)i;
+  }
+}
+
+__global__ void unkey_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                             int64_t n, double* __restrict__ sorted, int32_t* __restrict__ perm) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    sorted[i] = value_of(keys[i]);
+    perm[i] = (int32_t)vals[i];
+  }
+}
+
+// All 8 digit histograms in one read: hist8[pass][digit].
+__global__ void global_hist_kernel(const uint64_t* __restrict__ keys, int64_t n,
+                                   unsigned long long* __restrict__ hist8) {
+  __shared__ unsigned int h[8][kRadix];
+  for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[i];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xff], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) {
+    unsigned int v = (&h[0][0])[i];
+    if (v) atomicAdd(hist8 + i, (unsigned long long)v);
+  }
+}
+
+// Per-tile digit counts, digit-major: cnt[digit * ntiles + tile].
+__global__ void __launch_bounds__(kSortThreads)
+    tile_hist_kernel(const uint64_t* __restrict__ keys, int64_t n, int shift,
+                     uint32_t* __restrict__ cnt, int64_t ntiles) {
+  __shared__ unsigned int h[kRadix];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    int64_t i = base + it * kSortThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
+  }
+  __syncthreads();
+  cnt[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// Stable scatter.  Warp w owns tile keys [w*256, (w+1)*256) and ranks them in
+// order with __match_any_sync; warp counters are scanned digit-wise across
+// warps, keys are staged digit-sorted in shared memory and written out in
+// contiguous per-digit runs.
+__global__ void __launch_bounds__(kSortThreads)
+    scatter_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t n,
+                   int shift, const uint32_t* __restrict__ offs, int64_t ntiles,
+                   uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+  __shared__ unsigned int wc[kSortWarps][kRadix];
+  __shared__ unsigned int loff[kRadix];
+  __shared__ unsigned int goff[kRadix];
+  __shared__ uint64_t sk[kSortTile];
+  __shared__ uint32_t sv[kSortTile];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&wc[0][0])[i] = 0;
+  goff[threadIdx.x] = offs[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kSortTile;
+  const int64_t tn64 = n - base < kSortTile ? n - base : kSortTile;
+  const int tn = (int)tn64;
+  const unsigned lt = (1u << lane) - 1u;
+  uint64_t key[kItems];
+  uint32_t val[kItems];
+  int dig[kItems];
+  unsigned rank[kItems];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int li = warp * 32 * kItems + it * 32 + lane;  // tile-local index, in order
+    const bool ok = li < tn;
+    key[it] = ok ? kin[base + li] : 0ull;
+    val[it] = ok ? vin[base + li] : 0u;
+    const int d = ok ? (int)((key[it] >> shift) & 0xff) : -1;
+    dig[it] = d;
+    const unsigned active = __ballot_sync(0xffffffffu, ok);
+    unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (ok) {
+      peers &= active;
+      rank[it] = wc[warp][d] + __popc(peers & lt);
+    }
+    __syncwarp();
+    if (ok && (lane == __ffs(peers) - 1)) wc[warp][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {
+    const int d = threadIdx.x;
+    unsigned run = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+      unsigned c = wc[w][d];
+      wc[w][d] = run;
+      run += c;
+    }
+    loff[d] = run;  // tile total for digit d (scanned below)
+  }
+  __syncthreads();
+  // exclusive scan of loff over digits (256 entries, one per thread)
+  {
+    unsigned v = loff[threadIdx.x];
+    unsigned incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    __shared__ unsigned int wsum[kSortWarps];
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    unsigned wpre = 0;
+    for (int w = 0; w < warp; ++w) wpre += wsum[w];
+    __syncthreads();
+    loff[threadIdx.x] = wpre + incl - v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    if (dig[it] >= 0) {
+      const int d = dig[it];
+      const unsigned p = loff[d] + wc[warp][d] + rank[it];
+      sk[p] = key[it];
+      sv[p] = val[it];
+    }
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < tn; p += kSortThreads) {
+    const uint64_t k = sk[p];
+    const int d = (int)((k >> shift) & 0xff);
+    const int64_t o = (int64_t)goff[d] + (p - (int)loff[d]);
+    kout[o] = k;
+    vout[o] = sv[p];
+  }
+}
+
+// ---- generic exclusive scan of uint32 (values fit: counts <= 2^32) --------
+constexpr int kScanBlock = 1024;
+constexpr int kScanItems = 8;
+constexpr int kScanChunk = kScanBlock * kScanItems;
+
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* total) {
+  __shared__ unsigned ws[kScanBlock / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) ws[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned w = lane < kScanBlock / 32 ? ws[lane] : 0u;
+    unsigned wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < kScanBlock / 32) ws[lane] = wi - w;
+    if (lane == kScanBlock / 32 - 1) ws[kScanBlock / 32 - 1] = wi - w, *total = wi;
+  }
+  __syncthreads();
+  unsigned r = ws[warp] + incl - v;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kScanBlock)
+    scan_reduce_kernel(const uint32_t* __restrict__ in, int64_t n, uint32_t* __restrict__ sums) {
+  __shared__ unsigned tot;
+  const int64_t base = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kScanItems;
+  unsigned s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (base + i < n) s += in[base + i];
+  block_excl_scan(s, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kScanBlock)
+    scan_apply_kernel(const uint32_t* __restrict__ in, int64_t n,
+                      const uint32_t* __restrict__ block_off, uint32_t* __restrict__ out) {
+  __shared__ unsigned tot;
+  const int64_t base = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kScanItems;
+  unsigned v[kScanItems];
+  unsigned s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = base + i < n ? in[base + i] : 0u;
+    s += v[i];
+  }
+  unsigned run = block_excl_scan(s, &tot) + (block_off ? block_off[blockIdx.x] : 0u);
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) out[base + i] = run;
+    run += v[i];
+  }
+}
+
+// Exclusive scan, recursive over chunk sums.  tmp must hold scan_tmp_elems(n).
+cudaError_t excl_scan_u32(const uint32_t* in, int64_t n, uint32_t* out, uint32_t* tmp,
+                          cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t nb = (n + kScanChunk - 1) / kScanChunk;
+  if (nb == 1) {
+    scan_apply_kernel<<<1, kScanBlock, 0, st>>>(in, n, nullptr, out);
+    return cudaGetLastError();
+  }
+  uint32_t* sums = tmp;
+  uint32_t* sums_scanned = tmp + nb;
+  scan_reduce_kernel<<<(unsigned)nb, kScanBlock, 0, st>>>(in, n, sums);
+  cudaError_t e = excl_scan_u32(sums, nb, sums_scanned, tmp + 2 * nb, st);
+  if (e != cudaSuccess) return e;
+  scan_apply_kernel<<<(unsigned)nb, kScanBlock, 0, st>>>(in, n, sums_scanned, out);
+  return cudaGetLastError();
+}
+
+int64_t scan_tmp_elems(int64_t n) {
+  int64_t total = 0;
+  while (true) {
+    const int64_t nb = (n + kScanChunk - 1) / kScanChunk;
+    if (nb <= 1) break;
+    total += 2 * nb;
+    n = nb;
+  }
+  return total + 16;
+}
+
+__global__ void not_sorted_kernel(const double* __restrict__ x, int64_t n, int* __restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (__ldg(x + i) > __ldg(x + i + 1)) {
+      *flag = 1;
+      return;
+    }
+  }
+}
+
+__global__ void not_equal_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                 int64_t n, int* __restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!(__ldg(x + i) == __ldg(y + i))) {
+      *flag = 1;
+      return;
+    }
+  }
+}
+
+__global__ void nonfinite_kernel(const double* __restrict__ x, int64_t n, int* __restrict__ flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (!isfinite(__ldg(x + i))) {
+      *flag = 1;
+      return;
+    }
+  }
+}
+
+__global__ void iota_kernel(int32_t* __restrict__ p, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (int32_t)i;
+}
+
+inline unsigned grid_for(int64_t n, int bs) {
+  int64_t g = (n + bs - 1) / bs;
+  if (g > 148 * 32) g = 148 * 32;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+}  // namespace
+
+size_t radix_sort_workspace_bytes(int64_t n) {
+  const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+  size_t b = 0;
+  b += 2 * sizeof(uint64_t) * (size_t)n;                 // keys x2
+  b += 2 * sizeof(uint32_t) * (size_t)n;                 // vals x2
+  b += 2 * sizeof(uint32_t) * (size_t)(ntiles * kRadix); // cnt + offs
+  b += sizeof(uint32_t) * (size_t)scan_tmp_elems(ntiles * kRadix);
+  b += sizeof(unsigned long long) * 8 * kRadix;
+  return b + 1024;
+}
+
+static inline char* align_up(char* p) {
+  return (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255);
+}
+
+cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int32_t* perm,
+                                 void* workspace, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+  char* w = align_up((char*)workspace);
+  uint64_t* k0 = (uint64_t*)w; w = align_up(w + sizeof(uint64_t) * n);
+  uint64_t* k1 = (uint64_t*)w; w = align_up(w + sizeof(uint64_t) * n);
+  uint32_t* v0 = (uint32_t*)w; w = align_up(w + sizeof(uint32_t) * n);
+  uint32_t* v1 = (uint32_t*)w; w = align_up(w + sizeof(uint32_t) * n);
+  uint32_t* cnt = (uint32_t*)w; w = align_up(w + sizeof(uint32_t) * ntiles * kRadix);
+  uint32_t* offs = (uint32_t*)w; w = align_up(w + sizeof(uint32_t) * ntiles * kRadix);
+  uint32_t* stmp = (uint32_t*)w; w = align_up(w + sizeof(uint32_t) * scan_tmp_elems(ntiles * kRadix));
+  unsigned long long* hist8 = (unsigned long long*)w;
+
+  make_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, k0, v0);
+  cudaError_t e = cudaMemsetAsync(hist8, 0, sizeof(unsigned long long) * 8 * kRadix, st);
+  if (e != cudaSuccess) return e;
+  global_hist_kernel<<<grid_for(n, 256) < 1184 ? grid_for(n, 256) : 1184, 256, 0, st>>>(k0, n,
+                                                                                       hist8);
+  unsigned long long h8[8 * kRadix];
+  e = cudaMemcpyAsync(h8, hist8, sizeof(h8), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return e;
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return e;
+  uint64_t* kin = k0;
+  uint64_t* kout = k1;
+  uint32_t* vin = v0;
+  uint32_t* vout = v1;
+  for (int p = 0; p < 8; ++p) {
+    bool trivial = false;
+    for (int d = 0; d < kRadix; ++d)
+      if (h8[p * kRadix + d] == (unsigned long long)n) trivial = true;
+    if (trivial) continue;  // every key has the same digit: the pass is the identity
+    const int shift = 8 * p;
+    tile_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, n, shift, cnt, ntiles);
+    e = excl_scan_u32(cnt, ntiles * kRadix, offs, stmp, st);
+    if (e != cudaSuccess) return e;
+    scatter_kernel<<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, vin, n, shift, offs, ntiles,
+                                                              kout, vout);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    uint64_t* tk = kin; kin = kout; kout = tk;
+    uint32_t* tv = vin; vin = vout; vout = tv;
+  }
+  unkey_kernel<<<grid_for(n, 256), 256, 0, st>>>(kin, vin, n, sorted, perm);
+  return cudaGetLastError();
+}
+
+cudaError_t check_sorted(const double* x, int64_t n, int* d_flag, int* is_sorted,
+                         cudaStream_t st) {
+  *is_sorted = 1;
+  if (n < 2) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(d_flag, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  not_sorted_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, d_flag);
+  int h = 0;
+  e = cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return e;
+  e = cudaStreamSynchronize(st);
+  *is_sorted = h ? 0 : 1;
+  return e;
+}
+
+cudaError_t check_equal(const double* x, const double* y, int64_t n, int* d_flag, int* equal,
+                        cudaStream_t st) {
+  *equal = 1;
+  if (n < 1) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(d_flag, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  not_equal_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, y, n, d_flag);
+  int h = 0;
+  e = cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return e;
+  e = cudaStreamSynchronize(st);
+  *equal = h ? 0 : 1;
+  return e;
+}
+
+cudaError_t check_finite(const double* x, int64_t n, int* d_flag, int* finite, cudaStream_t st) {
+  *finite = 1;
+  if (n < 1) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(d_flag, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
+  nonfinite_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, d_flag);
+  int h = 0;
+  e = cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e != cudaSuccess) return e;
+  e = cudaStreamSynchronize(st);
+  *finite = h ? 0 : 1;
+  return e;
+}
+
+cudaError_t launch_iota(int32_t* p, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, n);
+  return cudaGetLastError();
+}
+
+}  // namespace fgt_b200

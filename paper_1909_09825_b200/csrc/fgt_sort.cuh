@@ -1,0 +1,21 @@
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace fgt_b200 {
+
+size_t radix_sort_workspace_bytes(int64_t n);
+// Stable ascending sort of x (n < 2^31) -> sorted values and the permutation
+// (sorted[i] == x[perm[i]]; ties keep original order, like the reference).
+cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int32_t* perm,
+                                 void* workspace, cudaStream_t st);
+cudaError_t check_sorted(const double* x, int64_t n, int* d_flag, int* is_sorted,
+                         cudaStream_t st);
+cudaError_t check_equal(const double* x, const double* y, int64_t n, int* d_flag, int* equal,
+                        cudaStream_t st);
+cudaError_t check_finite(const double* x, int64_t n, int* d_flag, int* finite, cudaStream_t st);
+cudaError_t launch_iota(int32_t* p, int64_t n, cudaStream_t st);
+
+}  // namespace fgt_b200

@@ -1,0 +1,252 @@
+"""Python host API of the transform path, mirroring the reference.
+
+C++ reference (proj/include/fgt1d/transform.hpp)      here
+  TransformRequest / TransformResult (:17-26)          TransformRequest / list of floats
+  TransformPlan (:32-47)                               TransformPlan (device plan handle)
+  plan(request, soe, precompute) (:53-54)              plan()
+  precompute_gap_table(plan) (:58)                     precompute_gap_table()
+  apply_same / apply_general (:65-75)                  apply_same() / apply_general()
+  direct(request, subset) (:80-81)                     direct()
+  preset_mode_count / preset_soe (:86-89)              soe.preset_mode_count / soe.preset_soe
+  detail::mode_sums (:101-102)                         mode_sums()
+Python binding (proj/bindings/pymodule.cpp)
+  gauss_transform (:37-60, :151-155)                   gauss_transform()
+  direct_transform (:62-72, :156-158)                  direct_transform()
+  uniform_points (:159-161)                            uniform_points()
+
+Every compute call goes through the C ABI (libfgt1d_b200.so) on the GPU.
+"""
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _capi
+from .soe import SoeApprox, SoeForm, cf_soe, fold, validate
+
+_PD = ctypes.POINTER(ctypes.c_double)
+_PI64 = ctypes.POINTER(ctypes.c_int64)
+_PU8 = ctypes.POINTER(ctypes.c_uint8)
+
+
+def _f64(a):
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64).reshape(-1))
+
+
+def _ptr(a):
+    return a.ctypes.data_as(_PD)
+
+
+@dataclass
+class TransformRequest:
+    targets: list = field(default_factory=list)
+    sources: list = field(default_factory=list)
+    strengths: list = field(default_factory=list)
+    delta: float = 1.0
+
+
+class TransformPlan:
+    """Device-resident plan: sorted copies, permutations, folded SOE, tile
+    partition.  Reusable across strength vectors (transform.hpp:28-31)."""
+
+    def __init__(self, handle, soe, delta, M, N):
+        self._h = handle
+        self.soe = soe
+        self.delta = delta
+        self._M, self._N = M, N
+        self.precomputed = False
+        self.gap_exponentials = []
+        self._sorted = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _capi.lib().fgt_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def _info(self):
+        M, N, ntiles = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        ne, same, ts, ss = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _capi.check(_capi.lib().fgt_plan_info(self._h, ctypes.byref(M), ctypes.byref(N),
+                                              ctypes.byref(ne), ctypes.byref(same),
+                                              ctypes.byref(ts), ctypes.byref(ss),
+                                              ctypes.byref(ntiles)))
+        return dict(M=M.value, N=N.value, n_modes=ne.value, same_points=bool(same.value),
+                    targets_were_sorted=bool(ts.value), sources_were_sorted=bool(ss.value),
+                    ntiles=ntiles.value)
+
+    @property
+    def same_points(self):
+        return self._info()["same_points"]
+
+    def _fetch_sorted(self):
+        if self._sorted is None:
+            sx = np.empty(self._M)
+            sy = np.empty(self._N)
+            tp = np.empty(self._M, dtype=np.int64)
+            sp = np.empty(self._N, dtype=np.int64)
+            _capi.check(_capi.lib().fgt_plan_copy_sorted(self._h, _ptr(sx), tp.ctypes.data_as(_PI64),
+                                                         _ptr(sy), sp.ctypes.data_as(_PI64)))
+            self._sorted = (sx, tp, sy, sp)
+        return self._sorted
+
+    @property
+    def sorted_targets(self):
+        return self._fetch_sorted()[0]
+
+    @property
+    def target_perm(self):
+        return self._fetch_sorted()[1]
+
+    @property
+    def sorted_sources(self):
+        return self._fetch_sorted()[2]
+
+    @property
+    def source_perm(self):
+        return self._fetch_sorted()[3]
+
+
+def _soe_args(soe):
+    tr, ti, wr, wi, sc = soe.arrays()
+    keep = (tr, ti, wr, wi, sc)
+    return keep, (_ptr(tr), _ptr(ti), _ptr(wr), _ptr(wi), sc.ctypes.data_as(_PU8), len(soe),
+                  int(soe.form))
+
+
+def plan(request, soe, precompute=False):
+    """fgt::plan (transform.cpp:200-219): validation order and error classes
+    follow the reference (ValueError for domain / invalid-argument errors)."""
+    x = _f64(request.targets)
+    y = _f64(request.sources)
+    a = _f64(request.strengths)
+    delta = float(request.delta)
+    if not (np.isfinite(delta) and delta > 0.0):
+        raise ValueError("delta must be positive and finite")
+    if not np.all(np.isfinite(x)):
+        raise ValueError("target coordinates must be finite")
+    if not np.all(np.isfinite(y)):
+        raise ValueError("source coordinates must be finite")
+    if a.size != y.size:
+        raise ValueError("one strength per source required")
+    validate(soe)
+    folded = soe if soe.form == SoeForm.FOLDED else fold(soe)
+    keep, sargs = _soe_args(folded)
+    h = ctypes.c_void_p()
+    _capi.check(_capi.lib().fgt_plan_create(_ptr(x), x.size, _ptr(y), y.size, delta, *sargs, 0, -1,
+                                            None, ctypes.byref(h)))
+    p = TransformPlan(h.value, folded, delta, x.size, y.size)
+    if precompute:
+        precompute_gap_table(p)
+    return p
+
+
+def precompute_gap_table(p):
+    """transform.cpp:221-237 -- API parity only; the device path forms gap
+    factors on the fly and never reads the table."""
+    if p.precomputed:
+        return
+    M, ne = p._M, len(p.soe)
+    if M >= 2 and ne > 0:
+        out = np.empty(2 * ne * (M - 1))
+        _capi.check(_capi.lib().fgt_plan_gap_table(p.handle, _ptr(out)))
+        p.gap_exponentials = (out[0::2] + 1j * out[1::2]).tolist()
+    p.precomputed = True
+
+
+def _apply(p, strengths, threads, same):
+    a = _f64(strengths)
+    out = np.empty(p._M)
+    fn = _capi.lib().fgt_apply_same if same else _capi.lib().fgt_apply_general
+    _capi.check(fn(p.handle, _ptr(a), a.size, _ptr(out), int(threads), 0, None))
+    return out
+
+
+def apply_general(p, strengths, num_threads=1):
+    return _apply(p, strengths, num_threads, False)
+
+
+def apply_same(p, strengths, num_threads=1):
+    return _apply(p, strengths, num_threads, True)
+
+
+def direct(request, target_subset=None):
+    """fgt::direct on the device (double-double accumulation)."""
+    x, y, a = _f64(request.targets), _f64(request.sources), _f64(request.strengths)
+    if a.size != y.size:
+        raise ValueError("one strength per source required")
+    sub = None if target_subset is None or len(target_subset) == 0 else np.ascontiguousarray(
+        np.asarray(target_subset, dtype=np.int64))
+    n = x.size if sub is None else sub.size
+    out = np.empty(n)
+    _capi.check(_capi.lib().fgt_direct(_ptr(x), x.size, _ptr(y), y.size, _ptr(a), float(request.delta),
+                                       None if sub is None else sub.ctypes.data_as(_PI64),
+                                       0 if sub is None else sub.size, _ptr(out)))
+    return out
+
+
+def mode_sums(p, strengths):
+    """detail::mode_sums: (hp, hm) as complex arrays [n_modes][M], sorted-target order."""
+    a = _f64(strengths)
+    if a.size != p._N:
+        raise ValueError("strengths length must match the planned source count")
+    ne, M = len(p.soe), p._M
+    hp = np.empty(2 * ne * M)
+    hm = np.empty(2 * ne * M)
+    _capi.check(_capi.lib().fgt_mode_sums(p.handle, _ptr(a), _ptr(hp), _ptr(hm)))
+    return ((hp[0::2] + 1j * hp[1::2]).reshape(ne, M), (hm[0::2] + 1j * hm[1::2]).reshape(ne, M))
+
+
+def gauss_transform(targets, sources, strengths, delta, soe=None, ne=4, threads=1):
+    """pymodule.cpp:37-60: plan(precompute) then apply_same / apply_general."""
+    req = TransformRequest(targets, sources, strengths, delta)
+    use = (soe if soe.form == SoeForm.FOLDED else fold(soe)) if soe is not None else fold(
+        cf_soe(2 * int(ne)))
+    p = plan(req, use, False)
+    res = apply_same(p, strengths, threads) if p.same_points else apply_general(p, strengths, threads)
+    return res.tolist()
+
+
+def direct_transform(targets, sources, strengths, delta):
+    return direct(TransformRequest(targets, sources, strengths, delta)).tolist()
+
+
+# -- counter RNG (rng.hpp:6-39, rng.cpp:7-29), vectorised ---------------------
+
+_GOLD = np.uint64(0x9E3779B97F4A7C15)
+
+
+def _mix64(z):
+    with np.errstate(over="ignore"):
+        z = z + _GOLD
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def counter_rand(seed, stream, i):
+    with np.errstate(over="ignore"):
+        base = _mix64(np.uint64(seed) ^ (np.uint64(stream) * np.uint64(0xA24BAED4963EE407)))
+        return _mix64(base + np.asarray(i, dtype=np.uint64) * _GOLD)
+
+
+def uniform_points_array(count, seed, stream=0, offset=0):
+    i = np.arange(offset, offset + count, dtype=np.uint64)
+    return (counter_rand(seed, stream, i) >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+
+def uniform_points(count, seed, stream=0):
+    return uniform_points_array(count, seed, stream).tolist()
+
+
+K_STREAM_SOURCES = 0
+K_STREAM_STRENGTHS = 1
+K_STREAM_EVAL_INDICES = 2
+K_STREAM_TARGETS = 3
