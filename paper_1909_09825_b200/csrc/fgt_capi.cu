@@ -9,8 +9,10 @@
 //   fgt_mode_sums      <- detail::mode_sums      proj/src/transform.cpp:310-350
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <complex>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -29,6 +31,13 @@ thread_local std::string g_last_error;
 
 namespace fgt_b200 {
 void set_last_error(const std::string& m) { g_last_error = m; }
+}  // namespace fgt_b200
+
+namespace {
+std::atomic<long long> g_launch_count{0};
+}
+namespace fgt_b200 {
+void note_launch(int n) { g_launch_count.fetch_add(n); }
 }  // namespace fgt_b200
 
 extern "C" int fgt_gap_table_device(const double* d_sorted_targets, int64_t M, int ne,
@@ -151,13 +160,13 @@ void build_modes(const Soe& folded, double delta, ModeParams& P, ModeTable& T) {
   fill_rmax(P);
 }
 
-bool all_finite_host(const double* v, int64_t n) {
-  for (int64_t i = 0; i < n; ++i)
-    if (!std::isfinite(v[i])) return false;
-  return true;
-}
-
 }  // namespace
+
+// Per-chunk persistent state for the two-phase (multi-GPU) apply.
+struct ChunkState {
+  double* bs = nullptr;  // strengths, sorted-source order
+  cplx* tile = nullptr;  // 5 * ne * ntiles
+};
 
 struct fgt_plan_s {
   int device = 0;
@@ -177,58 +186,90 @@ struct fgt_plan_s {
   int64_t* d_tile_ib = nullptr;
   double zprev0 = 0.0;
   int* d_flag = nullptr;
+  ChunkState cs;
 };
 
 namespace {
 
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// Uploads (or borrows) one coordinate set, checks finiteness, and sorts it.
-void prepare_set(const double* src, int64_t n, uint32_t flags, cudaStream_t st, int* d_flag,
-                 const char* what, double** d_sorted, bool* own, int32_t** d_perm,
-                 bool* was_sorted) {
+// ---- kernel-time profiling hook (bench.py roofline) -------------------------
+std::atomic<bool> g_profile{false};
+std::mutex g_prof_mu;
+struct ProfEv {
+  int kind;
+  cudaEvent_t a, b;
+};
+std::vector<ProfEv> g_prof_pending;
+double g_prof_ms[8] = {0};
+long long g_prof_cnt[8] = {0};
+
+struct ProfScope {
+  int kind;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(int k, cudaStream_t s) : kind(k), st(s) {
+    if (g_profile.load()) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEventRecord(b, st);
+      std::lock_guard<std::mutex> lk(g_prof_mu);
+      g_prof_pending.push_back({kind, a, b});
+    }
+  }
+};
+
+// Plan construction: device-resident originals -> all checks in one round
+// trip -> borrow / adopt / sort each set.
+struct SetSrc {
+  const double* dptr = nullptr;  // device copy of the input as given
+  bool tmp = false;              // dptr is a temporary we own
+};
+
+SetSrc stage_set(const double* src, int64_t n, uint32_t flags, cudaStream_t st) {
+  SetSrc r;
+  if (n == 0) return r;
+  if (flags & FGT_DEVICE_PTRS) {
+    r.dptr = src;
+    return r;
+  }
+  double* d = dmalloc<double>(n, st);
+  ck(cudaMemcpyAsync(d, src, sizeof(double) * n, cudaMemcpyHostToDevice, st), "upload points");
+  r.dptr = d;
+  r.tmp = true;
+  return r;
+}
+
+void adopt_set(const SetSrc& in, int64_t n, bool is_sorted, uint32_t flags, cudaStream_t st,
+               double** d_sorted, bool* own, int32_t** d_perm) {
   *d_sorted = nullptr;
   *d_perm = nullptr;
   *own = true;
-  *was_sorted = true;
   if (n == 0) return;
-  if (n >= ((int64_t)1 << 31)) raise(FGT_ERR_INVALID, std::string(what) + ": at most 2^31-1 points");
-  const bool dev = flags & FGT_DEVICE_PTRS;
-  if (!dev && !all_finite_host(src, n))
-    raise(FGT_ERR_DOMAIN, std::string(what) + " must be finite");
-  if (dev && (flags & FGT_ASSUME_SORTED) && (flags & FGT_BORROW)) {
-    int fin = 1;
-    ck(check_finite(src, n, d_flag, &fin, st), "check_finite");
-    if (!fin) raise(FGT_ERR_DOMAIN, std::string(what) + " must be finite");
-    *d_sorted = const_cast<double*>(src);
-    *own = false;
-    return;
-  }
-  double* d_in = dmalloc<double>(n, st);
-  ck(cudaMemcpyAsync(d_in, src, sizeof(double) * n,
-                     dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
-     "upload points");
-  if (dev) {
-    int fin = 1;
-    ck(check_finite(d_in, n, d_flag, &fin, st), "check_finite");
-    if (!fin) {
-      dfree(d_in, st);
-      raise(FGT_ERR_DOMAIN, std::string(what) + " must be finite");
+  if (is_sorted) {
+    if (in.tmp) {
+      *d_sorted = const_cast<double*>(in.dptr);
+    } else if (flags & FGT_BORROW) {
+      *d_sorted = const_cast<double*>(in.dptr);
+      *own = false;
+    } else {
+      double* d = dmalloc<double>(n, st);
+      ck(cudaMemcpyAsync(d, in.dptr, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
+      *d_sorted = d;
     }
-  }
-  int sorted = 1;
-  if (!(flags & FGT_ASSUME_SORTED)) ck(check_sorted(d_in, n, d_flag, &sorted, st), "check_sorted");
-  if (sorted) {
-    *d_sorted = d_in;
     return;
   }
-  *was_sorted = false;
   double* d_out = dmalloc<double>(n, st);
   int32_t* d_p = dmalloc<int32_t>(n, st);
   void* ws = dmalloc<char>(radix_sort_workspace_bytes(n), st);
-  ck(radix_sort_with_perm(d_in, n, d_out, d_p, ws, st), "radix sort");
+  ck(radix_sort_with_perm(in.dptr, n, d_out, d_p, ws, st), "radix sort");
   dfree(ws, st);
-  dfree(d_in, st);
+  if (in.tmp) dfree(const_cast<double*>(in.dptr), st);
   *d_sorted = d_out;
   *d_perm = d_p;
 }
@@ -243,6 +284,7 @@ void finish_plan(fgt_plan_s* p, cudaStream_t st) {
   build_modes(p->soe, p->delta, p->P, T);
   p->d_mt = dmalloc<ModeTable>(1, st);
   ck(cudaMemcpyAsync(p->d_mt, &T, sizeof(T), cudaMemcpyHostToDevice, st), "upload modes");
+  // the host ModeTable dies with this frame: make the copy complete
   ck(cudaStreamSynchronize(st), "plan sync");
 }
 
@@ -257,6 +299,8 @@ void destroy_plan(fgt_plan_s* p) {
   cudaFree(p->d_tile_ib);
   cudaFree(p->d_mt);
   cudaFree(p->d_flag);
+  cudaFree(p->cs.bs);
+  cudaFree(p->cs.tile);
   delete p;
 }
 
@@ -287,82 +331,128 @@ struct Work {
   }
 };
 
-struct ApplyCtx {
-  StreamArgs sa{};
-  TileState ts{};
-};
-
-// Strength upload + gather into sorted-source order, tile state allocation.
-ApplyCtx prepare_apply(fgt_plan_s* p, const double* strengths, uint32_t flags, Work& w) {
-  ApplyCtx c;
+// Strengths in sorted-source order (upload + gather as needed).
+const double* sorted_strengths(fgt_plan_s* p, const double* strengths, uint32_t flags, Work& w,
+                               double* into) {
   const bool dev = flags & FGT_DEVICE_PTRS;
   const double* alpha = strengths;
-  if (!dev && p->N > 0) {
-    double* d = w.get<double>(p->N);
+  if (p->N == 0) return alpha;
+  if (!dev) {
+    double* d = (p->d_sperm || !into) ? w.get<double>(p->N) : into;
     ck(cudaMemcpyAsync(d, strengths, sizeof(double) * p->N, cudaMemcpyHostToDevice, w.st),
        "upload strengths");
     alpha = d;
   }
-  const double* bs = alpha;
-  if (p->d_sperm && p->N > 0) {
-    double* g = w.get<double>(p->N);
+  if (p->d_sperm) {
+    double* g = into ? into : w.get<double>(p->N);
     ck(launch_gather(alpha, p->d_sperm, p->N, g, w.st), "gather strengths");
-    bs = g;
+    return g;
   }
-  c.sa = StreamArgs{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0};
-  const size_t nt = (size_t)p->ntiles * (size_t)p->P.ne;
-  cplx* block = w.get<cplx>(5 * nt);
-  c.ts = TileState{block, block + nt, block + 2 * nt, block + 3 * nt, block + 4 * nt};
-  return c;
+  if (into && alpha != into)
+    ck(cudaMemcpyAsync(into, alpha, sizeof(double) * p->N, cudaMemcpyDeviceToDevice, w.st), "copy");
+  return into ? into : alpha;
 }
 
+TileState tile_state(cplx* block, size_t nt) {
+  return TileState{block, block + nt, block + 2 * nt, block + 3 * nt, block + 4 * nt};
+}
+
+// apply_general / apply_same: K1 aggregates -> K2 carries -> K3 main.
 void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint32_t flags,
-               cudaStream_t st, const cplx* carry_in_host, cplx* totals_host, bool finish) {
+               cudaStream_t st) {
   ck(cudaSetDevice(p->device), "cudaSetDevice");
   const bool dev = flags & FGT_DEVICE_PTRS;
-  if (p->M == 0 && !totals_host) return;
+  if (p->M == 0) return;
   Work w{st, {}};
-  double* u = potentials;
-  if (!dev && finish && p->M > 0) u = w.get<double>(p->M);
-  if (p->N == 0 && !totals_host) {
+  double* u = dev ? potentials : w.get<double>(p->M);
+  if (p->N == 0) {
     ck(cudaMemsetAsync(u, 0, sizeof(double) * p->M, st), "zero potentials");
   } else {
-    ApplyCtx c = prepare_apply(p, strengths, flags, w);
-    const int ne = p->P.ne;
-    ck(launch_aggregate(c.sa, p->P, p->d_mt, c.ts, st), "tile aggregates");
-    cplx* d_cin = nullptr;
-    if (carry_in_host) {
-      d_cin = w.get<cplx>(2 * ne);
-      ck(cudaMemcpyAsync(d_cin, carry_in_host, sizeof(cplx) * 2 * ne, cudaMemcpyHostToDevice, st),
-         "carry in");
+    const double* bs = sorted_strengths(p, strengths, flags, w, nullptr);
+    const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0};
+    const size_t nt = (size_t)p->ntiles * (size_t)p->P.ne;
+    const TileState ts = tile_state(w.get<cplx>(5 * nt), nt);
+    {
+      ProfScope ps(0, st);
+      ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
     }
-    cplx* d_tot = nullptr;
-    if (totals_host) d_tot = w.get<cplx>(3 * ne);
-    ck(launch_carry_scan(c.ts, p->ntiles, ne, d_cin, d_tot, st), "carry scan");
-    if (totals_host) {
-      if (p->ntiles == 0) {
-        for (int k = 0; k < ne; ++k) {
-          totals_host[k] = {1.0, 0.0};
-          totals_host[ne + k] = {0.0, 0.0};
-          totals_host[2 * ne + k] = {0.0, 0.0};
-        }
-      } else {
-        ck(cudaMemcpyAsync(totals_host, d_tot, sizeof(cplx) * 3 * ne, cudaMemcpyDeviceToHost, st),
-           "totals");
-      }
+    {
+      ProfScope ps(1, st);
+      ck(launch_carry_scan(ts, p->ntiles, p->P.ne, nullptr, nullptr, st), "carry scan");
     }
-    if (finish && p->M > 0) {
-      OutArgs o;
-      o.u = u;
-      o.tperm = p->d_tperm;
-      o.u_offset = 0;
-      ck(launch_main(c.sa, p->P, p->d_mt, c.ts, o, st), "main pass");
+    OutArgs o;
+    o.u = u;
+    o.tperm = p->d_tperm;
+    {
+      ProfScope ps(2, st);
+      ck(launch_main(sa, p->P, p->d_mt, ts, o, st), "main pass");
     }
   }
-  if (!dev && finish && p->M > 0)
+  if (!dev) {
     ck(cudaMemcpyAsync(potentials, u, sizeof(double) * p->M, cudaMemcpyDeviceToHost, st),
        "download potentials");
-  if (!dev || totals_host) ck(cudaStreamSynchronize(st), "apply sync");
+    ck(cudaStreamSynchronize(st), "apply sync");
+  }
+}
+
+// Two-phase chunk apply.  Phase 1 keeps the sorted strengths and the tile
+// aggregates in the plan so phase 2 only runs the carry scan and K3.
+void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_host,
+                         uint32_t flags, cudaStream_t st) {
+  ck(cudaSetDevice(p->device), "cudaSetDevice");
+  const int ne = p->P.ne;
+  Work w{st, {}};
+  const size_t nt = (size_t)p->ntiles * (size_t)ne;
+  if (!p->cs.tile && nt) ck(cudaMalloc(&p->cs.tile, sizeof(cplx) * 5 * nt), "chunk state");
+  if (!p->cs.bs && p->N) ck(cudaMalloc(&p->cs.bs, sizeof(double) * p->N), "chunk state");
+  sorted_strengths(p, strengths, flags, w, p->cs.bs);
+  if (p->ntiles == 0) {
+    for (int k = 0; k < ne; ++k) {
+      totals_host[k] = {1.0, 0.0};
+      totals_host[ne + k] = {0.0, 0.0};
+      totals_host[2 * ne + k] = {0.0, 0.0};
+    }
+    ck(cudaStreamSynchronize(st), "sync");
+    return;
+  }
+  const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0};
+  const TileState ts = tile_state(p->cs.tile, nt);
+  ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
+  cplx* d_tot = w.get<cplx>(3 * ne);
+  ck(launch_carry_scan(ts, p->ntiles, ne, nullptr, d_tot, st), "chunk totals");
+  ck(cudaMemcpyAsync(totals_host, d_tot, sizeof(cplx) * 3 * ne, cudaMemcpyDeviceToHost, st),
+     "totals");
+  ck(cudaStreamSynchronize(st), "sync");
+}
+
+void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in_host, double* potentials,
+                      uint32_t flags, cudaStream_t st) {
+  ck(cudaSetDevice(p->device), "cudaSetDevice");
+  if (p->M == 0) return;
+  const bool dev = flags & FGT_DEVICE_PTRS;
+  const int ne = p->P.ne;
+  Work w{st, {}};
+  double* u = dev ? potentials : w.get<double>(p->M);
+  if (p->N == 0 && p->ntiles > 0 && !p->cs.tile)
+    raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
+  if (!p->cs.tile) raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
+  const size_t nt = (size_t)p->ntiles * (size_t)ne;
+  const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0};
+  const TileState ts = tile_state(p->cs.tile, nt);
+  cplx* d_cin = w.get<cplx>(2 * ne);
+  ck(cudaMemcpyAsync(d_cin, carry_in_host, sizeof(cplx) * 2 * ne, cudaMemcpyHostToDevice, st),
+     "carry in");
+  ck(launch_carry_scan(ts, p->ntiles, ne, d_cin, nullptr, st), "carry scan");
+  OutArgs o;
+  o.u = u;
+  o.tperm = p->d_tperm;
+  ck(launch_main(sa, p->P, p->d_mt, ts, o, st), "main pass");
+  if (!dev) {
+    ck(cudaMemcpyAsync(potentials, u, sizeof(double) * p->M, cudaMemcpyDeviceToHost, st),
+       "download potentials");
+  }
+  // carry_in_host was staged through pageable memory: complete before return
+  ck(cudaStreamSynchronize(st), "sync");
 }
 
 }  // namespace
@@ -440,46 +530,49 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
     require_device(device);
     cudaStream_t st = as_stream(stream);
     fgt_plan_s* p = new fgt_plan_s();
+    std::vector<void*> temps;
     try {
       ck(cudaGetDevice(&p->device), "cudaGetDevice");
       p->M = M;
       p->N = N;
       p->delta = delta;
       p->soe = soe;
-      ck(cudaMalloc(&p->d_flag, sizeof(int) * 4), "flag");
-      // finiteness of both sets first (the reference checks targets, then sources)
-      if (!(flags & FGT_DEVICE_PTRS)) {
-        if (!all_finite_host(targets, M)) raise(FGT_ERR_DOMAIN, "target coordinates must be finite");
-        if (!all_finite_host(sources, N)) raise(FGT_ERR_DOMAIN, "source coordinates must be finite");
+      if (M >= ((int64_t)1 << 31) || N >= ((int64_t)1 << 31))
+        raise(FGT_ERR_INVALID, "at most 2^31-1 points per set");
+      ck(cudaMalloc(&p->d_flag, sizeof(int) * 8), "flag");
+      ck(cudaMemsetAsync(p->d_flag, 0, sizeof(int) * 8, st), "flag");
+      SetSrc xs = stage_set(targets, M, flags, st);
+      if (xs.tmp) temps.push_back((void*)xs.dptr);
+      SetSrc ys = stage_set(sources, N, flags, st);
+      if (ys.tmp) temps.push_back((void*)ys.dptr);
+      // all structural checks in one device round trip
+      ck(launch_flag_nonfinite(xs.dptr, M, p->d_flag + 0, st), "finite");
+      ck(launch_flag_nonfinite(ys.dptr, N, p->d_flag + 1, st), "finite");
+      if (M == N) ck(launch_flag_unequal(xs.dptr, ys.dptr, M, p->d_flag + 2, st), "same points");
+      if (!(flags & FGT_ASSUME_SORTED)) {
+        ck(launch_flag_unsorted(xs.dptr, M, p->d_flag + 3, st), "sorted");
+        ck(launch_flag_unsorted(ys.dptr, N, p->d_flag + 4, st), "sorted");
       }
-      prepare_set(targets, M, flags, st, p->d_flag, "target coordinates", &p->d_xs, &p->own_xs,
-                  &p->d_tperm, &p->t_sorted);
-      prepare_set(sources, N, flags, st, p->d_flag, "source coordinates", &p->d_ys, &p->own_ys,
-                  &p->d_sperm, &p->s_sorted);
-      // same_points: identical vectors as given (transform.cpp:214-216)
-      if (M == N) {
-        int eq = 1;
-        if (M > 0) {
-          if (flags & FGT_DEVICE_PTRS) {
-            ck(check_equal(targets, sources, M, p->d_flag, &eq, st), "same points");
-          } else {
-            for (int64_t i = 0; i < M; ++i)
-              if (!(targets[i] == sources[i])) {
-                eq = 0;
-                break;
-              }
-          }
-        }
-        p->same_points = eq != 0;
-      }
+      int hf[8] = {0};
+      ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(hf), cudaMemcpyDeviceToHost, st), "flags");
+      ck(cudaStreamSynchronize(st), "flags sync");
+      // the reference checks targets, then sources (transform.cpp:202-204)
+      if (hf[0]) raise(FGT_ERR_DOMAIN, "target coordinates must be finite");
+      if (hf[1]) raise(FGT_ERR_DOMAIN, "source coordinates must be finite");
+      p->same_points = (M == N) && !hf[2];  // transform.cpp:214-216
+      p->t_sorted = !hf[3];
+      p->s_sorted = !hf[4];
+      temps.clear();  // ownership moves into adopt_set
+      adopt_set(xs, M, p->t_sorted, flags, st, &p->d_xs, &p->own_xs, &p->d_tperm);
+      adopt_set(ys, N, p->s_sorted, flags, st, &p->d_ys, &p->own_ys, &p->d_sperm);
       // coordinate before the first merged element: the element itself
       double x0 = 0, y0 = 0;
       if (M > 0) ck(cudaMemcpyAsync(&x0, p->d_xs, 8, cudaMemcpyDeviceToHost, st), "x0");
       if (N > 0) ck(cudaMemcpyAsync(&y0, p->d_ys, 8, cudaMemcpyDeviceToHost, st), "y0");
-      ck(cudaStreamSynchronize(st), "sync");
+      finish_plan(p, st);  // synchronizes
       p->zprev0 = (M > 0 && N > 0) ? std::fmin(x0, y0) : (M > 0 ? x0 : y0);
-      finish_plan(p, st);
     } catch (...) {
+      for (void* t : temps) cudaFreeAsync(t, st);
       destroy_plan(p);
       throw;
     }
@@ -559,7 +652,7 @@ int fgt_apply_general(fgt_plan_t p, const double* strengths, int64_t n_strengths
     if (!p) raise(FGT_ERR_INVALID, "NULL plan");
     if (n_strengths != p->N)
       raise(FGT_ERR_INVALID, "strengths length must match the planned source count");
-    run_apply(p, strengths, potentials, flags, as_stream(stream), nullptr, nullptr, true);
+    run_apply(p, strengths, potentials, flags, as_stream(stream));
   });
 }
 
@@ -576,7 +669,7 @@ int fgt_apply_same(fgt_plan_t p, const double* strengths, int64_t n_strengths,
     // target, so forward includes self and backward excludes it, exactly the
     // run_mode_same split (transform.cpp:97-113).
     (void)num_threads;
-    run_apply(p, strengths, potentials, flags, as_stream(stream), nullptr, nullptr, true);
+    run_apply(p, strengths, potentials, flags, as_stream(stream));
   });
 }
 
@@ -584,8 +677,8 @@ int fgt_apply_chunk_aggregate(fgt_plan_t p, const double* strengths, double* agg
                               uint32_t flags, void* stream) {
   return guarded([&] {
     if (!p) raise(FGT_ERR_INVALID, "NULL plan");
-    run_apply(p, strengths, nullptr, flags, as_stream(stream), nullptr,
-              reinterpret_cast<cplx*>(agg_out), false);
+    if (!agg_out) raise(FGT_ERR_INVALID, "agg_out must not be NULL");
+    run_chunk_aggregate(p, strengths, reinterpret_cast<cplx*>(agg_out), flags, as_stream(stream));
   });
 }
 
@@ -593,8 +686,10 @@ int fgt_apply_chunk_finish(fgt_plan_t p, const double* strengths, const double* 
                            double* potentials, uint32_t flags, void* stream) {
   return guarded([&] {
     if (!p) raise(FGT_ERR_INVALID, "NULL plan");
-    run_apply(p, strengths, potentials, flags, as_stream(stream),
-              reinterpret_cast<const cplx*>(carry_in), nullptr, true);
+    (void)strengths;  // kept from phase 1
+    if (!carry_in) raise(FGT_ERR_INVALID, "carry_in must not be NULL");
+    run_chunk_finish(p, reinterpret_cast<const cplx*>(carry_in), potentials, flags,
+                     as_stream(stream));
   });
 }
 
@@ -683,13 +778,16 @@ extern "C" int fgt_mode_sums(fgt_plan_t p, const double* strengths, double* hp, 
       ck(cudaMemsetAsync(d_hp, 0, sizeof(cplx) * cnt, st), "zero");
       ck(cudaMemsetAsync(d_hm, 0, sizeof(cplx) * cnt, st), "zero");
     } else {
-      ApplyCtx c = prepare_apply(p, strengths, 0, w);
-      ck(launch_aggregate(c.sa, p->P, p->d_mt, c.ts, st), "aggregates");
-      ck(launch_carry_scan(c.ts, p->ntiles, ne, nullptr, nullptr, st), "carry scan");
+      const double* bs = sorted_strengths(p, strengths, 0, w, nullptr);
+      const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0};
+      const size_t nt = (size_t)p->ntiles * (size_t)ne;
+      const TileState ts = tile_state(w.get<cplx>(5 * nt), nt);
+      ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "aggregates");
+      ck(launch_carry_scan(ts, p->ntiles, ne, nullptr, nullptr, st), "carry scan");
       OutArgs o;
       o.hp = d_hp;
       o.hm = d_hm;
-      ck(launch_mode_sums(c.sa, p->P, p->d_mt, c.ts, o, st), "mode sums");
+      ck(launch_mode_sums(sa, p->P, p->d_mt, ts, o, st), "mode sums");
     }
     if (cnt) {
       ck(cudaMemcpyAsync(hp, d_hp, sizeof(cplx) * cnt, cudaMemcpyDeviceToHost, st), "hp");
@@ -697,4 +795,34 @@ extern "C" int fgt_mode_sums(fgt_plan_t p, const double* strengths, double* hp, 
     }
     ck(cudaStreamSynchronize(st), "sync");
   });
+}
+
+// ---- instrumentation used by bench.py ------------------------------------
+
+extern "C" long long fgt_launch_counter(void) { return g_launch_count.load(); }
+
+extern "C" void fgt_profile_enable(int on) { g_profile.store(on != 0); }
+
+// ms[kind], counts[kind] for kind 0 = tile aggregates (K1), 1 = carry scan
+// (K2), 2 = main pass (K3); accumulated since the last read.  Synchronizes
+// on the recorded events.
+extern "C" int fgt_profile_read(double* ms, long long* counts, int nkinds) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& e : g_prof_pending) {
+    float t = 0.f;
+    cudaEventSynchronize(e.b);
+    cudaEventElapsedTime(&t, e.a, e.b);
+    g_prof_ms[e.kind] += t;
+    g_prof_cnt[e.kind] += 1;
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  g_prof_pending.clear();
+  for (int k = 0; k < nkinds && k < 8; ++k) {
+    if (ms) ms[k] = g_prof_ms[k];
+    if (counts) counts[k] = g_prof_cnt[k];
+    g_prof_ms[k] = 0.0;
+    g_prof_cnt[k] = 0;
+  }
+  return FGT_OK;
 }

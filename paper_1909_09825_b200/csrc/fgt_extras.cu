@@ -158,9 +158,53 @@ __global__ void uniform_kernel(double* __restrict__ out, int64_t n, uint64_t see
   }
 }
 
+// FP64 pipe probe: 8 independent DFMA chains per thread, fully unrolled.
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-9, x2 = x0 + 2e-9, x3 = x0 + 3e-9;
+  double x4 = x0 + 4e-9, x5 = x0 + 5e-9, x6 = x0 + 6e-9, x7 = x0 + 7e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  const double r = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+  if (r == 1.2345) out[0] = r;  // keep the chains alive
+}
+
 }  // namespace
 
 extern "C" {
+
+// Measured FP64 FMA throughput (TFLOP/s, FMA = 2 flops) of the current device
+// at its current clocks; used by bench.py as the fp64 roofline denominator.
+int fgt_fp64_peak(double* tflops, double* ms_out) {
+  int dev = 0, sms = 0;
+  CKR(cudaGetDevice(&dev), "device");
+  CKR(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "attr");
+  double* d = nullptr;
+  CKR(cudaMalloc(&d, 8), "malloc");
+  const int blocks = sms * 8, threads = 256, iters = 2048;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  fp64_probe_kernel<<<blocks, threads>>>(d, 64, 0.999999, 1e-7);  // warm-up
+  cudaEventRecord(e0);
+  fp64_probe_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+  cudaEventRecord(e1);
+  CKR(cudaEventSynchronize(e1), "probe");
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  const double fmas = (double)blocks * threads * iters * 16.0 * 8.0;
+  if (tflops) *tflops = 2.0 * fmas / (ms * 1e-3) / 1e12;
+  if (ms_out) *ms_out = ms;
+  return FGT_OK;
+}
+
 
 int fgt_direct(const double* targets, int64_t M, const double* sources, int64_t N,
                const double* strengths, double delta, const int64_t* subset, int64_t nsub,

@@ -14,6 +14,7 @@
 #include <math.h>
 
 #include "fgt_scan.cuh"
+#include "fgt_sort.cuh"
 
 namespace fgt_b200 {
 
@@ -554,6 +555,7 @@ cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int6
                              int64_t tile, int64_t ntiles, int64_t* tile_ib, cudaStream_t st) {
   const int64_t n = ntiles + 1;
   const int bs = 256;
+  note_launch();
   partition_kernel<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(xs, M, ys, N, tile, ntiles,
                                                                  tile_ib);
   return cudaGetLastError();
@@ -572,6 +574,7 @@ static cudaError_t launch_tile(const StreamArgs& a, const ModeParams& P, const M
     if (e != cudaSuccess) return e;
     configured[KIND] = true;
   }
+  note_launch();
   tile_kernel<KIND><<<(unsigned)a.ntiles, kThreads, smem, st>>>(a, P, mt, ts, o);
   return cudaGetLastError();
 }
@@ -594,6 +597,7 @@ cudaError_t launch_mode_sums(const StreamArgs& a, const ModeParams& P, const Mod
 cudaError_t launch_carry_scan(const TileState& ts, int64_t ntiles, int ne, const cplx* carry_in,
                               cplx* totals, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
+  note_launch();
   carry_scan_kernel<<<2 * ne, kScanThreads, 0, st>>>(ts, ntiles, ne, carry_in, totals);
   return cudaGetLastError();
 }
@@ -603,6 +607,7 @@ cudaError_t launch_gather(const double* alpha, const int32_t* perm, int64_t n, d
   if (n == 0) return cudaSuccess;
   int blocks = (int)((n + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
+  note_launch();
   gather_kernel<<<blocks, 256, 0, st>>>(alpha, perm, n, out);
   return cudaGetLastError();
 }

@@ -251,6 +251,7 @@ cudaError_t excl_scan_u32(const uint32_t* in, int64_t n, uint32_t* out, uint32_t
                           cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int64_t nb = (n + kScanChunk - 1) / kScanChunk;
+  note_launch(nb == 1 ? 1 : 2);
   if (nb == 1) {
     scan_apply_kernel<<<1, kScanBlock, 0, st>>>(in, n, nullptr, out);
     return cudaGetLastError();
@@ -350,6 +351,7 @@ cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int
   uint32_t* stmp = (uint32_t*)w; w = align_up(w + sizeof(uint32_t) * scan_tmp_elems(ntiles * kRadix));
   unsigned long long* hist8 = (unsigned long long*)w;
 
+  note_launch(2);
   make_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, k0, v0);
   cudaError_t e = cudaMemsetAsync(hist8, 0, sizeof(unsigned long long) * 8 * kRadix, st);
   if (e != cudaSuccess) return e;
@@ -370,6 +372,7 @@ cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int
       if (h8[p * kRadix + d] == (unsigned long long)n) trivial = true;
     if (trivial) continue;  // every key has the same digit: the pass is the identity
     const int shift = 8 * p;
+    note_launch(2);
     tile_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, n, shift, cnt, ntiles);
     e = excl_scan_u32(cnt, ntiles * kRadix, offs, stmp, st);
     if (e != cudaSuccess) return e;
@@ -380,6 +383,7 @@ cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int
     uint64_t* tk = kin; kin = kout; kout = tk;
     uint32_t* tv = vin; vin = vout; vout = tv;
   }
+  note_launch();
   unkey_kernel<<<grid_for(n, 256), 256, 0, st>>>(kin, vin, n, sorted, perm);
   return cudaGetLastError();
 }
@@ -426,6 +430,28 @@ cudaError_t check_finite(const double* x, int64_t n, int* d_flag, int* finite, c
   e = cudaStreamSynchronize(st);
   *finite = h ? 0 : 1;
   return e;
+}
+
+cudaError_t launch_flag_unsorted(const double* x, int64_t n, int* flag, cudaStream_t st) {
+  if (n < 2) return cudaSuccess;
+  note_launch();
+  not_sorted_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flag_unequal(const double* x, const double* y, int64_t n, int* flag,
+                                cudaStream_t st) {
+  if (n < 1) return cudaSuccess;
+  note_launch();
+  not_equal_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, y, n, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flag_nonfinite(const double* x, int64_t n, int* flag, cudaStream_t st) {
+  if (n < 1) return cudaSuccess;
+  note_launch();
+  nonfinite_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, flag);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_iota(int32_t* p, int64_t n, cudaStream_t st) {

@@ -6,6 +6,9 @@
 
 namespace fgt_b200 {
 
+// Launch accounting for bench.py's gpu_launches (fgt_capi.cu).
+void note_launch(int n = 1);
+
 size_t radix_sort_workspace_bytes(int64_t n);
 // Stable ascending sort of x (n < 2^31) -> sorted values and the permutation
 // (sorted[i] == x[perm[i]]; ties keep original order, like the reference).
@@ -16,6 +19,11 @@ cudaError_t check_sorted(const double* x, int64_t n, int* d_flag, int* is_sorted
 cudaError_t check_equal(const double* x, const double* y, int64_t n, int* d_flag, int* equal,
                         cudaStream_t st);
 cudaError_t check_finite(const double* x, int64_t n, int* d_flag, int* finite, cudaStream_t st);
+// Flag kernels (no sync): set *flag = 1 if the condition is found.
+cudaError_t launch_flag_unsorted(const double* x, int64_t n, int* flag, cudaStream_t st);
+cudaError_t launch_flag_unequal(const double* x, const double* y, int64_t n, int* flag,
+                                cudaStream_t st);
+cudaError_t launch_flag_nonfinite(const double* x, int64_t n, int* flag, cudaStream_t st);
 cudaError_t launch_iota(int32_t* p, int64_t n, cudaStream_t st);
 
 }  // namespace fgt_b200
