@@ -432,6 +432,8 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             es = float(t.item())
         # cross-check: e2e potentials equal the device-path potentials
+        one_step(args.delta)
+        torch.cuda.synchronize()
         same = bool(torch.equal(hu[:Mc], u[:Mc].cpu())) if Mc > 0 else True
         e2e = {"value": 2.0 * n / es, "unit": UNIT, "ms_per_step": es * 1e3,
                "h2d_bytes_per_step": int(8 * (Mc + 2 * Nc)) * world,

@@ -89,6 +89,20 @@ void require_device(int device) {
     raise(FGT_ERR_CUDA, "no CUDA device available: the B200 transform has no CPU fallback");
   }
   if (device >= 0) ck(cudaSetDevice(device), "cudaSetDevice");
+  // Keep stream-ordered allocations cached across plans/applies instead of
+  // returning them to the driver at every synchronization.
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  static std::once_flag once[64];
+  if (dev < 64)
+    std::call_once(once[dev], [dev] {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      cudaGetLastError();
+    });
 }
 
 template <class T>
