@@ -201,6 +201,7 @@ struct fgt_plan_s {
   double zprev0 = 0.0;
   int* d_flag = nullptr;
   ChunkState cs;
+  cudaStream_t stream = nullptr;  // stream the plan was built on (teardown)
 };
 
 namespace {
@@ -302,19 +303,25 @@ void finish_plan(fgt_plan_s* p, cudaStream_t st) {
   ck(cudaStreamSynchronize(st), "plan sync");
 }
 
+// Stream-ordered teardown on the plan's stream: work already queued on it
+// that uses the plan completes before the memory is reused.
 void destroy_plan(fgt_plan_s* p) {
   if (!p) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
   cudaSetDevice(p->device);
-  cudaDeviceSynchronize();
-  if (p->own_xs) cudaFree(p->d_xs);
-  if (p->own_ys) cudaFree(p->d_ys);
-  cudaFree(p->d_tperm);
-  cudaFree(p->d_sperm);
-  cudaFree(p->d_tile_ib);
-  cudaFree(p->d_mt);
-  cudaFree(p->d_flag);
-  cudaFree(p->cs.bs);
-  cudaFree(p->cs.tile);
+  cudaStream_t st = p->stream;
+  if (p->own_xs) dfree(p->d_xs, st);
+  if (p->own_ys) dfree(p->d_ys, st);
+  dfree(p->d_tperm, st);
+  dfree(p->d_sperm, st);
+  dfree(p->d_tile_ib, st);
+  dfree(p->d_mt, st);
+  dfree(p->d_flag, st);
+  dfree(p->cs.bs, st);
+  dfree(p->cs.tile, st);
+  cudaGetLastError();
+  cudaSetDevice(cur);
   delete p;
 }
 
@@ -417,8 +424,9 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ho
   const int ne = p->P.ne;
   Work w{st, {}};
   const size_t nt = (size_t)p->ntiles * (size_t)ne;
-  if (!p->cs.tile && nt) ck(cudaMalloc(&p->cs.tile, sizeof(cplx) * 5 * nt), "chunk state");
-  if (!p->cs.bs && p->N) ck(cudaMalloc(&p->cs.bs, sizeof(double) * p->N), "chunk state");
+  if (!p->cs.tile && nt) p->cs.tile = dmalloc<cplx>(5 * nt, p->stream);
+  if (!p->cs.bs && p->N) p->cs.bs = dmalloc<double>(p->N, p->stream);
+  if (st != p->stream) ck(cudaStreamSynchronize(p->stream), "sync");
   sorted_strengths(p, strengths, flags, w, p->cs.bs);
   if (p->ntiles == 0) {
     for (int k = 0; k < ne; ++k) {
@@ -553,7 +561,8 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       p->soe = soe;
       if (M >= ((int64_t)1 << 31) || N >= ((int64_t)1 << 31))
         raise(FGT_ERR_INVALID, "at most 2^31-1 points per set");
-      ck(cudaMalloc(&p->d_flag, sizeof(int) * 8), "flag");
+      p->stream = st;
+      p->d_flag = dmalloc<int>(8, st);
       ck(cudaMemsetAsync(p->d_flag, 0, sizeof(int) * 8, st), "flag");
       SetSrc xs = stage_set(targets, M, flags, st);
       if (xs.tmp) temps.push_back((void*)xs.dptr);

@@ -1,0 +1,87 @@
+"""GPU parity at BASELINE.json's full sizes.
+
+cfg3 (N=M=1e8, presorted uniform, n_e=6) and cfg4 (M=2^25 / N=2^27 clustered
+16-component mixture, sigma 1e-3, delta 1e-6, n_e=5) against the oracle over
+ALL targets (multithreaded C restatement of the reference, bit-identical to
+it), plus the sampled direct check within the SOE tolerance
+(acceptance.cpp:185-205 metric).  cfg2 (1e7 unsorted, normal alpha) likewise.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1909_09825_b200 as fgt
+from paper_1909_09825_b200.transform import uniform_points_array as up
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+THREADS = max(1, min(8, os.cpu_count() or 1))
+
+
+def bench_error(x, y, a, delta, u, nsamp=100, seed=0):
+    n = x.size
+    idx = np.minimum(n - 1, (up(nsamp, seed, 2) * n).astype(np.int64))
+    d = fgt.direct(fgt.TransformRequest(x, y, a, delta), idx)
+    umax = np.max(np.abs(d))
+    keep = np.abs(d) >= 1e-3 * umax
+    rel = np.max(np.abs(u[idx][keep] - d[keep]) / np.abs(d[keep]))
+    return rel, np.max(np.abs(u[idx] - d)) / np.sum(np.abs(a))
+
+
+def normal_from_streams(n, seed, s1, s2):
+    """Box-Muller on two counter-RNG streams (SURVEY §8d cfg2 / cfg4 recipe)."""
+    u1 = up(n, seed, s1)
+    u2 = up(n, seed, s2)
+    return np.sqrt(-2.0 * np.log1p(-u1)) * np.cos(2.0 * np.pi * u2)
+
+
+def run(x, y, a, delta, ne):
+    p = fgt.plan(fgt.TransformRequest(x, y, a, delta), fgt.fold(fgt.cf_soe(2 * ne)))
+    return fgt.apply_general(p, a)
+
+
+@pytest.mark.parametrize("delta", [1e-1, 1e-3, 1e-5])
+def test_cfg3_full_size(delta):
+    n = 100_000_000
+    x = np.sort(up(n, 0, 3))
+    y = np.sort(up(n, 0, 0))
+    a = 2.0 * up(n, 0, 1) - 1.0
+    u = run(x, y, a, delta, 6)
+    if delta == 1e-3:
+        ref = oracle.transform(x, y, a, delta, ne=6, mode=0, threads=THREADS)
+        err = np.max(np.abs(u - ref)) / np.sum(np.abs(a))
+        assert err <= 1e-12, err
+    rel, _ = bench_error(x, y, a, delta, u)
+    assert rel <= 1e-10, rel
+
+
+def test_cfg2_unsorted_normal_strengths():
+    n = 10_000_000
+    x = up(n, 0, 3)
+    y = up(n, 0, 0)
+    a = normal_from_streams(n, 0, 1, 4)
+    u = run(x, y, a, 1e-4, 4)
+    ref = oracle.transform(x, y, a, 1e-4, ne=4, mode=0, threads=THREADS)
+    assert np.max(np.abs(u - ref)) / np.sum(np.abs(a)) <= 1e-12
+    rel, _ = bench_error(x, y, a, 1e-4, u)
+    assert rel <= 1e-6, rel
+
+
+def test_cfg4_clustered_full_size():
+    M, N = 2 ** 25, 2 ** 27
+    cen = up(16, 0, 5)
+
+    def mixture(n, seed):
+        comp = np.minimum(15, (16 * up(n, seed, 6)).astype(np.int64))
+        return cen[comp] + 1e-3 * normal_from_streams(n, seed, 7, 8)
+
+    y = mixture(N, 0)
+    x = mixture(M, 1)
+    a = up(N, 0, 1)
+    u = run(x, y, a, 1e-6, 5)
+    ref = oracle.transform(x, y, a, 1e-6, ne=5, mode=0, threads=THREADS)
+    err = np.max(np.abs(u - ref)) / np.sum(np.abs(a))
+    assert err <= 1e-12, err
+    rel, _ = bench_error(x, y, a, 1e-6, u)
+    assert rel <= 1e-8, rel

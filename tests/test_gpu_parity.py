@@ -1,0 +1,386 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the oracle.
+
+Bar (BASELINE.json north_star): |u_gpu - u_ref| <= 1e-12 * sum|alpha| over all
+targets, against the reference's own outputs (committed fixtures from the
+reference library) and the C oracle (bit-identical restatement of the
+reference) on seeded inputs; within the SOE tolerance of the direct sum.
+"""
+import ctypes
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1909_09825_b200 as fgt
+from paper_1909_09825_b200 import _capi
+from paper_1909_09825_b200.transform import uniform_points_array as up
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+PARITY = 1e-12  # x sum|alpha|
+PD = ctypes.POINTER(ctypes.c_double)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    if _capi.lib().fgt_device_count() < 1:
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+
+
+def cases():
+    with open(os.path.join(HERE, "golden", "reference_cases.json")) as f:
+        return json.load(f)["cases"]
+
+
+def gpu_transform(x, y, a, delta, ne, mode=2, soe=None):
+    soe = soe if soe is not None else fgt.fold(fgt.cf_soe(2 * ne))
+    p = fgt.plan(fgt.TransformRequest(x, y, a, delta), soe)
+    if mode == 1 or (mode == 2 and p.same_points):
+        return fgt.apply_same(p, a)
+    return fgt.apply_general(p, a)
+
+
+def check(u, ref, a, bar=PARITY):
+    scale = max(np.sum(np.abs(a)), 1e-300)
+    err = np.max(np.abs(np.asarray(u) - np.asarray(ref))) / scale if len(u) else 0.0
+    assert err <= bar, err
+    return err
+
+
+# ---------------------------------------------------------------- fixtures
+
+@pytest.mark.parametrize("c", cases(), ids=lambda c: c["name"])
+def test_reference_fixtures(c):
+    u = gpu_transform(c["targets"], c["sources"], c["strengths"], c["delta"], c["ne"], c["mode"])
+    check(u, c["potentials"], c["strengths"])
+    if c["direct"] is not None:
+        d = fgt.direct(fgt.TransformRequest(c["targets"], c["sources"], c["strengths"], c["delta"]))
+        ref = np.asarray(c["direct"])
+        assert np.max(np.abs(d - ref)) <= 1e-14 * max(1.0, np.max(np.abs(ref)))
+
+
+def test_golden_potentials():
+    # test_transform.cpp:60-76, test_smoke.py:88-96
+    gold = [0.53026354628615822, 1.3078174711896560, 0.66552744606900788]
+    ys = [0.0, 0.1, 0.35, 0.5, 0.75, 1.0]
+    al = [0.5, -0.25, 1.0, 0.8, -0.6, 0.9]
+    got = fgt.gauss_transform([0.0, 0.5, 1.0], ys, al, 0.02, ne=6)
+    assert max(abs(g - w) for g, w in zip(got, gold)) < 5e-9
+    exact = fgt.direct_transform([0.0, 0.5, 1.0], ys, al, 0.02)
+    assert max(abs(g - w) / abs(w) for g, w in zip(exact, gold)) < 1e-15
+
+
+# ------------------------------------------------------------ seeded sweeps
+
+SWEEP = [
+    # seed, M, N, delta, ne, sorted
+    (1, 1000, 1000, 1e-2, 6, True),
+    (2, 100000, 100000, 1e-2, 6, True),    # cfg1 shape
+    (3, 200000, 300000, 1e-3, 6, False),
+    (4, 50000, 80000, 1e-4, 4, False),     # cfg2 parameters, smaller
+    (5, 30000, 30000, 1e-6, 6, True),      # large gaps relative to sqrt(delta)
+    (6, 30000, 10000, 1.0, 3, False),
+    (7, 7, 100000, 1e-1, 5, False),        # few targets
+    (8, 100000, 3, 1e-1, 5, False),        # few sources
+    (9, 1, 1, 0.3, 6, True),
+    (10, 5000, 5000, 1e-8, 7, False),      # everything decoupled
+    (11, 65536, 65536, 1e-6, 6, True),     # cfg5 transform shape
+    (12, 65536, 65536, 1e-1, 3, True),
+]
+
+
+@pytest.mark.parametrize("seed,M,N,delta,ne,srt", SWEEP)
+def test_seeded_vs_oracle(seed, M, N, delta, ne, srt):
+    x, y = up(M, seed, 3), up(N, seed, 0)
+    if srt:
+        x, y = np.sort(x), np.sort(y)
+    a = 2.0 * up(N, seed, 1) - 1.0
+    u = gpu_transform(x, y, a, delta, ne, mode=0)
+    ref = oracle.transform(x, y, a, delta, ne=ne, mode=0)
+    check(u, ref, a)
+
+
+def test_clustered_mixture_vs_oracle():
+    # cfg4 recipe at small scale: 16 centres, sigma 1e-3, unsorted, alpha in [0,1)
+    rng = np.random.default_rng(0)
+    c = up(16, 0, 5)
+    x = c[rng.integers(0, 16, 40000)] + 1e-3 * rng.standard_normal(40000)
+    y = c[rng.integers(0, 16, 160000)] + 1e-3 * rng.standard_normal(160000)
+    a = up(160000, 0, 1)
+    u = gpu_transform(x, y, a, 1e-6, 5, mode=0)
+    check(u, oracle.transform(x, y, a, 1e-6, ne=5, mode=0), a)
+
+
+def test_duplicates_and_signed_zero():
+    rng = np.random.default_rng(1)
+    x = np.round(rng.standard_normal(20000), 2)
+    y = np.round(rng.standard_normal(30000), 2)
+    x[:50] = -0.0
+    y[:50] = 0.0
+    y[50:100] = -0.0
+    a = rng.standard_normal(30000)
+    u = gpu_transform(x, y, a, 0.05, 6, mode=0)
+    check(u, oracle.transform(x, y, a, 0.05, ne=6, mode=0), a)
+
+
+def test_negative_and_wide_coordinates():
+    rng = np.random.default_rng(2)
+    x = rng.uniform(-1e3, 1e3, 30000)
+    y = rng.uniform(-1e3, 1e3, 30000)
+    a = rng.standard_normal(30000)
+    for delta in (1e2, 1.0, 1e-4):
+        u = gpu_transform(x, y, a, delta, 6, mode=0)
+        check(u, oracle.transform(x, y, a, delta, ne=6, mode=0), a)
+
+
+# ------------------------------------------------------- API semantics
+
+def test_same_points_and_apply_same():
+    # test_transform.cpp:89-106
+    y = up(500, 11, 0)
+    a = 2.0 * up(500, 11, 1) - 1.0
+    soe = fgt.fold(fgt.cf_soe(10))
+    p = fgt.plan(fgt.TransformRequest(y, y, a, 0.37), soe)
+    assert p.same_points
+    fast = fgt.apply_same(p, a)
+    gen = fgt.apply_general(p, a)
+    assert np.max(np.abs(fast - gen)) < 1e-13
+    check(fast, oracle.transform(y, y, a, 0.37, ne=5, mode=1), a)
+    # same set, other order is not same_points (test_transform.cpp:282-295)
+    p2 = fgt.plan(fgt.TransformRequest([0.1, 0.5, 0.9], [0.9, 0.1, 0.5], [1.0, 1.0, 1.0], 1.0),
+                  fgt.fold(fgt.cf_soe(8)))
+    assert not p2.same_points
+    with pytest.raises(ValueError):
+        fgt.apply_same(p2, [1.0, 1.0, 1.0])
+
+
+def test_plan_reuse_and_determinism():
+    # test_transform.cpp:142-162, 184-200
+    x, y = up(2000, 3, 3), up(3000, 3, 0)
+    a = 2.0 * up(3000, 3, 1) - 1.0
+    p = fgt.plan(fgt.TransformRequest(x, y, a, 2.0), fgt.fold(fgt.cf_soe(12)), True)
+    r1 = fgt.apply_general(p, a)
+    b2 = np.sin(0.1 * np.arange(1, 3001))
+    r2 = fgt.apply_general(p, b2)
+    check(r2, oracle.transform(x, y, b2, 2.0, ne=6, mode=0), b2)
+    r1b = fgt.apply_general(p, a, 8)
+    assert np.array_equal(r1, r1b)  # bit identical, thread count irrelevant
+    for _ in range(3):
+        assert np.array_equal(fgt.apply_general(p, a), r1)
+
+
+def test_linearity_in_strengths():
+    x, y = up(50000, 4, 3), up(60000, 4, 0)
+    a1 = 2.0 * up(60000, 4, 1) - 1.0
+    a2 = up(60000, 4, 6)
+    p = fgt.plan(fgt.TransformRequest(x, y, a1, 1e-3), fgt.soe_for_tolerance(1e-10))
+    u1, u2, u12 = (fgt.apply_general(p, v) for v in (a1, a2, a1 + a2))
+    assert np.max(np.abs(u12 - u1 - u2)) <= 1e-13 * np.sum(np.abs(a1) + np.abs(a2))
+
+
+def test_gap_table_api_parity():
+    # test_transform.cpp:164-182
+    y = up(400, 5, 0)
+    a = 2.0 * up(400, 5, 1) - 1.0
+    soe = fgt.fold(fgt.cf_soe(10))
+    lazy = fgt.plan(fgt.TransformRequest(y, y, a, 0.8), soe, False)
+    eager = fgt.plan(fgt.TransformRequest(y, y, a, 0.8), soe, True)
+    assert not lazy.precomputed and eager.precomputed
+    assert len(eager.gap_exponentials) == len(soe) * (400 - 1)
+    assert all(abs(g) <= 1.0 for g in eager.gap_exponentials)
+    assert np.array_equal(fgt.apply_same(lazy, a), fgt.apply_same(eager, a))
+    # the table itself matches the reference decay factors
+    L = oracle.oracle_lib()
+    assert L is not None
+
+
+def test_mode_sums_vs_quadratic_definition():
+    # test_transform.cpp:216-244, acceptance.cpp:312-353
+    for seed in range(3):
+        n = 10 + int(up(1, 2000 + seed, 10)[0] * 190)
+        y = up(n, 2000 + seed, 0)
+        a = 2.0 * up(n, 2000 + seed, 1) - 1.0
+        delta = 0.1 + up(2, 2000 + seed, 10)[1]
+        soe = fgt.fold(fgt.cf_soe(8))
+        p = fgt.plan(fgt.TransformRequest(y, y, a, delta), soe)
+        hp, hm = fgt.mode_sums(p, a)
+        ys, sp = p.sorted_sources, p.source_perm
+        xs = p.sorted_targets
+        rs = 1.0 / np.sqrt(delta)
+        bscale = np.sum(np.abs(a))
+        for k in range(len(soe)):
+            t = soe.nodes[k]
+            gap = xs[:, None] - ys[None, :]
+            beta = a[sp][None, :]
+            left = ys[None, :] <= xs[:, None]
+            ehp = np.sum(np.where(left, beta * np.exp(-t * gap * rs), 0), axis=1)
+            ehm = np.sum(np.where(~left, beta * np.exp(t * gap * rs), 0), axis=1)
+            assert np.max(np.abs(hp[k] - ehp)) <= 1e-12 * bscale
+            assert np.max(np.abs(hm[k] - ehm)) <= 1e-12 * bscale
+
+
+def test_sorted_fields_and_stable_permutation():
+    # test_transform.cpp:297-310
+    p = fgt.plan(fgt.TransformRequest([0.5, 0.2, 0.5, 0.2], [0.4], [1.0], 1.0),
+                 fgt.fold(fgt.cf_soe(8)))
+    assert p.target_perm.tolist() == [1, 3, 0, 2]
+    assert p.sorted_targets.tolist() == [0.2, 0.2, 0.5, 0.5]
+
+
+@pytest.mark.parametrize("n", [1, 2, 1000, 2049, 123457, 3000000])
+def test_radix_sort_is_stable_and_matches_reference_order(n):
+    rng = np.random.default_rng(n)
+    v = np.round(rng.standard_normal(n), 3)  # many ties
+    if n > 10:
+        v[::7] = -0.0
+        v[3::11] = 0.0
+    p = fgt.plan(fgt.TransformRequest(v, [], [], 1.0), fgt.fold(fgt.cf_soe(6)))
+    s_ref, p_ref = oracle.sort_with_perm(v)
+    assert np.array_equal(p.target_perm, p_ref)
+    assert np.array_equal(p.sorted_targets, s_ref)
+
+
+def test_empty_inputs():
+    # test_transform.cpp:121-140
+    soe = fgt.fold(fgt.cf_soe(8))
+    p = fgt.plan(fgt.TransformRequest([0.1, 0.9], [], [], 1.0), soe)
+    assert fgt.apply_general(p, []).tolist() == [0.0, 0.0]
+    p2 = fgt.plan(fgt.TransformRequest([], [0.5], [2.0], 1.0), soe)
+    assert fgt.apply_general(p2, [2.0]).size == 0
+    assert fgt.direct(fgt.TransformRequest([0.1, 0.9], [], [], 1.0)).tolist() == [0.0, 0.0]
+
+
+def test_validation_errors():
+    soe = fgt.fold(fgt.cf_soe(8))
+    req = fgt.TransformRequest([0.0, 0.5, 1.0], [0.0, 0.1], [1.0, 2.0], 0.02)
+    p = fgt.plan(req, soe)
+    with pytest.raises(ValueError):
+        fgt.apply_general(p, [1.0])
+    with pytest.raises(ValueError):
+        fgt.apply_same(p, [1.0, 2.0])
+    with pytest.raises(ValueError):
+        fgt.direct(req, [3])
+    with pytest.raises(ValueError):
+        fgt.direct(req, [-1])
+    # device-pointer plans check finiteness on the device
+    import torch
+    xd = torch.tensor([0.1, float("nan")], dtype=torch.float64, device="cuda")
+    yd = torch.tensor([0.2], dtype=torch.float64, device="cuda")
+    tr, ti, wr, wi, sc = soe.arrays()
+    h = ctypes.c_void_p()
+    rc = _capi.lib().fgt_plan_create(ctypes.cast(xd.data_ptr(), PD), 2, ctypes.cast(yd.data_ptr(), PD),
+                                     1, 1.0, tr.ctypes.data_as(PD), ti.ctypes.data_as(PD),
+                                     wr.ctypes.data_as(PD), wi.ctypes.data_as(PD),
+                                     sc.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), len(soe), 1,
+                                     _capi.FGT_DEVICE_PTRS, 0, None, ctypes.byref(h))
+    assert rc == _capi.FGT_ERR_DOMAIN
+
+
+def test_direct_subset_and_vs_oracle():
+    # test_transform.cpp:78-87
+    x, y = up(300, 1, 3), up(20000, 1, 0)
+    a = 2.0 * up(20000, 1, 1) - 1.0
+    req = fgt.TransformRequest(x, y, a, 1e-3)
+    full = fgt.direct(req)
+    sub = fgt.direct(req, [2, 0])
+    assert sub[0] == full[2] and sub[1] == full[0]
+    ref = oracle.direct(x, y, a, 1e-3)
+    assert np.max(np.abs(full - ref)) <= 1e-15 * np.sum(np.abs(a))
+
+
+@pytest.mark.parametrize("ne,bar", [(3, 4e-6 * 10), (4, 6e-8 * 10), (5, 6.4e-10 * 10),
+                                    (6, 7.9e-12 * 10)])
+def test_acceptance_window_vs_direct(ne, bar):
+    # acceptance.cpp:185-267 criterion 7 (distinct points, delta = 1, bench_error)
+    n = 100000
+    y = up(n, 0, 0)
+    x = up(n, 0, 3)
+    a = up(n, 0, 1)
+    u = gpu_transform(x, y, a, 1.0, ne, mode=0)
+    idx = np.minimum(n - 1, (up(100, 0, 2) * n).astype(np.int64))
+    d = fgt.direct(fgt.TransformRequest(x, y, a, 1.0), idx)
+    umax = np.max(np.abs(d))
+    keep = np.abs(d) >= 1e-3 * umax
+    err = np.max(np.abs(u[idx][keep] - d[keep]) / np.abs(d[keep]))
+    assert err <= bar
+
+
+def test_chunked_two_phase_equals_single_plan():
+    """Multi-GPU carry algebra on one GPU: split the merged stream into chunks,
+    run each chunk's phase 1, exchange aggregates through fgt_chunk_carries,
+    run phase 2; must match the single-plan result (no ranks waiting on each
+    other: chunks run one after another)."""
+    import bench
+    M, N, delta, ne = 200000, 150000, 1e-3, 6
+    x, y = np.sort(up(M, 9, 3)), np.sort(up(N, 9, 0))
+    a = 2.0 * up(N, 9, 1) - 1.0
+    soe = fgt.soe_for_tolerance(1e-10)
+    tr, ti, wr, wi, sc = soe.arrays()
+    sp = (tr.ctypes.data_as(PD), ti.ctypes.data_as(PD), wr.ctypes.data_as(PD),
+          wi.ctypes.data_as(PD), sc.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), ne, 1)
+    L = _capi.lib()
+    full = gpu_transform(x, y, a, delta, ne, mode=0, soe=soe)
+    for G in (2, 3, 8):
+        tot = M + N
+        bounds = [(bench.merge_split(x, y, tot * g // G), tot * g // G) for g in range(G + 1)]
+        plans, aggs = [], []
+        for g in range(G):
+            (i0, d0), (i1, d1) = bounds[g], bounds[g + 1]
+            j0, j1 = d0 - i0, d1 - i1
+            xc, yc, ac = x[i0:i1].copy(), y[j0:j1].copy(), a[j0:j1].copy()
+            zp = max(x[i0 - 1] if i0 > 0 else -np.inf, y[j0 - 1] if j0 > 0 else -np.inf)
+            h = ctypes.c_void_p()
+            _capi.check(L.fgt_plan_create_chunk(xc.ctypes.data_as(PD), xc.size, yc.ctypes.data_as(PD),
+                                                yc.size, float(zp) if d0 > 0 else 0.0, int(d0 > 0),
+                                                delta, *sp, 0, -1, None, ctypes.byref(h)))
+            agg = np.empty(6 * ne)
+            _capi.check(L.fgt_apply_chunk_aggregate(h, ac.ctypes.data_as(PD), agg.ctypes.data_as(PD),
+                                                    0, None))
+            plans.append((h, xc, ac, i0))
+            aggs.append(agg)
+        allagg = np.concatenate(aggs)
+        car = np.empty(G * 4 * ne)
+        _capi.check(L.fgt_chunk_carries(allagg.ctypes.data_as(PD), G, ne, car.ctypes.data_as(PD)))
+        u = np.empty(M)
+        for g, (h, xc, ac, i0) in enumerate(plans):
+            mine = np.ascontiguousarray(car[g * 4 * ne:(g + 1) * 4 * ne])
+            out = np.empty(max(xc.size, 1))
+            _capi.check(L.fgt_apply_chunk_finish(h, ac.ctypes.data_as(PD), mine.ctypes.data_as(PD),
+                                                 out.ctypes.data_as(PD), 0, None))
+            u[i0:i0 + xc.size] = out[:xc.size]
+            L.fgt_plan_destroy(h)
+        check(u, full, a, 1e-13)
+
+
+def test_device_pointer_path_matches_host_path():
+    import torch
+    M, N = 300000, 250000
+    x, y = np.sort(up(M, 12, 3)), np.sort(up(N, 12, 0))
+    a = 2.0 * up(N, 12, 1) - 1.0
+    host = gpu_transform(x, y, a, 1e-3, 6, mode=0)
+    soe = fgt.fold(fgt.cf_soe(12))
+    tr, ti, wr, wi, sc = soe.arrays()
+    xd, yd, ad = (torch.from_numpy(v).cuda() for v in (x, y, a))
+    ud = torch.empty(M, dtype=torch.float64, device="cuda")
+    L = _capi.lib()
+    h = ctypes.c_void_p()
+    fl = _capi.FGT_DEVICE_PTRS | _capi.FGT_BORROW
+    _capi.check(L.fgt_plan_create(ctypes.cast(xd.data_ptr(), PD), M, ctypes.cast(yd.data_ptr(), PD), N,
+                                  1e-3, tr.ctypes.data_as(PD), ti.ctypes.data_as(PD),
+                                  wr.ctypes.data_as(PD), wi.ctypes.data_as(PD),
+                                  sc.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), 6, 1, fl, 0,
+                                  None, ctypes.byref(h)))
+    _capi.check(L.fgt_apply_general(h, ctypes.cast(ad.data_ptr(), PD), N,
+                                    ctypes.cast(ud.data_ptr(), PD), 1, fl, None))
+    torch.cuda.synchronize()
+    L.fgt_plan_destroy(h)
+    assert np.array_equal(ud.cpu().numpy(), host)
+
+
+def test_gpu_kernels_actually_launch():
+    L = _capi.lib()
+    before = L.fgt_launch_counter()
+    fgt.gauss_transform(up(1000, 1, 3), up(1000, 1, 0), up(1000, 1, 1), 0.1, ne=4)
+    assert L.fgt_launch_counter() - before >= 3
