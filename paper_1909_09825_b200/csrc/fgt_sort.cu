@@ -330,7 +330,7 @@ size_t radix_sort_workspace_bytes(int64_t n) {
   b += 2 * sizeof(uint32_t) * (size_t)(ntiles * kRadix); // cnt + offs
   b += sizeof(uint32_t) * (size_t)scan_tmp_elems(ntiles * kRadix);
   b += sizeof(unsigned long long) * 8 * kRadix;
-  return b + 1024;
+  return b + 16 * 256;  // 8 regions, each re-aligned to 256 B
 }
 
 static inline char* align_up(char* p) {
