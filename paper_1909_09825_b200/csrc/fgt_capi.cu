@@ -291,9 +291,9 @@ void adopt_set(const SetSrc& in, int64_t n, bool is_sorted, uint32_t flags, cuda
 
 void finish_plan(fgt_plan_s* p, cudaStream_t st) {
   const int64_t L = p->M + p->N;
-  p->ntiles = (L + kTile - 1) / kTile;
+  p->ntiles = (L + kSeg - 1) / kSeg;
   p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
-  ck(launch_partition(p->d_xs, p->M, p->d_ys, p->N, kTile, p->ntiles, p->d_tile_ib, st),
+  ck(launch_partition(p->d_xs, p->M, p->d_ys, p->N, kSeg, p->ntiles, p->d_tile_ib, st),
      "partition");
   ModeTable T;
   build_modes(p->soe, p->delta, p->P, T);
@@ -374,9 +374,6 @@ const double* sorted_strengths(fgt_plan_s* p, const double* strengths, uint32_t 
   return into ? into : alpha;
 }
 
-TileState tile_state(cplx* block, size_t nt) {
-  return TileState{block, block + nt, block + 2 * nt, block + 3 * nt, block + 4 * nt};
-}
 
 // apply_general / apply_same: K1 aggregates -> K2 carries -> K3 main.
 void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint32_t flags,
@@ -391,8 +388,8 @@ void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint3
   } else {
     const double* bs = sorted_strengths(p, strengths, flags, w, nullptr);
     const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0};
-    const size_t nt = (size_t)p->ntiles * (size_t)p->P.ne;
-    const TileState ts = tile_state(w.get<cplx>(5 * nt), nt);
+    const TileState ts = tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, p->P.ne)),
+                                          p->ntiles, p->P.ne);
     {
       ProfScope ps(0, st);
       ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
@@ -423,8 +420,7 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ho
   ck(cudaSetDevice(p->device), "cudaSetDevice");
   const int ne = p->P.ne;
   Work w{st, {}};
-  const size_t nt = (size_t)p->ntiles * (size_t)ne;
-  if (!p->cs.tile && nt) p->cs.tile = dmalloc<cplx>(5 * nt, p->stream);
+  if (!p->cs.tile) p->cs.tile = dmalloc<cplx>(tile_state_elems(p->ntiles, ne), p->stream);
   if (!p->cs.bs && p->N) p->cs.bs = dmalloc<double>(p->N, p->stream);
   if (st != p->stream) ck(cudaStreamSynchronize(p->stream), "sync");
   sorted_strengths(p, strengths, flags, w, p->cs.bs);
@@ -438,7 +434,7 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ho
     return;
   }
   const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0};
-  const TileState ts = tile_state(p->cs.tile, nt);
+  const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
   ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
   cplx* d_tot = w.get<cplx>(3 * ne);
   ck(launch_carry_scan(ts, p->ntiles, ne, nullptr, d_tot, st), "chunk totals");
@@ -458,9 +454,8 @@ void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in_host, double* potentia
   if (p->N == 0 && p->ntiles > 0 && !p->cs.tile)
     raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
   if (!p->cs.tile) raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
-  const size_t nt = (size_t)p->ntiles * (size_t)ne;
   const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0};
-  const TileState ts = tile_state(p->cs.tile, nt);
+  const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
   cplx* d_cin = w.get<cplx>(2 * ne);
   ck(cudaMemcpyAsync(d_cin, carry_in_host, sizeof(cplx) * 2 * ne, cudaMemcpyHostToDevice, st),
      "carry in");
@@ -803,8 +798,8 @@ extern "C" int fgt_mode_sums(fgt_plan_t p, const double* strengths, double* hp, 
     } else {
       const double* bs = sorted_strengths(p, strengths, 0, w, nullptr);
       const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0};
-      const size_t nt = (size_t)p->ntiles * (size_t)ne;
-      const TileState ts = tile_state(w.get<cplx>(5 * nt), nt);
+      const TileState ts = tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, ne)),
+                                            p->ntiles, ne);
       ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "aggregates");
       ck(launch_carry_scan(ts, p->ntiles, ne, nullptr, nullptr, st), "carry scan");
       OutArgs o;

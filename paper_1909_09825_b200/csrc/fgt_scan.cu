@@ -1,15 +1,23 @@
 // Merged-stream SOE scan kernels (sm_100a).  Hot path of the fast Gauss
-// transform: replaces run_mode_general / apply_common of the reference
-// (proj/src/transform.cpp:119-149, 151-196).
+// transform: replaces run_mode_general / run_mode_same / apply_common of the
+// reference (proj/src/transform.cpp:97-149, 151-196).
 //
-//   K0 partition : merge-path split of the (targets, sources) stream into tiles
-//   K1 aggregate : per tile, per mode, the scan aggregate (A, F, G)
-//   K2 carry scan: exclusive scan of tile aggregates in both directions
-//   K3 main      : per tile, lane carries -> forward/backward recurrences ->
-//                  fused weighted real-part combine and scatter of u
+//   K0 partition : merge-path split of the (targets, sources) stream into
+//                  segments of kSeg merged elements (one warp each)
+//   K1 aggregate : per segment and mode, the scan aggregate (A, F, G) from the
+//                  real moments of the segment's sources (mode independent,
+//                  streamed once); exact per-element fallback for wide segments
+//   K2 carry scan: exclusive scan of the segment aggregates, both directions
+//                  (reduce / top / down-sweep)
+//   K3 main      : per warp: lane runs of kR merged elements in registers,
+//                  lane aggregates from lane moments, sequential lane carries,
+//                  forward/backward recurrences with the fused weighted
+//                  real-part combine, staged coalesced write / scatter of u
 //
-// Within a tile (CTA, kTile merged elements) each lane owns a run of kR
-// consecutive merged elements held in registers as (gap, weight) pairs.
+// Scan operator on (A, S): (A, S) then (A', S') = (A A', A' S + S').
+// Forward state at the element before a unit: Cf; after the unit it is
+// A Cf + F.  Backward state at the unit's last element: Cb; before the unit
+// (at the element preceding it) it is A Cb + G.
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -44,20 +52,46 @@ __device__ __forceinline__ int64_t merge_path(Ptr x, int64_t nx, Ptr y, int64_t 
   return lo;
 }
 
+// Coefficients of one mode: held in registers up to degree kRegDeg, read
+// from shared memory (broadcast) above it to bound register pressure.
+constexpr int kRegDeg = 8;
+
 template <int D>
-__device__ __forceinline__ cplx horner(const cplx (&c)[kMaxDeg + 1], double g) {
-  double pr = c[D].re, pi = c[D].im;
+struct Coef {
+  cplx c[(D >= 0 && D <= kRegDeg) ? D + 1 : 1];
+  const cplx* sm;
+  __device__ __forceinline__ void load(const ModeTable& mt, int k) {
+    sm = mt.coef[k];
+    if constexpr (D >= 0 && D <= kRegDeg) {
+#pragma unroll
+      for (int n = 0; n <= D; ++n) c[n] = sm[n];
+    }
+  }
+  __device__ __forceinline__ cplx operator[](int n) const {
+    if constexpr (D >= 0 && D <= kRegDeg) {
+      return c[n];
+    } else {
+      return sm[n];
+    }
+  }
+};
+
+template <int D>
+__device__ __forceinline__ cplx horner(const Coef<D>& c, double g) {
+  cplx t = c[D];
+  double pr = t.re, pi = t.im;
 #pragma unroll
   for (int n = D - 1; n >= 0; --n) {
-    pr = fma(pr, g, c[n].re);
-    pi = fma(pi, g, c[n].im);
+    const cplx cn = c[n];
+    pr = fma(pr, g, cn.re);
+    pi = fma(pi, g, cn.im);
   }
   return {pr, pi};
 }
 
-// Gap factor for mode coefficients c (fast path, degree D) or exact (D < 0).
+// Gap factor exp(-s g): Taylor polynomial of degree D (fast path) or exact.
 template <int D>
-__device__ __forceinline__ cplx gap_factor(const cplx (&c)[kMaxDeg + 1], cplx s, double g) {
+__device__ __forceinline__ cplx gap_factor(const Coef<D>& c, cplx s, double g) {
   if constexpr (D >= 0) {
     return horner<D>(c, g);
   } else {
@@ -65,155 +99,109 @@ __device__ __forceinline__ cplx gap_factor(const cplx (&c)[kMaxDeg + 1], cplx s,
   }
 }
 
-template <int D>
-__device__ __forceinline__ void load_coef(const ModeTable& mt, int k, cplx (&c)[kMaxDeg + 1]) {
-  if constexpr (D >= 0) {
+__device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
-    for (int n = 0; n <= D; ++n) c[n] = mt.coef[k][n];
-  }
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
 }
 
-// Pass 1: lane-run aggregates for every mode, carries in = 0.
-//   A = prod d_i, F = forward state at the run end, G = backward state at the
-//   element before the run.
-template <int D>
-__device__ __forceinline__ void pass1(const ModeTable& mt, int ne, const double (&g)[kR],
-                                   const double (&b)[kR], LaneAgg* out) {
-  for (int k = 0; k < ne; ++k) {
-    cplx c[kMaxDeg + 1];
-    load_coef<D>(mt, k, c);
-    const cplx s = mt.s[k];
-    cplx F = {0.0, 0.0}, P = {1.0, 0.0}, G = {0.0, 0.0};
-#pragma unroll
-    for (int i = 0; i < kR; ++i) {
-      cplx d = gap_factor<D>(c, s, g[i]);
-      F = cmad(d, F, cplx{b[i], 0.0});
-      P = cmul(P, d);
-      G.re = fma(b[i], P.re, G.re);
-      G.im = fma(b[i], P.im, G.im);
-    }
-    out[k] = LaneAgg{P, F, G};
-  }
+__device__ __forceinline__ void load_mode_table(const ModeTable* g, ModeTable& s) {
+  const double* src = reinterpret_cast<const double*>(g);
+  double* dst = reinterpret_cast<double*>(&s);
+  constexpr int n = sizeof(ModeTable) / sizeof(double);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
 
-// Pass 2: forward and backward recurrences seeded with the lane carries,
-// accumulating Re(mw_k (H + K)) into out[] (only target slots are used).
-// MS (mode-sums test hook, detail::mode_sums transform.cpp:310-350): instead
-// store H (= h+) and K (= h-) of every target, per mode, to ms.
-struct ModeSumsOut {
-  cplx* hp;  // [ne][M]
-  cplx* hm;
-  int64_t M;
-  int64_t t0;  // global sorted index of this lane's first target
-};
+// ---------------------------------------------------------------- geometry
 
-template <int D, bool MS>
-__device__ __forceinline__ void pass2(const ModeTable& mt, int ne, const double (&g)[kR],
-                                      const double (&b)[kR], unsigned tmask, const LaneAgg* carry,
-                                      double (&out)[kR], const ModeSumsOut& ms) {
-  for (int k = 0; k < ne; ++k) {
-    cplx c[kMaxDeg + 1];
-    load_coef<D>(mt, k, c);
-    const cplx s = mt.s[k];
-    const cplx mw = mt.mw[k];
-    cplx d[kR];
-    cplx H = carry[k].F;  // forward state at the element before the run
-    int64_t ti = ms.t0;
-#pragma unroll
-    for (int i = 0; i < kR; ++i) {
-      d[i] = gap_factor<D>(c, s, g[i]);
-      H = cmad(d[i], H, cplx{b[i], 0.0});
-      if constexpr (MS) {
-        if (tmask & (1u << i)) ms.hp[(int64_t)k * ms.M + ti++] = H;
-      } else {
-        out[i] = fma(mw.re, H.re, fma(-mw.im, H.im, out[i]));
-      }
-    }
-    cplx K = carry[k].G;  // backward state at the run's last element
-#pragma unroll
-    for (int i = kR - 1; i >= 0; --i) {
-      if constexpr (MS) {
-        if (tmask & (1u << i)) ms.hm[(int64_t)k * ms.M + (--ti)] = K;
-      } else {
-        out[i] = fma(mw.re, K.re, fma(-mw.im, K.im, out[i]));
-      }
-      K = cmul(d[i], cplx{K.re + b[i], K.im});
-    }
-  }
-}
-
-// ------------------------------------------------------------ tile body
-
-struct TileGeom {
-  int64_t ib, jb;  // first target / source of the tile
+struct SegGeom {
+  int64_t ib, jb;  // first target / source of the segment
   int nx, ny, len;
-  double zprev;
+  double zprev;  // coordinate of the merged element preceding the segment
+  double zlast;  // coordinate of the segment's last merged element
 };
 
-__device__ __forceinline__ TileGeom tile_geom(const StreamArgs& a, int64_t t) {
-  TileGeom tg;
+__device__ __forceinline__ SegGeom seg_geom(const StreamArgs& a, int64_t s) {
+  SegGeom g;
   const int64_t L = a.M + a.N;
-  const int64_t d0 = t * kTile;
-  const int64_t d1 = (d0 + kTile < L) ? d0 + kTile : L;
-  tg.ib = a.tile_ib[t];
-  const int64_t ie = a.tile_ib[t + 1];
-  tg.jb = d0 - tg.ib;
-  tg.nx = (int)(ie - tg.ib);
-  tg.ny = (int)((d1 - ie) - tg.jb);
-  tg.len = (int)(d1 - d0);
-  if (t == 0) {
-    tg.zprev = a.zprev0;
+  const int64_t d0 = s * kSeg;
+  const int64_t d1 = (d0 + kSeg < L) ? d0 + kSeg : L;
+  g.ib = a.seg_ib[s];
+  const int64_t ie = a.seg_ib[s + 1];
+  g.jb = d0 - g.ib;
+  const int64_t je = d1 - ie;
+  g.nx = (int)(ie - g.ib);
+  g.ny = (int)(je - g.jb);
+  g.len = (int)(d1 - d0);
+  if (s == 0) {
+    g.zprev = a.zprev0;
   } else {
-    double px = tg.ib > 0 ? a.xs[tg.ib - 1] : -INFINITY;
-    double py = tg.jb > 0 ? a.ys[tg.jb - 1] : -INFINITY;
-    tg.zprev = fmax(px, py);
+    const double px = g.ib > 0 ? a.xs[g.ib - 1] : -INFINITY;
+    const double py = g.jb > 0 ? a.ys[g.jb - 1] : -INFINITY;
+    g.zprev = fmax(px, py);
   }
-  return tg;
+  const double lx = g.nx > 0 ? a.xs[ie - 1] : -INFINITY;
+  const double ly = g.ny > 0 ? a.ys[je - 1] : -INFINITY;
+  g.zlast = fmax(lx, ly);
+  return g;
 }
+
+// ------------------------------------------------------------- lane runs
 
 struct LaneRun {
-  double g[kR];
-  double b[kR];
-  unsigned tmask;
-  int tfirst;
-  double gmax;
+  double g[kR];  // gap to the previous merged element
+  double b[kR];  // strength if source, 0 if target / padding
+  unsigned tmask;  // bit e: element e is a target
+  int tfirst;      // segment-local index of the lane's first target
+  double gmax;     // largest gap
+  double span;     // last coordinate of the run minus the coordinate before it
 };
 
-// Loads the tile into shared memory and merges this lane's run into registers.
-__device__ __forceinline__ void load_and_merge(const StreamArgs& a, const TileGeom& tg,
-                                               double* sx, double* sy, double* sb, LaneRun& r) {
-  for (int i = threadIdx.x; i < tg.nx; i += kThreads) sx[i] = __ldg(a.xs + tg.ib + i);
-  for (int j = threadIdx.x; j < tg.ny; j += kThreads) {
-    sy[j] = __ldg(a.ys + tg.jb + j);
-    sb[j] = __ldg(a.bs + tg.jb + j);
+// Segment data of one warp, staged in shared memory.
+struct SegData {
+  double* sx;
+  double* sy;
+  double* sb;
+};
+
+__device__ __forceinline__ void warp_load_segment(const StreamArgs& a, const SegGeom& g,
+                                                  SegData sd, int lane) {
+  for (int i = lane; i < g.nx; i += 32) sd.sx[i] = __ldg(a.xs + g.ib + i);
+  for (int j = lane; j < g.ny; j += 32) {
+    sd.sy[j] = __ldg(a.ys + g.jb + j);
+    sd.sb[j] = __ldg(a.bs + g.jb + j);
   }
-  __syncthreads();
-  const int d0 = threadIdx.x * kR;
-  const int dd = d0 < tg.len ? d0 : tg.len;
-  int i = (int)merge_path(sx, tg.nx, sy, tg.ny, dd);
+  __syncwarp();
+}
+
+__device__ __forceinline__ void lane_merge(const SegGeom& g, SegData sd, int lane, LaneRun& r) {
+  const int d0 = lane * kR;
+  const int dd = d0 < g.len ? d0 : g.len;
+  int i = (int)merge_path(sd.sx, g.nx, sd.sy, g.ny, dd);
   int j = dd - i;
   double prev;
   if (d0 == 0) {
-    prev = tg.zprev;
+    prev = g.zprev;
   } else {
-    double px = i > 0 ? sx[i - 1] : -INFINITY;
-    double py = j > 0 ? sy[j - 1] : -INFINITY;
+    const double px = i > 0 ? sd.sx[i - 1] : -INFINITY;
+    const double py = j > 0 ? sd.sy[j - 1] : -INFINITY;
     prev = fmax(px, py);
   }
+  const double start = prev;
   r.tfirst = i;
   r.tmask = 0u;
   r.gmax = 0.0;
 #pragma unroll
   for (int e = 0; e < kR; ++e) {
-    if (d0 + e < tg.len) {
-      const bool src = (j < tg.ny) && (i >= tg.nx || sy[j] <= sx[i]);
+    if (d0 + e < g.len) {
+      const bool src = (j < g.ny) && (i >= g.nx || sd.sy[j] <= sd.sx[i]);
       double z;
       if (src) {
-        z = sy[j];
-        r.b[e] = sb[j];
+        z = sd.sy[j];
+        r.b[e] = sd.sb[j];
         ++j;
       } else {
-        z = sx[i];
+        z = sd.sx[i];
         r.b[e] = 0.0;
         r.tmask |= 1u << e;
         ++i;
@@ -226,28 +214,158 @@ __device__ __forceinline__ void load_and_merge(const StreamArgs& a, const TileGe
     }
     r.gmax = fmax(r.gmax, r.g[e]);
   }
+  r.span = d0 < g.len ? prev - start : 0.0;
 }
 
-__device__ __forceinline__ double warp_max(double v) {
+// --------------------------------------------------------------- pass 1
+
+// Exact per-element lane aggregates (robust path for wide runs):
+//   A = prod d_i, F = forward state at the run end, G = backward state at
+//   the element before the run.
+template <int D>
+__device__ __forceinline__ void pass1_elements(const ModeTable& mt, int ne, const LaneRun& r,
+                                               LaneAgg* out) {
+  for (int k = 0; k < ne; ++k) {
+    Coef<D> c;
+    c.load(mt, k);
+    const cplx s = mt.s[k];
+    cplx F = {0.0, 0.0}, P = {1.0, 0.0}, G = {0.0, 0.0};
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+    for (int i = 0; i < kR; ++i) {
+      const cplx d = gap_factor<D>(c, s, r.g[i]);
+      F = cmad(d, F, cplx{r.b[i], 0.0});
+      P = cmul(P, d);
+      G.re = fma(r.b[i], P.re, G.re);
+      G.im = fma(r.b[i], P.im, G.im);
+    }
+    out[k] = LaneAgg{P, F, G};
+  }
 }
 
-// Dispatch on the warp-uniform Taylor degree.
-__device__ __forceinline__ void dispatch_pass1(int D, const ModeTable& mt, int ne,
+// Moment form of the lane aggregates: with h = span/2 and d_i the position of
+// source i relative to the run's midpoint,
+//   F = e^{-s h} sum_i b_i e^{+s d_i},  G = e^{-s h} sum_i b_i e^{-s d_i},
+//   A = (e^{-s h})^2,
+// and e^{-/+ s d} = sum_n (-/+ s)^n d^n / n! truncated at DM (|s| h <= rmax[DM]),
+// so the per-source work is mode independent: M_n = sum_i b_i d_i^n.
+template <int DM>
+__device__ __forceinline__ void pass1_moments(const ModeTable& mt, int ne, const LaneRun& r,
+                                              LaneAgg* out) {
+  const double h = 0.5 * r.span;
+  double M[DM + 1];
+#pragma unroll
+  for (int n = 0; n <= DM; ++n) M[n] = 0.0;
+  double pos = 0.0;
+#pragma unroll
+  for (int i = 0; i < kR; ++i) {
+    pos += r.g[i];
+    const double d = pos - h;
+    double p = r.b[i];
+    M[0] += p;
+#pragma unroll
+    for (int n = 1; n <= DM; ++n) {
+      p *= d;
+      M[n] += p;
+    }
+  }
+  for (int k = 0; k < ne; ++k) {
+    Coef<DM> c;
+    c.load(mt, k);
+    cplx ev = {0.0, 0.0}, od = {0.0, 0.0};
+#pragma unroll
+    for (int n = 0; n <= DM; ++n) {
+      if (n & 1) {
+        od.re = fma(c[n].re, M[n], od.re);
+        od.im = fma(c[n].im, M[n], od.im);
+      } else {
+        ev.re = fma(c[n].re, M[n], ev.re);
+        ev.im = fma(c[n].im, M[n], ev.im);
+      }
+    }
+    const cplx E = horner<DM>(c, h);
+    out[k].A = cmul(E, E);
+    out[k].F = cmul(E, cplx{ev.re - od.re, ev.im - od.im});
+    out[k].G = cmul(E, cplx{ev.re + od.re, ev.im + od.im});
+  }
+}
+
+__device__ __forceinline__ void dispatch_pass1(int D, int DM, const ModeTable& mt, int ne,
                                                const LaneRun& r, LaneAgg* out) {
+  if (D >= 0 && DM >= 0) {
+    switch (DM) {
+#define FGT_P1M(n)                           \
+  case n:                                    \
+    pass1_moments<n>(mt, ne, r, out);        \
+    return;
+      FGT_P1M(0) FGT_P1M(1) FGT_P1M(2) FGT_P1M(3) FGT_P1M(4) FGT_P1M(5) FGT_P1M(6)
+      FGT_P1M(7) FGT_P1M(8)
+#undef FGT_P1M
+      default:
+        break;
+    }
+  }
   switch (D) {
-#define FGT_P1(n) \
-  case n:         \
-    pass1<n>(mt, ne, r.g, r.b, out); \
-    break;
-    FGT_P1(0) FGT_P1(1) FGT_P1(2) FGT_P1(3) FGT_P1(4) FGT_P1(5) FGT_P1(6) FGT_P1(7)
-    FGT_P1(8) FGT_P1(9) FGT_P1(10) FGT_P1(11) FGT_P1(12) FGT_P1(13) FGT_P1(14)
-    FGT_P1(15) FGT_P1(16)
-#undef FGT_P1
+#define FGT_P1E(n)                           \
+  case n:                                    \
+    pass1_elements<n>(mt, ne, r, out);       \
+    return;
+    FGT_P1E(0) FGT_P1E(1) FGT_P1E(2) FGT_P1E(3) FGT_P1E(4) FGT_P1E(5) FGT_P1E(6) FGT_P1E(7)
+    FGT_P1E(8) FGT_P1E(9) FGT_P1E(10) FGT_P1E(11) FGT_P1E(12) FGT_P1E(13) FGT_P1E(14)
+    FGT_P1E(15) FGT_P1E(16)
+#undef FGT_P1E
     default:
-      pass1<-1>(mt, ne, r.g, r.b, out);
+      pass1_elements<-1>(mt, ne, r, out);
+  }
+}
+
+// --------------------------------------------------------------- pass 2
+
+// Mode-sums test hook (detail::mode_sums, transform.cpp:310-350): store H
+// (= h+) and K (= h-) of every target per mode instead of combining.
+struct ModeSumsOut {
+  cplx* hp;  // [ne][M]
+  cplx* hm;
+  int64_t M;
+  int64_t t0;  // global sorted index of this lane's first target
+};
+
+// Forward and backward recurrences seeded with the lane carries (carry[k].F
+// = forward state at the element before the run, carry[k].G = backward state
+// at the run's last element), accumulating Re(mw_k (H + K)) into out[] (only
+// target slots are used).  Gap factors are kept in registers between the two
+// sweeps.
+template <int D, bool MS>
+__device__ __forceinline__ void pass2(const ModeTable& mt, int ne, const LaneRun& r,
+                                      const LaneAgg* carry, double (&out)[kR],
+                                      const ModeSumsOut& ms) {
+  for (int k = 0; k < ne; ++k) {
+    Coef<D> c;
+    c.load(mt, k);
+    const cplx s = mt.s[k];
+    const cplx mw = mt.mw[k];
+    cplx d[kR];
+    cplx H = carry[k].F;
+    int64_t ti = ms.t0;
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      d[i] = gap_factor<D>(c, s, r.g[i]);
+      H = cmad(d[i], H, cplx{r.b[i], 0.0});
+      if constexpr (MS) {
+        if (r.tmask & (1u << i)) ms.hp[(int64_t)k * ms.M + ti++] = H;
+      } else {
+        out[i] = fma(mw.re, H.re, fma(-mw.im, H.im, out[i]));
+      }
+    }
+    cplx K = carry[k].G;
+#pragma unroll
+    for (int i = kR - 1; i >= 0; --i) {
+      if constexpr (MS) {
+        if (r.tmask & (1u << i)) ms.hm[(int64_t)k * ms.M + (--ti)] = K;
+      } else {
+        out[i] = fma(mw.re, K.re, fma(-mw.im, K.im, out[i]));
+      }
+      K = cmul(d[i], cplx{K.re + r.b[i], K.im});
+    }
   }
 }
 
@@ -256,51 +374,29 @@ __device__ __forceinline__ void dispatch_pass2(int D, const ModeTable& mt, int n
                                                const LaneRun& r, const LaneAgg* carry,
                                                double (&out)[kR], const ModeSumsOut& ms) {
   switch (D) {
-#define FGT_P2(n) \
-  case n:         \
-    pass2<n, MS>(mt, ne, r.g, r.b, r.tmask, carry, out, ms); \
+#define FGT_P2(n)                                 \
+  case n:                                         \
+    pass2<n, MS>(mt, ne, r, carry, out, ms);      \
     break;
     FGT_P2(0) FGT_P2(1) FGT_P2(2) FGT_P2(3) FGT_P2(4) FGT_P2(5) FGT_P2(6) FGT_P2(7)
     FGT_P2(8) FGT_P2(9) FGT_P2(10) FGT_P2(11) FGT_P2(12) FGT_P2(13) FGT_P2(14)
     FGT_P2(15) FGT_P2(16)
 #undef FGT_P2
     default:
-      pass2<-1, MS>(mt, ne, r.g, r.b, r.tmask, carry, out, ms);
+      pass2<-1, MS>(mt, ne, r, carry, out, ms);
   }
 }
 
-// Bytes of the aliased region: tile data (x, y, beta) during the merge, lane
-// aggregates / carries afterwards.
-__host__ __device__ __forceinline__ size_t tile_dyn_bytes(int ne) {
-  size_t data = sizeof(double) * 3 * kTile;
-  size_t aggs = sizeof(LaneAgg) * kThreads * (size_t)ne;
-  return data > aggs ? data : aggs;
-}
+// ------------------------------------------------- sequential lane scans
+// Lanes q < 2 ne of a warp: q < ne forward for mode q, ne <= q < 2 ne
+// backward for mode q - ne.  aggs is [32 lanes][ne].
 
-// Shared-memory layout of one tile CTA.
-struct TileSmem {
-  ModeTable mt;
-  LaneAgg wagg[kWarps][kMaxModes];  // warp aggregates, then warp carries
-  // followed by the dynamic region: max(3*kTile doubles, kThreads*ne LaneAgg)
-};
-
-__device__ __forceinline__ void load_mode_table(const ModeTable* g, ModeTable& s) {
-  const double* src = reinterpret_cast<const double*>(g);
-  double* dst = reinterpret_cast<double*>(&s);
-  constexpr int n = sizeof(ModeTable) / sizeof(double);
-  for (int i = threadIdx.x; i < n; i += kThreads) dst[i] = src[i];
-}
-
-// Sequential scans by lanes q < 2*ne of a warp: q < ne forward of mode q,
-// ne <= q < 2ne backward of mode q-ne.  `aggs` is [lanes][ne] LaneAgg.
-// reduce: combine lanes [l0, l0+n) into (A, F) / G.
-__device__ __forceinline__ LaneAgg seq_reduce(const LaneAgg* aggs, int ne, int l0, int n, int q) {
+__device__ __forceinline__ LaneAgg lanes_reduce(const LaneAgg* aggs, int ne, int q) {
   LaneAgg res{{1.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
   if (q < ne) {
-    const int k = q;
     cplx A = {1.0, 0.0}, F = {0.0, 0.0};
-    for (int l = l0; l < l0 + n; ++l) {
-      const LaneAgg& x = aggs[l * ne + k];
+    for (int l = 0; l < 32; ++l) {
+      const LaneAgg& x = aggs[l * ne + q];
       F = cmad(x.A, F, x.F);
       A = cmul(A, x.A);
     }
@@ -309,7 +405,7 @@ __device__ __forceinline__ LaneAgg seq_reduce(const LaneAgg* aggs, int ne, int l
   } else {
     const int k = q - ne;
     cplx G = {0.0, 0.0};
-    for (int l = l0 + n - 1; l >= l0; --l) {
+    for (int l = 31; l >= 0; --l) {
       const LaneAgg& x = aggs[l * ne + k];
       G = cmad(x.A, G, x.G);
     }
@@ -318,13 +414,12 @@ __device__ __forceinline__ LaneAgg seq_reduce(const LaneAgg* aggs, int ne, int l
   return res;
 }
 
-// Exclusive carries, written in place: forward carry into .F, backward into .G
-__device__ __forceinline__ void seq_carry(LaneAgg* aggs, int ne, int l0, int n, int q, cplx cin) {
+// Exclusive lane carries written in place: forward into .F, backward into .G
+__device__ __forceinline__ void lanes_carry(LaneAgg* aggs, int ne, int q, cplx cin) {
   if (q < ne) {
-    const int k = q;
     cplx c = cin;
-    for (int l = l0; l < l0 + n; ++l) {
-      LaneAgg& x = aggs[l * ne + k];
+    for (int l = 0; l < 32; ++l) {
+      LaneAgg& x = aggs[l * ne + q];
       const cplx A = x.A, F = x.F;
       x.F = c;
       c = cmad(A, c, F);
@@ -332,7 +427,7 @@ __device__ __forceinline__ void seq_carry(LaneAgg* aggs, int ne, int l0, int n, 
   } else {
     const int k = q - ne;
     cplx c = cin;
-    for (int l = l0 + n - 1; l >= l0; --l) {
+    for (int l = 31; l >= 0; --l) {
       LaneAgg& x = aggs[l * ne + k];
       const cplx A = x.A, G = x.G;
       x.G = c;
@@ -341,199 +436,364 @@ __device__ __forceinline__ void seq_carry(LaneAgg* aggs, int ne, int l0, int n, 
   }
 }
 
-// KIND: 0 = tile aggregates (K1), 1 = main pass (K3), 2 = mode sums (test hook)
-template <int KIND>
-__global__ void __launch_bounds__(kThreads, 4)
-    tile_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab, TileState ts,
-                OutArgs o) {
-  constexpr bool MAIN = KIND != 0;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TileSmem& S = *reinterpret_cast<TileSmem*>(smem_raw);
-  unsigned char* dyn = smem_raw + sizeof(TileSmem);
-  double* sx = reinterpret_cast<double*>(dyn);
-  double* sy = sx + kTile;
-  double* sb = sy + kTile;
-  LaneAgg* aggs = reinterpret_cast<LaneAgg*>(dyn);  // aliases sx/sy/sb after merge
-  double* su = reinterpret_cast<double*>(dyn + tile_dyn_bytes(P.ne));  // output staging
+// -------------------------------------------------------- shared memory
 
-  const int64_t t = blockIdx.x;
-  const int ne = P.ne;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+// Per-warp region: segment data (x, y, beta) during the merge, lane
+// aggregates / carries afterwards; plus the output staging buffer.
+__host__ __device__ __forceinline__ size_t warp_region_bytes(int ne) {
+  const size_t data = sizeof(double) * 3 * kSeg;
+  const size_t aggs = sizeof(LaneAgg) * 32 * (size_t)ne;
+  return (data > aggs ? data : aggs) + sizeof(double) * kSeg;
+}
 
-  load_mode_table(mtab, S.mt);
-  const TileGeom tg = tile_geom(a, t);
-  LaneRun r;
-  load_and_merge(a, tg, sx, sy, sb, r);
-  const int D = pick_degree(P, warp_max(r.gmax));
-  __syncthreads();  // tile data dead from here on; aggs alias it
+struct SegSmemView {
+  SegData sd;
+  LaneAgg* aggs;
+  double* su;
+};
 
-  LaneAgg* mine = aggs + threadIdx.x * ne;
-  dispatch_pass1(D, S.mt, ne, r, mine);
-  __syncwarp();
+__device__ __forceinline__ SegSmemView warp_smem(unsigned char* base, int ne, int warp) {
+  unsigned char* w = base + (size_t)warp * warp_region_bytes(ne);
+  SegSmemView v;
+  v.sd.sx = reinterpret_cast<double*>(w);
+  v.sd.sy = v.sd.sx + kSeg;
+  v.sd.sb = v.sd.sy + kSeg;
+  v.aggs = reinterpret_cast<LaneAgg*>(w);
+  const size_t data = sizeof(double) * 3 * kSeg;
+  const size_t aggs = sizeof(LaneAgg) * 32 * (size_t)ne;
+  v.su = reinterpret_cast<double*>(w + (data > aggs ? data : aggs));
+  return v;
+}
 
-  // Level A: warp aggregates.
-  if (lane < 2 * ne) {
-    LaneAgg w = seq_reduce(aggs, ne, warp * 32, 32, lane);
-    const int k = lane < ne ? lane : lane - ne;
-    if (lane < ne) {
-      S.wagg[warp][k].A = w.A;
-      S.wagg[warp][k].F = w.F;
-    } else {
-      S.wagg[warp][k].G = w.G;
+// ------------------------------------------------------------------- K1
+
+template <int DM>
+__device__ __forceinline__ void seg_moments(const StreamArgs& a, const SegGeom& g, double h,
+                                            int lane, double (&M)[kMaxMom + 1]) {
+#pragma unroll
+  for (int n = 0; n <= DM; ++n) M[n] = 0.0;
+  for (int j = lane; j < g.ny; j += 32) {
+    const double y = __ldg(a.ys + g.jb + j);
+    double p = __ldg(a.bs + g.jb + j);
+    const double d = (y - g.zprev) - h;
+    M[0] += p;
+#pragma unroll
+    for (int n = 1; n <= DM; ++n) {
+      p *= d;
+      M[n] += p;
     }
   }
-  __syncthreads();
+#pragma unroll
+  for (int n = 0; n <= DM; ++n) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M[n] += __shfl_xor_sync(0xffffffffu, M[n], o);
+  }
+}
 
-  if constexpr (!MAIN) {
-    // Tile aggregate -> global.
-    if (warp == 0 && lane < 2 * ne) {
-      const int k = lane < ne ? lane : lane - ne;
-      if (lane < ne) {
-        cplx A = {1.0, 0.0}, F = {0.0, 0.0};
-        for (int w = 0; w < kWarps; ++w) {
-          F = cmad(S.wagg[w][k].A, F, S.wagg[w][k].F);
-          A = cmul(A, S.wagg[w][k].A);
-        }
-        ts.A[(int64_t)k * a.ntiles + t] = A;
-        ts.F[(int64_t)k * a.ntiles + t] = F;
+template <int DM>
+__device__ __forceinline__ void seg_aggregate_moments(const StreamArgs& a, const SegGeom& g,
+                                                      const ModeTable& mt, int ne, int lane,
+                                                      int64_t s, TileState ts) {
+  const double L = g.zlast - g.zprev;
+  const double h = 0.5 * L;
+  double M[kMaxMom + 1];
+  seg_moments<DM>(a, g, h, lane, M);
+  if (lane < ne) {
+    const int k = lane;
+    cplx ev = {0.0, 0.0}, od = {0.0, 0.0};
+#pragma unroll
+    for (int n = 0; n <= DM; ++n) {
+      const cplx c = mt.coef[k][n];
+      if (n & 1) {
+        od.re = fma(c.re, M[n], od.re);
+        od.im = fma(c.im, M[n], od.im);
       } else {
-        cplx G = {0.0, 0.0};
-        for (int w = kWarps - 1; w >= 0; --w) G = cmad(S.wagg[w][k].A, G, S.wagg[w][k].G);
-        ts.G[(int64_t)k * a.ntiles + t] = G;
+        ev.re = fma(c.re, M[n], ev.re);
+        ev.im = fma(c.im, M[n], ev.im);
       }
     }
+    const cplx sk = mt.s[k];
+    const cplx E = decay_exact(sk.re, sk.im, h);
+    const int64_t o = (int64_t)k * a.nseg + s;
+    ts.A[o] = decay_exact(sk.re, sk.im, L);
+    ts.F[o] = cmul(E, cplx{ev.re - od.re, ev.im - od.im});
+    ts.G[o] = cmul(E, cplx{ev.re + od.re, ev.im + od.im});
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    seg_aggregate_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
+                         TileState ts) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ModeTable& mt = *reinterpret_cast<ModeTable*>(smem_raw);
+  unsigned char* wbase = smem_raw + sizeof(ModeTable);
+  load_mode_table(mtab, mt);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t s = (int64_t)blockIdx.x * kSegWarps + warp;
+  if (s >= a.nseg) return;
+  const int ne = P.ne;
+  const SegGeom g = seg_geom(a, s);
+  const int DM = pick_degree(P, 0.5 * (g.zlast - g.zprev));
+  switch (DM) {
+#define FGT_K1(n)                                                 \
+  case n:                                                         \
+    seg_aggregate_moments<n>(a, g, mt, ne, lane, s, ts);          \
+    return;
+    FGT_K1(0) FGT_K1(1) FGT_K1(2) FGT_K1(3) FGT_K1(4) FGT_K1(5) FGT_K1(6) FGT_K1(7)
+    FGT_K1(8) FGT_K1(9) FGT_K1(10) FGT_K1(11) FGT_K1(12) FGT_K1(13) FGT_K1(14)
+    FGT_K1(15) FGT_K1(16)
+#undef FGT_K1
+    default:
+      break;
+  }
+  // Wide segment: exact per-element lane aggregates + sequential reduction.
+  SegSmemView v = warp_smem(wbase, ne, warp);
+  warp_load_segment(a, g, v.sd, lane);
+  LaneRun r;
+  lane_merge(g, v.sd, lane, r);
+  __syncwarp();
+  pass1_elements<-1>(mt, ne, r, v.aggs + lane * ne);
+  __syncwarp();
+  if (lane < 2 * ne) {
+    const LaneAgg w = lanes_reduce(v.aggs, ne, lane);
+    const int k = lane < ne ? lane : lane - ne;
+    const int64_t o = (int64_t)k * a.nseg + s;
+    if (lane < ne) {
+      ts.A[o] = w.A;
+      ts.F[o] = w.F;
+    } else {
+      ts.G[o] = w.G;
+    }
+  }
+}
+
+// ------------------------------------------------------------------- K3
+
+template <bool MS>
+__global__ void __launch_bounds__(kThreads, 4)
+    seg_main_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
+                    TileState ts, OutArgs o) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ModeTable& mt = *reinterpret_cast<ModeTable*>(smem_raw);
+  unsigned char* wbase = smem_raw + sizeof(ModeTable);
+  load_mode_table(mtab, mt);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t s = (int64_t)blockIdx.x * kSegWarps + warp;
+  if (s >= a.nseg) return;
+  const int ne = P.ne;
+  const SegGeom g = seg_geom(a, s);
+  SegSmemView v = warp_smem(wbase, ne, warp);
+  warp_load_segment(a, g, v.sd, lane);
+  LaneRun r;
+  lane_merge(g, v.sd, lane, r);
+  const int D = pick_degree(P, warp_max(r.gmax));
+  const int DM = pick_degree(P, warp_max(0.5 * r.span));
+  __syncwarp();  // segment data dead: aggs alias it
+
+  LaneAgg* mine = v.aggs + lane * ne;
+  dispatch_pass1(D, DM, mt, ne, r, mine);
+  __syncwarp();
+  if (lane < 2 * ne) {
+    const int k = lane < ne ? lane : lane - ne;
+    const int64_t idx = (int64_t)k * a.nseg + s;
+    lanes_carry(v.aggs, ne, lane, lane < ne ? ts.Cf[idx] : ts.Cb[idx]);
+  }
+  __syncwarp();
+
+  double out[kR];
+#pragma unroll
+  for (int e = 0; e < kR; ++e) out[e] = 0.0;
+  if constexpr (MS) {
+    ModeSumsOut ms{o.hp, o.hm, a.M, o.u_offset + g.ib + r.tfirst};
+    dispatch_pass2<true>(D, mt, ne, r, mine, out, ms);
     return;
   } else {
-    // Level B: warp carries from the tile carries.
-    if (warp == 0 && lane < 2 * ne) {
-      const int k = lane < ne ? lane : lane - ne;
-      if (lane < ne) {
-        cplx c = ts.Cf[(int64_t)k * a.ntiles + t];
-        for (int w = 0; w < kWarps; ++w) {
-          const cplx A = S.wagg[w][k].A, F = S.wagg[w][k].F;
-          S.wagg[w][k].F = c;
-          c = cmad(A, c, F);
-        }
-      } else {
-        cplx c = ts.Cb[(int64_t)k * a.ntiles + t];
-        for (int w = kWarps - 1; w >= 0; --w) {
-          const cplx A = S.wagg[w][k].A, G = S.wagg[w][k].G;
-          S.wagg[w][k].G = c;
-          c = cmad(A, c, G);
-        }
-      }
-    }
-    __syncthreads();
-    // Level C: lane carries inside each warp.
-    if (lane < 2 * ne) {
-      const int k = lane < ne ? lane : lane - ne;
-      const cplx cin = lane < ne ? S.wagg[warp][k].F : S.wagg[warp][k].G;
-      seq_carry(aggs, ne, warp * 32, 32, lane, cin);
-    }
-    __syncwarp();
-
-    double out[kR];
-#pragma unroll
-    for (int e = 0; e < kR; ++e) out[e] = 0.0;
-    if constexpr (KIND == 2) {
-      ModeSumsOut ms{o.hp, o.hm, a.M, o.u_offset + tg.ib + r.tfirst};
-      dispatch_pass2<true>(D, S.mt, ne, r, mine, out, ms);
-      return;
-    } else {
-      dispatch_pass2<false>(D, S.mt, ne, r, mine, out, ModeSumsOut{nullptr, nullptr, 0, 0});
-    }
-
+    dispatch_pass2<false>(D, mt, ne, r, mine, out, ModeSumsOut{nullptr, nullptr, 0, 0});
     int tk = r.tfirst;
 #pragma unroll
     for (int e = 0; e < kR; ++e)
-      if (r.tmask & (1u << e)) su[tk++] = out[e];
-    __syncthreads();
-    const int64_t base = o.u_offset + tg.ib;
+      if (r.tmask & (1u << e)) v.su[tk++] = out[e];
+    __syncwarp();
+    const int64_t base = o.u_offset + g.ib;
     if (o.tperm) {
-      for (int i = threadIdx.x; i < tg.nx; i += kThreads) o.u[o.tperm[base + i]] = su[i];
+      for (int i = lane; i < g.nx; i += 32) o.u[o.tperm[base + i]] = v.su[i];
     } else {
-      for (int i = threadIdx.x; i < tg.nx; i += kThreads) o.u[base + i] = su[i];
+      for (int i = lane; i < g.nx; i += 32) o.u[base + i] = v.su[i];
     }
   }
 }
 
-// ------------------------------------------------------------ K0 / K2
+// ------------------------------------------------------------------- K0
 
 __global__ void partition_kernel(const double* __restrict__ xs, int64_t M,
-                                 const double* __restrict__ ys, int64_t N, int64_t tile,
-                                 int64_t ntiles, int64_t* __restrict__ tile_ib) {
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > ntiles) return;
-  int64_t diag = t * tile;
+                                 const double* __restrict__ ys, int64_t N, int64_t seg,
+                                 int64_t nseg, int64_t* __restrict__ seg_ib) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > nseg) return;
+  int64_t diag = t * seg;
   if (diag > M + N) diag = M + N;
-  tile_ib[t] = merge_path(xs, M, ys, N, diag);
+  seg_ib[t] = merge_path(xs, M, ys, N, diag);
 }
 
-constexpr int kScanThreads = 1024;
+// ------------------------------------------------------------------- K2
+// Scan of (a, s) pairs over segments, one (mode, direction) per blockIdx.y:
+// q < ne forward of mode q over F, q >= ne backward of mode q - ne over G in
+// reversed segment order.  Three phases: per-block reduce, top-level scan of
+// block aggregates (one CTA per q), per-block down-sweep writing carries.
 
-// One CTA per (mode, direction).  Thread-serial segments + a block scan of
-// the segment aggregates under (a, s) o (a', s') = (a a', a' s + s').
-__global__ void __launch_bounds__(kScanThreads)
-    carry_scan_kernel(TileState ts, int64_t ntiles, int ne, const cplx* __restrict__ carry_in,
-                      cplx* __restrict__ totals) {
-  __shared__ cplx sa[kScanThreads];
-  __shared__ cplx ss[kScanThreads];
-  const int k = blockIdx.x % ne;
-  const bool bwd = blockIdx.x >= ne;
-  const cplx* A = ts.A + (int64_t)k * ntiles;
-  const cplx* Sv = (bwd ? ts.G : ts.F) + (int64_t)k * ntiles;
-  cplx* C = (bwd ? ts.Cb : ts.Cf) + (int64_t)k * ntiles;
-  const int64_t per = (ntiles + kScanThreads - 1) / kScanThreads;
-  const int64_t r0 = (int64_t)threadIdx.x * per;
-  const int64_t r1 = (r0 + per < ntiles) ? r0 + per : ntiles;
-  cplx a = {1.0, 0.0}, s = {0.0, 0.0};
-  for (int64_t r = r0; r < r1; ++r) {
-    const int64_t b = bwd ? ntiles - 1 - r : r;
-    const cplx Ab = A[b];
-    s = cmad(Ab, s, Sv[b]);
-    a = cmul(a, Ab);
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 4;
+constexpr int kScanBlock = kScanThreads * kScanItems;
+
+struct Pair {
+  cplx a, s;
+};
+
+// earlier x then later y
+__device__ __forceinline__ Pair combine(Pair x, Pair y) {
+  return Pair{cmul(x.a, y.a), cmad(y.a, x.s, y.s)};
+}
+
+__device__ __forceinline__ Pair shfl_up_pair(Pair p, int off) {
+  Pair r;
+  r.a.re = __shfl_up_sync(0xffffffffu, p.a.re, off);
+  r.a.im = __shfl_up_sync(0xffffffffu, p.a.im, off);
+  r.s.re = __shfl_up_sync(0xffffffffu, p.s.re, off);
+  r.s.im = __shfl_up_sync(0xffffffffu, p.s.im, off);
+  return r;
+}
+
+// Block-wide exclusive scan; returns the exclusive prefix of this thread and
+// the block total.
+__device__ __forceinline__ Pair block_exclusive(Pair v, Pair* total) {
+  __shared__ Pair wtot[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Pair incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const Pair p = shfl_up_pair(incl, off);
+    if (lane >= off) incl = combine(p, incl);
   }
-  // inclusive Hillis-Steele scan over threads
-  sa[threadIdx.x] = a;
-  ss[threadIdx.x] = s;
+  if (lane == 31) wtot[warp] = incl;
   __syncthreads();
-  for (int off = 1; off < kScanThreads; off <<= 1) {
-    cplx pa = {1.0, 0.0}, ps = {0.0, 0.0};
+  Pair wpre{{1.0, 0.0}, {0.0, 0.0}};
+  for (int w = 0; w < warp; ++w) wpre = combine(wpre, wtot[w]);
+  Pair tot{{1.0, 0.0}, {0.0, 0.0}};
+  for (int w = 0; w < kScanThreads / 32; ++w) tot = combine(tot, wtot[w]);
+  *total = tot;
+  Pair excl = shfl_up_pair(incl, 1);
+  if (lane == 0) excl = Pair{{1.0, 0.0}, {0.0, 0.0}};
+  __syncthreads();
+  return combine(wpre, excl);
+}
+
+struct ScanArgs {
+  const cplx* A;
+  const cplx* F;
+  const cplx* G;
+  cplx* Cf;
+  cplx* Cb;
+  int64_t nseg;
+  int ne;
+  int64_t nblk;
+  cplx* blkagg;    // [2ne][nblk] (a, s) pairs as 2 complex
+  cplx* blkcarry;  // [2ne][nblk]
+};
+
+__device__ __forceinline__ Pair load_item(const ScanArgs& sa, int q, int64_t r) {
+  const bool bwd = q >= sa.ne;
+  const int k = bwd ? q - sa.ne : q;
+  const int64_t b = bwd ? sa.nseg - 1 - r : r;
+  const int64_t o = (int64_t)k * sa.nseg + b;
+  return Pair{sa.A[o], bwd ? sa.G[o] : sa.F[o]};
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(ScanArgs sa) {
+  const int q = blockIdx.y;
+  const int64_t r0 = (int64_t)blockIdx.x * kScanBlock + (int64_t)threadIdx.x * kScanItems;
+  Pair acc{{1.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (r0 + i < sa.nseg) acc = combine(acc, load_item(sa, q, r0 + i));
+  Pair tot;
+  block_exclusive(acc, &tot);
+  if (threadIdx.x == 0) {
+    sa.blkagg[((int64_t)q * sa.nblk + blockIdx.x) * 2 + 0] = tot.a;
+    sa.blkagg[((int64_t)q * sa.nblk + blockIdx.x) * 2 + 1] = tot.s;
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+    scan_top_kernel(ScanArgs sa, const cplx* __restrict__ carry_in, cplx* __restrict__ totals) {
+  __shared__ Pair sp[1024];
+  const int q = blockIdx.x;
+  const int ne = sa.ne;
+  const int64_t per = (sa.nblk + 1023) / 1024;
+  const int64_t r0 = (int64_t)threadIdx.x * per;
+  const int64_t r1 = r0 + per < sa.nblk ? r0 + per : sa.nblk;
+  const cplx* ag = sa.blkagg + (int64_t)q * sa.nblk * 2;
+  Pair acc{{1.0, 0.0}, {0.0, 0.0}};
+  for (int64_t r = r0; r < r1; ++r) acc = combine(acc, Pair{ag[2 * r], ag[2 * r + 1]});
+  // Hillis-Steele over 1024 thread aggregates (tiny)
+  sp[threadIdx.x] = acc;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    Pair p{{1.0, 0.0}, {0.0, 0.0}};
     const bool has = threadIdx.x >= off;
-    if (has) {
-      pa = sa[threadIdx.x - off];
-      ps = ss[threadIdx.x - off];
-    }
+    if (has) p = sp[threadIdx.x - off];
     __syncthreads();
     if (has) {
-      // earlier (pa, ps) then later (a, s)
-      s = cmad(a, ps, s);
-      a = cmul(pa, a);
-      sa[threadIdx.x] = a;
-      ss[threadIdx.x] = s;
+      acc = combine(p, acc);
+      sp[threadIdx.x] = acc;
     }
     __syncthreads();
   }
-  // exclusive prefix for this thread
-  cplx ea = {1.0, 0.0}, es = {0.0, 0.0};
-  if (threadIdx.x > 0) {
-    ea = sa[threadIdx.x - 1];
-    es = ss[threadIdx.x - 1];
-  }
-  const cplx cin = carry_in ? carry_in[(bwd ? ne : 0) + k] : cplx{0.0, 0.0};
-  cplx c = cmad(ea, cin, es);
+  Pair ex{{1.0, 0.0}, {0.0, 0.0}};
+  if (threadIdx.x > 0) ex = sp[threadIdx.x - 1];
+  const cplx cin = carry_in ? carry_in[q] : cplx{0.0, 0.0};
+  cplx c = cmad(ex.a, cin, ex.s);
+  cplx* bc = sa.blkcarry + (int64_t)q * sa.nblk;
   for (int64_t r = r0; r < r1; ++r) {
-    const int64_t b = bwd ? ntiles - 1 - r : r;
-    C[b] = c;
-    c = cmad(A[b], c, Sv[b]);
+    bc[r] = c;
+    c = cmad(ag[2 * r], c, ag[2 * r + 1]);
   }
-  if (totals && threadIdx.x == kScanThreads - 1) {
-    // totals layout: [ne] A, [ne] F-total, [ne] G-total
-    if (!bwd) {
-      totals[k] = a;
-      totals[ne + k] = s;
+  if (totals && threadIdx.x == 1023) {
+    const Pair t = sp[1023];
+    if (q < ne) {
+      totals[q] = t.a;       // A of the chunk
+      totals[ne + q] = t.s;  // F: forward state at the chunk end
     } else {
-      totals[2 * ne + k] = s;
+      totals[2 * ne + (q - ne)] = t.s;  // G: backward state at the chunk's z_prev
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kScanThreads) scan_down_kernel(ScanArgs sa) {
+  const int q = blockIdx.y;
+  const bool bwd = q >= sa.ne;
+  const int k = bwd ? q - sa.ne : q;
+  const int64_t r0 = (int64_t)blockIdx.x * kScanBlock + (int64_t)threadIdx.x * kScanItems;
+  Pair items[kScanItems];
+  Pair acc{{1.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    items[i] = r0 + i < sa.nseg ? load_item(sa, q, r0 + i) : Pair{{1.0, 0.0}, {0.0, 0.0}};
+    acc = combine(acc, items[i]);
+  }
+  Pair tot;
+  const Pair ex = block_exclusive(acc, &tot);
+  const cplx bcin = sa.blkcarry[(int64_t)q * sa.nblk + blockIdx.x];
+  cplx c = cmad(ex.a, bcin, ex.s);
+  cplx* C = bwd ? sa.Cb : sa.Cf;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    const int64_t r = r0 + i;
+    if (r < sa.nseg) {
+      const int64_t b = bwd ? sa.nseg - 1 - r : r;
+      C[(int64_t)k * sa.nseg + b] = c;
+      c = cmad(items[i].a, c, items[i].s);
     }
   }
 }
@@ -547,58 +807,89 @@ __global__ void gather_kernel(const double* __restrict__ alpha, const int32_t* _
 
 }  // namespace
 
-size_t tile_smem_bytes(int ne) {
-  return sizeof(TileSmem) + tile_dyn_bytes(ne) + sizeof(double) * kTile;
+// ============================================================== host side
+
+int64_t scan_blocks(int64_t nseg) { return (nseg + kScanBlock - 1) / kScanBlock; }
+
+size_t tile_state_elems(int64_t nseg, int ne) {
+  const size_t nt = (size_t)nseg * (size_t)ne;
+  return 5 * nt + (size_t)scan_blocks(nseg) * 2 * (size_t)ne * 3 + 8;
+}
+
+TileState tile_state_carve(cplx* base, int64_t nseg, int ne) {
+  const size_t nt = (size_t)nseg * (size_t)ne;
+  return TileState{base, base + nt, base + 2 * nt, base + 3 * nt, base + 4 * nt, base + 5 * nt};
+}
+
+size_t seg_smem_bytes(int ne) {
+  return sizeof(ModeTable) + (size_t)kSegWarps * warp_region_bytes(ne);
 }
 
 cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int64_t N,
-                             int64_t tile, int64_t ntiles, int64_t* tile_ib, cudaStream_t st) {
-  const int64_t n = ntiles + 1;
+                             int64_t seg, int64_t nseg, int64_t* seg_ib, cudaStream_t st) {
+  const int64_t n = nseg + 1;
   const int bs = 256;
   note_launch();
-  partition_kernel<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(xs, M, ys, N, tile, ntiles,
-                                                                 tile_ib);
+  partition_kernel<<<(unsigned)((n + bs - 1) / bs), bs, 0, st>>>(xs, M, ys, N, seg, nseg,
+                                                                 seg_ib);
   return cudaGetLastError();
 }
 
-template <int KIND>
-static cudaError_t launch_tile(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
-                               TileState ts, OutArgs o, cudaStream_t st) {
-  if (a.ntiles == 0) return cudaSuccess;
-  const size_t smem = tile_smem_bytes(P.ne);
-  static bool configured[3] = {false, false, false};
-  if (!configured[KIND]) {
-    cudaError_t e = cudaFuncSetAttribute(tile_kernel<KIND>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)tile_smem_bytes(kMaxModes));
-    if (e != cudaSuccess) return e;
-    configured[KIND] = true;
-  }
-  note_launch();
-  tile_kernel<KIND><<<(unsigned)a.ntiles, kThreads, smem, st>>>(a, P, mt, ts, o);
-  return cudaGetLastError();
+template <class K>
+static cudaError_t set_smem(K kernel, bool& done) {
+  if (done) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)seg_smem_bytes(kMaxModes));
+  if (e == cudaSuccess) done = true;
+  return e;
 }
 
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, cudaStream_t st) {
-  return launch_tile<0>(a, P, mt, ts, OutArgs{}, st);
+  if (a.nseg == 0) return cudaSuccess;
+  static bool done = false;
+  cudaError_t e = set_smem(seg_aggregate_kernel, done);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)((a.nseg + kSegWarps - 1) / kSegWarps);
+  note_launch();
+  seg_aggregate_kernel<<<grid, kThreads, seg_smem_bytes(P.ne), st>>>(a, P, mt, ts);
+  return cudaGetLastError();
+}
+
+template <bool MS>
+static cudaError_t launch_seg_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
+                                   TileState ts, OutArgs o, cudaStream_t st) {
+  if (a.nseg == 0) return cudaSuccess;
+  static bool done = false;
+  cudaError_t e = set_smem(seg_main_kernel<MS>, done);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)((a.nseg + kSegWarps - 1) / kSegWarps);
+  note_launch();
+  seg_main_kernel<MS><<<grid, kThreads, seg_smem_bytes(P.ne), st>>>(a, P, mt, ts, o);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                         TileState ts, OutArgs o, cudaStream_t st) {
-  return launch_tile<1>(a, P, mt, ts, o, st);
+  return launch_seg_main<false>(a, P, mt, ts, o, st);
 }
 
 cudaError_t launch_mode_sums(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, OutArgs o, cudaStream_t st) {
-  return launch_tile<2>(a, P, mt, ts, o, st);
+  return launch_seg_main<true>(a, P, mt, ts, o, st);
 }
 
-cudaError_t launch_carry_scan(const TileState& ts, int64_t ntiles, int ne, const cplx* carry_in,
+cudaError_t launch_carry_scan(const TileState& ts, int64_t nseg, int ne, const cplx* carry_in,
                               cplx* totals, cudaStream_t st) {
-  if (ntiles == 0) return cudaSuccess;
-  note_launch();
-  carry_scan_kernel<<<2 * ne, kScanThreads, 0, st>>>(ts, ntiles, ne, carry_in, totals);
+  if (nseg == 0) return cudaSuccess;
+  const int64_t nblk = scan_blocks(nseg);
+  ScanArgs sa{ts.A, ts.F, ts.G, ts.Cf, ts.Cb, nseg, ne, nblk, ts.blk,
+              ts.blk + (size_t)nblk * 2 * ne * 2};
+  const dim3 grid((unsigned)nblk, (unsigned)(2 * ne));
+  note_launch(3);
+  scan_reduce_kernel<<<grid, kScanThreads, 0, st>>>(sa);
+  scan_top_kernel<<<2 * ne, 1024, 0, st>>>(sa, carry_in, totals);
+  scan_down_kernel<<<grid, kScanThreads, 0, st>>>(sa);
   return cudaGetLastError();
 }
 

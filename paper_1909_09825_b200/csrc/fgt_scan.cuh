@@ -1,6 +1,6 @@
-// Tile kernels of the merged-stream SOE scan: K0 partition, K1 tile
-// aggregates, K2 carry scan over tiles, K3 main pass (see fgt_device.cuh and
-// DESIGN.md §3).
+// Segment kernels of the merged-stream SOE scan: K0 partition, K1 segment
+// aggregates, K2 carry scan over segments, K3 main pass (see fgt_device.cuh
+// and DESIGN.md §3).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -10,14 +10,14 @@
 
 namespace fgt_b200 {
 
-constexpr int kWarps = 4;               // warps per CTA (one tile per CTA)
 constexpr int kR = 8;                   // merged elements per lane run
-constexpr int kThreads = kWarps * 32;   // 128
-constexpr int kTile = kThreads * kR;    // 1024 merged elements per tile
+constexpr int kSeg = 32 * kR;           // merged elements per segment (one warp)
+constexpr int kSegWarps = 4;            // segments (warps) per CTA in K1 / K3
+constexpr int kThreads = 32 * kSegWarps;
+constexpr int kMaxMom = kMaxDeg;        // highest moment order of the expansions
 
-// Per-mode constants laid out in device memory (plan-owned), copied into
-// shared memory by every CTA: s_k, mw_k and the Taylor coefficients
-// c_{k,n} = (-s_k)^n / n! of the gap factor exp(-s_k g).
+// Per-mode constants laid out in device memory (plan-owned): s_k, mw_k and the
+// Taylor coefficients c_{k,n} = (-s_k)^n / n! of exp(-s_k g).
 struct ModeTable {
   cplx s[kMaxModes];
   cplx mw[kMaxModes];
@@ -30,8 +30,8 @@ struct StreamArgs {
   const double* ys;  // sorted sources (this chunk)
   int64_t N;
   const double* bs;  // strengths in sorted-source order
-  const int64_t* tile_ib;  // [ntiles+1] targets preceding each tile
-  int64_t ntiles;
+  const int64_t* seg_ib;  // [nseg+1] targets preceding each segment
+  int64_t nseg;
   double zprev0;  // coordinate of the element before this chunk (or its first)
 };
 
@@ -43,28 +43,36 @@ struct OutArgs {
   cplx* hm = nullptr;
 };
 
-// Aggregates / carries, [ne][ntiles] each.
+// Segment aggregates / carries, [ne][nseg] each, plus the K2 workspace.
 struct TileState {
   cplx* A;
   cplx* F;
   cplx* G;
   cplx* Cf;
   cplx* Cb;
+  cplx* blk;  // scan workspace: scan_blocks(nseg) * 2 * ne * 3 complex
 };
 
-size_t tile_smem_bytes(int ne);
+int64_t scan_blocks(int64_t nseg);
+// complex values needed for a TileState of nseg segments and ne modes
+size_t tile_state_elems(int64_t nseg, int ne);
+TileState tile_state_carve(cplx* base, int64_t nseg, int ne);
+
+size_t seg_smem_bytes(int ne);
 
 cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int64_t N,
-                             int64_t tile, int64_t ntiles, int64_t* tile_ib,
-                             cudaStream_t st);
+                             int64_t seg, int64_t nseg, int64_t* seg_ib, cudaStream_t st);
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, cudaStream_t st);
-cudaError_t launch_mode_sums(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
-                             TileState ts, OutArgs o, cudaStream_t st);
-cudaError_t launch_carry_scan(const TileState& ts, int64_t ntiles, int ne, const cplx* carry_in,
+// K2: exclusive carries per segment.  carry_in: 2*ne complex (forward carry at
+// the chunk's z_prev, backward carry at the chunk end) or nullptr; totals:
+// 3*ne complex (A, F, G of the whole chunk) or nullptr.
+cudaError_t launch_carry_scan(const TileState& ts, int64_t nseg, int ne, const cplx* carry_in,
                               cplx* totals, cudaStream_t st);
 cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                         TileState ts, OutArgs o, cudaStream_t st);
+cudaError_t launch_mode_sums(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
+                             TileState ts, OutArgs o, cudaStream_t st);
 cudaError_t launch_gather(const double* alpha, const int32_t* perm, int64_t n, double* out,
                           cudaStream_t st);
 
