@@ -196,8 +196,10 @@ struct fgt_plan_s {
   int32_t* d_sperm = nullptr;
   bool t_sorted = true, s_sorted = true;
   bool same_points = false;
-  int64_t ntiles = 0;
+  int64_t ntiles = 0;  // segments of kSeg merged elements
   int64_t* d_tile_ib = nullptr;
+  double2* d_seg_z = nullptr;
+  uint32_t* d_seg_mask = nullptr;
   double zprev0 = 0.0;
   int* d_flag = nullptr;
   ChunkState cs;
@@ -295,6 +297,11 @@ void finish_plan(fgt_plan_s* p, cudaStream_t st) {
   p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
   ck(launch_partition(p->d_xs, p->M, p->d_ys, p->N, kSeg, p->ntiles, p->d_tile_ib, st),
      "partition");
+  p->d_seg_z = dmalloc<double2>(p->ntiles, st);
+  p->d_seg_mask = dmalloc<uint32_t>((size_t)p->ntiles * (kSeg / 32), st);
+  ck(launch_seg_meta(p->d_xs, p->M, p->d_ys, p->N, p->d_tile_ib, p->ntiles, p->d_seg_z,
+                     p->d_seg_mask, st),
+     "segment metadata");
   ModeTable T;
   build_modes(p->soe, p->delta, p->P, T);
   p->d_mt = dmalloc<ModeTable>(1, st);
@@ -316,6 +323,8 @@ void destroy_plan(fgt_plan_s* p) {
   dfree(p->d_tperm, st);
   dfree(p->d_sperm, st);
   dfree(p->d_tile_ib, st);
+  dfree(p->d_seg_z, st);
+  dfree(p->d_seg_mask, st);
   dfree(p->d_mt, st);
   dfree(p->d_flag, st);
   dfree(p->cs.bs, st);
@@ -387,7 +396,8 @@ void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint3
     ck(cudaMemsetAsync(u, 0, sizeof(double) * p->M, st), "zero potentials");
   } else {
     const double* bs = sorted_strengths(p, strengths, flags, w, nullptr);
-    const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0};
+    const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0,
+                        p->d_seg_z, p->d_seg_mask};
     const TileState ts = tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, p->P.ne)),
                                           p->ntiles, p->P.ne);
     {
@@ -433,7 +443,8 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ho
     ck(cudaStreamSynchronize(st), "sync");
     return;
   }
-  const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0};
+  const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0,
+                        p->d_seg_z, p->d_seg_mask};
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
   ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
   cplx* d_tot = w.get<cplx>(3 * ne);
@@ -454,7 +465,8 @@ void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in_host, double* potentia
   if (p->N == 0 && p->ntiles > 0 && !p->cs.tile)
     raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
   if (!p->cs.tile) raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
-  const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0};
+  const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0,
+                        p->d_seg_z, p->d_seg_mask};
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
   cplx* d_cin = w.get<cplx>(2 * ne);
   ck(cudaMemcpyAsync(d_cin, carry_in_host, sizeof(cplx) * 2 * ne, cudaMemcpyHostToDevice, st),
@@ -797,7 +809,8 @@ extern "C" int fgt_mode_sums(fgt_plan_t p, const double* strengths, double* hp, 
       ck(cudaMemsetAsync(d_hm, 0, sizeof(cplx) * cnt, st), "zero");
     } else {
       const double* bs = sorted_strengths(p, strengths, 0, w, nullptr);
-      const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0};
+      const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0,
+                        p->d_seg_z, p->d_seg_mask};
       const TileState ts = tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, ne)),
                                             p->ntiles, ne);
       ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "aggregates");

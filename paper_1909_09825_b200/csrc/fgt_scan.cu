@@ -128,21 +128,14 @@ __device__ __forceinline__ SegGeom seg_geom(const StreamArgs& a, int64_t s) {
   const int64_t d1 = (d0 + kSeg < L) ? d0 + kSeg : L;
   g.ib = a.seg_ib[s];
   const int64_t ie = a.seg_ib[s + 1];
+  const double2 z = a.seg_z[s];
   g.jb = d0 - g.ib;
   const int64_t je = d1 - ie;
   g.nx = (int)(ie - g.ib);
   g.ny = (int)(je - g.jb);
   g.len = (int)(d1 - d0);
-  if (s == 0) {
-    g.zprev = a.zprev0;
-  } else {
-    const double px = g.ib > 0 ? a.xs[g.ib - 1] : -INFINITY;
-    const double py = g.jb > 0 ? a.ys[g.jb - 1] : -INFINITY;
-    g.zprev = fmax(px, py);
-  }
-  const double lx = g.nx > 0 ? a.xs[ie - 1] : -INFINITY;
-  const double ly = g.ny > 0 ? a.ys[je - 1] : -INFINITY;
-  g.zlast = fmax(lx, ly);
+  g.zprev = s == 0 ? a.zprev0 : z.x;
+  g.zlast = z.y;
   return g;
 }
 
@@ -157,64 +150,63 @@ struct LaneRun {
   double span;     // last coordinate of the run minus the coordinate before it
 };
 
-// Segment data of one warp, staged in shared memory.
-struct SegData {
-  double* sx;
-  double* sy;
-  double* sb;
-};
-
-__device__ __forceinline__ void warp_load_segment(const StreamArgs& a, const SegGeom& g,
-                                                  SegData sd, int lane) {
-  for (int i = lane; i < g.nx; i += 32) sd.sx[i] = __ldg(a.xs + g.ib + i);
-  for (int j = lane; j < g.ny; j += 32) {
-    sd.sy[j] = __ldg(a.ys + g.jb + j);
-    sd.sb[j] = __ldg(a.bs + g.jb + j);
-  }
-  __syncwarp();
-}
-
-__device__ __forceinline__ void lane_merge(const SegGeom& g, SegData sd, int lane, LaneRun& r) {
+// Lane run from the plan-time merge mask: no merge, no shared-memory
+// staging; every element is an independent load.
+__device__ __forceinline__ void lane_load(const StreamArgs& a, const SegGeom& g, int64_t s,
+                                          int lane, LaneRun& r) {
+  const uint32_t word = __ldg(a.seg_mask + s * (kSeg / 32) + (lane >> 2));
   const int d0 = lane * kR;
-  const int dd = d0 < g.len ? d0 : g.len;
-  int i = (int)merge_path(sd.sx, g.nx, sd.sy, g.ny, dd);
-  int j = dd - i;
-  double prev;
-  if (d0 == 0) {
-    prev = g.zprev;
-  } else {
-    const double px = i > 0 ? sd.sx[i - 1] : -INFINITY;
-    const double py = j > 0 ? sd.sy[j - 1] : -INFINITY;
-    prev = fmax(px, py);
+  const int nreal = g.len - d0 < 0 ? 0 : (g.len - d0 < kR ? g.len - d0 : kR);
+  const unsigned live = nreal >= 32 ? 0xffffffffu : ((1u << nreal) - 1u);
+  const unsigned byte = (word >> ((lane & 3) * 8)) & 0xffu & live;
+  const int nt = __popc(byte);
+  // exclusive warp prefix of the target counts
+  int incl = nt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
   }
+  const int i0 = incl - nt;
+  const int j0 = (d0 < g.len ? d0 : g.len) - i0;
+  r.tfirst = i0;
+  r.tmask = byte;
+  double z[kR];
+  double last = 0.0;
+#pragma unroll
+  for (int e = 0; e < kR; ++e) {
+    const int t = __popc(byte & ((1u << e) - 1u));
+    const int sidx = e - t;
+    if (e < nreal) {
+      if (byte & (1u << e)) {
+        z[e] = __ldg(a.xs + g.ib + i0 + t);
+        r.b[e] = 0.0;
+      } else {
+        z[e] = __ldg(a.ys + g.jb + j0 + sidx);
+        r.b[e] = __ldg(a.bs + g.jb + j0 + sidx);
+      }
+      last = z[e];
+    } else {
+      z[e] = 0.0;
+      r.b[e] = 0.0;
+    }
+  }
+  // coordinate preceding the run: the previous lane's last element
+  double prev = __shfl_up_sync(0xffffffffu, last, 1);
+  if (lane == 0) prev = g.zprev;
   const double start = prev;
-  r.tfirst = i;
-  r.tmask = 0u;
   r.gmax = 0.0;
 #pragma unroll
   for (int e = 0; e < kR; ++e) {
-    if (d0 + e < g.len) {
-      const bool src = (j < g.ny) && (i >= g.nx || sd.sy[j] <= sd.sx[i]);
-      double z;
-      if (src) {
-        z = sd.sy[j];
-        r.b[e] = sd.sb[j];
-        ++j;
-      } else {
-        z = sd.sx[i];
-        r.b[e] = 0.0;
-        r.tmask |= 1u << e;
-        ++i;
-      }
-      r.g[e] = z - prev;
-      prev = z;
+    if (e < nreal) {
+      r.g[e] = z[e] - prev;
+      prev = z[e];
     } else {
       r.g[e] = 0.0;
-      r.b[e] = 0.0;
     }
     r.gmax = fmax(r.gmax, r.g[e]);
   }
-  r.span = d0 < g.len ? prev - start : 0.0;
+  r.span = nreal > 0 ? prev - start : 0.0;
 }
 
 // --------------------------------------------------------------- pass 1
@@ -391,29 +383,6 @@ __device__ __forceinline__ void dispatch_pass2(int D, const ModeTable& mt, int n
 // Lanes q < 2 ne of a warp: q < ne forward for mode q, ne <= q < 2 ne
 // backward for mode q - ne.  aggs is [32 lanes][ne].
 
-__device__ __forceinline__ LaneAgg lanes_reduce(const LaneAgg* aggs, int ne, int q) {
-  LaneAgg res{{1.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-  if (q < ne) {
-    cplx A = {1.0, 0.0}, F = {0.0, 0.0};
-    for (int l = 0; l < 32; ++l) {
-      const LaneAgg& x = aggs[l * ne + q];
-      F = cmad(x.A, F, x.F);
-      A = cmul(A, x.A);
-    }
-    res.A = A;
-    res.F = F;
-  } else {
-    const int k = q - ne;
-    cplx G = {0.0, 0.0};
-    for (int l = 31; l >= 0; --l) {
-      const LaneAgg& x = aggs[l * ne + k];
-      G = cmad(x.A, G, x.G);
-    }
-    res.G = G;
-  }
-  return res;
-}
-
 // Exclusive lane carries written in place: forward into .F, backward into .G
 __device__ __forceinline__ void lanes_carry(LaneAgg* aggs, int ne, int q, cplx cin) {
   if (q < ne) {
@@ -438,16 +407,12 @@ __device__ __forceinline__ void lanes_carry(LaneAgg* aggs, int ne, int q, cplx c
 
 // -------------------------------------------------------- shared memory
 
-// Per-warp region: segment data (x, y, beta) during the merge, lane
-// aggregates / carries afterwards; plus the output staging buffer.
+// Per-warp region of K3: lane aggregates / carries, then the output staging.
 __host__ __device__ __forceinline__ size_t warp_region_bytes(int ne) {
-  const size_t data = sizeof(double) * 3 * kSeg;
-  const size_t aggs = sizeof(LaneAgg) * 32 * (size_t)ne;
-  return (data > aggs ? data : aggs) + sizeof(double) * kSeg;
+  return sizeof(LaneAgg) * 32 * (size_t)ne + sizeof(double) * kSeg;
 }
 
 struct SegSmemView {
-  SegData sd;
   LaneAgg* aggs;
   double* su;
 };
@@ -455,13 +420,8 @@ struct SegSmemView {
 __device__ __forceinline__ SegSmemView warp_smem(unsigned char* base, int ne, int warp) {
   unsigned char* w = base + (size_t)warp * warp_region_bytes(ne);
   SegSmemView v;
-  v.sd.sx = reinterpret_cast<double*>(w);
-  v.sd.sy = v.sd.sx + kSeg;
-  v.sd.sb = v.sd.sy + kSeg;
   v.aggs = reinterpret_cast<LaneAgg*>(w);
-  const size_t data = sizeof(double) * 3 * kSeg;
-  const size_t aggs = sizeof(LaneAgg) * 32 * (size_t)ne;
-  v.su = reinterpret_cast<double*>(w + (data > aggs ? data : aggs));
+  v.su = reinterpret_cast<double*>(w + sizeof(LaneAgg) * 32 * (size_t)ne);
   return v;
 }
 
@@ -512,21 +472,46 @@ __device__ __forceinline__ void seg_aggregate_moments(const StreamArgs& a, const
         ev.im = fma(c.im, M[n], ev.im);
       }
     }
-    const cplx sk = mt.s[k];
-    const cplx E = decay_exact(sk.re, sk.im, h);
+    Coef<DM> c;
+    c.load(mt, k);
+    const cplx E = horner<DM>(c, h);
     const int64_t o = (int64_t)k * a.nseg + s;
-    ts.A[o] = decay_exact(sk.re, sk.im, L);
+    ts.A[o] = cmul(E, E);
     ts.F[o] = cmul(E, cplx{ev.re - od.re, ev.im - od.im});
     ts.G[o] = cmul(E, cplx{ev.re + od.re, ev.im + od.im});
   }
 }
 
+// Ordered warp reduction of lane aggregates (lane 0 ends up with the total):
+// forward (A, F) left-to-right, backward G = G_left + A_left G_right.
+__device__ __forceinline__ LaneAgg warp_reduce_agg(LaneAgg v) {
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    LaneAgg r;
+    r.A.re = __shfl_down_sync(0xffffffffu, v.A.re, off);
+    r.A.im = __shfl_down_sync(0xffffffffu, v.A.im, off);
+    r.F.re = __shfl_down_sync(0xffffffffu, v.F.re, off);
+    r.F.im = __shfl_down_sync(0xffffffffu, v.F.im, off);
+    r.G.re = __shfl_down_sync(0xffffffffu, v.G.re, off);
+    r.G.im = __shfl_down_sync(0xffffffffu, v.G.im, off);
+    if (((threadIdx.x & 31) & (2 * off - 1)) == 0) {
+      const cplx F = cmad(r.A, v.F, r.F);
+      const cplx G = cmad(v.A, r.G, v.G);
+      v.A = cmul(v.A, r.A);
+      v.F = F;
+      v.G = G;
+    }
+  }
+  return v;
+}
+
+// K1: one warp per segment.  Moment path when the segment is narrow
+// (|s| h <= rmax[kRegDeg]); otherwise exact per-element lane aggregates from
+// the merge mask, reduced across the warp.
 __global__ void __launch_bounds__(kThreads)
     seg_aggregate_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
                          TileState ts) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  ModeTable& mt = *reinterpret_cast<ModeTable*>(smem_raw);
-  unsigned char* wbase = smem_raw + sizeof(ModeTable);
+  __shared__ ModeTable mt;
   load_mode_table(mtab, mt);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -541,28 +526,30 @@ __global__ void __launch_bounds__(kThreads)
     seg_aggregate_moments<n>(a, g, mt, ne, lane, s, ts);          \
     return;
     FGT_K1(0) FGT_K1(1) FGT_K1(2) FGT_K1(3) FGT_K1(4) FGT_K1(5) FGT_K1(6) FGT_K1(7)
-    FGT_K1(8) FGT_K1(9) FGT_K1(10) FGT_K1(11) FGT_K1(12) FGT_K1(13) FGT_K1(14)
-    FGT_K1(15) FGT_K1(16)
+    FGT_K1(8)
 #undef FGT_K1
     default:
       break;
   }
-  // Wide segment: exact per-element lane aggregates + sequential reduction.
-  SegSmemView v = warp_smem(wbase, ne, warp);
-  warp_load_segment(a, g, v.sd, lane);
+  // Wide segment: exact per-element lane aggregates, ordered warp reduction.
   LaneRun r;
-  lane_merge(g, v.sd, lane, r);
-  __syncwarp();
-  pass1_elements<-1>(mt, ne, r, v.aggs + lane * ne);
-  __syncwarp();
-  if (lane < 2 * ne) {
-    const LaneAgg w = lanes_reduce(v.aggs, ne, lane);
-    const int k = lane < ne ? lane : lane - ne;
-    const int64_t o = (int64_t)k * a.nseg + s;
-    if (lane < ne) {
+  lane_load(a, g, s, lane, r);
+  for (int k = 0; k < ne; ++k) {
+    const cplx sk = mt.s[k];
+    cplx F = {0.0, 0.0}, Pp = {1.0, 0.0}, G = {0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      const cplx d = decay_exact(sk.re, sk.im, r.g[i]);
+      F = cmad(d, F, cplx{r.b[i], 0.0});
+      Pp = cmul(Pp, d);
+      G.re = fma(r.b[i], Pp.re, G.re);
+      G.im = fma(r.b[i], Pp.im, G.im);
+    }
+    const LaneAgg w = warp_reduce_agg(LaneAgg{Pp, F, G});
+    if (lane == 0) {
+      const int64_t o = (int64_t)k * a.nseg + s;
       ts.A[o] = w.A;
       ts.F[o] = w.F;
-    } else {
       ts.G[o] = w.G;
     }
   }
@@ -585,12 +572,10 @@ __global__ void __launch_bounds__(kThreads, 4)
   const int ne = P.ne;
   const SegGeom g = seg_geom(a, s);
   SegSmemView v = warp_smem(wbase, ne, warp);
-  warp_load_segment(a, g, v.sd, lane);
   LaneRun r;
-  lane_merge(g, v.sd, lane, r);
+  lane_load(a, g, s, lane, r);
   const int D = pick_degree(P, warp_max(r.gmax));
   const int DM = pick_degree(P, warp_max(0.5 * r.span));
-  __syncwarp();  // segment data dead: aggs alias it
 
   LaneAgg* mine = v.aggs + lane * ne;
   dispatch_pass1(D, DM, mt, ne, r, mine);
@@ -635,6 +620,54 @@ __global__ void partition_kernel(const double* __restrict__ xs, int64_t M,
   int64_t diag = t * seg;
   if (diag > M + N) diag = M + N;
   seg_ib[t] = merge_path(xs, M, ys, N, diag);
+}
+
+// Plan-time segment metadata, one warp per segment: merge the segment's runs
+// straight from global memory once, record (zprev, zlast) and one bit per
+// merged element (1 = target) so that the apply kernels never merge.
+__global__ void __launch_bounds__(128)
+    seg_meta_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
+                    int64_t N, const int64_t* __restrict__ seg_ib, int64_t nseg,
+                    double2* __restrict__ seg_z, uint32_t* __restrict__ seg_mask) {
+  const int lane = threadIdx.x & 31;
+  const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (s >= nseg) return;
+  const int64_t L = M + N;
+  const int64_t d0 = s * kSeg;
+  const int64_t d1 = (d0 + kSeg < L) ? d0 + kSeg : L;
+  const int64_t ib = seg_ib[s], ie = seg_ib[s + 1];
+  const int64_t jb = d0 - ib, je = d1 - ie;
+  const int nx = (int)(ie - ib), ny = (int)(je - jb), len = (int)(d1 - d0);
+  const double* x = xs + ib;
+  const double* y = ys + jb;
+  const int ld = lane * kR;
+  const int dd = ld < len ? ld : len;
+  int i = (int)merge_path(x, (int64_t)nx, y, (int64_t)ny, (int64_t)dd);
+  int j = dd - i;
+  unsigned byte = 0u;
+#pragma unroll
+  for (int e = 0; e < kR; ++e) {
+    if (ld + e < len) {
+      const bool src = (j < ny) && (i >= nx || y[j] <= x[i]);
+      if (src) {
+        ++j;
+      } else {
+        byte |= 1u << e;
+        ++i;
+      }
+    }
+  }
+  unsigned w = byte << ((lane & 3) * 8);
+  w |= __shfl_down_sync(0xffffffffu, w, 1);
+  w |= __shfl_down_sync(0xffffffffu, w, 2);
+  if ((lane & 3) == 0) seg_mask[s * (kSeg / 32) + (lane >> 2)] = w;
+  if (lane == 0) {
+    const double px = ib > 0 ? xs[ib - 1] : -INFINITY;
+    const double py = jb > 0 ? ys[jb - 1] : -INFINITY;
+    const double lx = nx > 0 ? xs[ie - 1] : -INFINITY;
+    const double ly = ny > 0 ? ys[je - 1] : -INFINITY;
+    seg_z[s] = make_double2(fmax(px, py), fmax(lx, ly));
+  }
 }
 
 // ------------------------------------------------------------------- K2
@@ -835,6 +868,16 @@ cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int6
   return cudaGetLastError();
 }
 
+cudaError_t launch_seg_meta(const double* xs, int64_t M, const double* ys, int64_t N,
+                            const int64_t* seg_ib, int64_t nseg, double2* seg_z,
+                            uint32_t* seg_mask, cudaStream_t st) {
+  if (nseg == 0) return cudaSuccess;
+  note_launch();
+  seg_meta_kernel<<<(unsigned)((nseg + 3) / 4), 128, 0, st>>>(xs, M, ys, N, seg_ib, nseg, seg_z,
+                                                               seg_mask);
+  return cudaGetLastError();
+}
+
 template <class K>
 static cudaError_t set_smem(K kernel, bool& done) {
   if (done) return cudaSuccess;
@@ -847,12 +890,9 @@ static cudaError_t set_smem(K kernel, bool& done) {
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, cudaStream_t st) {
   if (a.nseg == 0) return cudaSuccess;
-  static bool done = false;
-  cudaError_t e = set_smem(seg_aggregate_kernel, done);
-  if (e != cudaSuccess) return e;
   const unsigned grid = (unsigned)((a.nseg + kSegWarps - 1) / kSegWarps);
   note_launch();
-  seg_aggregate_kernel<<<grid, kThreads, seg_smem_bytes(P.ne), st>>>(a, P, mt, ts);
+  seg_aggregate_kernel<<<grid, kThreads, 0, st>>>(a, P, mt, ts);
   return cudaGetLastError();
 }
 

@@ -33,6 +33,10 @@ struct StreamArgs {
   const int64_t* seg_ib;  // [nseg+1] targets preceding each segment
   int64_t nseg;
   double zprev0;  // coordinate of the element before this chunk (or its first)
+  // plan-time segment metadata (seg_meta): (zprev, zlast) per segment and
+  // the merged order as one bit per element (1 = target), 8 words/segment
+  const double2* seg_z;
+  const uint32_t* seg_mask;
 };
 
 struct OutArgs {
@@ -62,6 +66,10 @@ size_t seg_smem_bytes(int ne);
 
 cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int64_t N,
                              int64_t seg, int64_t nseg, int64_t* seg_ib, cudaStream_t st);
+// Plan-time segment metadata: seg_z[s] = (zprev, zlast), seg_mask.
+cudaError_t launch_seg_meta(const double* xs, int64_t M, const double* ys, int64_t N,
+                            const int64_t* seg_ib, int64_t nseg, double2* seg_z,
+                            uint32_t* seg_mask, cudaStream_t st);
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, cudaStream_t st);
 // K2: exclusive carries per segment.  carry_in: 2*ne complex (forward carry at
