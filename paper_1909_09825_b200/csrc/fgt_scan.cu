@@ -142,25 +142,39 @@ __device__ __forceinline__ SegGeom seg_geom(const StreamArgs& a, int64_t s) {
 // ------------------------------------------------------------- lane runs
 
 struct LaneRun {
-  double g[kR];  // gap to the previous merged element
-  double b[kR];  // strength if source, 0 if target / padding
+  double g[kR];    // gap to the previous merged element
+  double b[kR];    // strength if source, 0 if target / padding
   unsigned tmask;  // bit e: element e is a target
   int tfirst;      // segment-local index of the lane's first target
   double gmax;     // largest gap
-  double span;     // last coordinate of the run minus the coordinate before it
 };
 
+// Segment frame: centre zc and half-widths h0 = zc - zprev, h1 = zlast - zc.
+struct SegFrame {
+  double zc, h0, h1;
+};
+
+__device__ __forceinline__ SegFrame seg_frame(const SegGeom& g) {
+  const double h = 0.5 * (g.zlast - g.zprev);
+  SegFrame f;
+  f.zc = g.zprev + h;
+  f.h0 = f.zc - g.zprev;
+  f.h1 = g.zlast - f.zc;
+  return f;
+}
+
 // Lane run from the plan-time merge mask: no merge, no shared-memory
-// staging; every element is an independent load.
+// staging; every element is an independent load.  Coordinates are left in
+// r.g (converted to gaps by lane_gaps); zp = coordinate preceding the run,
+// zl = coordinate of its last element.
 __device__ __forceinline__ void lane_load(const StreamArgs& a, const SegGeom& g, int64_t s,
-                                          int lane, LaneRun& r) {
+                                          int lane, LaneRun& r, double& zp, double& zl) {
   const uint32_t word = __ldg(a.seg_mask + s * (kSeg / 32) + (lane >> 2));
   const int d0 = lane * kR;
   const int nreal = g.len - d0 < 0 ? 0 : (g.len - d0 < kR ? g.len - d0 : kR);
-  const unsigned live = nreal >= 32 ? 0xffffffffu : ((1u << nreal) - 1u);
+  const unsigned live = (1u << nreal) - 1u;
   const unsigned byte = (word >> ((lane & 3) * 8)) & 0xffu & live;
   const int nt = __popc(byte);
-  // exclusive warp prefix of the target counts
   int incl = nt;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -171,7 +185,6 @@ __device__ __forceinline__ void lane_load(const StreamArgs& a, const SegGeom& g,
   const int j0 = (d0 < g.len ? d0 : g.len) - i0;
   r.tfirst = i0;
   r.tmask = byte;
-  double z[kR];
   double last = 0.0;
 #pragma unroll
   for (int e = 0; e < kR; ++e) {
@@ -179,135 +192,22 @@ __device__ __forceinline__ void lane_load(const StreamArgs& a, const SegGeom& g,
     const int sidx = e - t;
     if (e < nreal) {
       if (byte & (1u << e)) {
-        z[e] = __ldg(a.xs + g.ib + i0 + t);
+        r.g[e] = __ldg(a.xs + g.ib + i0 + t);
         r.b[e] = 0.0;
       } else {
-        z[e] = __ldg(a.ys + g.jb + j0 + sidx);
+        r.g[e] = __ldg(a.ys + g.jb + j0 + sidx);
         r.b[e] = __ldg(a.bs + g.jb + j0 + sidx);
       }
-      last = z[e];
+      last = r.g[e];
     } else {
-      z[e] = 0.0;
+      r.g[e] = 0.0;
       r.b[e] = 0.0;
     }
   }
-  // coordinate preceding the run: the previous lane's last element
   double prev = __shfl_up_sync(0xffffffffu, last, 1);
   if (lane == 0) prev = g.zprev;
-  const double start = prev;
-  r.gmax = 0.0;
-#pragma unroll
-  for (int e = 0; e < kR; ++e) {
-    if (e < nreal) {
-      r.g[e] = z[e] - prev;
-      prev = z[e];
-    } else {
-      r.g[e] = 0.0;
-    }
-    r.gmax = fmax(r.gmax, r.g[e]);
-  }
-  r.span = nreal > 0 ? prev - start : 0.0;
-}
-
-// --------------------------------------------------------------- pass 1
-
-// Exact per-element lane aggregates (robust path for wide runs):
-//   A = prod d_i, F = forward state at the run end, G = backward state at
-//   the element before the run.
-template <int D>
-__device__ __forceinline__ void pass1_elements(const ModeTable& mt, int ne, const LaneRun& r,
-                                               LaneAgg* out) {
-  for (int k = 0; k < ne; ++k) {
-    Coef<D> c;
-    c.load(mt, k);
-    const cplx s = mt.s[k];
-    cplx F = {0.0, 0.0}, P = {1.0, 0.0}, G = {0.0, 0.0};
-#pragma unroll
-    for (int i = 0; i < kR; ++i) {
-      const cplx d = gap_factor<D>(c, s, r.g[i]);
-      F = cmad(d, F, cplx{r.b[i], 0.0});
-      P = cmul(P, d);
-      G.re = fma(r.b[i], P.re, G.re);
-      G.im = fma(r.b[i], P.im, G.im);
-    }
-    out[k] = LaneAgg{P, F, G};
-  }
-}
-
-// Moment form of the lane aggregates: with h = span/2 and d_i the position of
-// source i relative to the run's midpoint,
-//   F = e^{-s h} sum_i b_i e^{+s d_i},  G = e^{-s h} sum_i b_i e^{-s d_i},
-//   A = (e^{-s h})^2,
-// and e^{-/+ s d} = sum_n (-/+ s)^n d^n / n! truncated at DM (|s| h <= rmax[DM]),
-// so the per-source work is mode independent: M_n = sum_i b_i d_i^n.
-template <int DM>
-__device__ __forceinline__ void pass1_moments(const ModeTable& mt, int ne, const LaneRun& r,
-                                              LaneAgg* out) {
-  const double h = 0.5 * r.span;
-  double M[DM + 1];
-#pragma unroll
-  for (int n = 0; n <= DM; ++n) M[n] = 0.0;
-  double pos = 0.0;
-#pragma unroll
-  for (int i = 0; i < kR; ++i) {
-    pos += r.g[i];
-    const double d = pos - h;
-    double p = r.b[i];
-    M[0] += p;
-#pragma unroll
-    for (int n = 1; n <= DM; ++n) {
-      p *= d;
-      M[n] += p;
-    }
-  }
-  for (int k = 0; k < ne; ++k) {
-    Coef<DM> c;
-    c.load(mt, k);
-    cplx ev = {0.0, 0.0}, od = {0.0, 0.0};
-#pragma unroll
-    for (int n = 0; n <= DM; ++n) {
-      if (n & 1) {
-        od.re = fma(c[n].re, M[n], od.re);
-        od.im = fma(c[n].im, M[n], od.im);
-      } else {
-        ev.re = fma(c[n].re, M[n], ev.re);
-        ev.im = fma(c[n].im, M[n], ev.im);
-      }
-    }
-    const cplx E = horner<DM>(c, h);
-    out[k].A = cmul(E, E);
-    out[k].F = cmul(E, cplx{ev.re - od.re, ev.im - od.im});
-    out[k].G = cmul(E, cplx{ev.re + od.re, ev.im + od.im});
-  }
-}
-
-__device__ __forceinline__ void dispatch_pass1(int D, int DM, const ModeTable& mt, int ne,
-                                               const LaneRun& r, LaneAgg* out) {
-  if (D >= 0 && DM >= 0) {
-    switch (DM) {
-#define FGT_P1M(n)                           \
-  case n:                                    \
-    pass1_moments<n>(mt, ne, r, out);        \
-    return;
-      FGT_P1M(0) FGT_P1M(1) FGT_P1M(2) FGT_P1M(3) FGT_P1M(4) FGT_P1M(5) FGT_P1M(6)
-      FGT_P1M(7) FGT_P1M(8)
-#undef FGT_P1M
-      default:
-        break;
-    }
-  }
-  switch (D) {
-#define FGT_P1E(n)                           \
-  case n:                                    \
-    pass1_elements<n>(mt, ne, r, out);       \
-    return;
-    FGT_P1E(0) FGT_P1E(1) FGT_P1E(2) FGT_P1E(3) FGT_P1E(4) FGT_P1E(5) FGT_P1E(6) FGT_P1E(7)
-    FGT_P1E(8) FGT_P1E(9) FGT_P1E(10) FGT_P1E(11) FGT_P1E(12) FGT_P1E(13) FGT_P1E(14)
-    FGT_P1E(15) FGT_P1E(16)
-#undef FGT_P1E
-    default:
-      pass1_elements<-1>(mt, ne, r, out);
-  }
+  zp = prev;
+  zl = nreal > 0 ? last : prev;
 }
 
 // --------------------------------------------------------------- pass 2
@@ -321,14 +221,20 @@ struct ModeSumsOut {
   int64_t t0;  // global sorted index of this lane's first target
 };
 
-// Forward and backward recurrences seeded with the lane carries (carry[k].F
-// = forward state at the element before the run, carry[k].G = backward state
-// at the run's last element), accumulating Re(mw_k (H + K)) into out[] (only
-// target slots are used).  Gap factors are kept in registers between the two
-// sweeps.
+// Lane carries of one mode: cf = forward state at the element before the
+// run, cb = backward state at the run's last element.
+struct Carry {
+  cplx cf, cb;
+};
+
+// Forward and backward recurrences seeded with the lane carries,
+// accumulating Re(mw_k (H + K)) into out[] (only target slots are used).
+// With Kt_i = K_i + b_i the backward step is Kt_{i-1} = d_i Kt_i + b_{i-1},
+// the same multiply-add as the forward step; the two chains are independent
+// and interleaved for instruction-level parallelism.
 template <int D, bool MS>
 __device__ __forceinline__ void pass2(const ModeTable& mt, int ne, const LaneRun& r,
-                                      const LaneAgg* carry, double (&out)[kR],
+                                      const Carry* carry, double (&out)[kR],
                                       const ModeSumsOut& ms) {
   for (int k = 0; k < ne; ++k) {
     Coef<D> c;
@@ -336,34 +242,39 @@ __device__ __forceinline__ void pass2(const ModeTable& mt, int ne, const LaneRun
     const cplx s = mt.s[k];
     const cplx mw = mt.mw[k];
     cplx d[kR];
-    cplx H = carry[k].F;
-    int64_t ti = ms.t0;
 #pragma unroll
-    for (int i = 0; i < kR; ++i) {
-      d[i] = gap_factor<D>(c, s, r.g[i]);
-      H = cmad(d[i], H, cplx{r.b[i], 0.0});
-      if constexpr (MS) {
+    for (int i = 0; i < kR; ++i) d[i] = gap_factor<D>(c, s, r.g[i]);
+    cplx H = carry[k].cf;
+    cplx K = carry[k].cb;
+    K.re += r.b[kR - 1];
+    if constexpr (MS) {
+      int64_t ti = ms.t0;
+#pragma unroll
+      for (int i = 0; i < kR; ++i) {
+        H = cmad(d[i], H, cplx{r.b[i], 0.0});
         if (r.tmask & (1u << i)) ms.hp[(int64_t)k * ms.M + ti++] = H;
-      } else {
-        out[i] = fma(mw.re, H.re, fma(-mw.im, H.im, out[i]));
       }
-    }
-    cplx K = carry[k].G;
 #pragma unroll
-    for (int i = kR - 1; i >= 0; --i) {
-      if constexpr (MS) {
-        if (r.tmask & (1u << i)) ms.hm[(int64_t)k * ms.M + (--ti)] = K;
-      } else {
-        out[i] = fma(mw.re, K.re, fma(-mw.im, K.im, out[i]));
+      for (int i = kR - 1; i >= 0; --i) {
+        if (r.tmask & (1u << i)) ms.hm[(int64_t)k * ms.M + (--ti)] = K;  // b_i = 0
+        if (i > 0) K = cmad(d[i], K, cplx{r.b[i - 1], 0.0});
       }
-      K = cmul(d[i], cplx{K.re + r.b[i], K.im});
+    } else {
+#pragma unroll
+      for (int i = 0; i < kR; ++i) {
+        H = cmad(d[i], H, cplx{r.b[i], 0.0});
+        out[i] = fma(mw.re, H.re, fma(-mw.im, H.im, out[i]));
+        const int j = kR - 1 - i;
+        out[j] = fma(mw.re, K.re, fma(-mw.im, K.im, out[j]));
+        if (j > 0) K = cmad(d[j], K, cplx{r.b[j - 1], 0.0});
+      }
     }
   }
 }
 
 template <bool MS>
 __device__ __forceinline__ void dispatch_pass2(int D, const ModeTable& mt, int ne,
-                                               const LaneRun& r, const LaneAgg* carry,
+                                               const LaneRun& r, const Carry* carry,
                                                double (&out)[kR], const ModeSumsOut& ms) {
   switch (D) {
 #define FGT_P2(n)                                 \
@@ -379,63 +290,161 @@ __device__ __forceinline__ void dispatch_pass2(int D, const ModeTable& mt, int n
   }
 }
 
-// ------------------------------------------------- sequential lane scans
-// Lanes q < 2 ne of a warp: q < ne forward for mode q, ne <= q < 2 ne
-// backward for mode q - ne.  aggs is [32 lanes][ne].
+// ------------------------------------------------------- lane carries
 
-// Exclusive lane carries written in place: forward into .F, backward into .G
-__device__ __forceinline__ void lanes_carry(LaneAgg* aggs, int ne, int q, cplx cin) {
-  if (q < ne) {
-    cplx c = cin;
-    for (int l = 0; l < 32; ++l) {
-      LaneAgg& x = aggs[l * ne + q];
-      const cplx A = x.A, F = x.F;
-      x.F = c;
-      c = cmad(A, c, F);
+// Moment form (narrow segments, |s| max(h0, h1) <= rmax[DM]).  With
+// d = z - zc and M_n = sum_{sources of the lane} b d^n (mode independent),
+// P_n = exclusive prefix of M_n over lanes, S_n = suffix (lanes after):
+//   cf = e^{-s u} [ sum_n s^n/n! P_n + e^{-s h0} Cf_seg ],   u = zp - zc
+//   cb = e^{+s v} [ sum_n (-s)^n/n! S_n + e^{-s h1} Cb_seg ], v = zl - zc
+// All exponentials have |argument| <= rmax[DM] and are Taylor polynomials.
+template <int DM>
+__device__ __forceinline__ void carries_moments(const ModeTable& mt, int ne, const LaneRun& r,
+                                                const SegFrame& f, double zp, double zl,
+                                                int lane, cplx seg_term, Carry* out) {
+  double P[DM + 1], S[DM + 1];
+  {
+    double M[DM + 1];
+#pragma unroll
+    for (int n = 0; n <= DM; ++n) M[n] = 0.0;
+#pragma unroll
+    for (int e = 0; e < kR; ++e) {
+      const double d = r.g[e] - f.zc;  // r.g holds coordinates here
+      double p = r.b[e];
+      M[0] += p;
+#pragma unroll
+      for (int n = 1; n <= DM; ++n) {
+        p *= d;
+        M[n] += p;
+      }
     }
-  } else {
-    const int k = q - ne;
-    cplx c = cin;
-    for (int l = 31; l >= 0; --l) {
-      LaneAgg& x = aggs[l * ne + k];
-      const cplx A = x.A, G = x.G;
-      x.G = c;
-      c = cmad(A, c, G);
+#pragma unroll
+    for (int n = 0; n <= DM; ++n) {
+      double incl = M[n];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      const double tot = __shfl_sync(0xffffffffu, incl, 31);
+      P[n] = incl - M[n];
+      S[n] = tot - incl;
     }
   }
+  const double u = zp - f.zc, v = zl - f.zc;
+  for (int k = 0; k < ne; ++k) {
+    Coef<DM> c;
+    c.load(mt, k);
+    cplx fp = {0.0, 0.0}, bs = {0.0, 0.0};
+#pragma unroll
+    for (int n = 0; n <= DM; ++n) {
+      const cplx cn = c[n];
+      const double sg = (n & 1) ? -1.0 : 1.0;  // s^n/n! = (-1)^n c_n
+      fp.re = fma(sg * cn.re, P[n], fp.re);
+      fp.im = fma(sg * cn.im, P[n], fp.im);
+      bs.re = fma(cn.re, S[n], bs.re);
+      bs.im = fma(cn.im, S[n], bs.im);
+    }
+    // segment carries propagated to the frame: lane k holds mode k's forward
+    // term, lane ne + k the backward one
+    cplx tf, tb;
+    tf.re = __shfl_sync(0xffffffffu, seg_term.re, k);
+    tf.im = __shfl_sync(0xffffffffu, seg_term.im, k);
+    tb.re = __shfl_sync(0xffffffffu, seg_term.re, ne + k);
+    tb.im = __shfl_sync(0xffffffffu, seg_term.im, ne + k);
+    const cplx eu = horner<DM>(c, u);
+    const cplx ev = horner<DM>(c, -v);
+    out[k].cf = cmul(eu, cplx{fp.re + tf.re, fp.im + tf.im});
+    out[k].cb = cmul(ev, cplx{bs.re + tb.re, bs.im + tb.im});
+  }
+}
+
+// Robust form (wide segments): exact per-element lane aggregates and
+// shuffle (Kogge-Stone) exclusive scans across the warp, both directions.
+__device__ __forceinline__ void carries_scan(const ModeTable& mt, int ne, const LaneRun& r,
+                                             int lane, cplx cf_seg, cplx cb_seg, int q_has,
+                                             Carry* out) {
+  for (int k = 0; k < ne; ++k) {
+    const cplx sk = mt.s[k];
+    cplx F = {0.0, 0.0}, A = {1.0, 0.0}, G = {0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      const cplx d = decay_exact(sk.re, sk.im, r.g[i]);
+      F = cmad(d, F, cplx{r.b[i], 0.0});
+      A = cmul(A, d);
+      G.re = fma(r.b[i], A.re, G.re);
+      G.im = fma(r.b[i], A.im, G.im);
+    }
+    // forward inclusive scan of (A, F) over lanes (earlier then later)
+    cplx fa = A, ff = F;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      cplx pa, pf;
+      pa.re = __shfl_up_sync(0xffffffffu, fa.re, o);
+      pa.im = __shfl_up_sync(0xffffffffu, fa.im, o);
+      pf.re = __shfl_up_sync(0xffffffffu, ff.re, o);
+      pf.im = __shfl_up_sync(0xffffffffu, ff.im, o);
+      if (lane >= o) {
+        ff = cmad(fa, pf, ff);
+        fa = cmul(pa, fa);
+      }
+    }
+    // backward inclusive scan of (A, G) from the right
+    cplx ba = A, bg = G;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      cplx pa, pg;
+      pa.re = __shfl_down_sync(0xffffffffu, ba.re, o);
+      pa.im = __shfl_down_sync(0xffffffffu, ba.im, o);
+      pg.re = __shfl_down_sync(0xffffffffu, bg.re, o);
+      pg.im = __shfl_down_sync(0xffffffffu, bg.im, o);
+      if (lane + o < 32) {
+        bg = cmad(ba, pg, bg);
+        ba = cmul(ba, pa);
+      }
+    }
+    // exclusive: shift by one lane and apply the segment carries
+    const cplx cfs = {__shfl_sync(0xffffffffu, cf_seg.re, k), __shfl_sync(0xffffffffu, cf_seg.im, k)};
+    const cplx cbs = {__shfl_sync(0xffffffffu, cb_seg.re, ne + k),
+                      __shfl_sync(0xffffffffu, cb_seg.im, ne + k)};
+    cplx xa = {__shfl_up_sync(0xffffffffu, fa.re, 1), __shfl_up_sync(0xffffffffu, fa.im, 1)};
+    cplx xf = {__shfl_up_sync(0xffffffffu, ff.re, 1), __shfl_up_sync(0xffffffffu, ff.im, 1)};
+    if (lane == 0) {
+      xa = {1.0, 0.0};
+      xf = {0.0, 0.0};
+    }
+    cplx ya = {__shfl_down_sync(0xffffffffu, ba.re, 1), __shfl_down_sync(0xffffffffu, ba.im, 1)};
+    cplx yg = {__shfl_down_sync(0xffffffffu, bg.re, 1), __shfl_down_sync(0xffffffffu, bg.im, 1)};
+    if (lane == 31) {
+      ya = {1.0, 0.0};
+      yg = {0.0, 0.0};
+    }
+    out[k].cf = cmad(xa, cfs, xf);
+    out[k].cb = cmad(ya, cbs, yg);
+  }
+  (void)q_has;
 }
 
 // -------------------------------------------------------- shared memory
 
-// Per-warp region of K3: lane aggregates / carries, then the output staging.
+// Per-warp region of K3: lane carries, then the output staging.
 __host__ __device__ __forceinline__ size_t warp_region_bytes(int ne) {
-  return sizeof(LaneAgg) * 32 * (size_t)ne + sizeof(double) * kSeg;
-}
-
-struct SegSmemView {
-  LaneAgg* aggs;
-  double* su;
-};
-
-__device__ __forceinline__ SegSmemView warp_smem(unsigned char* base, int ne, int warp) {
-  unsigned char* w = base + (size_t)warp * warp_region_bytes(ne);
-  SegSmemView v;
-  v.aggs = reinterpret_cast<LaneAgg*>(w);
-  v.su = reinterpret_cast<double*>(w + sizeof(LaneAgg) * 32 * (size_t)ne);
-  return v;
+  return sizeof(Carry) * 32 * (size_t)ne + sizeof(double) * kSeg;
 }
 
 // ------------------------------------------------------------------- K1
 
 template <int DM>
-__device__ __forceinline__ void seg_moments(const StreamArgs& a, const SegGeom& g, double h,
-                                            int lane, double (&M)[kMaxMom + 1]) {
+__device__ __forceinline__ void seg_aggregate_moments(const StreamArgs& a, const SegGeom& g,
+                                                      const SegFrame& f, const ModeTable& mt,
+                                                      int ne, int lane, int64_t s, TileState ts) {
+  double M[DM + 1];
 #pragma unroll
   for (int n = 0; n <= DM; ++n) M[n] = 0.0;
   for (int j = lane; j < g.ny; j += 32) {
     const double y = __ldg(a.ys + g.jb + j);
     double p = __ldg(a.bs + g.jb + j);
-    const double d = (y - g.zprev) - h;
+    const double d = y - f.zc;
     M[0] += p;
 #pragma unroll
     for (int n = 1; n <= DM; ++n) {
@@ -448,37 +457,28 @@ __device__ __forceinline__ void seg_moments(const StreamArgs& a, const SegGeom& 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) M[n] += __shfl_xor_sync(0xffffffffu, M[n], o);
   }
-}
-
-template <int DM>
-__device__ __forceinline__ void seg_aggregate_moments(const StreamArgs& a, const SegGeom& g,
-                                                      const ModeTable& mt, int ne, int lane,
-                                                      int64_t s, TileState ts) {
-  const double L = g.zlast - g.zprev;
-  const double h = 0.5 * L;
-  double M[kMaxMom + 1];
-  seg_moments<DM>(a, g, h, lane, M);
   if (lane < ne) {
     const int k = lane;
+    Coef<DM> c;
+    c.load(mt, k);
     cplx ev = {0.0, 0.0}, od = {0.0, 0.0};
 #pragma unroll
     for (int n = 0; n <= DM; ++n) {
-      const cplx c = mt.coef[k][n];
+      const cplx cn = c[n];
       if (n & 1) {
-        od.re = fma(c.re, M[n], od.re);
-        od.im = fma(c.im, M[n], od.im);
+        od.re = fma(cn.re, M[n], od.re);
+        od.im = fma(cn.im, M[n], od.im);
       } else {
-        ev.re = fma(c.re, M[n], ev.re);
-        ev.im = fma(c.im, M[n], ev.im);
+        ev.re = fma(cn.re, M[n], ev.re);
+        ev.im = fma(cn.im, M[n], ev.im);
       }
     }
-    Coef<DM> c;
-    c.load(mt, k);
-    const cplx E = horner<DM>(c, h);
+    const cplx E0 = horner<DM>(c, f.h0);
+    const cplx E1 = horner<DM>(c, f.h1);
     const int64_t o = (int64_t)k * a.nseg + s;
-    ts.A[o] = cmul(E, E);
-    ts.F[o] = cmul(E, cplx{ev.re - od.re, ev.im - od.im});
-    ts.G[o] = cmul(E, cplx{ev.re + od.re, ev.im + od.im});
+    ts.A[o] = cmul(E0, E1);
+    ts.F[o] = cmul(E1, cplx{ev.re - od.re, ev.im - od.im});
+    ts.G[o] = cmul(E0, cplx{ev.re + od.re, ev.im + od.im});
   }
 }
 
@@ -505,9 +505,14 @@ __device__ __forceinline__ LaneAgg warp_reduce_agg(LaneAgg v) {
   return v;
 }
 
-// K1: one warp per segment.  Moment path when the segment is narrow
-// (|s| h <= rmax[kRegDeg]); otherwise exact per-element lane aggregates from
-// the merge mask, reduced across the warp.
+__device__ __forceinline__ int seg_moment_degree(const ModeParams& P, const SegFrame& f) {
+  const int DM = pick_degree(P, fmax(f.h0, f.h1));
+  return DM <= kRegDeg ? DM : -1;
+}
+
+// K1: warps loop over segments (grid-stride).  Moment path for narrow
+// segments; exact per-element lane aggregates reduced across the warp
+// otherwise.
 __global__ void __launch_bounds__(kThreads)
     seg_aggregate_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
                          TileState ts) {
@@ -515,42 +520,58 @@ __global__ void __launch_bounds__(kThreads)
   load_mode_table(mtab, mt);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t s = (int64_t)blockIdx.x * kSegWarps + warp;
-  if (s >= a.nseg) return;
   const int ne = P.ne;
-  const SegGeom g = seg_geom(a, s);
-  const int DM = pick_degree(P, 0.5 * (g.zlast - g.zprev));
-  switch (DM) {
-#define FGT_K1(n)                                                 \
-  case n:                                                         \
-    seg_aggregate_moments<n>(a, g, mt, ne, lane, s, ts);          \
-    return;
-    FGT_K1(0) FGT_K1(1) FGT_K1(2) FGT_K1(3) FGT_K1(4) FGT_K1(5) FGT_K1(6) FGT_K1(7)
-    FGT_K1(8)
+  for (int64_t s = (int64_t)blockIdx.x * kSegWarps + warp; s < a.nseg;
+       s += (int64_t)gridDim.x * kSegWarps) {
+    const SegGeom g = seg_geom(a, s);
+    const SegFrame f = seg_frame(g);
+    const int DM = seg_moment_degree(P, f);
+    switch (DM) {
+#define FGT_K1(n)                                                  \
+  case n:                                                          \
+    seg_aggregate_moments<n>(a, g, f, mt, ne, lane, s, ts);        \
+    continue;
+      FGT_K1(0) FGT_K1(1) FGT_K1(2) FGT_K1(3) FGT_K1(4) FGT_K1(5) FGT_K1(6) FGT_K1(7)
+      FGT_K1(8)
 #undef FGT_K1
-    default:
-      break;
-  }
-  // Wide segment: exact per-element lane aggregates, ordered warp reduction.
-  LaneRun r;
-  lane_load(a, g, s, lane, r);
-  for (int k = 0; k < ne; ++k) {
-    const cplx sk = mt.s[k];
-    cplx F = {0.0, 0.0}, Pp = {1.0, 0.0}, G = {0.0, 0.0};
-#pragma unroll
-    for (int i = 0; i < kR; ++i) {
-      const cplx d = decay_exact(sk.re, sk.im, r.g[i]);
-      F = cmad(d, F, cplx{r.b[i], 0.0});
-      Pp = cmul(Pp, d);
-      G.re = fma(r.b[i], Pp.re, G.re);
-      G.im = fma(r.b[i], Pp.im, G.im);
+      default:
+        break;
     }
-    const LaneAgg w = warp_reduce_agg(LaneAgg{Pp, F, G});
-    if (lane == 0) {
-      const int64_t o = (int64_t)k * a.nseg + s;
-      ts.A[o] = w.A;
-      ts.F[o] = w.F;
-      ts.G[o] = w.G;
+    LaneRun r;
+    double zp, zl;
+    lane_load(a, g, s, lane, r, zp, zl);
+    {
+      double prev = zp;
+      const int nreal = g.len - lane * kR;
+#pragma unroll
+      for (int e = 0; e < kR; ++e) {
+        if (e < nreal) {
+          const double z = r.g[e];
+          r.g[e] = z - prev;
+          prev = z;
+        } else {
+          r.g[e] = 0.0;
+        }
+      }
+    }
+    for (int k = 0; k < ne; ++k) {
+      const cplx sk = mt.s[k];
+      cplx F = {0.0, 0.0}, Pp = {1.0, 0.0}, G = {0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < kR; ++i) {
+        const cplx d = decay_exact(sk.re, sk.im, r.g[i]);
+        F = cmad(d, F, cplx{r.b[i], 0.0});
+        Pp = cmul(Pp, d);
+        G.re = fma(r.b[i], Pp.re, G.re);
+        G.im = fma(r.b[i], Pp.im, G.im);
+      }
+      const LaneAgg w = warp_reduce_agg(LaneAgg{Pp, F, G});
+      if (lane == 0) {
+        const int64_t o = (int64_t)k * a.nseg + s;
+        ts.A[o] = w.A;
+        ts.F[o] = w.F;
+        ts.G[o] = w.G;
+      }
     }
   }
 }
@@ -563,50 +584,100 @@ __global__ void __launch_bounds__(kThreads, 4)
                     TileState ts, OutArgs o) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ModeTable& mt = *reinterpret_cast<ModeTable*>(smem_raw);
-  unsigned char* wbase = smem_raw + sizeof(ModeTable);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ne = P.ne;
+  unsigned char* wreg = smem_raw + sizeof(ModeTable) + (size_t)warp * warp_region_bytes(ne);
+  Carry* carries = reinterpret_cast<Carry*>(wreg);
+  double* su = reinterpret_cast<double*>(wreg + sizeof(Carry) * 32 * (size_t)ne);
   load_mode_table(mtab, mt);
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t s = (int64_t)blockIdx.x * kSegWarps + warp;
-  if (s >= a.nseg) return;
-  const int ne = P.ne;
-  const SegGeom g = seg_geom(a, s);
-  SegSmemView v = warp_smem(wbase, ne, warp);
-  LaneRun r;
-  lane_load(a, g, s, lane, r);
-  const int D = pick_degree(P, warp_max(r.gmax));
-  const int DM = pick_degree(P, warp_max(0.5 * r.span));
-
-  LaneAgg* mine = v.aggs + lane * ne;
-  dispatch_pass1(D, DM, mt, ne, r, mine);
-  __syncwarp();
-  if (lane < 2 * ne) {
-    const int k = lane < ne ? lane : lane - ne;
-    const int64_t idx = (int64_t)k * a.nseg + s;
-    lanes_carry(v.aggs, ne, lane, lane < ne ? ts.Cf[idx] : ts.Cb[idx]);
-  }
-  __syncwarp();
-
-  double out[kR];
-#pragma unroll
-  for (int e = 0; e < kR; ++e) out[e] = 0.0;
-  if constexpr (MS) {
-    ModeSumsOut ms{o.hp, o.hm, a.M, o.u_offset + g.ib + r.tfirst};
-    dispatch_pass2<true>(D, mt, ne, r, mine, out, ms);
-    return;
-  } else {
-    dispatch_pass2<false>(D, mt, ne, r, mine, out, ModeSumsOut{nullptr, nullptr, 0, 0});
-    int tk = r.tfirst;
-#pragma unroll
-    for (int e = 0; e < kR; ++e)
-      if (r.tmask & (1u << e)) v.su[tk++] = out[e];
-    __syncwarp();
-    const int64_t base = o.u_offset + g.ib;
-    if (o.tperm) {
-      for (int i = lane; i < g.nx; i += 32) o.u[o.tperm[base + i]] = v.su[i];
-    } else {
-      for (int i = lane; i < g.nx; i += 32) o.u[base + i] = v.su[i];
+  for (int64_t s = (int64_t)blockIdx.x * kSegWarps + warp; s < a.nseg;
+       s += (int64_t)gridDim.x * kSegWarps) {
+    const SegGeom g = seg_geom(a, s);
+    const SegFrame f = seg_frame(g);
+    // segment carries: lane q < ne forward of mode q, ne <= q < 2ne backward
+    cplx seg_c = {0.0, 0.0};
+    if (lane < 2 * ne) {
+      const int k = lane < ne ? lane : lane - ne;
+      const int64_t idx = (int64_t)k * a.nseg + s;
+      seg_c = lane < ne ? ts.Cf[idx] : ts.Cb[idx];
     }
+    LaneRun r;
+    double zp, zl;
+    lane_load(a, g, s, lane, r, zp, zl);
+    const int nreal = g.len - lane * kR;
+    // gaps (coordinates are still needed by the moment path)
+    double gmax = 0.0;
+    {
+      double prev = zp;
+#pragma unroll
+      for (int e = 0; e < kR; ++e)
+        if (e < nreal) {
+          gmax = fmax(gmax, r.g[e] - prev);
+          prev = r.g[e];
+        }
+    }
+    const int D = pick_degree(P, warp_max(gmax));
+    const int DM = seg_moment_degree(P, f);
+    Carry* mine = carries + lane * ne;
+    bool done = false;
+    if (D >= 0) {
+      switch (DM) {
+#define FGT_CM(n)                                                                   \
+  case n: {                                                                         \
+    Coef<n> c;                                                                      \
+    cplx term = {0.0, 0.0};                                                         \
+    if (lane < 2 * ne) {                                                            \
+      const int k = lane < ne ? lane : lane - ne;                                   \
+      c.load(mt, k);                                                                \
+      term = cmul(horner<n>(c, lane < ne ? f.h0 : f.h1), seg_c);                    \
+    }                                                                               \
+    carries_moments<n>(mt, ne, r, f, zp, zl, lane, term, mine);                     \
+    done = true;                                                                    \
+  } break;
+        FGT_CM(0) FGT_CM(1) FGT_CM(2) FGT_CM(3) FGT_CM(4) FGT_CM(5)
+#undef FGT_CM
+        default:
+          break;
+      }
+    }
+    {
+      double prev = zp;
+#pragma unroll
+      for (int e = 0; e < kR; ++e) {
+        if (e < nreal) {
+          const double z = r.g[e];
+          r.g[e] = z - prev;
+          prev = z;
+        } else {
+          r.g[e] = 0.0;
+        }
+      }
+    }
+    if (!done) carries_scan(mt, ne, r, lane, seg_c, seg_c, 0, mine);
+    __syncwarp();
+
+    double out[kR];
+#pragma unroll
+    for (int e = 0; e < kR; ++e) out[e] = 0.0;
+    if constexpr (MS) {
+      ModeSumsOut ms{o.hp, o.hm, a.M, o.u_offset + g.ib + r.tfirst};
+      dispatch_pass2<true>(D, mt, ne, r, mine, out, ms);
+    } else {
+      dispatch_pass2<false>(D, mt, ne, r, mine, out, ModeSumsOut{nullptr, nullptr, 0, 0});
+      int tk = r.tfirst;
+#pragma unroll
+      for (int e = 0; e < kR; ++e)
+        if (r.tmask & (1u << e)) su[tk++] = out[e];
+      __syncwarp();
+      const int64_t base = o.u_offset + g.ib;
+      if (o.tperm) {
+        for (int i = lane; i < g.nx; i += 32) o.u[o.tperm[base + i]] = su[i];
+      } else {
+        for (int i = lane; i < g.nx; i += 32) o.u[base + i] = su[i];
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -842,6 +913,18 @@ __global__ void gather_kernel(const double* __restrict__ alpha, const int32_t* _
 
 // ============================================================== host side
 
+static int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      return v;
+    cudaGetLastError();
+    return 148;
+  }();
+  return n;
+}
+
 int64_t scan_blocks(int64_t nseg) { return (nseg + kScanBlock - 1) / kScanBlock; }
 
 size_t tile_state_elems(int64_t nseg, int ne) {
@@ -890,7 +973,9 @@ static cudaError_t set_smem(K kernel, bool& done) {
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, cudaStream_t st) {
   if (a.nseg == 0) return cudaSuccess;
-  const unsigned grid = (unsigned)((a.nseg + kSegWarps - 1) / kSegWarps);
+  int64_t want = (a.nseg + kSegWarps - 1) / kSegWarps;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
   note_launch();
   seg_aggregate_kernel<<<grid, kThreads, 0, st>>>(a, P, mt, ts);
   return cudaGetLastError();
@@ -903,7 +988,9 @@ static cudaError_t launch_seg_main(const StreamArgs& a, const ModeParams& P, con
   static bool done = false;
   cudaError_t e = set_smem(seg_main_kernel<MS>, done);
   if (e != cudaSuccess) return e;
-  const unsigned grid = (unsigned)((a.nseg + kSegWarps - 1) / kSegWarps);
+  int64_t want = (a.nseg + kSegWarps - 1) / kSegWarps;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
   note_launch();
   seg_main_kernel<MS><<<grid, kThreads, seg_smem_bytes(P.ne), st>>>(a, P, mt, ts, o);
   return cudaGetLastError();
