@@ -427,10 +427,9 @@ __device__ __forceinline__ void carries_scan(const ModeTable& mt, int ne, const 
 
 // -------------------------------------------------------- shared memory
 
-// Per-warp region of K3: lane carries, the output staging, and one
-// 2*kR-double prefetch slot per lane.
+// Per-warp region of K3: lane carries, then the output staging.
 __host__ __device__ __forceinline__ size_t warp_region_bytes(int ne) {
-  return sizeof(Carry) * 32 * (size_t)ne + sizeof(double) * kSeg + sizeof(double) * 32 * 2 * kR;
+  return sizeof(Carry) * 32 * (size_t)ne + sizeof(double) * kSeg;
 }
 
 // ------------------------------------------------------------------- K1
@@ -579,94 +578,6 @@ __global__ void __launch_bounds__(kThreads)
 
 // ------------------------------------------------------------------- K3
 
-// Per-segment metadata a lane needs to address its run (prefetched ahead).
-struct SegMeta {
-  int64_t ib, ie;
-  uint32_t word;  // this lane's merge-mask word
-  double2 z;      // (zprev, zlast)
-};
-
-__device__ __forceinline__ SegMeta load_meta(const StreamArgs& a, int64_t s, int lane) {
-  SegMeta m;
-  m.ib = a.seg_ib[s];
-  m.ie = a.seg_ib[s + 1];
-  m.word = __ldg(a.seg_mask + s * (kSeg / 32) + (lane >> 2));
-  m.z = a.seg_z[s];
-  return m;
-}
-
-__device__ __forceinline__ SegGeom geom_of(const StreamArgs& a, const SegMeta& m, int64_t s) {
-  SegGeom g;
-  const int64_t L = a.M + a.N;
-  const int64_t d0 = s * kSeg;
-  const int64_t d1 = (d0 + kSeg < L) ? d0 + kSeg : L;
-  g.ib = m.ib;
-  g.jb = d0 - m.ib;
-  g.nx = (int)(m.ie - m.ib);
-  g.ny = (int)((d1 - m.ie) - g.jb);
-  g.len = (int)(d1 - d0);
-  g.zprev = s == 0 ? a.zprev0 : m.z.x;
-  g.zlast = m.z.y;
-  return g;
-}
-
-// Lane layout of a run inside its segment.
-struct LaneLayout {
-  unsigned byte;  // target mask of the lane's real elements
-  int nreal, i0, j0;
-};
-
-__device__ __forceinline__ LaneLayout lane_layout(const SegGeom& g, uint32_t word, int lane) {
-  LaneLayout L;
-  const int d0 = lane * kR;
-  L.nreal = g.len - d0 < 0 ? 0 : (g.len - d0 < kR ? g.len - d0 : kR);
-  L.byte = (word >> ((lane & 3) * 8)) & 0xffu & ((1u << L.nreal) - 1u);
-  const int nt = __popc(L.byte);
-  int incl = nt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  L.i0 = incl - nt;
-  L.j0 = (d0 < g.len ? d0 : g.len) - L.i0;
-  return L;
-}
-
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-}
-
-// Asynchronous copy of the lane's coordinates (slots 0..7) and source
-// strengths (slots 8..15) into its private shared-memory slot.
-__device__ __forceinline__ void prefetch_run(const StreamArgs& a, const SegGeom& g,
-                                             const LaneLayout& L, double* slot) {
-#pragma unroll
-  for (int e = 0; e < kR; ++e) {
-    if (e < L.nreal) {
-      const int t = __popc(L.byte & ((1u << e) - 1u));
-      const int sidx = e - t;
-      if (L.byte & (1u << e)) {
-        cp_async8(slot + e, a.xs + g.ib + L.i0 + t);
-      } else {
-        cp_async8(slot + e, a.ys + g.jb + L.j0 + sidx);
-        cp_async8(slot + kR + e, a.bs + g.jb + L.j0 + sidx);
-      }
-    }
-  }
-  cp_async_commit();
-}
-
-// K3: persistent warps; while segment s is computed, the next segment's
-// elements stream into shared memory (cp.async) and the one after's
-// metadata into registers.
 template <bool MS>
 __global__ void __launch_bounds__(kThreads, 4)
     seg_main_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
@@ -678,64 +589,30 @@ __global__ void __launch_bounds__(kThreads, 4)
   unsigned char* wreg = smem_raw + sizeof(ModeTable) + (size_t)warp * warp_region_bytes(ne);
   Carry* carries = reinterpret_cast<Carry*>(wreg);
   double* su = reinterpret_cast<double*>(wreg + sizeof(Carry) * 32 * (size_t)ne);
-  double* slot = su + kSeg + lane * (2 * kR);
   load_mode_table(mtab, mt);
   __syncthreads();
-  const int64_t stride = (int64_t)gridDim.x * kSegWarps;
-  int64_t s = (int64_t)blockIdx.x * kSegWarps + warp;
-  if (s >= a.nseg) return;
-  // pipeline prologue: data of s in flight, metadata of s + stride loaded
-  SegMeta mcur = load_meta(a, s, lane);
-  SegGeom gcur = geom_of(a, mcur, s);
-  LaneLayout lcur = lane_layout(gcur, mcur.word, lane);
-  prefetch_run(a, gcur, lcur, slot);
-  SegMeta mnext{};
-  if (s + stride < a.nseg) mnext = load_meta(a, s + stride, lane);
-  for (; s < a.nseg; s += stride) {
-    const SegGeom g = gcur;
-    const LaneLayout L = lcur;
+  for (int64_t s = (int64_t)blockIdx.x * kSegWarps + warp; s < a.nseg;
+       s += (int64_t)gridDim.x * kSegWarps) {
+    const SegGeom g = seg_geom(a, s);
     const SegFrame f = seg_frame(g);
+    // segment carries: lane q < ne forward of mode q, ne <= q < 2ne backward
     cplx seg_c = {0.0, 0.0};
     if (lane < 2 * ne) {
       const int k = lane < ne ? lane : lane - ne;
       const int64_t idx = (int64_t)k * a.nseg + s;
       seg_c = lane < ne ? ts.Cf[idx] : ts.Cb[idx];
     }
-    // this segment's run: shared memory -> registers
-    cp_async_wait_all();
     LaneRun r;
-    r.tmask = L.byte;
-    r.tfirst = L.i0;
-    double last = 0.0;
-#pragma unroll
-    for (int e = 0; e < kR; ++e) {
-      if (e < L.nreal) {
-        r.g[e] = slot[e];
-        r.b[e] = (L.byte & (1u << e)) ? 0.0 : slot[kR + e];
-        last = r.g[e];
-      } else {
-        r.g[e] = 0.0;
-        r.b[e] = 0.0;
-      }
-    }
-    double zp = __shfl_up_sync(0xffffffffu, last, 1);
-    if (lane == 0) zp = g.zprev;
-    const double zl = L.nreal > 0 ? last : zp;
-    // next segment: issue its copies now (slot is free), fetch the metadata after it
-    const int64_t s1 = s + stride;
-    if (s1 < a.nseg) {
-      gcur = geom_of(a, mnext, s1);
-      lcur = lane_layout(gcur, mnext.word, lane);
-      prefetch_run(a, gcur, lcur, slot);
-      if (s1 + stride < a.nseg) mnext = load_meta(a, s1 + stride, lane);
-    }
-
+    double zp, zl;
+    lane_load(a, g, s, lane, r, zp, zl);
+    const int nreal = g.len - lane * kR;
+    // gaps (coordinates are still needed by the moment path)
     double gmax = 0.0;
     {
       double prev = zp;
 #pragma unroll
       for (int e = 0; e < kR; ++e)
-        if (e < L.nreal) {
+        if (e < nreal) {
           gmax = fmax(gmax, r.g[e] - prev);
           prev = r.g[e];
         }
@@ -768,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 4)
       double prev = zp;
 #pragma unroll
       for (int e = 0; e < kR; ++e) {
-        if (e < L.nreal) {
+        if (e < nreal) {
           const double z = r.g[e];
           r.g[e] = z - prev;
           prev = z;
