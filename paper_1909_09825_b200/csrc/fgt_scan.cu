@@ -208,6 +208,9 @@ __device__ __forceinline__ void lane_load(const StreamArgs& a, const SegGeom& g,
   if (lane == 0) prev = g.zprev;
   zp = prev;
   zl = nreal > 0 ? last : prev;
+  // padding elements sit on the run's last coordinate: their gaps are 0
+#pragma unroll
+  for (int e = 0; e < kR; ++e) r.g[e] = e < nreal ? r.g[e] : zl;
 }
 
 // --------------------------------------------------------------- pass 2
@@ -232,10 +235,15 @@ struct Carry {
 // With Kt_i = K_i + b_i the backward step is Kt_{i-1} = d_i Kt_i + b_{i-1},
 // the same multiply-add as the forward step; the two chains are independent
 // and interleaved for instruction-level parallelism.
+#ifndef FGT_MODE_UNROLL
+#define FGT_MODE_UNROLL 1
+#endif
+constexpr int kModeUnroll = FGT_MODE_UNROLL;
 template <int D, bool MS>
 __device__ __forceinline__ void pass2(const ModeTable& mt, int ne, const LaneRun& r,
                                       const Carry* carry, double (&out)[kR],
                                       const ModeSumsOut& ms) {
+#pragma unroll kModeUnroll
   for (int k = 0; k < ne; ++k) {
     Coef<D> c;
     c.load(mt, k);
@@ -540,20 +548,9 @@ __global__ void __launch_bounds__(kThreads)
     LaneRun r;
     double zp, zl;
     lane_load(a, g, s, lane, r, zp, zl);
-    {
-      double prev = zp;
-      const int nreal = g.len - lane * kR;
 #pragma unroll
-      for (int e = 0; e < kR; ++e) {
-        if (e < nreal) {
-          const double z = r.g[e];
-          r.g[e] = z - prev;
-          prev = z;
-        } else {
-          r.g[e] = 0.0;
-        }
-      }
-    }
+    for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
+    r.g[0] -= zp;
     for (int k = 0; k < ne; ++k) {
       const cplx sk = mt.s[k];
       cplx F = {0.0, 0.0}, Pp = {1.0, 0.0}, G = {0.0, 0.0};
@@ -578,8 +575,11 @@ __global__ void __launch_bounds__(kThreads)
 
 // ------------------------------------------------------------------- K3
 
+#ifndef FGT_K3_MINB
+#define FGT_K3_MINB 4
+#endif
 template <bool MS>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
     seg_main_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
                     TileState ts, OutArgs o) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -605,18 +605,10 @@ __global__ void __launch_bounds__(kThreads, 4)
     LaneRun r;
     double zp, zl;
     lane_load(a, g, s, lane, r, zp, zl);
-    const int nreal = g.len - lane * kR;
     // gaps (coordinates are still needed by the moment path)
-    double gmax = 0.0;
-    {
-      double prev = zp;
+    double gmax = r.g[0] - zp;
 #pragma unroll
-      for (int e = 0; e < kR; ++e)
-        if (e < nreal) {
-          gmax = fmax(gmax, r.g[e] - prev);
-          prev = r.g[e];
-        }
-    }
+    for (int e = 1; e < kR; ++e) gmax = fmax(gmax, r.g[e] - r.g[e - 1]);
     const int D = pick_degree(P, warp_max(gmax));
     const int DM = seg_moment_degree(P, f);
     Carry* mine = carries + lane * ne;
@@ -641,19 +633,9 @@ __global__ void __launch_bounds__(kThreads, 4)
           break;
       }
     }
-    {
-      double prev = zp;
 #pragma unroll
-      for (int e = 0; e < kR; ++e) {
-        if (e < nreal) {
-          const double z = r.g[e];
-          r.g[e] = z - prev;
-          prev = z;
-        } else {
-          r.g[e] = 0.0;
-        }
-      }
-    }
+    for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
+    r.g[0] -= zp;
     if (!done) carries_scan(mt, ne, r, lane, seg_c, seg_c, 0, mine);
     __syncwarp();
 

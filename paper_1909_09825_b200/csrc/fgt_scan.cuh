@@ -10,7 +10,10 @@
 
 namespace fgt_b200 {
 
-constexpr int kR = 8;                   // merged elements per lane run
+#ifndef FGT_KR
+#define FGT_KR 8
+#endif
+constexpr int kR = FGT_KR;              // merged elements per lane run
 constexpr int kSeg = 32 * kR;           // merged elements per segment (one warp)
 constexpr int kSegWarps = 4;            // segments (warps) per CTA in K1 / K3
 constexpr int kThreads = 32 * kSegWarps;
