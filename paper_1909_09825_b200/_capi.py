@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfgt1d_b200.so")
+LIB_PATH = os.environ.get("FGT1D_LIB") or os.path.join(_HERE, "lib", "libfgt1d_b200.so")
 
 FGT_OK = 0
 FGT_ERR_DOMAIN = 1
