@@ -575,14 +575,9 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       if (xs.tmp) temps.push_back((void*)xs.dptr);
       SetSrc ys = stage_set(sources, N, flags, st);
       if (ys.tmp) temps.push_back((void*)ys.dptr);
-      // all structural checks in one device round trip
-      ck(launch_flag_nonfinite(xs.dptr, M, p->d_flag + 0, st), "finite");
-      ck(launch_flag_nonfinite(ys.dptr, N, p->d_flag + 1, st), "finite");
-      if (M == N) ck(launch_flag_unequal(xs.dptr, ys.dptr, M, p->d_flag + 2, st), "same points");
-      if (!(flags & FGT_ASSUME_SORTED)) {
-        ck(launch_flag_unsorted(xs.dptr, M, p->d_flag + 3, st), "sorted");
-        ck(launch_flag_unsorted(ys.dptr, N, p->d_flag + 4, st), "sorted");
-      }
+      // all structural checks in one read of both sets, one round trip
+      ck(launch_plan_checks(xs.dptr, M, ys.dptr, N, !(flags & FGT_ASSUME_SORTED), p->d_flag, st),
+         "plan checks");
       int hf[8] = {0};
       ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(hf), cudaMemcpyDeviceToHost, st), "flags");
       ck(cudaStreamSynchronize(st), "flags sync");

@@ -307,6 +307,44 @@ __global__ void nonfinite_kernel(const double* __restrict__ x, int64_t n, int* _
   }
 }
 
+// All plan-time structural checks in one read of both sets:
+// flags[0] target non-finite, [1] source non-finite, [2] x[i] != y[i]
+// (only when M == N), [3] targets unsorted, [4] sources unsorted.
+__global__ void __launch_bounds__(256)
+    plan_checks_kernel(const double* __restrict__ x, int64_t M, const double* __restrict__ y,
+                       int64_t N, int check_sorted, int* __restrict__ flags) {
+  const int64_t n = M > N ? M : N;
+  const bool same_len = M == N;
+  int f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double xv = 0.0, yv = 0.0;
+    if (i < M) {
+      xv = __ldg(x + i);
+      f0 |= !isfinite(xv);
+      if (check_sorted && i + 1 < M) f3 |= xv > __ldg(x + i + 1);
+    }
+    if (i < N) {
+      yv = __ldg(y + i);
+      f1 |= !isfinite(yv);
+      if (check_sorted && i + 1 < N) f4 |= yv > __ldg(y + i + 1);
+    }
+    if (same_len) f2 |= !(xv == yv);
+  }
+  f0 = __any_sync(0xffffffffu, f0);
+  f1 = __any_sync(0xffffffffu, f1);
+  f2 = __any_sync(0xffffffffu, f2);
+  f3 = __any_sync(0xffffffffu, f3);
+  f4 = __any_sync(0xffffffffu, f4);
+  if ((threadIdx.x & 31) == 0) {
+    if (f0) flags[0] = 1;
+    if (f1) flags[1] = 1;
+    if (f2) flags[2] = 1;
+    if (f3) flags[3] = 1;
+    if (f4) flags[4] = 1;
+  }
+}
+
 __global__ void iota_kernel(int32_t* __restrict__ p, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -451,6 +489,15 @@ cudaError_t launch_flag_nonfinite(const double* x, int64_t n, int* flag, cudaStr
   if (n < 1) return cudaSuccess;
   note_launch();
   nonfinite_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plan_checks(const double* x, int64_t M, const double* y, int64_t N,
+                               int check_sorted, int* flags, cudaStream_t st) {
+  const int64_t n = M > N ? M : N;
+  if (n < 1) return cudaSuccess;
+  note_launch();
+  plan_checks_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, M, y, N, check_sorted, flags);
   return cudaGetLastError();
 }
 

@@ -24,6 +24,10 @@ cudaError_t launch_flag_unsorted(const double* x, int64_t n, int* flag, cudaStre
 cudaError_t launch_flag_unequal(const double* x, const double* y, int64_t n, int* flag,
                                 cudaStream_t st);
 cudaError_t launch_flag_nonfinite(const double* x, int64_t n, int* flag, cudaStream_t st);
+// Fused plan checks (flags[0..4]: x non-finite, y non-finite, x != y when
+// M == N, x unsorted, y unsorted); flags must be zeroed by the caller.
+cudaError_t launch_plan_checks(const double* x, int64_t M, const double* y, int64_t N,
+                               int check_sorted, int* flags, cudaStream_t st);
 cudaError_t launch_iota(int32_t* p, int64_t n, cudaStream_t st);
 
 }  // namespace fgt_b200
