@@ -675,50 +675,51 @@ __global__ void partition_kernel(const double* __restrict__ xs, int64_t M,
   seg_ib[t] = merge_path(xs, M, ys, N, diag);
 }
 
-// Plan-time segment metadata, one warp per segment: merge the segment's runs
-// straight from global memory once, record (zprev, zlast) and one bit per
-// merged element (1 = target) so that the apply kernels never merge.
+// Plan-time segment metadata, one warp per segment: stage the segment's
+// targets and sources in shared memory, place every target by ranking it
+// among the segment's sources (sources at equal coordinates come first), and
+// record (zprev, zlast) and one bit per merged element (1 = target) so that
+// the apply kernels never merge.
 __global__ void __launch_bounds__(128)
     seg_meta_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
                     int64_t N, const int64_t* __restrict__ seg_ib, int64_t nseg,
                     double2* __restrict__ seg_z, uint32_t* __restrict__ seg_mask) {
-  const int lane = threadIdx.x & 31;
-  const int64_t s = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  __shared__ double sx[4][kSeg];
+  __shared__ double sy[4][kSeg];
+  __shared__ unsigned smask[4][kSeg / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t s = (int64_t)blockIdx.x * 4 + warp;
   if (s >= nseg) return;
   const int64_t L = M + N;
   const int64_t d0 = s * kSeg;
   const int64_t d1 = (d0 + kSeg < L) ? d0 + kSeg : L;
   const int64_t ib = seg_ib[s], ie = seg_ib[s + 1];
   const int64_t jb = d0 - ib, je = d1 - ie;
-  const int nx = (int)(ie - ib), ny = (int)(je - jb), len = (int)(d1 - d0);
-  const double* x = xs + ib;
-  const double* y = ys + jb;
-  const int ld = lane * kR;
-  const int dd = ld < len ? ld : len;
-  int i = (int)merge_path(x, (int64_t)nx, y, (int64_t)ny, (int64_t)dd);
-  int j = dd - i;
-  unsigned byte = 0u;
-#pragma unroll
-  for (int e = 0; e < kR; ++e) {
-    if (ld + e < len) {
-      const bool src = (j < ny) && (i >= nx || y[j] <= x[i]);
-      if (src) {
-        ++j;
-      } else {
-        byte |= 1u << e;
-        ++i;
-      }
+  const int nx = (int)(ie - ib), ny = (int)(je - jb);
+  for (int i = lane; i < nx; i += 32) sx[warp][i] = __ldg(xs + ib + i);
+  for (int j = lane; j < ny; j += 32) sy[warp][j] = __ldg(ys + jb + j);
+  if (lane < kSeg / 32) smask[warp][lane] = 0u;
+  __syncwarp();
+  for (int i = lane; i < nx; i += 32) {
+    const double x = sx[warp][i];
+    int lo = 0, hi = ny;  // number of sources <= x
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sy[warp][mid] <= x)
+        lo = mid + 1;
+      else
+        hi = mid;
     }
+    const int p = i + lo;
+    atomicOr(&smask[warp][p >> 5], 1u << (p & 31));
   }
-  unsigned w = byte << ((lane & 3) * 8);
-  w |= __shfl_down_sync(0xffffffffu, w, 1);
-  w |= __shfl_down_sync(0xffffffffu, w, 2);
-  if ((lane & 3) == 0) seg_mask[s * (kSeg / 32) + (lane >> 2)] = w;
+  __syncwarp();
+  if (lane < kSeg / 32) seg_mask[s * (kSeg / 32) + lane] = smask[warp][lane];
   if (lane == 0) {
     const double px = ib > 0 ? xs[ib - 1] : -INFINITY;
     const double py = jb > 0 ? ys[jb - 1] : -INFINITY;
-    const double lx = nx > 0 ? xs[ie - 1] : -INFINITY;
-    const double ly = ny > 0 ? ys[je - 1] : -INFINITY;
+    const double lx = nx > 0 ? sx[warp][nx - 1] : -INFINITY;
+    const double ly = ny > 0 ? sy[warp][ny - 1] : -INFINITY;
     seg_z[s] = make_double2(fmax(px, py), fmax(lx, ly));
   }
 }
