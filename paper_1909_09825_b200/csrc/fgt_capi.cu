@@ -291,17 +291,22 @@ void adopt_set(const SetSrc& in, int64_t n, bool is_sorted, uint32_t flags, cuda
   *d_perm = d_p;
 }
 
-void finish_plan(fgt_plan_s* p, cudaStream_t st) {
+// Partition + speculative tile pass (checks and segment metadata) on the
+// arrays as given; valid metadata whenever they turn out to be sorted.
+void plan_tiles(fgt_plan_s* p, const double* xd, const double* yd, bool check_sorted,
+                cudaStream_t st) {
   const int64_t L = p->M + p->N;
-  p->ntiles = (L + kSeg - 1) / kSeg;
-  p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
-  ck(launch_partition(p->d_xs, p->M, p->d_ys, p->N, kSeg, p->ntiles, p->d_tile_ib, st),
-     "partition");
-  p->d_seg_z = dmalloc<double2>(p->ntiles, st);
-  p->d_seg_mask = dmalloc<uint32_t>((size_t)p->ntiles * (kSeg / 32), st);
-  ck(launch_seg_meta(p->d_xs, p->M, p->d_ys, p->N, p->d_tile_ib, p->ntiles, p->d_seg_z,
-                     p->d_seg_mask, st),
-     "segment metadata");
+  const int64_t ntl = (L + kPlanTile - 1) / kPlanTile;
+  if (ntl == 0) return;
+  int64_t* tib = dmalloc<int64_t>(ntl + 1, st);
+  ck(launch_partition(xd, p->M, yd, p->N, kPlanTile, ntl, tib, st), "partition");
+  ck(launch_plan_tiles(xd, p->M, yd, p->N, tib, ntl, p->ntiles, check_sorted ? 1 : 0,
+                       p->d_tile_ib, p->d_seg_z, p->d_seg_mask, p->d_flag, st),
+     "plan tiles");
+  dfree(tib, st);
+}
+
+void upload_modes(fgt_plan_s* p, cudaStream_t st) {
   ModeTable T;
   build_modes(p->soe, p->delta, p->P, T);
   p->d_mt = dmalloc<ModeTable>(1, st);
@@ -575,11 +580,18 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       if (xs.tmp) temps.push_back((void*)xs.dptr);
       SetSrc ys = stage_set(sources, N, flags, st);
       if (ys.tmp) temps.push_back((void*)ys.dptr);
-      // all structural checks in one read of both sets, one round trip
-      ck(launch_plan_checks(xs.dptr, M, ys.dptr, N, !(flags & FGT_ASSUME_SORTED), p->d_flag, st),
-         "plan checks");
+      const int64_t L = M + N;
+      p->ntiles = (L + kSeg - 1) / kSeg;
+      p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
+      p->d_seg_z = dmalloc<double2>(p->ntiles, st);
+      p->d_seg_mask = dmalloc<uint32_t>((size_t)p->ntiles * (kSeg / 32), st);
+      // one read of both sets: checks + (speculative) segment metadata
+      plan_tiles(p, xs.dptr, ys.dptr, !(flags & FGT_ASSUME_SORTED), st);
       int hf[8] = {0};
+      double x0 = 0, y0 = 0;
       ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(hf), cudaMemcpyDeviceToHost, st), "flags");
+      if (M > 0) ck(cudaMemcpyAsync(&x0, xs.dptr, 8, cudaMemcpyDeviceToHost, st), "x0");
+      if (N > 0) ck(cudaMemcpyAsync(&y0, ys.dptr, 8, cudaMemcpyDeviceToHost, st), "y0");
       ck(cudaStreamSynchronize(st), "flags sync");
       // the reference checks targets, then sources (transform.cpp:202-204)
       if (hf[0]) raise(FGT_ERR_DOMAIN, "target coordinates must be finite");
@@ -590,11 +602,14 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       temps.clear();  // ownership moves into adopt_set
       adopt_set(xs, M, p->t_sorted, flags, st, &p->d_xs, &p->own_xs, &p->d_tperm);
       adopt_set(ys, N, p->s_sorted, flags, st, &p->d_ys, &p->own_ys, &p->d_sperm);
+      if (!p->t_sorted || !p->s_sorted) {
+        // metadata of the sorted stream; first coordinates after sorting
+        plan_tiles(p, p->d_xs, p->d_ys, false, st);
+        if (M > 0) ck(cudaMemcpyAsync(&x0, p->d_xs, 8, cudaMemcpyDeviceToHost, st), "x0");
+        if (N > 0) ck(cudaMemcpyAsync(&y0, p->d_ys, 8, cudaMemcpyDeviceToHost, st), "y0");
+      }
+      upload_modes(p, st);  // synchronizes
       // coordinate before the first merged element: the element itself
-      double x0 = 0, y0 = 0;
-      if (M > 0) ck(cudaMemcpyAsync(&x0, p->d_xs, 8, cudaMemcpyDeviceToHost, st), "x0");
-      if (N > 0) ck(cudaMemcpyAsync(&y0, p->d_ys, 8, cudaMemcpyDeviceToHost, st), "y0");
-      finish_plan(p, st);  // synchronizes
       p->zprev0 = (M > 0 && N > 0) ? std::fmin(x0, y0) : (M > 0 ? x0 : y0);
     } catch (...) {
       for (void* t : temps) cudaFreeAsync(t, st);

@@ -675,52 +675,113 @@ __global__ void partition_kernel(const double* __restrict__ xs, int64_t M,
   seg_ib[t] = merge_path(xs, M, ys, N, diag);
 }
 
-// Plan-time segment metadata, one warp per segment: stage the segment's
-// targets and sources in shared memory, place every target by ranking it
-// among the segment's sources (sources at equal coordinates come first), and
-// record (zprev, zlast) and one bit per merged element (1 = target) so that
-// the apply kernels never merge.
+// Plan-time tile pass (one CTA per tile of kPlanTile merged elements,
+// speculative: run on the input as given).  Stages the tile's targets and
+// sources in shared memory and, in one read of both sets:
+//   - checks finiteness, sortedness (incl. the pair across the tile start)
+//     and, when M == N, element-wise equality of the two vectors
+//     (flags[0..4] as launch_plan_checks);
+//   - splits the tile into segments by merge path in shared memory
+//     (seg_ib), places every target of a segment by ranking it among the
+//     segment's sources (sources at equal coordinates first) -> one bit per
+//     merged element (seg_mask), and records (zprev, zlast) per segment.
 __global__ void __launch_bounds__(128)
-    seg_meta_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
-                    int64_t N, const int64_t* __restrict__ seg_ib, int64_t nseg,
-                    double2* __restrict__ seg_z, uint32_t* __restrict__ seg_mask) {
-  __shared__ double sx[4][kSeg];
-  __shared__ double sy[4][kSeg];
-  __shared__ unsigned smask[4][kSeg / 32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t s = (int64_t)blockIdx.x * 4 + warp;
-  if (s >= nseg) return;
+    plan_tile_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
+                     int64_t N, const int64_t* __restrict__ tile_ib, int64_t nseg,
+                     int check_sorted, int64_t* __restrict__ seg_ib, double2* __restrict__ seg_z,
+                     uint32_t* __restrict__ seg_mask, int* __restrict__ flags) {
+  extern __shared__ double tsm[];
+  double* sx = tsm;              // [kPlanTile]
+  double* sy = tsm + kPlanTile;  // [kPlanTile]
+  __shared__ int sib[kPlanSegs + 1];
+  __shared__ unsigned smask[kPlanSegs][kSeg / 32];
+  const int64_t t = blockIdx.x;
   const int64_t L = M + N;
-  const int64_t d0 = s * kSeg;
-  const int64_t d1 = (d0 + kSeg < L) ? d0 + kSeg : L;
-  const int64_t ib = seg_ib[s], ie = seg_ib[s + 1];
+  const int64_t d0 = t * kPlanTile;
+  const int64_t d1 = (d0 + kPlanTile < L) ? d0 + kPlanTile : L;
+  const int64_t ib = tile_ib[t], ie = tile_ib[t + 1];
   const int64_t jb = d0 - ib, je = d1 - ie;
-  const int nx = (int)(ie - ib), ny = (int)(je - jb);
-  for (int i = lane; i < nx; i += 32) sx[warp][i] = __ldg(xs + ib + i);
-  for (int j = lane; j < ny; j += 32) sy[warp][j] = __ldg(ys + jb + j);
-  if (lane < kSeg / 32) smask[warp][lane] = 0u;
-  __syncwarp();
-  for (int i = lane; i < nx; i += 32) {
-    const double x = sx[warp][i];
-    int lo = 0, hi = ny;  // number of sources <= x
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (sy[warp][mid] <= x)
-        lo = mid + 1;
-      else
-        hi = mid;
-    }
-    const int p = i + lo;
-    atomicOr(&smask[warp][p >> 5], 1u << (p & 31));
+  const int nx = (int)(ie - ib), ny = (int)(je - jb), len = (int)(d1 - d0);
+  int f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0;
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+    const double v = __ldg(xs + ib + i);
+    sx[i] = v;
+    f0 |= !isfinite(v);
+    if (M == N) f2 |= !(v == __ldg(ys + ib + i));
   }
-  __syncwarp();
-  if (lane < kSeg / 32) seg_mask[s * (kSeg / 32) + lane] = smask[warp][lane];
-  if (lane == 0) {
-    const double px = ib > 0 ? xs[ib - 1] : -INFINITY;
-    const double py = jb > 0 ? ys[jb - 1] : -INFINITY;
-    const double lx = nx > 0 ? sx[warp][nx - 1] : -INFINITY;
-    const double ly = ny > 0 ? sy[warp][ny - 1] : -INFINITY;
-    seg_z[s] = make_double2(fmax(px, py), fmax(lx, ly));
+  for (int j = threadIdx.x; j < ny; j += blockDim.x) {
+    const double v = __ldg(ys + jb + j);
+    sy[j] = v;
+    f1 |= !isfinite(v);
+  }
+  for (int w = threadIdx.x; w < kPlanSegs * (kSeg / 32); w += blockDim.x) (&smask[0][0])[w] = 0u;
+  __syncthreads();
+  if (check_sorted) {
+    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+      const double prev = i > 0 ? sx[i - 1] : (ib > 0 ? __ldg(xs + ib - 1) : -INFINITY);
+      f3 |= prev > sx[i];
+    }
+    for (int j = threadIdx.x; j < ny; j += blockDim.x) {
+      const double prev = j > 0 ? sy[j - 1] : (jb > 0 ? __ldg(ys + jb - 1) : -INFINITY);
+      f4 |= prev > sy[j];
+    }
+  }
+  // segment splits inside the tile
+  const int nsegs_tile = (len + kSeg - 1) / kSeg;
+  if (threadIdx.x <= nsegs_tile) {
+    const int dd = threadIdx.x * kSeg < len ? threadIdx.x * kSeg : len;
+    sib[threadIdx.x] = (int)merge_path(sx, (int64_t)nx, sy, (int64_t)ny, (int64_t)dd);
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = warp; k < nsegs_tile; k += blockDim.x / 32) {
+    const int i0 = sib[k], i1 = sib[k + 1];
+    const int sd0 = k * kSeg;
+    const int sd1 = (sd0 + kSeg < len) ? sd0 + kSeg : len;
+    const int j0 = sd0 - i0, j1 = sd1 - i1;
+    for (int i = i0 + lane; i < i1; i += 32) {
+      const double x = sx[i];
+      int lo = j0, hi = j1;  // sources of the segment <= x
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sy[mid] <= x)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      const int p = (i - i0) + (lo - j0);
+      if (p < kSeg) atomicOr(&smask[k][p >> 5], 1u << (p & 31));  // bound holds unless unsorted
+    }
+    __syncwarp();
+    const int64_t sg = t * kPlanSegs + k;
+    if (lane < kSeg / 32) seg_mask[sg * (kSeg / 32) + lane] = smask[k][lane];
+    if (lane == 0) {
+      seg_ib[sg] = ib + i0;
+      double px, py;
+      if (k == 0) {
+        px = ib > 0 ? __ldg(xs + ib - 1) : -INFINITY;
+        py = jb > 0 ? __ldg(ys + jb - 1) : -INFINITY;
+      } else {
+        px = i0 > 0 ? sx[i0 - 1] : -INFINITY;
+        py = j0 > 0 ? sy[j0 - 1] : -INFINITY;
+      }
+      const double lx = i1 > i0 ? sx[i1 - 1] : -INFINITY;
+      const double ly = j1 > j0 ? sy[j1 - 1] : -INFINITY;
+      seg_z[sg] = make_double2(fmax(px, py), fmax(lx, ly));
+      if (sg + 1 == nseg) seg_ib[nseg] = M;
+    }
+  }
+  f0 = __syncthreads_or(f0);
+  f1 = __syncthreads_or(f1);
+  f2 = __syncthreads_or(f2);
+  f3 = __syncthreads_or(f3);
+  f4 = __syncthreads_or(f4);
+  if (threadIdx.x == 0) {
+    if (f0) atomicOr(flags + 0, 1);
+    if (f1) atomicOr(flags + 1, 1);
+    if (f2) atomicOr(flags + 2, 1);
+    if (f3) atomicOr(flags + 3, 1);
+    if (f4) atomicOr(flags + 4, 1);
   }
 }
 
@@ -934,13 +995,22 @@ cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int6
   return cudaGetLastError();
 }
 
-cudaError_t launch_seg_meta(const double* xs, int64_t M, const double* ys, int64_t N,
-                            const int64_t* seg_ib, int64_t nseg, double2* seg_z,
-                            uint32_t* seg_mask, cudaStream_t st) {
-  if (nseg == 0) return cudaSuccess;
+cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int64_t N,
+                              const int64_t* tile_ib, int64_t ntiles, int64_t nseg,
+                              int check_sorted, int64_t* seg_ib, double2* seg_z,
+                              uint32_t* seg_mask, int* flags, cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  const size_t smem = sizeof(double) * 2 * kPlanTile;
+  static bool done = false;
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(plan_tile_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
   note_launch();
-  seg_meta_kernel<<<(unsigned)((nseg + 3) / 4), 128, 0, st>>>(xs, M, ys, N, seg_ib, nseg, seg_z,
-                                                               seg_mask);
+  plan_tile_kernel<<<(unsigned)ntiles, 128, smem, st>>>(xs, M, ys, N, tile_ib, nseg, check_sorted,
+                                                         seg_ib, seg_z, seg_mask, flags);
   return cudaGetLastError();
 }
 

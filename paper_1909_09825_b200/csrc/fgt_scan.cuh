@@ -18,6 +18,8 @@ constexpr int kSeg = 32 * kR;           // merged elements per segment (one warp
 constexpr int kSegWarps = 4;            // segments (warps) per CTA in K1 / K3
 constexpr int kThreads = 32 * kSegWarps;
 constexpr int kMaxMom = kMaxDeg;        // highest moment order of the expansions
+constexpr int kPlanSegs = 16;           // segments per plan tile
+constexpr int kPlanTile = kPlanSegs * kSeg;  // merged elements per plan tile
 
 // Per-mode constants laid out in device memory (plan-owned): s_k, mw_k and the
 // Taylor coefficients c_{k,n} = (-s_k)^n / n! of exp(-s_k g).
@@ -69,10 +71,14 @@ size_t seg_smem_bytes(int ne);
 
 cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int64_t N,
                              int64_t seg, int64_t nseg, int64_t* seg_ib, cudaStream_t st);
-// Plan-time segment metadata: seg_z[s] = (zprev, zlast), seg_mask.
-cudaError_t launch_seg_meta(const double* xs, int64_t M, const double* ys, int64_t N,
-                            const int64_t* seg_ib, int64_t nseg, double2* seg_z,
-                            uint32_t* seg_mask, cudaStream_t st);
+// Plan-time tile pass (speculative on unsorted input): checks (flags[0..4] =
+// x non-finite, y non-finite, x != y when M == N, x unsorted, y unsorted;
+// zeroed by the caller) and segment metadata seg_ib / seg_z / seg_mask.
+// tile_ib: launch_partition output at kPlanTile granularity.
+cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int64_t N,
+                              const int64_t* tile_ib, int64_t ntiles, int64_t nseg,
+                              int check_sorted, int64_t* seg_ib, double2* seg_z,
+                              uint32_t* seg_mask, int* flags, cudaStream_t st);
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, cudaStream_t st);
 // K2: exclusive carries per segment.  carry_in: 2*ne complex (forward carry at
