@@ -739,18 +739,26 @@ __global__ void __launch_bounds__(128)
     const int sd0 = k * kSeg;
     const int sd1 = (sd0 + kSeg < len) ? sd0 + kSeg : len;
     const int j0 = sd0 - i0, j1 = sd1 - i1;
-    for (int i = i0 + lane; i < i1; i += 32) {
-      const double x = sx[i];
-      int lo = j0, hi = j1;  // sources of the segment <= x
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (sy[mid] <= x)
-          lo = mid + 1;
-        else
-          hi = mid;
+    for (int base = i0; base < i1; base += 32) {
+      const int i = base + lane;
+      int p = kSeg;  // out of range: no bit
+      if (i < i1) {
+        const double x = sx[i];
+        int lo = j0, hi = j1;  // sources of the segment <= x
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (sy[mid] <= x)
+            lo = mid + 1;
+          else
+            hi = mid;
+        }
+        p = (i - i0) + (lo - j0);  // < kSeg unless the input is unsorted
       }
-      const int p = (i - i0) + (lo - j0);
-      if (p < kSeg) atomicOr(&smask[k][p >> 5], 1u << (p & 31));  // bound holds unless unsorted
+      // OR the bits of lanes that hit the same word, one atomic per word
+      const int word = p < kSeg ? (p >> 5) : -1;
+      const unsigned grp = __match_any_sync(0xffffffffu, word);
+      const unsigned bits = __reduce_or_sync(grp, word >= 0 ? (1u << (p & 31)) : 0u);
+      if (word >= 0 && lane == __ffs(grp) - 1) atomicOr(&smask[k][word], bits);
     }
     __syncwarp();
     const int64_t sg = t * kPlanSegs + k;
