@@ -449,15 +449,24 @@ __device__ __forceinline__ void seg_aggregate_moments(const StreamArgs& a, const
   double M[DM + 1];
 #pragma unroll
   for (int n = 0; n <= DM; ++n) M[n] = 0.0;
-  for (int j = lane; j < g.ny; j += 32) {
-    const double y = __ldg(a.ys + g.jb + j);
-    double p = __ldg(a.bs + g.jb + j);
-    const double d = y - f.zc;
-    M[0] += p;
+  for (int j0 = lane; j0 < g.ny; j0 += 4 * 32) {
+    double yv[4], bv[4];
 #pragma unroll
-    for (int n = 1; n <= DM; ++n) {
-      p *= d;
-      M[n] += p;
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * 32;
+      yv[u] = j < g.ny ? __ldg(a.ys + g.jb + j) : f.zc;
+      bv[u] = j < g.ny ? __ldg(a.bs + g.jb + j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double d = yv[u] - f.zc;
+      double p = bv[u];
+      M[0] += p;
+#pragma unroll
+      for (int n = 1; n <= DM; ++n) {
+        p *= d;
+        M[n] += p;
+      }
     }
   }
 #pragma unroll
@@ -703,16 +712,41 @@ __global__ void __launch_bounds__(128)
   const int64_t jb = d0 - ib, je = d1 - ie;
   const int nx = (int)(ie - ib), ny = (int)(je - jb), len = (int)(d1 - d0);
   int f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0;
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-    const double v = __ldg(xs + ib + i);
-    sx[i] = v;
-    f0 |= !isfinite(v);
-    if (M == N) f2 |= !(v == __ldg(ys + ib + i));
+  // staging with many independent loads in flight per thread
+  constexpr int kU = 8;
+  for (int i0 = threadIdx.x; i0 < nx; i0 += kU * 128) {
+    double v[kU], w[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * 128;
+      v[u] = i < nx ? __ldg(xs + ib + i) : 0.0;
+      w[u] = (M == N && i < nx) ? __ldg(ys + ib + i) : v[u];
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * 128;
+      if (i < nx) {
+        sx[i] = v[u];
+        f0 |= !isfinite(v[u]);
+        f2 |= !(v[u] == w[u]);
+      }
+    }
   }
-  for (int j = threadIdx.x; j < ny; j += blockDim.x) {
-    const double v = __ldg(ys + jb + j);
-    sy[j] = v;
-    f1 |= !isfinite(v);
+  for (int j0 = threadIdx.x; j0 < ny; j0 += kU * 128) {
+    double v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = j0 + u * 128;
+      v[u] = j < ny ? __ldg(ys + jb + j) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = j0 + u * 128;
+      if (j < ny) {
+        sy[j] = v[u];
+        f1 |= !isfinite(v[u]);
+      }
+    }
   }
   for (int w = threadIdx.x; w < kPlanSegs * (kSeg / 32); w += blockDim.x) (&smask[0][0])[w] = 0u;
   __syncthreads();
