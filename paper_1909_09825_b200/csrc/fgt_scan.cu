@@ -710,7 +710,14 @@ __global__ void __launch_bounds__(128)
   const int64_t d1 = (d0 + kPlanTile < L) ? d0 + kPlanTile : L;
   const int64_t ib = tile_ib[t], ie = tile_ib[t + 1];
   const int64_t jb = d0 - ib, je = d1 - ie;
-  const int nx = (int)(ie - ib), ny = (int)(je - jb), len = (int)(d1 - d0);
+  const int64_t nx64 = ie - ib, len64 = d1 - d0;
+  if (nx64 < 0 || nx64 > len64) {
+    // partition of an unsorted stream (speculative pass): metadata is
+    // recomputed after sorting; report "unsorted" and bail out safely
+    if (threadIdx.x == 0) atomicOr(flags + 3, 1);
+    return;
+  }
+  const int nx = (int)nx64, ny = (int)(je - jb), len = (int)len64;
   int f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0;
   // staging with many independent loads in flight per thread
   constexpr int kU = 8;
@@ -751,14 +758,12 @@ __global__ void __launch_bounds__(128)
   for (int w = threadIdx.x; w < kPlanSegs * (kSeg / 32); w += blockDim.x) (&smask[0][0])[w] = 0u;
   __syncthreads();
   if (check_sorted) {
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-      const double prev = i > 0 ? sx[i - 1] : (ib > 0 ? __ldg(xs + ib - 1) : -INFINITY);
-      f3 |= prev > sx[i];
+    if (threadIdx.x == 0) {
+      if (ib > 0 && nx > 0) f3 |= __ldg(xs + ib - 1) > sx[0];
+      if (jb > 0 && ny > 0) f4 |= __ldg(ys + jb - 1) > sy[0];
     }
-    for (int j = threadIdx.x; j < ny; j += blockDim.x) {
-      const double prev = j > 0 ? sy[j - 1] : (jb > 0 ? __ldg(ys + jb - 1) : -INFINITY);
-      f4 |= prev > sy[j];
-    }
+    for (int i = threadIdx.x + 1; i < nx; i += blockDim.x) f3 |= sx[i - 1] > sx[i];
+    for (int j = threadIdx.x + 1; j < ny; j += blockDim.x) f4 |= sy[j - 1] > sy[j];
   }
   // segment splits inside the tile
   const int nsegs_tile = (len + kSeg - 1) / kSeg;
