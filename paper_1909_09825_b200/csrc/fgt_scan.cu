@@ -705,7 +705,7 @@ __global__ void partition_kernel(const double* __restrict__ xs, int64_t M,
 //     (seg_ib), places every target of a segment by ranking it among the
 //     segment's sources (sources at equal coordinates first) -> one bit per
 //     merged element (seg_mask), and records (zprev, zlast) per segment.
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
     plan_tile_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
                      int64_t N, const int64_t* __restrict__ tile_ib, int64_t nseg,
                      int check_sorted, int64_t* __restrict__ seg_ib, double2* __restrict__ seg_z,
@@ -714,7 +714,6 @@ __global__ void __launch_bounds__(128)
   double* sx = tsm;              // [kPlanTile]
   double* sy = tsm + kPlanTile;  // [kPlanTile]
   __shared__ int sib[kPlanSegs + 1];
-  __shared__ unsigned smask[kPlanSegs][kSeg / 32];
   const int64_t t = blockIdx.x;
   const int64_t L = M + N;
   const int64_t d0 = t * kPlanTile;
@@ -750,7 +749,6 @@ __global__ void __launch_bounds__(128)
       f2 |= !(sx[i] == yv);
     }
   }
-  for (int w = threadIdx.x; w < kPlanSegs * (kSeg / 32); w += blockDim.x) (&smask[0][0])[w] = 0u;
   __syncthreads();
   if (check_sorted) {
     if (threadIdx.x == 0) {
@@ -773,30 +771,33 @@ __global__ void __launch_bounds__(128)
     const int sd0 = k * kSeg;
     const int sd1 = (sd0 + kSeg < len) ? sd0 + kSeg : len;
     const int j0 = sd0 - i0, j1 = sd1 - i1;
-    for (int base = i0; base < i1; base += 32) {
-      const int i = base + lane;
-      int p = kSeg;  // out of range: no bit
-      if (i < i1) {
-        const double x = sx[i];
-        int lo = j0, hi = j1;  // sources of the segment <= x
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (sy[mid] <= x)
-            lo = mid + 1;
-          else
-            hi = mid;
+    // each lane merges its window of kR positions (merge path in shared memory)
+    const int w0 = sd0 + lane * kR;
+    unsigned byte = 0u;
+    if (w0 < sd1 && i1 >= i0 && j1 >= j0) {
+      int i = (int)merge_path(sx, (int64_t)nx, sy, (int64_t)ny, (int64_t)w0);
+      int j = w0 - i;
+      double cx = i < i1 ? sx[i] : INFINITY;
+      double cy = j < j1 ? sy[j] : INFINITY;
+#pragma unroll
+      for (int e = 0; e < kR; ++e) {
+        if (w0 + e < sd1) {
+          if (cy <= cx && j < j1) {  // source first on ties
+            ++j;
+            cy = j < j1 ? sy[j] : INFINITY;
+          } else {
+            byte |= 1u << e;
+            ++i;
+            cx = i < i1 ? sx[i] : INFINITY;
+          }
         }
-        p = (i - i0) + (lo - j0);  // < kSeg unless the input is unsorted
       }
-      // OR the bits of lanes that hit the same word, one atomic per word
-      const int word = p < kSeg ? (p >> 5) : -1;
-      const unsigned grp = __match_any_sync(0xffffffffu, word);
-      const unsigned bits = __reduce_or_sync(grp, word >= 0 ? (1u << (p & 31)) : 0u);
-      if (word >= 0 && lane == __ffs(grp) - 1) atomicOr(&smask[k][word], bits);
     }
-    __syncwarp();
+    unsigned wd = byte << ((lane & 3) * 8);
+    wd |= __shfl_down_sync(0xffffffffu, wd, 1);
+    wd |= __shfl_down_sync(0xffffffffu, wd, 2);
     const int64_t sg = t * kPlanSegs + k;
-    if (lane < kSeg / 32) seg_mask[sg * (kSeg / 32) + lane] = smask[k][lane];
+    if ((lane & 3) == 0) seg_mask[sg * (kSeg / 32) + (lane >> 2)] = wd;
     if (lane == 0) {
       seg_ib[sg] = ib + i0;
       double px, py;
@@ -1051,7 +1052,7 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
     done = true;
   }
   note_launch();
-  plan_tile_kernel<<<(unsigned)ntiles, 128, smem, st>>>(xs, M, ys, N, tile_ib, nseg, check_sorted,
+  plan_tile_kernel<<<(unsigned)ntiles, 256, smem, st>>>(xs, M, ys, N, tile_ib, nseg, check_sorted,
                                                          seg_ib, seg_z, seg_mask, flags);
   return cudaGetLastError();
 }
