@@ -739,8 +739,16 @@ __global__ void __launch_bounds__(256)
   const bool check_same = (M == N) && *(volatile int*)(flags + 2) == 0;
   cp_async_wait_all();
   __syncthreads();
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) f0 |= !isfinite(sx[i]);
-  for (int j = threadIdx.x; j < ny; j += blockDim.x) f1 |= !isfinite(sy[j]);
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+    const double v = sx[i];
+    f0 |= !isfinite(v);
+    if (check_sorted && i > 0) f3 |= sx[i - 1] > v;
+  }
+  for (int j = threadIdx.x; j < ny; j += blockDim.x) {
+    const double v = sy[j];
+    f1 |= !isfinite(v);
+    if (check_sorted && j > 0) f4 |= sy[j - 1] > v;
+  }
   if (check_same) {
     for (int i = threadIdx.x; i < nx; i += blockDim.x) {
       const int64_t gi = ib + i;
@@ -755,8 +763,6 @@ __global__ void __launch_bounds__(256)
       if (ib > 0 && nx > 0) f3 |= __ldg(xs + ib - 1) > sx[0];
       if (jb > 0 && ny > 0) f4 |= __ldg(ys + jb - 1) > sy[0];
     }
-    for (int i = threadIdx.x + 1; i < nx; i += blockDim.x) f3 |= sx[i - 1] > sx[i];
-    for (int j = threadIdx.x + 1; j < ny; j += blockDim.x) f4 |= sy[j - 1] > sy[j];
   }
   // segment splits inside the tile
   const int nsegs_tile = (len + kSeg - 1) / kSeg;
@@ -775,7 +781,9 @@ __global__ void __launch_bounds__(256)
     const int w0 = sd0 + lane * kR;
     unsigned byte = 0u;
     if (w0 < sd1 && i1 >= i0 && j1 >= j0) {
-      int i = (int)merge_path(sx, (int64_t)nx, sy, (int64_t)ny, (int64_t)w0);
+      // merge path restricted to the segment: targets [i0, i1), sources [j0, j1)
+      int i = i0 + (int)merge_path(sx + i0, (int64_t)(i1 - i0), sy + j0, (int64_t)(j1 - j0),
+                                   (int64_t)(w0 - sd0));
       int j = w0 - i;
       double cx = i < i1 ? sx[i] : INFINITY;
       double cy = j < j1 ? sy[j] : INFINITY;
