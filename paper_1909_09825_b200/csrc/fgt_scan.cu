@@ -246,6 +246,46 @@ struct Carry {
 // With Kt_i = K_i + b_i the backward step is Kt_{i-1} = d_i Kt_i + b_{i-1},
 // the same multiply-add as the forward step; the two chains are independent
 // and interleaved for instruction-level parallelism.
+// Variant: two modes at a time, gap factors recomputed per direction (no
+// d[] storage) -> four independent chains per iteration.
+template <int D>
+__device__ __forceinline__ void pass2_pair_body(const ModeTable& mt, int k, bool two,
+                                                const LaneRun& r, const Carry* carry,
+                                                double (&out)[kR]) {
+  Coef<D> c0, c1;
+  c0.load(mt, k);
+  c1.load(mt, two ? k + 1 : k);
+  const cplx s0 = mt.s[k], s1 = mt.s[two ? k + 1 : k];
+  const cplx mw0 = mt.mw[k];
+  const cplx mw1 = two ? mt.mw[k + 1] : cplx{0.0, 0.0};
+  cplx H0 = carry[k].cf, K0 = carry[k].cb;
+  cplx H1 = two ? carry[k + 1].cf : cplx{0.0, 0.0};
+  cplx K1 = two ? carry[k + 1].cb : cplx{0.0, 0.0};
+  K0.re += r.b[kR - 1];
+  K1.re += r.b[kR - 1];
+#pragma unroll
+  for (int i = 0; i < kR; ++i) {
+    const int j = kR - 1 - i;
+    const cplx a0 = gap_factor<D>(c0, s0, r.g[i]);
+    const cplx a1 = gap_factor<D>(c1, s1, r.g[i]);
+    H0 = cmad(a0, H0, cplx{r.b[i], 0.0});
+    H1 = cmad(a1, H1, cplx{r.b[i], 0.0});
+    out[i] = fma(mw0.re, H0.re, fma(-mw0.im, H0.im, out[i]));
+    out[i] = fma(mw1.re, H1.re, fma(-mw1.im, H1.im, out[i]));
+    out[j] = fma(mw0.re, K0.re, fma(-mw0.im, K0.im, out[j]));
+    out[j] = fma(mw1.re, K1.re, fma(-mw1.im, K1.im, out[j]));
+    if (j > 0) {
+      const cplx e0 = gap_factor<D>(c0, s0, r.g[j]);
+      const cplx e1 = gap_factor<D>(c1, s1, r.g[j]);
+      K0 = cmad(e0, K0, cplx{r.b[j - 1], 0.0});
+      K1 = cmad(e1, K1, cplx{r.b[j - 1], 0.0});
+    }
+  }
+}
+
+#ifndef FGT_PASS2_PAIRS
+#define FGT_PASS2_PAIRS 0
+#endif
 #ifndef FGT_MODE_UNROLL
 #define FGT_MODE_UNROLL 1
 #endif
@@ -254,6 +294,12 @@ template <int D, bool MS>
 __device__ __forceinline__ void pass2(const ModeTable& mt, int ne, const LaneRun& r,
                                       const Carry* carry, double (&out)[kR],
                                       const ModeSumsOut& ms) {
+#if FGT_PASS2_PAIRS
+  if constexpr (!MS) {
+    for (int k = 0; k < ne; k += 2) pass2_pair_body<D>(mt, k, k + 1 < ne, r, carry, out);
+    return;
+  }
+#endif
 #pragma unroll kModeUnroll
   for (int k = 0; k < ne; ++k) {
     Coef<D> c;
