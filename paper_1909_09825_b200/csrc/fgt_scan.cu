@@ -640,6 +640,12 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ------------------------------------------------------------------- K3
+#ifndef FGT_PHASE_TIMING
+#define FGT_PHASE_TIMING 0
+#endif
+#if FGT_PHASE_TIMING
+__device__ unsigned long long g_phase_cycles[8];
+#endif
 
 #ifndef FGT_K3_MINB
 #define FGT_K3_MINB 4
@@ -659,6 +665,9 @@ __global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
   __syncthreads();
   for (int64_t s = (int64_t)blockIdx.x * kSegWarps + warp; s < a.nseg;
        s += (int64_t)gridDim.x * kSegWarps) {
+#if FGT_PHASE_TIMING
+    const long long t0 = clock64();
+#endif
     const SegGeom g = seg_geom(a, s);
     const SegFrame f = seg_frame(g);
     // segment carries: lane q < ne forward of mode q, ne <= q < 2ne backward
@@ -677,6 +686,9 @@ __global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
     for (int e = 1; e < kR; ++e) gmax = fmax(gmax, r.g[e] - r.g[e - 1]);
     const int D = pick_degree(P, warp_max(gmax));
     const int DM = seg_moment_degree(P, f);
+#if FGT_PHASE_TIMING
+    const long long t1 = clock64();
+#endif
     Carry* mine = carries + lane * ne;
     bool done = false;
     if (D >= 0) {
@@ -704,6 +716,9 @@ __global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
     r.g[0] -= zp;
     if (!done) carries_scan(mt, ne, r, lane, seg_c, seg_c, 0, mine);
     __syncwarp();
+#if FGT_PHASE_TIMING
+    const long long t2 = clock64();
+#endif
 
     double out[kR];
 #pragma unroll
@@ -713,6 +728,9 @@ __global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
       dispatch_pass2<true>(D, mt, ne, r, mine, out, ms);
     } else {
       dispatch_pass2<false>(D, mt, ne, r, mine, out, ModeSumsOut{nullptr, nullptr, 0, 0});
+#if FGT_PHASE_TIMING
+      const long long t3 = clock64();
+#endif
       int tk = r.tfirst;
 #pragma unroll
       for (int e = 0; e < kR; ++e)
@@ -724,6 +742,16 @@ __global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
       } else {
         for (int i = lane; i < g.nx; i += 32) o.u[base + i] = su[i];
       }
+#if FGT_PHASE_TIMING
+      const long long t4 = clock64();
+      if (lane == 0) {
+        atomicAdd(&g_phase_cycles[0], (unsigned long long)(t1 - t0));
+        atomicAdd(&g_phase_cycles[1], (unsigned long long)(t2 - t1));
+        atomicAdd(&g_phase_cycles[2], (unsigned long long)(t3 - t2));
+        atomicAdd(&g_phase_cycles[3], (unsigned long long)(t4 - t3));
+        atomicAdd(&g_phase_cycles[4], 1ull);
+      }
+#endif
     }
     __syncwarp();
   }
@@ -1181,3 +1209,17 @@ cudaError_t launch_gather(const double* alpha, const int32_t* perm, int64_t n, d
 }
 
 }  // namespace fgt_b200
+
+// Debug: per-phase warp cycles of K3 (only in FGT_PHASE_TIMING builds):
+// [0] loads+degrees, [1] carries, [2] pass 2, [3] output, [4] segments.
+extern "C" int fgt_debug_phase_cycles(unsigned long long* out) {
+#if FGT_PHASE_TIMING
+  cudaMemcpyFromSymbol(out, fgt_b200::g_phase_cycles, sizeof(unsigned long long) * 8);
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(fgt_b200::g_phase_cycles, z, sizeof(z));
+  return 1;
+#else
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  return 0;
+#endif
+}
