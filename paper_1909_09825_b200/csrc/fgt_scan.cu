@@ -174,6 +174,52 @@ __device__ __forceinline__ SegFrame seg_frame(const SegGeom& g) {
   return f;
 }
 
+// Lane run from the merged arrays: the coordinates (plan) and strengths (K1)
+// of the lane's kR merged positions are contiguous, so the loads depend only
+// on (segment, lane) and all issue at once.  Coordinates are left in r.g
+// (converted to gaps by the caller); zp = coordinate preceding the run, zl =
+// coordinate of its last element; padding elements sit on zl (gap 0).
+__device__ __forceinline__ void lane_load(const StreamArgs& a, const SegGeom& g, int64_t s,
+                                          int lane, LaneRun& r, double& zp, double& zl) {
+  const uint32_t word = __ldg(a.seg_mask + s * (kSeg / 32) + (lane >> 2));
+  const int d0 = lane * kR;
+  const int nreal = g.len - d0 < 0 ? 0 : (g.len - d0 < kR ? g.len - d0 : kR);
+  const double2* zs = reinterpret_cast<const double2*>(a.zm + s * kSeg + d0);
+  const double2* bs = reinterpret_cast<const double2*>(a.bm + s * kSeg + d0);
+#pragma unroll
+  for (int e = 0; e < kR; e += 2) {
+    const double2 zv = __ldg(zs + e / 2);
+    const double2 bv = *(bs + e / 2);
+    r.g[e] = zv.x;
+    r.g[e + 1] = zv.y;
+    r.b[e] = bv.x;
+    r.b[e + 1] = bv.y;
+  }
+  const unsigned byte = (word >> ((lane & 3) * 8)) & 0xffu & ((1u << nreal) - 1u);
+  const int nt = __popc(byte);
+  int incl = nt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  r.tfirst = incl - nt;
+  r.tmask = byte;
+  double last = 0.0;
+#pragma unroll
+  for (int e = 0; e < kR; ++e)
+    if (e < nreal) last = r.g[e];
+  double prev = __shfl_up_sync(0xffffffffu, last, 1);
+  if (lane == 0) prev = g.zprev;
+  zp = prev;
+  zl = nreal > 0 ? last : prev;
+#pragma unroll
+  for (int e = 0; e < kR; ++e) {
+    r.g[e] = e < nreal ? r.g[e] : zl;
+    r.b[e] = e < nreal ? r.b[e] : 0.0;
+  }
+}
+
 // --------------------------------------------------------------- pass 2
 
 // Mode-sums test hook (detail::mode_sums, transform.cpp:310-350): store H
@@ -442,12 +488,9 @@ __device__ __forceinline__ void carries_scan(const ModeTable& mt, int ne, const 
 
 // -------------------------------------------------------- shared memory
 
-// Per-warp region of K3: prefetch buffer (SegPrefetch), lane carries, output
-// staging.  (The prefetch struct is defined with K3; its size is fixed.)
-constexpr size_t kPrefetchBytes = sizeof(double) * 32 * 2 * kR + 16 + 16 + 4 * (kSeg / 32) +
-                                  sizeof(cplx) * 2 * kMaxModes;
+// Per-warp region of K3: lane carries, then the output staging.
 __host__ __device__ __forceinline__ size_t warp_region_bytes(int ne) {
-  return ((kPrefetchBytes + 15) / 16) * 16 + sizeof(Carry) * 32 * (size_t)ne + sizeof(double) * kSeg;
+  return sizeof(Carry) * 32 * (size_t)ne + sizeof(double) * kSeg;
 }
 
 // ------------------------------------------------------------------- K1
@@ -637,54 +680,6 @@ __device__ unsigned long long g_phase_cycles[8];
 #ifndef FGT_K3_MINB
 #define FGT_K3_MINB 4
 #endif
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8v(void* dst, const void* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
-}
-
-// Everything K3 reads for one segment, prefetched one iteration ahead with
-// cp.async (no registers held across the compute of the current segment).
-struct SegPrefetch {
-  double run[32][2 * kR];  // per lane: merged coordinates [0, kR), strengths [kR, 2kR)
-  int64_t ib[2];           // seg_ib[s], seg_ib[s + 1]
-  double2 z;               // (zprev, zlast)
-  uint32_t mask[kSeg / 32];
-  cplx cc[2 * kMaxModes];  // Cf[k][s] (k < ne), then Cb[k][s]
-};
-
-__device__ __forceinline__ void issue_prefetch(const StreamArgs& a, const TileState& ts, int ne,
-                                               int64_t s, int lane, SegPrefetch& pb) {
-  const double* zsrc = a.zm + s * kSeg + lane * kR;
-  const double* bsrc = a.bm + s * kSeg + lane * kR;
-#pragma unroll
-  for (int e = 0; e < kR; e += 2) {
-    cp_async16(&pb.run[lane][e], zsrc + e);
-    cp_async16(&pb.run[lane][kR + e], bsrc + e);
-  }
-  if (lane == 0) {
-    cp_async8v(&pb.ib[0], a.seg_ib + s);
-    cp_async8v(&pb.ib[1], a.seg_ib + s + 1);
-  } else if (lane == 1) {
-    cp_async16(&pb.z, a.seg_z + s);
-  } else if (lane == 2 || lane == 3) {
-    cp_async16(&pb.mask[4 * (lane - 2)], a.seg_mask + s * (kSeg / 32) + 4 * (lane - 2));
-  } else if (lane >= 4 && lane < 4 + 2 * ne) {
-    const int q = lane - 4;
-    const int k = q < ne ? q : q - ne;
-    cp_async16(&pb.cc[q], (q < ne ? ts.Cf : ts.Cb) + (int64_t)k * a.nseg + s);
-  }
-  cp_async_commit();
-}
-
-static_assert(sizeof(SegPrefetch) <= ((kPrefetchBytes + 15) / 16) * 16, "prefetch layout");
-
-// K3: persistent warps over segments.  While segment s is computed, the
-// next segment's run and metadata stream into shared memory (cp.async).
 template <bool MS>
 __global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
     seg_main_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
@@ -694,73 +689,28 @@ __global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ne = P.ne;
   unsigned char* wreg = smem_raw + sizeof(ModeTable) + (size_t)warp * warp_region_bytes(ne);
-  SegPrefetch& pb = *reinterpret_cast<SegPrefetch*>(wreg);
-  Carry* carries = reinterpret_cast<Carry*>(wreg + sizeof(SegPrefetch));
-  double* su = reinterpret_cast<double*>(wreg + sizeof(SegPrefetch) + sizeof(Carry) * 32 * (size_t)ne);
+  Carry* carries = reinterpret_cast<Carry*>(wreg);
+  double* su = reinterpret_cast<double*>(wreg + sizeof(Carry) * 32 * (size_t)ne);
   load_mode_table(mtab, mt);
   __syncthreads();
-  const int64_t stride = (int64_t)gridDim.x * kSegWarps;
-  const int64_t L = a.M + a.N;
-  int64_t s = (int64_t)blockIdx.x * kSegWarps + warp;
-  if (s < a.nseg) issue_prefetch(a, ts, ne, s, lane, pb);
-  for (; s < a.nseg; s += stride) {
+  for (int64_t s = (int64_t)blockIdx.x * kSegWarps + warp; s < a.nseg;
+       s += (int64_t)gridDim.x * kSegWarps) {
 #if FGT_PHASE_TIMING
     const long long t0 = clock64();
 #endif
-    cp_async_wait_all();
-    __syncwarp();
-    // ---- this segment from shared memory
-    SegGeom g;
-    {
-      const int64_t d0 = s * kSeg;
-      const int64_t d1 = (d0 + kSeg < L) ? d0 + kSeg : L;
-      g.ib = pb.ib[0];
-      const int64_t ie = pb.ib[1];
-      g.jb = d0 - g.ib;
-      g.nx = (int)(ie - g.ib);
-      g.ny = (int)((d1 - ie) - g.jb);
-      g.len = (int)(d1 - d0);
-      g.zprev = s == 0 ? a.zprev0 : pb.z.x;
-      g.zlast = pb.z.y;
-    }
+    const SegGeom g = seg_geom(a, s);
     const SegFrame f = seg_frame(g);
-    const cplx seg_c = lane < 2 * ne ? pb.cc[lane] : cplx{0.0, 0.0};
-    const uint32_t word = pb.mask[lane >> 2];
+    // segment carries: lane q < ne forward of mode q, ne <= q < 2ne backward
+    cplx seg_c = {0.0, 0.0};
+    if (lane < 2 * ne) {
+      const int k = lane < ne ? lane : lane - ne;
+      const int64_t idx = (int64_t)k * a.nseg + s;
+      seg_c = lane < ne ? ts.Cf[idx] : ts.Cb[idx];
+    }
     LaneRun r;
-    const int d0l = lane * kR;
-    const int nreal = g.len - d0l < 0 ? 0 : (g.len - d0l < kR ? g.len - d0l : kR);
-#pragma unroll
-    for (int e = 0; e < kR; ++e) {
-      r.g[e] = pb.run[lane][e];
-      r.b[e] = pb.run[lane][kR + e];
-    }
-    __syncwarp();
-    if (s + stride < a.nseg) issue_prefetch(a, ts, ne, s + stride, lane, pb);
-    // ---- run layout, padding, degrees
-    const unsigned byte = (word >> ((lane & 3) * 8)) & 0xffu & ((1u << nreal) - 1u);
-    {
-      const int nt = __popc(byte);
-      int incl = nt;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += v;
-      }
-      r.tfirst = incl - nt;
-      r.tmask = byte;
-    }
-    double last = 0.0;
-#pragma unroll
-    for (int e = 0; e < kR; ++e)
-      if (e < nreal) last = r.g[e];
-    double zp = __shfl_up_sync(0xffffffffu, last, 1);
-    if (lane == 0) zp = g.zprev;
-    const double zl = nreal > 0 ? last : zp;
-#pragma unroll
-    for (int e = 0; e < kR; ++e) {
-      r.g[e] = e < nreal ? r.g[e] : zl;
-      r.b[e] = e < nreal ? r.b[e] : 0.0;
-    }
+    double zp, zl;
+    lane_load(a, g, s, lane, r, zp, zl);
+    // gaps (coordinates are still needed by the moment path)
     double gmax = r.g[0] - zp;
 #pragma unroll
     for (int e = 1; e < kR; ++e) gmax = fmax(gmax, r.g[e] - r.g[e - 1]);
