@@ -179,7 +179,6 @@ void build_modes(const Soe& folded, double delta, ModeParams& P, ModeTable& T) {
 // Per-chunk persistent state for the two-phase (multi-GPU) apply.
 struct ChunkState {
   double* bs = nullptr;  // strengths, sorted-source order
-  double* bm = nullptr;  // strengths in merged order (K1 -> K3)
   cplx* tile = nullptr;  // 5 * ne * ntiles
 };
 
@@ -201,7 +200,6 @@ struct fgt_plan_s {
   int64_t* d_tile_ib = nullptr;
   double2* d_seg_z = nullptr;
   uint32_t* d_seg_mask = nullptr;
-  double* d_zm = nullptr;  // merged coordinates, kSeg-padded
   double zprev0 = 0.0;
   int* d_flag = nullptr;
   ChunkState cs;
@@ -303,7 +301,7 @@ void plan_tiles(fgt_plan_s* p, const double* xd, const double* yd, bool check_so
   int64_t* tib = dmalloc<int64_t>(ntl + 1, st);
   ck(launch_partition(xd, p->M, yd, p->N, kPlanTile, ntl, tib, st), "partition");
   ck(launch_plan_tiles(xd, p->M, yd, p->N, tib, ntl, p->ntiles, check_sorted ? 1 : 0,
-                       p->d_tile_ib, p->d_seg_z, p->d_seg_mask, p->d_zm, p->d_flag, st),
+                       p->d_tile_ib, p->d_seg_z, p->d_seg_mask, p->d_flag, st),
      "plan tiles");
   dfree(tib, st);
 }
@@ -332,8 +330,6 @@ void destroy_plan(fgt_plan_s* p) {
   dfree(p->d_tile_ib, st);
   dfree(p->d_seg_z, st);
   dfree(p->d_seg_mask, st);
-  dfree(p->d_zm, st);
-  dfree(p->cs.bm, st);
   dfree(p->d_mt, st);
   dfree(p->d_flag, st);
   dfree(p->cs.bs, st);
@@ -406,8 +402,7 @@ void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint3
   } else {
     const double* bs = sorted_strengths(p, strengths, flags, w, nullptr);
     const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0,
-                        p->d_seg_z, p->d_seg_mask, p->d_zm,
-                        w.get<double>((size_t)p->ntiles * kSeg)};
+                        p->d_seg_z, p->d_seg_mask};
     const TileState ts = tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, p->P.ne)),
                                           p->ntiles, p->P.ne);
     {
@@ -442,7 +437,6 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ho
   Work w{st, {}};
   if (!p->cs.tile) p->cs.tile = dmalloc<cplx>(tile_state_elems(p->ntiles, ne), p->stream);
   if (!p->cs.bs && p->N) p->cs.bs = dmalloc<double>(p->N, p->stream);
-  if (!p->cs.bm) p->cs.bm = dmalloc<double>((size_t)p->ntiles * kSeg, p->stream);
   if (st != p->stream) ck(cudaStreamSynchronize(p->stream), "sync");
   sorted_strengths(p, strengths, flags, w, p->cs.bs);
   if (p->ntiles == 0) {
@@ -455,7 +449,7 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ho
     return;
   }
   const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0,
-                        p->d_seg_z, p->d_seg_mask, p->d_zm, p->cs.bm};
+                        p->d_seg_z, p->d_seg_mask};
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
   ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
   cplx* d_tot = w.get<cplx>(3 * ne);
@@ -477,7 +471,7 @@ void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in_host, double* potentia
     raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
   if (!p->cs.tile) raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
   const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0,
-                        p->d_seg_z, p->d_seg_mask, p->d_zm, p->cs.bm};
+                        p->d_seg_z, p->d_seg_mask};
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
   cplx* d_cin = w.get<cplx>(2 * ne);
   ck(cudaMemcpyAsync(d_cin, carry_in_host, sizeof(cplx) * 2 * ne, cudaMemcpyHostToDevice, st),
@@ -591,7 +585,6 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
       p->d_seg_z = dmalloc<double2>(p->ntiles, st);
       p->d_seg_mask = dmalloc<uint32_t>((size_t)p->ntiles * (kSeg / 32), st);
-      p->d_zm = dmalloc<double>((size_t)p->ntiles * kSeg, st);
       // one read of both sets: checks + (speculative) segment metadata
       plan_tiles(p, xs.dptr, ys.dptr, !(flags & FGT_ASSUME_SORTED), st);
       int hf[8] = {0};
@@ -827,8 +820,7 @@ extern "C" int fgt_mode_sums(fgt_plan_t p, const double* strengths, double* hp, 
     } else {
       const double* bs = sorted_strengths(p, strengths, 0, w, nullptr);
       const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0,
-                        p->d_seg_z, p->d_seg_mask, p->d_zm,
-                        w.get<double>((size_t)p->ntiles * kSeg)};
+                        p->d_seg_z, p->d_seg_mask};
       const TileState ts = tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, ne)),
                                             p->ntiles, ne);
       ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "aggregates");

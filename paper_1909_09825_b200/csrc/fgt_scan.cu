@@ -174,28 +174,17 @@ __device__ __forceinline__ SegFrame seg_frame(const SegGeom& g) {
   return f;
 }
 
-// Lane run from the merged arrays: the coordinates (plan) and strengths (K1)
-// of the lane's kR merged positions are contiguous, so the loads depend only
-// on (segment, lane) and all issue at once.  Coordinates are left in r.g
-// (converted to gaps by the caller); zp = coordinate preceding the run, zl =
-// coordinate of its last element; padding elements sit on zl (gap 0).
+// Lane run from the plan-time merge mask: no merge, no shared-memory
+// staging; every element is an independent load.  Coordinates are left in
+// r.g (converted to gaps by lane_gaps); zp = coordinate preceding the run,
+// zl = coordinate of its last element.
 __device__ __forceinline__ void lane_load(const StreamArgs& a, const SegGeom& g, int64_t s,
                                           int lane, LaneRun& r, double& zp, double& zl) {
   const uint32_t word = __ldg(a.seg_mask + s * (kSeg / 32) + (lane >> 2));
   const int d0 = lane * kR;
   const int nreal = g.len - d0 < 0 ? 0 : (g.len - d0 < kR ? g.len - d0 : kR);
-  const double2* zs = reinterpret_cast<const double2*>(a.zm + s * kSeg + d0);
-  const double2* bs = reinterpret_cast<const double2*>(a.bm + s * kSeg + d0);
-#pragma unroll
-  for (int e = 0; e < kR; e += 2) {
-    const double2 zv = __ldg(zs + e / 2);
-    const double2 bv = *(bs + e / 2);
-    r.g[e] = zv.x;
-    r.g[e + 1] = zv.y;
-    r.b[e] = bv.x;
-    r.b[e + 1] = bv.y;
-  }
-  const unsigned byte = (word >> ((lane & 3) * 8)) & 0xffu & ((1u << nreal) - 1u);
+  const unsigned live = (1u << nreal) - 1u;
+  const unsigned byte = (word >> ((lane & 3) * 8)) & 0xffu & live;
   const int nt = __popc(byte);
   int incl = nt;
 #pragma unroll
@@ -203,21 +192,36 @@ __device__ __forceinline__ void lane_load(const StreamArgs& a, const SegGeom& g,
     const int v = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += v;
   }
-  r.tfirst = incl - nt;
+  const int i0 = incl - nt;
+  const int j0 = (d0 < g.len ? d0 : g.len) - i0;
+  r.tfirst = i0;
   r.tmask = byte;
   double last = 0.0;
 #pragma unroll
-  for (int e = 0; e < kR; ++e)
-    if (e < nreal) last = r.g[e];
+  for (int e = 0; e < kR; ++e) {
+    const int t = __popc(byte & ((1u << e) - 1u));
+    const int sidx = e - t;
+    if (e < nreal) {
+      if (byte & (1u << e)) {
+        r.g[e] = __ldg(a.xs + g.ib + i0 + t);
+        r.b[e] = 0.0;
+      } else {
+        r.g[e] = __ldg(a.ys + g.jb + j0 + sidx);
+        r.b[e] = __ldg(a.bs + g.jb + j0 + sidx);
+      }
+      last = r.g[e];
+    } else {
+      r.g[e] = 0.0;
+      r.b[e] = 0.0;
+    }
+  }
   double prev = __shfl_up_sync(0xffffffffu, last, 1);
   if (lane == 0) prev = g.zprev;
   zp = prev;
   zl = nreal > 0 ? last : prev;
+  // padding elements sit on the run's last coordinate: their gaps are 0
 #pragma unroll
-  for (int e = 0; e < kR; ++e) {
-    r.g[e] = e < nreal ? r.g[e] : zl;
-    r.b[e] = e < nreal ? r.b[e] : 0.0;
-  }
+  for (int e = 0; e < kR; ++e) r.g[e] = e < nreal ? r.g[e] : zl;
 }
 
 // --------------------------------------------------------------- pass 2
@@ -495,25 +499,31 @@ __host__ __device__ __forceinline__ size_t warp_region_bytes(int ne) {
 
 // ------------------------------------------------------------------- K1
 
-// Moment aggregates of a segment from the lane-held merged run (targets have
-// b = 0): M_n = sum b (z - zc)^n reduced over the warp, then per mode
-// A = e^{-s h0} e^{-s h1}, F = e^{-s h1} sum s^n/n! M_n, G = e^{-s h0} sum (-s)^n/n! M_n.
 template <int DM>
-__device__ __forceinline__ void seg_aggregate_moments(const ModeTable& mt, int ne, int lane,
-                                                      const SegFrame& f, const LaneRun& r,
-                                                      int64_t nseg, int64_t s, TileState ts) {
+__device__ __forceinline__ void seg_aggregate_moments(const StreamArgs& a, const SegGeom& g,
+                                                      const SegFrame& f, const ModeTable& mt,
+                                                      int ne, int lane, int64_t s, TileState ts) {
   double M[DM + 1];
 #pragma unroll
   for (int n = 0; n <= DM; ++n) M[n] = 0.0;
+  for (int j0 = lane; j0 < g.ny; j0 += 4 * 32) {
+    double yv[4], bv[4];
 #pragma unroll
-  for (int e = 0; e < kR; ++e) {
-    const double d = r.g[e] - f.zc;
-    double p = r.b[e];
-    M[0] += p;
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * 32;
+      yv[u] = j < g.ny ? __ldg(a.ys + g.jb + j) : f.zc;
+      bv[u] = j < g.ny ? __ldg(a.bs + g.jb + j) : 0.0;
+    }
 #pragma unroll
-    for (int n = 1; n <= DM; ++n) {
-      p *= d;
-      M[n] += p;
+    for (int u = 0; u < 4; ++u) {
+      const double d = yv[u] - f.zc;
+      double p = bv[u];
+      M[0] += p;
+#pragma unroll
+      for (int n = 1; n <= DM; ++n) {
+        p *= d;
+        M[n] += p;
+      }
     }
   }
 #pragma unroll
@@ -539,7 +549,7 @@ __device__ __forceinline__ void seg_aggregate_moments(const ModeTable& mt, int n
     }
     const cplx E0 = horner<DM>(c, f.h0);
     const cplx E1 = horner<DM>(c, f.h1);
-    const int64_t o = (int64_t)k * nseg + s;
+    const int64_t o = (int64_t)k * a.nseg + s;
     ts.A[o] = cmul(E0, E1);
     ts.F[o] = cmul(E1, cplx{ev.re - od.re, ev.im - od.im});
     ts.G[o] = cmul(E0, cplx{ev.re + od.re, ev.im + od.im});
@@ -574,10 +584,9 @@ __device__ __forceinline__ int seg_moment_degree(const ModeParams& P, const SegF
   return DM <= kRegDeg ? DM : -1;
 }
 
-// K1: warps loop over segments (grid-stride).  Each lane gathers the
-// strengths of its run's sources into merged order (bm, read back by K3 as a
-// contiguous run), then the segment aggregates come from moments (narrow
-// segments) or exact per-element lane aggregates reduced across the warp.
+// K1: warps loop over segments (grid-stride).  Moment path for narrow
+// segments; exact per-element lane aggregates reduced across the warp
+// otherwise.
 __global__ void __launch_bounds__(kThreads)
     seg_aggregate_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
                          TileState ts) {
@@ -590,53 +599,11 @@ __global__ void __launch_bounds__(kThreads)
        s += (int64_t)gridDim.x * kSegWarps) {
     const SegGeom g = seg_geom(a, s);
     const SegFrame f = seg_frame(g);
-    // this lane's run: coordinates from the plan, strengths gathered by source index
-    const uint32_t word = __ldg(a.seg_mask + s * (kSeg / 32) + (lane >> 2));
-    const int d0 = lane * kR;
-    const int nreal = g.len - d0 < 0 ? 0 : (g.len - d0 < kR ? g.len - d0 : kR);
-    const unsigned byte = (word >> ((lane & 3) * 8)) & 0xffu & ((1u << nreal) - 1u);
-    const int nt = __popc(byte);
-    int incl = nt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += v;
-    }
-    const int j0 = (d0 < g.len ? d0 : g.len) - (incl - nt);
-    LaneRun r;
-    const double2* zs = reinterpret_cast<const double2*>(a.zm + s * kSeg + d0);
-#pragma unroll
-    for (int e = 0; e < kR; e += 2) {
-      const double2 zv = __ldg(zs + e / 2);
-      r.g[e] = zv.x;
-      r.g[e + 1] = zv.y;
-    }
-#pragma unroll
-    for (int e = 0; e < kR; ++e) {
-      const int sidx = e - __popc(byte & ((1u << e) - 1u));
-      const bool src = e < nreal && !(byte & (1u << e));
-      r.b[e] = src ? __ldg(a.bs + g.jb + j0 + sidx) : 0.0;
-    }
-    {
-      double2* bo = reinterpret_cast<double2*>(a.bm + s * kSeg + d0);
-#pragma unroll
-      for (int e = 0; e < kR; e += 2) bo[e / 2] = make_double2(r.b[e], r.b[e + 1]);
-    }
-    double last = 0.0;
-#pragma unroll
-    for (int e = 0; e < kR; ++e)
-      if (e < nreal) last = r.g[e];
-    double zp = __shfl_up_sync(0xffffffffu, last, 1);
-    if (lane == 0) zp = g.zprev;
-    const double zl = nreal > 0 ? last : zp;
-#pragma unroll
-    for (int e = 0; e < kR; ++e) r.g[e] = e < nreal ? r.g[e] : zl;
-
     const int DM = seg_moment_degree(P, f);
     switch (DM) {
-#define FGT_K1(n)                                                        \
-  case n:                                                                \
-    seg_aggregate_moments<n>(mt, ne, lane, f, r, a.nseg, s, ts);         \
+#define FGT_K1(n)                                                  \
+  case n:                                                          \
+    seg_aggregate_moments<n>(a, g, f, mt, ne, lane, s, ts);        \
     continue;
       FGT_K1(0) FGT_K1(1) FGT_K1(2) FGT_K1(3) FGT_K1(4) FGT_K1(5) FGT_K1(6) FGT_K1(7)
       FGT_K1(8)
@@ -644,6 +611,9 @@ __global__ void __launch_bounds__(kThreads)
       default:
         break;
     }
+    LaneRun r;
+    double zp, zl;
+    lane_load(a, g, s, lane, r, zp, zl);
 #pragma unroll
     for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
     r.g[0] -= zp;
@@ -813,8 +783,7 @@ __global__ void __launch_bounds__(256)
     plan_tile_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
                      int64_t N, const int64_t* __restrict__ tile_ib, int64_t nseg,
                      int check_sorted, int64_t* __restrict__ seg_ib, double2* __restrict__ seg_z,
-                     uint32_t* __restrict__ seg_mask, double* __restrict__ zm,
-                     int* __restrict__ flags) {
+                     uint32_t* __restrict__ seg_mask, int* __restrict__ flags) {
   extern __shared__ double tsm[];
   double* sx = tsm;              // [kPlanTile]
   double* sy = tsm + kPlanTile;  // [kPlanTile]
@@ -885,9 +854,6 @@ __global__ void __launch_bounds__(256)
     // each lane merges its window of kR positions (merge path in shared memory)
     const int w0 = sd0 + lane * kR;
     unsigned byte = 0u;
-    double zw[kR];
-#pragma unroll
-    for (int e = 0; e < kR; ++e) zw[e] = 0.0;
     if (w0 < sd1 && i1 >= i0 && j1 >= j0) {
       // merge path restricted to the segment: targets [i0, i1), sources [j0, j1)
       int i = i0 + (int)merge_path(sx + i0, (int64_t)(i1 - i0), sy + j0, (int64_t)(j1 - j0),
@@ -899,11 +865,9 @@ __global__ void __launch_bounds__(256)
       for (int e = 0; e < kR; ++e) {
         if (w0 + e < sd1) {
           if (cy <= cx && j < j1) {  // source first on ties
-            zw[e] = cy;
             ++j;
             cy = j < j1 ? sy[j] : INFINITY;
           } else {
-            zw[e] = cx;
             byte |= 1u << e;
             ++i;
             cx = i < i1 ? sx[i] : INFINITY;
@@ -916,11 +880,6 @@ __global__ void __launch_bounds__(256)
     wd |= __shfl_down_sync(0xffffffffu, wd, 2);
     const int64_t sg = t * kPlanSegs + k;
     if ((lane & 3) == 0) seg_mask[sg * (kSeg / 32) + (lane >> 2)] = wd;
-    {
-      double2* zo = reinterpret_cast<double2*>(zm + sg * kSeg + lane * kR);
-#pragma unroll
-      for (int e = 0; e < kR; e += 2) zo[e / 2] = make_double2(zw[e], zw[e + 1]);
-    }
     if (lane == 0) {
       seg_ib[sg] = ib + i0;
       double px, py;
@@ -1164,7 +1123,7 @@ cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int6
 cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int64_t N,
                               const int64_t* tile_ib, int64_t ntiles, int64_t nseg,
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
-                              uint32_t* seg_mask, double* zm, int* flags, cudaStream_t st) {
+                              uint32_t* seg_mask, int* flags, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
   const size_t smem = sizeof(double) * 2 * kPlanTile;
   static bool done = false;
@@ -1176,7 +1135,7 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
   }
   note_launch();
   plan_tile_kernel<<<(unsigned)ntiles, 256, smem, st>>>(xs, M, ys, N, tile_ib, nseg, check_sorted,
-                                                         seg_ib, seg_z, seg_mask, zm, flags);
+                                                         seg_ib, seg_z, seg_mask, flags);
   return cudaGetLastError();
 }
 

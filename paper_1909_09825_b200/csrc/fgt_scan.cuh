@@ -42,10 +42,6 @@ struct StreamArgs {
   // the merged order as one bit per element (1 = target), 8 words/segment
   const double2* seg_z;
   const uint32_t* seg_mask;
-  // merged stream, kSeg-padded per segment: coordinates (plan) and strengths
-  // (written by K1 each apply: beta for a source, 0 for a target)
-  const double* zm;
-  double* bm;
 };
 
 struct OutArgs {
@@ -82,7 +78,7 @@ cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int6
 cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int64_t N,
                               const int64_t* tile_ib, int64_t ntiles, int64_t nseg,
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
-                              uint32_t* seg_mask, double* zm, int* flags, cudaStream_t st);
+                              uint32_t* seg_mask, int* flags, cudaStream_t st);
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, cudaStream_t st);
 // K2: exclusive carries per segment.  carry_in: 2*ne complex (forward carry at
