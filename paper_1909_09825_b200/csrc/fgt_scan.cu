@@ -397,6 +397,10 @@ __device__ __forceinline__ void carries_moments(const ModeTable& mt, int ne, con
     }
   }
   const double u = zp - f.zc, v = zl - f.zc;
+#ifndef FGT_CARRY_UNROLL
+#define FGT_CARRY_UNROLL 1
+#endif
+#pragma unroll FGT_CARRY_UNROLL
   for (int k = 0; k < ne; ++k) {
     Coef<DM> c;
     c.load(mt, k);
