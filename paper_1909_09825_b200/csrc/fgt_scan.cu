@@ -283,6 +283,10 @@ __device__ __forceinline__ void pass2_pair_body(const ModeTable& mt, int k, bool
   }
 }
 
+#ifndef FGT_CARRY_UNROLL
+#define FGT_CARRY_UNROLL 1
+#endif
+constexpr int kCarryUnroll = FGT_CARRY_UNROLL;
 #ifndef FGT_PASS2_PAIRS
 #define FGT_PASS2_PAIRS 0
 #endif
@@ -397,10 +401,7 @@ __device__ __forceinline__ void carries_moments(const ModeTable& mt, int ne, con
     }
   }
   const double u = zp - f.zc, v = zl - f.zc;
-#ifndef FGT_CARRY_UNROLL
-#define FGT_CARRY_UNROLL 1
-#endif
-#pragma unroll FGT_CARRY_UNROLL
+#pragma unroll kCarryUnroll
   for (int k = 0; k < ne; ++k) {
     Coef<DM> c;
     c.load(mt, k);
