@@ -171,6 +171,7 @@ void build_modes(const Soe& folded, double delta, ModeParams& P, ModeTable& T) {
     }
   }
   P.smax = smax;
+  T.smax = smax;
   fill_rmax(P);
 }
 
@@ -200,6 +201,12 @@ struct fgt_plan_s {
   int64_t* d_tile_ib = nullptr;
   double2* d_seg_z = nullptr;
   uint32_t* d_seg_mask = nullptr;
+  // batched plans (fgt_batch_create)
+  bool batch = false;
+  int nbatch = 0;
+  int64_t* d_seg_jb = nullptr;
+  int4* d_seg_info = nullptr;
+  ModeTable* d_mtb = nullptr;
   double zprev0 = 0.0;
   int* d_flag = nullptr;
   ChunkState cs;
@@ -330,6 +337,9 @@ void destroy_plan(fgt_plan_s* p) {
   dfree(p->d_tile_ib, st);
   dfree(p->d_seg_z, st);
   dfree(p->d_seg_mask, st);
+  dfree(p->d_seg_jb, st);
+  dfree(p->d_seg_info, st);
+  dfree(p->d_mtb, st);
   dfree(p->d_mt, st);
   dfree(p->d_flag, st);
   dfree(p->cs.bs, st);
@@ -402,7 +412,7 @@ void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint3
   } else {
     const double* bs = sorted_strengths(p, strengths, flags, w, nullptr);
     const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0,
-                        p->d_seg_z, p->d_seg_mask};
+                        p->d_seg_z, p->d_seg_mask, p->d_seg_info, p->d_seg_jb, p->d_mtb};
     const TileState ts = tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, p->P.ne)),
                                           p->ntiles, p->P.ne);
     {
@@ -449,7 +459,7 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ho
     return;
   }
   const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0,
-                        p->d_seg_z, p->d_seg_mask};
+                        p->d_seg_z, p->d_seg_mask, p->d_seg_info, p->d_seg_jb, p->d_mtb};
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
   ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
   cplx* d_tot = w.get<cplx>(3 * ne);
@@ -471,7 +481,7 @@ void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in_host, double* potentia
     raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
   if (!p->cs.tile) raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
   const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0,
-                        p->d_seg_z, p->d_seg_mask};
+                        p->d_seg_z, p->d_seg_mask, p->d_seg_info, p->d_seg_jb, p->d_mtb};
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
   cplx* d_cin = w.get<cplx>(2 * ne);
   ck(cudaMemcpyAsync(d_cin, carry_in_host, sizeof(cplx) * 2 * ne, cudaMemcpyHostToDevice, st),
@@ -820,7 +830,7 @@ extern "C" int fgt_mode_sums(fgt_plan_t p, const double* strengths, double* hp, 
     } else {
       const double* bs = sorted_strengths(p, strengths, 0, w, nullptr);
       const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0,
-                        p->d_seg_z, p->d_seg_mask};
+                        p->d_seg_z, p->d_seg_mask, p->d_seg_info, p->d_seg_jb, p->d_mtb};
       const TileState ts = tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, ne)),
                                             p->ntiles, ne);
       ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "aggregates");
@@ -866,4 +876,120 @@ extern "C" int fgt_profile_read(double* ms, long long* counts, int nkinds) {
     g_prof_cnt[k] = 0;
   }
   return FGT_OK;
+}
+
+// ---- batched transforms (BASELINE cfg 5) ---------------------------------
+// B independent presorted transforms in one plan: targets / sources are the
+// concatenation of the transforms' sets (host offsets t_off / s_off, B+1
+// entries), one delta per transform, one SOE for all.  Every transform's
+// stream starts at a segment boundary with zprev = -inf, so transforms never
+// couple; each segment reads its transform's mode table.  Apply with
+// fgt_apply_general (strengths / potentials concatenated the same way).
+extern "C" int fgt_batch_create(int B, const double* targets, const int64_t* t_off,
+                                const double* sources, const int64_t* s_off,
+                                const double* deltas, const double* t_re, const double* t_im,
+                                const double* w_re, const double* w_im, const uint8_t* self_conj,
+                                int n_modes, int form, uint32_t flags, int device, void* stream,
+                                fgt_plan_t* out) {
+  return guarded([&] {
+    if (!out) raise(FGT_ERR_INVALID, "out must not be NULL");
+    *out = nullptr;
+    if (B < 1) raise(FGT_ERR_INVALID, "batch needs at least one transform");
+    if (!t_off || !s_off || !deltas) raise(FGT_ERR_INVALID, "offsets / deltas must not be NULL");
+    if (t_off[0] != 0 || s_off[0] != 0) raise(FGT_ERR_INVALID, "offsets must start at 0");
+    for (int b = 0; b < B; ++b) {
+      if (t_off[b + 1] < t_off[b] || s_off[b + 1] < s_off[b])
+        raise(FGT_ERR_INVALID, "offsets must be non-decreasing");
+      check_delta(deltas[b]);
+    }
+    const int64_t M = t_off[B], N = s_off[B];
+    if (M >= ((int64_t)1 << 31) || N >= ((int64_t)1 << 31))
+      raise(FGT_ERR_INVALID, "at most 2^31-1 points per set");
+    Soe soe = resolve_soe(t_re, t_im, w_re, w_im, self_conj, n_modes, form);
+    require_device(device);
+    cudaStream_t st = as_stream(stream);
+    fgt_plan_s* p = new fgt_plan_s();
+    std::vector<void*> temps;
+    try {
+      ck(cudaGetDevice(&p->device), "cudaGetDevice");
+      p->M = M;
+      p->N = N;
+      p->delta = deltas[0];
+      p->soe = soe;
+      p->batch = true;
+      p->nbatch = B;
+      p->stream = st;
+      p->d_flag = dmalloc<int>(8, st);
+      ck(cudaMemsetAsync(p->d_flag, 0, sizeof(int) * 8, st), "flag");
+      SetSrc xs = stage_set(targets, M, flags, st);
+      SetSrc ys = stage_set(sources, N, flags, st);
+      if (xs.tmp) temps.push_back((void*)xs.dptr);
+      if (ys.tmp) temps.push_back((void*)ys.dptr);
+      // segment / tile layout per transform
+      std::vector<int64_t> seg_base(B + 1, 0), tile_base(B + 1, 0);
+      for (int b = 0; b < B; ++b) {
+        const int64_t L = (t_off[b + 1] - t_off[b]) + (s_off[b + 1] - s_off[b]);
+        seg_base[b + 1] = seg_base[b] + (L + kSeg - 1) / kSeg;
+        tile_base[b + 1] = tile_base[b] + (L + kPlanTile - 1) / kPlanTile;
+      }
+      const int64_t nseg = seg_base[B], ntl = tile_base[B];
+      std::vector<int32_t> tile_tid(ntl);
+      for (int b = 0; b < B; ++b)
+        for (int64_t t = tile_base[b]; t < tile_base[b + 1]; ++t) tile_tid[t] = b;
+      p->ntiles = nseg;
+      p->d_tile_ib = dmalloc<int64_t>(nseg + 1, st);
+      p->d_seg_jb = dmalloc<int64_t>(nseg + 1, st);
+      p->d_seg_info = dmalloc<int4>(nseg + 1, st);
+      p->d_seg_z = dmalloc<double2>(nseg + 1, st);
+      p->d_seg_mask = dmalloc<uint32_t>((size_t)(nseg + 1) * (kSeg / 32), st);
+      Work w{st, {}};
+      int64_t* d_toff = w.get<int64_t>(B + 1);
+      int64_t* d_soff = w.get<int64_t>(B + 1);
+      int64_t* d_sbase = w.get<int64_t>(B + 1);
+      int64_t* d_tbase = w.get<int64_t>(B + 1);
+      int32_t* d_ttid = w.get<int32_t>(ntl + 1);
+      int64_t* d_tib = w.get<int64_t>(ntl + 1);
+      ck(cudaMemcpyAsync(d_toff, t_off, 8 * (B + 1), cudaMemcpyHostToDevice, st), "offsets");
+      ck(cudaMemcpyAsync(d_soff, s_off, 8 * (B + 1), cudaMemcpyHostToDevice, st), "offsets");
+      ck(cudaMemcpyAsync(d_sbase, seg_base.data(), 8 * (B + 1), cudaMemcpyHostToDevice, st), "bases");
+      ck(cudaMemcpyAsync(d_tbase, tile_base.data(), 8 * (B + 1), cudaMemcpyHostToDevice, st), "bases");
+      if (ntl)
+        ck(cudaMemcpyAsync(d_ttid, tile_tid.data(), 4 * ntl, cudaMemcpyHostToDevice, st), "tile map");
+      ck(launch_batch_plan(xs.dptr, ys.dptr, d_toff, d_soff, d_sbase, d_tbase, d_ttid, B, ntl,
+                           d_tib, p->d_tile_ib, p->d_seg_jb, p->d_seg_info, p->d_seg_z,
+                           p->d_seg_mask, p->d_flag, st),
+         "batch plan");
+      int hf[8] = {0};
+      ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(hf), cudaMemcpyDeviceToHost, st), "flags");
+      // per-transform mode tables
+      std::vector<ModeTable> tabs(B);
+      ModeParams P0{};
+      for (int b = 0; b < B; ++b) {
+        ModeParams Pb;
+        build_modes(p->soe, deltas[b], Pb, tabs[b]);
+        if (b == 0) P0 = Pb;
+      }
+      p->P = P0;
+      p->d_mtb = dmalloc<ModeTable>(B, st);
+      ck(cudaMemcpyAsync(p->d_mtb, tabs.data(), sizeof(ModeTable) * B, cudaMemcpyHostToDevice, st),
+         "mode tables");
+      p->d_mt = dmalloc<ModeTable>(1, st);
+      ck(cudaMemcpyAsync(p->d_mt, tabs.data(), sizeof(ModeTable), cudaMemcpyHostToDevice, st),
+         "mode table");
+      ck(cudaStreamSynchronize(st), "batch plan sync");
+      if (hf[0]) raise(FGT_ERR_DOMAIN, "target coordinates must be finite");
+      if (hf[1]) raise(FGT_ERR_DOMAIN, "source coordinates must be finite");
+      if (hf[3] || hf[4])
+        raise(FGT_ERR_INVALID, "batched transforms require each transform's points sorted");
+      temps.clear();
+      adopt_set(xs, M, true, flags, st, &p->d_xs, &p->own_xs, &p->d_tperm);
+      adopt_set(ys, N, true, flags, st, &p->d_ys, &p->own_ys, &p->d_sperm);
+      p->same_points = false;
+    } catch (...) {
+      for (void* t : temps) cudaFreeAsync(t, st);
+      destroy_plan(p);
+      throw;
+    }
+    *out = p;
+  });
 }

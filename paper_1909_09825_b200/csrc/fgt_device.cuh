@@ -65,8 +65,8 @@ __device__ __forceinline__ cplx decay_exact(double sre, double sim, double g) {
 
 // Warp-uniform Taylor degree for a max scaled gap r = smax * gmax;
 // -1 selects the exact path.
-__device__ __forceinline__ int pick_degree(const ModeParams& P, double gmax) {
-  double r = P.smax * gmax;
+__device__ __forceinline__ int pick_degree(const ModeParams& P, double smax, double gmax) {
+  double r = smax * gmax;
   if (!(r == r)) return -1;
 #pragma unroll
   for (int D = 0; D <= kMaxDeg; ++D)

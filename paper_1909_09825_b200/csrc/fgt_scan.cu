@@ -130,10 +130,25 @@ struct SegGeom {
   int nx, ny, len;
   double zprev;  // coordinate of the merged element preceding the segment
   double zlast;  // coordinate of the segment's last merged element
+  int tid;       // transform of the segment (batched plans)
 };
 
 __device__ __forceinline__ SegGeom seg_geom(const StreamArgs& a, int64_t s) {
   SegGeom g;
+  g.tid = 0;
+  if (a.seg_info) {
+    const int4 info = a.seg_info[s];
+    const double2 z = a.seg_z[s];
+    g.ib = a.seg_ib[s];
+    g.jb = a.seg_jb[s];
+    g.len = info.x;
+    g.nx = info.y;
+    g.ny = info.x - info.y;
+    g.tid = info.z;
+    g.zprev = z.x;
+    g.zlast = z.y;
+    return g;
+  }
   const int64_t L = a.M + a.N;
   const int64_t d0 = s * kSeg;
   const int64_t d1 = (d0 + kSeg < L) ? d0 + kSeg : L;
@@ -584,8 +599,9 @@ __device__ __forceinline__ LaneAgg warp_reduce_agg(LaneAgg v) {
   return v;
 }
 
-__device__ __forceinline__ int seg_moment_degree(const ModeParams& P, const SegFrame& f) {
-  const int DM = pick_degree(P, fmax(f.h0, f.h1));
+__device__ __forceinline__ int seg_moment_degree(const ModeParams& P, double smax,
+                                                 const SegFrame& f) {
+  const int DM = pick_degree(P, smax, fmax(f.h0, f.h1));
   return DM <= kRegDeg ? DM : -1;
 }
 
@@ -604,11 +620,12 @@ __global__ void __launch_bounds__(kThreads)
        s += (int64_t)gridDim.x * kSegWarps) {
     const SegGeom g = seg_geom(a, s);
     const SegFrame f = seg_frame(g);
-    const int DM = seg_moment_degree(P, f);
+    const ModeTable& mx = a.mtb ? a.mtb[g.tid] : mt;
+    const int DM = seg_moment_degree(P, mx.smax, f);
     switch (DM) {
 #define FGT_K1(n)                                                  \
   case n:                                                          \
-    seg_aggregate_moments<n>(a, g, f, mt, ne, lane, s, ts);        \
+    seg_aggregate_moments<n>(a, g, f, mx, ne, lane, s, ts);        \
     continue;
       FGT_K1(0) FGT_K1(1) FGT_K1(2) FGT_K1(3) FGT_K1(4) FGT_K1(5) FGT_K1(6) FGT_K1(7)
       FGT_K1(8)
@@ -623,7 +640,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
     r.g[0] -= zp;
     for (int k = 0; k < ne; ++k) {
-      const cplx sk = mt.s[k];
+      const cplx sk = mx.s[k];
       cplx F = {0.0, 0.0}, Pp = {1.0, 0.0}, G = {0.0, 0.0};
 #pragma unroll
       for (int i = 0; i < kR; ++i) {
@@ -689,8 +706,9 @@ __global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
     double gmax = r.g[0] - zp;
 #pragma unroll
     for (int e = 1; e < kR; ++e) gmax = fmax(gmax, r.g[e] - r.g[e - 1]);
-    const int D = pick_degree(P, warp_max(gmax));
-    const int DM = seg_moment_degree(P, f);
+    const ModeTable& mx = a.mtb ? a.mtb[g.tid] : mt;
+    const int D = pick_degree(P, mx.smax, warp_max(gmax));
+    const int DM = seg_moment_degree(P, mx.smax, f);
 #if FGT_PHASE_TIMING
     const long long t1 = clock64();
 #endif
@@ -704,10 +722,10 @@ __global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
     cplx term = {0.0, 0.0};                                                         \
     if (lane < 2 * ne) {                                                            \
       const int k = lane < ne ? lane : lane - ne;                                   \
-      c.load(mt, k);                                                                \
+      c.load(mx, k);                                                                \
       term = cmul(horner<n>(c, lane < ne ? f.h0 : f.h1), seg_c);                    \
     }                                                                               \
-    carries_moments<n>(mt, ne, r, f, zp, zl, lane, term, mine);                     \
+    carries_moments<n>(mx, ne, r, f, zp, zl, lane, term, mine);                     \
     done = true;                                                                    \
   } break;
         FGT_CM(0) FGT_CM(1) FGT_CM(2) FGT_CM(3) FGT_CM(4) FGT_CM(5)
@@ -719,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
 #pragma unroll
     for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
     r.g[0] -= zp;
-    if (!done) carries_scan(mt, ne, r, lane, seg_c, seg_c, 0, mine);
+    if (!done) carries_scan(mx, ne, r, lane, seg_c, seg_c, 0, mine);
     __syncwarp();
 #if FGT_PHASE_TIMING
     const long long t2 = clock64();
@@ -730,9 +748,9 @@ __global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
     for (int e = 0; e < kR; ++e) out[e] = 0.0;
     if constexpr (MS) {
       ModeSumsOut ms{o.hp, o.hm, a.M, o.u_offset + g.ib + r.tfirst};
-      dispatch_pass2<true>(D, mt, ne, r, mine, out, ms);
+      dispatch_pass2<true>(D, mx, ne, r, mine, out, ms);
     } else {
-      dispatch_pass2<false>(D, mt, ne, r, mine, out, ModeSumsOut{nullptr, nullptr, 0, 0});
+      dispatch_pass2<false>(D, mx, ne, r, mine, out, ModeSumsOut{nullptr, nullptr, 0, 0});
 #if FGT_PHASE_TIMING
       const long long t3 = clock64();
 #endif
@@ -784,22 +802,35 @@ __global__ void partition_kernel(const double* __restrict__ xs, int64_t M,
 //     (seg_ib), places every target of a segment by ranking it among the
 //     segment's sources (sources at equal coordinates first) -> one bit per
 //     merged element (seg_mask), and records (zprev, zlast) per segment.
-__global__ void __launch_bounds__(256)
-    plan_tile_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
-                     int64_t N, const int64_t* __restrict__ tile_ib, int64_t nseg,
-                     int check_sorted, int64_t* __restrict__ seg_ib, double2* __restrict__ seg_z,
-                     uint32_t* __restrict__ seg_mask, int* __restrict__ flags) {
+// Tile context: the (transform-local) arrays a plan tile works on and where
+// its segment metadata goes.
+struct TileCtx {
+  const double* x;  // targets of the stream the tile belongs to
+  int64_t M;
+  const double* y;  // sources
+  int64_t N;
+  int64_t ib, ie;    // local target range of the tile
+  int64_t d0, d1;    // local merged range
+  int64_t seg0;      // global index of the tile's first segment
+  int64_t xoff, yoff;  // global offsets of the local arrays (batched plans)
+  int tid;
+};
+
+template <bool BATCH>
+__device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorted,
+                                               int64_t nseg, int64_t* __restrict__ seg_ib,
+                                               int64_t* __restrict__ seg_jb,
+                                               int4* __restrict__ seg_info,
+                                               double2* __restrict__ seg_z,
+                                               uint32_t* __restrict__ seg_mask,
+                                               int* __restrict__ flags) {
   extern __shared__ double tsm[];
   double* sx = tsm;              // [kPlanTile]
   double* sy = tsm + kPlanTile;  // [kPlanTile]
   __shared__ int sib[kPlanSegs + 1];
-  const int64_t t = blockIdx.x;
-  const int64_t L = M + N;
-  const int64_t d0 = t * kPlanTile;
-  const int64_t d1 = (d0 + kPlanTile < L) ? d0 + kPlanTile : L;
-  const int64_t ib = tile_ib[t], ie = tile_ib[t + 1];
-  const int64_t jb = d0 - ib, je = d1 - ie;
-  const int64_t nx64 = ie - ib, len64 = d1 - d0;
+  const int64_t ib = c.ib, ie = c.ie;
+  const int64_t jb = c.d0 - ib, je = c.d1 - ie;
+  const int64_t nx64 = ie - ib, len64 = c.d1 - c.d0;
   if (nx64 < 0 || nx64 > len64) {
     // partition of an unsorted stream (speculative pass): metadata is
     // recomputed after sorting; report "unsorted" and bail out safely
@@ -809,13 +840,13 @@ __global__ void __launch_bounds__(256)
   const int nx = (int)nx64, ny = (int)(je - jb), len = (int)len64;
   int f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0;
   // asynchronous staging: every element in flight at once, no registers
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) cp_async8(sx + i, xs + ib + i);
-  for (int j = threadIdx.x; j < ny; j += blockDim.x) cp_async8(sy + j, ys + jb + j);
+  for (int i = threadIdx.x; i < nx; i += blockDim.x) cp_async8(sx + i, c.x + ib + i);
+  for (int j = threadIdx.x; j < ny; j += blockDim.x) cp_async8(sy + j, c.y + jb + j);
   cp_async_commit();
   // same-points needs x[i] == y[i] for every i; skip once any tile has seen
   // a mismatch (distinct point sets), otherwise compare against the staged
   // sources where the index ranges overlap (they do when x == y)
-  const bool check_same = (M == N) && *(volatile int*)(flags + 2) == 0;
+  const bool check_same = !BATCH && (c.M == c.N) && *(volatile int*)(flags + 2) == 0;
   cp_async_wait_all();
   __syncthreads();
   for (int i = threadIdx.x; i < nx; i += blockDim.x) {
@@ -832,16 +863,14 @@ __global__ void __launch_bounds__(256)
     for (int i = threadIdx.x; i < nx; i += blockDim.x) {
       const int64_t gi = ib + i;
       const int64_t jl = gi - jb;
-      const double yv = (jl >= 0 && jl < ny) ? sy[jl] : __ldg(ys + gi);
+      const double yv = (jl >= 0 && jl < ny) ? sy[jl] : __ldg(c.y + gi);
       f2 |= !(sx[i] == yv);
     }
   }
   __syncthreads();
-  if (check_sorted) {
-    if (threadIdx.x == 0) {
-      if (ib > 0 && nx > 0) f3 |= __ldg(xs + ib - 1) > sx[0];
-      if (jb > 0 && ny > 0) f4 |= __ldg(ys + jb - 1) > sy[0];
-    }
+  if (check_sorted && threadIdx.x == 0) {
+    if (ib > 0 && nx > 0) f3 |= __ldg(c.x + ib - 1) > sx[0];
+    if (jb > 0 && ny > 0) f4 |= __ldg(c.y + jb - 1) > sy[0];
   }
   // segment splits inside the tile
   const int nsegs_tile = (len + kSeg - 1) / kSeg;
@@ -883,14 +912,19 @@ __global__ void __launch_bounds__(256)
     unsigned wd = byte << ((lane & 3) * 8);
     wd |= __shfl_down_sync(0xffffffffu, wd, 1);
     wd |= __shfl_down_sync(0xffffffffu, wd, 2);
-    const int64_t sg = t * kPlanSegs + k;
+    const int64_t sg = c.seg0 + k;
     if ((lane & 3) == 0) seg_mask[sg * (kSeg / 32) + (lane >> 2)] = wd;
     if (lane == 0) {
-      seg_ib[sg] = ib + i0;
+      seg_ib[sg] = c.xoff + ib + i0;
+      if constexpr (BATCH) {
+        seg_jb[sg] = c.yoff + jb + j0;
+        seg_info[sg] = make_int4(sd1 - sd0, i1 - i0, c.tid, 0);
+      }
       double px, py;
       if (k == 0) {
-        px = ib > 0 ? __ldg(xs + ib - 1) : -INFINITY;
-        py = jb > 0 ? __ldg(ys + jb - 1) : -INFINITY;
+        // -inf at the start of a stream (a new transform never couples back)
+        px = ib > 0 ? __ldg(c.x + ib - 1) : -INFINITY;
+        py = jb > 0 ? __ldg(c.y + jb - 1) : -INFINITY;
       } else {
         px = i0 > 0 ? sx[i0 - 1] : -INFINITY;
         py = j0 > 0 ? sy[j0 - 1] : -INFINITY;
@@ -898,7 +932,7 @@ __global__ void __launch_bounds__(256)
       const double lx = i1 > i0 ? sx[i1 - 1] : -INFINITY;
       const double ly = j1 > j0 ? sy[j1 - 1] : -INFINITY;
       seg_z[sg] = make_double2(fmax(px, py), fmax(lx, ly));
-      if (sg + 1 == nseg) seg_ib[nseg] = M;
+      if (!BATCH && sg + 1 == nseg) seg_ib[nseg] = c.M;
     }
   }
   f0 = __syncthreads_or(f0);
@@ -913,6 +947,76 @@ __global__ void __launch_bounds__(256)
     if (f3) atomicOr(flags + 3, 1);
     if (f4) atomicOr(flags + 4, 1);
   }
+}
+
+__global__ void __launch_bounds__(256)
+    plan_tile_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
+                     int64_t N, const int64_t* __restrict__ tile_ib, int64_t nseg,
+                     int check_sorted, int64_t* __restrict__ seg_ib, double2* __restrict__ seg_z,
+                     uint32_t* __restrict__ seg_mask, int* __restrict__ flags) {
+  const int64_t t = blockIdx.x;
+  const int64_t L = M + N;
+  TileCtx c;
+  c.x = xs;
+  c.M = M;
+  c.y = ys;
+  c.N = N;
+  c.ib = tile_ib[t];
+  c.ie = tile_ib[t + 1];
+  c.d0 = t * kPlanTile;
+  c.d1 = (c.d0 + kPlanTile < L) ? c.d0 + kPlanTile : L;
+  c.seg0 = t * kPlanSegs;
+  c.xoff = c.yoff = 0;
+  c.tid = 0;
+  plan_tile_body<false>(c, check_sorted, nseg, seg_ib, nullptr, nullptr, seg_z, seg_mask, flags);
+}
+
+struct BatchArgs {
+  const double* xs;
+  const double* ys;
+  const int64_t* t_off;
+  const int64_t* s_off;
+  const int64_t* seg_base;
+  const int64_t* tile_base;
+  const int32_t* tile_tid;
+};
+
+__device__ __forceinline__ TileCtx batch_ctx(const BatchArgs& b, int64_t gt, const int64_t* tile_ib) {
+  TileCtx c;
+  const int tid = b.tile_tid[gt];
+  const int64_t lt = gt - b.tile_base[tid];
+  c.tid = tid;
+  c.xoff = b.t_off[tid];
+  c.yoff = b.s_off[tid];
+  c.x = b.xs + c.xoff;
+  c.M = b.t_off[tid + 1] - c.xoff;
+  c.y = b.ys + c.yoff;
+  c.N = b.s_off[tid + 1] - c.yoff;
+  const int64_t L = c.M + c.N;
+  c.d0 = lt * kPlanTile;
+  c.d1 = (c.d0 + kPlanTile < L) ? c.d0 + kPlanTile : L;
+  c.seg0 = b.seg_base[tid] + lt * kPlanSegs;
+  if (tile_ib) {
+    c.ib = tile_ib[gt];
+    c.ie = gt + 1 < b.tile_base[tid + 1] ? tile_ib[gt + 1] : c.M;
+  }
+  return c;
+}
+
+__global__ void batch_partition_kernel(BatchArgs b, int64_t ntiles, int64_t* __restrict__ tile_ib) {
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gt >= ntiles) return;
+  const TileCtx c = batch_ctx(b, gt, nullptr);
+  tile_ib[gt] = merge_path(c.x, c.M, c.y, c.N, c.d0);
+}
+
+__global__ void __launch_bounds__(256)
+    batch_plan_tile_kernel(BatchArgs b, const int64_t* __restrict__ tile_ib,
+                           int64_t* __restrict__ seg_ib, int64_t* __restrict__ seg_jb,
+                           int4* __restrict__ seg_info, double2* __restrict__ seg_z,
+                           uint32_t* __restrict__ seg_mask, int* __restrict__ flags) {
+  const TileCtx c = batch_ctx(b, blockIdx.x, tile_ib);
+  plan_tile_body<true>(c, 1, 0, seg_ib, seg_jb, seg_info, seg_z, seg_mask, flags);
 }
 
 // ------------------------------------------------------------------- K2
@@ -1141,6 +1245,30 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
   note_launch();
   plan_tile_kernel<<<(unsigned)ntiles, 256, smem, st>>>(xs, M, ys, N, tile_ib, nseg, check_sorted,
                                                          seg_ib, seg_z, seg_mask, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t* t_off,
+                              const int64_t* s_off, const int64_t* seg_base,
+                              const int64_t* tile_base, const int32_t* tile_tid, int B,
+                              int64_t ntiles, int64_t* tile_ib, int64_t* seg_ib, int64_t* seg_jb,
+                              int4* seg_info, double2* seg_z, uint32_t* seg_mask, int* flags,
+                              cudaStream_t st) {
+  (void)B;
+  if (ntiles == 0) return cudaSuccess;
+  const BatchArgs b{xs, ys, t_off, s_off, seg_base, tile_base, tile_tid};
+  note_launch(2);
+  batch_partition_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(b, ntiles, tile_ib);
+  const size_t smem = sizeof(double) * 2 * kPlanTile;
+  static bool done = false;
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(batch_plan_tile_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
+  batch_plan_tile_kernel<<<(unsigned)ntiles, 256, smem, st>>>(b, tile_ib, seg_ib, seg_jb, seg_info,
+                                                              seg_z, seg_mask, flags);
   return cudaGetLastError();
 }
 

@@ -27,6 +27,8 @@ struct ModeTable {
   cplx s[kMaxModes];
   cplx mw[kMaxModes];
   cplx coef[kMaxModes][kMaxDeg + 1];
+  double smax;  // max_k |s_k| (degree selection)
+  double pad;
 };
 
 struct StreamArgs {
@@ -42,6 +44,12 @@ struct StreamArgs {
   // the merged order as one bit per element (1 = target), 8 words/segment
   const double2* seg_z;
   const uint32_t* seg_mask;
+  // batched transforms (nullptr for a single stream): per segment
+  // (len, nx, transform, 0) with seg_ib = global first target and
+  // seg_jb = global first source; per-transform mode tables
+  const int4* seg_info = nullptr;
+  const int64_t* seg_jb = nullptr;
+  const ModeTable* mtb = nullptr;
 };
 
 struct OutArgs {
@@ -79,6 +87,18 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
                               const int64_t* tile_ib, int64_t ntiles, int64_t nseg,
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
                               uint32_t* seg_mask, int* flags, cudaStream_t st);
+// Batched plans: per-transform offsets (B+1 each, concatenated arrays) and
+// the first global segment of each transform (B+1).  Partition at
+// kPlanTile granularity inside each transform, then the tile pass writes the
+// per-segment metadata (seg_ib, seg_jb, seg_info, seg_z, seg_mask; zprev of
+// each transform's first segment = -inf, so transforms never couple) and the
+// flags (0/1: non-finite, 3/4: a transform's targets / sources unsorted).
+cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t* t_off,
+                              const int64_t* s_off, const int64_t* seg_base,
+                              const int64_t* tile_base, const int32_t* tile_tid, int B,
+                              int64_t ntiles, int64_t* tile_ib, int64_t* seg_ib, int64_t* seg_jb,
+                              int4* seg_info, double2* seg_z, uint32_t* seg_mask, int* flags,
+                              cudaStream_t st);
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, cudaStream_t st);
 // K2: exclusive carries per segment.  carry_in: 2*ne complex (forward carry at

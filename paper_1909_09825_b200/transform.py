@@ -204,6 +204,50 @@ def mode_sums(p, strengths):
     return ((hp[0::2] + 1j * hp[1::2]).reshape(ne, M), (hm[0::2] + 1j * hm[1::2]).reshape(ne, M))
 
 
+class BatchPlan:
+    """B independent presorted transforms planned together (BASELINE cfg 5)."""
+
+    def __init__(self, targets, sources, deltas, soe):
+        self.t_off = np.concatenate([[0], np.cumsum([len(t) for t in targets])]).astype(np.int64)
+        self.s_off = np.concatenate([[0], np.cumsum([len(s) for s in sources])]).astype(np.int64)
+        x = _f64(np.concatenate([np.asarray(t, dtype=np.float64) for t in targets]) if targets else [])
+        y = _f64(np.concatenate([np.asarray(v, dtype=np.float64) for v in sources]) if sources else [])
+        d = _f64(deltas)
+        if d.size != len(targets) or len(sources) != len(targets):
+            raise ValueError("one delta, target set and source set per transform")
+        folded = soe if soe.form == SoeForm.FOLDED else fold(soe)
+        self.soe = folded
+        self._keep, sargs = _soe_args(folded)
+        h = ctypes.c_void_p()
+        _capi.check(_capi.lib().fgt_batch_create(len(targets), _ptr(x), self.t_off.ctypes.data_as(_PI64),
+                                                 _ptr(y), self.s_off.ctypes.data_as(_PI64), _ptr(d),
+                                                 *sargs, 0, -1, None, ctypes.byref(h)))
+        self._h = h.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _capi.lib().fgt_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def apply(self, strengths):
+        a = _f64(np.concatenate([np.asarray(v, dtype=np.float64) for v in strengths]) if strengths else [])
+        if a.size != self.s_off[-1]:
+            raise ValueError("strengths must match the batch's sources")
+        out = np.empty(int(self.t_off[-1]))
+        _capi.check(_capi.lib().fgt_apply_general(self._h, _ptr(a), a.size, _ptr(out), 1, 0, None))
+        return [out[self.t_off[b]:self.t_off[b + 1]] for b in range(len(self.t_off) - 1)]
+
+
+def batch_transform(targets, sources, strengths, deltas, soe):
+    """Independent transforms u_b = G_{delta_b}(x_b, y_b) alpha_b in one batched plan
+    (each x_b, y_b sorted)."""
+    return BatchPlan(targets, sources, deltas, soe).apply(strengths)
+
+
 def gauss_transform(targets, sources, strengths, delta, soe=None, ne=4, threads=1):
     """pymodule.cpp:37-60: plan(precompute) then apply_same / apply_general."""
     req = TransformRequest(targets, sources, strengths, delta)

@@ -384,3 +384,44 @@ def test_gpu_kernels_actually_launch():
     before = L.fgt_launch_counter()
     fgt.gauss_transform(up(1000, 1, 3), up(1000, 1, 0), up(1000, 1, 1), 0.1, ne=4)
     assert L.fgt_launch_counter() - before >= 3
+
+
+# ------------------------------------------------------- batched transforms
+
+def test_batched_transforms_vs_oracle():
+    """BASELINE cfg 5 shape (scaled down): independent presorted transforms
+    with per-transform delta (log-uniform in [1e-6, 1e-1]) in one plan;
+    ragged sizes including empty sets."""
+    rng = np.random.default_rng(5)
+    B = 48
+    sizes = [(int(m), int(n)) for m, n in rng.integers(0, 3000, size=(B, 2))]
+    sizes[3] = (0, 500)
+    sizes[7] = (400, 0)
+    sizes[11] = (1, 1)
+    sizes[19] = (5000, 4100)
+    xs = [np.sort(up(m, 100 + b, 3)) for b, (m, n) in enumerate(sizes)]
+    ys = [np.sort(up(n, 100 + b, 0)) for b, (m, n) in enumerate(sizes)]
+    al = [2.0 * up(n, 100 + b, 1) - 1.0 for b, (m, n) in enumerate(sizes)]
+    deltas = 10.0 ** (-6.0 + 5.0 * up(B, 0, 9))
+    for ne in (3, 4, 6):
+        soe = fgt.fold(fgt.cf_soe(2 * ne))
+        out = fgt.batch_transform(xs, ys, al, deltas, soe)
+        for b in range(B):
+            ref = oracle.transform(xs[b], ys[b], al[b], deltas[b], ne=ne, mode=0)
+            assert out[b].size == ref.size
+            if ref.size:
+                check(out[b], ref, al[b] if al[b].size else [1.0])
+
+
+def test_batched_rejects_unsorted_and_reuses_plan():
+    soe = fgt.fold(fgt.cf_soe(8))
+    with pytest.raises(ValueError):
+        fgt.batch_transform([np.array([0.5, 0.1])], [np.array([0.2])], [np.array([1.0])], [0.1], soe)
+    xs = [np.sort(up(1000, 7, 3)), np.sort(up(700, 8, 3))]
+    ys = [np.sort(up(900, 7, 0)), np.sort(up(1200, 8, 0))]
+    bp = fgt.BatchPlan(xs, ys, [1e-3, 1e-5], soe)
+    for seed in (1, 2):
+        al = [up(900, seed, 1), up(1200, seed, 6)]
+        out = bp.apply(al)
+        for b, d in enumerate([1e-3, 1e-5]):
+            check(out[b], oracle.transform(xs[b], ys[b], al[b], d, ne=4, mode=0), al[b])
