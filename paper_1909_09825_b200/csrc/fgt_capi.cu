@@ -207,6 +207,8 @@ struct fgt_plan_s {
   int64_t* d_seg_jb = nullptr;
   int4* d_seg_info = nullptr;
   ModeTable* d_mtb = nullptr;
+  // segment classes (launch_classify): K1 / K3 wide-path segment counts
+  int64_t nwide1 = -1, nwide3 = -1;
   double zprev0 = 0.0;
   int* d_flag = nullptr;
   ChunkState cs;
@@ -296,6 +298,42 @@ void adopt_set(const SetSrc& in, int64_t n, bool is_sorted, uint32_t flags, cuda
   if (in.tmp) dfree(const_cast<double*>(in.dptr), st);
   *d_sorted = d_out;
   *d_perm = d_p;
+}
+
+// d_flag: check flags 0..4, then two 64-bit segment-class counters.
+constexpr int kFlagInts = 12;
+unsigned long long* class_counts(fgt_plan_s* p) {
+  return reinterpret_cast<unsigned long long*>(p->d_flag + 8);
+}
+
+StreamArgs stream_args(const fgt_plan_s* p, const double* bs) {
+  StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0,
+                p->d_seg_z, p->d_seg_mask, p->d_seg_info, p->d_seg_jb, p->d_mtb};
+  sa.nwide1 = p->nwide1;
+  sa.nwide3 = p->nwide3;
+  return sa;
+}
+
+// Queue the segment classification; the counts land in h[0..1] once the
+// stream is synchronized (see take_classes).
+void queue_classify(fgt_plan_s* p, unsigned long long* h, cudaStream_t st,
+                    bool check_flags = false) {
+  const StreamArgs sa = stream_args(p, nullptr);
+  ck(launch_classify(sa, p->P, p->P.smax, check_flags ? p->d_flag : nullptr, class_counts(p), st),
+     "classify");
+  ck(cudaMemcpyAsync(h, class_counts(p), 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                     st),
+     "class counts");
+}
+void take_classes(fgt_plan_s* p, const unsigned long long* h) {
+  p->nwide1 = (int64_t)h[0];
+  p->nwide3 = (int64_t)h[1];
+}
+void classify_sync(fgt_plan_s* p, cudaStream_t st) {
+  unsigned long long h[2] = {0, 0};
+  queue_classify(p, h, st);
+  ck(cudaStreamSynchronize(st), "classify sync");
+  take_classes(p, h);
 }
 
 // Partition + speculative tile pass (checks and segment metadata) on the
@@ -411,8 +449,7 @@ void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint3
     ck(cudaMemsetAsync(u, 0, sizeof(double) * p->M, st), "zero potentials");
   } else {
     const double* bs = sorted_strengths(p, strengths, flags, w, nullptr);
-    const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0,
-                        p->d_seg_z, p->d_seg_mask, p->d_seg_info, p->d_seg_jb, p->d_mtb};
+    const StreamArgs sa = stream_args(p, bs);
     const TileState ts = tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, p->P.ne)),
                                           p->ntiles, p->P.ne);
     {
@@ -458,8 +495,7 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ho
     ck(cudaStreamSynchronize(st), "sync");
     return;
   }
-  const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0,
-                        p->d_seg_z, p->d_seg_mask, p->d_seg_info, p->d_seg_jb, p->d_mtb};
+  const StreamArgs sa = stream_args(p, p->cs.bs);
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
   ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
   cplx* d_tot = w.get<cplx>(3 * ne);
@@ -480,8 +516,7 @@ void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in_host, double* potentia
   if (p->N == 0 && p->ntiles > 0 && !p->cs.tile)
     raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
   if (!p->cs.tile) raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
-  const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, p->cs.bs, p->d_tile_ib, p->ntiles, p->zprev0,
-                        p->d_seg_z, p->d_seg_mask, p->d_seg_info, p->d_seg_jb, p->d_mtb};
+  const StreamArgs sa = stream_args(p, p->cs.bs);
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
   cplx* d_cin = w.get<cplx>(2 * ne);
   ck(cudaMemcpyAsync(d_cin, carry_in_host, sizeof(cplx) * 2 * ne, cudaMemcpyHostToDevice, st),
@@ -584,8 +619,8 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       if (M >= ((int64_t)1 << 31) || N >= ((int64_t)1 << 31))
         raise(FGT_ERR_INVALID, "at most 2^31-1 points per set");
       p->stream = st;
-      p->d_flag = dmalloc<int>(8, st);
-      ck(cudaMemsetAsync(p->d_flag, 0, sizeof(int) * 8, st), "flag");
+      p->d_flag = dmalloc<int>(kFlagInts, st);
+      ck(cudaMemsetAsync(p->d_flag, 0, sizeof(int) * kFlagInts, st), "flag");
       SetSrc xs = stage_set(targets, M, flags, st);
       if (xs.tmp) temps.push_back((void*)xs.dptr);
       SetSrc ys = stage_set(sources, N, flags, st);
@@ -621,6 +656,7 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       upload_modes(p, st);  // synchronizes
       // coordinate before the first merged element: the element itself
       p->zprev0 = (M > 0 && N > 0) ? std::fmin(x0, y0) : (M > 0 ? x0 : y0);
+      classify_sync(p, st);
     } catch (...) {
       for (void* t : temps) cudaFreeAsync(t, st);
       destroy_plan(p);
@@ -639,8 +675,17 @@ int fgt_plan_create_chunk(const double* sorted_targets, int64_t M, const double*
                            self_conj, n_modes, form, flags | FGT_ASSUME_SORTED, device, stream,
                            out);
   if (rc != FGT_OK) return rc;
-  if (has_prev) (*out)->zprev0 = z_prev;
   (*out)->same_points = false;
+  if (has_prev) {
+    (*out)->zprev0 = z_prev;
+    // segment 0's frame starts at z_prev: reclassify
+    int rc2 = guarded([&] { classify_sync(*out, (*out)->stream); });
+    if (rc2 != FGT_OK) {
+      destroy_plan(*out);
+      *out = nullptr;
+      return rc2;
+    }
+  }
   return FGT_OK;
 }
 
@@ -829,8 +874,7 @@ extern "C" int fgt_mode_sums(fgt_plan_t p, const double* strengths, double* hp, 
       ck(cudaMemsetAsync(d_hm, 0, sizeof(cplx) * cnt, st), "zero");
     } else {
       const double* bs = sorted_strengths(p, strengths, 0, w, nullptr);
-      const StreamArgs sa{p->d_xs, p->M, p->d_ys, p->N, bs, p->d_tile_ib, p->ntiles, p->zprev0,
-                        p->d_seg_z, p->d_seg_mask, p->d_seg_info, p->d_seg_jb, p->d_mtb};
+      const StreamArgs sa = stream_args(p, bs);
       const TileState ts = tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, ne)),
                                             p->ntiles, ne);
       ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "aggregates");
@@ -919,8 +963,8 @@ extern "C" int fgt_batch_create(int B, const double* targets, const int64_t* t_o
       p->batch = true;
       p->nbatch = B;
       p->stream = st;
-      p->d_flag = dmalloc<int>(8, st);
-      ck(cudaMemsetAsync(p->d_flag, 0, sizeof(int) * 8, st), "flag");
+      p->d_flag = dmalloc<int>(kFlagInts, st);
+      ck(cudaMemsetAsync(p->d_flag, 0, sizeof(int) * kFlagInts, st), "flag");
       SetSrc xs = stage_set(targets, M, flags, st);
       SetSrc ys = stage_set(sources, N, flags, st);
       if (xs.tmp) temps.push_back((void*)xs.dptr);
@@ -961,22 +1005,27 @@ extern "C" int fgt_batch_create(int B, const double* targets, const int64_t* t_o
          "batch plan");
       int hf[8] = {0};
       ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(hf), cudaMemcpyDeviceToHost, st), "flags");
-      // per-transform mode tables
-      std::vector<ModeTable> tabs(B);
-      ModeParams P0{};
-      for (int b = 0; b < B; ++b) {
-        ModeParams Pb;
-        build_modes(p->soe, deltas[b], Pb, tabs[b]);
-        if (b == 0) P0 = Pb;
+      // per-transform mode tables (device-built), the shared one of transform 0
+      ModeTable T0;
+      build_modes(p->soe, deltas[0], p->P, T0);
+      BatchModeBase base{};
+      base.ne = p->P.ne;
+      for (int k = 0; k < base.ne; ++k) {
+        base.t[k] = {p->soe.nodes[k].real(), p->soe.nodes[k].imag()};
+        base.mw[k] = {p->P.mw_re[k], p->P.mw_im[k]};
       }
-      p->P = P0;
+      double* d_deltas = w.get<double>(B);
+      ck(cudaMemcpyAsync(d_deltas, deltas, sizeof(double) * B, cudaMemcpyHostToDevice, st),
+         "deltas");
       p->d_mtb = dmalloc<ModeTable>(B, st);
-      ck(cudaMemcpyAsync(p->d_mtb, tabs.data(), sizeof(ModeTable) * B, cudaMemcpyHostToDevice, st),
-         "mode tables");
+      ck(launch_batch_modes(base, d_deltas, B, p->d_mtb, st), "mode tables");
       p->d_mt = dmalloc<ModeTable>(1, st);
-      ck(cudaMemcpyAsync(p->d_mt, tabs.data(), sizeof(ModeTable), cudaMemcpyHostToDevice, st),
+      ck(cudaMemcpyAsync(p->d_mt, &T0, sizeof(ModeTable), cudaMemcpyHostToDevice, st),
          "mode table");
+      unsigned long long hc[2] = {0, 0};
+      queue_classify(p, hc, st, true);
       ck(cudaStreamSynchronize(st), "batch plan sync");
+      take_classes(p, hc);
       if (hf[0]) raise(FGT_ERR_DOMAIN, "target coordinates must be finite");
       if (hf[1]) raise(FGT_ERR_DOMAIN, "source coordinates must be finite");
       if (hf[3] || hf[4])

@@ -20,6 +20,7 @@
 // (at the element preceding it) it is A Cb + G.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stddef.h>
 
 #include "fgt_scan.cuh"
 #include "fgt_sort.cuh"
@@ -99,6 +100,33 @@ __device__ __forceinline__ cplx gap_factor(const Coef<D>& c, cplx s, double g) {
   }
 }
 
+// Gap factors of a lane run, exp(-s_k g_i) for i < kR: Horner with the
+// element loop inside (each coefficient read once per run, kR independent
+// chains); exact for D < 0.  Same operation order as horner<D>.
+template <int D>
+__device__ __forceinline__ void gap_factors(const ModeTable& mt, int k, const double (&g)[kR],
+                                            cplx (&d)[kR]) {
+  if constexpr (D < 0) {
+    const cplx s = mt.s[k];
+#pragma unroll
+    for (int i = 0; i < kR; ++i) d[i] = decay_exact(s.re, s.im, g[i]);
+  } else {
+    const cplx* cf = mt.coef[k];
+    const cplx top = cf[D];
+#pragma unroll
+    for (int i = 0; i < kR; ++i) d[i] = top;
+#pragma unroll
+    for (int n = D - 1; n >= 0; --n) {
+      const cplx c = cf[n];
+#pragma unroll
+      for (int i = 0; i < kR; ++i) {
+        d[i].re = fma(d[i].re, g[i], c.re);
+        d[i].im = fma(d[i].im, g[i], c.im);
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
@@ -122,6 +150,25 @@ __device__ __forceinline__ void load_mode_table(const ModeTable* g, ModeTable& s
   constexpr int n = sizeof(ModeTable) / sizeof(double);
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
 }
+
+// One warp copies a transform's mode table (the rows of its ne modes) into
+// its shared-memory slot (batched plans).
+__device__ __forceinline__ void warp_load_table(const ModeTable* g, ModeTable& s, int ne,
+                                                int lane) {
+  __syncwarp();
+  const double* src = reinterpret_cast<const double*>(g);
+  double* dst = reinterpret_cast<double*>(&s);
+  constexpr int kHead = 4 * kMaxModes;  // s[], mw[]
+  constexpr int kRow = 2 * (kMaxDeg + 1);
+  const int n = kHead + kRow * ne;
+  for (int i = lane; i < n; i += 32) dst[i] = __ldg(src + i);
+  if (lane == 0) s.smax = __ldg(&g->smax);
+  __syncwarp();
+}
+static_assert(offsetof(ModeTable, coef) == sizeof(double) * 4 * kMaxModes, "table layout");
+
+// Consecutive segments a warp walks in batched plans before striding.
+constexpr int kBatchGroup = 16;
 
 // ---------------------------------------------------------------- geometry
 
@@ -256,103 +303,72 @@ struct Carry {
   cplx cf, cb;
 };
 
-// Forward and backward recurrences seeded with the lane carries,
+// Forward and backward recurrences of one mode over the lane run from its
+// gap factors d[], seeded with the lane carries (H = cf, K = cb),
 // accumulating Re(mw_k (H + K)) into out[] (only target slots are used).
 // With Kt_i = K_i + b_i the backward step is Kt_{i-1} = d_i Kt_i + b_{i-1},
 // the same multiply-add as the forward step; the two chains are independent
 // and interleaved for instruction-level parallelism.
-// Variant: two modes at a time, gap factors recomputed per direction (no
-// d[] storage) -> four independent chains per iteration.
-template <int D>
-__device__ __forceinline__ void pass2_pair_body(const ModeTable& mt, int k, bool two,
-                                                const LaneRun& r, const Carry* carry,
-                                                double (&out)[kR]) {
-  Coef<D> c0, c1;
-  c0.load(mt, k);
-  c1.load(mt, two ? k + 1 : k);
-  const cplx s0 = mt.s[k], s1 = mt.s[two ? k + 1 : k];
-  const cplx mw0 = mt.mw[k];
-  const cplx mw1 = two ? mt.mw[k + 1] : cplx{0.0, 0.0};
-  cplx H0 = carry[k].cf, K0 = carry[k].cb;
-  cplx H1 = two ? carry[k + 1].cf : cplx{0.0, 0.0};
-  cplx K1 = two ? carry[k + 1].cb : cplx{0.0, 0.0};
-  K0.re += r.b[kR - 1];
-  K1.re += r.b[kR - 1];
+template <bool MS>
+__device__ __forceinline__ void chains_mode(const cplx (&d)[kR], cplx mw, const LaneRun& r,
+                                            cplx H, cplx K, int k, double (&out)[kR],
+                                            const ModeSumsOut& ms) {
+  K.re += r.b[kR - 1];
+  if constexpr (MS) {
+    int64_t ti = ms.t0;
 #pragma unroll
-  for (int i = 0; i < kR; ++i) {
-    const int j = kR - 1 - i;
-    const cplx a0 = gap_factor<D>(c0, s0, r.g[i]);
-    const cplx a1 = gap_factor<D>(c1, s1, r.g[i]);
-    H0 = cmad(a0, H0, cplx{r.b[i], 0.0});
-    H1 = cmad(a1, H1, cplx{r.b[i], 0.0});
-    out[i] = fma(mw0.re, H0.re, fma(-mw0.im, H0.im, out[i]));
-    out[i] = fma(mw1.re, H1.re, fma(-mw1.im, H1.im, out[i]));
-    out[j] = fma(mw0.re, K0.re, fma(-mw0.im, K0.im, out[j]));
-    out[j] = fma(mw1.re, K1.re, fma(-mw1.im, K1.im, out[j]));
-    if (j > 0) {
-      const cplx e0 = gap_factor<D>(c0, s0, r.g[j]);
-      const cplx e1 = gap_factor<D>(c1, s1, r.g[j]);
-      K0 = cmad(e0, K0, cplx{r.b[j - 1], 0.0});
-      K1 = cmad(e1, K1, cplx{r.b[j - 1], 0.0});
+    for (int i = 0; i < kR; ++i) {
+      H = cmad(d[i], H, cplx{r.b[i], 0.0});
+      if (r.tmask & (1u << i)) ms.hp[(int64_t)k * ms.M + ti++] = H;
+    }
+#pragma unroll
+    for (int i = kR - 1; i >= 0; --i) {
+      if (r.tmask & (1u << i)) ms.hm[(int64_t)k * ms.M + (--ti)] = K;  // b_i = 0
+      if (i > 0) K = cmad(d[i], K, cplx{r.b[i - 1], 0.0});
+    }
+  } else {
+    (void)k;
+    (void)ms;
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      H = cmad(d[i], H, cplx{r.b[i], 0.0});
+      out[i] = fma(mw.re, H.re, fma(-mw.im, H.im, out[i]));
+      const int j = kR - 1 - i;
+      out[j] = fma(mw.re, K.re, fma(-mw.im, K.im, out[j]));
+      if (j > 0) K = cmad(d[j], K, cplx{r.b[j - 1], 0.0});
     }
   }
 }
 
+#ifndef FGT_P2_COEF
+#define FGT_P2_COEF 0
+#endif
 #ifndef FGT_CARRY_UNROLL
 #define FGT_CARRY_UNROLL 1
 #endif
 constexpr int kCarryUnroll = FGT_CARRY_UNROLL;
-#ifndef FGT_PASS2_PAIRS
-#define FGT_PASS2_PAIRS 0
-#endif
 #ifndef FGT_MODE_UNROLL
 #define FGT_MODE_UNROLL 1
 #endif
 constexpr int kModeUnroll = FGT_MODE_UNROLL;
+
+// Narrow segments: lane carries already in shared memory (moment form).
 template <int D, bool MS>
 __device__ __forceinline__ void pass2(const ModeTable& mt, int ne, const LaneRun& r,
                                       const Carry* carry, double (&out)[kR],
                                       const ModeSumsOut& ms) {
-#if FGT_PASS2_PAIRS
-  if constexpr (!MS) {
-    for (int k = 0; k < ne; k += 2) pass2_pair_body<D>(mt, k, k + 1 < ne, r, carry, out);
-    return;
-  }
-#endif
 #pragma unroll kModeUnroll
   for (int k = 0; k < ne; ++k) {
+    cplx d[kR];
+#if FGT_P2_COEF
     Coef<D> c;
     c.load(mt, k);
-    const cplx s = mt.s[k];
-    const cplx mw = mt.mw[k];
-    cplx d[kR];
 #pragma unroll
-    for (int i = 0; i < kR; ++i) d[i] = gap_factor<D>(c, s, r.g[i]);
-    cplx H = carry[k].cf;
-    cplx K = carry[k].cb;
-    K.re += r.b[kR - 1];
-    if constexpr (MS) {
-      int64_t ti = ms.t0;
-#pragma unroll
-      for (int i = 0; i < kR; ++i) {
-        H = cmad(d[i], H, cplx{r.b[i], 0.0});
-        if (r.tmask & (1u << i)) ms.hp[(int64_t)k * ms.M + ti++] = H;
-      }
-#pragma unroll
-      for (int i = kR - 1; i >= 0; --i) {
-        if (r.tmask & (1u << i)) ms.hm[(int64_t)k * ms.M + (--ti)] = K;  // b_i = 0
-        if (i > 0) K = cmad(d[i], K, cplx{r.b[i - 1], 0.0});
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < kR; ++i) {
-        H = cmad(d[i], H, cplx{r.b[i], 0.0});
-        out[i] = fma(mw.re, H.re, fma(-mw.im, H.im, out[i]));
-        const int j = kR - 1 - i;
-        out[j] = fma(mw.re, K.re, fma(-mw.im, K.im, out[j]));
-        if (j > 0) K = cmad(d[j], K, cplx{r.b[j - 1], 0.0});
-      }
-    }
+    for (int i = 0; i < kR; ++i) d[i] = gap_factor<D>(c, mt.s[k], r.g[i]);
+#else
+    gap_factors<D>(mt, k, r.g, d);
+#endif
+    chains_mode<MS>(d, mt.mw[k], r, carry[k].cf, carry[k].cb, k, out, ms);
   }
 }
 
@@ -444,70 +460,100 @@ __device__ __forceinline__ void carries_moments(const ModeTable& mt, int ne, con
   }
 }
 
-// Robust form (wide segments): exact per-element lane aggregates and
-// shuffle (Kogge-Stone) exclusive scans across the warp, both directions.
-__device__ __forceinline__ void carries_scan(const ModeTable& mt, int ne, const LaneRun& r,
-                                             int lane, cplx cf_seg, cplx cb_seg, int q_has,
-                                             Carry* out) {
+// Lane carries by shuffle (Kogge-Stone) scans of the lane aggregates (A, F,
+// G) across the warp, both directions, seeded with the segment carries
+// (cfs at the element before the segment, cbs at its last element).
+__device__ __forceinline__ void lane_scan(cplx A, cplx F, cplx G, int lane, cplx cfs, cplx cbs,
+                                          cplx& cf, cplx& cb) {
+  // forward inclusive scan of (A, F) over lanes (earlier then later)
+  cplx fa = A, ff = F;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    cplx pa, pf;
+    pa.re = __shfl_up_sync(0xffffffffu, fa.re, o);
+    pa.im = __shfl_up_sync(0xffffffffu, fa.im, o);
+    pf.re = __shfl_up_sync(0xffffffffu, ff.re, o);
+    pf.im = __shfl_up_sync(0xffffffffu, ff.im, o);
+    if (lane >= o) {
+      ff = cmad(fa, pf, ff);
+      fa = cmul(pa, fa);
+    }
+  }
+  // backward inclusive scan of (A, G) from the right
+  cplx ba = A, bg = G;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    cplx pa, pg;
+    pa.re = __shfl_down_sync(0xffffffffu, ba.re, o);
+    pa.im = __shfl_down_sync(0xffffffffu, ba.im, o);
+    pg.re = __shfl_down_sync(0xffffffffu, bg.re, o);
+    pg.im = __shfl_down_sync(0xffffffffu, bg.im, o);
+    if (lane + o < 32) {
+      bg = cmad(ba, pg, bg);
+      ba = cmul(ba, pa);
+    }
+  }
+  // exclusive: shift by one lane and apply the segment carries
+  cplx xa = {__shfl_up_sync(0xffffffffu, fa.re, 1), __shfl_up_sync(0xffffffffu, fa.im, 1)};
+  cplx xf = {__shfl_up_sync(0xffffffffu, ff.re, 1), __shfl_up_sync(0xffffffffu, ff.im, 1)};
+  if (lane == 0) {
+    xa = {1.0, 0.0};
+    xf = {0.0, 0.0};
+  }
+  cplx ya = {__shfl_down_sync(0xffffffffu, ba.re, 1), __shfl_down_sync(0xffffffffu, ba.im, 1)};
+  cplx yg = {__shfl_down_sync(0xffffffffu, bg.re, 1), __shfl_down_sync(0xffffffffu, bg.im, 1)};
+  if (lane == 31) {
+    ya = {1.0, 0.0};
+    yg = {0.0, 0.0};
+  }
+  cf = cmad(xa, cfs, xf);
+  cb = cmad(ya, cbs, yg);
+}
+
+// Wide segments (no moment form): per mode, the gap factors of the lane run
+// once (degree-D Taylor, exact for D < 0), the lane aggregates from them,
+// the lane carries by warp scans, then both chains -- one evaluation of
+// exp(-s g) per element and mode.
+template <int D, bool MS>
+__device__ __forceinline__ void wide_modes(const ModeTable& mt, int ne, const LaneRun& r, int lane,
+                                           cplx seg_c, double (&out)[kR],
+                                           const ModeSumsOut& ms) {
   for (int k = 0; k < ne; ++k) {
-    const cplx sk = mt.s[k];
+    cplx d[kR];
+    gap_factors<D>(mt, k, r.g, d);
     cplx F = {0.0, 0.0}, A = {1.0, 0.0}, G = {0.0, 0.0};
 #pragma unroll
     for (int i = 0; i < kR; ++i) {
-      const cplx d = decay_exact(sk.re, sk.im, r.g[i]);
-      F = cmad(d, F, cplx{r.b[i], 0.0});
-      A = cmul(A, d);
+      F = cmad(d[i], F, cplx{r.b[i], 0.0});
+      A = cmul(A, d[i]);
       G.re = fma(r.b[i], A.re, G.re);
       G.im = fma(r.b[i], A.im, G.im);
     }
-    // forward inclusive scan of (A, F) over lanes (earlier then later)
-    cplx fa = A, ff = F;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      cplx pa, pf;
-      pa.re = __shfl_up_sync(0xffffffffu, fa.re, o);
-      pa.im = __shfl_up_sync(0xffffffffu, fa.im, o);
-      pf.re = __shfl_up_sync(0xffffffffu, ff.re, o);
-      pf.im = __shfl_up_sync(0xffffffffu, ff.im, o);
-      if (lane >= o) {
-        ff = cmad(fa, pf, ff);
-        fa = cmul(pa, fa);
-      }
-    }
-    // backward inclusive scan of (A, G) from the right
-    cplx ba = A, bg = G;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      cplx pa, pg;
-      pa.re = __shfl_down_sync(0xffffffffu, ba.re, o);
-      pa.im = __shfl_down_sync(0xffffffffu, ba.im, o);
-      pg.re = __shfl_down_sync(0xffffffffu, bg.re, o);
-      pg.im = __shfl_down_sync(0xffffffffu, bg.im, o);
-      if (lane + o < 32) {
-        bg = cmad(ba, pg, bg);
-        ba = cmul(ba, pa);
-      }
-    }
-    // exclusive: shift by one lane and apply the segment carries
-    const cplx cfs = {__shfl_sync(0xffffffffu, cf_seg.re, k), __shfl_sync(0xffffffffu, cf_seg.im, k)};
-    const cplx cbs = {__shfl_sync(0xffffffffu, cb_seg.re, ne + k),
-                      __shfl_sync(0xffffffffu, cb_seg.im, ne + k)};
-    cplx xa = {__shfl_up_sync(0xffffffffu, fa.re, 1), __shfl_up_sync(0xffffffffu, fa.im, 1)};
-    cplx xf = {__shfl_up_sync(0xffffffffu, ff.re, 1), __shfl_up_sync(0xffffffffu, ff.im, 1)};
-    if (lane == 0) {
-      xa = {1.0, 0.0};
-      xf = {0.0, 0.0};
-    }
-    cplx ya = {__shfl_down_sync(0xffffffffu, ba.re, 1), __shfl_down_sync(0xffffffffu, ba.im, 1)};
-    cplx yg = {__shfl_down_sync(0xffffffffu, bg.re, 1), __shfl_down_sync(0xffffffffu, bg.im, 1)};
-    if (lane == 31) {
-      ya = {1.0, 0.0};
-      yg = {0.0, 0.0};
-    }
-    out[k].cf = cmad(xa, cfs, xf);
-    out[k].cb = cmad(ya, cbs, yg);
+    const cplx cfs = {__shfl_sync(0xffffffffu, seg_c.re, k), __shfl_sync(0xffffffffu, seg_c.im, k)};
+    const cplx cbs = {__shfl_sync(0xffffffffu, seg_c.re, ne + k),
+                      __shfl_sync(0xffffffffu, seg_c.im, ne + k)};
+    cplx cf, cb;
+    lane_scan(A, F, G, lane, cfs, cbs, cf, cb);
+    chains_mode<MS>(d, mt.mw[k], r, cf, cb, k, out, ms);
   }
-  (void)q_has;
+}
+
+template <bool MS>
+__device__ __forceinline__ void dispatch_wide(int D, const ModeTable& mt, int ne, const LaneRun& r,
+                                              int lane, cplx seg_c, double (&out)[kR],
+                                              const ModeSumsOut& ms) {
+  switch (D) {
+#define FGT_WD(n)                                      \
+  case n:                                              \
+    wide_modes<n, MS>(mt, ne, r, lane, seg_c, out, ms); \
+    break;
+    FGT_WD(0) FGT_WD(1) FGT_WD(2) FGT_WD(3) FGT_WD(4) FGT_WD(5) FGT_WD(6) FGT_WD(7)
+    FGT_WD(8) FGT_WD(9) FGT_WD(10) FGT_WD(11) FGT_WD(12) FGT_WD(13) FGT_WD(14)
+    FGT_WD(15) FGT_WD(16)
+#undef FGT_WD
+    default:
+      wide_modes<-1, MS>(mt, ne, r, lane, seg_c, out, ms);
+  }
 }
 
 // -------------------------------------------------------- shared memory
@@ -605,59 +651,174 @@ __device__ __forceinline__ int seg_moment_degree(const ModeParams& P, double sma
   return DM <= kRegDeg ? DM : -1;
 }
 
-// K1: warps loop over segments (grid-stride).  Moment path for narrow
-// segments; exact per-element lane aggregates reduced across the warp
-// otherwise.
+// Highest moment degree K3 keeps in registers.  A segment narrow enough for
+// it has every gap below 2 rmax[kK3Moments] < rmax[kMaxDeg], so its gap
+// factors take the Taylor path.
+constexpr int kK3Moments = 5;
+
+// Segment classes (both kernels and the plan-time count use these).
+__device__ __forceinline__ bool k1_narrow(int DM) { return DM >= 0 && DM <= kRegDeg; }
+__device__ __forceinline__ bool k3_narrow(int DM) { return DM >= 0 && DM <= kK3Moments; }
+
+__device__ __forceinline__ double seg_smax(const StreamArgs& a, const SegGeom& g, double smax) {
+  return a.mtb ? __ldg(&a.mtb[g.tid].smax) : smax;
+}
+
+// Wide segments: lane aggregates from the gap factors (degree-D Taylor,
+// exact for D < 0), reduced across the warp in lane order.
+template <int D>
+__device__ __forceinline__ void seg_aggregate_wide(const ModeTable& mt, int ne, int lane,
+                                                   const LaneRun& r, int64_t nseg, int64_t s,
+                                                   TileState ts) {
+  for (int k = 0; k < ne; ++k) {
+    cplx d[kR];
+    gap_factors<D>(mt, k, r.g, d);
+    cplx F = {0.0, 0.0}, Pp = {1.0, 0.0}, G = {0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      F = cmad(d[i], F, cplx{r.b[i], 0.0});
+      Pp = cmul(Pp, d[i]);
+      G.re = fma(r.b[i], Pp.re, G.re);
+      G.im = fma(r.b[i], Pp.im, G.im);
+    }
+    const LaneAgg w = warp_reduce_agg(LaneAgg{Pp, F, G});
+    if (lane == 0) {
+      const int64_t o = (int64_t)k * nseg + s;
+      ts.A[o] = w.A;
+      ts.F[o] = w.F;
+      ts.G[o] = w.G;
+    }
+  }
+}
+
+// K1: warps loop over segments (grid-stride; groups of kBatchGroup for
+// batched plans).  Two variants with their own register allocation: the
+// moment path for narrow segments (WIDE = false) and per-element lane
+// aggregates reduced across the warp for the others (WIDE = true); each
+// skips the other's segments.
+template <bool WIDE>
 __global__ void __launch_bounds__(kThreads)
     seg_aggregate_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
                          TileState ts) {
-  __shared__ ModeTable mt;
-  load_mode_table(mtab, mt);
-  __syncthreads();
+  __shared__ ModeTable tabs[kSegWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool batched = a.mtb != nullptr;
+  if (!batched) load_mode_table(mtab, tabs[0]);
+  __syncthreads();
+  ModeTable& mx = batched ? tabs[warp] : tabs[0];
+  int cached_tid = -1;
   const int ne = P.ne;
-  for (int64_t s = (int64_t)blockIdx.x * kSegWarps + warp; s < a.nseg;
-       s += (int64_t)gridDim.x * kSegWarps) {
-    const SegGeom g = seg_geom(a, s);
-    const SegFrame f = seg_frame(g);
-    const ModeTable& mx = a.mtb ? a.mtb[g.tid] : mt;
-    const int DM = seg_moment_degree(P, mx.smax, f);
-    switch (DM) {
+  const int64_t Gs = batched ? kBatchGroup : 1;
+  for (int64_t s0 = ((int64_t)blockIdx.x * kSegWarps + warp) * Gs; s0 < a.nseg;
+       s0 += (int64_t)gridDim.x * kSegWarps * Gs) {
+    const int64_t s1 = s0 + Gs < a.nseg ? s0 + Gs : a.nseg;
+    for (int64_t s = s0; s < s1; ++s) {
+      const SegGeom g = seg_geom(a, s);
+      const SegFrame f = seg_frame(g);
+      const int DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
+      if (k1_narrow(DM) == WIDE) continue;
+      if (batched && g.tid != cached_tid) {
+        warp_load_table(a.mtb + g.tid, mx, ne, lane);
+        cached_tid = g.tid;
+      }
+      if constexpr (!WIDE) {
+        switch (DM) {
 #define FGT_K1(n)                                                  \
   case n:                                                          \
     seg_aggregate_moments<n>(a, g, f, mx, ne, lane, s, ts);        \
-    continue;
-      FGT_K1(0) FGT_K1(1) FGT_K1(2) FGT_K1(3) FGT_K1(4) FGT_K1(5) FGT_K1(6) FGT_K1(7)
-      FGT_K1(8)
+    break;
+          FGT_K1(0) FGT_K1(1) FGT_K1(2) FGT_K1(3) FGT_K1(4) FGT_K1(5) FGT_K1(6) FGT_K1(7)
+          FGT_K1(8)
 #undef FGT_K1
-      default:
-        break;
-    }
-    LaneRun r;
-    double zp, zl;
-    lane_load(a, g, s, lane, r, zp, zl);
+          default:
+            break;
+        }
+      } else {
+        LaneRun r;
+        double zp, zl;
+        lane_load(a, g, s, lane, r, zp, zl);
 #pragma unroll
-    for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
-    r.g[0] -= zp;
-    for (int k = 0; k < ne; ++k) {
-      const cplx sk = mx.s[k];
-      cplx F = {0.0, 0.0}, Pp = {1.0, 0.0}, G = {0.0, 0.0};
+        for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
+        r.g[0] -= zp;
+        double gmax = r.g[0];
 #pragma unroll
-      for (int i = 0; i < kR; ++i) {
-        const cplx d = decay_exact(sk.re, sk.im, r.g[i]);
-        F = cmad(d, F, cplx{r.b[i], 0.0});
-        Pp = cmul(Pp, d);
-        G.re = fma(r.b[i], Pp.re, G.re);
-        G.im = fma(r.b[i], Pp.im, G.im);
-      }
-      const LaneAgg w = warp_reduce_agg(LaneAgg{Pp, F, G});
-      if (lane == 0) {
-        const int64_t o = (int64_t)k * a.nseg + s;
-        ts.A[o] = w.A;
-        ts.F[o] = w.F;
-        ts.G[o] = w.G;
+        for (int e = 1; e < kR; ++e) gmax = fmax(gmax, r.g[e]);
+        switch (pick_degree(P, mx.smax, warp_max(gmax))) {
+#define FGT_K1W(n)                                           \
+  case n:                                                    \
+    seg_aggregate_wide<n>(mx, ne, lane, r, a.nseg, s, ts);   \
+    break;
+          FGT_K1W(0) FGT_K1W(1) FGT_K1W(2) FGT_K1W(3) FGT_K1W(4) FGT_K1W(5) FGT_K1W(6)
+          FGT_K1W(7) FGT_K1W(8) FGT_K1W(9) FGT_K1W(10) FGT_K1W(11) FGT_K1W(12) FGT_K1W(13)
+          FGT_K1W(14) FGT_K1W(15) FGT_K1W(16)
+#undef FGT_K1W
+          default:
+            seg_aggregate_wide<-1>(mx, ne, lane, r, a.nseg, s, ts);
+        }
       }
     }
+  }
+}
+
+// Batched plans: one thread per transform writes its mode table.
+__global__ void batch_modes_kernel(BatchModeBase base, const double* __restrict__ deltas, int B,
+                                   ModeTable* __restrict__ out) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const double isq = 1.0 / sqrt(deltas[b]);  // as build_modes (host)
+  ModeTable& T = out[b];
+  double smax = 0.0;
+  for (int k = 0; k < kMaxModes; ++k) {
+    if (k < base.ne) {
+      const cplx s = {base.t[k].re * isq, base.t[k].im * isq};
+      T.s[k] = s;
+      T.mw[k] = base.mw[k];
+      smax = fmax(smax, hypot(s.re, s.im));
+      const cplx ms = {-s.re, -s.im};
+      cplx c = {1.0, 0.0};
+      T.coef[k][0] = c;
+      T.coef[k][1] = ms;
+      c = ms;
+      for (int n = 2; n <= kMaxDeg; ++n) {
+        c = cmul(c, ms);
+        c.re /= (double)n;
+        c.im /= (double)n;
+        T.coef[k][n] = c;
+      }
+    } else {
+      T.s[k] = {0.0, 0.0};
+      T.mw[k] = {0.0, 0.0};
+      for (int n = 0; n <= kMaxDeg; ++n) T.coef[k][n] = {0.0, 0.0};
+    }
+  }
+  T.smax = smax;
+  T.pad = 0.0;
+}
+
+// Plan-time segment classes: counts[0] = K1 wide segments, counts[1] = K3.
+__global__ void classify_kernel(StreamArgs a, ModeParams P, double smax,
+                                const int* __restrict__ skip_flags,
+                                unsigned long long* __restrict__ counts) {
+  // metadata of a rejected batch (non-finite / unsorted) is not valid
+  if (skip_flags && (skip_flags[0] | skip_flags[1] | skip_flags[3] | skip_flags[4])) return;
+  const int lane = threadIdx.x & 31;
+  unsigned long long c1 = 0, c3 = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s0 = (int64_t)blockIdx.x * blockDim.x; s0 < a.nseg; s0 += stride) {
+    const int64_t s = s0 + threadIdx.x;
+    bool w1 = false, w3 = false;
+    if (s < a.nseg) {
+      const SegGeom g = seg_geom(a, s);
+      const int DM = seg_moment_degree(P, seg_smax(a, g, smax), seg_frame(g));
+      w1 = !k1_narrow(DM);
+      w3 = !k3_narrow(DM);
+    }
+    c1 += __popc(__ballot_sync(0xffffffffu, w1));
+    c3 += __popc(__ballot_sync(0xffffffffu, w3));
+  }
+  if (lane == 0) {
+    atomicAdd(counts, c1);
+    atomicAdd(counts + 1, c3);
   }
 }
 
@@ -672,50 +833,67 @@ __device__ unsigned long long g_phase_cycles[8];
 #ifndef FGT_K3_MINB
 #define FGT_K3_MINB 4
 #endif
-template <bool MS>
-__global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
+#ifndef FGT_K3W_MINB
+#define FGT_K3W_MINB 3
+#endif
+template <bool MS, bool WIDE>
+__global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
     seg_main_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
                     TileState ts, OutArgs o) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  ModeTable& mt = *reinterpret_cast<ModeTable*>(smem_raw);
+  // kSegWarps mode tables (slot 0 shared by the CTA for single plans, one per
+  // warp for batched plans), then the per-warp regions
+  ModeTable* tabs = reinterpret_cast<ModeTable*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ne = P.ne;
-  unsigned char* wreg = smem_raw + sizeof(ModeTable) + (size_t)warp * warp_region_bytes(ne);
+  const bool batched = a.mtb != nullptr;
+  unsigned char* wreg = smem_raw + sizeof(ModeTable) * (batched ? kSegWarps : 1) +
+                        (size_t)warp * warp_region_bytes(ne);
   Carry* carries = reinterpret_cast<Carry*>(wreg);
   double* su = reinterpret_cast<double*>(wreg + sizeof(Carry) * 32 * (size_t)ne);
-  load_mode_table(mtab, mt);
+  if (!batched) load_mode_table(mtab, tabs[0]);
   __syncthreads();
-  for (int64_t s = (int64_t)blockIdx.x * kSegWarps + warp; s < a.nseg;
-       s += (int64_t)gridDim.x * kSegWarps) {
+  ModeTable& mx = batched ? tabs[warp] : tabs[0];
+  int cached_tid = -1;
+  // batched plans walk groups of kBatchGroup consecutive segments (mostly
+  // one transform: one table load per group); single plans go segment-wise
+  const int64_t G = batched ? kBatchGroup : 1;
+  for (int64_t s0 = ((int64_t)blockIdx.x * kSegWarps + warp) * G; s0 < a.nseg;
+       s0 += (int64_t)gridDim.x * kSegWarps * G) {
+    const int64_t s1 = s0 + G < a.nseg ? s0 + G : a.nseg;
+    for (int64_t s = s0; s < s1; ++s) {
 #if FGT_PHASE_TIMING
-    const long long t0 = clock64();
+      const long long t0 = clock64();
 #endif
-    const SegGeom g = seg_geom(a, s);
-    const SegFrame f = seg_frame(g);
-    // segment carries: lane q < ne forward of mode q, ne <= q < 2ne backward
-    cplx seg_c = {0.0, 0.0};
-    if (lane < 2 * ne) {
-      const int k = lane < ne ? lane : lane - ne;
-      const int64_t idx = (int64_t)k * a.nseg + s;
-      seg_c = lane < ne ? ts.Cf[idx] : ts.Cb[idx];
-    }
-    LaneRun r;
-    double zp, zl;
-    lane_load(a, g, s, lane, r, zp, zl);
-    // gaps (coordinates are still needed by the moment path)
-    double gmax = r.g[0] - zp;
+      const SegGeom g = seg_geom(a, s);
+      const SegFrame f = seg_frame(g);
+      const int DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
+      if (k3_narrow(DM) == WIDE) continue;
+      if (batched && g.tid != cached_tid) {
+        warp_load_table(a.mtb + g.tid, mx, ne, lane);
+        cached_tid = g.tid;
+      }
+      // segment carries: lane q < ne forward of mode q, ne <= q < 2ne backward
+      cplx seg_c = {0.0, 0.0};
+      if (lane < 2 * ne) {
+        const int k = lane < ne ? lane : lane - ne;
+        const int64_t idx = (int64_t)k * a.nseg + s;
+        seg_c = lane < ne ? ts.Cf[idx] : ts.Cb[idx];
+      }
+      LaneRun r;
+      double zp, zl;
+      lane_load(a, g, s, lane, r, zp, zl);
+      // gaps (coordinates are still needed by the moment path)
+      double gmax = r.g[0] - zp;
 #pragma unroll
-    for (int e = 1; e < kR; ++e) gmax = fmax(gmax, r.g[e] - r.g[e - 1]);
-    const ModeTable& mx = a.mtb ? a.mtb[g.tid] : mt;
-    const int D = pick_degree(P, mx.smax, warp_max(gmax));
-    const int DM = seg_moment_degree(P, mx.smax, f);
+      for (int e = 1; e < kR; ++e) gmax = fmax(gmax, r.g[e] - r.g[e - 1]);
+      const int D = pick_degree(P, mx.smax, warp_max(gmax));
 #if FGT_PHASE_TIMING
-    const long long t1 = clock64();
+      const long long t1 = clock64();
 #endif
-    Carry* mine = carries + lane * ne;
-    bool done = false;
-    if (D >= 0) {
-      switch (DM) {
+      Carry* mine = carries + lane * ne;
+      if constexpr (!WIDE) {
+        switch (DM) {
 #define FGT_CM(n)                                                                   \
   case n: {                                                                         \
     Coef<n> c;                                                                      \
@@ -726,57 +904,59 @@ __global__ void __launch_bounds__(kThreads, FGT_K3_MINB)
       term = cmul(horner<n>(c, lane < ne ? f.h0 : f.h1), seg_c);                    \
     }                                                                               \
     carries_moments<n>(mx, ne, r, f, zp, zl, lane, term, mine);                     \
-    done = true;                                                                    \
   } break;
-        FGT_CM(0) FGT_CM(1) FGT_CM(2) FGT_CM(3) FGT_CM(4) FGT_CM(5)
+          FGT_CM(0) FGT_CM(1) FGT_CM(2) FGT_CM(3) FGT_CM(4) FGT_CM(5)
 #undef FGT_CM
-        default:
-          break;
+          default:
+            break;
+        }
+        static_assert(kK3Moments == 5, "FGT_CM cases");
       }
-    }
 #pragma unroll
-    for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
-    r.g[0] -= zp;
-    if (!done) carries_scan(mx, ne, r, lane, seg_c, seg_c, 0, mine);
-    __syncwarp();
+      for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
+      r.g[0] -= zp;
+      if constexpr (!WIDE) __syncwarp();
 #if FGT_PHASE_TIMING
-    const long long t2 = clock64();
+      const long long t2 = clock64();
 #endif
 
-    double out[kR];
+      double out[kR];
 #pragma unroll
-    for (int e = 0; e < kR; ++e) out[e] = 0.0;
-    if constexpr (MS) {
-      ModeSumsOut ms{o.hp, o.hm, a.M, o.u_offset + g.ib + r.tfirst};
-      dispatch_pass2<true>(D, mx, ne, r, mine, out, ms);
-    } else {
-      dispatch_pass2<false>(D, mx, ne, r, mine, out, ModeSumsOut{nullptr, nullptr, 0, 0});
+      for (int e = 0; e < kR; ++e) out[e] = 0.0;
+      const ModeSumsOut ms = MS ? ModeSumsOut{o.hp, o.hm, a.M, o.u_offset + g.ib + r.tfirst}
+                                : ModeSumsOut{nullptr, nullptr, 0, 0};
+      if constexpr (!WIDE)
+        dispatch_pass2<MS>(D, mx, ne, r, mine, out, ms);
+      else
+        dispatch_wide<MS>(D, mx, ne, r, lane, seg_c, out, ms);
+      if constexpr (!MS) {
 #if FGT_PHASE_TIMING
-      const long long t3 = clock64();
+        const long long t3 = clock64();
 #endif
-      int tk = r.tfirst;
+        int tk = r.tfirst;
 #pragma unroll
-      for (int e = 0; e < kR; ++e)
-        if (r.tmask & (1u << e)) su[tk++] = out[e];
+        for (int e = 0; e < kR; ++e)
+          if (r.tmask & (1u << e)) su[tk++] = out[e];
+        __syncwarp();
+        const int64_t base = o.u_offset + g.ib;
+        if (o.tperm) {
+          for (int i = lane; i < g.nx; i += 32) o.u[o.tperm[base + i]] = su[i];
+        } else {
+          for (int i = lane; i < g.nx; i += 32) o.u[base + i] = su[i];
+        }
+#if FGT_PHASE_TIMING
+        const long long t4 = clock64();
+        if (lane == 0) {
+          atomicAdd(&g_phase_cycles[0], (unsigned long long)(t1 - t0));
+          atomicAdd(&g_phase_cycles[1], (unsigned long long)(t2 - t1));
+          atomicAdd(&g_phase_cycles[2], (unsigned long long)(t3 - t2));
+          atomicAdd(&g_phase_cycles[3], (unsigned long long)(t4 - t3));
+          atomicAdd(&g_phase_cycles[4], 1ull);
+        }
+#endif
+      }
       __syncwarp();
-      const int64_t base = o.u_offset + g.ib;
-      if (o.tperm) {
-        for (int i = lane; i < g.nx; i += 32) o.u[o.tperm[base + i]] = su[i];
-      } else {
-        for (int i = lane; i < g.nx; i += 32) o.u[base + i] = su[i];
-      }
-#if FGT_PHASE_TIMING
-      const long long t4 = clock64();
-      if (lane == 0) {
-        atomicAdd(&g_phase_cycles[0], (unsigned long long)(t1 - t0));
-        atomicAdd(&g_phase_cycles[1], (unsigned long long)(t2 - t1));
-        atomicAdd(&g_phase_cycles[2], (unsigned long long)(t3 - t2));
-        atomicAdd(&g_phase_cycles[3], (unsigned long long)(t4 - t3));
-        atomicAdd(&g_phase_cycles[4], 1ull);
-      }
-#endif
     }
-    __syncwarp();
   }
 }
 
@@ -1215,8 +1395,8 @@ TileState tile_state_carve(cplx* base, int64_t nseg, int ne) {
   return TileState{base, base + nt, base + 2 * nt, base + 3 * nt, base + 4 * nt, base + 5 * nt};
 }
 
-size_t seg_smem_bytes(int ne) {
-  return sizeof(ModeTable) + (size_t)kSegWarps * warp_region_bytes(ne);
+size_t seg_smem_bytes(int ne, bool batched) {
+  return sizeof(ModeTable) * (batched ? kSegWarps : 1) + (size_t)kSegWarps * warp_region_bytes(ne);
 }
 
 cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int64_t N,
@@ -1276,7 +1456,7 @@ template <class K>
 static cudaError_t set_smem(K kernel, bool& done) {
   if (done) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)seg_smem_bytes(kMaxModes));
+                                       (int)seg_smem_bytes(kMaxModes, true));
   if (e == cudaSuccess) done = true;
   return e;
 }
@@ -1284,11 +1464,54 @@ static cudaError_t set_smem(K kernel, bool& done) {
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, cudaStream_t st) {
   if (a.nseg == 0) return cudaSuccess;
-  int64_t want = (a.nseg + kSegWarps - 1) / kSegWarps;
+  const int64_t per_cta = (int64_t)kSegWarps * (a.mtb ? kBatchGroup : 1);
+  int64_t want = (a.nseg + per_cta - 1) / per_cta;
   const int64_t cap = (int64_t)num_sms() * 16;
   const unsigned grid = (unsigned)(want < cap ? want : cap);
+  if (a.nwide1 != 0) {
+    note_launch();
+    seg_aggregate_kernel<true><<<grid, kThreads, 0, st>>>(a, P, mt, ts);
+  }
+  if (a.nwide1 != a.nseg) {
+    note_launch();
+    seg_aggregate_kernel<false><<<grid, kThreads, 0, st>>>(a, P, mt, ts);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_batch_modes(const BatchModeBase& base, const double* deltas, int B,
+                               ModeTable* out, cudaStream_t st) {
+  if (B <= 0) return cudaSuccess;
   note_launch();
-  seg_aggregate_kernel<<<grid, kThreads, 0, st>>>(a, P, mt, ts);
+  batch_modes_kernel<<<(B + 127) / 128, 128, 0, st>>>(base, deltas, B, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_classify(const StreamArgs& a, const ModeParams& P, double smax,
+                            const int* skip_flags, unsigned long long* counts, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), st);
+  if (e != cudaSuccess || a.nseg == 0) return e;
+  const int64_t want = (a.nseg + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  note_launch();
+  classify_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(a, P, smax, skip_flags,
+                                                                       counts);
+  return cudaGetLastError();
+}
+
+template <bool MS, bool WIDE>
+static cudaError_t launch_seg_main_variant(const StreamArgs& a, const ModeParams& P,
+                                           const ModeTable* mt, TileState ts, OutArgs o,
+                                           cudaStream_t st) {
+  static bool done = false;
+  cudaError_t e = set_smem(seg_main_kernel<MS, WIDE>, done);
+  if (e != cudaSuccess) return e;
+  const int64_t per_cta = (int64_t)kSegWarps * (a.mtb ? kBatchGroup : 1);
+  int64_t want = (a.nseg + per_cta - 1) / per_cta;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
+  note_launch();
+  seg_main_kernel<MS, WIDE><<<grid, kThreads, seg_smem_bytes(P.ne, a.mtb != nullptr), st>>>(a, P, mt, ts, o);
   return cudaGetLastError();
 }
 
@@ -1296,15 +1519,12 @@ template <bool MS>
 static cudaError_t launch_seg_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                                    TileState ts, OutArgs o, cudaStream_t st) {
   if (a.nseg == 0) return cudaSuccess;
-  static bool done = false;
-  cudaError_t e = set_smem(seg_main_kernel<MS>, done);
-  if (e != cudaSuccess) return e;
-  int64_t want = (a.nseg + kSegWarps - 1) / kSegWarps;
-  const int64_t cap = (int64_t)num_sms() * 8;
-  const unsigned grid = (unsigned)(want < cap ? want : cap);
-  note_launch();
-  seg_main_kernel<MS><<<grid, kThreads, seg_smem_bytes(P.ne), st>>>(a, P, mt, ts, o);
-  return cudaGetLastError();
+  if (a.nwide3 != 0) {
+    cudaError_t e = launch_seg_main_variant<MS, true>(a, P, mt, ts, o, st);
+    if (e != cudaSuccess) return e;
+  }
+  if (a.nwide3 != a.nseg) return launch_seg_main_variant<MS, false>(a, P, mt, ts, o, st);
+  return cudaSuccess;
 }
 
 cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,

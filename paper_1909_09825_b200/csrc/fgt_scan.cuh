@@ -50,6 +50,9 @@ struct StreamArgs {
   const int4* seg_info = nullptr;
   const int64_t* seg_jb = nullptr;
   const ModeTable* mtb = nullptr;
+  // plan-time segment classes (classify_segments): segments too wide for the
+  // moment form of K1 / K3; -1 = unknown (both kernel variants run)
+  int64_t nwide1 = -1, nwide3 = -1;
 };
 
 struct OutArgs {
@@ -75,7 +78,7 @@ int64_t scan_blocks(int64_t nseg);
 size_t tile_state_elems(int64_t nseg, int ne);
 TileState tile_state_carve(cplx* base, int64_t nseg, int ne);
 
-size_t seg_smem_bytes(int ne);
+size_t seg_smem_bytes(int ne, bool batched);
 
 cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int64_t N,
                              int64_t seg, int64_t nseg, int64_t* seg_ib, cudaStream_t st);
@@ -99,6 +102,21 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
                               int64_t ntiles, int64_t* tile_ib, int64_t* seg_ib, int64_t* seg_jb,
                               int4* seg_info, double2* seg_z, uint32_t* seg_mask, int* flags,
                               cudaStream_t st);
+// Per-transform mode tables of a batched plan, built on the device:
+// s_k = t_k / sqrt(delta_b), mw_k, Taylor coefficients of exp(-s g)
+// (c_0 = 1 and c_1 = -s exact), smax.  deltas: device array of B.
+struct BatchModeBase {
+  int ne;
+  cplx t[kMaxModes];   // folded SOE nodes
+  cplx mw[kMaxModes];  // multiplier * weight
+};
+cudaError_t launch_batch_modes(const BatchModeBase& base, const double* deltas, int B,
+                               ModeTable* out, cudaStream_t st);
+// Plan-time classification: counts[0] / counts[1] = segments that K1 / K3
+// process on their wide (per-element) path.  smax: the single plan's
+// max |s_k| (batched plans read their tables).
+cudaError_t launch_classify(const StreamArgs& a, const ModeParams& P, double smax,
+                            const int* skip_flags, unsigned long long* counts, cudaStream_t st);
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, cudaStream_t st);
 // K2: exclusive carries per segment.  carry_in: 2*ne complex (forward carry at

@@ -221,6 +221,21 @@ def test_mode_sums_vs_quadratic_definition():
             assert np.max(np.abs(hm[k] - ehm)) <= 1e-12 * bscale
 
 
+@pytest.mark.parametrize("delta", [10.0, 1e-4])
+def test_mode_sums_vs_oracle_narrow_and_wide(delta):
+    # delta = 10: every segment takes the moment (narrow) path of K1 and K3;
+    # delta = 1e-4: every segment the per-element (wide) path
+    x, y = up(30000, 77, 3), up(40000, 77, 0)
+    a = 2.0 * up(40000, 77, 1) - 1.0
+    soe = fgt.fold(fgt.cf_soe(12))
+    p = fgt.plan(fgt.TransformRequest(x, y, a, delta), soe)
+    hp, hm = fgt.mode_sums(p, a)
+    rp, rm = oracle.mode_sums(x, y, a, delta, 6)
+    bar = 1e-12 * np.sum(np.abs(a))
+    assert np.max(np.abs(hp - rp)) <= bar
+    assert np.max(np.abs(hm - rm)) <= bar
+
+
 def test_sorted_fields_and_stable_permutation():
     # test_transform.cpp:297-310
     p = fgt.plan(fgt.TransformRequest([0.5, 0.2, 0.5, 0.2], [0.4], [1.0], 1.0),
@@ -411,6 +426,20 @@ def test_batched_transforms_vs_oracle():
             assert out[b].size == ref.size
             if ref.size:
                 check(out[b], ref, al[b] if al[b].size else [1.0])
+
+
+def test_batched_mixed_segment_classes():
+    # transforms large enough that narrow (moment) and wide (per-element)
+    # segments of K1 and K3 meet in one batched plan
+    deltas = [10.0, 1.0, 0.1, 1e-3, 1e-5, 1e-7]
+    n = 60000
+    xs = [np.sort(up(n, 300 + b, 3)) for b in range(len(deltas))]
+    ys = [np.sort(up(n, 300 + b, 0)) for b in range(len(deltas))]
+    al = [2.0 * up(n, 300 + b, 1) - 1.0 for b in range(len(deltas))]
+    soe = fgt.soe_for_tolerance(1e-10)
+    out = fgt.batch_transform(xs, ys, al, deltas, soe)
+    for b, d in enumerate(deltas):
+        check(out[b], oracle.transform(xs[b], ys[b], al[b], d, ne=len(soe), mode=0), al[b])
 
 
 def test_batched_rejects_unsorted_and_reuses_plan():

@@ -67,6 +67,20 @@ def timed(step, steps, warmup):
     return e0.elapsed_time(e1) / steps
 
 
+def kernel_ms(fn, reps=3):
+    """Average K1/K2/K3 durations (profiling events on the launching stream)."""
+    L.fgt_profile_enable(1)
+    L.fgt_profile_read(None, None, 3)
+    for _ in range(reps):
+        fn()
+    torch.cuda.synchronize()
+    kms = np.zeros(3)
+    kcnt = (ctypes.c_longlong * 3)()
+    L.fgt_profile_read(kms.ctypes.data_as(PD), kcnt, 3)
+    L.fgt_profile_enable(0)
+    return {k: kms[i] / max(1, kcnt[i]) for i, k in enumerate(("K1", "K2", "K3"))}
+
+
 def single_config(name, x, y, a, delta, tol, steps, warmup, extra):
     keep, sp = soe_args(tol)
     M, N = x.numel(), y.numel()
@@ -92,8 +106,9 @@ def single_config(name, x, y, a, delta, tol, steps, warmup, extra):
     ms = timed(step, steps, warmup)
     hh = plan()
     ms_apply = timed(lambda: apply(hh), steps, warmup)
+    kms = kernel_ms(lambda: apply(hh))
     L.fgt_plan_destroy(hh)
-    line = {"config": name, "metric": "(M+N) points/s", "value": (M + N) / (ms / 1e3),
+    line = {"kernels_ms": kms, "config": name, "metric": "(M+N) points/s", "value": (M + N) / (ms / 1e3),
             "ms_per_step": ms, "apply_ms": ms_apply,
             "apply_value": (M + N) / (ms_apply / 1e3), "plan_ms": ms - ms_apply,
             "M": M, "N": N, "delta": delta, "tol": tol, "n_e": len(keep[0]), "steps": steps,
@@ -125,7 +140,7 @@ def cfg4(steps, warmup):
                   {"data": "16-component mixture sigma 1e-3, unsorted, alpha U[0,1)"})
 
 
-def cfg5(steps, warmup, B=4096, n=65536):
+def cfg5(steps, warmup, B=4096, n=65536, fixed_delta=None, tols=(1e-3, 1e-6, 1e-10)):
     # per transform b: seed b, sorted uniform targets / sources, alpha = 2u-1
     x = torch.empty(B, n, dtype=torch.float64, device=dev)
     y = torch.empty(B, n, dtype=torch.float64, device=dev)
@@ -138,10 +153,14 @@ def cfg5(steps, warmup, B=4096, n=65536):
     y = torch.sort(y, dim=1).values.contiguous()
     a.mul_(2.0).sub_(1.0)
     deltas = 10.0 ** (-6.0 + 5.0 * up(B, 0, 9))
+    dlabel = "log-uniform [1e-6, 1e-1] (stream 9)"
+    if fixed_delta is not None:
+        deltas = np.full(B, fixed_delta)
+        dlabel = "all %g" % fixed_delta
     off = np.arange(B + 1, dtype=np.int64) * n
     u = torch.empty(B * n, dtype=torch.float64, device=dev)
     fl = _capi.FGT_DEVICE_PTRS | _capi.FGT_BORROW
-    for tol in (1e-3, 1e-6, 1e-10):
+    for tol in tols:
         keep, sp = soe_args(tol)
 
         def plan():
@@ -164,13 +183,14 @@ def cfg5(steps, warmup, B=4096, n=65536):
         ms = timed(step, steps, warmup)
         hh = plan()
         ms_apply = timed(lambda: apply(hh), steps, warmup)
+        kms = kernel_ms(lambda: apply(hh))
         L.fgt_plan_destroy(hh)
         pts = 2.0 * B * n
         print(json.dumps({"config": "cfg5", "metric": "(M+N) points/s", "value": pts / (ms / 1e3),
                           "ms_per_step": ms, "apply_ms": ms_apply,
                           "apply_value": pts / (ms_apply / 1e3), "plan_ms": ms - ms_apply,
                           "transforms": B, "M_each": n, "N_each": n, "tol": tol,
-                          "n_e": len(keep[0]), "deltas": "log-uniform [1e-6, 1e-1] (stream 9)",
+                          "n_e": len(keep[0]), "kernels_ms": kms, "deltas": dlabel,
                           "steps": steps, "warmup": warmup}), flush=True)
 
 
@@ -179,6 +199,11 @@ if __name__ == "__main__":
     ap.add_argument("--configs", default="2,4,5")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--cfg5-deltas", default="", help="comma list: run cfg5 with one fixed delta each")
     args = ap.parse_args()
+    for d in [v for v in args.cfg5_deltas.split(",") if v]:
+        cfg5(args.steps, args.warmup, fixed_delta=float(d), tols=(1e-10,))
+    if args.cfg5_deltas:
+        sys.exit(0)
     for c in args.configs.split(","):
         {"2": cfg2, "4": cfg4, "5": cfg5}[c.strip()](args.steps, args.warmup)
