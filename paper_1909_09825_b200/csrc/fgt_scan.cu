@@ -127,15 +127,29 @@ __device__ __forceinline__ void gap_factors(const ModeTable& mt, int k, const do
   }
 }
 
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+// Runtime-degree variant for the wide kernels (one code path for every
+// degree keeps them small in the instruction cache); D < 0: exact.
+__device__ __forceinline__ void gap_factors_rt(const ModeTable& mt, int k, int D,
+                                               const double (&g)[kR], cplx (&d)[kR]) {
+  if (D < 0) {
+    const cplx s = mt.s[k];
+#pragma unroll
+    for (int i = 0; i < kR; ++i) d[i] = decay_exact(s.re, s.im, g[i]);
+    return;
+  }
+  const cplx* cf = mt.coef[k];
+  const cplx top = cf[D];
+#pragma unroll
+  for (int i = 0; i < kR; ++i) d[i] = top;
+#pragma unroll 1
+  for (int n = D - 1; n >= 0; --n) {
+    const cplx c = cf[n];
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      d[i].re = fma(d[i].re, g[i], c.re);
+      d[i].im = fma(d[i].im, g[i], c.im);
+    }
+  }
 }
 
 __device__ __forceinline__ double warp_max(double v) {
@@ -514,13 +528,13 @@ __device__ __forceinline__ void lane_scan(cplx A, cplx F, cplx G, int lane, cplx
 // once (degree-D Taylor, exact for D < 0), the lane aggregates from them,
 // the lane carries by warp scans, then both chains -- one evaluation of
 // exp(-s g) per element and mode.
-template <int D, bool MS>
-__device__ __forceinline__ void wide_modes(const ModeTable& mt, int ne, const LaneRun& r, int lane,
-                                           cplx seg_c, double (&out)[kR],
+template <bool MS>
+__device__ __forceinline__ void wide_modes(const ModeTable& mt, int ne, int D, const LaneRun& r,
+                                           int lane, cplx seg_c, double (&out)[kR],
                                            const ModeSumsOut& ms) {
   for (int k = 0; k < ne; ++k) {
     cplx d[kR];
-    gap_factors<D>(mt, k, r.g, d);
+    gap_factors_rt(mt, k, D, r.g, d);
     cplx F = {0.0, 0.0}, A = {1.0, 0.0}, G = {0.0, 0.0};
 #pragma unroll
     for (int i = 0; i < kR; ++i) {
@@ -535,24 +549,6 @@ __device__ __forceinline__ void wide_modes(const ModeTable& mt, int ne, const La
     cplx cf, cb;
     lane_scan(A, F, G, lane, cfs, cbs, cf, cb);
     chains_mode<MS>(d, mt.mw[k], r, cf, cb, k, out, ms);
-  }
-}
-
-template <bool MS>
-__device__ __forceinline__ void dispatch_wide(int D, const ModeTable& mt, int ne, const LaneRun& r,
-                                              int lane, cplx seg_c, double (&out)[kR],
-                                              const ModeSumsOut& ms) {
-  switch (D) {
-#define FGT_WD(n)                                      \
-  case n:                                              \
-    wide_modes<n, MS>(mt, ne, r, lane, seg_c, out, ms); \
-    break;
-    FGT_WD(0) FGT_WD(1) FGT_WD(2) FGT_WD(3) FGT_WD(4) FGT_WD(5) FGT_WD(6) FGT_WD(7)
-    FGT_WD(8) FGT_WD(9) FGT_WD(10) FGT_WD(11) FGT_WD(12) FGT_WD(13) FGT_WD(14)
-    FGT_WD(15) FGT_WD(16)
-#undef FGT_WD
-    default:
-      wide_modes<-1, MS>(mt, ne, r, lane, seg_c, out, ms);
   }
 }
 
@@ -655,6 +651,11 @@ __device__ __forceinline__ int seg_moment_degree(const ModeParams& P, double sma
 // it has every gap below 2 rmax[kK3Moments] < rmax[kMaxDeg], so its gap
 // factors take the Taylor path.
 constexpr int kK3Moments = 5;
+// Highest lane-moment degree of the K1 wide path.
+#ifndef FGT_LANE_MOM_MAX
+#define FGT_LANE_MOM_MAX 12
+#endif
+constexpr int kLaneMomMax = FGT_LANE_MOM_MAX;
 
 // Segment classes (both kernels and the plan-time count use these).
 __device__ __forceinline__ bool k1_narrow(int DM) { return DM >= 0 && DM <= kRegDeg; }
@@ -666,13 +667,12 @@ __device__ __forceinline__ double seg_smax(const StreamArgs& a, const SegGeom& g
 
 // Wide segments: lane aggregates from the gap factors (degree-D Taylor,
 // exact for D < 0), reduced across the warp in lane order.
-template <int D>
-__device__ __forceinline__ void seg_aggregate_wide(const ModeTable& mt, int ne, int lane,
+__device__ __forceinline__ void seg_aggregate_wide(const ModeTable& mt, int ne, int D, int lane,
                                                    const LaneRun& r, int64_t nseg, int64_t s,
                                                    TileState ts) {
   for (int k = 0; k < ne; ++k) {
     cplx d[kR];
-    gap_factors<D>(mt, k, r.g, d);
+    gap_factors_rt(mt, k, D, r.g, d);
     cplx F = {0.0, 0.0}, Pp = {1.0, 0.0}, G = {0.0, 0.0};
 #pragma unroll
     for (int i = 0; i < kR; ++i) {
@@ -682,6 +682,59 @@ __device__ __forceinline__ void seg_aggregate_wide(const ModeTable& mt, int ne, 
       G.im = fma(r.b[i], Pp.im, G.im);
     }
     const LaneAgg w = warp_reduce_agg(LaneAgg{Pp, F, G});
+    if (lane == 0) {
+      const int64_t o = (int64_t)k * nseg + s;
+      ts.A[o] = w.A;
+      ts.F[o] = w.F;
+      ts.G[o] = w.G;
+    }
+  }
+}
+
+// Wide segments whose lane runs are narrow: lane aggregates from the lane's
+// source moments about its centre (the segment moment form of
+// seg_aggregate_moments applied to one run, frame (zp, zl)), reduced across
+// the warp.  r.g holds coordinates.
+template <int DL>
+__device__ __forceinline__ void seg_aggregate_lanes(const ModeTable& mt, int ne, int lane,
+                                                    const LaneRun& r, double zp, double zl,
+                                                    int64_t nseg, int64_t s, TileState ts) {
+  const double h = 0.5 * (zl - zp);
+  const double zc = zp + h;
+  const double h0 = zc - zp, h1 = zl - zc;
+  double M[DL + 1];
+#pragma unroll
+  for (int n = 0; n <= DL; ++n) M[n] = 0.0;
+#pragma unroll
+  for (int e = 0; e < kR; ++e) {
+    const double d = r.g[e] - zc;
+    double p = r.b[e];
+    M[0] += p;
+#pragma unroll
+    for (int n = 1; n <= DL; ++n) {
+      p *= d;
+      M[n] += p;
+    }
+  }
+  for (int k = 0; k < ne; ++k) {
+    Coef<DL> c;
+    c.load(mt, k);
+    cplx ev = {0.0, 0.0}, od = {0.0, 0.0};
+#pragma unroll
+    for (int n = 0; n <= DL; ++n) {
+      const cplx cn = c[n];
+      if (n & 1) {
+        od.re = fma(cn.re, M[n], od.re);
+        od.im = fma(cn.im, M[n], od.im);
+      } else {
+        ev.re = fma(cn.re, M[n], ev.re);
+        ev.im = fma(cn.im, M[n], ev.im);
+      }
+    }
+    const cplx E0 = horner<DL>(c, h0);
+    const cplx E1 = horner<DL>(c, h1);
+    const LaneAgg w = warp_reduce_agg(LaneAgg{cmul(E0, E1), cmul(E1, cplx{ev.re - od.re, ev.im - od.im}),
+                                              cmul(E0, cplx{ev.re + od.re, ev.im + od.im})});
     if (lane == 0) {
       const int64_t o = (int64_t)k * nseg + s;
       ts.A[o] = w.A;
@@ -737,24 +790,24 @@ __global__ void __launch_bounds__(kThreads)
         LaneRun r;
         double zp, zl;
         lane_load(a, g, s, lane, r, zp, zl);
+        // lane-run moments when the runs are narrow enough (a few degrees)
+        const int DL = pick_degree(P, mx.smax, warp_max(0.5 * (zl - zp)));
+        if (DL >= 0 && DL <= kLaneMomMax) {
+          if (DL <= 4)
+            seg_aggregate_lanes<4>(mx, ne, lane, r, zp, zl, a.nseg, s, ts);
+          else if (DL <= 8)
+            seg_aggregate_lanes<8>(mx, ne, lane, r, zp, zl, a.nseg, s, ts);
+          else
+            seg_aggregate_lanes<kLaneMomMax>(mx, ne, lane, r, zp, zl, a.nseg, s, ts);
+          continue;
+        }
 #pragma unroll
         for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
         r.g[0] -= zp;
         double gmax = r.g[0];
 #pragma unroll
         for (int e = 1; e < kR; ++e) gmax = fmax(gmax, r.g[e]);
-        switch (pick_degree(P, mx.smax, warp_max(gmax))) {
-#define FGT_K1W(n)                                           \
-  case n:                                                    \
-    seg_aggregate_wide<n>(mx, ne, lane, r, a.nseg, s, ts);   \
-    break;
-          FGT_K1W(0) FGT_K1W(1) FGT_K1W(2) FGT_K1W(3) FGT_K1W(4) FGT_K1W(5) FGT_K1W(6)
-          FGT_K1W(7) FGT_K1W(8) FGT_K1W(9) FGT_K1W(10) FGT_K1W(11) FGT_K1W(12) FGT_K1W(13)
-          FGT_K1W(14) FGT_K1W(15) FGT_K1W(16)
-#undef FGT_K1W
-          default:
-            seg_aggregate_wide<-1>(mx, ne, lane, r, a.nseg, s, ts);
-        }
+        seg_aggregate_wide(mx, ne, pick_degree(P, mx.smax, warp_max(gmax)), lane, r, a.nseg, s, ts);
       }
     }
   }
@@ -928,7 +981,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
       if constexpr (!WIDE)
         dispatch_pass2<MS>(D, mx, ne, r, mine, out, ms);
       else
-        dispatch_wide<MS>(D, mx, ne, r, lane, seg_c, out, ms);
+        wide_modes<MS>(mx, ne, D, r, lane, seg_c, out, ms);
       if constexpr (!MS) {
 #if FGT_PHASE_TIMING
         const long long t3 = clock64();
@@ -996,6 +1049,77 @@ struct TileCtx {
   int tid;
 };
 
+constexpr int kPlanThreads = 256;
+constexpr int kPlanPer = kPlanTile / kPlanThreads;  // merged positions per thread
+static_assert(kPlanPer == 16 && kSeg % kPlanPer == 0, "plan tile layout");
+
+// ---- TMA bulk staging (one mbarrier per CTA)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Staging plan of n values g[0..n) into a shared buffer: the 16-byte aligned
+// interior by one bulk copy, an unaligned head / tail element by plain
+// loads.  The values land at s = buf + head, s[0..n).
+struct Stage {
+  int head;         // 1 when g is not 16-byte aligned (g[0] loaded by a thread)
+  int i0, i1;       // interior [i0, i1) (bulk)
+  int tail;         // 1 when g[n-1] lies past the interior
+};
+__device__ __forceinline__ Stage stage_plan(const double* g, int n) {
+  Stage st;
+  st.head = (n > 0 && (reinterpret_cast<uintptr_t>(g) & 15u)) ? 1 : 0;
+  st.i0 = st.head;
+  int i1 = st.i0 + ((n - st.i0) & ~1);
+  if (i1 < st.i0) i1 = st.i0;
+  st.i1 = i1;
+  st.tail = (n > st.i1) ? 1 : 0;
+  return st;
+}
+
+// 32-bit merge path in shared memory (sources first at ties).
+__device__ __forceinline__ int merge_path_smem(const double* x, int nx, const double* y, int ny,
+                                               int diag) {
+  int lo = diag - ny > 0 ? diag - ny : 0;
+  int hi = diag < nx ? diag : nx;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (x[mid - 1] < y[diag - mid])
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
 template <bool BATCH>
 __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorted,
                                                int64_t nseg, int64_t* __restrict__ seg_ib,
@@ -1004,10 +1128,10 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
                                                double2* __restrict__ seg_z,
                                                uint32_t* __restrict__ seg_mask,
                                                int* __restrict__ flags) {
-  extern __shared__ double tsm[];
-  double* sx = tsm;              // [kPlanTile]
-  double* sy = tsm + kPlanTile;  // [kPlanTile]
+  extern __shared__ __align__(16) double tsm[];
   __shared__ int sib[kPlanSegs + 1];
+  __shared__ int sflags;
+  __shared__ __align__(8) uint64_t bar;
   const int64_t ib = c.ib, ie = c.ie;
   const int64_t jb = c.d0 - ib, je = c.d1 - ie;
   const int64_t nx64 = ie - ib, len64 = c.d1 - c.d0;
@@ -1018,114 +1142,120 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
     return;
   }
   const int nx = (int)nx64, ny = (int)(je - jb), len = (int)len64;
+  const int t = threadIdx.x, lane = t & 31;
+  const double* gx = c.x + ib;
+  const double* gy = c.y + jb;
+  const Stage stx = stage_plan(gx, nx), sty = stage_plan(gy, ny);
+  double* sx = tsm + stx.head;                  // [kPlanTile + 1] (sentinel)
+  double* sy = tsm + (kPlanTile + 2) + sty.head;
+  if (t == 0) {
+    sflags = 0;
+    mbar_init(&bar);
+  }
+  __syncthreads();
+  if (t == 0) {
+    const unsigned bx = 8u * (unsigned)(stx.i1 - stx.i0), by = 8u * (unsigned)(sty.i1 - sty.i0);
+    mbar_expect(&bar, bx + by);
+    if (bx) bulk_g2s(sx + stx.i0, gx + stx.i0, bx, &bar);
+    if (by) bulk_g2s(sy + sty.i0, gy + sty.i0, by, &bar);
+  }
+  if (t == 1 && stx.head) sx[0] = __ldg(gx);
+  if (t == 2 && stx.tail) sx[nx - 1] = __ldg(gx + nx - 1);
+  if (t == 3 && sty.head) sy[0] = __ldg(gy);
+  if (t == 4 && sty.tail) sy[ny - 1] = __ldg(gy + ny - 1);
+  if (t == 5) sx[nx] = INFINITY;  // merge sentinels
+  if (t == 6) sy[ny] = INFINITY;
+  // neighbours across the tile start (sortedness)
+  const double xprev = (t == 0 && ib > 0 && nx > 0) ? __ldg(gx - 1) : -INFINITY;
+  const double yprev = (t == 0 && jb > 0 && ny > 0) ? __ldg(gy - 1) : -INFINITY;
+  mbar_wait(&bar, 0);
+  __syncthreads();
   int f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0;
-  // asynchronous staging: every element in flight at once, no registers
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) cp_async8(sx + i, c.x + ib + i);
-  for (int j = threadIdx.x; j < ny; j += blockDim.x) cp_async8(sy + j, c.y + jb + j);
-  cp_async_commit();
+  for (int i = t; i < nx; i += kPlanThreads) {
+    const double v = sx[i];
+    f0 |= !isfinite(v);
+    if (check_sorted) f3 |= (i > 0 ? sx[i - 1] : xprev) > v;
+  }
+  for (int j = t; j < ny; j += kPlanThreads) {
+    const double v = sy[j];
+    f1 |= !isfinite(v);
+    if (check_sorted) f4 |= (j > 0 ? sy[j - 1] : yprev) > v;
+  }
   // same-points needs x[i] == y[i] for every i; skip once any tile has seen
   // a mismatch (distinct point sets), otherwise compare against the staged
   // sources where the index ranges overlap (they do when x == y)
-  const bool check_same = !BATCH && (c.M == c.N) && *(volatile int*)(flags + 2) == 0;
-  cp_async_wait_all();
-  __syncthreads();
-  for (int i = threadIdx.x; i < nx; i += blockDim.x) {
-    const double v = sx[i];
-    f0 |= !isfinite(v);
-    if (check_sorted && i > 0) f3 |= sx[i - 1] > v;
-  }
-  for (int j = threadIdx.x; j < ny; j += blockDim.x) {
-    const double v = sy[j];
-    f1 |= !isfinite(v);
-    if (check_sorted && j > 0) f4 |= sy[j - 1] > v;
-  }
-  if (check_same) {
-    for (int i = threadIdx.x; i < nx; i += blockDim.x) {
+  if (!BATCH && (c.M == c.N) && *(volatile int*)(flags + 2) == 0) {
+    for (int i = t; i < nx; i += kPlanThreads) {
       const int64_t gi = ib + i;
       const int64_t jl = gi - jb;
       const double yv = (jl >= 0 && jl < ny) ? sy[jl] : __ldg(c.y + gi);
       f2 |= !(sx[i] == yv);
     }
   }
-  __syncthreads();
-  if (check_sorted && threadIdx.x == 0) {
-    if (ib > 0 && nx > 0) f3 |= __ldg(c.x + ib - 1) > sx[0];
-    if (jb > 0 && ny > 0) f4 |= __ldg(c.y + jb - 1) > sy[0];
+  // merge: thread t owns merged positions [16 t, 16 t + 16) of the tile
+  const int d0 = t * kPlanPer;
+  unsigned bits = 0u;
+  if (d0 < len) {
+    int i = merge_path_smem(sx, nx, sy, ny, d0);
+    int j = d0 - i;
+    if ((d0 % kSeg) == 0) sib[d0 / kSeg] = i;
+    double cx = sx[i < nx ? i : nx];
+    double cy = sy[j < ny ? j : ny];
+#pragma unroll
+    for (int e = 0; e < kPlanPer; ++e) {
+      if (d0 + e < len) {
+        const bool tgt = !(cy <= cx);  // sources first on ties
+        bits |= (unsigned)tgt << e;
+        if (tgt) {
+          ++i;
+          cx = sx[i < nx ? i : nx];
+        } else {
+          ++j;
+          cy = sy[j < ny ? j : ny];
+        }
+      }
+    }
   }
-  // segment splits inside the tile
   const int nsegs_tile = (len + kSeg - 1) / kSeg;
-  if (threadIdx.x <= nsegs_tile) {
-    const int dd = threadIdx.x * kSeg < len ? threadIdx.x * kSeg : len;
-    sib[threadIdx.x] = (int)merge_path(sx, (int64_t)nx, sy, (int64_t)ny, (int64_t)dd);
-  }
+  if (t == 0) sib[nsegs_tile] = nx;
+  // mask: two threads per 32-bit word, same layout as bit (merged pos % 32)
+  unsigned wd = bits << ((t & 1) * 16);
+  wd |= __shfl_down_sync(0xffffffffu, wd, 1);
+  if ((t & 1) == 0 && d0 < nsegs_tile * kSeg) seg_mask[c.seg0 * (kSeg / 32) + (t >> 1)] = wd;
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int k = warp; k < nsegs_tile; k += blockDim.x / 32) {
+  if (t < nsegs_tile) {
+    const int k = t;
     const int i0 = sib[k], i1 = sib[k + 1];
     const int sd0 = k * kSeg;
     const int sd1 = (sd0 + kSeg < len) ? sd0 + kSeg : len;
     const int j0 = sd0 - i0, j1 = sd1 - i1;
-    // each lane merges its window of kR positions (merge path in shared memory)
-    const int w0 = sd0 + lane * kR;
-    unsigned byte = 0u;
-    if (w0 < sd1 && i1 >= i0 && j1 >= j0) {
-      // merge path restricted to the segment: targets [i0, i1), sources [j0, j1)
-      int i = i0 + (int)merge_path(sx + i0, (int64_t)(i1 - i0), sy + j0, (int64_t)(j1 - j0),
-                                   (int64_t)(w0 - sd0));
-      int j = w0 - i;
-      double cx = i < i1 ? sx[i] : INFINITY;
-      double cy = j < j1 ? sy[j] : INFINITY;
-#pragma unroll
-      for (int e = 0; e < kR; ++e) {
-        if (w0 + e < sd1) {
-          if (cy <= cx && j < j1) {  // source first on ties
-            ++j;
-            cy = j < j1 ? sy[j] : INFINITY;
-          } else {
-            byte |= 1u << e;
-            ++i;
-            cx = i < i1 ? sx[i] : INFINITY;
-          }
-        }
-      }
-    }
-    unsigned wd = byte << ((lane & 3) * 8);
-    wd |= __shfl_down_sync(0xffffffffu, wd, 1);
-    wd |= __shfl_down_sync(0xffffffffu, wd, 2);
     const int64_t sg = c.seg0 + k;
-    if ((lane & 3) == 0) seg_mask[sg * (kSeg / 32) + (lane >> 2)] = wd;
-    if (lane == 0) {
-      seg_ib[sg] = c.xoff + ib + i0;
-      if constexpr (BATCH) {
-        seg_jb[sg] = c.yoff + jb + j0;
-        seg_info[sg] = make_int4(sd1 - sd0, i1 - i0, c.tid, 0);
-      }
-      double px, py;
-      if (k == 0) {
-        // -inf at the start of a stream (a new transform never couples back)
-        px = ib > 0 ? __ldg(c.x + ib - 1) : -INFINITY;
-        py = jb > 0 ? __ldg(c.y + jb - 1) : -INFINITY;
-      } else {
-        px = i0 > 0 ? sx[i0 - 1] : -INFINITY;
-        py = j0 > 0 ? sy[j0 - 1] : -INFINITY;
-      }
-      const double lx = i1 > i0 ? sx[i1 - 1] : -INFINITY;
-      const double ly = j1 > j0 ? sy[j1 - 1] : -INFINITY;
-      seg_z[sg] = make_double2(fmax(px, py), fmax(lx, ly));
-      if (!BATCH && sg + 1 == nseg) seg_ib[nseg] = c.M;
+    seg_ib[sg] = c.xoff + ib + i0;
+    if constexpr (BATCH) {
+      seg_jb[sg] = c.yoff + jb + j0;
+      seg_info[sg] = make_int4(sd1 - sd0, i1 - i0, c.tid, 0);
     }
+    double px, py;
+    if (k == 0) {
+      // -inf at the start of a stream (a new transform never couples back)
+      px = ib > 0 ? __ldg(c.x + ib - 1) : -INFINITY;
+      py = jb > 0 ? __ldg(c.y + jb - 1) : -INFINITY;
+    } else {
+      px = i0 > 0 ? sx[i0 - 1] : -INFINITY;
+      py = j0 > 0 ? sy[j0 - 1] : -INFINITY;
+    }
+    const double lx = i1 > i0 ? sx[i1 - 1] : -INFINITY;
+    const double ly = j1 > j0 ? sy[j1 - 1] : -INFINITY;
+    seg_z[sg] = make_double2(fmax(px, py), fmax(lx, ly));
+    if (!BATCH && sg + 1 == nseg) seg_ib[nseg] = c.M;
   }
-  f0 = __syncthreads_or(f0);
-  f1 = __syncthreads_or(f1);
-  f2 = __syncthreads_or(f2);
-  f3 = __syncthreads_or(f3);
-  f4 = __syncthreads_or(f4);
-  if (threadIdx.x == 0) {
-    if (f0) atomicOr(flags + 0, 1);
-    if (f1) atomicOr(flags + 1, 1);
-    if (f2) atomicOr(flags + 2, 1);
-    if (f3) atomicOr(flags + 3, 1);
-    if (f4) atomicOr(flags + 4, 1);
+  int fl = (f0 ? 1 : 0) | (f1 ? 2 : 0) | (f2 ? 4 : 0) | (f3 ? 8 : 0) | (f4 ? 16 : 0);
+  fl = __reduce_or_sync(0xffffffffu, fl);
+  if (lane == 0 && fl) atomicOr(&sflags, fl);
+  __syncthreads();
+  if (t == 0 && sflags) {
+    for (int q = 0; q < 5; ++q)
+      if (sflags & (1 << q)) atomicOr(flags + q, 1);
   }
 }
 
@@ -1414,7 +1544,7 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
                               uint32_t* seg_mask, int* flags, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * 2 * kPlanTile;
+  const size_t smem = sizeof(double) * 2 * (kPlanTile + 2);  // + head slot, sentinel
   static bool done = false;
   if (!done) {
     cudaError_t e = cudaFuncSetAttribute(plan_tile_kernel,
@@ -1439,7 +1569,7 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
   const BatchArgs b{xs, ys, t_off, s_off, seg_base, tile_base, tile_tid};
   note_launch(2);
   batch_partition_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(b, ntiles, tile_ib);
-  const size_t smem = sizeof(double) * 2 * kPlanTile;
+  const size_t smem = sizeof(double) * 2 * (kPlanTile + 2);  // + head slot, sentinel
   static bool done = false;
   if (!done) {
     cudaError_t e = cudaFuncSetAttribute(batch_plan_tile_kernel,

@@ -394,6 +394,39 @@ def test_device_pointer_path_matches_host_path():
     assert np.array_equal(ud.cpu().numpy(), host)
 
 
+@pytest.mark.parametrize("ox,oy", [(1, 0), (0, 1), (1, 1), (3, 2)])
+def test_device_pointers_not_16_byte_aligned(ox, oy):
+    # borrowed device arrays at odd element offsets: the plan's bulk staging
+    # must handle 8-byte aligned starts and ends (head / tail elements)
+    import torch
+    M, N = 70001, 50003
+    x, y = np.sort(up(M, 13, 3)), np.sort(up(N, 13, 0))
+    a = 2.0 * up(N, 13, 1) - 1.0
+    host = gpu_transform(x, y, a, 1e-3, 6, mode=0)
+    soe = fgt.fold(fgt.cf_soe(12))
+    tr, ti, wr, wi, sc = soe.arrays()
+    xb = torch.zeros(M + 8, dtype=torch.float64, device="cuda")
+    yb = torch.zeros(N + 8, dtype=torch.float64, device="cuda")
+    xb[ox:ox + M] = torch.from_numpy(x).cuda()
+    yb[oy:oy + N] = torch.from_numpy(y).cuda()
+    xd, yd = xb[ox:ox + M], yb[oy:oy + N]
+    ad = torch.from_numpy(a).cuda()
+    ud = torch.empty(M, dtype=torch.float64, device="cuda")
+    L = _capi.lib()
+    h = ctypes.c_void_p()
+    fl = _capi.FGT_DEVICE_PTRS | _capi.FGT_BORROW
+    _capi.check(L.fgt_plan_create(ctypes.cast(xd.data_ptr(), PD), M, ctypes.cast(yd.data_ptr(), PD), N,
+                                  1e-3, tr.ctypes.data_as(PD), ti.ctypes.data_as(PD),
+                                  wr.ctypes.data_as(PD), wi.ctypes.data_as(PD),
+                                  sc.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), 6, 1, fl, 0,
+                                  None, ctypes.byref(h)))
+    _capi.check(L.fgt_apply_general(h, ctypes.cast(ad.data_ptr(), PD), N,
+                                    ctypes.cast(ud.data_ptr(), PD), 1, fl, None))
+    torch.cuda.synchronize()
+    L.fgt_plan_destroy(h)
+    assert np.array_equal(ud.cpu().numpy(), host)
+
+
 def test_gpu_kernels_actually_launch():
     L = _capi.lib()
     before = L.fgt_launch_counter()

@@ -199,6 +199,7 @@ if __name__ == "__main__":
     ap.add_argument("--configs", default="2,4,5")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--tols", default="1e-3,1e-6,1e-10", help="cfg5 tolerances")
     ap.add_argument("--cfg5-deltas", default="", help="comma list: run cfg5 with one fixed delta each")
     args = ap.parse_args()
     for d in [v for v in args.cfg5_deltas.split(",") if v]:
@@ -206,4 +207,7 @@ if __name__ == "__main__":
     if args.cfg5_deltas:
         sys.exit(0)
     for c in args.configs.split(","):
-        {"2": cfg2, "4": cfg4, "5": cfg5}[c.strip()](args.steps, args.warmup)
+        if c.strip() == "5":
+            cfg5(args.steps, args.warmup, tols=tuple(float(t) for t in args.tols.split(",")))
+        else:
+            {"2": cfg2, "4": cfg4}[c.strip()](args.steps, args.warmup)
