@@ -184,6 +184,53 @@ static_assert(offsetof(ModeTable, coef) == sizeof(double) * 4 * kMaxModes, "tabl
 // Consecutive segments a warp walks in batched plans before striding.
 constexpr int kBatchGroup = 16;
 
+// ---- TMA bulk staging on mbarriers
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+}
+
 // ---------------------------------------------------------------- geometry
 
 struct SegGeom {
@@ -300,6 +347,153 @@ __device__ __forceinline__ void lane_load(const StreamArgs& a, const SegGeom& g,
   for (int e = 0; e < kR; ++e) r.g[e] = e < nreal ? r.g[e] : zl;
 }
 
+// ---------------------------------------------------------- segment stage
+// K3 streaming: a warp's next segment (targets, sources, strengths) is
+// copied into its shared-memory stage by TMA bulk copies while the current
+// one is computed.  Layout: xy[kStageXY] holds x at slot ox, y at slot oy;
+// b[kStageB] holds b at slot ob.  Bulk copies need 16-byte aligned source,
+// destination and size: an unaligned first / last element is copied by an
+// 8-byte cp.async instead (lanes 1..6).
+constexpr int kStageXY = kSeg + 4;
+constexpr int kStageB = kSeg + 2;
+// + mask words (32 B), segment carries (2 kMaxModes complex), mbarrier
+constexpr size_t kStageBytes =
+    sizeof(double) * (kStageXY + kStageB) + 32 + sizeof(cplx) * 2 * kMaxModes + 16;
+
+struct StagePtrs {
+  double* xy;
+  double* bb;
+  uint32_t* mask;  // [kSeg / 32]
+  cplx* car;       // [2 kMaxModes]: forward carries of modes 0..ne-1, then backward
+  uint64_t* bar;
+};
+__device__ __forceinline__ StagePtrs stage_ptrs(unsigned char* base) {
+  StagePtrs p;
+  p.xy = reinterpret_cast<double*>(base);
+  p.bb = p.xy + kStageXY;
+  p.mask = reinterpret_cast<uint32_t*>(p.bb + kStageB);
+  p.car = reinterpret_cast<cplx*>(p.mask + kSeg / 32);
+  p.bar = reinterpret_cast<uint64_t*>(p.car + 2 * kMaxModes);
+  return p;
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
+struct StageSlots {
+  int ox, oy, ob;
+};
+
+__device__ __forceinline__ int misaligned16(const double* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15u) ? 1 : 0;
+}
+
+__device__ __forceinline__ StageSlots stage_slots(const StreamArgs& a, const SegGeom& g) {
+  StageSlots o;
+  const int hx = g.nx > 0 ? misaligned16(a.xs + g.ib) : 0;
+  const int hy = g.ny > 0 ? misaligned16(a.ys + g.jb) : 0;
+  o.ox = hx;
+  o.oy = hx + g.nx;
+  o.oy += (o.oy + hy) & 1;  // y's first aligned element on an even slot
+  o.ob = g.ny > 0 ? misaligned16(a.bs + g.jb) : 0;
+  return o;
+}
+
+// Copy of n values from src to slot o of buf (o odd iff src is misaligned):
+// the aligned interior by lane 0 (bulk, counted in *bytes), head / tail by
+// lanes hl / tl.
+__device__ __forceinline__ void stage_array(double* buf, int o, const double* src, int n, int lane,
+                                            int hl, int tl, uint64_t* bar, bool issue_bulk) {
+  if (n <= 0) return;
+  const int h = o & 1;  // head element copied separately
+  int c = (n - h) & ~1;
+  if (c < 0) c = 0;
+  if (issue_bulk && c > 0) bulk_g2s(buf + o + h, src + h, 8u * (unsigned)c, bar);
+  if (lane == hl && h) cp_async8(buf + o, src);
+  if (lane == tl && h + c < n) cp_async8(buf + o + n - 1, src + n - 1);
+}
+
+__device__ __forceinline__ unsigned stage_bulk_bytes(const StageSlots& o, const SegGeom& g) {
+  auto cnt = [](int h, int n) {
+    if (n <= 0) return 0;
+    const int c = (n - h) & ~1;
+    return c > 0 ? c : 0;
+  };
+  return 8u * (unsigned)(cnt(o.ox & 1, g.nx) + cnt(o.oy & 1, g.ny) + cnt(o.ob & 1, g.ny));
+}
+
+__device__ __forceinline__ void stage_issue(const StreamArgs& a, const TileState& ts, int ne,
+                                            int64_t s, const SegGeom& g, const StagePtrs& sp,
+                                            int lane) {
+  const StageSlots o = stage_slots(a, g);
+  if (lane == 0) {
+    fence_proxy_async();  // earlier generic reads of the stage before async writes
+    mbar_expect(sp.bar, stage_bulk_bytes(o, g) + 32u);
+    bulk_g2s(sp.mask, a.seg_mask + s * (kSeg / 32), 32u, sp.bar);
+  }
+  stage_array(sp.xy, o.ox, a.xs + g.ib, g.nx, lane, 1, 2, sp.bar, lane == 0);
+  stage_array(sp.xy, o.oy, a.ys + g.jb, g.ny, lane, 3, 4, sp.bar, lane == 0);
+  stage_array(sp.bb, o.ob, a.bs + g.jb, g.ny, lane, 5, 6, sp.bar, lane == 0);
+  if (lane < 2 * ne) {
+    const int k = lane < ne ? lane : lane - ne;
+    const int64_t idx = (int64_t)k * a.nseg + s;
+    cp_async16(sp.car + lane, lane < ne ? ts.Cf + idx : ts.Cb + idx);
+  }
+  cp_async_commit();
+}
+
+// lane_load from the stage (mask word of the lane prefetched by the caller)
+__device__ __forceinline__ void lane_load_stage(const StreamArgs& a, const SegGeom& g,
+                                                const double* xy, const double* bb,
+                                                uint32_t word, int lane, LaneRun& r, double& zp,
+                                                double& zl) {
+  const StageSlots so = stage_slots(a, g);
+  const double* sx = xy + so.ox;
+  const double* sy = xy + so.oy;
+  const double* sb = bb + so.ob;
+  const int d0 = lane * kR;
+  const int nreal = g.len - d0 < 0 ? 0 : (g.len - d0 < kR ? g.len - d0 : kR);
+  const unsigned live = (1u << nreal) - 1u;
+  const unsigned byte = (word >> ((lane & 3) * 8)) & 0xffu & live;
+  const int nt = __popc(byte);
+  int incl = nt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int i0 = incl - nt;
+  const int j0 = (d0 < g.len ? d0 : g.len) - i0;
+  r.tfirst = i0;
+  r.tmask = byte;
+  double last = 0.0;
+#pragma unroll
+  for (int e = 0; e < kR; ++e) {
+    const int t = __popc(byte & ((1u << e) - 1u));
+    const int sidx = e - t;
+    if (e < nreal) {
+      if (byte & (1u << e)) {
+        r.g[e] = sx[i0 + t];
+        r.b[e] = 0.0;
+      } else {
+        r.g[e] = sy[j0 + sidx];
+        r.b[e] = sb[j0 + sidx];
+      }
+      last = r.g[e];
+    } else {
+      r.g[e] = 0.0;
+      r.b[e] = 0.0;
+    }
+  }
+  double prev = __shfl_up_sync(0xffffffffu, last, 1);
+  if (lane == 0) prev = g.zprev;
+  zp = prev;
+  zl = nreal > 0 ? last : prev;
+#pragma unroll
+  for (int e = 0; e < kR; ++e) r.g[e] = e < nreal ? r.g[e] : zl;
+}
+
 // --------------------------------------------------------------- pass 2
 
 // Mode-sums test hook (detail::mode_sums, transform.cpp:310-350): store H
@@ -366,11 +560,53 @@ constexpr int kCarryUnroll = FGT_CARRY_UNROLL;
 #endif
 constexpr int kModeUnroll = FGT_MODE_UNROLL;
 
+#ifndef FGT_P2_PAIRS
+#define FGT_P2_PAIRS 0
+#endif
+// Two modes at once: four independent chains (more ILP, more registers).
+template <int D>
+__device__ __forceinline__ void pass2_two(const ModeTable& mt, int k, const LaneRun& r,
+                                          const Carry* carry, double (&out)[kR]) {
+  cplx d0[kR], d1[kR];
+  gap_factors<D>(mt, k, r.g, d0);
+  gap_factors<D>(mt, k + 1, r.g, d1);
+  const cplx mw0 = mt.mw[k], mw1 = mt.mw[k + 1];
+  cplx H0 = carry[k].cf, K0 = carry[k].cb, H1 = carry[k + 1].cf, K1 = carry[k + 1].cb;
+  K0.re += r.b[kR - 1];
+  K1.re += r.b[kR - 1];
+#pragma unroll
+  for (int i = 0; i < kR; ++i) {
+    const int j = kR - 1 - i;
+    H0 = cmad(d0[i], H0, cplx{r.b[i], 0.0});
+    H1 = cmad(d1[i], H1, cplx{r.b[i], 0.0});
+    out[i] = fma(mw0.re, H0.re, fma(-mw0.im, H0.im, out[i]));
+    out[i] = fma(mw1.re, H1.re, fma(-mw1.im, H1.im, out[i]));
+    out[j] = fma(mw0.re, K0.re, fma(-mw0.im, K0.im, out[j]));
+    out[j] = fma(mw1.re, K1.re, fma(-mw1.im, K1.im, out[j]));
+    if (j > 0) {
+      K0 = cmad(d0[j], K0, cplx{r.b[j - 1], 0.0});
+      K1 = cmad(d1[j], K1, cplx{r.b[j - 1], 0.0});
+    }
+  }
+}
+
 // Narrow segments: lane carries already in shared memory (moment form).
 template <int D, bool MS>
 __device__ __forceinline__ void pass2(const ModeTable& mt, int ne, const LaneRun& r,
                                       const Carry* carry, double (&out)[kR],
                                       const ModeSumsOut& ms) {
+#if FGT_P2_PAIRS
+  if constexpr (!MS) {
+    int k = 0;
+    for (; k + 1 < ne; k += 2) pass2_two<D>(mt, k, r, carry, out);
+    if (k < ne) {
+      cplx d[kR];
+      gap_factors<D>(mt, k, r.g, d);
+      chains_mode<false>(d, mt.mw[k], r, carry[k].cf, carry[k].cb, k, out, ms);
+    }
+    return;
+  }
+#endif
 #pragma unroll kModeUnroll
   for (int k = 0; k < ne; ++k) {
     cplx d[kR];
@@ -561,31 +797,29 @@ __host__ __device__ __forceinline__ size_t warp_region_bytes(int ne) {
 
 // ------------------------------------------------------------------- K1
 
+// Segment aggregates from the source moments about the segment centre.
+// Moments of this lane's sources (up to kK1Per, loaded by the caller),
+// warp-reduced; lanes k < ne turn them into mode k's (A, F, G).
+constexpr int kK1Per = kSeg / 32;  // sources per lane (a segment has <= kSeg)
+
 template <int DM>
-__device__ __forceinline__ void seg_aggregate_moments(const StreamArgs& a, const SegGeom& g,
-                                                      const SegFrame& f, const ModeTable& mt,
-                                                      int ne, int lane, int64_t s, TileState ts) {
+__device__ __forceinline__ void seg_aggregate_from(const SegFrame& f, const ModeTable& mt, int ne,
+                                                   int lane, int64_t nseg, int64_t s,
+                                                   const TileState& ts,
+                                                   const double (&yv)[kK1Per],
+                                                   const double (&bv)[kK1Per]) {
   double M[DM + 1];
 #pragma unroll
   for (int n = 0; n <= DM; ++n) M[n] = 0.0;
-  for (int j0 = lane; j0 < g.ny; j0 += 4 * 32) {
-    double yv[4], bv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int j = j0 + u * 32;
-      yv[u] = j < g.ny ? __ldg(a.ys + g.jb + j) : f.zc;
-      bv[u] = j < g.ny ? __ldg(a.bs + g.jb + j) : 0.0;
-    }
+  for (int u = 0; u < kK1Per; ++u) {
+    const double d = yv[u] - f.zc;
+    double p = bv[u];
+    M[0] += p;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double d = yv[u] - f.zc;
-      double p = bv[u];
-      M[0] += p;
-#pragma unroll
-      for (int n = 1; n <= DM; ++n) {
-        p *= d;
-        M[n] += p;
-      }
+    for (int n = 1; n <= DM; ++n) {
+      p *= d;
+      M[n] += p;
     }
   }
 #pragma unroll
@@ -611,10 +845,21 @@ __device__ __forceinline__ void seg_aggregate_moments(const StreamArgs& a, const
     }
     const cplx E0 = horner<DM>(c, f.h0);
     const cplx E1 = horner<DM>(c, f.h1);
-    const int64_t o = (int64_t)k * a.nseg + s;
+    const int64_t o = (int64_t)k * nseg + s;
     ts.A[o] = cmul(E0, E1);
     ts.F[o] = cmul(E1, cplx{ev.re - od.re, ev.im - od.im});
     ts.G[o] = cmul(E0, cplx{ev.re + od.re, ev.im + od.im});
+  }
+}
+
+// Issue the loads of a segment's sources (lane-strided; padding = centre, 0).
+__device__ __forceinline__ void k1_load(const StreamArgs& a, const SegGeom& g, double zc,
+                                        int lane, double (&yv)[kK1Per], double (&bv)[kK1Per]) {
+#pragma unroll
+  for (int u = 0; u < kK1Per; ++u) {
+    const int j = lane + u * 32;
+    yv[u] = j < g.ny ? __ldg(a.ys + g.jb + j) : zc;
+    bv[u] = j < g.ny ? __ldg(a.bs + g.jb + j) : 0.0;
   }
 }
 
@@ -761,32 +1006,76 @@ __global__ void __launch_bounds__(kThreads)
   ModeTable& mx = batched ? tabs[warp] : tabs[0];
   int cached_tid = -1;
   const int ne = P.ne;
-  const int64_t Gs = batched ? kBatchGroup : 1;
-  for (int64_t s0 = ((int64_t)blockIdx.x * kSegWarps + warp) * Gs; s0 < a.nseg;
-       s0 += (int64_t)gridDim.x * kSegWarps * Gs) {
-    const int64_t s1 = s0 + Gs < a.nseg ? s0 + Gs : a.nseg;
-    for (int64_t s = s0; s < s1; ++s) {
-      const SegGeom g = seg_geom(a, s);
-      const SegFrame f = seg_frame(g);
-      const int DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
-      if (k1_narrow(DM) == WIDE) continue;
+  if constexpr (!WIDE) {
+    // contiguous range per warp (metadata from L1); the next narrow
+    // segment's sources are loaded into registers before this one is reduced
+    const int64_t nwarps = (int64_t)gridDim.x * kSegWarps;
+    const int64_t wid = (int64_t)blockIdx.x * kSegWarps + warp;
+    const int64_t per = (a.nseg + nwarps - 1) / nwarps;
+    const int64_t S0 = wid * per;
+    const int64_t S1 = S0 + per < a.nseg ? S0 + per : a.nseg;
+    auto next_narrow = [&](int64_t s, SegGeom& g, SegFrame& f, int& DM) -> int64_t {
+      for (; s < S1; ++s) {
+        g = seg_geom(a, s);
+        f = seg_frame(g);
+        DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
+        if (k1_narrow(DM)) return s;
+      }
+      return S1;
+    };
+    SegGeom g;
+    SegFrame f;
+    int DM = -1;
+    double yv[kK1Per], bv[kK1Per];
+    int64_t s = next_narrow(S0, g, f, DM);
+    if (s < S1) k1_load(a, g, f.zc, lane, yv, bv);
+    while (s < S1) {
+      SegGeom gn;
+      SegFrame fn;
+      int DMn = -1;
+      double yn[kK1Per], bn[kK1Per];
+      const int64_t sn = next_narrow(s + 1, gn, fn, DMn);
+      if (sn < S1) k1_load(a, gn, fn.zc, lane, yn, bn);
       if (batched && g.tid != cached_tid) {
         warp_load_table(a.mtb + g.tid, mx, ne, lane);
         cached_tid = g.tid;
       }
-      if constexpr (!WIDE) {
-        switch (DM) {
-#define FGT_K1(n)                                                  \
-  case n:                                                          \
-    seg_aggregate_moments<n>(a, g, f, mx, ne, lane, s, ts);        \
+      switch (DM) {
+#define FGT_K1(n)                                                   \
+  case n:                                                           \
+    seg_aggregate_from<n>(f, mx, ne, lane, a.nseg, s, ts, yv, bv);  \
     break;
-          FGT_K1(0) FGT_K1(1) FGT_K1(2) FGT_K1(3) FGT_K1(4) FGT_K1(5) FGT_K1(6) FGT_K1(7)
-          FGT_K1(8)
+        FGT_K1(0) FGT_K1(1) FGT_K1(2) FGT_K1(3) FGT_K1(4) FGT_K1(5) FGT_K1(6) FGT_K1(7)
+        FGT_K1(8)
 #undef FGT_K1
-          default:
-            break;
+        default:
+          break;
+      }
+      s = sn;
+      g = gn;
+      f = fn;
+      DM = DMn;
+#pragma unroll
+      for (int u = 0; u < kK1Per; ++u) {
+        yv[u] = yn[u];
+        bv[u] = bn[u];
+      }
+    }
+    return;
+  } else {
+    const int64_t Gs = batched ? kBatchGroup : 1;
+    for (int64_t s0 = ((int64_t)blockIdx.x * kSegWarps + warp) * Gs; s0 < a.nseg;
+         s0 += (int64_t)gridDim.x * kSegWarps * Gs) {
+      const int64_t s1 = s0 + Gs < a.nseg ? s0 + Gs : a.nseg;
+      for (int64_t s = s0; s < s1; ++s) {
+        const SegGeom g = seg_geom(a, s);
+        const SegFrame f = seg_frame(g);
+        const int DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
+        if (k1_narrow(DM)) continue;
+        if (batched && g.tid != cached_tid) {
+          warp_load_table(a.mtb + g.tid, mx, ne, lane);
+          cached_tid = g.tid;
         }
-      } else {
         LaneRun r;
         double zp, zl;
         lane_load(a, g, s, lane, r, zp, zl);
@@ -886,67 +1175,24 @@ __device__ unsigned long long g_phase_cycles[8];
 #ifndef FGT_K3_MINB
 #define FGT_K3_MINB 4
 #endif
-#ifndef FGT_K3W_MINB
-#define FGT_K3W_MINB 3
-#endif
+// One segment of K3 once its lane runs are in registers (r.g = coordinates):
+// segment carries, lane carries (moment form for narrow segments, warp scans
+// for wide ones), both chains of every mode, staged write of u.
 template <bool MS, bool WIDE>
-__global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
-    seg_main_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
-                    TileState ts, OutArgs o) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  // kSegWarps mode tables (slot 0 shared by the CTA for single plans, one per
-  // warp for batched plans), then the per-warp regions
-  ModeTable* tabs = reinterpret_cast<ModeTable*>(smem_raw);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+__device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParams& P,
+                                            const ModeTable& mx, const OutArgs& o,
+                                            const SegGeom& g, const SegFrame& f, int DM,
+                                            cplx seg_c, LaneRun& r, double zp, double zl,
+                                            int lane, Carry* carries, double* su) {
   const int ne = P.ne;
-  const bool batched = a.mtb != nullptr;
-  unsigned char* wreg = smem_raw + sizeof(ModeTable) * (batched ? kSegWarps : 1) +
-                        (size_t)warp * warp_region_bytes(ne);
-  Carry* carries = reinterpret_cast<Carry*>(wreg);
-  double* su = reinterpret_cast<double*>(wreg + sizeof(Carry) * 32 * (size_t)ne);
-  if (!batched) load_mode_table(mtab, tabs[0]);
-  __syncthreads();
-  ModeTable& mx = batched ? tabs[warp] : tabs[0];
-  int cached_tid = -1;
-  // batched plans walk groups of kBatchGroup consecutive segments (mostly
-  // one transform: one table load per group); single plans go segment-wise
-  const int64_t G = batched ? kBatchGroup : 1;
-  for (int64_t s0 = ((int64_t)blockIdx.x * kSegWarps + warp) * G; s0 < a.nseg;
-       s0 += (int64_t)gridDim.x * kSegWarps * G) {
-    const int64_t s1 = s0 + G < a.nseg ? s0 + G : a.nseg;
-    for (int64_t s = s0; s < s1; ++s) {
-#if FGT_PHASE_TIMING
-      const long long t0 = clock64();
-#endif
-      const SegGeom g = seg_geom(a, s);
-      const SegFrame f = seg_frame(g);
-      const int DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
-      if (k3_narrow(DM) == WIDE) continue;
-      if (batched && g.tid != cached_tid) {
-        warp_load_table(a.mtb + g.tid, mx, ne, lane);
-        cached_tid = g.tid;
-      }
-      // segment carries: lane q < ne forward of mode q, ne <= q < 2ne backward
-      cplx seg_c = {0.0, 0.0};
-      if (lane < 2 * ne) {
-        const int k = lane < ne ? lane : lane - ne;
-        const int64_t idx = (int64_t)k * a.nseg + s;
-        seg_c = lane < ne ? ts.Cf[idx] : ts.Cb[idx];
-      }
-      LaneRun r;
-      double zp, zl;
-      lane_load(a, g, s, lane, r, zp, zl);
-      // gaps (coordinates are still needed by the moment path)
-      double gmax = r.g[0] - zp;
+  // gaps (coordinates are still needed by the moment path)
+  double gmax = r.g[0] - zp;
 #pragma unroll
-      for (int e = 1; e < kR; ++e) gmax = fmax(gmax, r.g[e] - r.g[e - 1]);
-      const int D = pick_degree(P, mx.smax, warp_max(gmax));
-#if FGT_PHASE_TIMING
-      const long long t1 = clock64();
-#endif
-      Carry* mine = carries + lane * ne;
-      if constexpr (!WIDE) {
-        switch (DM) {
+  for (int e = 1; e < kR; ++e) gmax = fmax(gmax, r.g[e] - r.g[e - 1]);
+  const int D = pick_degree(P, mx.smax, warp_max(gmax));
+  Carry* mine = carries + lane * ne;
+  if constexpr (!WIDE) {
+    switch (DM) {
 #define FGT_CM(n)                                                                   \
   case n: {                                                                         \
     Coef<n> c;                                                                      \
@@ -958,57 +1204,159 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
     }                                                                               \
     carries_moments<n>(mx, ne, r, f, zp, zl, lane, term, mine);                     \
   } break;
-          FGT_CM(0) FGT_CM(1) FGT_CM(2) FGT_CM(3) FGT_CM(4) FGT_CM(5)
+      FGT_CM(0) FGT_CM(1) FGT_CM(2) FGT_CM(3) FGT_CM(4) FGT_CM(5)
 #undef FGT_CM
-          default:
-            break;
-        }
-        static_assert(kK3Moments == 5, "FGT_CM cases");
-      }
+      default:
+        break;
+    }
+    static_assert(kK3Moments == 5, "FGT_CM cases");
+  }
 #pragma unroll
-      for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
-      r.g[0] -= zp;
-      if constexpr (!WIDE) __syncwarp();
-#if FGT_PHASE_TIMING
-      const long long t2 = clock64();
-#endif
+  for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
+  r.g[0] -= zp;
+  if constexpr (!WIDE) __syncwarp();
+  double out[kR];
+#pragma unroll
+  for (int e = 0; e < kR; ++e) out[e] = 0.0;
+  const ModeSumsOut ms = MS ? ModeSumsOut{o.hp, o.hm, a.M, o.u_offset + g.ib + r.tfirst}
+                            : ModeSumsOut{nullptr, nullptr, 0, 0};
+  if constexpr (!WIDE)
+    dispatch_pass2<MS>(D, mx, ne, r, mine, out, ms);
+  else
+    wide_modes<MS>(mx, ne, D, r, lane, seg_c, out, ms);
+  if constexpr (!MS) {
+    int tk = r.tfirst;
+#pragma unroll
+    for (int e = 0; e < kR; ++e)
+      if (r.tmask & (1u << e)) su[tk++] = out[e];
+    __syncwarp();
+    const int64_t base = o.u_offset + g.ib;
+    if (o.tperm) {
+      for (int i = lane; i < g.nx; i += 32) o.u[o.tperm[base + i]] = su[i];
+    } else {
+      for (int i = lane; i < g.nx; i += 32) o.u[base + i] = su[i];
+    }
+  }
+  __syncwarp();
+}
 
-      double out[kR];
-#pragma unroll
-      for (int e = 0; e < kR; ++e) out[e] = 0.0;
-      const ModeSumsOut ms = MS ? ModeSumsOut{o.hp, o.hm, a.M, o.u_offset + g.ib + r.tfirst}
-                                : ModeSumsOut{nullptr, nullptr, 0, 0};
-      if constexpr (!WIDE)
-        dispatch_pass2<MS>(D, mx, ne, r, mine, out, ms);
-      else
-        wide_modes<MS>(mx, ne, D, r, lane, seg_c, out, ms);
-      if constexpr (!MS) {
-#if FGT_PHASE_TIMING
-        const long long t3 = clock64();
+__device__ __forceinline__ cplx load_seg_carry(const TileState& ts, int64_t nseg, int64_t s,
+                                               int ne, int lane) {
+  cplx c = {0.0, 0.0};
+  if (lane < 2 * ne) {
+    const int k = lane < ne ? lane : lane - ne;
+    const int64_t idx = (int64_t)k * nseg + s;
+    c = lane < ne ? ts.Cf[idx] : ts.Cb[idx];
+  }
+  return c;
+}
+
+#ifndef FGT_K3W_MINB
+#define FGT_K3W_MINB 3
 #endif
-        int tk = r.tfirst;
-#pragma unroll
-        for (int e = 0; e < kR; ++e)
-          if (r.tmask & (1u << e)) su[tk++] = out[e];
-        __syncwarp();
-        const int64_t base = o.u_offset + g.ib;
-        if (o.tperm) {
-          for (int i = lane; i < g.nx; i += 32) o.u[o.tperm[base + i]] = su[i];
-        } else {
-          for (int i = lane; i < g.nx; i += 32) o.u[base + i] = su[i];
-        }
-#if FGT_PHASE_TIMING
-        const long long t4 = clock64();
-        if (lane == 0) {
-          atomicAdd(&g_phase_cycles[0], (unsigned long long)(t1 - t0));
-          atomicAdd(&g_phase_cycles[1], (unsigned long long)(t2 - t1));
-          atomicAdd(&g_phase_cycles[2], (unsigned long long)(t3 - t2));
-          atomicAdd(&g_phase_cycles[3], (unsigned long long)(t4 - t3));
-          atomicAdd(&g_phase_cycles[4], 1ull);
-        }
+// Streaming (TMA-staged) segment loop per variant; measured on B200: the
+// narrow kernel is FP64-latency bound and gains nothing, see DESIGN.md.
+#ifndef FGT_K3_STREAM
+#define FGT_K3_STREAM 0
 #endif
+#ifndef FGT_K3W_STREAM
+#define FGT_K3W_STREAM 1
+#endif
+template <bool WIDE>
+__host__ __device__ constexpr bool k3_stream() {
+  return WIDE ? FGT_K3W_STREAM != 0 : FGT_K3_STREAM != 0;
+}
+// K3.  Narrow variant (WIDE = false): every warp streams a contiguous range
+// of segments; the next segment's data is staged in shared memory by TMA
+// bulk copies while the current one is computed.  Wide variant: grid-stride
+// (groups of kBatchGroup for batched plans) with direct loads.  Each skips
+// the other's segments.
+template <bool MS, bool WIDE>
+__global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
+    seg_main_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
+                    TileState ts, OutArgs o) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // mode tables (slot 0 shared by the CTA for single plans, one per warp for
+  // batched plans), then the per-warp regions (+ the stage when streaming)
+  ModeTable* tabs = reinterpret_cast<ModeTable*>(smem_raw);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ne = P.ne;
+  const bool batched = a.mtb != nullptr;
+  constexpr bool STREAM = k3_stream<WIDE>();
+  const size_t wbytes = warp_region_bytes(ne) + (STREAM ? kStageBytes : 0);
+  unsigned char* wreg =
+      smem_raw + sizeof(ModeTable) * (batched ? kSegWarps : 1) + (size_t)warp * wbytes;
+  Carry* carries = reinterpret_cast<Carry*>(wreg);
+  double* su = reinterpret_cast<double*>(wreg + sizeof(Carry) * 32 * (size_t)ne);
+  if (!batched) load_mode_table(mtab, tabs[0]);
+  ModeTable& mx = batched ? tabs[warp] : tabs[0];
+  int cached_tid = -1;
+  if constexpr (STREAM) {
+    const StagePtrs sp = stage_ptrs(wreg + warp_region_bytes(ne));
+    if (lane == 0) mbar_init(sp.bar);
+    __syncthreads();
+    const int64_t nwarps = (int64_t)gridDim.x * kSegWarps;
+    const int64_t wid = (int64_t)blockIdx.x * kSegWarps + warp;
+    const int64_t per = (a.nseg + nwarps - 1) / nwarps;
+    const int64_t S0 = wid * per;
+    const int64_t S1 = S0 + per < a.nseg ? S0 + per : a.nseg;
+    // next narrow segment at or after s (S1 if none); issues its staging
+    auto issue_next = [&](int64_t s) -> int64_t {
+      for (; s < S1; ++s) {
+        const SegGeom g = seg_geom(a, s);
+        if (k3_narrow(seg_moment_degree(P, seg_smax(a, g, P.smax), seg_frame(g))) != WIDE) {
+          stage_issue(a, ts, ne, s, g, sp, lane);
+          return s;
+        }
       }
+      return S1;
+    };
+    unsigned parity = 0;
+    int64_t s = issue_next(S0);
+    while (s < S1) {
+      const SegGeom g = seg_geom(a, s);
+      const SegFrame f = seg_frame(g);
+      const int DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
+      if (batched && g.tid != cached_tid) {
+        warp_load_table(a.mtb + g.tid, mx, ne, lane);
+        cached_tid = g.tid;
+      }
+      cp_async_wait_all();
+      mbar_wait(sp.bar, parity);
+      parity ^= 1u;
       __syncwarp();
+      LaneRun r;
+      double zp, zl;
+      lane_load_stage(a, g, sp.xy, sp.bb, sp.mask[lane >> 2], lane, r, zp, zl);
+      const cplx seg_c = lane < 2 * ne ? sp.car[lane] : cplx{0.0, 0.0};
+      __syncwarp();  // stage free: the next segment's copies go in now
+      const int64_t sn = issue_next(s + 1);
+      seg_compute<MS, WIDE>(a, P, mx, o, g, f, DM, seg_c, r, zp, zl, lane, carries, su);
+      s = sn;
+    }
+  } else {
+    __syncthreads();
+    // batched plans walk groups of kBatchGroup consecutive segments (mostly
+    // one transform: one table load per group); single plans go segment-wise
+    const int64_t G = batched ? kBatchGroup : 1;
+    for (int64_t s0 = ((int64_t)blockIdx.x * kSegWarps + warp) * G; s0 < a.nseg;
+         s0 += (int64_t)gridDim.x * kSegWarps * G) {
+      const int64_t s1 = s0 + G < a.nseg ? s0 + G : a.nseg;
+      for (int64_t s = s0; s < s1; ++s) {
+        const SegGeom g = seg_geom(a, s);
+        const SegFrame f = seg_frame(g);
+        const int DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
+        if (k3_narrow(DM) == WIDE) continue;
+        if (batched && g.tid != cached_tid) {
+          warp_load_table(a.mtb + g.tid, mx, ne, lane);
+          cached_tid = g.tid;
+        }
+        const cplx seg_c = load_seg_carry(ts, a.nseg, s, ne, lane);
+        LaneRun r;
+        double zp, zl;
+        lane_load(a, g, s, lane, r, zp, zl);
+        seg_compute<MS, WIDE>(a, P, mx, o, g, f, DM, seg_c, r, zp, zl, lane, carries, su);
+      }
     }
   }
 }
@@ -1052,39 +1400,6 @@ struct TileCtx {
 constexpr int kPlanThreads = 256;
 constexpr int kPlanPer = kPlanTile / kPlanThreads;  // merged positions per thread
 static_assert(kPlanPer == 16 && kSeg % kPlanPer == 0, "plan tile layout");
-
-// ---- TMA bulk staging (one mbarrier per CTA)
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_expect(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  unsigned done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 
 // Staging plan of n values g[0..n) into a shared buffer: the 16-byte aligned
 // interior by one bulk copy, an unaligned head / tail element by plain
@@ -1525,8 +1840,9 @@ TileState tile_state_carve(cplx* base, int64_t nseg, int ne) {
   return TileState{base, base + nt, base + 2 * nt, base + 3 * nt, base + 4 * nt, base + 5 * nt};
 }
 
-size_t seg_smem_bytes(int ne, bool batched) {
-  return sizeof(ModeTable) * (batched ? kSegWarps : 1) + (size_t)kSegWarps * warp_region_bytes(ne);
+size_t seg_smem_bytes(int ne, bool batched, bool stream) {
+  return sizeof(ModeTable) * (batched ? kSegWarps : 1) +
+         (size_t)kSegWarps * (warp_region_bytes(ne) + (stream ? kStageBytes : 0));
 }
 
 cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int64_t N,
@@ -1586,7 +1902,7 @@ template <class K>
 static cudaError_t set_smem(K kernel, bool& done) {
   if (done) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)seg_smem_bytes(kMaxModes, true));
+                                       (int)seg_smem_bytes(kMaxModes, true, true));
   if (e == cudaSuccess) done = true;
   return e;
 }
@@ -1636,12 +1952,25 @@ static cudaError_t launch_seg_main_variant(const StreamArgs& a, const ModeParams
   static bool done = false;
   cudaError_t e = set_smem(seg_main_kernel<MS, WIDE>, done);
   if (e != cudaSuccess) return e;
-  const int64_t per_cta = (int64_t)kSegWarps * (a.mtb ? kBatchGroup : 1);
-  int64_t want = (a.nseg + per_cta - 1) / per_cta;
-  const int64_t cap = (int64_t)num_sms() * 8;
+  const size_t smem = seg_smem_bytes(P.ne, a.mtb != nullptr, k3_stream<WIDE>());
+  int64_t want, cap;
+  if constexpr (!k3_stream<WIDE>()) {
+    const int64_t per_cta = (int64_t)kSegWarps * (a.mtb ? kBatchGroup : 1);
+    want = (a.nseg + per_cta - 1) / per_cta;
+    cap = (int64_t)num_sms() * 8;
+  } else {
+    // streaming: one resident wave, contiguous segment ranges per warp
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg_main_kernel<MS, WIDE>, kThreads,
+                                                      smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    want = (a.nseg + kSegWarps - 1) / kSegWarps;
+    cap = (int64_t)num_sms() * per_sm;
+  }
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   note_launch();
-  seg_main_kernel<MS, WIDE><<<grid, kThreads, seg_smem_bytes(P.ne, a.mtb != nullptr), st>>>(a, P, mt, ts, o);
+  seg_main_kernel<MS, WIDE><<<grid, kThreads, smem, st>>>(a, P, mt, ts, o);
   return cudaGetLastError();
 }
 
