@@ -12,7 +12,7 @@ from .soe import (SoeApprox, SoeForm, cf_soe, evaluate, fold, load_coefficient_t
                   save_coefficient_table, soe_for_tolerance, unfold, validate)
 from .transform import (BatchPlan, TransformPlan, TransformRequest, apply_general, apply_same,
                         batch_transform, direct,
-                        direct_transform, gauss_transform, mode_sums, plan,
+                        direct_transform, gauss_transform, gauss_transform_device, mode_sums, plan,
                         precompute_gap_table, uniform_points, uniform_points_array)
 
 __version__ = "0.1.0"
@@ -20,7 +20,7 @@ __version__ = "0.1.0"
 __all__ = [
     "BatchPlan", "DeviceError", "NumericalError", "batch_transform", "SoeApprox", "SoeForm", "TransformPlan", "TransformRequest",
     "apply_general", "apply_same", "cf_soe", "direct", "direct_transform", "evaluate", "fold",
-    "gauss_transform", "load_coefficient_table", "mode_count_for_tolerance", "mode_sums", "plan",
+    "gauss_transform", "gauss_transform_device", "load_coefficient_table", "mode_count_for_tolerance", "mode_sums", "plan",
     "precompute_gap_table", "preset_mode_count", "preset_soe", "save_coefficient_table",
     "soe_for_tolerance", "unfold", "uniform_points", "uniform_points_array", "validate",
 ]

@@ -248,8 +248,50 @@ def batch_transform(targets, sources, strengths, deltas, soe):
     return BatchPlan(targets, sources, deltas, soe).apply(strengths)
 
 
+def _is_cuda_tensor(v):
+    return type(v).__module__.startswith("torch") and getattr(v, "is_cuda", False)
+
+
+def gauss_transform_device(targets, sources, strengths, delta, soe=None, ne=4):
+    """Device-array entry: float64 CUDA tensors in, a CUDA
+    tensor of potentials (original target order) out, on the current stream;
+    nothing crosses PCIe.  Same validation and error classes as gauss_transform."""
+    import torch
+    x = targets.reshape(-1).to(torch.float64).contiguous()
+    y = sources.reshape(-1).to(torch.float64).contiguous()
+    a = strengths.reshape(-1).to(torch.float64).contiguous()
+    if a.numel() != y.numel():
+        raise ValueError("one strength per source required")
+    use = (soe if soe.form == SoeForm.FOLDED else fold(soe)) if soe is not None else fold(
+        cf_soe(2 * int(ne)))
+    validate(use)
+    keep, sargs = _soe_args(use)
+    dev = x.device
+    st = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+    fl = _capi.FGT_DEVICE_PTRS
+    L = _capi.lib()
+    h = ctypes.c_void_p()
+    _capi.check(L.fgt_plan_create(ctypes.cast(x.data_ptr(), _PD), x.numel(),
+                                  ctypes.cast(y.data_ptr(), _PD), y.numel(), float(delta), *sargs,
+                                  fl, dev.index or 0, st, ctypes.byref(h)))
+    try:
+        u = torch.empty(x.numel(), dtype=torch.float64, device=dev)
+        same = ctypes.c_int()
+        _capi.check(L.fgt_plan_info(h, None, None, None, ctypes.byref(same), None, None, None))
+        fn = L.fgt_apply_same if same.value else L.fgt_apply_general
+        _capi.check(fn(h, ctypes.cast(a.data_ptr(), _PD), a.numel(), ctypes.cast(u.data_ptr(), _PD),
+                       1, fl, st))
+    finally:
+        L.fgt_plan_destroy(h)
+    del keep
+    return u
+
+
 def gauss_transform(targets, sources, strengths, delta, soe=None, ne=4, threads=1):
-    """pymodule.cpp:37-60: plan(precompute) then apply_same / apply_general."""
+    """pymodule.cpp:37-60: plan(precompute) then apply_same / apply_general.
+    CUDA tensors are transformed on the device (gauss_transform_device)."""
+    if _is_cuda_tensor(targets):
+        return gauss_transform_device(targets, sources, strengths, delta, soe, ne)
     req = TransformRequest(targets, sources, strengths, delta)
     use = (soe if soe.form == SoeForm.FOLDED else fold(soe)) if soe is not None else fold(
         cf_soe(2 * int(ne)))

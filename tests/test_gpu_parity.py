@@ -427,6 +427,24 @@ def test_device_pointers_not_16_byte_aligned(ox, oy):
     assert np.array_equal(ud.cpu().numpy(), host)
 
 
+def test_gauss_transform_accepts_device_arrays():
+    # pymodule.cpp:37-60 entry with CUDA tensors in and out
+    import torch
+    x, y = up(40000, 31, 3), up(30000, 31, 0)
+    a = 2.0 * up(30000, 31, 1) - 1.0
+    host = np.array(fgt.gauss_transform(x, y, a, 1e-3, ne=6))
+    ud = fgt.gauss_transform(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(),
+                             torch.from_numpy(a).cuda(), 1e-3, ne=6)
+    assert ud.is_cuda and ud.dtype == torch.float64
+    assert np.array_equal(ud.cpu().numpy(), host)
+    # same points on the device take apply_same, like the host entry
+    yd = torch.from_numpy(y).cuda()
+    us = fgt.gauss_transform(yd, yd, torch.from_numpy(a).cuda(), 1e-3, ne=6)
+    assert np.array_equal(us.cpu().numpy(), np.array(fgt.gauss_transform(y, y, a, 1e-3, ne=6)))
+    with pytest.raises(ValueError):
+        fgt.gauss_transform(yd, yd, yd[:5], 1e-3)
+
+
 def test_gpu_kernels_actually_launch():
     L = _capi.lib()
     before = L.fgt_launch_counter()
