@@ -231,6 +231,23 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
+// Segment walk of one warp: chunks of kWalkChunk consecutive segments dealt
+// round-robin over the warps (consecutive segments keep prefetch chains and
+// metadata in L1; round-robin chunks keep clustered work balanced).
+constexpr int64_t kWalkChunk = 16;
+struct WarpWalk {
+  int64_t wid, nwarps, nseg;
+  __device__ __forceinline__ int64_t first() const {
+    const int64_t s = wid * kWalkChunk;
+    return s < nseg ? s : nseg;
+  }
+  __device__ __forceinline__ int64_t next(int64_t s) const {
+    if ((s + 1) % kWalkChunk != 0 && s + 1 < nseg) return s + 1;
+    const int64_t c = (s / kWalkChunk + nwarps) * kWalkChunk;
+    return c < nseg ? c : nseg;
+  }
+};
+
 // ---------------------------------------------------------------- geometry
 
 struct SegGeom {
@@ -1009,13 +1026,11 @@ __global__ void __launch_bounds__(kThreads)
   if constexpr (!WIDE) {
     // contiguous range per warp (metadata from L1); the next narrow
     // segment's sources are loaded into registers before this one is reduced
-    const int64_t nwarps = (int64_t)gridDim.x * kSegWarps;
-    const int64_t wid = (int64_t)blockIdx.x * kSegWarps + warp;
-    const int64_t per = (a.nseg + nwarps - 1) / nwarps;
-    const int64_t S0 = wid * per;
-    const int64_t S1 = S0 + per < a.nseg ? S0 + per : a.nseg;
+    const WarpWalk walk{(int64_t)blockIdx.x * kSegWarps + warp, (int64_t)gridDim.x * kSegWarps,
+                        a.nseg};
+    const int64_t S1 = a.nseg;
     auto next_narrow = [&](int64_t s, SegGeom& g, SegFrame& f, int& DM) -> int64_t {
-      for (; s < S1; ++s) {
+      for (; s < S1; s = walk.next(s)) {
         g = seg_geom(a, s);
         f = seg_frame(g);
         DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
@@ -1027,14 +1042,14 @@ __global__ void __launch_bounds__(kThreads)
     SegFrame f;
     int DM = -1;
     double yv[kK1Per], bv[kK1Per];
-    int64_t s = next_narrow(S0, g, f, DM);
+    int64_t s = next_narrow(walk.first(), g, f, DM);
     if (s < S1) k1_load(a, g, f.zc, lane, yv, bv);
     while (s < S1) {
       SegGeom gn;
       SegFrame fn;
       int DMn = -1;
       double yn[kK1Per], bn[kK1Per];
-      const int64_t sn = next_narrow(s + 1, gn, fn, DMn);
+      const int64_t sn = next_narrow(walk.next(s), gn, fn, DMn);
       if (sn < S1) k1_load(a, gn, fn.zc, lane, yn, bn);
       if (batched && g.tid != cached_tid) {
         warp_load_table(a.mtb + g.tid, mx, ne, lane);
@@ -1295,14 +1310,12 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
     const StagePtrs sp = stage_ptrs(wreg + warp_region_bytes(ne));
     if (lane == 0) mbar_init(sp.bar);
     __syncthreads();
-    const int64_t nwarps = (int64_t)gridDim.x * kSegWarps;
-    const int64_t wid = (int64_t)blockIdx.x * kSegWarps + warp;
-    const int64_t per = (a.nseg + nwarps - 1) / nwarps;
-    const int64_t S0 = wid * per;
-    const int64_t S1 = S0 + per < a.nseg ? S0 + per : a.nseg;
+    const WarpWalk walk{(int64_t)blockIdx.x * kSegWarps + warp, (int64_t)gridDim.x * kSegWarps,
+                        a.nseg};
+    const int64_t S1 = a.nseg;
     // next narrow segment at or after s (S1 if none); issues its staging
     auto issue_next = [&](int64_t s) -> int64_t {
-      for (; s < S1; ++s) {
+      for (; s < S1; s = walk.next(s)) {
         const SegGeom g = seg_geom(a, s);
         if (k3_narrow(seg_moment_degree(P, seg_smax(a, g, P.smax), seg_frame(g))) != WIDE) {
           stage_issue(a, ts, ne, s, g, sp, lane);
@@ -1312,7 +1325,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
       return S1;
     };
     unsigned parity = 0;
-    int64_t s = issue_next(S0);
+    int64_t s = issue_next(walk.first());
     while (s < S1) {
       const SegGeom g = seg_geom(a, s);
       const SegFrame f = seg_frame(g);
@@ -1330,7 +1343,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
       lane_load_stage(a, g, sp.xy, sp.bb, sp.mask[lane >> 2], lane, r, zp, zl);
       const cplx seg_c = lane < 2 * ne ? sp.car[lane] : cplx{0.0, 0.0};
       __syncwarp();  // stage free: the next segment's copies go in now
-      const int64_t sn = issue_next(s + 1);
+      const int64_t sn = issue_next(walk.next(s));
       seg_compute<MS, WIDE>(a, P, mx, o, g, f, DM, seg_c, r, zp, zl, lane, carries, su);
       s = sn;
     }
