@@ -200,6 +200,8 @@ struct fgt_plan_s {
   int64_t ntiles = 0;  // segments of kSeg merged elements
   int64_t* d_tile_ib = nullptr;
   double2* d_seg_z = nullptr;
+  double2* d_seg_gap = nullptr;  // per segment: largest inner gap, first coordinate
+  int* d_seg_deg = nullptr;      // per segment: packed degrees (classify_kernel)
   uint32_t* d_seg_mask = nullptr;
   // batched plans (fgt_batch_create)
   bool batch = false;
@@ -311,6 +313,7 @@ StreamArgs stream_args(const fgt_plan_s* p, const double* bs) {
                 p->d_seg_z, p->d_seg_mask, p->d_seg_info, p->d_seg_jb, p->d_mtb};
   sa.nwide1 = p->nwide1;
   sa.nwide3 = p->nwide3;
+  sa.seg_deg = p->d_seg_deg;
   return sa;
 }
 
@@ -319,7 +322,8 @@ StreamArgs stream_args(const fgt_plan_s* p, const double* bs) {
 void queue_classify(fgt_plan_s* p, unsigned long long* h, cudaStream_t st,
                     bool check_flags = false) {
   const StreamArgs sa = stream_args(p, nullptr);
-  ck(launch_classify(sa, p->P, p->P.smax, check_flags ? p->d_flag : nullptr, class_counts(p), st),
+  ck(launch_classify(sa, p->P, p->P.smax, p->d_seg_gap, p->d_seg_deg,
+                     check_flags ? p->d_flag : nullptr, class_counts(p), st),
      "classify");
   ck(cudaMemcpyAsync(h, class_counts(p), 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                      st),
@@ -346,7 +350,7 @@ void plan_tiles(fgt_plan_s* p, const double* xd, const double* yd, bool check_so
   int64_t* tib = dmalloc<int64_t>(ntl + 1, st);
   ck(launch_partition(xd, p->M, yd, p->N, kPlanTile, ntl, tib, st), "partition");
   ck(launch_plan_tiles(xd, p->M, yd, p->N, tib, ntl, p->ntiles, check_sorted ? 1 : 0,
-                       p->d_tile_ib, p->d_seg_z, p->d_seg_mask, p->d_flag, st),
+                       p->d_tile_ib, p->d_seg_z, p->d_seg_mask, p->d_seg_gap, p->d_flag, st),
      "plan tiles");
   dfree(tib, st);
 }
@@ -374,6 +378,8 @@ void destroy_plan(fgt_plan_s* p) {
   dfree(p->d_sperm, st);
   dfree(p->d_tile_ib, st);
   dfree(p->d_seg_z, st);
+  dfree(p->d_seg_gap, st);
+  dfree(p->d_seg_deg, st);
   dfree(p->d_seg_mask, st);
   dfree(p->d_seg_jb, st);
   dfree(p->d_seg_info, st);
@@ -629,6 +635,8 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       p->ntiles = (L + kSeg - 1) / kSeg;
       p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
       p->d_seg_z = dmalloc<double2>(p->ntiles, st);
+      p->d_seg_gap = dmalloc<double2>(p->ntiles, st);
+      p->d_seg_deg = dmalloc<int>(p->ntiles, st);
       p->d_seg_mask = dmalloc<uint32_t>((size_t)p->ntiles * (kSeg / 32), st);
       // one read of both sets: checks + (speculative) segment metadata
       plan_tiles(p, xs.dptr, ys.dptr, !(flags & FGT_ASSUME_SORTED), st);
@@ -985,6 +993,8 @@ extern "C" int fgt_batch_create(int B, const double* targets, const int64_t* t_o
       p->d_seg_jb = dmalloc<int64_t>(nseg + 1, st);
       p->d_seg_info = dmalloc<int4>(nseg + 1, st);
       p->d_seg_z = dmalloc<double2>(nseg + 1, st);
+      p->d_seg_gap = dmalloc<double2>(nseg + 1, st);
+      p->d_seg_deg = dmalloc<int>(nseg + 1, st);
       p->d_seg_mask = dmalloc<uint32_t>((size_t)(nseg + 1) * (kSeg / 32), st);
       Work w{st, {}};
       int64_t* d_toff = w.get<int64_t>(B + 1);
@@ -1001,7 +1011,7 @@ extern "C" int fgt_batch_create(int B, const double* targets, const int64_t* t_o
         ck(cudaMemcpyAsync(d_ttid, tile_tid.data(), 4 * ntl, cudaMemcpyHostToDevice, st), "tile map");
       ck(launch_batch_plan(xs.dptr, ys.dptr, d_toff, d_soff, d_sbase, d_tbase, d_ttid, B, ntl,
                            d_tib, p->d_tile_ib, p->d_seg_jb, p->d_seg_info, p->d_seg_z,
-                           p->d_seg_mask, p->d_flag, st),
+                           p->d_seg_mask, p->d_seg_gap, p->d_flag, st),
          "batch plan");
       int hf[8] = {0};
       ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(hf), cudaMemcpyDeviceToHost, st), "flags");

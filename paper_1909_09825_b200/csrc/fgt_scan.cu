@@ -923,6 +923,9 @@ constexpr int kLaneMomMax = FGT_LANE_MOM_MAX;
 __device__ __forceinline__ bool k1_narrow(int DM) { return DM >= 0 && DM <= kRegDeg; }
 __device__ __forceinline__ bool k3_narrow(int DM) { return DM >= 0 && DM <= kK3Moments; }
 
+__device__ __forceinline__ int seg_deg_D(int deg) { return (deg & 0xff) - 1; }
+__device__ __forceinline__ int seg_deg_DM(int deg) { return ((deg >> 8) & 0xff) - 1; }
+
 __device__ __forceinline__ double seg_smax(const StreamArgs& a, const SegGeom& g, double smax) {
   return a.mtb ? __ldg(&a.mtb[g.tid].smax) : smax;
 }
@@ -1031,10 +1034,12 @@ __global__ void __launch_bounds__(kThreads)
     const int64_t S1 = a.nseg;
     auto next_narrow = [&](int64_t s, SegGeom& g, SegFrame& f, int& DM) -> int64_t {
       for (; s < S1; s = walk.next(s)) {
-        g = seg_geom(a, s);
-        f = seg_frame(g);
-        DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
-        if (k1_narrow(DM)) return s;
+        DM = seg_deg_DM(__ldg(a.seg_deg + s));
+        if (k1_narrow(DM)) {
+          g = seg_geom(a, s);
+          f = seg_frame(g);
+          return s;
+        }
       }
       return S1;
     };
@@ -1083,10 +1088,9 @@ __global__ void __launch_bounds__(kThreads)
          s0 += (int64_t)gridDim.x * kSegWarps * Gs) {
       const int64_t s1 = s0 + Gs < a.nseg ? s0 + Gs : a.nseg;
       for (int64_t s = s0; s < s1; ++s) {
+        const int deg = __ldg(a.seg_deg + s);
+        if (k1_narrow(seg_deg_DM(deg))) continue;
         const SegGeom g = seg_geom(a, s);
-        const SegFrame f = seg_frame(g);
-        const int DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
-        if (k1_narrow(DM)) continue;
         if (batched && g.tid != cached_tid) {
           warp_load_table(a.mtb + g.tid, mx, ne, lane);
           cached_tid = g.tid;
@@ -1108,10 +1112,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
         r.g[0] -= zp;
-        double gmax = r.g[0];
-#pragma unroll
-        for (int e = 1; e < kR; ++e) gmax = fmax(gmax, r.g[e]);
-        seg_aggregate_wide(mx, ne, pick_degree(P, mx.smax, warp_max(gmax)), lane, r, a.nseg, s, ts);
+        seg_aggregate_wide(mx, ne, seg_deg_D(deg), lane, r, a.nseg, s, ts);
       }
     }
   }
@@ -1154,6 +1155,7 @@ __global__ void batch_modes_kernel(BatchModeBase base, const double* __restrict_
 
 // Plan-time segment classes: counts[0] = K1 wide segments, counts[1] = K3.
 __global__ void classify_kernel(StreamArgs a, ModeParams P, double smax,
+                                const double2* __restrict__ seg_gap, int* __restrict__ seg_deg,
                                 const int* __restrict__ skip_flags,
                                 unsigned long long* __restrict__ counts) {
   // metadata of a rejected batch (non-finite / unsorted) is not valid
@@ -1166,7 +1168,13 @@ __global__ void classify_kernel(StreamArgs a, ModeParams P, double smax,
     bool w1 = false, w3 = false;
     if (s < a.nseg) {
       const SegGeom g = seg_geom(a, s);
-      const int DM = seg_moment_degree(P, seg_smax(a, g, smax), seg_frame(g));
+      const double sm = seg_smax(a, g, smax);
+      const int DM = seg_moment_degree(P, sm, seg_frame(g));
+      // the gap factors' degree: largest gap of the segment including the
+      // one from the element before it (as the kernels' lane runs see them)
+      const double2 gz = seg_gap[s];
+      const int D = pick_degree(P, sm, fmax(gz.x, gz.y - g.zprev));
+      seg_deg[s] = (D + 1) | ((DM + 1) << 8);
       w1 = !k1_narrow(DM);
       w3 = !k3_narrow(DM);
     }
@@ -1196,15 +1204,10 @@ __device__ unsigned long long g_phase_cycles[8];
 template <bool MS, bool WIDE>
 __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParams& P,
                                             const ModeTable& mx, const OutArgs& o,
-                                            const SegGeom& g, const SegFrame& f, int DM,
+                                            const SegGeom& g, const SegFrame& f, int D, int DM,
                                             cplx seg_c, LaneRun& r, double zp, double zl,
                                             int lane, Carry* carries, double* su) {
   const int ne = P.ne;
-  // gaps (coordinates are still needed by the moment path)
-  double gmax = r.g[0] - zp;
-#pragma unroll
-  for (int e = 1; e < kR; ++e) gmax = fmax(gmax, r.g[e] - r.g[e - 1]);
-  const int D = pick_degree(P, mx.smax, warp_max(gmax));
   Carry* mine = carries + lane * ne;
   if constexpr (!WIDE) {
     switch (DM) {
@@ -1317,7 +1320,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
     auto issue_next = [&](int64_t s) -> int64_t {
       for (; s < S1; s = walk.next(s)) {
         const SegGeom g = seg_geom(a, s);
-        if (k3_narrow(seg_moment_degree(P, seg_smax(a, g, P.smax), seg_frame(g))) != WIDE) {
+        if (k3_narrow(seg_deg_DM(__ldg(a.seg_deg + s))) != WIDE) {
           stage_issue(a, ts, ne, s, g, sp, lane);
           return s;
         }
@@ -1329,7 +1332,8 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
     while (s < S1) {
       const SegGeom g = seg_geom(a, s);
       const SegFrame f = seg_frame(g);
-      const int DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
+      const int deg = __ldg(a.seg_deg + s);
+      const int D = seg_deg_D(deg), DM = seg_deg_DM(deg);
       if (batched && g.tid != cached_tid) {
         warp_load_table(a.mtb + g.tid, mx, ne, lane);
         cached_tid = g.tid;
@@ -1344,7 +1348,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
       const cplx seg_c = lane < 2 * ne ? sp.car[lane] : cplx{0.0, 0.0};
       __syncwarp();  // stage free: the next segment's copies go in now
       const int64_t sn = issue_next(walk.next(s));
-      seg_compute<MS, WIDE>(a, P, mx, o, g, f, DM, seg_c, r, zp, zl, lane, carries, su);
+      seg_compute<MS, WIDE>(a, P, mx, o, g, f, D, DM, seg_c, r, zp, zl, lane, carries, su);
       s = sn;
     }
   } else {
@@ -1356,10 +1360,11 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
          s0 += (int64_t)gridDim.x * kSegWarps * G) {
       const int64_t s1 = s0 + G < a.nseg ? s0 + G : a.nseg;
       for (int64_t s = s0; s < s1; ++s) {
+        const int deg = __ldg(a.seg_deg + s);
+        const int D = seg_deg_D(deg), DM = seg_deg_DM(deg);
+        if (k3_narrow(DM) == WIDE) continue;
         const SegGeom g = seg_geom(a, s);
         const SegFrame f = seg_frame(g);
-        const int DM = seg_moment_degree(P, seg_smax(a, g, P.smax), f);
-        if (k3_narrow(DM) == WIDE) continue;
         if (batched && g.tid != cached_tid) {
           warp_load_table(a.mtb + g.tid, mx, ne, lane);
           cached_tid = g.tid;
@@ -1368,7 +1373,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
         LaneRun r;
         double zp, zl;
         lane_load(a, g, s, lane, r, zp, zl);
-        seg_compute<MS, WIDE>(a, P, mx, o, g, f, DM, seg_c, r, zp, zl, lane, carries, su);
+        seg_compute<MS, WIDE>(a, P, mx, o, g, f, D, DM, seg_c, r, zp, zl, lane, carries, su);
       }
     }
   }
@@ -1455,6 +1460,7 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
                                                int4* __restrict__ seg_info,
                                                double2* __restrict__ seg_z,
                                                uint32_t* __restrict__ seg_mask,
+                                               double2* __restrict__ seg_gap,
                                                int* __restrict__ flags) {
   extern __shared__ __align__(16) double tsm[];
   __shared__ int sib[kPlanSegs + 1];
@@ -1520,19 +1526,28 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
       f2 |= !(sx[i] == yv);
     }
   }
-  // merge: thread t owns merged positions [16 t, 16 t + 16) of the tile
+  // merge: thread t owns merged positions [16 t, 16 t + 16) of the tile; it
+  // also tracks the largest gap between consecutive elements of its window
+  // (the gap into a segment's first element is left to classify_kernel)
   const int d0 = t * kPlanPer;
   unsigned bits = 0u;
+  double gmx = 0.0, zfirst = 0.0;
   if (d0 < len) {
     int i = merge_path_smem(sx, nx, sy, ny, d0);
     int j = d0 - i;
     if ((d0 % kSeg) == 0) sib[d0 / kSeg] = i;
     double cx = sx[i < nx ? i : nx];
     double cy = sy[j < ny ? j : ny];
+    double zp = fmax(i > 0 ? sx[i - 1] : -INFINITY, j > 0 ? sy[j - 1] : -INFINITY);
+    const bool seg_start = (d0 % kSeg) == 0;
 #pragma unroll
     for (int e = 0; e < kPlanPer; ++e) {
       if (d0 + e < len) {
         const bool tgt = !(cy <= cx);  // sources first on ties
+        const double z = tgt ? cx : cy;
+        if (e > 0 || !seg_start) gmx = fmax(gmx, z - zp);
+        if (e == 0) zfirst = z;
+        zp = z;
         bits |= (unsigned)tgt << e;
         if (tgt) {
           ++i;
@@ -1544,6 +1559,10 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
       }
     }
   }
+  // per segment (16 threads = half a warp): largest gap, first coordinate
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) gmx = fmax(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
+  if ((d0 % kSeg) == 0 && d0 < len) seg_gap[c.seg0 + d0 / kSeg] = make_double2(gmx, zfirst);
   const int nsegs_tile = (len + kSeg - 1) / kSeg;
   if (t == 0) sib[nsegs_tile] = nx;
   // mask: two threads per 32-bit word, same layout as bit (merged pos % 32)
@@ -1591,7 +1610,8 @@ __global__ void __launch_bounds__(256)
     plan_tile_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
                      int64_t N, const int64_t* __restrict__ tile_ib, int64_t nseg,
                      int check_sorted, int64_t* __restrict__ seg_ib, double2* __restrict__ seg_z,
-                     uint32_t* __restrict__ seg_mask, int* __restrict__ flags) {
+                     uint32_t* __restrict__ seg_mask, double2* __restrict__ seg_gap,
+                     int* __restrict__ flags) {
   const int64_t t = blockIdx.x;
   const int64_t L = M + N;
   TileCtx c;
@@ -1606,7 +1626,8 @@ __global__ void __launch_bounds__(256)
   c.seg0 = t * kPlanSegs;
   c.xoff = c.yoff = 0;
   c.tid = 0;
-  plan_tile_body<false>(c, check_sorted, nseg, seg_ib, nullptr, nullptr, seg_z, seg_mask, flags);
+  plan_tile_body<false>(c, check_sorted, nseg, seg_ib, nullptr, nullptr, seg_z, seg_mask, seg_gap,
+                        flags);
 }
 
 struct BatchArgs {
@@ -1652,9 +1673,10 @@ __global__ void __launch_bounds__(256)
     batch_plan_tile_kernel(BatchArgs b, const int64_t* __restrict__ tile_ib,
                            int64_t* __restrict__ seg_ib, int64_t* __restrict__ seg_jb,
                            int4* __restrict__ seg_info, double2* __restrict__ seg_z,
-                           uint32_t* __restrict__ seg_mask, int* __restrict__ flags) {
+                           uint32_t* __restrict__ seg_mask, double2* __restrict__ seg_gap,
+                           int* __restrict__ flags) {
   const TileCtx c = batch_ctx(b, blockIdx.x, tile_ib);
-  plan_tile_body<true>(c, 1, 0, seg_ib, seg_jb, seg_info, seg_z, seg_mask, flags);
+  plan_tile_body<true>(c, 1, 0, seg_ib, seg_jb, seg_info, seg_z, seg_mask, seg_gap, flags);
 }
 
 // ------------------------------------------------------------------- K2
@@ -1871,7 +1893,7 @@ cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int6
 cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int64_t N,
                               const int64_t* tile_ib, int64_t ntiles, int64_t nseg,
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
-                              uint32_t* seg_mask, int* flags, cudaStream_t st) {
+                              uint32_t* seg_mask, double2* seg_gap, int* flags, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
   const size_t smem = sizeof(double) * 2 * (kPlanTile + 2);  // + head slot, sentinel
   static bool done = false;
@@ -1883,7 +1905,7 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
   }
   note_launch();
   plan_tile_kernel<<<(unsigned)ntiles, 256, smem, st>>>(xs, M, ys, N, tile_ib, nseg, check_sorted,
-                                                         seg_ib, seg_z, seg_mask, flags);
+                                                         seg_ib, seg_z, seg_mask, seg_gap, flags);
   return cudaGetLastError();
 }
 
@@ -1891,8 +1913,8 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
                               const int64_t* s_off, const int64_t* seg_base,
                               const int64_t* tile_base, const int32_t* tile_tid, int B,
                               int64_t ntiles, int64_t* tile_ib, int64_t* seg_ib, int64_t* seg_jb,
-                              int4* seg_info, double2* seg_z, uint32_t* seg_mask, int* flags,
-                              cudaStream_t st) {
+                              int4* seg_info, double2* seg_z, uint32_t* seg_mask,
+                              double2* seg_gap, int* flags, cudaStream_t st) {
   (void)B;
   if (ntiles == 0) return cudaSuccess;
   const BatchArgs b{xs, ys, t_off, s_off, seg_base, tile_base, tile_tid};
@@ -1907,7 +1929,7 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
     done = true;
   }
   batch_plan_tile_kernel<<<(unsigned)ntiles, 256, smem, st>>>(b, tile_ib, seg_ib, seg_jb, seg_info,
-                                                              seg_z, seg_mask, flags);
+                                                              seg_z, seg_mask, seg_gap, flags);
   return cudaGetLastError();
 }
 
@@ -1947,14 +1969,15 @@ cudaError_t launch_batch_modes(const BatchModeBase& base, const double* deltas, 
 }
 
 cudaError_t launch_classify(const StreamArgs& a, const ModeParams& P, double smax,
-                            const int* skip_flags, unsigned long long* counts, cudaStream_t st) {
+                            const double2* seg_gap, int* seg_deg, const int* skip_flags,
+                            unsigned long long* counts, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), st);
   if (e != cudaSuccess || a.nseg == 0) return e;
   const int64_t want = (a.nseg + 255) / 256;
   const int64_t cap = (int64_t)num_sms() * 8;
   note_launch();
-  classify_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(a, P, smax, skip_flags,
-                                                                       counts);
+  classify_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(a, P, smax, seg_gap, seg_deg,
+                                                                       skip_flags, counts);
   return cudaGetLastError();
 }
 

@@ -53,6 +53,9 @@ struct StreamArgs {
   // plan-time segment classes (classify_segments): segments too wide for the
   // moment form of K1 / K3; -1 = unknown (both kernel variants run)
   int64_t nwide1 = -1, nwide3 = -1;
+  // plan-time degrees per segment: (D + 1) | (DM + 1) << 8 with D the Taylor
+  // degree of its gap factors and DM its moment degree (-1 = none)
+  const int* seg_deg = nullptr;
 };
 
 struct OutArgs {
@@ -86,10 +89,11 @@ cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int6
 // x non-finite, y non-finite, x != y when M == N, x unsorted, y unsorted;
 // zeroed by the caller) and segment metadata seg_ib / seg_z / seg_mask.
 // tile_ib: launch_partition output at kPlanTile granularity.
+// seg_gap: per segment (largest gap between its elements, its first coordinate).
 cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int64_t N,
                               const int64_t* tile_ib, int64_t ntiles, int64_t nseg,
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
-                              uint32_t* seg_mask, int* flags, cudaStream_t st);
+                              uint32_t* seg_mask, double2* seg_gap, int* flags, cudaStream_t st);
 // Batched plans: per-transform offsets (B+1 each, concatenated arrays) and
 // the first global segment of each transform (B+1).  Partition at
 // kPlanTile granularity inside each transform, then the tile pass writes the
@@ -100,8 +104,8 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
                               const int64_t* s_off, const int64_t* seg_base,
                               const int64_t* tile_base, const int32_t* tile_tid, int B,
                               int64_t ntiles, int64_t* tile_ib, int64_t* seg_ib, int64_t* seg_jb,
-                              int4* seg_info, double2* seg_z, uint32_t* seg_mask, int* flags,
-                              cudaStream_t st);
+                              int4* seg_info, double2* seg_z, uint32_t* seg_mask,
+                              double2* seg_gap, int* flags, cudaStream_t st);
 // Per-transform mode tables of a batched plan, built on the device:
 // s_k = t_k / sqrt(delta_b), mw_k, Taylor coefficients of exp(-s g)
 // (c_0 = 1 and c_1 = -s exact), smax.  deltas: device array of B.
@@ -115,8 +119,10 @@ cudaError_t launch_batch_modes(const BatchModeBase& base, const double* deltas, 
 // Plan-time classification: counts[0] / counts[1] = segments that K1 / K3
 // process on their wide (per-element) path.  smax: the single plan's
 // max |s_k| (batched plans read their tables).
+// Also writes seg_deg (see StreamArgs) from seg_gap and the segment frames.
 cudaError_t launch_classify(const StreamArgs& a, const ModeParams& P, double smax,
-                            const int* skip_flags, unsigned long long* counts, cudaStream_t st);
+                            const double2* seg_gap, int* seg_deg, const int* skip_flags,
+                            unsigned long long* counts, cudaStream_t st);
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, cudaStream_t st);
 // K2: exclusive carries per segment.  carry_in: 2*ne complex (forward carry at
