@@ -336,25 +336,25 @@ __device__ __forceinline__ void lane_load(const StreamArgs& a, const SegGeom& g,
   const int j0 = (d0 < g.len ? d0 : g.len) - i0;
   r.tfirst = i0;
   r.tmask = byte;
-  double last = 0.0;
+  // element e of the run is target number popc(byte & (2^e - 1)) or source
+  // number e - that; branch-free address select, predicated loads
+  const double* px = a.xs + g.ib + i0;
+  const double* py = a.ys + g.jb + j0;
+  const double* pb = a.bs + g.jb + j0;
+  int t = 0;
 #pragma unroll
   for (int e = 0; e < kR; ++e) {
-    const int t = __popc(byte & ((1u << e) - 1u));
-    const int sidx = e - t;
-    if (e < nreal) {
-      if (byte & (1u << e)) {
-        r.g[e] = __ldg(a.xs + g.ib + i0 + t);
-        r.b[e] = 0.0;
-      } else {
-        r.g[e] = __ldg(a.ys + g.jb + j0 + sidx);
-        r.b[e] = __ldg(a.bs + g.jb + j0 + sidx);
-      }
-      last = r.g[e];
-    } else {
-      r.g[e] = 0.0;
-      r.b[e] = 0.0;
-    }
+    const bool tg = (byte >> e) & 1u;
+    const bool real = e < nreal;
+    const double* pz = tg ? px + t : py + (e - t);
+    r.g[e] = real ? __ldg(pz) : 0.0;
+    r.b[e] = (real && !tg) ? __ldg(pb + (e - t)) : 0.0;
+    t += tg;
   }
+  double last = 0.0;
+#pragma unroll
+  for (int e = 0; e < kR; ++e)
+    if (e < nreal) last = r.g[e];
   double prev = __shfl_up_sync(0xffffffffu, last, 1);
   if (lane == 0) prev = g.zprev;
   zp = prev;
@@ -1250,9 +1250,19 @@ __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParam
     __syncwarp();
     const int64_t base = o.u_offset + g.ib;
     if (o.tperm) {
-      for (int i = lane; i < g.nx; i += 32) o.u[o.tperm[base + i]] = su[i];
+      const int32_t* tp = o.tperm + base;
+#pragma unroll
+      for (int q = 0; q < kSeg / 32; ++q) {
+        const int i = lane + 32 * q;
+        if (i < g.nx) o.u[tp[i]] = su[i];
+      }
     } else {
-      for (int i = lane; i < g.nx; i += 32) o.u[base + i] = su[i];
+      double* up = o.u + base;
+#pragma unroll
+      for (int q = 0; q < kSeg / 32; ++q) {
+        const int i = lane + 32 * q;
+        if (i < g.nx) up[i] = su[i];
+      }
     }
   }
   __syncwarp();
