@@ -1425,8 +1425,8 @@ struct TileCtx {
   int tid;
 };
 
-constexpr int kPlanThreads = 256;
-constexpr int kPlanPer = kPlanTile / kPlanThreads;  // merged positions per thread
+constexpr int kPlanPer = 16;                         // merged positions per thread
+constexpr int kPlanThreads = kPlanTile / kPlanPer;
 static_assert(kPlanPer == 16 && kSeg % kPlanPer == 0, "plan tile layout");
 
 // Staging plan of n values g[0..n) into a shared buffer: the 16-byte aligned
@@ -1616,7 +1616,7 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
   }
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kPlanThreads)
     plan_tile_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
                      int64_t N, const int64_t* __restrict__ tile_ib, int64_t nseg,
                      int check_sorted, int64_t* __restrict__ seg_ib, double2* __restrict__ seg_z,
@@ -1679,7 +1679,7 @@ __global__ void batch_partition_kernel(BatchArgs b, int64_t ntiles, int64_t* __r
   tile_ib[gt] = merge_path(c.x, c.M, c.y, c.N, c.d0);
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kPlanThreads)
     batch_plan_tile_kernel(BatchArgs b, const int64_t* __restrict__ tile_ib,
                            int64_t* __restrict__ seg_ib, int64_t* __restrict__ seg_jb,
                            int4* __restrict__ seg_info, double2* __restrict__ seg_z,
@@ -1914,7 +1914,7 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
     done = true;
   }
   note_launch();
-  plan_tile_kernel<<<(unsigned)ntiles, 256, smem, st>>>(xs, M, ys, N, tile_ib, nseg, check_sorted,
+  plan_tile_kernel<<<(unsigned)ntiles, kPlanThreads, smem, st>>>(xs, M, ys, N, tile_ib, nseg, check_sorted,
                                                          seg_ib, seg_z, seg_mask, seg_gap, flags);
   return cudaGetLastError();
 }
@@ -1938,7 +1938,7 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
     if (e != cudaSuccess) return e;
     done = true;
   }
-  batch_plan_tile_kernel<<<(unsigned)ntiles, 256, smem, st>>>(b, tile_ib, seg_ib, seg_jb, seg_info,
+  batch_plan_tile_kernel<<<(unsigned)ntiles, kPlanThreads, smem, st>>>(b, tile_ib, seg_ib, seg_jb, seg_info,
                                                               seg_z, seg_mask, seg_gap, flags);
   return cudaGetLastError();
 }

@@ -18,7 +18,10 @@ constexpr int kSeg = 32 * kR;           // merged elements per segment (one warp
 constexpr int kSegWarps = 4;            // segments (warps) per CTA in K1 / K3
 constexpr int kThreads = 32 * kSegWarps;
 constexpr int kMaxMom = kMaxDeg;        // highest moment order of the expansions
-constexpr int kPlanSegs = 16;           // segments per plan tile
+#ifndef FGT_PLAN_SEGS
+#define FGT_PLAN_SEGS 16
+#endif
+constexpr int kPlanSegs = FGT_PLAN_SEGS;  // segments per plan tile
 constexpr int kPlanTile = kPlanSegs * kSeg;  // merged elements per plan tile
 
 // Per-mode constants laid out in device memory (plan-owned): s_k, mw_k and the
