@@ -152,16 +152,43 @@ def run_reference(args):
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
+    """SM clock and throttle reasons sampled DURING the timed region: NVML
+    polled every 2 ms (pynvml), nvidia-smi -lms as the fallback."""
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
 
-    def __init__(self, index):
+    def __init__(self, index, pci_bus_id=None):
         self.index = index
+        self.pci = pci_bus_id
         self.proc = None
         self.lines = []
+        self.nv = None
+        self.samples = []
+        self.stop_flag = threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        if self.pci:
+            try:
+                return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(self.pci)
+            except Exception:
+                pass
+        return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
 
     def start(self):
+        try:
+            self.nv, self.h = self._nvml_handle()
+            self.max_mhz = float(self.nv.nvmlDeviceGetMaxClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -172,11 +199,41 @@ class ClockSampler:
         except (OSError, FileNotFoundError):
             self.proc = None
 
+    def _poll(self):
+        nv, h = self.nv, self.h
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop_flag.is_set():
+            try:
+                self.samples.append((time.perf_counter(),
+                                     float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                     int(get_reasons(h))))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
-    def stop(self):
+    def stop(self, window=None):
+        """window: (t0, t1) perf_counter bounds of the timed region; NVML
+        samples outside it are dropped."""
+        if self.nv is not None:
+            self.stop_flag.set()
+            self.thread.join(timeout=2)
+            smp = self.samples
+            if window is not None:
+                inside = [x for x in smp if window[0] <= x[0] <= window[1]]
+                smp = inside or smp[-1:]
+            reasons = set()
+            for _, _, bits in smp:
+                for b, nm in self.REASONS.items():
+                    if bits & b:
+                        reasons.add(nm)
+            sm = [c for _, c, _ in smp]
+            return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": self.max_mhz,
+                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -199,7 +256,7 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
 # ------------------------------------------------------------------ main arm
@@ -333,13 +390,20 @@ def main():
         one_step(args.delta)
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local)
+    try:
+        pr = torch.cuda.get_device_properties(dev)
+        pci = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+    except Exception:
+        pci = None
+    clocks = ClockSampler(local, pci)
     clocks.start()
     time.sleep(0.3)
     launches0 = L.fgt_launch_counter()
+    tw0 = time.perf_counter()
     ms = timed(args.steps, args.delta)
+    tw1 = time.perf_counter()
     launches = L.fgt_launch_counter() - launches0
-    clk = clocks.stop()
+    clk = clocks.stop((tw0, tw1))
     value = 2.0 * n / (ms / 1e3)
 
     # ---- per-kernel durations (CUDA events on the launching stream)
