@@ -19,7 +19,10 @@ namespace {
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kItems = 8;                                   // keys per lane per tile
+#ifndef FGT_SORT_ITEMS
+#define FGT_SORT_ITEMS 12
+#endif
+constexpr int kItems = FGT_SORT_ITEMS;                      // keys per lane per tile
 constexpr int kSortTile = kSortThreads * kItems;            // 2048 keys per CTA
 constexpr int kRadix = 256;
 
@@ -88,6 +91,8 @@ __global__ void __launch_bounds__(kSortThreads)
   cnt[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
+constexpr size_t kScatterSmem = (sizeof(uint64_t) + sizeof(uint32_t)) * kSortTile;
+
 // Stable scatter.  Warp w owns tile keys [w*256, (w+1)*256) and ranks them in
 // order with __match_any_sync; warp counters are scanned digit-wise across
 // warps, keys are staged digit-sorted in shared memory and written out in
@@ -99,8 +104,9 @@ __global__ void __launch_bounds__(kSortThreads)
   __shared__ unsigned int wc[kSortWarps][kRadix];
   __shared__ unsigned int loff[kRadix];
   __shared__ unsigned int goff[kRadix];
-  __shared__ uint64_t sk[kSortTile];
-  __shared__ uint32_t sv[kSortTile];
+  extern __shared__ __align__(16) unsigned char sort_dyn[];  // staging (kScatterSmem)
+  uint64_t* sk = reinterpret_cast<uint64_t*>(sort_dyn);
+  uint32_t* sv = reinterpret_cast<uint32_t*>(sk + kSortTile);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&wc[0][0])[i] = 0;
   goff[threadIdx.x] = offs[(int64_t)threadIdx.x * ntiles + blockIdx.x];
@@ -414,8 +420,15 @@ cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int
     tile_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, n, shift, cnt, ntiles);
     e = excl_scan_u32(cnt, ntiles * kRadix, offs, stmp, st);
     if (e != cudaSuccess) return e;
-    scatter_kernel<<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, vin, n, shift, offs, ntiles,
-                                                              kout, vout);
+    static bool smem_set = false;
+    if (!smem_set) {
+      e = cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kScatterSmem);
+      if (e != cudaSuccess) return e;
+      smem_set = true;
+    }
+    scatter_kernel<<<(unsigned)ntiles, kSortThreads, kScatterSmem, st>>>(kin, vin, n, shift, offs,
+                                                                         ntiles, kout, vout);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     uint64_t* tk = kin; kin = kout; kout = tk;
