@@ -1850,11 +1850,29 @@ __global__ void __launch_bounds__(kScanThreads) scan_down_kernel(ScanArgs sa) {
   }
 }
 
+// out[i] = alpha[perm[i]]: random reads; kGatherILP independent gathers per
+// thread in flight (coalesced index loads first, then the data loads).
+constexpr int kGatherILP = 8;
 __global__ void gather_kernel(const double* __restrict__ alpha, const int32_t* __restrict__ perm,
                               int64_t n, double* __restrict__ out) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (; i < n; i += stride) out[i] = __ldg(alpha + perm[i]);
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n;
+       i0 += stride * kGatherILP) {
+    int32_t p[kGatherILP];
+#pragma unroll
+    for (int u = 0; u < kGatherILP; ++u) {
+      const int64_t i = i0 + u * stride;
+      p[u] = i < n ? __ldg(perm + i) : 0;
+    }
+    double v[kGatherILP];
+#pragma unroll
+    for (int u = 0; u < kGatherILP; ++u) v[u] = __ldg(alpha + p[u]);
+#pragma unroll
+    for (int u = 0; u < kGatherILP; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n) out[i] = v[u];
+    }
+  }
 }
 
 }  // namespace
