@@ -259,6 +259,28 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
+def link_bandwidth(dev, stream, nbytes=512 << 20, reps=3):
+    """Pinned host <-> device copy bandwidth (GB/s), best of reps, CUDA events."""
+    import torch
+    h = torch.empty(nbytes // 8, dtype=torch.float64, pin_memory=True)
+    d = torch.empty(nbytes // 8, dtype=torch.float64, device=dev)
+    out = {}
+    for name, (dst, src) in (("h2d_gbs", (d, h)), ("d2h_gbs", (h, d))):
+        best = None
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dst.copy_(src, non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        out[name] = nbytes / (best / 1e3) / 1e9
+    del h, d
+    return out
+
+
 # ------------------------------------------------------------------ main arm
 
 def merge_split(x, y, diag):
@@ -502,6 +524,12 @@ def main():
         e2e = {"value": 2.0 * n / es, "unit": UNIT, "ms_per_step": es * 1e3,
                "h2d_bytes_per_step": int(8 * (Mc + 2 * Nc)) * world,
                "d2h_bytes_per_step": int(8 * Mc) * world, "matches_device_path": same}
+        # the host link bounds e2e: measured pinned copy bandwidth per direction,
+        # floor = this rank's h2d / BW_h2d + d2h / BW_d2h (the API is synchronous)
+        bw = link_bandwidth(dev, stream)
+        floor = 8 * (Mc + 2 * Nc) / bw["h2d_gbs"] / 1e9 + 8 * Mc / bw["d2h_gbs"] / 1e9
+        e2e["link"] = {**bw, "floor_ms": floor * 1e3, "frac": floor / es,
+                       "note": "e2e time vs the sequential host-link floor of its own bytes"}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
