@@ -543,6 +543,14 @@ def main():
                           f"{r['t_sort']:.3f}/{r['t_pre']:.3f}/{r['t_rem']:.3f} s"),
                "cpu": cpu_info(), "nproc": os.cpu_count()}
 
+    # DRAM traffic of one apply from the committed ncu --set full capture
+    # (dram__bytes_read.sum + dram__bytes_write.sum over its launches)
+    traffic = {}
+    tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    if n == int(1e8) and world == 1 and os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -556,7 +564,8 @@ def main():
                        "l2": "inputs (3.2 GB) >> 126 MB L2; no flush needed"},
             "roofline": {"bound": "fp64", "achieved": achieved_fp64, "peak": peak.value,
                          "unit": "TFLOP/s", "frac": (achieved_fp64 / peak.value) if achieved_fp64 else None,
-                         "traffic": None,
+                         "traffic": traffic.get("dram_bytes_per_apply"),
+                         "traffic_source": traffic.get("source"),
                          "kernel": "apply = K1 tile aggregates + K2 carry scan + K3 main pass",
                          "work": f"SURVEY 8(d) W = n_e(48 + 4M/(M+N)) = {W:.0f} fp64-pipe instr/pt, "
                                  "counted as FMA-2 flops",
