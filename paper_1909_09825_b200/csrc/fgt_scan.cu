@@ -1946,13 +1946,9 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
                               uint32_t* seg_mask, double2* seg_gap, int* flags, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
   const size_t smem = sizeof(double) * 2 * (kPlanTile + 2);  // + head slot, sentinel
-  static bool done = false;
-  if (!done) {
-    cudaError_t e = cudaFuncSetAttribute(plan_tile_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    done = true;
-  }
+  static std::atomic<unsigned long long> done{0};
+  cudaError_t e = ensure_dynamic_smem(plan_tile_kernel, (int)smem, done);
+  if (e != cudaSuccess) return e;
   note_launch();
   plan_tile_kernel<<<(unsigned)ntiles, kPlanThreads, smem, st>>>(xs, M, ys, N, tile_ib, nseg, check_sorted,
                                                          seg_ib, seg_z, seg_mask, seg_gap, flags);
@@ -1971,25 +1967,17 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
   note_launch(2);
   batch_partition_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(b, ntiles, tile_ib);
   const size_t smem = sizeof(double) * 2 * (kPlanTile + 2);  // + head slot, sentinel
-  static bool done = false;
-  if (!done) {
-    cudaError_t e = cudaFuncSetAttribute(batch_plan_tile_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    done = true;
-  }
+  static std::atomic<unsigned long long> done{0};
+  cudaError_t e = ensure_dynamic_smem(batch_plan_tile_kernel, (int)smem, done);
+  if (e != cudaSuccess) return e;
   batch_plan_tile_kernel<<<(unsigned)ntiles, kPlanThreads, smem, st>>>(b, tile_ib, seg_ib, seg_jb, seg_info,
                                                               seg_z, seg_mask, seg_gap, flags);
   return cudaGetLastError();
 }
 
 template <class K>
-static cudaError_t set_smem(K kernel, bool& done) {
-  if (done) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)seg_smem_bytes(kMaxModes, true, true));
-  if (e == cudaSuccess) done = true;
-  return e;
+static cudaError_t set_smem(K kernel, std::atomic<unsigned long long>& done) {
+  return ensure_dynamic_smem(kernel, (int)seg_smem_bytes(kMaxModes, true, true), done);
 }
 
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
@@ -2035,7 +2023,7 @@ template <bool MS, bool WIDE>
 static cudaError_t launch_seg_main_variant(const StreamArgs& a, const ModeParams& P,
                                            const ModeTable* mt, TileState ts, OutArgs o,
                                            cudaStream_t st) {
-  static bool done = false;
+  static std::atomic<unsigned long long> done{0};
   cudaError_t e = set_smem(seg_main_kernel<MS, WIDE>, done);
   if (e != cudaSuccess) return e;
   const size_t smem = seg_smem_bytes(P.ne, a.mtb != nullptr, k3_stream<WIDE>());

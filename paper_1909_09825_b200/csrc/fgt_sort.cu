@@ -420,13 +420,9 @@ cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int
     tile_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, n, shift, cnt, ntiles);
     e = excl_scan_u32(cnt, ntiles * kRadix, offs, stmp, st);
     if (e != cudaSuccess) return e;
-    static bool smem_set = false;
-    if (!smem_set) {
-      e = cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kScatterSmem);
-      if (e != cudaSuccess) return e;
-      smem_set = true;
-    }
+    static std::atomic<unsigned long long> smem_set{0};
+    e = ensure_dynamic_smem(scatter_kernel, (int)kScatterSmem, smem_set);
+    if (e != cudaSuccess) return e;
     scatter_kernel<<<(unsigned)ntiles, kSortThreads, kScatterSmem, st>>>(kin, vin, n, shift, offs,
                                                                          ntiles, kout, vout);
     e = cudaGetLastError();

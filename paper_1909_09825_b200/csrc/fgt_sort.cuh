@@ -4,6 +4,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace fgt_b200 {
 
 // Launch accounting for bench.py's gpu_launches (fgt_capi.cu).
@@ -29,5 +31,20 @@ cudaError_t launch_flag_nonfinite(const double* x, int64_t n, int* flag, cudaStr
 cudaError_t launch_plan_checks(const double* x, int64_t M, const double* y, int64_t N,
                                int check_sorted, int* flags, cudaStream_t st);
 cudaError_t launch_iota(int32_t* p, int64_t n, cudaStream_t st);
+
+
+// Raise a kernel's dynamic shared-memory limit once per device (the
+// attribute is per device; mask: one bit per device ordinal < 64).
+template <class K>
+inline cudaError_t ensure_dynamic_smem(K kernel, int bytes, std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) mask.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 }  // namespace fgt_b200
