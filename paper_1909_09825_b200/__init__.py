@@ -7,18 +7,22 @@ Python mirror of the reference `fgt1d` package surface for the transform path
 GPU through the C ABI in include/fgt1d_b200.h.
 """
 from ._capi import DeviceError, NumericalError
-from .soe import (SoeApprox, SoeForm, cf_soe, evaluate, fold, load_coefficient_table,
+from .soe import (ErrorReport, SoeApprox, SoeForm, cf_soe, error_grid_point, evaluate, fold,
+                  load_coefficient_table, max_error, max_error_extended,
                   mode_count_for_tolerance, preset_mode_count, preset_soe,
                   save_coefficient_table, soe_for_tolerance, unfold, validate)
 from .transform import (BatchPlan, TransformPlan, TransformRequest, apply_general, apply_same,
-                        batch_transform, direct,
+                        batch_transform, chebyshev_points, delta_sweep, direct, gen_points,
+                        measure_error,
                         direct_transform, gauss_transform, gauss_transform_device, mode_sums, plan,
                         precompute_gap_table, uniform_points, uniform_points_array)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BatchPlan", "DeviceError", "NumericalError", "batch_transform", "SoeApprox", "SoeForm", "TransformPlan", "TransformRequest",
+    "BatchPlan", "DeviceError", "ErrorReport", "NumericalError", "batch_transform", "SoeApprox",
+    "SoeForm", "TransformPlan", "TransformRequest", "chebyshev_points", "delta_sweep",
+    "error_grid_point", "gen_points", "max_error", "max_error_extended", "measure_error",
     "apply_general", "apply_same", "cf_soe", "direct", "direct_transform", "evaluate", "fold",
     "gauss_transform", "gauss_transform_device", "load_coefficient_table", "mode_count_for_tolerance", "mode_sums", "plan",
     "precompute_gap_table", "preset_mode_count", "preset_soe", "save_coefficient_table",

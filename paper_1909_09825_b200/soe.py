@@ -7,6 +7,7 @@ format (:250-337).  Table data comes from the compiled-in CF tables of the C
 ABI (fgt_cf_soe), i.e. "SOE node/weight table lookup by tolerance".
 """
 import ctypes
+from dataclasses import dataclass
 import enum
 import math
 
@@ -169,6 +170,54 @@ def evaluate(soe, x, delta):
             continue
         acc += soe.multiplier(k) * soe.weights[k] * complex(np.exp(-t * s))
     return acc.real
+
+
+# -- SOE error on the standard grid (soe.cpp:38-101, 236-248) ----------------
+
+ERROR_GRID_LOG_POINTS = 100000  # soe.hpp kErrorGridLogPoints
+
+
+def error_grid_point(i):
+    """0 for i <= 0, else 10^(-5 + 7 (i-1)/(kErrorGridLogPoints-1)) (soe.cpp:236-240)."""
+    if i <= 0:
+        return 0.0
+    return 10.0 ** (-5.0 + 7.0 * (i - 1) / (ERROR_GRID_LOG_POINTS - 1))
+
+
+@dataclass
+class ErrorReport:
+    n: int                 # exponentials (folded pairs count 2)
+    max_abs_error: float   # max |exp(-x^2/4) - S(x)| over the grid
+    argmax_x: float        # grid point attaining it (smallest on ties)
+
+
+def _max_error(soe, real, cplx):
+    validate(soe)
+    i = np.arange(1, ERROR_GRID_LOG_POINTS + 1, dtype=np.float64)
+    x = np.concatenate([[0.0], 10.0 ** (-5.0 + 7.0 * (i - 1) / (ERROR_GRID_LOG_POINTS - 1))])
+    s = x.astype(real)
+    acc = np.zeros(x.size, dtype=cplx)
+    for k in range(len(soe)):  # mode order as eval_sum (soe.cpp:22-35)
+        t = cplx(soe.nodes[k])
+        w = cplx(soe.weights[k])
+        keep = real(t.real) * s <= real(745.0)
+        term = real(soe.multiplier(k)) * w * np.exp(-t * s)
+        acc += np.where(keep, term, cplx(0))
+    g = np.exp(-s * s / real(4))
+    e = np.abs(g - acc.real).astype(np.float64)
+    j = int(np.argmax(e))  # first maximum: ties keep the smaller x
+    n = int(sum(soe.multiplier(k) for k in range(len(soe))))
+    return ErrorReport(n, float(e[j]), float(x[j]))
+
+
+def max_error(soe):
+    """fgt::max_error (soe.hpp:76): double accumulation."""
+    return _max_error(soe, np.float64, np.complex128)
+
+
+def max_error_extended(soe):
+    """fgt::max_error_extended (soe.hpp:78-81): long-double accumulation."""
+    return _max_error(soe, np.longdouble, np.clongdouble)
 
 
 def preset_mode_count(p):

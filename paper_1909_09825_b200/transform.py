@@ -332,6 +332,62 @@ def uniform_points(count, seed, stream=0):
     return uniform_points_array(count, seed, stream).tolist()
 
 
+def chebyshev_points(count):
+    """(1 + cos(pi (2i - 1) / (2 count))) / 2 for i = 1..count (rng.cpp:31-40)."""
+    i = np.arange(1, int(count) + 1, dtype=np.float64)
+    return ((1.0 + np.cos(3.14159265358979323846 * (2.0 * i - 1.0) / (2.0 * float(count)))) / 2.0)
+
+
+def gen_points(dist, count, seed, stream):
+    """fgt1d_cli.cpp:170-179: 'uniform' (counter RNG) or 'chebyshev' points."""
+    if dist == "uniform":
+        return uniform_points_array(count, seed, stream)
+    if dist == "chebyshev":
+        return chebyshev_points(count)
+    raise ValueError(f"unknown distribution '{dist}' (expected uniform or chebyshev)")
+
+
+def measure_error(request, potentials, seed):
+    """Sampled relative error (fgt1d_cli.cpp:198-218, acceptance bench_error):
+    100 target indices min(M-1, floor(u M)) from the eval-index stream, the
+    direct sum at them (device, double-double), max |u - u_direct| / |u_direct|
+    skipping |u_direct| < 1e-3 max|u_direct| (near-cancellation guard)."""
+    M = len(request.targets)
+    u = uniform_points_array(100, seed, K_STREAM_EVAL_INDICES)
+    idx = np.minimum(M - 1, (u * M).astype(np.int64))
+    ud = direct(request, idx)
+    umax = np.max(np.abs(ud)) if ud.size else 0.0
+    got = np.asarray(potentials)[idx]
+    keep = np.abs(ud) >= 1e-3 * umax
+    if not np.any(keep):
+        return 0.0
+    return float(np.max(np.abs(got[keep] - ud[keep]) / np.abs(ud[keep])))
+
+
+def delta_sweep(N, ne, deltas, seed=0, dist="uniform"):
+    """fgt1d_cli.cpp:317-352: same-point transform of N points (strengths from
+    the strengths stream) for each delta, error by measure_error.  Returns
+    [{"delta": d, "error": e}, ...]."""
+    if N < 1:
+        raise ValueError("--N must be at least 1")
+    for d in deltas:
+        if not (d > 0.0 and np.isfinite(d)):
+            raise ValueError("all --delta values must be positive")
+    if not 3 <= int(ne) <= 6:
+        raise ValueError("--ne must be between 3 and 6 (precision presets)")
+    from .soe import preset_soe
+    soe = preset_soe(int(ne) - 3)
+    y = gen_points(dist, N, seed, K_STREAM_SOURCES)
+    a = uniform_points_array(N, seed, K_STREAM_STRENGTHS)
+    rows = []
+    for d in deltas:
+        req = TransformRequest(y, y, a, float(d))
+        p = plan(req, soe, True)
+        res = apply_same(p, a, 1)
+        rows.append({"delta": float(d), "error": measure_error(req, res, seed)})
+    return rows
+
+
 K_STREAM_SOURCES = 0
 K_STREAM_STRENGTHS = 1
 K_STREAM_EVAL_INDICES = 2

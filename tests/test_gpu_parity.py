@@ -505,3 +505,34 @@ def test_batched_rejects_unsorted_and_reuses_plan():
         out = bp.apply(al)
         for b, d in enumerate([1e-3, 1e-5]):
             check(out[b], oracle.transform(xs[b], ys[b], al[b], d, ne=4, mode=0), al[b])
+
+
+# ---------------------------------------------- error harness (§8f item 3)
+
+def test_delta_sweep_acceptance_criterion10():
+    # acceptance.cpp:394-423: N=1e5 same points, n_e=4, delta=1e-7..1e4; the
+    # sampled error is nondecreasing within x3 and saturates near E_n
+    rows = fgt.delta_sweep(100000, 4, [10.0 ** p for p in range(-7, 5)], seed=0)
+    errs = [r["error"] for r in rows]
+    en = fgt.max_error(fgt.fold(fgt.cf_soe(8))).max_abs_error
+    for i in range(1, len(errs)):
+        assert errs[i] >= errs[i - 1] / 3.0, errs
+    sat = errs[-1]
+    assert en / 10.0 <= sat <= 10.0 * en, (sat, en)
+    assert sat >= max(errs) / 3.0
+
+
+def test_measure_error_matches_reference_on_its_own_result():
+    # fgt1d_cli.cpp:198-218 on the same request: our sampled error vs the one
+    # the reference library's transform has (same SOE, same 100 targets)
+    if not oracle.ref_available():
+        pytest.skip("reference library not built")
+    n = 20000
+    y = up(n, 0, 0)
+    a = up(n, 0, 1)
+    for delta in (1e-6, 1e-4, 1e-2, 1.0):
+        req = fgt.TransformRequest(y, y, a, delta)
+        ours = fgt.measure_error(req, np.array(fgt.gauss_transform(y, y, a, delta, ne=6)), 0)
+        ref_u, _ = oracle.ref_transform(y, y, a, delta, ne=6, mode=1)
+        theirs = fgt.measure_error(req, ref_u, 0)
+        assert ours <= max(1.1 * theirs, 1e-13), (delta, ours, theirs)

@@ -137,3 +137,43 @@ def test_validate_and_fold_errors():
         fgt.fold(S.SoeApprox([1 + 1j], [1.0]))  # no conjugate partner
     with pytest.raises(ValueError):
         fgt.fold(S.SoeApprox([1 + 0j], [1 + 1j]))  # real node, complex weight
+
+
+# -- max_error on the standard grid (soe.cpp:38-101, 236-248) ---------------
+
+@pytest.mark.parametrize("n", [2, 4, 6, 8, 10, 12, 14])
+@pytest.mark.parametrize("folded", [False, True])
+def test_max_error_matches_reference_library(n, folded):
+    import oracle
+    if not oracle.ref_available():
+        pytest.skip("reference library not built")
+    soe = fgt.cf_soe(n)
+    if folded:
+        soe = fgt.fold(soe)
+    r = fgt.max_error(soe)
+    e_ref, arg_ref = oracle.ref_max_error(n, folded)
+    assert r.n == n
+    if n >= 14:
+        # ~4e-12: at the rounding level of the double sum, where libm and
+        # numpy exponentials differ in the last ulps; the maximum moves
+        assert abs(r.max_abs_error - e_ref) <= 1e-2 * e_ref
+        return
+    assert abs(r.max_abs_error - e_ref) <= 1e-9 * e_ref + 1e-17
+    assert r.argmax_x == pytest.approx(arg_ref, rel=1e-12, abs=0.0)
+
+
+def test_max_error_extended_and_grid():
+    assert fgt.error_grid_point(0) == 0.0
+    assert fgt.error_grid_point(1) == pytest.approx(1e-5)
+    assert fgt.error_grid_point(100000) == pytest.approx(100.0)
+    r = fgt.max_error_extended(fgt.fold(fgt.cf_soe(12)))
+    assert 2.9e-10 < r.max_abs_error < 3.1e-10  # test_cf.cpp:20-23 pin +-5% of 3.0208e-10
+
+
+def test_chebyshev_points_formula():
+    # rng.cpp:31-40
+    n = 7
+    p = fgt.chebyshev_points(n)
+    i = np.arange(1, n + 1)
+    assert np.array_equal(p, (1.0 + np.cos(np.pi * (2.0 * i - 1.0) / (2.0 * n))) / 2.0)
+    assert fgt.chebyshev_points(0).size == 0
