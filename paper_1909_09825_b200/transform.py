@@ -364,6 +364,17 @@ def measure_error(request, potentials, seed):
     return float(np.max(np.abs(got[keep] - ud[keep]) / np.abs(ud[keep])))
 
 
+def preset_for_ne(ne):
+    """fgt1d_cli.cpp:181-195: precision presets for n_e = 3..6, otherwise
+    fold(cf_soe(2 n_e)) for 1..7."""
+    from .soe import preset_soe
+    if 3 <= ne <= 6:
+        return preset_soe(ne - 3)
+    if 1 <= ne <= 7:
+        return fold(cf_soe(2 * ne))
+    raise ValueError("--ne must be between 1 and 7")
+
+
 def delta_sweep(N, ne, deltas, seed=0, dist="uniform"):
     """fgt1d_cli.cpp:317-352: same-point transform of N points (strengths from
     the strengths stream) for each delta, error by measure_error.  Returns
@@ -373,10 +384,7 @@ def delta_sweep(N, ne, deltas, seed=0, dist="uniform"):
     for d in deltas:
         if not (d > 0.0 and np.isfinite(d)):
             raise ValueError("all --delta values must be positive")
-    if not 3 <= int(ne) <= 6:
-        raise ValueError("--ne must be between 3 and 6 (precision presets)")
-    from .soe import preset_soe
-    soe = preset_soe(int(ne) - 3)
+    soe = preset_for_ne(int(ne))
     y = gen_points(dist, N, seed, K_STREAM_SOURCES)
     a = uniform_points_array(N, seed, K_STREAM_STRENGTHS)
     rows = []
