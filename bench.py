@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=float, default=1e8, help="targets = sources per transform")
+    ap.add_argument("--n", "--size", dest="n", type=float, default=1e8,
+                    help="targets = sources per transform (--size under torchrun)")
     ap.add_argument("--delta", type=float, default=1e-3)
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--seed", type=int, default=0)
@@ -307,10 +308,32 @@ def main():
     from paper_1909_09825_b200.soe import soe_for_tolerance
 
     rank, world, local = env_rank()
+    # FGT_BENCH_BACKEND=gloo is a test hook: several ranks may then share one
+    # GPU (the multi-rank code path runs; its timings mean nothing)
+    backend = os.environ.get("FGT_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+
+    def gather_aggs(t):
+        """all_gather of this rank's chunk aggregates (device tensor)."""
+        if backend == "nccl":
+            out = torch.empty(world * t.numel(), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(out, t)
+            return out.cpu().numpy()
+        parts = [torch.empty_like(t.cpu()) for _ in range(world)]
+        dist.all_gather(parts, t.cpu())
+        return torch.cat(parts).numpy()
+
+    def reduce_max(v):
+        t = torch.tensor([v], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
     L = _capi.lib()
     stream = torch.cuda.current_stream()
     sh = ctypes.c_void_p(stream.cuda_stream)
@@ -373,10 +396,7 @@ def main():
             agg = np.empty(6 * ne)
             _capi.check(L.fgt_apply_chunk_aggregate(h, ctypes.cast(ac.data_ptr(), PD),
                                                     agg.ctypes.data_as(PD), flags, sh))
-            t = torch.from_numpy(agg).to(dev)
-            gathered = torch.empty(world * 6 * ne, dtype=torch.float64, device=dev)
-            dist.all_gather_into_tensor(gathered, t)
-            allagg = gathered.cpu().numpy()
+            allagg = gather_aggs(torch.from_numpy(agg).to(dev))
             carries = np.empty(world * 4 * ne)
             _capi.check(L.fgt_chunk_carries(allagg.ctypes.data_as(PD), world, ne,
                                             carries.ctypes.data_as(PD)))
@@ -388,7 +408,10 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
 
     def timed(steps, delta):
         barrier()
@@ -403,9 +426,7 @@ def main():
         barrier()
         ms = e0.elapsed_time(e1) / steps
         if world > 1:
-            t = torch.tensor([ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            ms = reduce_max(ms)
         return ms
 
     for _ in range(max(args.warmup, 0)):
@@ -439,7 +460,7 @@ def main():
     kcnt = (ctypes.c_longlong * 3)()
     L.fgt_profile_read(kms.ctypes.data_as(PD), kcnt, 3)
     L.fgt_profile_enable(0)
-    kavg = [kms[i] / max(1, kcnt[i]) for i in range(3)]
+    kavg = [kms[i] / prof_steps for i in range(3)]  # per step (K2 runs twice with chunks)
     apply_ms = sum(kavg)
 
     # ---- FP64 peak (measured) and roofline
@@ -493,10 +514,7 @@ def main():
                 agg = np.empty(6 * ne)
                 _capi.check(L.fgt_apply_chunk_aggregate(h, ctypes.cast(ha.data_ptr(), PD),
                                                         agg.ctypes.data_as(PD), 0, sh))
-                t = torch.from_numpy(agg).to(dev)
-                gathered = torch.empty(world * 6 * ne, dtype=torch.float64, device=dev)
-                dist.all_gather_into_tensor(gathered, t)
-                allagg = gathered.cpu().numpy()
+                allagg = gather_aggs(torch.from_numpy(agg).to(dev))
                 carries = np.empty(world * 4 * ne)
                 _capi.check(L.fgt_chunk_carries(allagg.ctypes.data_as(PD), world, ne,
                                                 carries.ctypes.data_as(PD)))
@@ -514,9 +532,7 @@ def main():
         barrier()
         es = (time.perf_counter() - t0) / args.e2e_steps
         if world > 1:
-            t = torch.tensor([es], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            es = float(t.item())
+            es = reduce_max(es)
         # cross-check: e2e potentials equal the device-path potentials
         one_step(args.delta)
         torch.cuda.synchronize()

@@ -503,9 +503,15 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ho
   }
   const StreamArgs sa = stream_args(p, p->cs.bs);
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
-  ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
+  {
+    ProfScope ps(0, st);
+    ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
+  }
   cplx* d_tot = w.get<cplx>(3 * ne);
-  ck(launch_carry_scan(ts, p->ntiles, ne, nullptr, d_tot, st), "chunk totals");
+  {
+    ProfScope ps(1, st);
+    ck(launch_carry_scan(ts, p->ntiles, ne, nullptr, d_tot, st), "chunk totals");
+  }
   ck(cudaMemcpyAsync(totals_host, d_tot, sizeof(cplx) * 3 * ne, cudaMemcpyDeviceToHost, st),
      "totals");
   ck(cudaStreamSynchronize(st), "sync");
@@ -527,11 +533,17 @@ void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in_host, double* potentia
   cplx* d_cin = w.get<cplx>(2 * ne);
   ck(cudaMemcpyAsync(d_cin, carry_in_host, sizeof(cplx) * 2 * ne, cudaMemcpyHostToDevice, st),
      "carry in");
-  ck(launch_carry_scan(ts, p->ntiles, ne, d_cin, nullptr, st), "carry scan");
+  {
+    ProfScope ps(1, st);
+    ck(launch_carry_scan(ts, p->ntiles, ne, d_cin, nullptr, st), "carry scan");
+  }
   OutArgs o;
   o.u = u;
   o.tperm = p->d_tperm;
-  ck(launch_main(sa, p->P, p->d_mt, ts, o, st), "main pass");
+  {
+    ProfScope ps(2, st);
+    ck(launch_main(sa, p->P, p->d_mt, ts, o, st), "main pass");
+  }
   if (!dev) {
     ck(cudaMemcpyAsync(potentials, u, sizeof(double) * p->M, cudaMemcpyDeviceToHost, st),
        "download potentials");
