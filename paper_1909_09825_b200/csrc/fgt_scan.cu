@@ -90,16 +90,6 @@ __device__ __forceinline__ cplx horner(const Coef<D>& c, double g) {
   return {pr, pi};
 }
 
-// Gap factor exp(-s g): Taylor polynomial of degree D (fast path) or exact.
-template <int D>
-__device__ __forceinline__ cplx gap_factor(const Coef<D>& c, cplx s, double g) {
-  if constexpr (D >= 0) {
-    return horner<D>(c, g);
-  } else {
-    return decay_exact(s.re, s.im, g);
-  }
-}
-
 // Gap factors of a lane run, exp(-s_k g_i) for i < kR: Horner with the
 // element loop inside (each coefficient read once per run, kR independent
 // chains); exact for D < 0.  Same operation order as horner<D>.
@@ -565,9 +555,6 @@ __device__ __forceinline__ void chains_mode(const cplx (&d)[kR], cplx mw, const 
   }
 }
 
-#ifndef FGT_P2_COEF
-#define FGT_P2_COEF 0
-#endif
 #ifndef FGT_CARRY_UNROLL
 #define FGT_CARRY_UNROLL 1
 #endif
@@ -627,14 +614,7 @@ __device__ __forceinline__ void pass2(const ModeTable& mt, int ne, const LaneRun
 #pragma unroll kModeUnroll
   for (int k = 0; k < ne; ++k) {
     cplx d[kR];
-#if FGT_P2_COEF
-    Coef<D> c;
-    c.load(mt, k);
-#pragma unroll
-    for (int i = 0; i < kR; ++i) d[i] = gap_factor<D>(c, mt.s[k], r.g[i]);
-#else
     gap_factors<D>(mt, k, r.g, d);
-#endif
     chains_mode<MS>(d, mt.mw[k], r, carry[k].cf, carry[k].cb, k, out, ms);
   }
 }
@@ -1188,12 +1168,6 @@ __global__ void classify_kernel(StreamArgs a, ModeParams P, double smax,
 }
 
 // ------------------------------------------------------------------- K3
-#ifndef FGT_PHASE_TIMING
-#define FGT_PHASE_TIMING 0
-#endif
-#if FGT_PHASE_TIMING
-__device__ unsigned long long g_phase_cycles[8];
-#endif
 
 #ifndef FGT_K3_MINB
 #define FGT_K3_MINB 4
@@ -2095,17 +2069,3 @@ cudaError_t launch_gather(const double* alpha, const int32_t* perm, int64_t n, d
 }
 
 }  // namespace fgt_b200
-
-// Debug: per-phase warp cycles of K3 (only in FGT_PHASE_TIMING builds):
-// [0] loads+degrees, [1] carries, [2] pass 2, [3] output, [4] segments.
-extern "C" int fgt_debug_phase_cycles(unsigned long long* out) {
-#if FGT_PHASE_TIMING
-  cudaMemcpyFromSymbol(out, fgt_b200::g_phase_cycles, sizeof(unsigned long long) * 8);
-  unsigned long long z[8] = {0};
-  cudaMemcpyToSymbol(fgt_b200::g_phase_cycles, z, sizeof(z));
-  return 1;
-#else
-  for (int i = 0; i < 8; ++i) out[i] = 0;
-  return 0;
-#endif
-}

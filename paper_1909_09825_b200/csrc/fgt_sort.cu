@@ -1,13 +1,11 @@
 // Sort / permutation plumbing of plan(): the device replacement of
 // sort_with_perm (proj/src/transform.cpp:27-39, std::sort of (value, index)
-// pairs => ascending, ties in original order) and of the same-points test
-// (transform.cpp:214-216).
+// pairs => ascending, ties in original order).  The structural checks
+// (finite, sorted, same points) run in the plan tile pass (fgt_scan.cu).
 //
-//   is_sorted       : skip the sort entirely when the input is already ordered
 //   radix sort      : stable LSD, 8-bit digits over order-preserving u64 keys
 //                     with a u32 index payload; passes whose digit is constant
 //                     across all keys are skipped (one global histogram pass)
-//   same_points     : element-wise equality of the two coordinate vectors
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -282,81 +280,6 @@ int64_t scan_tmp_elems(int64_t n) {
   return total + 16;
 }
 
-__global__ void not_sorted_kernel(const double* __restrict__ x, int64_t n, int* __restrict__ flag) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (__ldg(x + i) > __ldg(x + i + 1)) {
-      *flag = 1;
-      return;
-    }
-  }
-}
-
-__global__ void not_equal_kernel(const double* __restrict__ x, const double* __restrict__ y,
-                                 int64_t n, int* __restrict__ flag) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (!(__ldg(x + i) == __ldg(y + i))) {
-      *flag = 1;
-      return;
-    }
-  }
-}
-
-__global__ void nonfinite_kernel(const double* __restrict__ x, int64_t n, int* __restrict__ flag) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (!isfinite(__ldg(x + i))) {
-      *flag = 1;
-      return;
-    }
-  }
-}
-
-// All plan-time structural checks in one read of both sets:
-// flags[0] target non-finite, [1] source non-finite, [2] x[i] != y[i]
-// (only when M == N), [3] targets unsorted, [4] sources unsorted.
-__global__ void __launch_bounds__(256)
-    plan_checks_kernel(const double* __restrict__ x, int64_t M, const double* __restrict__ y,
-                       int64_t N, int check_sorted, int* __restrict__ flags) {
-  const int64_t n = M > N ? M : N;
-  const bool same_len = M == N;
-  int f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double xv = 0.0, yv = 0.0;
-    if (i < M) {
-      xv = __ldg(x + i);
-      f0 |= !isfinite(xv);
-      if (check_sorted && i + 1 < M) f3 |= xv > __ldg(x + i + 1);
-    }
-    if (i < N) {
-      yv = __ldg(y + i);
-      f1 |= !isfinite(yv);
-      if (check_sorted && i + 1 < N) f4 |= yv > __ldg(y + i + 1);
-    }
-    if (same_len) f2 |= !(xv == yv);
-  }
-  f0 = __any_sync(0xffffffffu, f0);
-  f1 = __any_sync(0xffffffffu, f1);
-  f2 = __any_sync(0xffffffffu, f2);
-  f3 = __any_sync(0xffffffffu, f3);
-  f4 = __any_sync(0xffffffffu, f4);
-  if ((threadIdx.x & 31) == 0) {
-    if (f0) flags[0] = 1;
-    if (f1) flags[1] = 1;
-    if (f2) flags[2] = 1;
-    if (f3) flags[3] = 1;
-    if (f4) flags[4] = 1;
-  }
-}
-
-__global__ void iota_kernel(int32_t* __restrict__ p, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = (int32_t)i;
-}
-
 inline unsigned grid_for(int64_t n, int bs) {
   int64_t g = (n + bs - 1) / bs;
   if (g > 148 * 32) g = 148 * 32;
@@ -432,87 +355,6 @@ cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int
   }
   note_launch();
   unkey_kernel<<<grid_for(n, 256), 256, 0, st>>>(kin, vin, n, sorted, perm);
-  return cudaGetLastError();
-}
-
-cudaError_t check_sorted(const double* x, int64_t n, int* d_flag, int* is_sorted,
-                         cudaStream_t st) {
-  *is_sorted = 1;
-  if (n < 2) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(d_flag, 0, sizeof(int), st);
-  if (e != cudaSuccess) return e;
-  not_sorted_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, d_flag);
-  int h = 0;
-  e = cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return e;
-  e = cudaStreamSynchronize(st);
-  *is_sorted = h ? 0 : 1;
-  return e;
-}
-
-cudaError_t check_equal(const double* x, const double* y, int64_t n, int* d_flag, int* equal,
-                        cudaStream_t st) {
-  *equal = 1;
-  if (n < 1) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(d_flag, 0, sizeof(int), st);
-  if (e != cudaSuccess) return e;
-  not_equal_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, y, n, d_flag);
-  int h = 0;
-  e = cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return e;
-  e = cudaStreamSynchronize(st);
-  *equal = h ? 0 : 1;
-  return e;
-}
-
-cudaError_t check_finite(const double* x, int64_t n, int* d_flag, int* finite, cudaStream_t st) {
-  *finite = 1;
-  if (n < 1) return cudaSuccess;
-  cudaError_t e = cudaMemsetAsync(d_flag, 0, sizeof(int), st);
-  if (e != cudaSuccess) return e;
-  nonfinite_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, d_flag);
-  int h = 0;
-  e = cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return e;
-  e = cudaStreamSynchronize(st);
-  *finite = h ? 0 : 1;
-  return e;
-}
-
-cudaError_t launch_flag_unsorted(const double* x, int64_t n, int* flag, cudaStream_t st) {
-  if (n < 2) return cudaSuccess;
-  note_launch();
-  not_sorted_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, flag);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_flag_unequal(const double* x, const double* y, int64_t n, int* flag,
-                                cudaStream_t st) {
-  if (n < 1) return cudaSuccess;
-  note_launch();
-  not_equal_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, y, n, flag);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_flag_nonfinite(const double* x, int64_t n, int* flag, cudaStream_t st) {
-  if (n < 1) return cudaSuccess;
-  note_launch();
-  nonfinite_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, flag);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_plan_checks(const double* x, int64_t M, const double* y, int64_t N,
-                               int check_sorted, int* flags, cudaStream_t st) {
-  const int64_t n = M > N ? M : N;
-  if (n < 1) return cudaSuccess;
-  note_launch();
-  plan_checks_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, M, y, N, check_sorted, flags);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_iota(int32_t* p, int64_t n, cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  iota_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, n);
   return cudaGetLastError();
 }
 
