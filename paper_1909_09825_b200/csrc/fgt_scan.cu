@@ -892,7 +892,11 @@ __device__ __forceinline__ int seg_moment_degree(const ModeParams& P, double sma
 // Highest moment degree K3 keeps in registers.  A segment narrow enough for
 // it has every gap below 2 rmax[kK3Moments] < rmax[kMaxDeg], so its gap
 // factors take the Taylor path.
-constexpr int kK3Moments = 5;
+#ifndef FGT_K3_MOMENTS
+#define FGT_K3_MOMENTS 5
+#endif
+constexpr int kK3Moments = FGT_K3_MOMENTS;
+static_assert(kK3Moments >= 0 && kK3Moments <= kRegDeg, "K3 moment degree");
 // Highest lane-moment degree of the K1 wide path.
 #ifndef FGT_LANE_MOM_MAX
 #define FGT_LANE_MOM_MAX 12
@@ -1197,11 +1201,20 @@ __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParam
     carries_moments<n>(mx, ne, r, f, zp, zl, lane, term, mine);                     \
   } break;
       FGT_CM(0) FGT_CM(1) FGT_CM(2) FGT_CM(3) FGT_CM(4) FGT_CM(5)
+#if FGT_K3_MOMENTS >= 6
+      FGT_CM(6)
+#endif
+#if FGT_K3_MOMENTS >= 7
+      FGT_CM(7)
+#endif
+#if FGT_K3_MOMENTS >= 8
+      FGT_CM(8)
+#endif
 #undef FGT_CM
       default:
         break;
     }
-    static_assert(kK3Moments == 5, "FGT_CM cases");
+    static_assert(kK3Moments >= 5, "FGT_CM cases");
   }
 #pragma unroll
   for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
