@@ -302,6 +302,29 @@ void adopt_set(const SetSrc& in, int64_t n, bool is_sorted, uint32_t flags, cuda
   *d_perm = d_p;
 }
 
+// Small per-thread pinned buffer for the plan's device -> host reads (flags,
+// first coordinates, class counts): async copies into pageable memory would
+// synchronise the stream each.  Falls back to nullptr (pageable) if pinned
+// allocation fails.
+struct PinnedScratch {
+  unsigned char* p = nullptr;
+  ~PinnedScratch() {
+    if (p) cudaFreeHost(p);
+  }
+};
+unsigned char* pinned_scratch() {
+  thread_local PinnedScratch s;
+  if (!s.p) {
+    void* q = nullptr;
+    if (cudaMallocHost(&q, 256) == cudaSuccess) {
+      s.p = static_cast<unsigned char*>(q);
+    } else {
+      cudaGetLastError();
+    }
+  }
+  return s.p;
+}
+
 // d_flag: check flags 0..4, then two 64-bit segment-class counters.
 constexpr int kFlagInts = 12;
 unsigned long long* class_counts(fgt_plan_s* p) {
@@ -334,7 +357,9 @@ void take_classes(fgt_plan_s* p, const unsigned long long* h) {
   p->nwide3 = (int64_t)h[1];
 }
 void classify_sync(fgt_plan_s* p, cudaStream_t st) {
-  unsigned long long h[2] = {0, 0};
+  unsigned long long hl[2] = {0, 0};
+  unsigned char* pin = pinned_scratch();
+  unsigned long long* h = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hl;
   queue_classify(p, h, st);
   ck(cudaStreamSynchronize(st), "classify sync");
   take_classes(p, h);
@@ -355,14 +380,15 @@ void plan_tiles(fgt_plan_s* p, const double* xd, const double* yd, bool check_so
   dfree(tib, st);
 }
 
+// Mode table of a single plan: built on the host, stored by a kernel
+// parameter (stream-ordered, no synchronisation).
 void upload_modes(fgt_plan_s* p, cudaStream_t st) {
   ModeTable T;
   build_modes(p->soe, p->delta, p->P, T);
   p->d_mt = dmalloc<ModeTable>(1, st);
-  ck(cudaMemcpyAsync(p->d_mt, &T, sizeof(T), cudaMemcpyHostToDevice, st), "upload modes");
-  // the host ModeTable dies with this frame: make the copy complete
-  ck(cudaStreamSynchronize(st), "plan sync");
+  ck(launch_store_table(T, p->d_mt, st), "store mode table");
 }
+
 
 // Stream-ordered teardown on the plan's stream: work already queued on it
 // that uses the plan completes before the memory is reused.
@@ -652,11 +678,16 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       p->d_seg_mask = dmalloc<uint32_t>((size_t)p->ntiles * (kSeg / 32), st);
       // one read of both sets: checks + (speculative) segment metadata
       plan_tiles(p, xs.dptr, ys.dptr, !(flags & FGT_ASSUME_SORTED), st);
-      int hf[8] = {0};
-      double x0 = 0, y0 = 0;
-      ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(hf), cudaMemcpyDeviceToHost, st), "flags");
-      if (M > 0) ck(cudaMemcpyAsync(&x0, xs.dptr, 8, cudaMemcpyDeviceToHost, st), "x0");
-      if (N > 0) ck(cudaMemcpyAsync(&y0, ys.dptr, 8, cudaMemcpyDeviceToHost, st), "y0");
+      // flags and first coordinates in one round trip (pinned scratch)
+      unsigned char* pin = pinned_scratch();
+      int hfl[8] = {0};
+      double xyl[2] = {0.0, 0.0};
+      int* hf = pin ? reinterpret_cast<int*>(pin) : hfl;
+      double* xy0 = pin ? reinterpret_cast<double*>(pin + 32) : xyl;
+      xy0[0] = xy0[1] = 0.0;
+      ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(int) * 8, cudaMemcpyDeviceToHost, st), "flags");
+      if (M > 0) ck(cudaMemcpyAsync(xy0, xs.dptr, 8, cudaMemcpyDeviceToHost, st), "x0");
+      if (N > 0) ck(cudaMemcpyAsync(xy0 + 1, ys.dptr, 8, cudaMemcpyDeviceToHost, st), "y0");
       ck(cudaStreamSynchronize(st), "flags sync");
       // the reference checks targets, then sources (transform.cpp:202-204)
       if (hf[0]) raise(FGT_ERR_DOMAIN, "target coordinates must be finite");
@@ -670,11 +701,13 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       if (!p->t_sorted || !p->s_sorted) {
         // metadata of the sorted stream; first coordinates after sorting
         plan_tiles(p, p->d_xs, p->d_ys, false, st);
-        if (M > 0) ck(cudaMemcpyAsync(&x0, p->d_xs, 8, cudaMemcpyDeviceToHost, st), "x0");
-        if (N > 0) ck(cudaMemcpyAsync(&y0, p->d_ys, 8, cudaMemcpyDeviceToHost, st), "y0");
+        if (M > 0) ck(cudaMemcpyAsync(xy0, p->d_xs, 8, cudaMemcpyDeviceToHost, st), "x0");
+        if (N > 0) ck(cudaMemcpyAsync(xy0 + 1, p->d_ys, 8, cudaMemcpyDeviceToHost, st), "y0");
+        ck(cudaStreamSynchronize(st), "sorted sync");
       }
-      upload_modes(p, st);  // synchronizes
+      upload_modes(p, st);
       // coordinate before the first merged element: the element itself
+      const double x0 = xy0[0], y0 = xy0[1];
       p->zprev0 = (M > 0 && N > 0) ? std::fmin(x0, y0) : (M > 0 ? x0 : y0);
       classify_sync(p, st);
     } catch (...) {
@@ -1025,8 +1058,10 @@ extern "C" int fgt_batch_create(int B, const double* targets, const int64_t* t_o
                            d_tib, p->d_tile_ib, p->d_seg_jb, p->d_seg_info, p->d_seg_z,
                            p->d_seg_mask, p->d_seg_gap, p->d_flag, st),
          "batch plan");
-      int hf[8] = {0};
-      ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(hf), cudaMemcpyDeviceToHost, st), "flags");
+      unsigned char* pin = pinned_scratch();
+      int hfl[8] = {0};
+      int* hf = pin ? reinterpret_cast<int*>(pin) : hfl;
+      ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(int) * 8, cudaMemcpyDeviceToHost, st), "flags");
       // per-transform mode tables (device-built), the shared one of transform 0
       ModeTable T0;
       build_modes(p->soe, deltas[0], p->P, T0);
@@ -1042,9 +1077,9 @@ extern "C" int fgt_batch_create(int B, const double* targets, const int64_t* t_o
       p->d_mtb = dmalloc<ModeTable>(B, st);
       ck(launch_batch_modes(base, d_deltas, B, p->d_mtb, st), "mode tables");
       p->d_mt = dmalloc<ModeTable>(1, st);
-      ck(cudaMemcpyAsync(p->d_mt, &T0, sizeof(ModeTable), cudaMemcpyHostToDevice, st),
-         "mode table");
-      unsigned long long hc[2] = {0, 0};
+      ck(launch_store_table(T0, p->d_mt, st), "mode table");
+      unsigned long long hcl[2] = {0, 0};
+      unsigned long long* hc = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hcl;
       queue_classify(p, hc, st, true);
       ck(cudaStreamSynchronize(st), "batch plan sync");
       take_classes(p, hc);

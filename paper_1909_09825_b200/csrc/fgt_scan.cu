@@ -1102,6 +1102,13 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+__global__ void store_table_kernel(ModeTable T, ModeTable* __restrict__ out) {
+  const double* src = reinterpret_cast<const double*>(&T);
+  double* dst = reinterpret_cast<double*>(out);
+  for (int i = threadIdx.x; i < (int)(sizeof(ModeTable) / sizeof(double)); i += blockDim.x)
+    dst[i] = src[i];
+}
+
 // Batched plans: one thread per transform writes its mode table.
 __global__ void batch_modes_kernel(BatchModeBase base, const double* __restrict__ deltas, int B,
                                    ModeTable* __restrict__ out) {
@@ -1982,6 +1989,12 @@ cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const Mod
     note_launch();
     seg_aggregate_kernel<false><<<grid, kThreads, 0, st>>>(a, P, mt, ts);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_store_table(const ModeTable& T, ModeTable* out, cudaStream_t st) {
+  note_launch();
+  store_table_kernel<<<1, 128, 0, st>>>(T, out);
   return cudaGetLastError();
 }
 

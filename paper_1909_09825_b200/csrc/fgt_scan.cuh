@@ -117,6 +117,9 @@ struct BatchModeBase {
   cplx t[kMaxModes];   // folded SOE nodes
   cplx mw[kMaxModes];  // multiplier * weight
 };
+// Store a mode table built on the host through a kernel parameter (no
+// pageable copy, no implicit stream synchronisation).
+cudaError_t launch_store_table(const ModeTable& T, ModeTable* out, cudaStream_t st);
 cudaError_t launch_batch_modes(const BatchModeBase& base, const double* deltas, int B,
                                ModeTable* out, cudaStream_t st);
 // Plan-time classification: counts[0] / counts[1] = segments that K1 / K3
