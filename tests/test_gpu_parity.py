@@ -536,3 +536,57 @@ def test_measure_error_matches_reference_on_its_own_result():
         ref_u, _ = oracle.ref_transform(y, y, a, delta, ne=6, mode=1)
         theirs = fgt.measure_error(req, ref_u, 0)
         assert ours <= max(1.1 * theirs, 1e-13), (delta, ours, theirs)
+
+
+# --------------------------- plan tile checks: non-finite / nearly-sorted
+
+def _plan_rc(x, y):
+    import torch
+    soe = fgt.fold(fgt.cf_soe(8))
+    tr, ti, wr, wi, sc = soe.arrays()
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    yd = torch.from_numpy(np.ascontiguousarray(y)).cuda()
+    h = ctypes.c_void_p()
+    rc = _capi.lib().fgt_plan_create(ctypes.cast(xd.data_ptr(), PD), x.size,
+                                     ctypes.cast(yd.data_ptr(), PD), y.size, 1e-3,
+                                     tr.ctypes.data_as(PD), ti.ctypes.data_as(PD),
+                                     wr.ctypes.data_as(PD), wi.ctypes.data_as(PD),
+                                     sc.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), len(soe), 1,
+                                     _capi.FGT_DEVICE_PTRS, 0, None, ctypes.byref(h))
+    msg = _capi.lib().fgt_last_error().decode() if rc else ""
+    if rc == 0:
+        _capi.lib().fgt_plan_destroy(h)
+    return rc, msg
+
+
+@pytest.mark.parametrize("srt", [True, False])
+def test_nonfinite_detected_anywhere(srt):
+    # transform.cpp:21-25 check_points: every coordinate, targets before sources
+    rng = np.random.default_rng(31)
+    for trial in range(12):
+        n, m = int(rng.integers(1, 20000)), int(rng.integers(1, 20000))
+        x, y = up(n, trial, 3), up(m, trial, 0)
+        if srt:
+            x, y = np.sort(x), np.sort(y)
+        bad = [np.nan, np.inf, -np.inf][trial % 3]
+        which = trial % 2
+        arr = x if which == 0 else y
+        pos = [0, arr.size - 1, int(rng.integers(0, arr.size))][trial % 3]
+        arr[pos] = bad
+        rc, msg = _plan_rc(x, y)
+        assert rc == _capi.FGT_ERR_DOMAIN, (trial, srt, which, pos, bad)
+        assert ("target" if which == 0 else "source") in msg, msg
+
+
+def test_nearly_sorted_inputs_are_sorted_first():
+    # one adjacent swap at tile / segment boundaries must be detected
+    n = 3 * 4096 + 77
+    for pos in (0, 127, 255, 256, 2047, 2048, 4095, 4096, 8191, n - 2):
+        x, y = np.sort(up(n, 40, 3)), np.sort(up(n, 40, 0))
+        for arr in (x, y):
+            a2 = arr.copy()
+            a2[pos], a2[pos + 1] = a2[pos + 1], a2[pos]
+            xx, yy = (a2, y) if arr is x else (x, a2)
+            a = 2.0 * up(n, 40, 1) - 1.0
+            u = gpu_transform(xx, yy, a, 1e-3, 6, mode=0)
+            check(u, oracle.transform(xx, yy, a, 1e-3, ne=6, mode=0), a)
