@@ -308,9 +308,21 @@ __device__ __forceinline__ SegFrame seg_frame(const SegGeom& g) {
 // staging; every element is an independent load.  Coordinates are left in
 // r.g (converted to gaps by lane_gaps); zp = coordinate preceding the run,
 // zl = coordinate of its last element.
+__device__ __forceinline__ uint32_t lane_mask_word(const StreamArgs& a, int64_t s, int lane) {
+  return __ldg(a.seg_mask + s * (kSeg / 32) + (lane >> 2));
+}
+
+// word: this lane's merge-mask word of segment s (prefetched by the caller)
+__device__ __forceinline__ void lane_load_w(const StreamArgs& a, const SegGeom& g, uint32_t word,
+                                            int lane, LaneRun& r, double& zp, double& zl);
+
 __device__ __forceinline__ void lane_load(const StreamArgs& a, const SegGeom& g, int64_t s,
                                           int lane, LaneRun& r, double& zp, double& zl) {
-  const uint32_t word = __ldg(a.seg_mask + s * (kSeg / 32) + (lane >> 2));
+  lane_load_w(a, g, lane_mask_word(a, s, lane), lane, r, zp, zl);
+}
+
+__device__ __forceinline__ void lane_load_w(const StreamArgs& a, const SegGeom& g, uint32_t word,
+                                            int lane, LaneRun& r, double& zp, double& zl) {
   const int d0 = lane * kR;
   const int nreal = g.len - d0 < 0 ? 0 : (g.len - d0 < kR ? g.len - d0 : kR);
   const unsigned live = (1u << nreal) - 1u;
@@ -1361,21 +1373,33 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
     __syncthreads();
     const WarpWalk walk{(int64_t)blockIdx.x * kSegWarps + warp, (int64_t)gridDim.x * kSegWarps,
                         a.nseg};
-    for (int64_t s = walk.first(); s < a.nseg; s = walk.next(s)) {
+    // the next segment's mask word and carries are loaded while this one is
+    // computed (its element loads then start without a dependent round trip)
+    int64_t s = walk.first();
+    uint32_t word = s < a.nseg ? lane_mask_word(a, s, lane) : 0u;
+    cplx seg_c = s < a.nseg ? load_seg_carry(ts, a.nseg, s, ne, lane) : cplx{0.0, 0.0};
+    while (s < a.nseg) {
+      const int64_t sn = walk.next(s);
+      const uint32_t word_n = sn < a.nseg ? lane_mask_word(a, sn, lane) : 0u;
+      const cplx seg_c_n =
+          sn < a.nseg ? load_seg_carry(ts, a.nseg, sn, ne, lane) : cplx{0.0, 0.0};
       const int deg = __ldg(a.seg_deg + s);
       const int D = seg_deg_D(deg), DM = seg_deg_DM(deg);
-      if (!k3_narrow(DM)) continue;
-      const SegGeom g = seg_geom(a, s);
-      const SegFrame f = seg_frame(g);
-      if (batched && g.tid != cached_tid) {
-        warp_load_table(a.mtb + g.tid, mx, ne, lane);
-        cached_tid = g.tid;
+      if (k3_narrow(DM)) {
+        const SegGeom g = seg_geom(a, s);
+        const SegFrame f = seg_frame(g);
+        if (batched && g.tid != cached_tid) {
+          warp_load_table(a.mtb + g.tid, mx, ne, lane);
+          cached_tid = g.tid;
+        }
+        LaneRun r;
+        double zp, zl;
+        lane_load_w(a, g, word, lane, r, zp, zl);
+        seg_compute<MS, WIDE>(a, P, mx, o, g, f, D, DM, seg_c, r, zp, zl, lane, carries, su);
       }
-      const cplx seg_c = load_seg_carry(ts, a.nseg, s, ne, lane);
-      LaneRun r;
-      double zp, zl;
-      lane_load(a, g, s, lane, r, zp, zl);
-      seg_compute<MS, WIDE>(a, P, mx, o, g, f, D, DM, seg_c, r, zp, zl, lane, carries, su);
+      s = sn;
+      word = word_n;
+      seg_c = seg_c_n;
     }
   } else {
     __syncthreads();
