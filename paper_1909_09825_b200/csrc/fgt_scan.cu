@@ -1736,7 +1736,10 @@ __global__ void __launch_bounds__(kPlanThreads)
 // block aggregates (one CTA per q), per-block down-sweep writing carries.
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 4;
+#ifndef FGT_SCAN_ITEMS
+#define FGT_SCAN_ITEMS 2
+#endif
+constexpr int kScanItems = FGT_SCAN_ITEMS;
 constexpr int kScanBlock = kScanThreads * kScanItems;
 
 struct Pair {
