@@ -224,7 +224,10 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // Segment walk of one warp: chunks of kWalkChunk consecutive segments dealt
 // round-robin over the warps (consecutive segments keep prefetch chains and
 // metadata in L1; round-robin chunks keep clustered work balanced).
-constexpr int64_t kWalkChunk = 16;
+#ifndef FGT_WALK_CHUNK
+#define FGT_WALK_CHUNK 8
+#endif
+constexpr int64_t kWalkChunk = FGT_WALK_CHUNK;
 struct WarpWalk {
   int64_t wid, nwarps, nseg;
   __device__ __forceinline__ int64_t first() const {
@@ -1736,6 +1739,13 @@ __global__ void __launch_bounds__(kPlanThreads)
 // block aggregates (one CTA per q), per-block down-sweep writing carries.
 
 constexpr int kScanThreads = 256;
+// Grid caps (CTAs per SM) of K1 and of the K3 non-streaming variants.
+#ifndef FGT_K1_GRID
+#define FGT_K1_GRID 16
+#endif
+#ifndef FGT_K3_GRID
+#define FGT_K3_GRID 64
+#endif
 #ifndef FGT_SCAN_ITEMS
 #define FGT_SCAN_ITEMS 2
 #endif
@@ -2006,7 +2016,7 @@ cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const Mod
   if (a.nseg == 0) return cudaSuccess;
   const int64_t per_cta = (int64_t)kSegWarps * (a.mtb ? kBatchGroup : 1);
   int64_t want = (a.nseg + per_cta - 1) / per_cta;
-  const int64_t cap = (int64_t)num_sms() * 16;
+  const int64_t cap = (int64_t)num_sms() * FGT_K1_GRID;
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   if (a.nwide1 != 0) {
     note_launch();
@@ -2058,7 +2068,7 @@ static cudaError_t launch_seg_main_variant(const StreamArgs& a, const ModeParams
   if constexpr (!k3_stream<WIDE>()) {
     const int64_t per_cta = (int64_t)kSegWarps * (a.mtb ? kBatchGroup : 1);
     want = (a.nseg + per_cta - 1) / per_cta;
-    cap = (int64_t)num_sms() * 8;
+    cap = (int64_t)num_sms() * FGT_K3_GRID;
   } else {
     // streaming: one resident wave, contiguous segment ranges per warp
     int per_sm = 0;
