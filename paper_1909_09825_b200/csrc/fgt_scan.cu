@@ -1013,8 +1013,11 @@ __device__ __forceinline__ void seg_aggregate_lanes(const ModeTable& mt, int ne,
 // moment path for narrow segments (WIDE = false) and per-element lane
 // aggregates reduced across the warp for the others (WIDE = true); each
 // skips the other's segments.
+#ifndef FGT_K1_MINB
+#define FGT_K1_MINB 4
+#endif
 template <bool WIDE>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, FGT_K1_MINB)
     seg_aggregate_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
                          TileState ts) {
   __shared__ ModeTable tabs[kSegWarps];
@@ -1738,7 +1741,10 @@ __global__ void __launch_bounds__(kPlanThreads)
 // reversed segment order.  Three phases: per-block reduce, top-level scan of
 // block aggregates (one CTA per q), per-block down-sweep writing carries.
 
-constexpr int kScanThreads = 256;
+#ifndef FGT_SCAN_THREADS
+#define FGT_SCAN_THREADS 128
+#endif
+constexpr int kScanThreads = FGT_SCAN_THREADS;
 // Grid caps (CTAs per SM) of K1 and of the K3 non-streaming variants.
 #ifndef FGT_K1_GRID
 #define FGT_K1_GRID 16

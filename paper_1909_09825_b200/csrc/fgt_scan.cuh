@@ -15,7 +15,10 @@ namespace fgt_b200 {
 #endif
 constexpr int kR = FGT_KR;              // merged elements per lane run
 constexpr int kSeg = 32 * kR;           // merged elements per segment (one warp)
-constexpr int kSegWarps = 4;            // segments (warps) per CTA in K1 / K3
+#ifndef FGT_SEG_WARPS
+#define FGT_SEG_WARPS 4
+#endif
+constexpr int kSegWarps = FGT_SEG_WARPS;  // segments (warps) per CTA in K1 / K3
 constexpr int kThreads = 32 * kSegWarps;
 constexpr int kMaxMom = kMaxDeg;        // highest moment order of the expansions
 #ifndef FGT_PLAN_SEGS
