@@ -172,7 +172,10 @@ __device__ __forceinline__ void warp_load_table(const ModeTable* g, ModeTable& s
 static_assert(offsetof(ModeTable, coef) == sizeof(double) * 4 * kMaxModes, "table layout");
 
 // Consecutive segments a warp walks in batched plans before striding.
-constexpr int kBatchGroup = 16;
+#ifndef FGT_BATCH_GROUP
+#define FGT_BATCH_GROUP 16
+#endif
+constexpr int kBatchGroup = FGT_BATCH_GROUP;
 
 // ---- TMA bulk staging on mbarriers
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -1745,9 +1748,13 @@ __global__ void __launch_bounds__(kPlanThreads)
 #define FGT_SCAN_THREADS 128
 #endif
 constexpr int kScanThreads = FGT_SCAN_THREADS;
-// Grid caps (CTAs per SM) of K1 and of the K3 non-streaming variants.
+// Grid caps (CTAs per SM) of K1 and of the K3 non-streaming variants; waves
+// of resident CTAs for the streaming (wide) K3.
+#ifndef FGT_K3W_WAVES
+#define FGT_K3W_WAVES 32
+#endif
 #ifndef FGT_K1_GRID
-#define FGT_K1_GRID 16
+#define FGT_K1_GRID 64
 #endif
 #ifndef FGT_K3_GRID
 #define FGT_K3_GRID 64
@@ -2083,7 +2090,7 @@ static cudaError_t launch_seg_main_variant(const StreamArgs& a, const ModeParams
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     want = (a.nseg + kSegWarps - 1) / kSegWarps;
-    cap = (int64_t)num_sms() * per_sm;
+    cap = (int64_t)num_sms() * per_sm * FGT_K3W_WAVES;
   }
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   note_launch();
