@@ -1539,8 +1539,11 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
   const double* gx = c.x + ib;
   const double* gy = c.y + jb;
   const Stage stx = stage_plan(gx, nx), sty = stage_plan(gy, ny);
-  double* sx = tsm + stx.head;                  // [kPlanTile + 1] (sentinel)
-  double* sy = tsm + (kPlanTile + 2) + sty.head;
+  // one buffer for both sets (nx + ny <= kPlanTile): x (+ sentinel) first,
+  // y from the next even slot (16-byte aligned interiors)
+  const int oy = (stx.head + nx + 1 + 1) & ~1;
+  double* sx = tsm + stx.head;
+  double* sy = tsm + oy + sty.head;
   if (t == 0) {
     sflags = 0;
     mbar_init(&bar);
@@ -1989,7 +1992,7 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
                               uint32_t* seg_mask, double2* seg_gap, int* flags, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * 2 * (kPlanTile + 2);  // + head slot, sentinel
+  const size_t smem = sizeof(double) * (kPlanTile + 8);  // both sets, heads, sentinels
   static std::atomic<unsigned long long> done{0};
   cudaError_t e = ensure_dynamic_smem(plan_tile_kernel, (int)smem, done);
   if (e != cudaSuccess) return e;
@@ -2010,7 +2013,7 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
   const BatchArgs b{xs, ys, t_off, s_off, seg_base, tile_base, tile_tid};
   note_launch(2);
   batch_partition_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(b, ntiles, tile_ib);
-  const size_t smem = sizeof(double) * 2 * (kPlanTile + 2);  // + head slot, sentinel
+  const size_t smem = sizeof(double) * (kPlanTile + 8);  // both sets, heads, sentinels
   static std::atomic<unsigned long long> done{0};
   cudaError_t e = ensure_dynamic_smem(batch_plan_tile_kernel, (int)smem, done);
   if (e != cudaSuccess) return e;
