@@ -1474,6 +1474,9 @@ struct TileCtx {
   int tid;
 };
 
+#ifndef FGT_PLAN_MINB
+#define FGT_PLAN_MINB 6
+#endif
 constexpr int kPlanPer = 16;                         // merged positions per thread
 constexpr int kPlanThreads = kPlanTile / kPlanPer;
 static_assert(kPlanPer == 16 && kSeg % kPlanPer == 0, "plan tile layout");
@@ -1668,7 +1671,7 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
   }
 }
 
-__global__ void __launch_bounds__(kPlanThreads)
+__global__ void __launch_bounds__(kPlanThreads, FGT_PLAN_MINB)
     plan_tile_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
                      int64_t N, const int64_t* __restrict__ tile_ib, int64_t nseg,
                      int check_sorted, int64_t* __restrict__ seg_ib, double2* __restrict__ seg_z,
@@ -1731,7 +1734,7 @@ __global__ void batch_partition_kernel(BatchArgs b, int64_t ntiles, int64_t* __r
   tile_ib[gt] = merge_path(c.x, c.M, c.y, c.N, c.d0);
 }
 
-__global__ void __launch_bounds__(kPlanThreads)
+__global__ void __launch_bounds__(kPlanThreads, FGT_PLAN_MINB)
     batch_plan_tile_kernel(BatchArgs b, const int64_t* __restrict__ tile_ib,
                            int64_t* __restrict__ seg_ib, int64_t* __restrict__ seg_jb,
                            int4* __restrict__ seg_info, double2* __restrict__ seg_z,
