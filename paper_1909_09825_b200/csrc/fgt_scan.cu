@@ -231,6 +231,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 #define FGT_WALK_CHUNK 8
 #endif
 constexpr int64_t kWalkChunk = FGT_WALK_CHUNK;
+static_assert((kWalkChunk & (kWalkChunk - 1)) == 0, "walk chunk: power of two");
 struct WarpWalk {
   int64_t wid, nwarps, nseg;
   __device__ __forceinline__ int64_t first() const {
@@ -238,8 +239,11 @@ struct WarpWalk {
     return s < nseg ? s : nseg;
   }
   __device__ __forceinline__ int64_t next(int64_t s) const {
-    if ((s + 1) % kWalkChunk != 0 && s + 1 < nseg) return s + 1;
-    const int64_t c = (s / kWalkChunk + nwarps) * kWalkChunk;
+    // unsigned mask / shift (s >= 0): a signed 64-bit % or / costs more
+    const uint64_t n1 = (uint64_t)s + 1;
+    if ((n1 & (uint64_t)(kWalkChunk - 1)) != 0 && (int64_t)n1 < nseg) return (int64_t)n1;
+    const int64_t c = (int64_t)((((uint64_t)s / (uint64_t)kWalkChunk) + (uint64_t)nwarps) *
+                                (uint64_t)kWalkChunk);
     return c < nseg ? c : nseg;
   }
 };
