@@ -1605,27 +1605,35 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
     int i = merge_path_smem(sx, nx, sy, ny, d0);
     int j = d0 - i;
     if ((d0 % kSeg) == 0) sib[d0 / kSeg] = i;
-    double cx = sx[i < nx ? i : nx];
-    double cy = sy[j < ny ? j : ny];
+    // no index clamps: on sorted input the merge never reads past a set's
+    // sentinel; on unsorted input (flagged, redone after the sort) it can
+    // run up to kPlanPer past it, into the buffer's padding
+    double cx = sx[i];
+    double cy = sy[j];
     double zp = fmax(i > 0 ? sx[i - 1] : -INFINITY, j > 0 ? sy[j - 1] : -INFINITY);
     const bool seg_start = (d0 % kSeg) == 0;
-#pragma unroll
-    for (int e = 0; e < kPlanPer; ++e) {
-      if (d0 + e < len) {
-        const bool tgt = !(cy <= cx);  // sources first on ties
-        const double z = tgt ? cx : cy;
-        if (e > 0 || !seg_start) gmx = fmax(gmx, z - zp);
-        if (e == 0) zfirst = z;
-        zp = z;
-        bits |= (unsigned)tgt << e;
-        if (tgt) {
-          ++i;
-          cx = sx[i < nx ? i : nx];
-        } else {
-          ++j;
-          cy = sy[j < ny ? j : ny];
-        }
+    auto step = [&](int e) {
+      const bool tgt = !(cy <= cx);  // sources first on ties
+      const double z = tgt ? cx : cy;
+      if (e > 0 || !seg_start) gmx = fmax(gmx, z - zp);
+      if (e == 0) zfirst = z;
+      zp = z;
+      bits |= (unsigned)tgt << e;
+      if (tgt) {
+        ++i;
+        cx = sx[i];
+      } else {
+        ++j;
+        cy = sy[j];
       }
+    };
+    if (d0 + kPlanPer <= len) {
+#pragma unroll
+      for (int e = 0; e < kPlanPer; ++e) step(e);
+    } else {
+#pragma unroll
+      for (int e = 0; e < kPlanPer; ++e)
+        if (d0 + e < len) step(e);
     }
   }
   // per segment (16 threads = half a warp): largest gap, first coordinate
@@ -1999,7 +2007,8 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
                               uint32_t* seg_mask, double2* seg_gap, int* flags, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  const size_t smem = sizeof(double) * (kPlanTile + 8);  // both sets, heads, sentinels
+  // both sets, heads, sentinels + padding for merge overruns on unsorted input
+  const size_t smem = sizeof(double) * (kPlanTile + 8 + 2 * kPlanPer);
   static std::atomic<unsigned long long> done{0};
   cudaError_t e = ensure_dynamic_smem(plan_tile_kernel, (int)smem, done);
   if (e != cudaSuccess) return e;
@@ -2020,7 +2029,8 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
   const BatchArgs b{xs, ys, t_off, s_off, seg_base, tile_base, tile_tid};
   note_launch(2);
   batch_partition_kernel<<<(unsigned)((ntiles + 255) / 256), 256, 0, st>>>(b, ntiles, tile_ib);
-  const size_t smem = sizeof(double) * (kPlanTile + 8);  // both sets, heads, sentinels
+  // both sets, heads, sentinels + padding for merge overruns on unsorted input
+  const size_t smem = sizeof(double) * (kPlanTile + 8 + 2 * kPlanPer);
   static std::atomic<unsigned long long> done{0};
   cudaError_t e = ensure_dynamic_smem(batch_plan_tile_kernel, (int)smem, done);
   if (e != cudaSuccess) return e;
