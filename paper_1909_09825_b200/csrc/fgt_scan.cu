@@ -670,7 +670,7 @@ __device__ __forceinline__ void dispatch_pass2(int D, const ModeTable& mt, int n
 template <int DM>
 __device__ __forceinline__ void carries_moments(const ModeTable& mt, int ne, const LaneRun& r,
                                                 const SegFrame& f, double zp, double zl,
-                                                int lane, cplx seg_term, Carry* out) {
+                                                int lane, const cplx* terms, Carry* out) {
   double P[DM + 1], S[DM + 1];
   {
     double M[DM + 1];
@@ -715,13 +715,10 @@ __device__ __forceinline__ void carries_moments(const ModeTable& mt, int ne, con
       bs.re = fma(cn.re, S[n], bs.re);
       bs.im = fma(cn.im, S[n], bs.im);
     }
-    // segment carries propagated to the frame: lane k holds mode k's forward
-    // term, lane ne + k the backward one
-    cplx tf, tb;
-    tf.re = __shfl_sync(0xffffffffu, seg_term.re, k);
-    tf.im = __shfl_sync(0xffffffffu, seg_term.im, k);
-    tb.re = __shfl_sync(0xffffffffu, seg_term.re, ne + k);
-    tb.im = __shfl_sync(0xffffffffu, seg_term.im, ne + k);
+    // segment carries propagated to the frame (shared memory, written by
+    // lanes k and ne + k: broadcast reads)
+    const cplx tf = terms[k];
+    const cplx tb = terms[ne + k];
     const cplx eu = horner<DM>(c, u);
     const cplx ev = horner<DM>(c, -v);
     out[k].cf = cmul(eu, cplx{fp.re + tf.re, fp.im + tf.im});
@@ -811,7 +808,8 @@ __device__ __forceinline__ void wide_modes(const ModeTable& mt, int ne, int D, c
 
 // Per-warp region of K3: lane carries, then the output staging.
 __host__ __device__ __forceinline__ size_t warp_region_bytes(int ne) {
-  return sizeof(Carry) * 32 * (size_t)ne + sizeof(double) * kSeg;
+  // lane carries, output staging, segment-carry terms
+  return sizeof(Carry) * 32 * (size_t)ne + sizeof(double) * kSeg + sizeof(cplx) * 2 * kMaxModes;
 }
 
 // ------------------------------------------------------------------- K1
@@ -1220,17 +1218,18 @@ __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParam
   const int ne = P.ne;
   Carry* mine = carries + lane * ne;
   if constexpr (!WIDE) {
+    cplx* terms = reinterpret_cast<cplx*>(su + kSeg);  // [2 kMaxModes]
     switch (DM) {
 #define FGT_CM(n)                                                                   \
   case n: {                                                                         \
-    Coef<n> c;                                                                      \
-    cplx term = {0.0, 0.0};                                                         \
     if (lane < 2 * ne) {                                                            \
+      Coef<n> c;                                                                    \
       const int k = lane < ne ? lane : lane - ne;                                   \
       c.load(mx, k);                                                                \
-      term = cmul(horner<n>(c, lane < ne ? f.h0 : f.h1), seg_c);                    \
+      terms[lane] = cmul(horner<n>(c, lane < ne ? f.h0 : f.h1), seg_c);             \
     }                                                                               \
-    carries_moments<n>(mx, ne, r, f, zp, zl, lane, term, mine);                     \
+    __syncwarp();                                                                   \
+    carries_moments<n>(mx, ne, r, f, zp, zl, lane, terms, mine);                    \
   } break;
       FGT_CM(0) FGT_CM(1) FGT_CM(2) FGT_CM(3) FGT_CM(4) FGT_CM(5)
 #if FGT_K3_MOMENTS >= 6
