@@ -782,7 +782,7 @@ __device__ __forceinline__ void lane_scan(cplx A, cplx F, cplx G, int lane, cplx
 // exp(-s g) per element and mode.
 template <bool MS>
 __device__ __forceinline__ void wide_modes(const ModeTable& mt, int ne, int D, const LaneRun& r,
-                                           int lane, cplx seg_c, double (&out)[kR],
+                                           int lane, const cplx* terms, double (&out)[kR],
                                            const ModeSumsOut& ms) {
   for (int k = 0; k < ne; ++k) {
     cplx d[kR];
@@ -795,9 +795,8 @@ __device__ __forceinline__ void wide_modes(const ModeTable& mt, int ne, int D, c
       G.re = fma(r.b[i], A.re, G.re);
       G.im = fma(r.b[i], A.im, G.im);
     }
-    const cplx cfs = {__shfl_sync(0xffffffffu, seg_c.re, k), __shfl_sync(0xffffffffu, seg_c.im, k)};
-    const cplx cbs = {__shfl_sync(0xffffffffu, seg_c.re, ne + k),
-                      __shfl_sync(0xffffffffu, seg_c.im, ne + k)};
+    const cplx cfs = terms[k];  // segment carries (shared memory, broadcast)
+    const cplx cbs = terms[ne + k];
     cplx cf, cb;
     lane_scan(A, F, G, lane, cfs, cbs, cf, cb);
     chains_mode<MS>(d, mt.mw[k], r, cf, cb, k, out, ms);
@@ -1259,7 +1258,12 @@ __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParam
   if constexpr (!WIDE)
     dispatch_pass2<MS>(D, mx, ne, r, mine, out, ms);
   else
-    wide_modes<MS>(mx, ne, D, r, lane, seg_c, out, ms);
+  {
+    cplx* terms = reinterpret_cast<cplx*>(su + kSeg);
+    if (lane < 2 * ne) terms[lane] = seg_c;
+    __syncwarp();
+    wide_modes<MS>(mx, ne, D, r, lane, terms, out, ms);
+  }
   if constexpr (!MS) {
     int tk = r.tfirst;
 #pragma unroll
