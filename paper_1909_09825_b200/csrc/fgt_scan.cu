@@ -641,21 +641,27 @@ __device__ __forceinline__ void pass2(const ModeTable& mt, int ne, const LaneRun
   }
 }
 
-template <bool MS>
+// Degrees above MAXD are never requested by the caller; they fall through to
+// the MAXD (or, for MAXD = kMaxDeg, the exact) instantiation, so the kernel
+// only carries the code (and register demand) of the degrees it can see.
+template <bool MS, int MAXD>
 __device__ __forceinline__ void dispatch_pass2(int D, const ModeTable& mt, int ne,
                                                const LaneRun& r, const Carry* carry,
                                                double (&out)[kR], const ModeSumsOut& ms) {
   switch (D) {
-#define FGT_P2(n)                                 \
-  case n:                                         \
-    pass2<n, MS>(mt, ne, r, carry, out, ms);      \
-    break;
+#define FGT_P2(n)                                   \
+  case n:                                           \
+    if constexpr (n <= MAXD) {                      \
+      pass2<n, MS>(mt, ne, r, carry, out, ms);      \
+      return;                                       \
+    }                                               \
+    [[fallthrough]];
     FGT_P2(0) FGT_P2(1) FGT_P2(2) FGT_P2(3) FGT_P2(4) FGT_P2(5) FGT_P2(6) FGT_P2(7)
     FGT_P2(8) FGT_P2(9) FGT_P2(10) FGT_P2(11) FGT_P2(12) FGT_P2(13) FGT_P2(14)
     FGT_P2(15) FGT_P2(16)
 #undef FGT_P2
     default:
-      pass2<-1, MS>(mt, ne, r, carry, out, ms);
+      pass2<(MAXD < kMaxDeg ? MAXD : -1), MS>(mt, ne, r, carry, out, ms);
   }
 }
 
@@ -916,6 +922,14 @@ __device__ __forceinline__ int seg_moment_degree(const ModeParams& P, double sma
 #endif
 constexpr int kK3Moments = FGT_K3_MOMENTS;
 static_assert(kK3Moments >= 0 && kK3Moments <= kRegDeg, "K3 moment degree");
+// Largest gap-factor degree of a narrow segment: every gap is at most
+// h0 + h1 <= 2 rmax[DM] / |s|, and 2 rmax[5] = 0.0117 < rmax[6] = 0.0167
+// (rmax[D] = ((D+1)! 2^-54)^(1/(D+1))), so DM <= 5 implies D <= 6.
+#ifndef FGT_NARROW_MAXD
+#define FGT_NARROW_MAXD (kK3Moments <= 5 ? 6 : kMaxDeg)
+#endif
+constexpr int kNarrowMaxD = FGT_NARROW_MAXD;
+static_assert(kNarrowMaxD >= 6 && kNarrowMaxD <= kMaxDeg, "narrow degree bound");
 // Highest lane-moment degree of the K1 wide path.
 #ifndef FGT_LANE_MOM_MAX
 #define FGT_LANE_MOM_MAX 12
@@ -1256,7 +1270,7 @@ __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParam
   const ModeSumsOut ms = MS ? ModeSumsOut{o.hp, o.hm, a.M, o.u_offset + g.ib + r.tfirst}
                             : ModeSumsOut{nullptr, nullptr, 0, 0};
   if constexpr (!WIDE)
-    dispatch_pass2<MS>(D, mx, ne, r, mine, out, ms);
+    dispatch_pass2<MS, kNarrowMaxD>(D, mx, ne, r, mine, out, ms);
   else
   {
     cplx* terms = reinterpret_cast<cplx*>(su + kSeg);
