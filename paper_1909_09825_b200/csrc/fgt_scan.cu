@@ -732,6 +732,118 @@ __device__ __forceinline__ void carries_moments(const ModeTable& mt, int ne, con
   }
 }
 
+// Collapsed form (narrow segments, potentials only).  Every exponential of a
+// narrow segment has |s t| <= rmax[DN] with DN the degree for its full width
+// h0 + h1, so the modes fold into ONE real polynomial
+//   G(t) = Re sum_k mw_k e^{-s_k t} = sum_{n<=DN} g_n t^n,  g_n = Re sum_k mw_k c_kn
+// (c_kn = (-s_k)^n/n!, the table's Taylor coefficients).  With w = z - zc,
+// v_j = z_j - zc, Pre_m / Tot_m = prefix / total over the segment's sources of
+// b v^m, and the segment carries at the frame centre Tf_k = e^{-s_k h0} Cf_k,
+// Tb_k = e^{-s_k h1} Cb_k, a target's potential is a degree-DN polynomial in
+// its own w:
+//   u = sum_q w^q [ E_q + sum_{m+q odd} 2 (-1)^m C(m+q, m) g_{m+q} Pre_m ]
+//   E_q = Re sum_k mw_k c_kq (Tf_k + (-1)^q Tb_k)
+//         + (-1)^q sum_m C(m+q, m) g_{m+q} Tot_m
+// (forward pairs sum_n g_n (w - v)^n, backward pairs sum_n g_n (v - w)^n, and
+// Suf = Tot - Pre).  Mode-independent per element: no gap factors, no chains.
+// Terms: each is bounded by sum|mw| (|s| 2h)^n / n! |b|, so the rounding stays
+// at eps sum|mw| sum|b| like the per-mode form.
+__host__ __device__ constexpr double binom_c(int n, int m) {
+  double r = 1.0;
+  for (int i = 1; i <= m; ++i) r = r * (n - m + i) / i;
+  return r;
+}
+
+template <int DN>
+__device__ __forceinline__ void collapsed_segment(const ModeTable& mt, int ne, const LaneRun& r,
+                                                  const SegFrame& f, int lane,
+                                                  const cplx* terms, double* su) {
+  constexpr int NM = DN + 1;
+  double pre[NM], tot[NM];
+  {
+    double M[NM];
+#pragma unroll
+    for (int n = 0; n < NM; ++n) M[n] = 0.0;
+#pragma unroll
+    for (int e = 0; e < kR; ++e) {
+      const double d = r.g[e] - f.zc;  // r.g holds coordinates here
+      double p = r.b[e];
+      M[0] += p;
+#pragma unroll
+      for (int n = 1; n < NM; ++n) {
+        p *= d;
+        M[n] += p;
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NM; ++n) {
+      double incl = M[n];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      tot[n] = __shfl_sync(0xffffffffu, incl, 31);
+      pre[n] = incl - M[n];
+    }
+  }
+  // g_n and the carry part of E_n on lane n
+  double gl = 0.0, cl = 0.0;
+  if (lane < NM) {
+    const double sg = (lane & 1) ? -1.0 : 1.0;
+    for (int k = 0; k < ne; ++k) {
+      const cplx x = cmul(mt.mw[k], mt.coef[k][lane]);
+      const cplx tf = terms[k], tb = terms[ne + k];
+      gl += x.re;
+      cl = fma(x.re, fma(sg, tb.re, tf.re), fma(-x.im, fma(sg, tb.im, tf.im), cl));
+    }
+  }
+  double g[NM], E[NM];
+#pragma unroll
+  for (int n = 0; n < NM; ++n) {
+    g[n] = __shfl_sync(0xffffffffu, gl, n);
+    E[n] = __shfl_sync(0xffffffffu, cl, n);
+  }
+#pragma unroll
+  for (int q = 0; q < NM; ++q) {
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m + q < NM; ++m) acc = fma(binom_c(m + q, m) * g[m + q], tot[m], acc);
+    E[q] += (q & 1) ? -acc : acc;
+  }
+  // odd-order pair coefficients H(m, q) = 2 (-1)^m C(m+q, m) g_{m+q}
+  double H[NM][NM];
+#pragma unroll
+  for (int q = 0; q < NM; ++q)
+#pragma unroll
+    for (int m = 0; m < NM; ++m)
+      H[m][q] = (((m + q) & 1) && m + q < NM)
+                    ? ((m & 1) ? -2.0 : 2.0) * binom_c(m + q, m) * g[(m + q) < NM ? m + q : 0]
+                    : 0.0;
+  int tk = r.tfirst;
+#pragma unroll
+  for (int e = 0; e < kR; ++e) {
+    const double w = r.g[e] - f.zc;
+    double p = r.b[e];  // 0 for targets: the prefix is exclusive for them
+    pre[0] += p;
+#pragma unroll
+    for (int m = 1; m < NM; ++m) {
+      p *= w;
+      pre[m] += p;
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int q = DN; q >= 0; --q) {
+      double c = E[q];
+#pragma unroll
+      for (int m = 0; m + q < NM; ++m)
+        if ((m + q) & 1) c = fma(H[m][q], pre[m], c);
+      acc = q == DN ? c : fma(acc, w, c);
+    }
+    if (r.tmask & (1u << e)) su[tk++] = acc;
+  }
+}
+
 // Lane carries by shuffle (Kogge-Stone) scans of the lane aggregates (A, F,
 // G) across the warp, both directions, seeded with the segment carries
 // (cfs at the element before the segment, cbs at its last element).
@@ -929,7 +1041,7 @@ static_assert(kK3Moments >= 0 && kK3Moments <= kRegDeg, "K3 moment degree");
 #define FGT_NARROW_MAXD (kK3Moments <= 5 ? 6 : kMaxDeg)
 #endif
 constexpr int kNarrowMaxD = FGT_NARROW_MAXD;
-static_assert(kNarrowMaxD >= 6 && kNarrowMaxD <= kMaxDeg, "narrow degree bound");
+static_assert(kNarrowMaxD >= 6 && kNarrowMaxD <= 8, "narrow degree bound");
 // Highest lane-moment degree of the K1 wide path.
 #ifndef FGT_LANE_MOM_MAX
 #define FGT_LANE_MOM_MAX 12
@@ -942,6 +1054,8 @@ __device__ __forceinline__ bool k3_narrow(int DM) { return DM >= 0 && DM <= kK3M
 
 __device__ __forceinline__ int seg_deg_D(int deg) { return (deg & 0xff) - 1; }
 __device__ __forceinline__ int seg_deg_DM(int deg) { return ((deg >> 8) & 0xff) - 1; }
+// degree of the collapsed form (full segment width h0 + h1)
+__device__ __forceinline__ int seg_deg_DN(int deg) { return ((deg >> 16) & 0xff) - 1; }
 
 __device__ __forceinline__ double seg_smax(const StreamArgs& a, const SegGeom& g, double smax) {
   return a.mtb ? __ldg(&a.mtb[g.tid].smax) : smax;
@@ -1201,7 +1315,9 @@ __global__ void classify_kernel(StreamArgs a, ModeParams P, double smax,
       // one from the element before it (as the kernels' lane runs see them)
       const double2 gz = seg_gap[s];
       const int D = pick_degree(P, sm, fmax(gz.x, gz.y - g.zprev));
-      seg_deg[s] = (D + 1) | ((DM + 1) << 8);
+      const SegFrame f = seg_frame(g);
+      const int DN = pick_degree(P, sm, f.h0 + f.h1);
+      seg_deg[s] = (D + 1) | ((DM + 1) << 8) | ((DN + 1) << 16);
       w1 = !k1_narrow(DM);
       w3 = !k3_narrow(DM);
     }
@@ -1226,11 +1342,39 @@ template <bool MS, bool WIDE>
 __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParams& P,
                                             const ModeTable& mx, const OutArgs& o,
                                             const SegGeom& g, const SegFrame& f, int D, int DM,
-                                            cplx seg_c, LaneRun& r, double zp, double zl,
+                                            int DN, cplx seg_c, LaneRun& r, double zp, double zl,
                                             int lane, Carry* carries, double* su) {
   const int ne = P.ne;
   Carry* mine = carries + lane * ne;
-  if constexpr (!WIDE) {
+  if constexpr (!WIDE && !MS) {
+    (void)D;
+    (void)DM;
+    (void)zp;
+    (void)zl;
+    (void)mine;
+    cplx* terms = reinterpret_cast<cplx*>(su + kSeg);  // [2 kMaxModes]
+    switch (DN <= kNarrowMaxD ? DN : kNarrowMaxD) {
+#define FGT_CS(n)                                                                   \
+  case n:                                                                           \
+    if constexpr (n <= kNarrowMaxD) {                                               \
+      if (lane < 2 * ne) {                                                          \
+        Coef<n> c;                                                                  \
+        const int k = lane < ne ? lane : lane - ne;                                 \
+        c.load(mx, k);                                                              \
+        terms[lane] = cmul(horner<n>(c, lane < ne ? f.h0 : f.h1), seg_c);           \
+      }                                                                             \
+      __syncwarp();                                                                 \
+      collapsed_segment<n>(mx, ne, r, f, lane, terms, su);                          \
+      break;                                                                        \
+    }                                                                               \
+    [[fallthrough]];
+      FGT_CS(0) FGT_CS(1) FGT_CS(2) FGT_CS(3) FGT_CS(4) FGT_CS(5) FGT_CS(6) FGT_CS(7)
+      FGT_CS(8)
+#undef FGT_CS
+      default:
+        break;
+    }
+  } else if constexpr (!WIDE) {
     cplx* terms = reinterpret_cast<cplx*>(su + kSeg);  // [2 kMaxModes]
     switch (DM) {
 #define FGT_CM(n)                                                                   \
@@ -1260,29 +1404,32 @@ __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParam
     }
     static_assert(kK3Moments >= 5, "FGT_CM cases");
   }
+  if constexpr (WIDE || MS) {
 #pragma unroll
-  for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
-  r.g[0] -= zp;
-  if constexpr (!WIDE) __syncwarp();
-  double out[kR];
+    for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
+    r.g[0] -= zp;
+    if constexpr (!WIDE) __syncwarp();
+    double out[kR];
 #pragma unroll
-  for (int e = 0; e < kR; ++e) out[e] = 0.0;
-  const ModeSumsOut ms = MS ? ModeSumsOut{o.hp, o.hm, a.M, o.u_offset + g.ib + r.tfirst}
-                            : ModeSumsOut{nullptr, nullptr, 0, 0};
-  if constexpr (!WIDE)
-    dispatch_pass2<MS, kNarrowMaxD>(D, mx, ne, r, mine, out, ms);
-  else
-  {
-    cplx* terms = reinterpret_cast<cplx*>(su + kSeg);
-    if (lane < 2 * ne) terms[lane] = seg_c;
-    __syncwarp();
-    wide_modes<MS>(mx, ne, D, r, lane, terms, out, ms);
+    for (int e = 0; e < kR; ++e) out[e] = 0.0;
+    const ModeSumsOut ms = MS ? ModeSumsOut{o.hp, o.hm, a.M, o.u_offset + g.ib + r.tfirst}
+                              : ModeSumsOut{nullptr, nullptr, 0, 0};
+    if constexpr (!WIDE) {
+      dispatch_pass2<MS, kNarrowMaxD>(D, mx, ne, r, mine, out, ms);
+    } else {
+      cplx* terms = reinterpret_cast<cplx*>(su + kSeg);
+      if (lane < 2 * ne) terms[lane] = seg_c;
+      __syncwarp();
+      wide_modes<MS>(mx, ne, D, r, lane, terms, out, ms);
+    }
+    if constexpr (!MS) {
+      int tk = r.tfirst;
+#pragma unroll
+      for (int e = 0; e < kR; ++e)
+        if (r.tmask & (1u << e)) su[tk++] = out[e];
+    }
   }
   if constexpr (!MS) {
-    int tk = r.tfirst;
-#pragma unroll
-    for (int e = 0; e < kR; ++e)
-      if (r.tmask & (1u << e)) su[tk++] = out[e];
     __syncwarp();
     const int64_t base = o.u_offset + g.ib;
     if (o.tperm) {
@@ -1318,10 +1465,11 @@ __device__ __forceinline__ cplx load_seg_carry(const TileState& ts, int64_t nseg
 #ifndef FGT_K3W_MINB
 #define FGT_K3W_MINB 3
 #endif
-// Streaming (TMA-staged) segment loop per variant; measured on B200: the
-// narrow kernel is FP64-latency bound and gains nothing, see DESIGN.md.
+// Streaming (TMA-staged) segment loop per variant.  Both stream: the narrow
+// kernel's collapsed form leaves it bound by its load latency, which the
+// stage hides (cfg 3 K3 2.49 -> 1.52 ms on B200).
 #ifndef FGT_K3_STREAM
-#define FGT_K3_STREAM 0
+#define FGT_K3_STREAM 1
 #endif
 #ifndef FGT_K3W_STREAM
 #define FGT_K3W_STREAM 1
@@ -1394,7 +1542,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
       const cplx seg_c = lane < 2 * ne ? sp.car[lane] : cplx{0.0, 0.0};
       __syncwarp();  // stage free: the next segment's copies go in now
       const int64_t sn = issue_next(walk.next(s));
-      seg_compute<MS, WIDE>(a, P, mx, o, g, f, D, DM, seg_c, r, zp, zl, lane, carries, su);
+      seg_compute<MS, WIDE>(a, P, mx, o, g, f, D, DM, seg_deg_DN(deg), seg_c, r, zp, zl, lane, carries, su);
       s = sn;
     }
   } else if constexpr (!WIDE) {
@@ -1425,7 +1573,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
         LaneRun r;
         double zp, zl;
         lane_load_w(a, g, word, lane, r, zp, zl);
-        seg_compute<MS, WIDE>(a, P, mx, o, g, f, D, DM, seg_c, r, zp, zl, lane, carries, su);
+        seg_compute<MS, WIDE>(a, P, mx, o, g, f, D, DM, seg_deg_DN(deg), seg_c, r, zp, zl, lane, carries, su);
       }
       s = sn;
       word = word_n;
@@ -1453,7 +1601,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
         LaneRun r;
         double zp, zl;
         lane_load(a, g, s, lane, r, zp, zl);
-        seg_compute<MS, WIDE>(a, P, mx, o, g, f, D, DM, seg_c, r, zp, zl, lane, carries, su);
+        seg_compute<MS, WIDE>(a, P, mx, o, g, f, D, DM, seg_deg_DN(deg), seg_c, r, zp, zl, lane, carries, su);
       }
     }
   }
