@@ -152,6 +152,7 @@ void build_modes(const Soe& folded, double delta, ModeParams& P, ModeTable& T) {
   P.ne = ne;
   const double isq = 1.0 / std::sqrt(delta);
   double smax = 0.0;
+  long double gpoly[kCollDeg + 1] = {};
   for (int k = 0; k < ne; ++k) {
     const double sre = folded.nodes[k].real() * isq;
     const double sim = folded.nodes[k].imag() * isq;
@@ -165,11 +166,18 @@ void build_modes(const Soe& folded, double delta, ModeParams& P, ModeTable& T) {
     smax = std::fmax(smax, std::hypot(sre, sim));
     std::complex<long double> c(1.0L, 0.0L);
     const std::complex<long double> ms(-(long double)sre, -(long double)sim);
+    const std::complex<long double> lmw((long double)mw.real(), (long double)mw.imag());
     for (int n = 0; n <= kMaxDeg; ++n) {
       T.coef[k][n] = {(double)c.real(), (double)c.imag()};
+      if (n <= kCollDeg) {
+        const std::complex<long double> x = lmw * c;
+        T.mwc[k][n] = {(double)x.real(), (double)x.imag()};
+        gpoly[n] += x.real();
+      }
       c = c * ms / (long double)(n + 1);
     }
   }
+  for (int n = 0; n <= kCollDeg; ++n) T.gpoly[n] = (double)gpoly[n];
   P.smax = smax;
   T.smax = smax;
   fill_rmax(P);

@@ -157,6 +157,8 @@ __device__ __forceinline__ void load_mode_table(const ModeTable* g, ModeTable& s
 
 // One warp copies a transform's mode table (the rows of its ne modes) into
 // its shared-memory slot (batched plans).
+// COLL: also the collapsed-form rows (narrow K3 only).
+template <bool COLL = false>
 __device__ __forceinline__ void warp_load_table(const ModeTable* g, ModeTable& s, int ne,
                                                 int lane) {
   __syncwarp();
@@ -167,6 +169,15 @@ __device__ __forceinline__ void warp_load_table(const ModeTable* g, ModeTable& s
   const int n = kHead + kRow * ne;
   for (int i = lane; i < n; i += 32) dst[i] = __ldg(src + i);
   if (lane == 0) s.smax = __ldg(&g->smax);
+  if constexpr (COLL) {
+  // collapsed-form rows and polynomial
+  constexpr int kOff = offsetof(ModeTable, mwc) / sizeof(double);
+  constexpr int kCRow = 2 * (kCollDeg + 1);
+  const int nc = kCRow * ne;
+  for (int i = lane; i < nc; i += 32) dst[kOff + i] = __ldg(src + kOff + i);
+  constexpr int kOffG = offsetof(ModeTable, gpoly) / sizeof(double);
+  if (lane <= kCollDeg) dst[kOffG + lane] = __ldg(src + kOffG + lane);
+  }
   __syncwarp();
 }
 static_assert(offsetof(ModeTable, coef) == sizeof(double) * 4 * kMaxModes, "table layout");
@@ -788,20 +799,19 @@ __device__ __forceinline__ void collapsed_segment(const ModeTable& mt, int ne, c
     }
   }
   // g_n and the carry part of E_n on lane n
-  double gl = 0.0, cl = 0.0;
+  double cl = 0.0;
   if (lane < NM) {
     const double sg = (lane & 1) ? -1.0 : 1.0;
     for (int k = 0; k < ne; ++k) {
-      const cplx x = cmul(mt.mw[k], mt.coef[k][lane]);
+      const cplx x = mt.mwc[k][lane];
       const cplx tf = terms[k], tb = terms[ne + k];
-      gl += x.re;
       cl = fma(x.re, fma(sg, tb.re, tf.re), fma(-x.im, fma(sg, tb.im, tf.im), cl));
     }
   }
   double g[NM], E[NM];
 #pragma unroll
   for (int n = 0; n < NM; ++n) {
-    g[n] = __shfl_sync(0xffffffffu, gl, n);
+    g[n] = mt.gpoly[n];
     E[n] = __shfl_sync(0xffffffffu, cl, n);
   }
 #pragma unroll
@@ -840,7 +850,7 @@ __device__ __forceinline__ void collapsed_segment(const ModeTable& mt, int ne, c
         if ((m + q) & 1) c = fma(H[m][q], pre[m], c);
       acc = q == DN ? c : fma(acc, w, c);
     }
-    if (r.tmask & (1u << e)) su[tk++] = acc;
+    if (r.tmask & (1u << e)) su[tk++] = acc;  // staged: coalesced stores after
   }
 }
 
@@ -1041,7 +1051,7 @@ static_assert(kK3Moments >= 0 && kK3Moments <= kRegDeg, "K3 moment degree");
 #define FGT_NARROW_MAXD (kK3Moments <= 5 ? 6 : kMaxDeg)
 #endif
 constexpr int kNarrowMaxD = FGT_NARROW_MAXD;
-static_assert(kNarrowMaxD >= 6 && kNarrowMaxD <= 8, "narrow degree bound");
+static_assert(kNarrowMaxD >= 6 && kNarrowMaxD <= kCollDeg, "narrow degree bound");
 // Highest lane-moment degree of the K1 wide path.
 #ifndef FGT_LANE_MOM_MAX
 #define FGT_LANE_MOM_MAX 12
@@ -1292,6 +1302,16 @@ __global__ void batch_modes_kernel(BatchModeBase base, const double* __restrict_
   }
   T.smax = smax;
   T.pad = 0.0;
+  for (int n = 0; n <= kCollDeg; ++n) {
+    double gn = 0.0;
+    for (int k = 0; k < kMaxModes; ++k) {
+      const cplx x = cmul(T.mw[k], T.coef[k][n]);
+      T.mwc[k][n] = x;
+      gn += x.re;
+    }
+    T.gpoly[n] = gn;
+  }
+  T.pad2 = 0.0;
 }
 
 // Plan-time segment classes: counts[0] = K1 wide segments, counts[1] = K3.
@@ -1529,7 +1549,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
       const int deg = __ldg(a.seg_deg + s);
       const int D = seg_deg_D(deg), DM = seg_deg_DM(deg);
       if (batched && g.tid != cached_tid) {
-        warp_load_table(a.mtb + g.tid, mx, ne, lane);
+        warp_load_table<!WIDE && !MS>(a.mtb + g.tid, mx, ne, lane);
         cached_tid = g.tid;
       }
       cp_async_wait_all();
@@ -1567,7 +1587,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
         const SegGeom g = seg_geom(a, s);
         const SegFrame f = seg_frame(g);
         if (batched && g.tid != cached_tid) {
-          warp_load_table(a.mtb + g.tid, mx, ne, lane);
+          warp_load_table<!WIDE && !MS>(a.mtb + g.tid, mx, ne, lane);
           cached_tid = g.tid;
         }
         LaneRun r;
@@ -1594,7 +1614,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
         const SegGeom g = seg_geom(a, s);
         const SegFrame f = seg_frame(g);
         if (batched && g.tid != cached_tid) {
-          warp_load_table(a.mtb + g.tid, mx, ne, lane);
+          warp_load_table<!WIDE && !MS>(a.mtb + g.tid, mx, ne, lane);
           cached_tid = g.tid;
         }
         const cplx seg_c = load_seg_carry(ts, a.nseg, s, ne, lane);
@@ -1933,6 +1953,9 @@ __global__ void __launch_bounds__(kPlanThreads, FGT_PLAN_MINB)
 constexpr int kScanThreads = FGT_SCAN_THREADS;
 // Grid caps (CTAs per SM) of K1 and of the K3 non-streaming variants; waves
 // of resident CTAs for the streaming (wide) K3.
+#ifndef FGT_K3N_WAVES
+#define FGT_K3N_WAVES 32
+#endif
 #ifndef FGT_K3W_WAVES
 #define FGT_K3W_WAVES 32
 #endif
@@ -2275,7 +2298,7 @@ static cudaError_t launch_seg_main_variant(const StreamArgs& a, const ModeParams
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     want = (a.nseg + kSegWarps - 1) / kSegWarps;
-    cap = (int64_t)num_sms() * per_sm * FGT_K3W_WAVES;
+    cap = (int64_t)num_sms() * per_sm * (WIDE ? FGT_K3W_WAVES : FGT_K3N_WAVES);
   }
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   note_launch();

@@ -29,12 +29,20 @@ constexpr int kPlanTile = kPlanSegs * kSeg;  // merged elements per plan tile
 
 // Per-mode constants laid out in device memory (plan-owned): s_k, mw_k and the
 // Taylor coefficients c_{k,n} = (-s_k)^n / n! of exp(-s_k g).
+// Highest degree of the collapsed (mode-folded) polynomial of narrow segments.
+constexpr int kCollDeg = 8;
+
 struct ModeTable {
   cplx s[kMaxModes];
   cplx mw[kMaxModes];
   cplx coef[kMaxModes][kMaxDeg + 1];
   double smax;  // max_k |s_k| (degree selection)
   double pad;
+  // collapsed form of narrow segments (fgt_scan.cu collapsed_segment):
+  // mwc[k][n] = mw_k coef[k][n], gpoly[n] = Re sum_k mwc[k][n]
+  cplx mwc[kMaxModes][kCollDeg + 1];
+  double gpoly[kCollDeg + 1];
+  double pad2;
 };
 
 struct StreamArgs {
