@@ -6,6 +6,7 @@ import sys
 from collections import defaultdict
 
 rows = list(csv.reader(open(sys.argv[1])))
+SORTCOL = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 acc = defaultdict(lambda: [0, 0, ""])
 fname = "?"
@@ -31,5 +32,5 @@ for r in rows:
         acc[cur][1] += int(float(r[icol] or 0))
         total += s
 print("total samples", total)
-for k, (s, n, src) in sorted(acc.items(), key=lambda kv: -kv[1][0])[:top]:
+for k, (s, n, src) in sorted(acc.items(), key=lambda kv: -kv[1][SORTCOL])[:top]:
     print(f"{100.0 * s / max(total, 1):5.1f}% {s:7d} {n:11d} {k[0]}:{k[1]:<5d} {src}")
