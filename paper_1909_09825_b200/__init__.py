@@ -15,7 +15,8 @@ from .transform import (BatchPlan, TransformPlan, TransformRequest, apply_genera
                         batch_transform, chebyshev_points, delta_sweep, direct, gen_points,
                         measure_error,
                         direct_transform, gauss_transform, gauss_transform_device, mode_sums, plan,
-                        precompute_gap_table, uniform_points, uniform_points_array)
+                        precompute_gap_table, transform_host, uniform_points,
+                        uniform_points_array)
 
 __version__ = "0.1.0"
 
@@ -24,7 +25,7 @@ __all__ = [
     "SoeForm", "TransformPlan", "TransformRequest", "chebyshev_points", "delta_sweep",
     "error_grid_point", "gen_points", "max_error", "max_error_extended", "measure_error",
     "apply_general", "apply_same", "cf_soe", "direct", "direct_transform", "evaluate", "fold",
-    "gauss_transform", "gauss_transform_device", "load_coefficient_table", "mode_count_for_tolerance", "mode_sums", "plan",
+    "gauss_transform", "gauss_transform_device", "transform_host", "load_coefficient_table", "mode_count_for_tolerance", "mode_sums", "plan",
     "precompute_gap_table", "preset_mode_count", "preset_soe", "save_coefficient_table",
     "soe_for_tolerance", "unfold", "uniform_points", "uniform_points_array", "validate",
 ]

@@ -62,6 +62,8 @@ SIGNATURES = {
     "fgt_chunk_carries": (_I, [_PD, _I, _I, _PD]),
     "fgt_gauss_transform": (_I, [_PD, _I64, _PD, _I64, _PD, _D, _PD, _PD, _PD, _PD, _PU8, _I, _I,
                                  _I, _I, _PD]),
+    "fgt_transform_host": (_I, [_PD, _I64, _PD, _I64, _PD, _D, _PD, _PD, _PD, _PD, _PU8, _I, _I,
+                                _PD, _I, _VP]),
     "fgt_direct": (_I, [_PD, _I64, _PD, _I64, _PD, _D, _PI64, _I64, _PD]),
     "fgt_uniform_points_device": (_I, [_VP, _I64, _U64, _U64, _U64, _VP]),
     "fgt_sort_device": (_I, [_VP, _I64, _VP, _VP, _VP]),

@@ -10,10 +10,12 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <complex>
 #include <mutex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -586,6 +588,396 @@ void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in_host, double* potentia
   ck(cudaStreamSynchronize(st), "sync");
 }
 
+// ------------------------------------------------ pipelined host transform
+//
+// One-shot transform from host buffers with the PCIe copies overlapped.  A
+// plan-then-apply call must upload x, y, alpha and download u back to back
+// (57 ms of link time at N = M = 1e8); here the sources go first, the
+// targets follow in G chunks, and each chunk's potentials download while
+// the next chunk's targets upload (the link is full duplex), so the
+// download hides behind the target upload.  This works because a chunk's
+// aggregates (A, F, G of the merged-stream chunk) depend on its
+// sources and its two boundary coordinates only: they are computed from
+// source-only chunk plans while the targets are still in flight, the
+// carries follow with the multi-GPU chunk algebra (fgt_chunk_carries), and
+// every target chunk is planned and finished as soon as it lands.  Chunk
+// boundaries are merge-path splits of the host arrays.
+//
+// The device work is queued without host round trips (a small device ->
+// host copy on the compute stream would queue behind the multi-megabyte
+// potential downloads on the copy engine): the chunk plans' checks land in
+// one flag array read once per phase, and the kernel variants of both
+// segment classes run (each skips the other's segments).  Sortedness and
+// finiteness are checked on the device (chunk tile passes) and at the chunk
+// boundaries on the host; any violation drops to the full plan / apply path
+// on the already uploaded arrays, which sorts, reports errors and returns
+// the reference's results and exceptions.
+
+int64_t merge_split_host(const double* x, int64_t M, const double* y, int64_t N, int64_t d) {
+  // targets among the first d merged elements (sources first on ties)
+  int64_t lo = d - N > 0 ? d - N : 0, hi = d < M ? d : M;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) / 2;
+    if (x[mid - 1] < y[d - mid])
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// decay_factor (transform.cpp:60-68) on the host: 1 at d = 0, exactly 0 past
+// the underflow exponent.
+std::complex<double> host_decay(double sre, double sim, double d) {
+  if (d == 0.0) return {1.0, 0.0};
+  if (sre * d > 745.0) return {0.0, 0.0};
+  return std::exp(std::complex<double>(-sre * d, -sim * d));
+}
+
+// Pipeline sizes: merged points below which one plan / apply is used, and
+// merged points per chunk.  The environment variables FGT_PIPE_MIN /
+// FGT_PIPE_CHUNK override them (test hook: many small chunks).
+int64_t pipe_knob(const char* name, int64_t dflt) {
+  const char* v = std::getenv(name);
+  if (!v || !*v) return dflt;
+  const long long n = std::atoll(v);
+  return n > 0 ? (int64_t)n : dflt;
+}
+
+// Chunk plan over device slices, queued on st with no host round trip: the
+// checks (sortedness of each slice included) land in flag[0..7], segment
+// classes stay unknown.  The caller owns flag.
+fgt_plan_s* pipe_chunk_plan(const double* dx, int64_t M, const double* dy, int64_t N,
+                            const Soe& soe, double delta, const ModeTable& T, const ModeParams& P,
+                            double zprev, int* flag, cudaStream_t st) {
+  fgt_plan_s* p = new fgt_plan_s();
+  try {
+    ck(cudaGetDevice(&p->device), "cudaGetDevice");
+    p->M = M;
+    p->N = N;
+    p->soe = soe;
+    p->P = P;
+    p->delta = delta;
+    p->stream = st;
+    p->ntiles = (M + N + kSeg - 1) / kSeg;
+    p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
+    p->d_seg_z = dmalloc<double2>(p->ntiles, st);
+    p->d_seg_gap = dmalloc<double2>(p->ntiles, st);
+    p->d_seg_deg = dmalloc<int>(p->ntiles, st);
+    p->d_seg_mask = dmalloc<uint32_t>((size_t)p->ntiles * (kSeg / 32), st);
+    p->d_xs = const_cast<double*>(dx);
+    p->d_ys = const_cast<double*>(dy);
+    p->own_xs = p->own_ys = false;
+    p->d_flag = flag;
+    plan_tiles(p, dx, dy, true, st);
+    p->d_mt = dmalloc<ModeTable>(1, st);
+    ck(launch_store_table(T, p->d_mt, st), "store mode table");
+    p->zprev0 = zprev;
+    const StreamArgs sa = stream_args(p, nullptr);
+    ck(launch_classify(sa, p->P, p->P.smax, p->d_seg_gap, p->d_seg_deg, nullptr,
+                       class_counts(p), st),
+       "classify");
+    p->nwide1 = p->nwide3 = -1;
+  } catch (...) {
+    p->d_flag = nullptr;
+    destroy_plan(p);
+    throw;
+  }
+  return p;
+}
+void pipe_chunk_destroy(fgt_plan_s* p) {
+  p->d_flag = nullptr;  // owned by the pipeline
+  destroy_plan(p);
+}
+
+struct PipeChunk {
+  int64_t i0, i1, j0, j1;
+  double zprev, zlast;
+};
+
+struct PipeStreams {
+  cudaStream_t in = nullptr, out = nullptr;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t event() {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ev.push_back(e);
+    return e;
+  }
+  ~PipeStreams() {
+    if (in) cudaStreamSynchronize(in);
+    if (out) cudaStreamSynchronize(out);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (in) cudaStreamDestroy(in);
+    if (out) cudaStreamDestroy(out);
+  }
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  explicit PinnedBuf(size_t n) { ck(cudaMallocHost(&p, n), "pinned buffer"); }
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+// Plan / apply (host or device pointers per flags) for the small and the
+// fallback cases.
+void plan_apply(const double* x, int64_t M, const double* y, int64_t N, const double* a,
+                double* u, double delta, const Soe& soe, uint32_t flags, cudaStream_t st) {
+  std::vector<double> tr, ti, wr, wi;
+  std::vector<uint8_t> sc;
+  for (size_t k = 0; k < soe.nodes.size(); ++k) {
+    tr.push_back(soe.nodes[k].real());
+    ti.push_back(soe.nodes[k].imag());
+    wr.push_back(soe.weights[k].real());
+    wi.push_back(soe.weights[k].imag());
+    sc.push_back(soe.self_conj[k]);
+  }
+  fgt_plan_t p = nullptr;
+  int rc = fgt_plan_create(x, M, y, N, delta, tr.data(), ti.data(), wr.data(), wi.data(),
+                           sc.data(), (int)tr.size(), FGT_SOE_FOLDED, flags, -1, st, &p);
+  if (rc != FGT_OK) raise(rc, g_last_error);
+  rc = fgt_apply_general(p, a, N, u, 1, flags, st);
+  fgt_plan_destroy(p);
+  if (rc != FGT_OK) raise(rc, g_last_error);
+}
+
+void transform_host(const double* x, int64_t M, const double* y, int64_t N, const double* alpha,
+                    double* u, double delta, const Soe& soe, cudaStream_t st) {
+  if (M == 0) return;
+  const int64_t L = M + N;
+  if (N == 0 || L < pipe_knob("FGT_PIPE_MIN", (int64_t)1 << 22)) {
+    plan_apply(x, M, y, N, alpha, u, delta, soe, 0, st);
+    return;
+  }
+  // chunks of the merged stream (merge path on the host arrays; validated below)
+  int64_t G = L / pipe_knob("FGT_PIPE_CHUNK", 12500000);
+  G = G < 2 ? 2 : (G > 64 ? 64 : G);
+  std::vector<PipeChunk> ch(G);
+  bool ok = true;
+  int64_t ip = 0;
+  for (int64_t g = 0; g < G; ++g) {
+    const int64_t d0 = L * g / G, d1 = L * (g + 1) / G;
+    const int64_t i1 = g + 1 == G ? M : merge_split_host(x, M, y, N, d1);
+    PipeChunk& c = ch[g];
+    c.i0 = ip;
+    c.i1 = i1;
+    c.j0 = d0 - ip;
+    c.j1 = d1 - i1;
+    ok = ok && c.i1 >= c.i0 && c.j1 >= c.j0;
+    ip = i1;
+  }
+  if (ok) {
+    // merged element before the chunk / the chunk's last one: the larger of
+    // the last target and the last source so far (sorted prefixes)
+    auto last = [&](int64_t i, int64_t j) {
+      const double a = i > 0 ? x[i - 1] : -INFINITY, b = j > 0 ? y[j - 1] : -INFINITY;
+      return a > b ? a : b;
+    };
+    for (int64_t g = 0; g < G; ++g) {
+      PipeChunk& c = ch[g];
+      // boundary order between chunks (each chunk's inside is checked on the device)
+      if (c.i0 > 0 && c.i0 < M) ok = ok && x[c.i0 - 1] <= x[c.i0];
+      if (c.j0 > 0 && c.j0 < N) ok = ok && y[c.j0 - 1] <= y[c.j0];
+      c.zprev = g == 0 ? std::fmin(x[0], y[0]) : last(c.i0, c.j0);
+      c.zlast = last(c.i1, c.j1);
+    }
+  }
+  const int ne = (int)soe.nodes.size();
+  ModeParams P;
+  ModeTable T;
+  build_modes(soe, delta, P, T);
+  // FGT_PIPE_TRACE=1: host timestamps of the phases and device arrival
+  // times of the target chunks on stderr
+  const bool trace = pipe_knob("FGT_PIPE_TRACE", 0) != 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto stamp = [&](const char* what) {
+    if (trace)
+      std::fprintf(stderr, "pipe %-24s %8.3f ms\n", what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                       .count());
+  };
+
+  double* dx = dmalloc<double>(M, st);
+  double* dy = dmalloc<double>(N, st);
+  double* da = dmalloc<double>(N, st);
+  double* du = dmalloc<double>(M, st);
+  int* dflag = dmalloc<int>((size_t)2 * G * kFlagInts, st);
+  cplx* d_agg = dmalloc<cplx>((size_t)G * 3 * ne, st);
+  cplx* d_car = dmalloc<cplx>((size_t)G * 2 * ne, st);
+  struct Free {
+    cudaStream_t st;
+    std::vector<void*> p;
+    ~Free() {
+      for (void* q : p) cudaFreeAsync(q, st);
+      cudaStreamSynchronize(st);
+    }
+  } fr{st, {dx, dy, da, du, dflag, d_agg, d_car}};
+  ck(cudaMemsetAsync(dflag, 0, sizeof(int) * 2 * G * kFlagInts, st), "flags");
+  PipeStreams ps;
+  ck(cudaStreamCreateWithFlags(&ps.in, cudaStreamNonBlocking), "stream");
+  ck(cudaStreamCreateWithFlags(&ps.out, cudaStreamNonBlocking), "stream");
+  // the buffers were allocated on st: the copy streams start after that
+  cudaEvent_t ready = ps.event();
+  ck(cudaEventRecord(ready, st), "event");
+  ck(cudaStreamWaitEvent(ps.in, ready, 0), "wait");
+  auto h2d = [&](double* d, const double* h, int64_t n) {
+    if (n > 0)
+      ck(cudaMemcpyAsync(d, h, sizeof(double) * n, cudaMemcpyHostToDevice, ps.in), "upload");
+  };
+  // the full path on the uploaded arrays: sorts, checks, reference errors
+  auto fallback = [&]() {
+    ck(cudaStreamSynchronize(ps.in), "upload sync");
+    ck(cudaStreamSynchronize(ps.out), "download sync");
+    ck(cudaStreamSynchronize(st), "sync");
+    plan_apply(dx, M, dy, N, da, du, delta, soe, FGT_DEVICE_PTRS, st);
+    ck(cudaMemcpyAsync(u, du, sizeof(double) * M, cudaMemcpyDeviceToHost, st), "download");
+    ck(cudaStreamSynchronize(st), "download sync");
+  };
+  if (!ok) {  // not sorted (or NaN at a split)
+    h2d(dx, x, M);
+    h2d(dy, y, N);
+    h2d(da, alpha, N);
+    return fallback();
+  }
+  // every upload is queued up front: sources by chunk, then targets by chunk
+  std::vector<cudaEvent_t> ev_src(G), ev_tgt(G);
+  for (int64_t g = 0; g < G; ++g) {
+    h2d(dy + ch[g].j0, y + ch[g].j0, ch[g].j1 - ch[g].j0);
+    h2d(da + ch[g].j0, alpha + ch[g].j0, ch[g].j1 - ch[g].j0);
+    ev_src[g] = ps.event();
+    ck(cudaEventRecord(ev_src[g], ps.in), "event");
+  }
+  std::vector<cudaEvent_t> tev;  // trace: timing events on the copy streams
+  auto tmark = [&](cudaStream_t s) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    tev.push_back(e);
+  };
+  tmark(ps.in);
+  for (int64_t g = 0; g < G; ++g) {
+    h2d(dx + ch[g].i0, x + ch[g].i0, ch[g].i1 - ch[g].i0);
+    ev_tgt[g] = ps.event();
+    ck(cudaEventRecord(ev_tgt[g], ps.in), "event");
+  }
+  tmark(ps.in);
+  stamp("uploads queued");
+  PinnedBuf pin(sizeof(cplx) * (size_t)G * 5 * ne + sizeof(int) * 2 * G * kFlagInts);
+  cplx* h_agg = static_cast<cplx*>(pin.p);   // [G][3 ne]: A', F', G' (source span)
+  cplx* h_car = h_agg + (size_t)G * 3 * ne;  // [G][2 ne]: carries
+  int* h_flag = reinterpret_cast<int*>(h_car + (size_t)G * 2 * ne);
+  auto flags_bad = [&](int64_t g0, int64_t g1) {
+    for (int64_t g = g0; g < g1; ++g) {
+      const int* f = h_flag + g * kFlagInts;
+      if (f[0] || f[1] || f[3] || f[4]) return true;
+    }
+    return false;
+  };
+  // phase 1: aggregates of every chunk from its sources alone
+  for (int64_t g = 0; g < G; ++g) {
+    const PipeChunk& c = ch[g];
+    const int64_t Ng = c.j1 - c.j0;
+    if (!Ng) continue;
+    ck(cudaStreamWaitEvent(st, ev_src[g], 0), "wait");
+    fgt_plan_s* p = pipe_chunk_plan(dx, 0, dy + c.j0, Ng, soe, delta, T, P, c.zprev,
+                                    dflag + g * kFlagInts, st);
+    {
+      Work w{st, {}};
+      const StreamArgs sa = stream_args(p, da + c.j0);
+      const TileState ts =
+          tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, ne)), p->ntiles, ne);
+      ck(launch_aggregate(sa, P, p->d_mt, ts, st), "chunk aggregates");
+      ck(launch_carry_scan(ts, p->ntiles, ne, nullptr, d_agg + g * 3 * ne, st), "chunk totals");
+    }
+    pipe_chunk_destroy(p);
+  }
+  ck(cudaMemcpyAsync(h_agg, d_agg, sizeof(cplx) * G * 3 * ne, cudaMemcpyDeviceToHost, st),
+     "aggregates");
+  ck(cudaMemcpyAsync(h_flag, dflag, sizeof(int) * G * kFlagInts, cudaMemcpyDeviceToHost, st),
+     "flags");
+  ck(cudaStreamSynchronize(st), "aggregates sync");
+  stamp("sources + aggregates");
+  if (flags_bad(0, G)) return fallback();
+  // extend each source span to the chunk's last merged element, then the
+  // carry algebra of the multi-GPU path
+  std::vector<double> aggs((size_t)G * 6 * ne);
+  using C = std::complex<double>;
+  C* A = reinterpret_cast<C*>(aggs.data());
+  for (int64_t g = 0; g < G; ++g) {
+    const PipeChunk& c = ch[g];
+    const bool src = c.j1 > c.j0;
+    const double ylast = src ? y[c.j1 - 1] : c.zprev;
+    for (int k = 0; k < ne; ++k) {
+      const C e = host_decay(P.s_re[k], P.s_im[k], c.zlast - ylast);
+      C a1(1.0, 0.0), f1(0.0, 0.0), g1(0.0, 0.0);
+      if (src) {
+        const cplx* h = h_agg + g * 3 * ne;
+        a1 = C(h[k].re, h[k].im);
+        f1 = C(h[ne + k].re, h[ne + k].im);
+        g1 = C(h[2 * ne + k].re, h[2 * ne + k].im);
+      }
+      A[g * 3 * ne + k] = a1 * e;
+      A[g * 3 * ne + ne + k] = f1 * e;
+      A[g * 3 * ne + 2 * ne + k] = g1;
+    }
+  }
+  {
+    const int rc = fgt_chunk_carries(aggs.data(), (int)G, ne, reinterpret_cast<double*>(h_car));
+    if (rc != FGT_OK) raise(rc, g_last_error);
+  }
+  ck(cudaMemcpyAsync(d_car, h_car, sizeof(cplx) * G * 2 * ne, cudaMemcpyHostToDevice, st), "carries");
+  // phase 2: every target chunk is planned and finished as it lands; its
+  // potentials download on the out stream while the next chunk uploads
+  int* dflag2 = dflag + G * kFlagInts;
+  for (int64_t g = 0; g < G; ++g) {
+    const PipeChunk& c = ch[g];
+    const int64_t Mg = c.i1 - c.i0, Ng = c.j1 - c.j0;
+    if (!Mg) continue;
+    ck(cudaStreamWaitEvent(st, ev_tgt[g], 0), "wait");
+    fgt_plan_s* p = pipe_chunk_plan(dx + c.i0, Mg, dy + c.j0, Ng, soe, delta, T, P, c.zprev,
+                                    dflag2 + g * kFlagInts, st);
+    {
+      Work w{st, {}};
+      const StreamArgs sa = stream_args(p, Ng ? da + c.j0 : da);
+      const TileState ts =
+          tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, ne)), p->ntiles, ne);
+      ck(launch_aggregate(sa, P, p->d_mt, ts, st), "tile aggregates");
+      ck(launch_carry_scan(ts, p->ntiles, ne, d_car + g * 2 * ne, nullptr, st), "carry scan");
+      OutArgs o;
+      o.u = du + c.i0;
+      ck(launch_main(sa, P, p->d_mt, ts, o, st), "main pass");
+    }
+    pipe_chunk_destroy(p);
+    cudaEvent_t done = ps.event();
+    ck(cudaEventRecord(done, st), "event");
+    ck(cudaStreamWaitEvent(ps.out, done, 0), "wait");
+    if (g == 0) tmark(ps.out);
+    ck(cudaMemcpyAsync(u + c.i0, du + c.i0, sizeof(double) * Mg, cudaMemcpyDeviceToHost, ps.out),
+       "download");
+  }
+  tmark(ps.out);
+  stamp("phase 2 queued");
+  ck(cudaMemcpyAsync(h_flag + G * kFlagInts, dflag2, sizeof(int) * G * kFlagInts,
+                     cudaMemcpyDeviceToHost, st),
+     "flags");
+  ck(cudaStreamSynchronize(st), "sync");
+  if (flags_bad(G, 2 * G)) return fallback();
+  ck(cudaStreamSynchronize(ps.out), "download sync");
+  stamp("downloads done");
+  if (trace && tev.size() == 4) {
+    float a = 0.f, b = 0.f, c = 0.f;
+    cudaEventElapsedTime(&a, tev[0], tev[1]);
+    cudaEventElapsedTime(&b, tev[0], tev[2]);
+    cudaEventElapsedTime(&c, tev[0], tev[3]);
+    std::fprintf(stderr, "pipe device: targets uploaded %.3f, first download start %.3f, "
+                 "downloads done %.3f ms after the sources\n", a, b, c);
+  }
+  for (cudaEvent_t e : tev) cudaEventDestroy(e);
+}
+
 }  // namespace
 
 // ======================================================================= C
@@ -897,14 +1289,29 @@ int fgt_gauss_transform(const double* targets, int64_t M, const double* sources,
     n_modes = cnt;
     form = FGT_SOE_FOLDED;
   }
-  fgt_plan_t p = nullptr;
-  int rc = fgt_plan_create(targets, M, sources, N, delta, t_re, t_im, w_re, w_im, self_conj,
-                           n_modes, form, 0, -1, nullptr, &p);
-  if (rc != FGT_OK) return rc;
-  rc = p->same_points ? fgt_apply_same(p, strengths, N, potentials, threads, 0, nullptr)
-                      : fgt_apply_general(p, strengths, N, potentials, threads, 0, nullptr);
-  fgt_plan_destroy(p);
-  return rc;
+  // same_points: apply_same and apply_general agree on the merged stream
+  // (every source precedes its equal target), so one path serves both
+  (void)threads;
+  return fgt_transform_host(targets, M, sources, N, strengths, delta, t_re, t_im, w_re, w_im,
+                            self_conj, n_modes, form, potentials, -1, nullptr);
+}
+
+int fgt_transform_host(const double* targets, int64_t M, const double* sources, int64_t N,
+                       const double* strengths, double delta, const double* t_re,
+                       const double* t_im, const double* w_re, const double* w_im,
+                       const uint8_t* self_conj, int n_modes, int form, double* potentials,
+                       int device, void* stream) {
+  return guarded([&] {
+    if (M < 0 || N < 0) raise(FGT_ERR_INVALID, "negative point count");
+    if ((M > 0 && (!targets || !potentials)) || (N > 0 && (!sources || !strengths)))
+      raise(FGT_ERR_INVALID, "NULL buffer");
+    if (M >= ((int64_t)1 << 31) || N >= ((int64_t)1 << 31))
+      raise(FGT_ERR_INVALID, "at most 2^31-1 points per set");
+    check_delta(delta);
+    Soe soe = resolve_soe(t_re, t_im, w_re, w_im, self_conj, n_modes, form);
+    require_device(device);
+    transform_host(targets, M, sources, N, strengths, potentials, delta, soe, as_stream(stream));
+  });
 }
 
 }  // extern "C"

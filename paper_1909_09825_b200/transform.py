@@ -292,12 +292,35 @@ def gauss_transform(targets, sources, strengths, delta, soe=None, ne=4, threads=
     CUDA tensors are transformed on the device (gauss_transform_device)."""
     if _is_cuda_tensor(targets):
         return gauss_transform_device(targets, sources, strengths, delta, soe, ne)
-    req = TransformRequest(targets, sources, strengths, delta)
     use = (soe if soe.form == SoeForm.FOLDED else fold(soe)) if soe is not None else fold(
         cf_soe(2 * int(ne)))
-    p = plan(req, use, False)
-    res = apply_same(p, strengths, threads) if p.same_points else apply_general(p, strengths, threads)
-    return res.tolist()
+    return transform_host(targets, sources, strengths, delta, use).tolist()
+
+
+def transform_host(targets, sources, strengths, delta, soe):
+    """One-shot transform of host arrays through fgt_transform_host: the
+    plan -> apply_general result (apply_same agrees on identical sets), with
+    the PCIe uploads / downloads overlapped for large presorted inputs.
+    Validation order and error classes as plan() (transform.cpp:200-219)."""
+    x = _f64(targets)
+    y = _f64(sources)
+    a = _f64(strengths)
+    delta = float(delta)
+    if not (np.isfinite(delta) and delta > 0.0):
+        raise ValueError("delta must be positive and finite")
+    if not np.all(np.isfinite(x)):
+        raise ValueError("target coordinates must be finite")
+    if not np.all(np.isfinite(y)):
+        raise ValueError("source coordinates must be finite")
+    if a.size != y.size:
+        raise ValueError("one strength per source required")
+    validate(soe)
+    keep, sargs = _soe_args(soe)
+    u = np.empty(x.size)
+    _capi.check(_capi.lib().fgt_transform_host(_ptr(x), x.size, _ptr(y), y.size, _ptr(a), delta,
+                                               *sargs, _ptr(u), -1, None))
+    del keep
+    return u
 
 
 def direct_transform(targets, sources, strengths, delta):
