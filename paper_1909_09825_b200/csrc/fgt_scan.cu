@@ -934,9 +934,12 @@ __device__ __forceinline__ void wide_modes(const ModeTable& mt, int ne, int D, c
 // -------------------------------------------------------- shared memory
 
 // Per-warp region of K3: lane carries, then the output staging.
-__host__ __device__ __forceinline__ size_t warp_region_bytes(int ne) {
+// lane_carries: false for the collapsed narrow path (potentials only),
+// which keeps no per-lane carries in shared memory.
+__host__ __device__ __forceinline__ size_t warp_region_bytes(int ne, bool lane_carries = true) {
   // lane carries, output staging, segment-carry terms
-  return sizeof(Carry) * 32 * (size_t)ne + sizeof(double) * kSeg + sizeof(cplx) * 2 * kMaxModes;
+  return (lane_carries ? sizeof(Carry) * 32 * (size_t)ne : 0) + sizeof(double) * kSeg +
+         sizeof(cplx) * 2 * kMaxModes;
 }
 
 // ------------------------------------------------------------------- K1
@@ -1162,7 +1165,10 @@ template <bool WIDE>
 __global__ void __launch_bounds__(kThreads, FGT_K1_MINB)
     seg_aggregate_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
                          TileState ts) {
-  __shared__ ModeTable tabs[kSegWarps];
+  // one mode table per warp for batched plans, one per CTA otherwise
+  // (dynamic: the smaller footprint leaves more of the SM's L1 to the loads)
+  extern __shared__ __align__(16) unsigned char k1_smem[];
+  ModeTable* tabs = reinterpret_cast<ModeTable*>(k1_smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool batched = a.mtb != nullptr;
   if (!batched) load_mode_table(mtab, tabs[0]);
@@ -1353,7 +1359,7 @@ __global__ void classify_kernel(StreamArgs a, ModeParams P, double smax,
 // ------------------------------------------------------------------- K3
 
 #ifndef FGT_K3_MINB
-#define FGT_K3_MINB 4
+#define FGT_K3_MINB 5
 #endif
 // One segment of K3 once its lane runs are in registers (r.g = coordinates):
 // segment carries, lane carries (moment form for narrow segments, warp scans
@@ -1515,16 +1521,17 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
   const int ne = P.ne;
   const bool batched = a.mtb != nullptr;
   constexpr bool STREAM = k3_stream<WIDE>();
-  const size_t wbytes = warp_region_bytes(ne) + (STREAM ? kStageBytes : 0);
+  constexpr bool LC = WIDE || MS;  // lane carries kept in shared memory
+  const size_t wbytes = warp_region_bytes(ne, LC) + (STREAM ? kStageBytes : 0);
   unsigned char* wreg =
       smem_raw + sizeof(ModeTable) * (batched ? kSegWarps : 1) + (size_t)warp * wbytes;
   Carry* carries = reinterpret_cast<Carry*>(wreg);
-  double* su = reinterpret_cast<double*>(wreg + sizeof(Carry) * 32 * (size_t)ne);
+  double* su = reinterpret_cast<double*>(wreg + (LC ? sizeof(Carry) * 32 * (size_t)ne : 0));
   if (!batched) load_mode_table(mtab, tabs[0]);
   ModeTable& mx = batched ? tabs[warp] : tabs[0];
   int cached_tid = -1;
   if constexpr (STREAM) {
-    const StagePtrs sp = stage_ptrs(wreg + warp_region_bytes(ne));
+    const StagePtrs sp = stage_ptrs(wreg + warp_region_bytes(ne, LC));
     if (lane == 0) mbar_init(sp.bar);
     __syncthreads();
     const WarpWalk walk{(int64_t)blockIdx.x * kSegWarps + warp, (int64_t)gridDim.x * kSegWarps,
@@ -2175,9 +2182,9 @@ TileState tile_state_carve(cplx* base, int64_t nseg, int ne) {
   return TileState{base, base + nt, base + 2 * nt, base + 3 * nt, base + 4 * nt, base + 5 * nt};
 }
 
-size_t seg_smem_bytes(int ne, bool batched, bool stream) {
+size_t seg_smem_bytes(int ne, bool batched, bool stream, bool lane_carries) {
   return sizeof(ModeTable) * (batched ? kSegWarps : 1) +
-         (size_t)kSegWarps * (warp_region_bytes(ne) + (stream ? kStageBytes : 0));
+         (size_t)kSegWarps * (warp_region_bytes(ne, lane_carries) + (stream ? kStageBytes : 0));
 }
 
 cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int64_t N,
@@ -2229,7 +2236,7 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
 
 template <class K>
 static cudaError_t set_smem(K kernel, std::atomic<unsigned long long>& done) {
-  return ensure_dynamic_smem(kernel, (int)seg_smem_bytes(kMaxModes, true, true), done);
+  return ensure_dynamic_smem(kernel, (int)seg_smem_bytes(kMaxModes, true, true, true), done);
 }
 
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
@@ -2239,13 +2246,14 @@ cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const Mod
   int64_t want = (a.nseg + per_cta - 1) / per_cta;
   const int64_t cap = (int64_t)num_sms() * FGT_K1_GRID;
   const unsigned grid = (unsigned)(want < cap ? want : cap);
+  const size_t smem = sizeof(ModeTable) * (a.mtb ? kSegWarps : 1);
   if (a.nwide1 != 0) {
     note_launch();
-    seg_aggregate_kernel<true><<<grid, kThreads, 0, st>>>(a, P, mt, ts);
+    seg_aggregate_kernel<true><<<grid, kThreads, smem, st>>>(a, P, mt, ts);
   }
   if (a.nwide1 != a.nseg) {
     note_launch();
-    seg_aggregate_kernel<false><<<grid, kThreads, 0, st>>>(a, P, mt, ts);
+    seg_aggregate_kernel<false><<<grid, kThreads, smem, st>>>(a, P, mt, ts);
   }
   return cudaGetLastError();
 }
@@ -2284,7 +2292,7 @@ static cudaError_t launch_seg_main_variant(const StreamArgs& a, const ModeParams
   static std::atomic<unsigned long long> done{0};
   cudaError_t e = set_smem(seg_main_kernel<MS, WIDE>, done);
   if (e != cudaSuccess) return e;
-  const size_t smem = seg_smem_bytes(P.ne, a.mtb != nullptr, k3_stream<WIDE>());
+  const size_t smem = seg_smem_bytes(P.ne, a.mtb != nullptr, k3_stream<WIDE>(), WIDE || MS);
   int64_t want, cap;
   if constexpr (!k3_stream<WIDE>()) {
     const int64_t per_cta = (int64_t)kSegWarps * (a.mtb ? kBatchGroup : 1);

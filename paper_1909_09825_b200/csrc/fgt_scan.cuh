@@ -95,7 +95,7 @@ int64_t scan_blocks(int64_t nseg);
 size_t tile_state_elems(int64_t nseg, int ne);
 TileState tile_state_carve(cplx* base, int64_t nseg, int ne);
 
-size_t seg_smem_bytes(int ne, bool batched, bool stream);
+size_t seg_smem_bytes(int ne, bool batched, bool stream, bool lane_carries = true);
 
 cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int64_t N,
                              int64_t seg, int64_t nseg, int64_t* seg_ib, cudaStream_t st);

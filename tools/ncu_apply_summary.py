@@ -39,7 +39,9 @@ json.dump({"source": "ncu --set full --clock-control none (tools/profile_round.s
                      "(reduce/top/down), K3 narrow",
            "kernels": kern, "dram_bytes_per_apply": tot, "algorithmic_bytes_per_apply": 16 * 2e8},
           open("profiles/r01_apply_ncu.json", "w"), indent=1)
+k3 = [k for k in kern if "seg_main_kernel" in k["kernel"]]
 json.dump({"kernel": "apply = K1 + K2 + K3 (cfg3, N=M=1e8, n_e=6)", "dram_bytes_per_apply": tot,
+           "k3_dram_bytes_per_launch": k3[0]["dram_bytes"] if k3 else None,
            "source": "profiles/r01_apply_ncu.json (ncu --set full, dram__bytes_read.sum + "
                      "dram__bytes_write.sum over the apply's launches)"},
           open("profiles/traffic.json", "w"), indent=1)
