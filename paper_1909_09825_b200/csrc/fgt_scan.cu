@@ -394,8 +394,8 @@ __device__ __forceinline__ void lane_load_w(const StreamArgs& a, const SegGeom& 
 // b[kStageB] holds b at slot ob.  Bulk copies need 16-byte aligned source,
 // destination and size: an unaligned first / last element is copied by an
 // 8-byte cp.async instead (lanes 1..6).
-constexpr int kStageXY = kSeg + 4;
-constexpr int kStageB = kSeg + 2;
+constexpr int kStageXY = kSeg + 16;  // + alignment slots and slack for the branch-free decode
+constexpr int kStageB = kSeg + 12;
 // + mask words (32 B), segment carries (2 kMaxModes complex), mbarrier
 constexpr size_t kStageBytes =
     sizeof(double) * (kStageXY + kStageB) + 32 + sizeof(cplx) * 2 * kMaxModes + 16;
@@ -507,24 +507,21 @@ __device__ __forceinline__ void lane_load_stage(const StreamArgs& a, const SegGe
   const int j0 = (d0 < g.len ? d0 : g.len) - i0;
   r.tfirst = i0;
   r.tmask = byte;
+  // branch-free: one running slot per set, the element's set picks the slot
+  // (past the run, reads stay inside the stage's slack and are discarded)
+  int ix = so.ox + i0, iy = so.oy + j0, ib = j0;
   double last = 0.0;
 #pragma unroll
   for (int e = 0; e < kR; ++e) {
-    const int t = __popc(byte & ((1u << e) - 1u));
-    const int sidx = e - t;
-    if (e < nreal) {
-      if (byte & (1u << e)) {
-        r.g[e] = sx[i0 + t];
-        r.b[e] = 0.0;
-      } else {
-        r.g[e] = sy[j0 + sidx];
-        r.b[e] = sb[j0 + sidx];
-      }
-      last = r.g[e];
-    } else {
-      r.g[e] = 0.0;
-      r.b[e] = 0.0;
-    }
+    const bool tg = (byte >> e) & 1u;
+    const double v = xy[tg ? ix : iy];
+    const double bv = sb[ib];
+    r.g[e] = v;
+    r.b[e] = (tg || e >= nreal) ? 0.0 : bv;
+    if (e < nreal) last = v;
+    ix += tg;
+    iy += !tg;
+    ib += !tg;
   }
   double prev = __shfl_up_sync(0xffffffffu, last, 1);
   if (lane == 0) prev = g.zprev;
