@@ -489,8 +489,6 @@ __device__ __forceinline__ void lane_load_stage(const StreamArgs& a, const SegGe
                                                 uint32_t word, int lane, LaneRun& r, double& zp,
                                                 double& zl) {
   const StageSlots so = stage_slots(a, g);
-  const double* sx = xy + so.ox;
-  const double* sy = xy + so.oy;
   const double* sb = bb + so.ob;
   const int d0 = lane * kR;
   const int nreal = g.len - d0 < 0 ? 0 : (g.len - d0 < kR ? g.len - d0 : kR);
