@@ -353,8 +353,9 @@ StreamArgs stream_args(const fgt_plan_s* p, const double* bs) {
 // Queue the segment classification; the counts land in h[0..1] once the
 // stream is synchronized (see take_classes).
 void queue_classify(fgt_plan_s* p, unsigned long long* h, cudaStream_t st,
-                    bool check_flags = false) {
-  const StreamArgs sa = stream_args(p, nullptr);
+                    bool check_flags = false, bool zprev0_first = false) {
+  StreamArgs sa = stream_args(p, nullptr);
+  sa.zprev0_first = zprev0_first;
   ck(launch_classify(sa, p->P, p->P.smax, p->d_seg_gap, p->d_seg_deg,
                      check_flags ? p->d_flag : nullptr, class_counts(p), st),
      "classify");
@@ -1078,13 +1079,19 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       p->d_seg_mask = dmalloc<uint32_t>((size_t)p->ntiles * (kSeg / 32), st);
       // one read of both sets: checks + (speculative) segment metadata
       plan_tiles(p, xs.dptr, ys.dptr, !(flags & FGT_ASSUME_SORTED), st);
-      // flags and first coordinates in one round trip (pinned scratch)
+      upload_modes(p, st);
+      // speculative classification (valid when both sets are sorted: segment
+      // 0 starts at its own first element), flags, first coordinates and
+      // class counts in one round trip (pinned scratch)
       unsigned char* pin = pinned_scratch();
       int hfl[8] = {0};
       double xyl[2] = {0.0, 0.0};
+      unsigned long long hcl[2] = {0, 0};
       int* hf = pin ? reinterpret_cast<int*>(pin) : hfl;
       double* xy0 = pin ? reinterpret_cast<double*>(pin + 32) : xyl;
+      unsigned long long* hc = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hcl;
       xy0[0] = xy0[1] = 0.0;
+      queue_classify(p, hc, st, false, true);
       ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(int) * 8, cudaMemcpyDeviceToHost, st), "flags");
       if (M > 0) ck(cudaMemcpyAsync(xy0, xs.dptr, 8, cudaMemcpyDeviceToHost, st), "x0");
       if (N > 0) ck(cudaMemcpyAsync(xy0 + 1, ys.dptr, 8, cudaMemcpyDeviceToHost, st), "y0");
@@ -1105,11 +1112,13 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
         if (N > 0) ck(cudaMemcpyAsync(xy0 + 1, p->d_ys, 8, cudaMemcpyDeviceToHost, st), "y0");
         ck(cudaStreamSynchronize(st), "sorted sync");
       }
-      upload_modes(p, st);
       // coordinate before the first merged element: the element itself
       const double x0 = xy0[0], y0 = xy0[1];
       p->zprev0 = (M > 0 && N > 0) ? std::fmin(x0, y0) : (M > 0 ? x0 : y0);
-      classify_sync(p, st);
+      if (!p->t_sorted || !p->s_sorted)
+        classify_sync(p, st);
+      else
+        take_classes(p, hc);
     } catch (...) {
       for (void* t : temps) cudaFreeAsync(t, st);
       destroy_plan(p);

@@ -1329,12 +1329,13 @@ __global__ void classify_kernel(StreamArgs a, ModeParams P, double smax,
     const int64_t s = s0 + threadIdx.x;
     bool w1 = false, w3 = false;
     if (s < a.nseg) {
-      const SegGeom g = seg_geom(a, s);
+      SegGeom g = seg_geom(a, s);
+      const double2 gz = seg_gap[s];
+      if (s == 0 && a.zprev0_first) g.zprev = gz.y;
       const double sm = seg_smax(a, g, smax);
       const int DM = seg_moment_degree(P, sm, seg_frame(g));
       // the gap factors' degree: largest gap of the segment including the
       // one from the element before it (as the kernels' lane runs see them)
-      const double2 gz = seg_gap[s];
       const int D = pick_degree(P, sm, fmax(gz.x, gz.y - g.zprev));
       const SegFrame f = seg_frame(g);
       const int DN = pick_degree(P, sm, f.h0 + f.h1);

@@ -70,6 +70,9 @@ struct StreamArgs {
   // plan-time degrees per segment: (D + 1) | (DM + 1) << 8 with D the Taylor
   // degree of its gap factors and DM its moment degree (-1 = none)
   const int* seg_deg = nullptr;
+  // classify_kernel only: segment 0's zprev is its own first element (a
+  // plan without a predecessor, classified before zprev0 is known on the host)
+  bool zprev0_first = false;
 };
 
 struct OutArgs {
