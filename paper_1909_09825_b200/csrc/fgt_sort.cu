@@ -219,7 +219,7 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* total)
 }
 
 __global__ void __launch_bounds__(kScanBlock)
-    scan_reduce_kernel(const uint32_t* __restrict__ in, int64_t n, uint32_t* __restrict__ sums) {
+    sort_scan_reduce_kernel(const uint32_t* __restrict__ in, int64_t n, uint32_t* __restrict__ sums) {
   __shared__ unsigned tot;
   const int64_t base = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kScanItems;
   unsigned s = 0;
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kScanBlock)
 }
 
 __global__ void __launch_bounds__(kScanBlock)
-    scan_apply_kernel(const uint32_t* __restrict__ in, int64_t n,
+    sort_scan_apply_kernel(const uint32_t* __restrict__ in, int64_t n,
                       const uint32_t* __restrict__ block_off, uint32_t* __restrict__ out) {
   __shared__ unsigned tot;
   const int64_t base = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kScanItems;
@@ -257,15 +257,15 @@ cudaError_t excl_scan_u32(const uint32_t* in, int64_t n, uint32_t* out, uint32_t
   const int64_t nb = (n + kScanChunk - 1) / kScanChunk;
   note_launch(nb == 1 ? 1 : 2);
   if (nb == 1) {
-    scan_apply_kernel<<<1, kScanBlock, 0, st>>>(in, n, nullptr, out);
+    sort_scan_apply_kernel<<<1, kScanBlock, 0, st>>>(in, n, nullptr, out);
     return cudaGetLastError();
   }
   uint32_t* sums = tmp;
   uint32_t* sums_scanned = tmp + nb;
-  scan_reduce_kernel<<<(unsigned)nb, kScanBlock, 0, st>>>(in, n, sums);
+  sort_scan_reduce_kernel<<<(unsigned)nb, kScanBlock, 0, st>>>(in, n, sums);
   cudaError_t e = excl_scan_u32(sums, nb, sums_scanned, tmp + 2 * nb, st);
   if (e != cudaSuccess) return e;
-  scan_apply_kernel<<<(unsigned)nb, kScanBlock, 0, st>>>(in, n, sums_scanned, out);
+  sort_scan_apply_kernel<<<(unsigned)nb, kScanBlock, 0, st>>>(in, n, sums_scanned, out);
   return cudaGetLastError();
 }
 

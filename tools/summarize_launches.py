@@ -27,6 +27,21 @@ def main(path, out=None):
     lines = [f"{'kernel':45s} {'launches':>8s} {'total_us':>11s} {'avg_us':>10s} {'share':>6s}"]
     for k, v in tot.most_common():
         lines.append(f"{k[:45]:45s} {cnt[k]:8d} {v:11.1f} {v / cnt[k]:10.1f} {100 * v / s:5.1f}%")
+    # bench.py's untimed setup (synthetic data: RNG + radix sort, FP64 peak
+    # probe, torch elementwise) vs the kernels of the timed step
+    setup = ("uniform_kernel", "make_keys_kernel", "tile_hist_kernel", "global_hist_kernel",
+             "sort_scan_reduce_kernel", "sort_scan_apply_kernel", "scan_apply_kernel", "scatter_kernel", "unkey_kernel", "fp64_probe_kernel", "at::",
+             "void at::", "native::")
+    step = {k: v for k, v in tot.items() if not k.startswith(setup)}
+    nstep = max((cnt[k] for k in step if "seg_main_kernel" in k), default=0)
+    if step and nstep:
+        ss = sum(step.values())
+        lines.append("")
+        lines.append(f"timed-step kernels only (setup excluded), {nstep} steps in the list; "
+                     f"per step {ss / nstep:.1f} us")
+        lines.append(f"{'kernel':45s} {'per_step_us':>11s} {'share':>6s}")
+        for k, v in sorted(step.items(), key=lambda kv: -kv[1]):
+            lines.append(f"{k[:45]:45s} {v / nstep:11.1f} {100 * v / ss:5.1f}%")
     text = "\n".join(lines)
     print(text)
     if out:
