@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--check", action="store_true",
+                    help="N>1: rank 0 also runs the whole transform as one plan and reports "
+                         "max|u_ranks - u_single| / sum|alpha| (multi_rank_check)")
     return ap.parse_args()
 
 
@@ -379,6 +382,19 @@ def main():
     Mc, Nc = i1 - i0, j1 - j0
     u = torch.empty(max(Mc, 1), dtype=torch.float64, device=dev)
     flags = _capi.FGT_DEVICE_PTRS | _capi.FGT_BORROW
+    # device buffers of the multi-rank exchange (6 n_e doubles per rank)
+    agg_dev = torch.empty(6 * ne, dtype=torch.float64, device=dev)
+    allagg_dev = torch.empty(world * 6 * ne, dtype=torch.float64, device=dev)
+    car_dev = torch.empty(4 * ne, dtype=torch.float64, device=dev)
+
+    def gather_dev(t, out):
+        """all_gather of this rank's device aggregates into `out` (device)."""
+        if backend == "nccl":
+            dist.all_gather_into_tensor(out, t)
+        else:
+            parts = [torch.empty_like(t.cpu()) for _ in range(world)]
+            dist.all_gather(parts, t.cpu())
+            out.copy_(torch.cat(parts))
 
     def one_step(delta):
         h = ctypes.c_void_p()
@@ -393,17 +409,18 @@ def main():
                                                 ctypes.cast(yc.data_ptr(), PD), Nc, float(z_prev),
                                                 int(has_prev), delta, *soe_ptrs, flags, local, sh,
                                                 ctypes.byref(h)))
-            agg = np.empty(6 * ne)
+            # device-side exchange: aggregates -> all_gather -> this chunk's
+            # carries, all stream-ordered (no host round trip in the step)
+            fd = flags | _capi.FGT_DEVICE_AGGS
             _capi.check(L.fgt_apply_chunk_aggregate(h, ctypes.cast(ac.data_ptr(), PD),
-                                                    agg.ctypes.data_as(PD), flags, sh))
-            allagg = gather_aggs(torch.from_numpy(agg).to(dev))
-            carries = np.empty(world * 4 * ne)
-            _capi.check(L.fgt_chunk_carries(allagg.ctypes.data_as(PD), world, ne,
-                                            carries.ctypes.data_as(PD)))
-            mine = np.ascontiguousarray(carries[rank * 4 * ne:(rank + 1) * 4 * ne])
+                                                    ctypes.cast(agg_dev.data_ptr(), PD), fd, sh))
+            gather_dev(agg_dev, allagg_dev)
+            _capi.check(L.fgt_chunk_carries_device(ctypes.c_void_p(allagg_dev.data_ptr()), world,
+                                                   ne, rank, ctypes.c_void_p(car_dev.data_ptr()),
+                                                   sh))
             _capi.check(L.fgt_apply_chunk_finish(h, ctypes.cast(ac.data_ptr(), PD),
-                                                 mine.ctypes.data_as(PD),
-                                                 ctypes.cast(u.data_ptr(), PD), flags, sh))
+                                                 ctypes.cast(car_dev.data_ptr(), PD),
+                                                 ctypes.cast(u.data_ptr(), PD), fd, sh))
         L.fgt_plan_destroy(h)
 
     def barrier():
@@ -448,6 +465,37 @@ def main():
     launches = L.fgt_launch_counter() - launches0
     clk = clocks.stop((tw0, tw1))
     value = 2.0 * n / (ms / 1e3)
+
+    # ---- multi-rank correctness: the ranks' chunk potentials vs one plan
+    mr_check = None
+    if args.check and world > 1:
+        def allgather_cpu(t):
+            """all_gather of equal-size CPU tensors over either backend."""
+            src = t.to(dev) if backend == "nccl" else t
+            parts = [torch.zeros_like(src) for _ in range(world)]
+            dist.all_gather(parts, src)
+            return [p_.cpu() for p_ in parts]
+        one_step(args.delta)
+        torch.cuda.synchronize()
+        cnts = allgather_cpu(torch.tensor([Mc], dtype=torch.int64))
+        mx = int(max(c.item() for c in cnts))
+        buf = torch.zeros(mx, dtype=torch.float64)
+        buf[:Mc] = u[:Mc].cpu()
+        parts = allgather_cpu(buf)
+        if rank == 0:
+            u_ranks = torch.cat([parts[r][:int(cnts[r].item())] for r in range(world)])
+            h = ctypes.c_void_p()
+            u_one = torch.empty(n, dtype=torch.float64, device=dev)
+            _capi.check(L.fgt_plan_create(ctypes.cast(x.data_ptr(), PD), n,
+                                          ctypes.cast(y.data_ptr(), PD), n, args.delta, *soe_ptrs,
+                                          flags, local, sh, ctypes.byref(h)))
+            _capi.check(L.fgt_apply_general(h, ctypes.cast(a.data_ptr(), PD), n,
+                                            ctypes.cast(u_one.data_ptr(), PD), 1, flags, sh))
+            L.fgt_plan_destroy(h)
+            torch.cuda.synchronize()
+            err = float((u_ranks - u_one.cpu()).abs().max() / a.abs().sum().cpu())
+            mr_check = {"max_abs_diff_over_sum_abs_alpha": err, "pass": err <= 1e-12,
+                        "reference": "one plan over the whole stream on rank 0's GPU"}
 
     # ---- per-kernel durations (CUDA events on the launching stream)
     L.fgt_profile_enable(1)
@@ -624,6 +672,8 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if mr_check is not None:
+            line["multi_rank_check"] = mr_check
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

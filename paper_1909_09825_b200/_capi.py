@@ -21,6 +21,7 @@ FGT_ERR_NOMEM = 5
 FGT_DEVICE_PTRS = 1
 FGT_ASSUME_SORTED = 2
 FGT_BORROW = 4
+FGT_DEVICE_AGGS = 8
 
 FGT_SOE_FULL = 0
 FGT_SOE_FOLDED = 1
@@ -62,6 +63,7 @@ SIGNATURES = {
     "fgt_chunk_carries": (_I, [_PD, _I, _I, _PD]),
     "fgt_gauss_transform": (_I, [_PD, _I64, _PD, _I64, _PD, _D, _PD, _PD, _PD, _PD, _PU8, _I, _I,
                                  _I, _I, _PD]),
+    "fgt_chunk_carries_device": (_I, [_VP, _I, _I, _I, _VP, _VP]),
     "fgt_transform_host": (_I, [_PD, _I64, _PD, _I64, _PD, _D, _PD, _PD, _PD, _PD, _PU8, _I, _I,
                                 _PD, _I, _VP]),
     "fgt_direct": (_I, [_PD, _I64, _PD, _I64, _PD, _D, _PI64, _I64, _PD]),

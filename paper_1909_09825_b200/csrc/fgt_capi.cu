@@ -520,8 +520,9 @@ void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint3
 
 // Two-phase chunk apply.  Phase 1 keeps the sorted strengths and the tile
 // aggregates in the plan so phase 2 only runs the carry scan and K3.
-void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_host,
+void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_out,
                          uint32_t flags, cudaStream_t st) {
+  const bool dev_aggs = flags & FGT_DEVICE_AGGS;
   ck(cudaSetDevice(p->device), "cudaSetDevice");
   const int ne = p->P.ne;
   Work w{st, {}};
@@ -530,10 +531,13 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ho
   if (st != p->stream) ck(cudaStreamSynchronize(p->stream), "sync");
   sorted_strengths(p, strengths, flags, w, p->cs.bs);
   if (p->ntiles == 0) {
-    for (int k = 0; k < ne; ++k) {
-      totals_host[k] = {1.0, 0.0};
-      totals_host[ne + k] = {0.0, 0.0};
-      totals_host[2 * ne + k] = {0.0, 0.0};
+    std::vector<cplx> id(3 * ne, cplx{0.0, 0.0});
+    for (int k = 0; k < ne; ++k) id[k] = {1.0, 0.0};
+    if (dev_aggs) {
+      ck(cudaMemcpyAsync(totals_out, id.data(), sizeof(cplx) * 3 * ne, cudaMemcpyHostToDevice, st),
+         "identity aggregates");
+    } else {
+      std::memcpy(totals_out, id.data(), sizeof(cplx) * 3 * ne);
     }
     ck(cudaStreamSynchronize(st), "sync");
     return;
@@ -544,18 +548,20 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ho
     ProfScope ps(0, st);
     ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
   }
-  cplx* d_tot = w.get<cplx>(3 * ne);
+  cplx* d_tot = dev_aggs ? totals_out : w.get<cplx>(3 * ne);
   {
     ProfScope ps(1, st);
     ck(launch_carry_scan(ts, p->ntiles, ne, nullptr, d_tot, st), "chunk totals");
   }
-  ck(cudaMemcpyAsync(totals_host, d_tot, sizeof(cplx) * 3 * ne, cudaMemcpyDeviceToHost, st),
+  if (dev_aggs) return;  // stream-ordered: the caller gathers the device totals
+  ck(cudaMemcpyAsync(totals_out, d_tot, sizeof(cplx) * 3 * ne, cudaMemcpyDeviceToHost, st),
      "totals");
   ck(cudaStreamSynchronize(st), "sync");
 }
 
-void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in_host, double* potentials,
+void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in, double* potentials,
                       uint32_t flags, cudaStream_t st) {
+  const bool dev_aggs = flags & FGT_DEVICE_AGGS;
   ck(cudaSetDevice(p->device), "cudaSetDevice");
   if (p->M == 0) return;
   const bool dev = flags & FGT_DEVICE_PTRS;
@@ -567,9 +573,13 @@ void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in_host, double* potentia
   if (!p->cs.tile) raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
   const StreamArgs sa = stream_args(p, p->cs.bs);
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
-  cplx* d_cin = w.get<cplx>(2 * ne);
-  ck(cudaMemcpyAsync(d_cin, carry_in_host, sizeof(cplx) * 2 * ne, cudaMemcpyHostToDevice, st),
-     "carry in");
+  const cplx* d_cin = carry_in;
+  if (!dev_aggs) {
+    cplx* d = w.get<cplx>(2 * ne);
+    ck(cudaMemcpyAsync(d, carry_in, sizeof(cplx) * 2 * ne, cudaMemcpyHostToDevice, st),
+       "carry in");
+    d_cin = d;
+  }
   {
     ProfScope ps(1, st);
     ck(launch_carry_scan(ts, p->ntiles, ne, d_cin, nullptr, st), "carry scan");
@@ -585,8 +595,8 @@ void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in_host, double* potentia
     ck(cudaMemcpyAsync(potentials, u, sizeof(double) * p->M, cudaMemcpyDeviceToHost, st),
        "download potentials");
   }
-  // carry_in_host was staged through pageable memory: complete before return
-  ck(cudaStreamSynchronize(st), "sync");
+  // a host carry_in was staged through pageable memory: complete before return
+  if (!dev_aggs || !dev) ck(cudaStreamSynchronize(st), "sync");
 }
 
 // ------------------------------------------------ pipelined host transform
@@ -1041,10 +1051,16 @@ int fgt_mode_count_for_tolerance(double tol) {
   return -FGT_ERR_DOMAIN;
 }
 
-int fgt_plan_create(const double* targets, int64_t M, const double* sources, int64_t N,
-                    double delta, const double* t_re, const double* t_im, const double* w_re,
-                    const double* w_im, const uint8_t* self_conj, int n_modes, int form,
-                    uint32_t flags, int device, void* stream, fgt_plan_t* out) {
+}  // extern "C"
+
+namespace {
+// fgt_plan_create; has_prev: a chunk plan whose stream continues after z_prev
+// (segment 0 is framed from z_prev, classified in the same round trip)
+int plan_create_impl(const double* targets, int64_t M, const double* sources, int64_t N,
+                     double delta, const double* t_re, const double* t_im, const double* w_re,
+                     const double* w_im, const uint8_t* self_conj, int n_modes, int form,
+                     uint32_t flags, int device, void* stream, fgt_plan_t* out, bool has_prev,
+                     double z_prev) {
   return guarded([&] {
     if (!out) raise(FGT_ERR_INVALID, "out must not be NULL");
     *out = nullptr;
@@ -1091,7 +1107,8 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       double* xy0 = pin ? reinterpret_cast<double*>(pin + 32) : xyl;
       unsigned long long* hc = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hcl;
       xy0[0] = xy0[1] = 0.0;
-      queue_classify(p, hc, st, false, true);
+      if (has_prev) p->zprev0 = z_prev;
+      queue_classify(p, hc, st, false, !has_prev);
       ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(int) * 8, cudaMemcpyDeviceToHost, st), "flags");
       if (M > 0) ck(cudaMemcpyAsync(xy0, xs.dptr, 8, cudaMemcpyDeviceToHost, st), "x0");
       if (N > 0) ck(cudaMemcpyAsync(xy0 + 1, ys.dptr, 8, cudaMemcpyDeviceToHost, st), "y0");
@@ -1114,7 +1131,7 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
       }
       // coordinate before the first merged element: the element itself
       const double x0 = xy0[0], y0 = xy0[1];
-      p->zprev0 = (M > 0 && N > 0) ? std::fmin(x0, y0) : (M > 0 ? x0 : y0);
+      p->zprev0 = has_prev ? z_prev : (M > 0 && N > 0) ? std::fmin(x0, y0) : (M > 0 ? x0 : y0);
       if (!p->t_sorted || !p->s_sorted)
         classify_sync(p, st);
       else
@@ -1128,26 +1145,28 @@ int fgt_plan_create(const double* targets, int64_t M, const double* sources, int
   });
 }
 
+}  // namespace
+
+extern "C" {
+
+int fgt_plan_create(const double* targets, int64_t M, const double* sources, int64_t N,
+                    double delta, const double* t_re, const double* t_im, const double* w_re,
+                    const double* w_im, const uint8_t* self_conj, int n_modes, int form,
+                    uint32_t flags, int device, void* stream, fgt_plan_t* out) {
+  return plan_create_impl(targets, M, sources, N, delta, t_re, t_im, w_re, w_im, self_conj,
+                          n_modes, form, flags, device, stream, out, false, 0.0);
+}
+
 int fgt_plan_create_chunk(const double* sorted_targets, int64_t M, const double* sorted_sources,
                           int64_t N, double z_prev, int has_prev, double delta,
                           const double* t_re, const double* t_im, const double* w_re,
                           const double* w_im, const uint8_t* self_conj, int n_modes, int form,
                           uint32_t flags, int device, void* stream, fgt_plan_t* out) {
-  int rc = fgt_plan_create(sorted_targets, M, sorted_sources, N, delta, t_re, t_im, w_re, w_im,
-                           self_conj, n_modes, form, flags | FGT_ASSUME_SORTED, device, stream,
-                           out);
+  int rc = plan_create_impl(sorted_targets, M, sorted_sources, N, delta, t_re, t_im, w_re, w_im,
+                            self_conj, n_modes, form, flags | FGT_ASSUME_SORTED, device, stream,
+                            out, has_prev != 0, z_prev);
   if (rc != FGT_OK) return rc;
   (*out)->same_points = false;
-  if (has_prev) {
-    (*out)->zprev0 = z_prev;
-    // segment 0's frame starts at z_prev: reclassify
-    int rc2 = guarded([&] { classify_sync(*out, (*out)->stream); });
-    if (rc2 != FGT_OK) {
-      destroy_plan(*out);
-      *out = nullptr;
-      return rc2;
-    }
-  }
   return FGT_OK;
 }
 
@@ -1277,6 +1296,18 @@ int fgt_chunk_carries(const double* aggs, int n_chunks, int ne, double* carries_
               A.real() * b.imag() + A.imag() * b.real() + G.imag());
       }
     }
+  });
+}
+
+int fgt_chunk_carries_device(const double* aggs, int n_chunks, int ne, int rank,
+                             double* carry_out, void* stream) {
+  return guarded([&] {
+    if (n_chunks < 1 || ne < 0 || ne > kMaxModes || rank < 0 || rank >= n_chunks)
+      raise(FGT_ERR_INVALID, "bad sizes");
+    if (!aggs || !carry_out) raise(FGT_ERR_INVALID, "NULL buffer");
+    ck(launch_chunk_carries(reinterpret_cast<const cplx*>(aggs), n_chunks, ne, rank,
+                            reinterpret_cast<cplx*>(carry_out), as_stream(stream)),
+       "chunk carries");
   });
 }
 

@@ -2322,6 +2322,34 @@ static cudaError_t launch_seg_main(const StreamArgs& a, const ModeParams& P, con
   return cudaSuccess;
 }
 
+// Chunk g's forward carry is the forward state at its z_prev from all chunks
+// to its left, C+_g = A_{g-1} C+_{g-1} + F_{g-1}; the backward carry is the
+// mirror image, C-_g = A_{g+1} C-_{g+1} + G_{g+1} (fgt_chunk_carries).
+__global__ void chunk_carries_kernel(const cplx* __restrict__ a, int G, int ne, int rank,
+                                     cplx* __restrict__ out) {
+  const int k = threadIdx.x;
+  if (k >= ne) return;
+  cplx f = {0.0, 0.0};
+  for (int g = 0; g < rank; ++g) {
+    const cplx A = a[g * 3 * ne + k], F = a[g * 3 * ne + ne + k];
+    f = cplx{A.re * f.re - A.im * f.im + F.re, A.re * f.im + A.im * f.re + F.im};
+  }
+  cplx b = {0.0, 0.0};
+  for (int g = G - 1; g > rank; --g) {
+    const cplx A = a[g * 3 * ne + k], Gg = a[g * 3 * ne + 2 * ne + k];
+    b = cplx{A.re * b.re - A.im * b.im + Gg.re, A.re * b.im + A.im * b.re + Gg.im};
+  }
+  out[k] = f;
+  out[ne + k] = b;
+}
+
+cudaError_t launch_chunk_carries(const cplx* aggs, int n_chunks, int ne, int rank, cplx* out,
+                                 cudaStream_t st) {
+  note_launch();
+  chunk_carries_kernel<<<1, 32, 0, st>>>(aggs, n_chunks, ne, rank, out);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                         TileState ts, OutArgs o, cudaStream_t st) {
   return launch_seg_main<false>(a, P, mt, ts, o, st);

@@ -150,6 +150,10 @@ cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const Mod
 // 3*ne complex (A, F, G of the whole chunk) or nullptr.
 cudaError_t launch_carry_scan(const TileState& ts, int64_t nseg, int ne, const cplx* carry_in,
                               cplx* totals, cudaStream_t st);
+// Chunk carries of one chunk from the gathered chunk aggregates (the
+// algebra of fgt_chunk_carries, one thread per mode).
+cudaError_t launch_chunk_carries(const cplx* aggs, int n_chunks, int ne, int rank, cplx* out,
+                                 cudaStream_t st);
 cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                         TileState ts, OutArgs o, cudaStream_t st);
 cudaError_t launch_mode_sums(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,

@@ -1,0 +1,45 @@
+"""bench.py's multi-rank path end to end (N > 1 ranks under torchrun).
+
+The box has one GPU, so the ranks share it and exchange over gloo
+(FGT_BENCH_BACKEND=gloo, the bench's test hook); the device-side aggregate
+exchange (FGT_DEVICE_AGGS, fgt_chunk_carries_device) and the host-buffer e2e
+chunk path run as they would over NCCL.  --check makes rank 0 compare the
+ranks' potentials with one plan over the whole stream.  Timings here mean
+nothing (ranks share a GPU)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from paper_1909_09825_b200 import _capi
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_bench_multirank_device_exchange(world):
+    if _capi.lib().fgt_device_count() < 1:
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+    env = dict(os.environ, FGT_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           "bench.py", "--gpus", str(world), "--steps", "2", "--warmup", "1", "--size", "300000",
+           "--no-cpu-baseline", "--no-sweep", "--e2e-steps", "1", "--check"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout  # rank 0 alone prints
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == world
+    assert d["multi_rank_check"]["pass"], d["multi_rank_check"]
+    assert d["e2e"]["matches_device_path"], d["e2e"]

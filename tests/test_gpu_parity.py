@@ -369,6 +369,66 @@ def test_chunked_two_phase_equals_single_plan():
         check(u, full, a, 1e-13)
 
 
+def test_chunked_device_exchange_equals_single_plan():
+    """The multi-GPU path with no host round trip (FGT_DEVICE_AGGS): chunk
+    aggregates land in one device array (the all_gather's output), each
+    chunk's carries come from fgt_chunk_carries_device, phase 2 reads them on
+    the device; same bar as the host exchange, and the device carries equal
+    the host algebra's."""
+    import torch
+    import bench
+    M, N, delta, ne = 180000, 220000, 1e-4, 6
+    x, y = np.sort(up(M, 12, 3)), np.sort(up(N, 12, 0))
+    a = 2.0 * up(N, 12, 1) - 1.0
+    soe = fgt.soe_for_tolerance(1e-10)
+    tr, ti, wr, wi, sc = soe.arrays()
+    sp = (tr.ctypes.data_as(PD), ti.ctypes.data_as(PD), wr.ctypes.data_as(PD),
+          wi.ctypes.data_as(PD), sc.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), ne, 1)
+    L = _capi.lib()
+    dev = torch.device("cuda", 0)
+    st = torch.cuda.current_stream()
+    sh = ctypes.c_void_p(st.cuda_stream)
+    full = gpu_transform(x, y, a, delta, ne, mode=0, soe=soe)
+    dx, dy, da = (torch.from_numpy(v).to(dev) for v in (x, y, a))
+    fl = _capi.FGT_DEVICE_PTRS | _capi.FGT_BORROW | _capi.FGT_DEVICE_AGGS
+    for G in (1, 2, 5, 8):
+        tot = M + N
+        bounds = [(bench.merge_split(x, y, tot * g // G), tot * g // G) for g in range(G + 1)]
+        aggs = torch.empty(G * 6 * ne, dtype=torch.float64, device=dev)
+        u = torch.zeros(M, dtype=torch.float64, device=dev)
+        plans = []
+        for g in range(G):
+            (i0, d0), (i1, d1) = bounds[g], bounds[g + 1]
+            j0, j1 = d0 - i0, d1 - i1
+            zp = max(x[i0 - 1] if i0 > 0 else -np.inf, y[j0 - 1] if j0 > 0 else -np.inf)
+            h = ctypes.c_void_p()
+            _capi.check(L.fgt_plan_create_chunk(ctypes.cast(dx[i0:].data_ptr(), PD), i1 - i0,
+                                                ctypes.cast(dy[j0:].data_ptr(), PD), j1 - j0,
+                                                float(zp) if d0 > 0 else 0.0, int(d0 > 0), delta,
+                                                *sp, fl, 0, sh, ctypes.byref(h)))
+            _capi.check(L.fgt_apply_chunk_aggregate(
+                h, ctypes.cast(da[j0:].data_ptr(), PD),
+                ctypes.cast(aggs[g * 6 * ne:].data_ptr(), PD), fl, sh))
+            plans.append((h, i0, j0))
+        host_car = np.empty(G * 4 * ne)
+        agg_h = aggs.cpu().numpy()
+        _capi.check(L.fgt_chunk_carries(agg_h.ctypes.data_as(PD), G, ne,
+                                        host_car.ctypes.data_as(PD)))
+        car = torch.empty(4 * ne, dtype=torch.float64, device=dev)
+        for g, (h, i0, j0) in enumerate(plans):
+            _capi.check(L.fgt_chunk_carries_device(ctypes.c_void_p(aggs.data_ptr()), G, ne, g,
+                                                   ctypes.c_void_p(car.data_ptr()), sh))
+            assert np.allclose(car.cpu().numpy(), host_car[g * 4 * ne:(g + 1) * 4 * ne],
+                               rtol=1e-15, atol=1e-300)
+            _capi.check(L.fgt_apply_chunk_finish(h, ctypes.cast(da[j0:].data_ptr(), PD),
+                                                 ctypes.cast(car.data_ptr(), PD),
+                                                 ctypes.cast(u[i0:].data_ptr(), PD), fl, sh))
+        torch.cuda.synchronize()
+        for h, _, _ in plans:
+            L.fgt_plan_destroy(h)
+        check(u.cpu().numpy(), full, a, 1e-13)
+
+
 def test_device_pointer_path_matches_host_path():
     import torch
     M, N = 300000, 250000
