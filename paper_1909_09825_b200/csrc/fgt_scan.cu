@@ -440,20 +440,6 @@ __device__ __forceinline__ StageSlots stage_slots(const StreamArgs& a, const Seg
   return o;
 }
 
-// Copy of n values from src to slot o of buf (o odd iff src is misaligned):
-// the aligned interior by lane 0 (bulk, counted in *bytes), head / tail by
-// lanes hl / tl.
-__device__ __forceinline__ void stage_array(double* buf, int o, const double* src, int n, int lane,
-                                            int hl, int tl, uint64_t* bar, bool issue_bulk) {
-  if (n <= 0) return;
-  const int h = o & 1;  // head element copied separately
-  int c = (n - h) & ~1;
-  if (c < 0) c = 0;
-  if (issue_bulk && c > 0) bulk_g2s(buf + o + h, src + h, 8u * (unsigned)c, bar);
-  if (lane == hl && h) cp_async8(buf + o, src);
-  if (lane == tl && h + c < n) cp_async8(buf + o + n - 1, src + n - 1);
-}
-
 __device__ __forceinline__ unsigned stage_bulk_bytes(const StageSlots& o, const SegGeom& g) {
   auto cnt = [](int h, int n) {
     if (n <= 0) return 0;
@@ -463,6 +449,12 @@ __device__ __forceinline__ unsigned stage_bulk_bytes(const StageSlots& o, const 
   return 8u * (unsigned)(cnt(o.ox & 1, g.nx) + cnt(o.oy & 1, g.ny) + cnt(o.ob & 1, g.ny));
 }
 
+// Lane-parallel issue: lanes 0..2 bulk-copy the 16-byte aligned interior of
+// x / y / b (slot o + h, h = 1 when the array's first element is not
+// 16-byte aligned), lane 3 the mask words, lanes 4..9 the unaligned head /
+// tail elements of the three arrays by 8-byte cp.async, lanes 10.. the 2 ne
+// segment carries by 16-byte cp.async.  Each lane selects its own array, so
+// the warp issues one instance of each copy path.
 __device__ __forceinline__ void stage_issue(const StreamArgs& a, const TileState& ts, int ne,
                                             int64_t s, const SegGeom& g, const StagePtrs& sp,
                                             int lane) {
@@ -470,15 +462,28 @@ __device__ __forceinline__ void stage_issue(const StreamArgs& a, const TileState
   if (lane == 0) {
     fence_proxy_async();  // earlier generic reads of the stage before async writes
     mbar_expect(sp.bar, stage_bulk_bytes(o, g) + 32u);
-    bulk_g2s(sp.mask, a.seg_mask + s * (kSeg / 32), 32u, sp.bar);
   }
-  stage_array(sp.xy, o.ox, a.xs + g.ib, g.nx, lane, 1, 2, sp.bar, lane == 0);
-  stage_array(sp.xy, o.oy, a.ys + g.jb, g.ny, lane, 3, 4, sp.bar, lane == 0);
-  stage_array(sp.bb, o.ob, a.bs + g.jb, g.ny, lane, 5, 6, sp.bar, lane == 0);
-  if (lane < 2 * ne) {
-    const int k = lane < ne ? lane : lane - ne;
+  __syncwarp();
+  const int arr = lane < 3 ? lane : ((lane - 4) >> 1);  // 0 x, 1 y, 2 b (lanes < 10)
+  const double* src = arr == 0 ? a.xs + g.ib : (arr == 1 ? a.ys + g.jb : a.bs + g.jb);
+  const int n = arr == 0 ? g.nx : g.ny;
+  const int so = arr == 0 ? o.ox : (arr == 1 ? o.oy : o.ob);
+  double* buf = arr == 2 ? sp.bb : sp.xy;
+  const int h = so & 1;
+  int c = (n - h) & ~1;
+  if (c < 0) c = 0;
+  if (lane < 3) {
+    if (n > 0 && c > 0) bulk_g2s(buf + so + h, src + h, 8u * (unsigned)c, sp.bar);
+  } else if (lane == 3) {
+    bulk_g2s(sp.mask, a.seg_mask + s * (kSeg / 32), 32u, sp.bar);
+  } else if (lane < 10) {
+    const bool tail = (lane - 4) & 1;
+    const int e = tail ? n - 1 : 0;
+    if (n > 0 && (tail ? h + c < n : h != 0)) cp_async8(buf + so + e, src + e);
+  } else if (lane < 10 + 2 * ne) {
+    const int q = lane - 10, k = q < ne ? q : q - ne;
     const int64_t idx = (int64_t)k * a.nseg + s;
-    cp_async16(sp.car + lane, lane < ne ? ts.Cf + idx : ts.Cb + idx);
+    cp_async16(sp.car + q, q < ne ? ts.Cf + idx : ts.Cb + idx);
   }
   cp_async_commit();
 }
