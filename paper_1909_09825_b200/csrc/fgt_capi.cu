@@ -582,7 +582,8 @@ void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in, double* potentials,
   }
   {
     ProfScope ps(1, st);
-    ck(launch_carry_scan(ts, p->ntiles, ne, d_cin, nullptr, st), "carry scan");
+    // phase 1's block aggregates are still in the tile state: top + down only
+    ck(launch_carry_scan(ts, p->ntiles, ne, d_cin, nullptr, st, false), "carry scan");
   }
   OutArgs o;
   o.u = u;
