@@ -56,6 +56,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--chunk-path", action="store_true",
+                    help="N=1: run the multi-GPU chunk path (plan_create_chunk, device "
+                         "aggregate exchange, finish) instead of one plan: the per-rank "
+                         "step of a multi-GPU run at this per-rank size")
     ap.add_argument("--check", action="store_true",
                     help="N>1: rank 0 also runs the whole transform as one plan and reports "
                          "max|u_ranks - u_single| / sum|alpha| (multi_rank_check)")
@@ -389,7 +393,9 @@ def main():
 
     def gather_dev(t, out):
         """all_gather of this rank's device aggregates into `out` (device)."""
-        if backend == "nccl":
+        if world == 1:
+            out.copy_(t)
+        elif backend == "nccl":
             dist.all_gather_into_tensor(out, t)
         else:
             parts = [torch.empty_like(t.cpu()) for _ in range(world)]
@@ -398,7 +404,7 @@ def main():
 
     def one_step(delta):
         h = ctypes.c_void_p()
-        if world == 1:
+        if world == 1 and not args.chunk_path:
             _capi.check(L.fgt_plan_create(ctypes.cast(xc.data_ptr(), PD), Mc,
                                           ctypes.cast(yc.data_ptr(), PD), Nc, delta, *soe_ptrs,
                                           flags, local, sh, ctypes.byref(h)))
@@ -636,7 +642,8 @@ def main():
             "config": {"workload": f"cfg3: N=M={n:.0e} presorted uniform [0,1], alpha=2u-1, "
                                    f"delta={args.delta:g}, tol={args.tol:g} (n_e={ne})",
                        "n_e": ne, "delta": args.delta, "M": n, "N": n,
-                       "parallelism": f"merged-stream chunks x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"merged-stream chunks x{world}" if world > 1 else
+                                       "1 GPU (chunk path)" if args.chunk_path else "1 GPU"),
                        "l2": "inputs (3.2 GB) >> 126 MB L2; no flush needed"},
             # dominant kernel: K3 (main pass) -- reads x, y, alpha and writes u,
             # 16 B per merged point, timed by CUDA events on the launching stream

@@ -189,8 +189,9 @@ void build_modes(const Soe& folded, double delta, ModeParams& P, ModeTable& T) {
 
 // Per-chunk persistent state for the two-phase (multi-GPU) apply.
 struct ChunkState {
-  double* bs = nullptr;  // strengths, sorted-source order
-  cplx* tile = nullptr;  // 5 * ne * ntiles
+  double* bs = nullptr;            // strengths, sorted-source order (owned copy)
+  const double* bs_dev = nullptr;  // or the caller's device strengths (already sorted order)
+  cplx* tile = nullptr;            // 5 * ne * ntiles
 };
 
 struct fgt_plan_s {
@@ -527,9 +528,16 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ou
   const int ne = p->P.ne;
   Work w{st, {}};
   if (!p->cs.tile) p->cs.tile = dmalloc<cplx>(tile_state_elems(p->ntiles, ne), p->stream);
-  if (!p->cs.bs && p->N) p->cs.bs = dmalloc<double>(p->N, p->stream);
+  // device strengths of presorted sources are used in place (the caller
+  // passes them again to phase 2); otherwise the plan keeps a sorted copy
+  const bool borrow = (flags & FGT_DEVICE_PTRS) && !p->d_sperm;
+  if (!borrow && !p->cs.bs && p->N) p->cs.bs = dmalloc<double>(p->N, p->stream);
   if (st != p->stream) ck(cudaStreamSynchronize(p->stream), "sync");
-  sorted_strengths(p, strengths, flags, w, p->cs.bs);
+  if (borrow)
+    p->cs.bs_dev = strengths;
+  else
+    sorted_strengths(p, strengths, flags, w, p->cs.bs);
+  const double* bs = borrow ? strengths : p->cs.bs;
   if (p->ntiles == 0) {
     std::vector<cplx> id(3 * ne, cplx{0.0, 0.0});
     for (int k = 0; k < ne; ++k) id[k] = {1.0, 0.0};
@@ -542,7 +550,7 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ou
     ck(cudaStreamSynchronize(st), "sync");
     return;
   }
-  const StreamArgs sa = stream_args(p, p->cs.bs);
+  const StreamArgs sa = stream_args(p, bs);
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
   {
     ProfScope ps(0, st);
@@ -550,8 +558,9 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ou
   }
   cplx* d_tot = dev_aggs ? totals_out : w.get<cplx>(3 * ne);
   {
+    // block reduce + top level only: phase 2's down-sweep writes the carries
     ProfScope ps(1, st);
-    ck(launch_carry_scan(ts, p->ntiles, ne, nullptr, d_tot, st), "chunk totals");
+    ck(launch_carry_scan(ts, p->ntiles, ne, nullptr, d_tot, st, true, false), "chunk totals");
   }
   if (dev_aggs) return;  // stream-ordered: the caller gathers the device totals
   ck(cudaMemcpyAsync(totals_out, d_tot, sizeof(cplx) * 3 * ne, cudaMemcpyDeviceToHost, st),
@@ -559,8 +568,8 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ou
   ck(cudaStreamSynchronize(st), "sync");
 }
 
-void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in, double* potentials,
-                      uint32_t flags, cudaStream_t st) {
+void run_chunk_finish(fgt_plan_s* p, const double* strengths, const cplx* carry_in,
+                      double* potentials, uint32_t flags, cudaStream_t st) {
   const bool dev_aggs = flags & FGT_DEVICE_AGGS;
   ck(cudaSetDevice(p->device), "cudaSetDevice");
   if (p->M == 0) return;
@@ -571,7 +580,9 @@ void run_chunk_finish(fgt_plan_s* p, const cplx* carry_in, double* potentials,
   if (p->N == 0 && p->ntiles > 0 && !p->cs.tile)
     raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
   if (!p->cs.tile) raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish before fgt_apply_chunk_aggregate");
-  const StreamArgs sa = stream_args(p, p->cs.bs);
+  if (p->cs.bs_dev && p->cs.bs_dev != strengths)
+    raise(FGT_ERR_INVALID, "fgt_apply_chunk_finish: pass the strengths given to phase 1");
+  const StreamArgs sa = stream_args(p, p->cs.bs_dev ? p->cs.bs_dev : p->cs.bs);
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
   const cplx* d_cin = carry_in;
   if (!dev_aggs) {
@@ -1263,9 +1274,8 @@ int fgt_apply_chunk_finish(fgt_plan_t p, const double* strengths, const double* 
                            double* potentials, uint32_t flags, void* stream) {
   return guarded([&] {
     if (!p) raise(FGT_ERR_INVALID, "NULL plan");
-    (void)strengths;  // kept from phase 1
     if (!carry_in) raise(FGT_ERR_INVALID, "carry_in must not be NULL");
-    run_chunk_finish(p, reinterpret_cast<const cplx*>(carry_in), potentials, flags,
+    run_chunk_finish(p, strengths, reinterpret_cast<const cplx*>(carry_in), potentials, flags,
                      as_stream(stream));
   });
 }

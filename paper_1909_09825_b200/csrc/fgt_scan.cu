@@ -2366,16 +2366,16 @@ cudaError_t launch_mode_sums(const StreamArgs& a, const ModeParams& P, const Mod
 }
 
 cudaError_t launch_carry_scan(const TileState& ts, int64_t nseg, int ne, const cplx* carry_in,
-                              cplx* totals, cudaStream_t st, bool reduce) {
+                              cplx* totals, cudaStream_t st, bool reduce, bool down) {
   if (nseg == 0) return cudaSuccess;
   const int64_t nblk = scan_blocks(nseg);
   ScanArgs sa{ts.A, ts.F, ts.G, ts.Cf, ts.Cb, nseg, ne, nblk, ts.blk,
               ts.blk + (size_t)nblk * 2 * ne * 2};
   const dim3 grid((unsigned)nblk, (unsigned)(2 * ne));
-  note_launch(reduce ? 3 : 2);
+  note_launch(1 + (reduce ? 1 : 0) + (down ? 1 : 0));
   if (reduce) scan_reduce_kernel<<<grid, kScanThreads, 0, st>>>(sa);
   scan_top_kernel<<<2 * ne, 1024, 0, st>>>(sa, carry_in, totals);
-  scan_down_kernel<<<grid, kScanThreads, 0, st>>>(sa);
+  if (down) scan_down_kernel<<<grid, kScanThreads, 0, st>>>(sa);
   return cudaGetLastError();
 }
 

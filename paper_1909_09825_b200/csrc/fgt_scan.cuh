@@ -149,9 +149,11 @@ cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const Mod
 // the chunk's z_prev, backward carry at the chunk end) or nullptr; totals:
 // 3*ne complex (A, F, G of the whole chunk) or nullptr.  reduce = false
 // reuses the block aggregates of an earlier scan of the same TileState (a
-// chunk's phase 2: only the carry-in changed).
+// chunk's phase 2: only the carry-in changed); down = false stops after the
+// top level (a chunk's phase 1: only the totals are needed).
 cudaError_t launch_carry_scan(const TileState& ts, int64_t nseg, int ne, const cplx* carry_in,
-                              cplx* totals, cudaStream_t st, bool reduce = true);
+                              cplx* totals, cudaStream_t st, bool reduce = true,
+                              bool down = true);
 // Chunk carries of one chunk from the gathered chunk aggregates (the
 // algebra of fgt_chunk_carries, one thread per mode).
 cudaError_t launch_chunk_carries(const cplx* aggs, int n_chunks, int ne, int rank, cplx* out,
