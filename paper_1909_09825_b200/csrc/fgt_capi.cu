@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <complex>
+#include <memory>
 #include <mutex>
 #include <cstdio>
 #include <cstdlib>
@@ -311,6 +312,78 @@ void adopt_set(const SetSrc& in, int64_t n, bool is_sorted, uint32_t flags, cuda
   if (in.tmp) dfree(const_cast<double*>(in.dptr), st);
   *d_sorted = d_out;
   *d_perm = d_p;
+}
+
+struct PinnedBuf {
+  void* p = nullptr;
+  explicit PinnedBuf(size_t n) { ck(cudaMallocHost(&p, n), "pinned buffer"); }
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+// Both sets unsorted: the two radix sorts run concurrently, the second on a
+// side stream, and share one host read of their digit histograms (small
+// sorts are launch / latency bound: overlapping them hides most of it).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  ~SideStream() {
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (s) cudaStreamDestroy(s);
+  }
+};
+SideStream& side_stream() {
+  thread_local SideStream ss;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  thread_local int ss_dev = -1;
+  if (ss.s && ss_dev != dev) {  // a stream belongs to one device
+    cudaEventDestroy(ss.fork);
+    cudaEventDestroy(ss.join);
+    cudaStreamDestroy(ss.s);
+    ss.s = nullptr;
+  }
+  if (!ss.s) {
+    ck(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking), "side stream");
+    ck(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming), "event");
+    ss_dev = dev;
+  }
+  return ss;
+}
+
+void sort_both_sets(const SetSrc& xs, int64_t M, const SetSrc& ys, int64_t N, cudaStream_t st,
+                    double** d_xs, int32_t** d_tperm, double** d_ys, int32_t** d_sperm) {
+  SideStream& ss = side_stream();
+  double* xo = dmalloc<double>(M, st);
+  int32_t* xp = dmalloc<int32_t>(M, st);
+  void* xw = dmalloc<char>(radix_sort_workspace_bytes(M), st);
+  double* yo = dmalloc<double>(N, st);
+  int32_t* yp = dmalloc<int32_t>(N, st);
+  void* yw = dmalloc<char>(radix_sort_workspace_bytes(N), st);
+  ck(cudaEventRecord(ss.fork, st), "fork");
+  ck(cudaStreamWaitEvent(ss.s, ss.fork, 0), "fork");
+  thread_local std::unique_ptr<PinnedBuf> pin;  // two histograms, pinned (async copies)
+  if (!pin) pin.reset(new PinnedBuf(2 * sizeof(unsigned long long) * kSortHistWords));
+  unsigned long long* h = static_cast<unsigned long long*>(pin->p);
+  ck(radix_sort_begin(xs.dptr, M, xw, h, st), "radix sort");
+  ck(radix_sort_begin(ys.dptr, N, yw, h + kSortHistWords, ss.s), "radix sort");
+  ck(cudaStreamSynchronize(st), "sort sync");
+  ck(cudaStreamSynchronize(ss.s), "sort sync");
+  ck(radix_sort_end(M, xo, xp, xw, h, st), "radix sort");
+  ck(radix_sort_end(N, yo, yp, yw, h + kSortHistWords, ss.s), "radix sort");
+  ck(cudaEventRecord(ss.join, ss.s), "join");
+  ck(cudaStreamWaitEvent(st, ss.join, 0), "join");
+  dfree(xw, st);
+  dfree(yw, st);
+  if (xs.tmp) dfree(const_cast<double*>(xs.dptr), st);
+  if (ys.tmp) dfree(const_cast<double*>(ys.dptr), st);
+  *d_xs = xo;
+  *d_tperm = xp;
+  *d_ys = yo;
+  *d_sperm = yp;
 }
 
 // Small per-thread pinned buffer for the plan's device -> host reads (flags,
@@ -736,13 +809,6 @@ struct PipeStreams {
   }
 };
 
-struct PinnedBuf {
-  void* p = nullptr;
-  explicit PinnedBuf(size_t n) { ck(cudaMallocHost(&p, n), "pinned buffer"); }
-  ~PinnedBuf() {
-    if (p) cudaFreeHost(p);
-  }
-};
 
 // Plan / apply (host or device pointers per flags) for the small and the
 // fallback cases.
@@ -1131,9 +1197,14 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
       p->same_points = (M == N) && !hf[2];  // transform.cpp:214-216
       p->t_sorted = !hf[3];
       p->s_sorted = !hf[4];
-      temps.clear();  // ownership moves into adopt_set
-      adopt_set(xs, M, p->t_sorted, flags, st, &p->d_xs, &p->own_xs, &p->d_tperm);
-      adopt_set(ys, N, p->s_sorted, flags, st, &p->d_ys, &p->own_ys, &p->d_sperm);
+      temps.clear();  // ownership moves into adopt_set / sort_both_sets
+      if (!p->t_sorted && !p->s_sorted && M > 0 && N > 0) {
+        sort_both_sets(xs, M, ys, N, st, &p->d_xs, &p->d_tperm, &p->d_ys, &p->d_sperm);
+        p->own_xs = p->own_ys = true;
+      } else {
+        adopt_set(xs, M, p->t_sorted, flags, st, &p->d_xs, &p->own_xs, &p->d_tperm);
+        adopt_set(ys, N, p->s_sorted, flags, st, &p->d_ys, &p->own_ys, &p->d_sperm);
+      }
       if (!p->t_sorted || !p->s_sorted) {
         // metadata of the sorted stream; first coordinates after sorting
         plan_tiles(p, p->d_xs, p->d_ys, false, st);

@@ -304,35 +304,51 @@ static inline char* align_up(char* p) {
   return (char*)(((uintptr_t)p + 255) & ~(uintptr_t)255);
 }
 
-cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int32_t* perm,
-                                 void* workspace, cudaStream_t st) {
+// Workspace layout of one sort.
+struct SortWs {
+  uint64_t *k0, *k1;
+  uint32_t *v0, *v1, *cnt, *offs, *stmp;
+  unsigned long long* hist8;
+};
+static SortWs sort_ws(void* workspace, int64_t n) {
+  const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+  SortWs w;
+  char* p = align_up((char*)workspace);
+  w.k0 = (uint64_t*)p; p = align_up(p + sizeof(uint64_t) * n);
+  w.k1 = (uint64_t*)p; p = align_up(p + sizeof(uint64_t) * n);
+  w.v0 = (uint32_t*)p; p = align_up(p + sizeof(uint32_t) * n);
+  w.v1 = (uint32_t*)p; p = align_up(p + sizeof(uint32_t) * n);
+  w.cnt = (uint32_t*)p; p = align_up(p + sizeof(uint32_t) * ntiles * kRadix);
+  w.offs = (uint32_t*)p; p = align_up(p + sizeof(uint32_t) * ntiles * kRadix);
+  w.stmp = (uint32_t*)p; p = align_up(p + sizeof(uint32_t) * scan_tmp_elems(ntiles * kRadix));
+  w.hist8 = (unsigned long long*)p;
+  return w;
+}
+
+cudaError_t radix_sort_begin(const double* x, int64_t n, void* workspace,
+                             unsigned long long* hist_host, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const SortWs w = sort_ws(workspace, n);
+  note_launch(2);
+  make_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, w.k0, w.v0);
+  cudaError_t e = cudaMemsetAsync(w.hist8, 0, sizeof(unsigned long long) * 8 * kRadix, st);
+  if (e != cudaSuccess) return e;
+  global_hist_kernel<<<grid_for(n, 256) < 1184 ? grid_for(n, 256) : 1184, 256, 0, st>>>(w.k0, n,
+                                                                                       w.hist8);
+  return cudaMemcpyAsync(hist_host, w.hist8, sizeof(unsigned long long) * 8 * kRadix,
+                         cudaMemcpyDeviceToHost, st);
+}
+
+cudaError_t radix_sort_end(int64_t n, double* sorted, int32_t* perm, void* workspace,
+                           const unsigned long long* h8, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
-  char* w = align_up((char*)workspace);
-  uint64_t* k0 = (uint64_t*)w; w = align_up(w + sizeof(uint64_t) * n);
-  uint64_t* k1 = (uint64_t*)w; w = align_up(w + sizeof(uint64_t) * n);
-  uint32_t* v0 = (uint32_t*)w; w = align_up(w + sizeof(uint32_t) * n);
-  uint32_t* v1 = (uint32_t*)w; w = align_up(w + sizeof(uint32_t) * n);
-  uint32_t* cnt = (uint32_t*)w; w = align_up(w + sizeof(uint32_t) * ntiles * kRadix);
-  uint32_t* offs = (uint32_t*)w; w = align_up(w + sizeof(uint32_t) * ntiles * kRadix);
-  uint32_t* stmp = (uint32_t*)w; w = align_up(w + sizeof(uint32_t) * scan_tmp_elems(ntiles * kRadix));
-  unsigned long long* hist8 = (unsigned long long*)w;
-
-  note_launch(2);
-  make_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, k0, v0);
-  cudaError_t e = cudaMemsetAsync(hist8, 0, sizeof(unsigned long long) * 8 * kRadix, st);
-  if (e != cudaSuccess) return e;
-  global_hist_kernel<<<grid_for(n, 256) < 1184 ? grid_for(n, 256) : 1184, 256, 0, st>>>(k0, n,
-                                                                                       hist8);
-  unsigned long long h8[8 * kRadix];
-  e = cudaMemcpyAsync(h8, hist8, sizeof(h8), cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return e;
-  e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) return e;
-  uint64_t* kin = k0;
-  uint64_t* kout = k1;
-  uint32_t* vin = v0;
-  uint32_t* vout = v1;
+  const SortWs w = sort_ws(workspace, n);
+  uint64_t* kin = w.k0;
+  uint64_t* kout = w.k1;
+  uint32_t* vin = w.v0;
+  uint32_t* vout = w.v1;
+  cudaError_t e = cudaSuccess;
   for (int p = 0; p < 8; ++p) {
     bool trivial = false;
     for (int d = 0; d < kRadix; ++d)
@@ -340,13 +356,13 @@ cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int
     if (trivial) continue;  // every key has the same digit: the pass is the identity
     const int shift = 8 * p;
     note_launch(2);
-    tile_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, n, shift, cnt, ntiles);
-    e = excl_scan_u32(cnt, ntiles * kRadix, offs, stmp, st);
+    tile_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, n, shift, w.cnt, ntiles);
+    e = excl_scan_u32(w.cnt, ntiles * kRadix, w.offs, w.stmp, st);
     if (e != cudaSuccess) return e;
     static std::atomic<unsigned long long> smem_set{0};
     e = ensure_dynamic_smem(scatter_kernel, (int)kScatterSmem, smem_set);
     if (e != cudaSuccess) return e;
-    scatter_kernel<<<(unsigned)ntiles, kSortThreads, kScatterSmem, st>>>(kin, vin, n, shift, offs,
+    scatter_kernel<<<(unsigned)ntiles, kSortThreads, kScatterSmem, st>>>(kin, vin, n, shift, w.offs,
                                                                          ntiles, kout, vout);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -356,6 +372,17 @@ cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int
   note_launch();
   unkey_kernel<<<grid_for(n, 256), 256, 0, st>>>(kin, vin, n, sorted, perm);
   return cudaGetLastError();
+}
+
+cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int32_t* perm,
+                                 void* workspace, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  unsigned long long h8[8 * kRadix];
+  cudaError_t e = radix_sort_begin(x, n, workspace, h8, st);
+  if (e != cudaSuccess) return e;
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return e;
+  return radix_sort_end(n, sorted, perm, workspace, h8, st);
 }
 
 }  // namespace fgt_b200

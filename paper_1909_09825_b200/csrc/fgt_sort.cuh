@@ -16,6 +16,15 @@ size_t radix_sort_workspace_bytes(int64_t n);
 // (sorted[i] == x[perm[i]]; ties keep original order, like the reference).
 cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int32_t* perm,
                                  void* workspace, cudaStream_t st);
+// The same in two halves around one host read, so that several sorts can
+// share it: begin queues the keys and the digit histograms and copies the
+// histograms (8 * 256 u64) to hist_host; once they have landed (the caller
+// synchronizes st), end queues the passes that are not the identity.
+constexpr int kSortHistWords = 8 * 256;
+cudaError_t radix_sort_begin(const double* x, int64_t n, void* workspace,
+                             unsigned long long* hist_host, cudaStream_t st);
+cudaError_t radix_sort_end(int64_t n, double* sorted, int32_t* perm, void* workspace,
+                           const unsigned long long* hist_host, cudaStream_t st);
 // Raise a kernel's dynamic shared-memory limit once per device (the
 // attribute is per device; mask: one bit per device ordinal < 64).
 template <class K>
