@@ -372,8 +372,8 @@ void sort_both_sets(const SetSrc& xs, int64_t M, const SetSrc& ys, int64_t N, cu
   ck(radix_sort_begin(ys.dptr, N, yw, h + kSortHistWords, ss.s), "radix sort");
   ck(cudaStreamSynchronize(st), "sort sync");
   ck(cudaStreamSynchronize(ss.s), "sort sync");
-  ck(radix_sort_end(M, xo, xp, xw, h, st), "radix sort");
-  ck(radix_sort_end(N, yo, yp, yw, h + kSortHistWords, ss.s), "radix sort");
+  ck(radix_sort_end(xs.dptr, M, xo, xp, xw, h, st), "radix sort");
+  ck(radix_sort_end(ys.dptr, N, yo, yp, yw, h + kSortHistWords, ss.s), "radix sort");
   ck(cudaEventRecord(ss.join, ss.s), "join");
   ck(cudaStreamWaitEvent(st, ss.join, 0), "join");
   dfree(xw, st);

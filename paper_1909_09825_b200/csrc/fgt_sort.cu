@@ -5,7 +5,9 @@
 //
 //   radix sort      : stable LSD, 8-bit digits over order-preserving u64 keys
 //                     with a u32 index payload; passes whose digit is constant
-//                     across all keys are skipped (one global histogram pass)
+//                     across all keys are skipped (one global histogram pass);
+//                     the first pass forms the keys from the values, the last
+//                     writes the sorted values and the permutation
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -35,33 +37,25 @@ __device__ __forceinline__ double value_of(uint64_t k) {
   return __longlong_as_double((long long)k);
 }
 
-__global__ void make_keys_kernel(const double* __restrict__ x, int64_t n,
-                                 uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+// Every digit constant: all keys equal, the stable order is the input order.
+__global__ void identity_sort_kernel(const double* __restrict__ x, int64_t n,
+                                     double* __restrict__ sorted, int32_t* __restrict__ perm) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    keys[i] = key_of(__ldg(x + i));
-    vals[i] = (uint32_t)i;
-  }
-}
-
-__global__ void unkey_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
-                             int64_t n, double* __restrict__ sorted, int32_t* __restrict__ perm) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    sorted[i] = value_of(keys[i]);
-    perm[i] = (int32_t)vals[i];
+    sorted[i] = value_of(key_of(x[i]));
+    perm[i] = (int32_t)i;
   }
 }
 
 // All 8 digit histograms in one read: hist8[pass][digit].
-__global__ void global_hist_kernel(const uint64_t* __restrict__ keys, int64_t n,
+__global__ void global_hist_kernel(const double* __restrict__ x, int64_t n,
                                    unsigned long long* __restrict__ hist8) {
   __shared__ unsigned int h[8][kRadix];
   for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    uint64_t k = keys[i];
+    const uint64_t k = key_of(__ldg(x + i));
 #pragma unroll
     for (int p = 0; p < 8; ++p) atomicAdd(&h[p][(k >> (8 * p)) & 0xff], 1u);
   }
@@ -72,10 +66,12 @@ __global__ void global_hist_kernel(const uint64_t* __restrict__ keys, int64_t n,
   }
 }
 
-// Per-tile digit counts, digit-major: cnt[digit * ntiles + tile].
+// Per-tile digit counts, digit-major: cnt[digit * ntiles + tile].  FIRST:
+// the keys are formed from the input values on the fly (no key array yet).
+template <bool FIRST>
 __global__ void __launch_bounds__(kSortThreads)
-    tile_hist_kernel(const uint64_t* __restrict__ keys, int64_t n, int shift,
-                     uint32_t* __restrict__ cnt, int64_t ntiles) {
+    tile_hist_kernel(const uint64_t* __restrict__ keys, const double* __restrict__ x, int64_t n,
+                     int shift, uint32_t* __restrict__ cnt, int64_t ntiles) {
   __shared__ unsigned int h[kRadix];
   h[threadIdx.x] = 0;
   __syncthreads();
@@ -83,7 +79,10 @@ __global__ void __launch_bounds__(kSortThreads)
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
     int64_t i = base + it * kSortThreads + threadIdx.x;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 0xff], 1u);
+    if (i < n) {
+      const uint64_t k = FIRST ? key_of(__ldg(x + i)) : keys[i];
+      atomicAdd(&h[(k >> shift) & 0xff], 1u);
+    }
   }
   __syncthreads();
   cnt[(int64_t)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
@@ -95,10 +94,15 @@ constexpr size_t kScatterSmem = (sizeof(uint64_t) + sizeof(uint32_t)) * kSortTil
 // order with __match_any_sync; warp counters are scanned digit-wise across
 // warps, keys are staged digit-sorted in shared memory and written out in
 // contiguous per-digit runs.
+// FIRST: keys from the input values and the identity payload; LAST: the
+// sorted values and the permutation written instead of keys / payload.
+template <bool FIRST, bool LAST>
 __global__ void __launch_bounds__(kSortThreads)
-    scatter_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t n,
-                   int shift, const uint32_t* __restrict__ offs, int64_t ntiles,
-                   uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+    scatter_kernel(const uint64_t* __restrict__ kin, const uint32_t* __restrict__ vin,
+                   const double* __restrict__ x, int64_t n, int shift,
+                   const uint32_t* __restrict__ offs, int64_t ntiles, uint64_t* __restrict__ kout,
+                   uint32_t* __restrict__ vout, double* __restrict__ sorted,
+                   int32_t* __restrict__ perm) {
   __shared__ unsigned int wc[kSortWarps][kRadix];
   __shared__ unsigned int loff[kRadix];
   __shared__ unsigned int goff[kRadix];
@@ -121,8 +125,13 @@ __global__ void __launch_bounds__(kSortThreads)
   for (int it = 0; it < kItems; ++it) {
     const int li = warp * 32 * kItems + it * 32 + lane;  // tile-local index, in order
     const bool ok = li < tn;
-    key[it] = ok ? kin[base + li] : 0ull;
-    val[it] = ok ? vin[base + li] : 0u;
+    if constexpr (FIRST) {
+      key[it] = ok ? key_of(__ldg(x + base + li)) : 0ull;
+      val[it] = (uint32_t)(base + li);
+    } else {
+      key[it] = ok ? kin[base + li] : 0ull;
+      val[it] = ok ? vin[base + li] : 0u;
+    }
     const int d = ok ? (int)((key[it] >> shift) & 0xff) : -1;
     dig[it] = d;
     const unsigned active = __ballot_sync(0xffffffffu, ok);
@@ -180,8 +189,13 @@ __global__ void __launch_bounds__(kSortThreads)
     const uint64_t k = sk[p];
     const int d = (int)((k >> shift) & 0xff);
     const int64_t o = (int64_t)goff[d] + (p - (int)loff[d]);
-    kout[o] = k;
-    vout[o] = sv[p];
+    if constexpr (LAST) {
+      sorted[o] = value_of(k);
+      perm[o] = (int32_t)sv[p];
+    } else {
+      kout[o] = k;
+      vout[o] = sv[p];
+    }
   }
 }
 
@@ -329,49 +343,81 @@ cudaError_t radix_sort_begin(const double* x, int64_t n, void* workspace,
                              unsigned long long* hist_host, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const SortWs w = sort_ws(workspace, n);
-  note_launch(2);
-  make_keys_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, w.k0, w.v0);
+  note_launch(1);
   cudaError_t e = cudaMemsetAsync(w.hist8, 0, sizeof(unsigned long long) * 8 * kRadix, st);
   if (e != cudaSuccess) return e;
-  global_hist_kernel<<<grid_for(n, 256) < 1184 ? grid_for(n, 256) : 1184, 256, 0, st>>>(w.k0, n,
+  global_hist_kernel<<<grid_for(n, 256) < 1184 ? grid_for(n, 256) : 1184, 256, 0, st>>>(x, n,
                                                                                        w.hist8);
   return cudaMemcpyAsync(hist_host, w.hist8, sizeof(unsigned long long) * 8 * kRadix,
                          cudaMemcpyDeviceToHost, st);
 }
 
-cudaError_t radix_sort_end(int64_t n, double* sorted, int32_t* perm, void* workspace,
-                           const unsigned long long* h8, cudaStream_t st) {
+template <bool F, bool L>
+static cudaError_t scatter_pass(const uint64_t* kin, const uint32_t* vin, const double* x,
+                                int64_t n, int shift, const uint32_t* offs, int64_t ntiles,
+                                uint64_t* kout, uint32_t* vout, double* sorted, int32_t* perm,
+                                cudaStream_t st) {
+  static std::atomic<unsigned long long> smem_set{0};
+  cudaError_t e = ensure_dynamic_smem(scatter_kernel<F, L>, (int)kScatterSmem, smem_set);
+  if (e != cudaSuccess) return e;
+  scatter_kernel<F, L><<<(unsigned)ntiles, kSortThreads, kScatterSmem, st>>>(
+      kin, vin, x, n, shift, offs, ntiles, kout, vout, sorted, perm);
+  return cudaGetLastError();
+}
+
+// The first pass reads the values (keys formed on the fly), the last one
+// writes the sorted values and the permutation: no separate key / unkey pass.
+cudaError_t radix_sort_end(const double* x, int64_t n, double* sorted, int32_t* perm,
+                           void* workspace, const unsigned long long* h8, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
   const SortWs w = sort_ws(workspace, n);
+  int passes[8], np = 0;
+  for (int p = 0; p < 8; ++p) {
+    bool trivial = false;
+    for (int d = 0; d < kRadix; ++d)
+      if (h8[p * kRadix + d] == (unsigned long long)n) trivial = true;
+    if (!trivial) passes[np++] = p;  // a constant digit's pass is the identity
+  }
+  if (np == 0) {
+    note_launch();
+    identity_sort_kernel<<<grid_for(n, 256), 256, 0, st>>>(x, n, sorted, perm);
+    return cudaGetLastError();
+  }
   uint64_t* kin = w.k0;
   uint64_t* kout = w.k1;
   uint32_t* vin = w.v0;
   uint32_t* vout = w.v1;
   cudaError_t e = cudaSuccess;
-  for (int p = 0; p < 8; ++p) {
-    bool trivial = false;
-    for (int d = 0; d < kRadix; ++d)
-      if (h8[p * kRadix + d] == (unsigned long long)n) trivial = true;
-    if (trivial) continue;  // every key has the same digit: the pass is the identity
-    const int shift = 8 * p;
+  for (int q = 0; q < np; ++q) {
+    const int shift = 8 * passes[q];
+    const bool first = q == 0, last = q + 1 == np;
     note_launch(2);
-    tile_hist_kernel<<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, n, shift, w.cnt, ntiles);
+    if (first)
+      tile_hist_kernel<true><<<(unsigned)ntiles, kSortThreads, 0, st>>>(nullptr, x, n, shift, w.cnt,
+                                                                        ntiles);
+    else
+      tile_hist_kernel<false><<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, nullptr, n, shift,
+                                                                         w.cnt, ntiles);
     e = excl_scan_u32(w.cnt, ntiles * kRadix, w.offs, w.stmp, st);
     if (e != cudaSuccess) return e;
-    static std::atomic<unsigned long long> smem_set{0};
-    e = ensure_dynamic_smem(scatter_kernel, (int)kScatterSmem, smem_set);
-    if (e != cudaSuccess) return e;
-    scatter_kernel<<<(unsigned)ntiles, kSortThreads, kScatterSmem, st>>>(kin, vin, n, shift, w.offs,
-                                                                         ntiles, kout, vout);
-    e = cudaGetLastError();
+    if (first && last)
+      e = scatter_pass<true, true>(nullptr, nullptr, x, n, shift, w.offs, ntiles, nullptr, nullptr,
+                                   sorted, perm, st);
+    else if (first)
+      e = scatter_pass<true, false>(nullptr, nullptr, x, n, shift, w.offs, ntiles, kout, vout,
+                                    nullptr, nullptr, st);
+    else if (last)
+      e = scatter_pass<false, true>(kin, vin, nullptr, n, shift, w.offs, ntiles, nullptr, nullptr,
+                                    sorted, perm, st);
+    else
+      e = scatter_pass<false, false>(kin, vin, nullptr, n, shift, w.offs, ntiles, kout, vout,
+                                     nullptr, nullptr, st);
     if (e != cudaSuccess) return e;
     uint64_t* tk = kin; kin = kout; kout = tk;
     uint32_t* tv = vin; vin = vout; vout = tv;
   }
-  note_launch();
-  unkey_kernel<<<grid_for(n, 256), 256, 0, st>>>(kin, vin, n, sorted, perm);
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int32_t* perm,
@@ -382,7 +428,7 @@ cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int
   if (e != cudaSuccess) return e;
   e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return e;
-  return radix_sort_end(n, sorted, perm, workspace, h8, st);
+  return radix_sort_end(x, n, sorted, perm, workspace, h8, st);
 }
 
 }  // namespace fgt_b200

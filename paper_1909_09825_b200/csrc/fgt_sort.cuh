@@ -23,8 +23,8 @@ cudaError_t radix_sort_with_perm(const double* x, int64_t n, double* sorted, int
 constexpr int kSortHistWords = 8 * 256;
 cudaError_t radix_sort_begin(const double* x, int64_t n, void* workspace,
                              unsigned long long* hist_host, cudaStream_t st);
-cudaError_t radix_sort_end(int64_t n, double* sorted, int32_t* perm, void* workspace,
-                           const unsigned long long* hist_host, cudaStream_t st);
+cudaError_t radix_sort_end(const double* x, int64_t n, double* sorted, int32_t* perm,
+                           void* workspace, const unsigned long long* hist_host, cudaStream_t st);
 // Raise a kernel's dynamic shared-memory limit once per device (the
 // attribute is per device; mask: one bit per device ordinal < 64).
 template <class K>
