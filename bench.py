@@ -16,10 +16,20 @@ pass with fused weighted real-part combine) + plan destroy.  Metric:
 (M+N) points/s over the whole job.  Under torchrun (N>1) the merged stream is
 split into contiguous chunks of equal element count (merge path); each rank
 runs the two-phase chunk API with one NCCL all_gather of the chunk aggregates
-(3 n_e complex per rank) between the phases.
+(3 n_e complex per rank) between the phases, all on the device
+(FGT_DEVICE_AGGS, fgt_chunk_carries_device).
+
+"e2e" is the same transform from pinned HOST buffers through the one-shot
+fgt_transform_host (N=1: uploads / downloads overlapped with the device
+work) or the chunk API with host buffers (N>1), copies inside the timed
+region.  "roofline" is K3 (the dominant kernel) against HBM at 16 B per
+merged point; "cpu_baseline" times the reference library (oracle/_ref) on a
+bounded sample.
 
   python bench.py [--gpus N --steps K --warmup W]        # our arm
   python bench.py --impl reference [...]                  # reference CPU arm
+  --check        (N>1) compare the ranks' potentials with one plan
+  --chunk-path   (N=1) time the chunk path: the per-rank step of a multi-GPU run
 """
 import argparse
 import ctypes
