@@ -71,8 +71,9 @@ def parse():
                          "aggregate exchange, finish) instead of one plan: the per-rank "
                          "step of a multi-GPU run at this per-rank size")
     ap.add_argument("--check", action="store_true",
-                    help="N>1: rank 0 also runs the whole transform as one plan and reports "
-                         "max|u_ranks - u_single| / sum|alpha| (multi_rank_check)")
+                    help="N>1 (or --chunk-path): rank 0 also runs the whole transform as one "
+                         "plan and reports max|u_ranks - u_single| / sum|alpha| "
+                         "(multi_rank_check)")
     return ap.parse_args()
 
 
@@ -484,9 +485,11 @@ def main():
 
     # ---- multi-rank correctness: the ranks' chunk potentials vs one plan
     mr_check = None
-    if args.check and world > 1:
+    if args.check and (world > 1 or args.chunk_path):
         def allgather_cpu(t):
             """all_gather of equal-size CPU tensors over either backend."""
+            if world == 1:
+                return [t]
             src = t.to(dev) if backend == "nccl" else t
             parts = [torch.zeros_like(src) for _ in range(world)]
             dist.all_gather(parts, src)

@@ -43,3 +43,17 @@ def test_bench_multirank_device_exchange(world):
     assert d["n_gpus"] == world
     assert d["multi_rank_check"]["pass"], d["multi_rank_check"]
     assert d["e2e"]["matches_device_path"], d["e2e"]
+
+
+def test_bench_chunk_path_single_rank():
+    """--chunk-path on one GPU: the per-rank step of the multi-GPU path, checked
+    against one plan."""
+    if _capi.lib().fgt_device_count() < 1:
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+    cmd = [sys.executable, "bench.py", "--steps", "2", "--warmup", "1", "--size", "400000",
+           "--no-cpu-baseline", "--no-sweep", "--no-e2e", "--chunk-path", "--check"]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["config"]["parallelism"] == "1 GPU (chunk path)"
+    assert d["multi_rank_check"]["pass"], d["multi_rank_check"]
