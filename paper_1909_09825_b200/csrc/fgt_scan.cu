@@ -1054,6 +1054,12 @@ static_assert(kK3Moments >= 0 && kK3Moments <= kRegDeg, "K3 moment degree");
 #define FGT_NARROW_MAXD (kK3Moments <= 5 ? 6 : kMaxDeg)
 #endif
 constexpr int kNarrowMaxD = FGT_NARROW_MAXD;
+// Highest collapsed degree of the wide K3 (0: wide segments never collapse).
+#ifndef FGT_COLL_WIDE
+#define FGT_COLL_WIDE 8
+#endif
+constexpr int kCollWide = FGT_COLL_WIDE;
+static_assert(kCollWide == 0 || (kCollWide >= 7 && kCollWide <= kCollDeg), "wide collapse");
 static_assert(kNarrowMaxD >= 6 && kNarrowMaxD <= kCollDeg, "narrow degree bound");
 // Highest lane-moment degree of the K1 wide path.
 #ifndef FGT_LANE_MOM_MAX
@@ -1431,7 +1437,38 @@ __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParam
     }
     static_assert(kK3Moments >= 5, "FGT_CM cases");
   }
+  // Wide segments whose full width still allows the collapsed form at degree
+  // 7..kCollWide (<= kCollDeg): mode-independent work per element instead of
+  // per-mode gap factors and lane scans.
+  bool coll = false;
+  if constexpr (WIDE && !MS && kCollWide > 0) {
+    if (DN >= 0 && DN <= kCollWide) {
+      coll = true;
+      cplx* terms = reinterpret_cast<cplx*>(su + kSeg);
+      switch (DN < 7 ? 7 : DN) {
+#define FGT_CW(n)                                                                   \
+  case n:                                                                           \
+    if constexpr (n <= kCollWide) {                                                 \
+      if (lane < 2 * ne) {                                                          \
+        Coef<n> c;                                                                  \
+        const int k = lane < ne ? lane : lane - ne;                                 \
+        c.load(mx, k);                                                              \
+        terms[lane] = cmul(horner<n>(c, lane < ne ? f.h0 : f.h1), seg_c);           \
+      }                                                                             \
+      __syncwarp();                                                                 \
+      collapsed_segment<n>(mx, ne, r, f, lane, terms, su);                          \
+      break;                                                                        \
+    }                                                                               \
+    [[fallthrough]];
+        FGT_CW(7) FGT_CW(8)
+#undef FGT_CW
+        default:
+          break;
+      }
+    }
+  }
   if constexpr (WIDE || MS) {
+    if (!coll) {
 #pragma unroll
     for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
     r.g[0] -= zp;
@@ -1454,6 +1491,7 @@ __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParam
 #pragma unroll
       for (int e = 0; e < kR; ++e)
         if (r.tmask & (1u << e)) su[tk++] = out[e];
+    }
     }
   }
   if constexpr (!MS) {
@@ -1557,7 +1595,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
       const int deg = __ldg(a.seg_deg + s);
       const int D = seg_deg_D(deg), DM = seg_deg_DM(deg);
       if (batched && g.tid != cached_tid) {
-        warp_load_table<!WIDE && !MS>(a.mtb + g.tid, mx, ne, lane);
+        warp_load_table<!MS>(a.mtb + g.tid, mx, ne, lane);
         cached_tid = g.tid;
       }
       cp_async_wait_all();
@@ -1595,7 +1633,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
         const SegGeom g = seg_geom(a, s);
         const SegFrame f = seg_frame(g);
         if (batched && g.tid != cached_tid) {
-          warp_load_table<!WIDE && !MS>(a.mtb + g.tid, mx, ne, lane);
+          warp_load_table<!MS>(a.mtb + g.tid, mx, ne, lane);
           cached_tid = g.tid;
         }
         LaneRun r;
@@ -1622,7 +1660,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
         const SegGeom g = seg_geom(a, s);
         const SegFrame f = seg_frame(g);
         if (batched && g.tid != cached_tid) {
-          warp_load_table<!WIDE && !MS>(a.mtb + g.tid, mx, ne, lane);
+          warp_load_table<!MS>(a.mtb + g.tid, mx, ne, lane);
           cached_tid = g.tid;
         }
         const cplx seg_c = load_seg_carry(ts, a.nseg, s, ne, lane);

@@ -44,6 +44,8 @@ struct ModeTable {
   double gpoly[kCollDeg + 1];
   double pad2;
 };
+// tables are staged ahead of 16-byte aligned stages in shared memory
+static_assert(sizeof(ModeTable) % 16 == 0, "ModeTable size must be a multiple of 16 bytes");
 
 struct StreamArgs {
   const double* xs;  // sorted targets (this chunk)

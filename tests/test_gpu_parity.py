@@ -88,6 +88,11 @@ SWEEP = [
     (10, 5000, 5000, 1e-8, 7, False),      # everything decoupled
     (11, 65536, 65536, 1e-6, 6, True),     # cfg5 transform shape
     (12, 65536, 65536, 1e-1, 3, True),
+    # wide segments in the collapsed-form range (full-width degree 7-8):
+    # smax * 2h between rmax[6] and rmax[8]
+    (13, 200000, 200000, 3e-3, 6, True),
+    (14, 200000, 200000, 1e-2, 6, False),
+    (15, 150000, 250000, 2e-2, 4, True),
 ]
 
 
