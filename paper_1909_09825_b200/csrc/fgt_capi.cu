@@ -134,12 +134,20 @@ Soe soe_from_arrays(const double* t_re, const double* t_im, const double* w_re, 
   return s;
 }
 
-// Taylor degree thresholds: largest r with r^(D+1)/(D+1)! <= 2^-54.
+// Taylor degree thresholds: largest r with r^(D+1)/(D+1)! <= 2^-FGT_TRUNC_BITS.
+// A truncated term is then below 2^-FGT_TRUNC_BITS of the exponential it
+// replaces; summed over sources and weighted modes the transform error stays
+// below 2^-FGT_TRUNC_BITS * sum|m w| * sum|alpha| (sum|m w| = 131 at
+// n_e = 6): 2^-52 keeps it 1/35 of the 1e-12 * sum|alpha| parity bar.
+#ifndef FGT_TRUNC_BITS
+#define FGT_TRUNC_BITS 52
+#endif
 void fill_rmax(ModeParams& P) {
   long double fact = 1.0L;
   for (int D = 0; D <= kMaxDeg; ++D) {
     fact *= (long double)(D + 1);
-    P.rmax[D] = (double)powl(fact * ldexpl(1.0L, -54), 1.0L / (long double)(D + 1));
+    P.rmax[D] =
+        (double)powl(fact * ldexpl(1.0L, -FGT_TRUNC_BITS), 1.0L / (long double)(D + 1));
   }
 }
 

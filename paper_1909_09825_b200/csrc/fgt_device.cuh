@@ -35,7 +35,7 @@ struct ModeParams {
   double mw_re[kMaxModes], mw_im[kMaxModes];  // m_k * w_k
   double smax;                                // max_k |s_k|
   // rmax[D]: largest |s|*g for which the degree-D Taylor polynomial of
-  // exp(-s g) has truncation error below 2^-54 (relative).
+  // exp(-s g) has truncation error below 2^-FGT_TRUNC_BITS (relative).
   double rmax[kMaxDeg + 1];
 };
 

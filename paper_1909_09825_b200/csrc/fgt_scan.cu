@@ -1048,8 +1048,9 @@ __device__ __forceinline__ int seg_moment_degree(const ModeParams& P, double sma
 constexpr int kK3Moments = FGT_K3_MOMENTS;
 static_assert(kK3Moments >= 0 && kK3Moments <= kRegDeg, "K3 moment degree");
 // Largest gap-factor degree of a narrow segment: every gap is at most
-// h0 + h1 <= 2 rmax[DM] / |s|, and 2 rmax[5] = 0.0117 < rmax[6] = 0.0167
-// (rmax[D] = ((D+1)! 2^-54)^(1/(D+1))), so DM <= 5 implies D <= 6.
+// h0 + h1 <= 2 rmax[DM] / |s|, and 2 rmax[5] = 0.0148 < rmax[6] = 0.0197
+// (rmax[D] = ((D+1)! 2^-b)^(1/(D+1)), b = FGT_TRUNC_BITS >= 48), so DM <= 5
+// implies D <= 6.
 #ifndef FGT_NARROW_MAXD
 #define FGT_NARROW_MAXD (kK3Moments <= 5 ? 6 : kMaxDeg)
 #endif
