@@ -849,7 +849,12 @@ void transform_host(const double* x, int64_t M, const double* y, int64_t N, cons
     return;
   }
   // chunks of the merged stream (merge path on the host arrays; validated below)
-  int64_t G = L / pipe_knob("FGT_PIPE_CHUNK", 12500000);
+  // chunk: about L / 4 merged points, within [2.5M, 12.5M] (measured: fewer,
+  // larger chunks leave a long last-chunk tail; smaller ones cost per-chunk
+  // plan overhead)
+  int64_t dflt = L / 4;
+  dflt = dflt < 2500000 ? 2500000 : (dflt > 12500000 ? 12500000 : dflt);
+  int64_t G = L / pipe_knob("FGT_PIPE_CHUNK", dflt);
   G = G < 2 ? 2 : (G > 64 ? 64 : G);
   std::vector<PipeChunk> ch(G);
   bool ok = true;
