@@ -1033,10 +1033,16 @@ __device__ __forceinline__ LaneAgg warp_reduce_agg(LaneAgg v) {
   return v;
 }
 
+// Highest segment-moment degree (narrow K1; coefficients above kRegDeg are
+// read from the shared-memory table).  Segments beyond it take the wide K1.
+#ifndef FGT_K1_MAXDM
+#define FGT_K1_MAXDM 12
+#endif
+static_assert(FGT_K1_MAXDM >= kRegDeg && FGT_K1_MAXDM <= kMaxDeg, "K1 moment degree");
 __device__ __forceinline__ int seg_moment_degree(const ModeParams& P, double smax,
                                                  const SegFrame& f) {
   const int DM = pick_degree(P, smax, fmax(f.h0, f.h1));
-  return DM <= kRegDeg ? DM : -1;
+  return DM <= FGT_K1_MAXDM ? DM : -1;
 }
 
 // Highest moment degree K3 keeps in registers.  A segment narrow enough for
@@ -1069,7 +1075,7 @@ static_assert(kNarrowMaxD >= 6 && kNarrowMaxD <= kCollDeg, "narrow degree bound"
 constexpr int kLaneMomMax = FGT_LANE_MOM_MAX;
 
 // Segment classes (both kernels and the plan-time count use these).
-__device__ __forceinline__ bool k1_narrow(int DM) { return DM >= 0 && DM <= kRegDeg; }
+__device__ __forceinline__ bool k1_narrow(int DM) { return DM >= 0 && DM <= FGT_K1_MAXDM; }
 __device__ __forceinline__ bool k3_narrow(int DM) { return DM >= 0 && DM <= kK3Moments; }
 
 __device__ __forceinline__ int seg_deg_D(int deg) { return (deg & 0xff) - 1; }
@@ -1218,12 +1224,14 @@ __global__ void __launch_bounds__(kThreads, FGT_K1_MINB)
         cached_tid = g.tid;
       }
       switch (DM) {
-#define FGT_K1(n)                                                   \
-  case n:                                                           \
-    seg_aggregate_from<n>(f, mx, ne, lane, a.nseg, s, ts, yv, bv);  \
+#define FGT_K1(n)                                                     \
+  case n:                                                             \
+    if constexpr (n <= FGT_K1_MAXDM)                                  \
+      seg_aggregate_from<n>(f, mx, ne, lane, a.nseg, s, ts, yv, bv);  \
     break;
         FGT_K1(0) FGT_K1(1) FGT_K1(2) FGT_K1(3) FGT_K1(4) FGT_K1(5) FGT_K1(6) FGT_K1(7)
-        FGT_K1(8)
+        FGT_K1(8) FGT_K1(9) FGT_K1(10) FGT_K1(11) FGT_K1(12) FGT_K1(13) FGT_K1(14)
+        FGT_K1(15) FGT_K1(16)
 #undef FGT_K1
         default:
           break;
