@@ -1759,6 +1759,9 @@ __device__ __forceinline__ int merge_path_smem(const double* x, int nx, const do
   return lo;
 }
 
+#ifndef FGT_PLAN_TWO_LEVEL
+#define FGT_PLAN_TWO_LEVEL 1
+#endif
 template <bool BATCH>
 __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorted,
                                                int64_t nseg, int64_t* __restrict__ seg_ib,
@@ -1839,12 +1842,41 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
   // also tracks the largest gap between consecutive elements of its window
   // (the gap into a segment's first element is left to classify_kernel)
   const int d0 = t * kPlanPer;
+  const int nsegs_tile = (len + kSeg - 1) / kSeg;
   unsigned bits = 0u;
   double gmx = 0.0, zfirst = 0.0;
+#if FGT_PLAN_TWO_LEVEL
+  // merge-path splits in two levels: the segment starts over the whole tile,
+  // then every other window inside its segment's split range (fewer
+  // shared-memory probes: the pass is bound by shared-memory traffic)
+  if ((d0 % kSeg) == 0 && d0 < len) sib[d0 / kSeg] = merge_path_smem(sx, nx, sy, ny, d0);
+  if (t == 0) sib[nsegs_tile] = nx;
+  __syncthreads();
+#endif
   if (d0 < len) {
+#if FGT_PLAN_TWO_LEVEL
+    int i;
+    {
+      const int k = d0 / kSeg, D0 = k * kSeg;
+      const int D1 = D0 + kSeg < len ? D0 + kSeg : len;
+      const int ilo = sib[k], ihi = sib[k + 1];
+      const int jhi = D1 - ihi;
+      int lo = d0 - jhi > ilo ? d0 - jhi : ilo;
+      int hi = ilo + (d0 - D0) < ihi ? ilo + (d0 - D0) : ihi;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sx[mid - 1] < sy[d0 - mid])
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      i = lo;
+    }
+#else
     int i = merge_path_smem(sx, nx, sy, ny, d0);
-    int j = d0 - i;
     if ((d0 % kSeg) == 0) sib[d0 / kSeg] = i;
+#endif
+    int j = d0 - i;
     // no index clamps: on sorted input the merge never reads past a set's
     // sentinel; on unsorted input (flagged, redone after the sort) it can
     // run up to kPlanPer past it, into the buffer's padding
@@ -1880,8 +1912,9 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
 #pragma unroll
   for (int o = 8; o > 0; o >>= 1) gmx = fmax(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
   if ((d0 % kSeg) == 0 && d0 < len) seg_gap[c.seg0 + d0 / kSeg] = make_double2(gmx, zfirst);
-  const int nsegs_tile = (len + kSeg - 1) / kSeg;
+#if !FGT_PLAN_TWO_LEVEL
   if (t == 0) sib[nsegs_tile] = nx;
+#endif
   // mask: two threads per 32-bit word, same layout as bit (merged pos % 32)
   unsigned wd = bits << ((t & 1) * 16);
   wd |= __shfl_down_sync(0xffffffffu, wd, 1);
