@@ -30,9 +30,11 @@ def main(path, out=None):
     # bench.py's untimed setup (synthetic data: RNG + radix sort, FP64 peak
     # probe, torch elementwise) vs the kernels of the timed step
     setup = ("uniform_kernel", "make_keys_kernel", "tile_hist_kernel", "global_hist_kernel",
-             "sort_scan_reduce_kernel", "sort_scan_apply_kernel", "scan_apply_kernel", "scatter_kernel", "unkey_kernel", "fp64_probe_kernel", "at::",
+             "sort_scan_reduce_kernel", "sort_scan_apply_kernel", "scan_apply_kernel", "scatter_kernel",
+             "identity_sort_kernel", "unkey_kernel", "fp64_probe_kernel", "at::",
              "void at::", "native::")
-    step = {k: v for k, v in tot.items() if not k.startswith(setup)}
+    step = {k: v for k, v in tot.items()
+            if not (k[5:] if k.startswith("void ") else k).startswith(setup)}
     nstep = max((cnt[k] for k in step if "seg_main_kernel" in k), default=0)
     if step and nstep:
         ss = sum(step.values())
