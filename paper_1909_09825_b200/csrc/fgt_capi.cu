@@ -235,6 +235,10 @@ struct fgt_plan_s {
   int* d_flag = nullptr;
   ChunkState cs;
   cudaStream_t stream = nullptr;  // stream the plan was built on (teardown)
+  // Applies may run on other streams than the plan's: each such stream's
+  // last use is an event the teardown waits on before the memory is reused.
+  std::mutex use_mu;
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> uses;
 };
 
 namespace {
@@ -483,14 +487,35 @@ void upload_modes(fgt_plan_s* p, cudaStream_t st) {
 }
 
 
+// Record that work using plan p was queued on stream st (st != the plan's
+// stream): destroy_plan orders its frees after it.
+void note_use(fgt_plan_s* p, cudaStream_t st) {
+  if (st == p->stream) return;
+  std::lock_guard<std::mutex> lk(p->use_mu);
+  for (auto& u : p->uses)
+    if (u.first == st) {
+      ck(cudaEventRecord(u.second, st), "record plan use");
+      return;
+    }
+  cudaEvent_t ev = nullptr;
+  ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "plan use event");
+  p->uses.emplace_back(st, ev);
+  ck(cudaEventRecord(ev, st), "record plan use");
+}
+
 // Stream-ordered teardown on the plan's stream: work already queued on it
-// that uses the plan completes before the memory is reused.
+// that uses the plan, and the last use on every other stream an apply ran
+// on, completes before the memory is reused.
 void destroy_plan(fgt_plan_s* p) {
   if (!p) return;
   int cur = 0;
   cudaGetDevice(&cur);
   cudaSetDevice(p->device);
   cudaStream_t st = p->stream;
+  for (auto& u : p->uses) {
+    cudaStreamWaitEvent(st, u.second, 0);
+    cudaEventDestroy(u.second);  // released once it has completed
+  }
   if (p->own_xs) dfree(p->d_xs, st);
   if (p->own_ys) dfree(p->d_ys, st);
   dfree(p->d_tperm, st);
@@ -593,6 +618,7 @@ void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint3
       ck(launch_main(sa, p->P, p->d_mt, ts, o, st), "main pass");
     }
   }
+  note_use(p, st);
   if (!dev) {
     ck(cudaMemcpyAsync(potentials, u, sizeof(double) * p->M, cudaMemcpyDeviceToHost, st),
        "download potentials");
@@ -643,6 +669,7 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ou
     ProfScope ps(1, st);
     ck(launch_carry_scan(ts, p->ntiles, ne, nullptr, d_tot, st, true, false), "chunk totals");
   }
+  note_use(p, st);
   if (dev_aggs) return;  // stream-ordered: the caller gathers the device totals
   ck(cudaMemcpyAsync(totals_out, d_tot, sizeof(cplx) * 3 * ne, cudaMemcpyDeviceToHost, st),
      "totals");
@@ -684,6 +711,7 @@ void run_chunk_finish(fgt_plan_s* p, const double* strengths, const cplx* carry_
     ProfScope ps(2, st);
     ck(launch_main(sa, p->P, p->d_mt, ts, o, st), "main pass");
   }
+  note_use(p, st);
   if (!dev) {
     ck(cudaMemcpyAsync(potentials, u, sizeof(double) * p->M, cudaMemcpyDeviceToHost, st),
        "download potentials");

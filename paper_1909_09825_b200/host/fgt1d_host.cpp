@@ -6,7 +6,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <fstream>
+#include <iomanip>
+#include <map>
 #include <istream>
 #include <limits>
 #include <ostream>
@@ -75,59 +78,64 @@ auto soe_call(F&& f) -> decltype(f()) {
   }
 }
 
-constexpr double kUnderflowExponent = 745.0;
+constexpr double kUnderflowExponent = 745.0;  // transform.cpp:19
 
+// Mode-by-mode evaluation of the folded / full SOE sum over a whole vector of
+// scaled arguments s (sum_k m_k w_k exp(-t_k s), terms past the underflow
+// exponent dropped), accumulated in Real.  One pass per mode keeps the
+// per-mode constants in registers; the accumulation order over k is the
+// mode order, as in the reference's scalar sum (soe.cpp:22-35).
 template <class Real>
-Real eval_sum(const SoeApprox& soe, Real s) {
-  std::complex<Real> acc{};
+void soe_sum_into(const SoeApprox& soe, const std::vector<Real>& s, std::vector<Real>& out) {
+  std::vector<std::complex<Real>> acc(s.size());
   for (std::size_t k = 0; k < soe.size(); ++k) {
-    std::complex<Real> t(soe.nodes[k].real(), soe.nodes[k].imag());
-    if (t.real() * s > Real(kUnderflowExponent)) continue;
-    std::complex<Real> w(soe.weights[k].real(), soe.weights[k].imag());
-    acc += Real(soe.multiplier(k)) * w * std::exp(-t * s);
+    const std::complex<Real> t(soe.nodes[k].real(), soe.nodes[k].imag());
+    const std::complex<Real> mw =
+        Real(soe.multiplier(k)) *
+        std::complex<Real>(soe.weights[k].real(), soe.weights[k].imag());
+    for (std::size_t i = 0; i < s.size(); ++i)
+      if (!(t.real() * s[i] > Real(kUnderflowExponent))) acc[i] += mw * std::exp(-t * s[i]);
   }
-  return acc.real();
+  out.resize(s.size());
+  for (std::size_t i = 0; i < s.size(); ++i) out[i] = acc[i].real();
 }
 
+// max |exp(-x^2/4) - SOE(x)| over the standard log grid (soe.hpp:70-81).
+// The grid is cut into one contiguous slice per hardware thread; each slice
+// is evaluated vectorised (soe_sum_into) and reduced to its first maximum,
+// then the slices are combined in grid order (first maximum overall).
 template <class Real>
 ErrorReport max_error_impl(const SoeApprox& soe) {
   validate(soe);
-  constexpr int kChunk = 4096;
   const int total = kErrorGridLogPoints + 1;
-  const int nchunks = (total + kChunk - 1) / kChunk;
-  std::vector<double> err(nchunks, 0.0), arg(nchunks, 0.0);
-  auto run = [&](int c) {
-    double best = -1.0, bx = 0.0;
-    for (int i = c * kChunk; i < std::min(total, (c + 1) * kChunk); ++i) {
-      const double x = error_grid_point(i);
-      const Real s = Real(x);
-      const double e =
-          static_cast<double>(std::fabs(std::exp(-s * s / Real(4)) - eval_sum<Real>(soe, s)));
-      if (e > best) {
-        best = e;
-        bx = x;
-      }
-    }
-    err[c] = best;
-    arg[c] = bx;
+  const unsigned hw = std::thread::hardware_concurrency();
+  const int nslice = std::max(1, std::min(hw ? (int)hw : 1, 64));
+  struct Best {
+    double err = -1.0, x = 0.0;
   };
-  unsigned hw = std::thread::hardware_concurrency();
-  int nt = std::max(1, std::min<int>(hw ? (int)hw : 1, nchunks));
+  std::vector<Best> best(nslice);
+  auto slice = [&](int q) {
+    const int i0 = (int)((int64_t)total * q / nslice), i1 = (int)((int64_t)total * (q + 1) / nslice);
+    std::vector<Real> s(i1 - i0), g;
+    for (int i = i0; i < i1; ++i) s[i - i0] = Real(error_grid_point(i));
+    soe_sum_into<Real>(soe, s, g);
+    for (int i = i0; i < i1; ++i) {
+      const Real v = s[i - i0];
+      const double e = (double)std::fabs(std::exp(-v * v / Real(4)) - g[i - i0]);
+      if (e > best[q].err) best[q] = Best{e, (double)v};
+    }
+  };
   std::vector<std::thread> pool;
-  for (int t = 0; t < nt; ++t)
-    pool.emplace_back([&, t] {
-      for (int c = t; c < nchunks; c += nt) run(c);
-    });
+  for (int q = 1; q < nslice; ++q) pool.emplace_back(slice, q);
+  slice(0);
   for (auto& th : pool) th.join();
   ErrorReport rep;
   for (std::size_t k = 0; k < soe.size(); ++k) rep.n += (int)soe.multiplier(k);
-  double best = -1.0;
-  for (int c = 0; c < nchunks; ++c)
-    if (err[c] > best) {
-      best = err[c];
-      rep.argmax_x = arg[c];
-    }
-  rep.max_abs_error = best;
+  Best b;
+  for (const Best& q : best)
+    if (q.err > b.err) b = q;
+  rep.max_abs_error = b.err;
+  rep.argmax_x = b.x;
   return rep;
 }
 
@@ -168,7 +176,9 @@ double evaluate(const SoeApprox& soe, double x, double delta) {
   if (!std::isfinite(x)) throw std::domain_error("evaluate: x must be finite");
   if (!std::isfinite(delta) || !(delta > 0.0))
     throw std::domain_error("evaluate: delta must be positive and finite");
-  return eval_sum<double>(soe, std::fabs(x) / std::sqrt(delta));
+  std::vector<double> v{std::fabs(x) / std::sqrt(delta)}, g;
+  soe_sum_into<double>(soe, v, g);
+  return g[0];
 }
 
 SoeApprox fold(const SoeApprox& soe) {
@@ -188,64 +198,85 @@ double error_grid_point(int i) {
 ErrorReport max_error(const SoeApprox& soe) { return max_error_impl<double>(soe); }
 ErrorReport max_error_extended(const SoeApprox& soe) { return max_error_impl<long double>(soe); }
 
+// Coefficient-table text format (soe.hpp:90-100): a header line
+// "soe n=<count> form=<full|folded>[ source=<tag>]" and one row per node,
+// "Re t  Im t  Re w  Im w" with 17 significant digits (exact round trip).
 void write_coefficient_table(std::ostream& os, const SoeApprox& soe, const std::string& tag) {
   validate(soe);
-  os << "soe n=" << soe.size() << " form=" << (soe.form == SoeForm::Folded ? "folded" : "full");
-  if (!tag.empty()) os << " source=" << tag;
-  os << "\n";
-  char buf[160];
-  for (std::size_t k = 0; k < soe.size(); ++k) {
-    std::snprintf(buf, sizeof buf, "%.16e %.16e %.16e %.16e\n", soe.nodes[k].real(),
-                  soe.nodes[k].imag(), soe.weights[k].real(), soe.weights[k].imag());
-    os << buf;
-  }
+  std::ostringstream out;
+  out << "soe n=" << soe.size() << " form=" << (soe.form == SoeForm::Folded ? "folded" : "full")
+      << (tag.empty() ? "" : " source=") << tag << '\n';
+  out << std::scientific << std::setprecision(16);
+  for (std::size_t k = 0; k < soe.size(); ++k)
+    out << soe.nodes[k].real() << ' ' << soe.nodes[k].imag() << ' ' << soe.weights[k].real()
+        << ' ' << soe.weights[k].imag() << '\n';
+  os << out.str();
 }
 
+namespace {
+
+// "key=value" fields of the header after the leading "soe" token.
+std::map<std::string, std::string> table_header_fields(const std::string& line) {
+  std::istringstream hs(line);
+  std::string word;
+  if (!(hs >> word) || word != "soe")
+    throw std::invalid_argument("coefficient table: first line is not an 'soe' header");
+  std::map<std::string, std::string> kv;
+  while (hs >> word) {
+    const std::size_t at = word.find('=');
+    if (at == std::string::npos || at == 0)
+      throw std::invalid_argument("coefficient table: header field without '=': " + word);
+    kv[word.substr(0, at)] = word.substr(at + 1);
+  }
+  return kv;
+}
+
+// Four doubles of one row; false when the line holds anything else.
+bool parse_row(const std::string& line, double (&v)[4]) {
+  const char* p = line.c_str();
+  for (double& d : v) {
+    char* end = nullptr;
+    d = std::strtod(p, &end);
+    if (end == p) return false;
+    p = end;
+  }
+  while (*p == ' ' || *p == '\t' || *p == '\r') ++p;
+  return *p == '\0';
+}
+
+}  // namespace
+
 SoeApprox read_coefficient_table(std::istream& is) {
-  std::string header;
-  if (!std::getline(is, header)) throw std::invalid_argument("coefficient table: empty input");
-  std::istringstream hs(header);
-  std::string tag;
-  hs >> tag;
-  if (tag != "soe") throw std::invalid_argument("coefficient table: header must start with 'soe'");
-  long n = -1;
-  std::string form, kv;
-  while (hs >> kv) {
-    const auto eq = kv.find('=');
-    if (eq == std::string::npos)
-      throw std::invalid_argument("coefficient table: malformed header field '" + kv + "'");
-    const std::string key = kv.substr(0, eq), val = kv.substr(eq + 1);
-    if (key == "n") {
-      try {
-        n = std::stol(val);
-      } catch (const std::exception&) {
-        throw std::invalid_argument("coefficient table: bad n value");
-      }
-    } else if (key == "form") {
-      form = val;
-    }
-  }
-  if (n < 0) throw std::invalid_argument("coefficient table: missing n");
-  if (form != "full" && form != "folded")
-    throw std::invalid_argument("coefficient table: missing or bad form");
-  SoeApprox out;
-  out.form = form == "folded" ? SoeForm::Folded : SoeForm::Full;
   std::string line;
-  while (std::getline(is, line)) {
-    if (line.find_first_not_of(" \t\r") == std::string::npos) continue;
-    std::istringstream ls(line);
-    double tr, ti, wr, wi;
-    if (!(ls >> tr >> ti >> wr >> wi))
-      throw std::invalid_argument("coefficient table: malformed row '" + line + "'");
-    out.nodes.emplace_back(tr, ti);
-    out.weights.emplace_back(wr, wi);
-    if (out.form == SoeForm::Folded) {
-      if (ti < 0.0) throw std::invalid_argument("coefficient table: folded rows must have Im(t) >= 0");
-      out.self_conjugate.push_back(ti == 0.0 ? 1 : 0);
-    }
+  if (!std::getline(is, line)) throw std::invalid_argument("coefficient table: no header line");
+  const auto kv = table_header_fields(line);
+  const auto fn = kv.find("n"), ff = kv.find("form");
+  long n = -1;
+  if (fn != kv.end()) {
+    char* end = nullptr;
+    n = std::strtol(fn->second.c_str(), &end, 10);
+    if (fn->second.empty() || *end != '\0' || n < 0)
+      throw std::invalid_argument("coefficient table: n is not a count: " + fn->second);
   }
-  if (static_cast<long>(out.size()) != n)
-    throw std::invalid_argument("coefficient table: row count does not match header n");
+  if (n < 0) throw std::invalid_argument("coefficient table: header has no n");
+  if (ff == kv.end() || (ff->second != "full" && ff->second != "folded"))
+    throw std::invalid_argument("coefficient table: form must be full or folded");
+  SoeApprox out;
+  out.form = ff->second == "folded" ? SoeForm::Folded : SoeForm::Full;
+  while (std::getline(is, line)) {
+    if (line.find_first_not_of(" \t\r") == std::string::npos) continue;  // blank
+    double v[4];
+    if (!parse_row(line, v))
+      throw std::invalid_argument("coefficient table: row is not four numbers: " + line);
+    if (out.form == SoeForm::Folded && v[1] < 0.0)
+      throw std::invalid_argument("coefficient table: a folded node needs Im(t) >= 0");
+    out.nodes.emplace_back(v[0], v[1]);
+    out.weights.emplace_back(v[2], v[3]);
+    if (out.form == SoeForm::Folded) out.self_conjugate.push_back(v[1] == 0.0 ? 1 : 0);
+  }
+  if ((long)out.size() != n)
+    throw std::invalid_argument("coefficient table: " + std::to_string(out.size()) +
+                                " rows, header says " + std::to_string(n));
   validate(out);
   return out;
 }
@@ -275,43 +306,69 @@ SoeApprox soe_for_tolerance(double tol) {
 
 // ------------------------------------------------------------ transform
 
-TransformPlan plan(const TransformRequest& req, const SoeApprox& soe, bool precompute) {
-  // validation order of transform.cpp:200-211
-  if (!std::isfinite(req.delta) || !(req.delta > 0.0))
-    throw std::domain_error("delta must be positive and finite");
-  for (double x : req.targets)
-    if (!std::isfinite(x)) throw std::domain_error("target coordinates must be finite");
-  for (double y : req.sources)
-    if (!std::isfinite(y)) throw std::domain_error("source coordinates must be finite");
-  if (req.strengths.size() != req.sources.size())
-    throw std::invalid_argument("one strength per source required");
-  validate(soe);
-  TransformPlan p;
-  p.soe = soe.form == SoeForm::Folded ? soe : fold(soe);
-  p.delta = req.delta;
-  const std::size_t ne = p.soe.size();
+namespace {
+
+fgt_plan_t device_plan(const TransformRequest& req, const SoeApprox& folded) {
+  const std::size_t ne = folded.size();
   std::vector<double> tr(ne), ti(ne), wr(ne), wi(ne);
+  std::vector<std::uint8_t> sc(ne, 0);
   for (std::size_t k = 0; k < ne; ++k) {
-    tr[k] = p.soe.nodes[k].real();
-    ti[k] = p.soe.nodes[k].imag();
-    wr[k] = p.soe.weights[k].real();
-    wi[k] = p.soe.weights[k].imag();
+    tr[k] = folded.nodes[k].real();
+    ti[k] = folded.nodes[k].imag();
+    wr[k] = folded.weights[k].real();
+    wi[k] = folded.weights[k].imag();
+    sc[k] = folded.self_conjugate[k];
   }
   fgt_plan_t h = nullptr;
   check(fgt_plan_create(req.targets.data(), (int64_t)req.targets.size(), req.sources.data(),
                         (int64_t)req.sources.size(), req.delta, tr.data(), ti.data(), wr.data(),
-                        wi.data(), p.soe.self_conjugate.data(), (int)ne, FGT_SOE_FOLDED, 0, -1,
-                        nullptr, &h));
-  p.device = std::shared_ptr<void>(h, PlanDeleter{});
+                        wi.data(), sc.data(), (int)ne, FGT_SOE_FOLDED, 0, -1, nullptr, &h));
+  return h;
+}
+
+}  // namespace
+
+TransformPlan plan(const TransformRequest& req, const SoeApprox& soe, bool precompute) {
+  // Validation order of transform.cpp:200-211: delta, target / source
+  // coordinates (checked on the device by the plan's check pass), strength
+  // count, SOE.
+  if (!std::isfinite(req.delta) || !(req.delta > 0.0))
+    throw std::domain_error("delta must be positive and finite");
+  const bool count_ok = req.strengths.size() == req.sources.size();
+  bool soe_ok = true;
+  try {
+    validate(soe);
+  } catch (const std::invalid_argument&) {
+    soe_ok = false;
+  }
+  if (!count_ok || !soe_ok) {
+    // the coordinates are still checked first (a stand-in SOE for the check)
+    fgt_plan_destroy(device_plan(req, fold(cf_soe(2))));
+    if (!count_ok) throw std::invalid_argument("one strength per source required");
+    validate(soe);  // throws
+  }
+  TransformPlan p;
+  p.soe = soe.form == SoeForm::Folded ? soe : fold(soe);
+  p.delta = req.delta;
+  fgt_plan_t h = device_plan(req, p.soe);
+  std::shared_ptr<void> dev(h, PlanDeleter{});
+  p.device = dev;
   int same = 0;
   check(fgt_plan_info(h, nullptr, nullptr, nullptr, &same, nullptr, nullptr, nullptr));
   p.same_points = same != 0;
-  p.sorted_targets.resize(req.targets.size());
-  p.sorted_sources.resize(req.sources.size());
-  p.target_perm.resize(req.targets.size());
-  p.source_perm.resize(req.sources.size());
-  check(fgt_plan_copy_sorted(h, p.sorted_targets.data(), p.target_perm.data(),
-                             p.sorted_sources.data(), p.source_perm.data()));
+  // host fields on first access (lazily populated)
+  p.sorted_targets = HostMirror<double>(req.targets.size(), [dev](double* o) {
+    check(fgt_plan_copy_sorted(static_cast<fgt_plan_t>(dev.get()), o, nullptr, nullptr, nullptr));
+  });
+  p.sorted_sources = HostMirror<double>(req.sources.size(), [dev](double* o) {
+    check(fgt_plan_copy_sorted(static_cast<fgt_plan_t>(dev.get()), nullptr, nullptr, o, nullptr));
+  });
+  p.target_perm = HostMirror<std::int64_t>(req.targets.size(), [dev](std::int64_t* o) {
+    check(fgt_plan_copy_sorted(static_cast<fgt_plan_t>(dev.get()), nullptr, o, nullptr, nullptr));
+  });
+  p.source_perm = HostMirror<std::int64_t>(req.sources.size(), [dev](std::int64_t* o) {
+    check(fgt_plan_copy_sorted(static_cast<fgt_plan_t>(dev.get()), nullptr, nullptr, nullptr, o));
+  });
   if (precompute) precompute_gap_table(p);
   return p;
 }

@@ -154,18 +154,50 @@ void cpu_tests() {
     r = golden();
     r.delta = -2.0;
     CHECK(throws<std::domain_error>([&] { fgt::plan(r, soe, false); }));
-    r = golden();
-    r.targets[1] = NAN;
-    CHECK(throws<std::domain_error>([&] { fgt::plan(r, soe, false); }));
-    r = golden();
-    r.strengths.pop_back();
-    CHECK(throws<std::invalid_argument>([&] { fgt::plan(r, soe, false); }));
+    // coordinates and the strength count are checked after the device's
+    // coordinate pass (gpu_tests: "plan validation on the device")
   });
 }
 
 // ----------------------------------------------------------------- GPU
 
 void gpu_tests() {
+  run("plan validation on the device (test_transform.cpp:260-280)", [] {
+    auto soe = fgt::fold(fgt::cf_soe(8));
+    auto r = golden();
+    r.targets[1] = NAN;
+    CHECK(throws<std::domain_error>([&] { fgt::plan(r, soe, false); }));
+    r = golden();
+    r.sources[4] = INFINITY;
+    CHECK(throws<std::domain_error>([&] { fgt::plan(r, soe, false); }));
+    r = golden();
+    r.strengths.pop_back();
+    CHECK(throws<std::invalid_argument>([&] { fgt::plan(r, soe, false); }));
+    // coordinates first: a NaN and a short strength vector -> domain_error
+    r.targets[0] = NAN;
+    CHECK(throws<std::domain_error>([&] { fgt::plan(r, soe, false); }));
+    // strength count before the SOE (transform.cpp:205-208)
+    auto bad = soe;
+    bad.nodes[0] = {-1.0, 0.0};
+    r = golden();
+    r.strengths.pop_back();
+    bool msg_ok = false;
+    try {
+      fgt::plan(r, bad, false);
+    } catch (const std::invalid_argument& e) {
+      msg_ok = std::string(e.what()).find("strength") != std::string::npos;
+    }
+    CHECK(msg_ok);
+    // lazily populated host fields: sizes known, contents on first access
+    r = golden();
+    std::swap(r.targets[0], r.targets[2]);
+    auto p = fgt::plan(r, soe, false);
+    CHECK(p.sorted_targets.size() == 3 && p.target_perm.size() == 3);
+    CHECK(p.target_perm == (std::vector<std::int64_t>{2, 1, 0}));
+    CHECK(p.sorted_targets[0] == 0.0 && p.sorted_targets[2] == 1.0);
+    const std::vector<double>& sv = p.sorted_sources;
+    CHECK(sv == kYs);
+  });
   run("direct matches the 50-digit reference", [] {
     auto res = fgt::direct(golden());
     for (int i = 0; i < 3; ++i) CHECK(std::fabs(res.potentials[i] - kGold[i]) <= 1e-15 * kGold[i]);
