@@ -57,6 +57,9 @@ def oracle_lib():
         L.oracle_mode_sums.restype = ctypes.c_int
         L.oracle_mode_sums.argtypes = [_PD, ctypes.c_int64, _PD, _PI64, ctypes.c_int64, _PD,
                                        ctypes.c_double, _PD, _PD, ctypes.c_int, _PD, _PD]
+        L.oracle_gap_table.restype = None
+        L.oracle_gap_table.argtypes = [_PD, ctypes.c_int64, ctypes.c_double, _PD, _PD, ctypes.c_int,
+                                       _PD]
         L.oracle_counter_rand.restype = ctypes.c_uint64
         L.oracle_counter_rand.argtypes = [ctypes.c_uint64] * 3
         L.oracle_uniform01.restype = ctypes.c_double
@@ -94,6 +97,12 @@ def ref_lib():
                                         ctypes.c_double, ctypes.c_int, _PD, _PD]
         L.fgt_ref_max_error.restype = ctypes.c_int
         L.fgt_ref_max_error.argtypes = [ctypes.c_int, ctypes.c_int, _PD, _PD]
+        L.fgt_ref_gap_table.restype = ctypes.c_int
+        L.fgt_ref_gap_table.argtypes = [_PD, ctypes.c_int64, ctypes.c_double, ctypes.c_int, _PD]
+        L.fgt_ref_uniform_points.restype = ctypes.c_int
+        L.fgt_ref_uniform_points.argtypes = [ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint64, _PD]
+        L.fgt_ref_counter_rand.restype = ctypes.c_uint64
+        L.fgt_ref_counter_rand.argtypes = [ctypes.c_uint64] * 3
         L.fgt_ref_set_table_dir(TABLE_DIR.encode())
         _ref = L
     return _ref
@@ -250,3 +259,34 @@ def ref_max_error(n, fold_it=False):
     if rc:
         raise ValueError(L.fgt_ref_last_error().decode())
     return e.value, a.value
+
+
+def ref_gap_table(x, delta, ne):
+    """The reference's precompute_gap_table for targets x (mode-major, complex)."""
+    L = ref_lib()
+    x = _f(x)
+    out = np.empty(2 * ne * max(x.size - 1, 0))
+    rc = L.fgt_ref_gap_table(_p(x), x.size, float(delta), ne, _p(out))
+    if rc:
+        raise ValueError(L.fgt_ref_last_error().decode())
+    return out[0::2] + 1j * out[1::2]
+
+
+def ref_uniform_points(count, seed, stream):
+    """rng::uniform_points of the reference library."""
+    L = ref_lib()
+    out = np.empty(int(count))
+    rc = L.fgt_ref_uniform_points(int(count), int(seed), int(stream), _p(out))
+    if rc:
+        raise ValueError(L.fgt_ref_last_error().decode())
+    return out
+
+
+def gap_table(xs_sorted, delta, ne):
+    """C restatement of precompute_gap_table on sorted targets (complex)."""
+    xs = _f(xs_sorted)
+    t, _mw = folded_table(2 * ne)
+    tr, ti = np.ascontiguousarray(t.real), np.ascontiguousarray(t.imag)
+    out = np.empty(2 * ne * max(xs.size - 1, 0))
+    oracle_lib().oracle_gap_table(_p(xs), xs.size, float(delta), _p(tr), _p(ti), len(t), _p(out))
+    return out[0::2] + 1j * out[1::2]

@@ -26,6 +26,7 @@
 #include "fgt1d/cf.hpp"
 #include "fgt1d/errors.hpp"
 #include "fgt1d/soe.hpp"
+#include "fgt1d/rng.hpp"
 #include "fgt1d/transform.hpp"
 
 namespace {
@@ -180,6 +181,33 @@ int fgt_ref_max_error(int n, int fold_it, double* err, double* argmax) {
     *err = rep.max_abs_error;
     *argmax = rep.argmax_x;
   })
+}
+
+// precompute_gap_table (transform.cpp:221-237) of the plan of sorted or
+// unsorted targets x (sources = x): mode-major, interleaved re/im,
+// out[(k*(M-1) + i)*2 + {0,1}].
+int fgt_ref_gap_table(const double* x, int64_t M, double delta, int ne, double* out) {
+  FGT_REF_TRY({
+    std::vector<double> a(M, 1.0);
+    auto req = make_req(x, M, x, M, a.data(), delta);
+    auto plan = fgt::plan(req, fgt::fold(fgt::cf_soe(2 * ne)), true);
+    for (std::size_t i = 0; i < plan.gap_exponentials.size(); ++i) {
+      out[2 * i] = plan.gap_exponentials[i].real();
+      out[2 * i + 1] = plan.gap_exponentials[i].imag();
+    }
+  })
+}
+
+// rng::uniform_points (rng.cpp:24-29) and rng::counter_rand (rng.cpp:7-17).
+int fgt_ref_uniform_points(int64_t count, uint64_t seed, uint64_t stream, double* out) {
+  FGT_REF_TRY({
+    auto v = fgt::rng::uniform_points((std::size_t)count, seed, stream);
+    std::memcpy(out, v.data(), sizeof(double) * v.size());
+  })
+}
+
+uint64_t fgt_ref_counter_rand(uint64_t seed, uint64_t stream, uint64_t i) {
+  return fgt::rng::counter_rand(seed, stream, i);
 }
 
 }  // extern "C"

@@ -421,8 +421,10 @@ unsigned char* pinned_scratch() {
   return s.p;
 }
 
-// d_flag: check flags 0..4, then two 64-bit segment-class counters.
-constexpr int kFlagInts = 12;
+// d_flag: tile-pass check flags 0..4, two 64-bit segment-class counters at
+// ints 8..11, element-wise check flags (launch_check_points) at 12..16.
+constexpr int kFlagInts = 20;
+constexpr int kFullCheck = 12;
 unsigned long long* class_counts(fgt_plan_s* p) {
   return reinterpret_cast<unsigned long long*>(p->d_flag + 8);
 }
@@ -1232,6 +1234,17 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
       if (M > 0) ck(cudaMemcpyAsync(xy0, xs.dptr, 8, cudaMemcpyDeviceToHost, st), "x0");
       if (N > 0) ck(cudaMemcpyAsync(xy0 + 1, ys.dptr, 8, cudaMemcpyDeviceToHost, st), "y0");
       ck(cudaStreamSynchronize(st), "flags sync");
+      const bool tile_flagged = hf[3] || hf[4];
+      if (tile_flagged && !(flags & FGT_ASSUME_SORTED)) {
+        // unsorted input: the merge-path tiles of the speculative pass need
+        // not cover every element, so every check is redone element-wise on
+        // the arrays as given
+        int* fc = p->d_flag + kFullCheck;
+        ck(cudaMemsetAsync(fc, 0, sizeof(int) * 5, st), "flag");
+        ck(launch_check_points(xs.dptr, M, ys.dptr, N, fc, st), "check points");
+        ck(cudaMemcpyAsync(hf, fc, sizeof(int) * 5, cudaMemcpyDeviceToHost, st), "flags");
+        ck(cudaStreamSynchronize(st), "flags sync");
+      }
       // the reference checks targets, then sources (transform.cpp:202-204)
       if (hf[0]) raise(FGT_ERR_DOMAIN, "target coordinates must be finite");
       if (hf[1]) raise(FGT_ERR_DOMAIN, "source coordinates must be finite");
@@ -1246,7 +1259,7 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
         adopt_set(xs, M, p->t_sorted, flags, st, &p->d_xs, &p->own_xs, &p->d_tperm);
         adopt_set(ys, N, p->s_sorted, flags, st, &p->d_ys, &p->own_ys, &p->d_sperm);
       }
-      if (!p->t_sorted || !p->s_sorted) {
+      if (!p->t_sorted || !p->s_sorted || tile_flagged) {
         // metadata of the sorted stream; first coordinates after sorting
         plan_tiles(p, p->d_xs, p->d_ys, false, st);
         if (M > 0) ck(cudaMemcpyAsync(xy0, p->d_xs, 8, cudaMemcpyDeviceToHost, st), "x0");
@@ -1256,7 +1269,7 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
       // coordinate before the first merged element: the element itself
       const double x0 = xy0[0], y0 = xy0[1];
       p->zprev0 = has_prev ? z_prev : (M > 0 && N > 0) ? std::fmin(x0, y0) : (M > 0 ? x0 : y0);
-      if (!p->t_sorted || !p->s_sorted)
+      if (!p->t_sorted || !p->s_sorted || tile_flagged)
         classify_sync(p, st);
       else
         take_classes(p, hc);

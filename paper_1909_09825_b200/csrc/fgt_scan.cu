@@ -1721,9 +1721,15 @@ struct TileCtx {
 #ifndef FGT_PLAN_MINB
 #define FGT_PLAN_MINB 6
 #endif
-constexpr int kPlanPer = 16;                         // merged positions per thread
-constexpr int kPlanThreads = kPlanTile / kPlanPer;
-static_assert(kPlanPer == 16 && kSeg % kPlanPer == 0, "plan tile layout");
+// Merged positions per thread: one per segment of the tile, so a tile of
+// kPlanSegs segments has kSeg threads.  An odd window (15) spreads the
+// threads' merge reads over the shared-memory banks (the window starts are
+// ~7.5 doubles apart in each set; an even window of 16 put them 8 doubles =
+// 64 bytes apart, i.e. on the same banks).
+constexpr int kPlanPer = kPlanSegs;
+constexpr int kPlanThreads = kSeg;
+constexpr int kPlanWords = kPlanTile / 32;  // merge-mask words per tile
+static_assert(kPlanPer < 32 && kSeg % 32 == 0, "plan tile layout");
 
 // Staging plan of n values g[0..n) into a shared buffer: the 16-byte aligned
 // interior by one bulk copy, an unaligned head / tail element by plain
@@ -1759,9 +1765,6 @@ __device__ __forceinline__ int merge_path_smem(const double* x, int nx, const do
   return lo;
 }
 
-#ifndef FGT_PLAN_TWO_LEVEL
-#define FGT_PLAN_TWO_LEVEL 1
-#endif
 template <bool BATCH>
 __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorted,
                                                int64_t nseg, int64_t* __restrict__ seg_ib,
@@ -1773,14 +1776,17 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
                                                int* __restrict__ flags) {
   extern __shared__ __align__(16) double tsm[];
   __shared__ int sib[kPlanSegs + 1];
+  __shared__ uint32_t smask[kPlanWords];
+  __shared__ unsigned long long sgap[kPlanSegs];  // largest inner gap (bits of a double >= 0)
+  __shared__ double szf[kPlanSegs];               // first coordinate of each segment
   __shared__ int sflags;
   __shared__ __align__(8) uint64_t bar;
   const int64_t ib = c.ib, ie = c.ie;
   const int64_t jb = c.d0 - ib, je = c.d1 - ie;
   const int64_t nx64 = ie - ib, len64 = c.d1 - c.d0;
   if (nx64 < 0 || nx64 > len64) {
-    // partition of an unsorted stream (speculative pass): metadata is
-    // recomputed after sorting; report "unsorted" and bail out safely
+    // partition of an unsorted stream (speculative pass): the host re-checks
+    // the whole input (launch_check_points) and sorts; report and bail out
     if (threadIdx.x == 0) atomicOr(flags + 3, 1);
     return;
   }
@@ -1798,6 +1804,8 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
     sflags = 0;
     mbar_init(&bar);
   }
+  for (int w = t; w < kPlanWords; w += kPlanThreads) smask[w] = 0u;
+  if (t < kPlanSegs) sgap[t] = 0ull;
   __syncthreads();
   if (t == 0) {
     const unsigned bx = 8u * (unsigned)(stx.i1 - stx.i0), by = 8u * (unsigned)(sty.i1 - sty.i0);
@@ -1838,26 +1846,21 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
       f2 |= !(sx[i] == yv);
     }
   }
-  // merge: thread t owns merged positions [16 t, 16 t + 16) of the tile; it
-  // also tracks the largest gap between consecutive elements of its window
-  // (the gap into a segment's first element is left to classify_kernel)
-  const int d0 = t * kPlanPer;
-  const int nsegs_tile = (len + kSeg - 1) / kSeg;
-  unsigned bits = 0u;
-  double gmx = 0.0, zfirst = 0.0;
-#if FGT_PLAN_TWO_LEVEL
   // merge-path splits in two levels: the segment starts over the whole tile,
-  // then every other window inside its segment's split range (fewer
-  // shared-memory probes: the pass is bound by shared-memory traffic)
-  if ((d0 % kSeg) == 0 && d0 < len) sib[d0 / kSeg] = merge_path_smem(sx, nx, sy, ny, d0);
+  // then every thread's window inside its segment's split range
+  const int nsegs_tile = (len + kSeg - 1) / kSeg;
+  if (t < nsegs_tile) sib[t] = merge_path_smem(sx, nx, sy, ny, t * kSeg);
   if (t == 0) sib[nsegs_tile] = nx;
   __syncthreads();
-#endif
+  // merge: thread t owns merged positions [kPlanPer t, kPlanPer (t + 1)); it
+  // sets their mask bits (1 = target) and tracks the largest gap between
+  // consecutive elements per segment (the gap into a segment's first
+  // element is left to classify_kernel, which knows zprev)
+  const int d0 = t * kPlanPer;
   if (d0 < len) {
-#if FGT_PLAN_TWO_LEVEL
+    const int k = d0 / kSeg, D0 = k * kSeg;
     int i;
     {
-      const int k = d0 / kSeg, D0 = k * kSeg;
       const int D1 = D0 + kSeg < len ? D0 + kSeg : len;
       const int ilo = sib[k], ihi = sib[k + 1];
       const int jhi = D1 - ihi;
@@ -1872,10 +1875,6 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
       }
       i = lo;
     }
-#else
-    int i = merge_path_smem(sx, nx, sy, ny, d0);
-    if ((d0 % kSeg) == 0) sib[d0 / kSeg] = i;
-#endif
     int j = d0 - i;
     // no index clamps: on sorted input the merge never reads past a set's
     // sentinel; on unsorted input (flagged, redone after the sort) it can
@@ -1883,45 +1882,46 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
     double cx = sx[i];
     double cy = sy[j];
     double zp = fmax(i > 0 ? sx[i - 1] : -INFINITY, j > 0 ? sy[j - 1] : -INFINITY);
-    const bool seg_start = (d0 % kSeg) == 0;
-    auto step = [&](int e) {
-      const bool tgt = !(cy <= cx);  // sources first on ties
-      const double z = tgt ? cx : cy;
-      if (e > 0 || !seg_start) gmx = fmax(gmx, z - zp);
-      if (e == 0) zfirst = z;
-      zp = z;
-      bits |= (unsigned)tgt << e;
-      if (tgt) {
-        ++i;
-        cx = sx[i];
-      } else {
-        ++j;
-        cy = sy[j];
+    const int kb = D0 + kSeg;  // first position of the next segment
+    unsigned bits = 0u;
+    double ga = 0.0, gb = 0.0;
+#pragma unroll
+    for (int e = 0; e < kPlanPer; ++e) {
+      const int p = d0 + e;
+      if (p < len) {
+        const bool tgt = !(cy <= cx);  // sources first on ties
+        const double z = tgt ? cx : cy;
+        if (p == D0 || p == kb) {
+          szf[p / kSeg] = z;  // tile-local segment index
+        } else if (p < kb) {
+          ga = fmax(ga, z - zp);
+        } else {
+          gb = fmax(gb, z - zp);
+        }
+        zp = z;
+        bits |= (unsigned)tgt << e;
+        if (tgt) {
+          ++i;
+          cx = sx[i];
+        } else {
+          ++j;
+          cy = sy[j];
+        }
       }
-    };
-    if (d0 + kPlanPer <= len) {
-#pragma unroll
-      for (int e = 0; e < kPlanPer; ++e) step(e);
-    } else {
-#pragma unroll
-      for (int e = 0; e < kPlanPer; ++e)
-        if (d0 + e < len) step(e);
     }
+    const int sh = d0 & 31;
+    atomicOr(&smask[d0 >> 5], bits << sh);
+    if (sh + kPlanPer > 32) atomicOr(&smask[(d0 >> 5) + 1], bits >> (32 - sh));
+    atomicMax(&sgap[k], (unsigned long long)__double_as_longlong(ga));
+    if (d0 + kPlanPer > kb && k + 1 < kPlanSegs)
+      atomicMax(&sgap[k + 1], (unsigned long long)__double_as_longlong(gb));
   }
-  // per segment (16 threads = half a warp): largest gap, first coordinate
-#pragma unroll
-  for (int o = 8; o > 0; o >>= 1) gmx = fmax(gmx, __shfl_xor_sync(0xffffffffu, gmx, o));
-  if ((d0 % kSeg) == 0 && d0 < len) seg_gap[c.seg0 + d0 / kSeg] = make_double2(gmx, zfirst);
-#if !FGT_PLAN_TWO_LEVEL
-  if (t == 0) sib[nsegs_tile] = nx;
-#endif
-  // mask: two threads per 32-bit word, same layout as bit (merged pos % 32)
-  unsigned wd = bits << ((t & 1) * 16);
-  wd |= __shfl_down_sync(0xffffffffu, wd, 1);
-  if ((t & 1) == 0 && d0 < nsegs_tile * kSeg) seg_mask[c.seg0 * (kSeg / 32) + (t >> 1)] = wd;
   __syncthreads();
+  for (int w = t; w < nsegs_tile * (kSeg / 32); w += kPlanThreads)
+    seg_mask[c.seg0 * (kSeg / 32) + w] = smask[w];
   if (t < nsegs_tile) {
     const int k = t;
+    seg_gap[c.seg0 + k] = make_double2(__longlong_as_double((long long)sgap[k]), szf[k]);
     const int i0 = sib[k], i1 = sib[k + 1];
     const int sd0 = k * kSeg;
     const int sd1 = (sd0 + kSeg < len) ? sd0 + kSeg : len;
@@ -2027,6 +2027,40 @@ __global__ void __launch_bounds__(kPlanThreads, FGT_PLAN_MINB)
                            int* __restrict__ flags) {
   const TileCtx c = batch_ctx(b, blockIdx.x, tile_ib);
   plan_tile_body<true>(c, 1, 0, seg_ib, seg_jb, seg_info, seg_z, seg_mask, seg_gap, flags);
+}
+
+// Element-wise checks of the input as given (no partition involved):
+// flags[0] / [1] a non-finite target / source, [2] x[i] != y[i] somewhere
+// (M == N only), [3] / [4] targets / sources out of order.  The plan's tile
+// pass checks a sorted input in the same read as its metadata; on input it
+// finds unsorted (whose merge-path tiles need not cover every element) the
+// host runs this pass over the original arrays (check_points, transform.cpp:
+// 21-25; same_points, :214-216).
+__global__ void check_points_kernel(const double* __restrict__ x, int64_t M,
+                                    const double* __restrict__ y, int64_t N,
+                                    int* __restrict__ flags) {
+  const int64_t L = M > N ? M : N;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int f = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L; i += stride) {
+    double xv = 0.0, yv = 0.0;
+    if (i < M) {
+      xv = __ldg(x + i);
+      f |= !isfinite(xv) ? 1 : 0;
+      if (i > 0 && __ldg(x + i - 1) > xv) f |= 8;
+    }
+    if (i < N) {
+      yv = __ldg(y + i);
+      f |= !isfinite(yv) ? 2 : 0;
+      if (i > 0 && __ldg(y + i - 1) > yv) f |= 16;
+    }
+    if (M == N && !(xv == yv)) f |= 4;
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) {
+    for (int q = 0; q < 5; ++q)
+      if (f & (1 << q)) atomicOr(flags + q, 1);
+  }
 }
 
 // ------------------------------------------------------------------- K2
@@ -2291,6 +2325,18 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
   note_launch();
   plan_tile_kernel<<<(unsigned)ntiles, kPlanThreads, smem, st>>>(xs, M, ys, N, tile_ib, nseg, check_sorted,
                                                          seg_ib, seg_z, seg_mask, seg_gap, flags);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_points(const double* xs, int64_t M, const double* ys, int64_t N,
+                                int* flags, cudaStream_t st) {
+  const int64_t L = M > N ? M : N;
+  if (L == 0) return cudaSuccess;
+  int64_t blocks = (L + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  note_launch();
+  check_points_kernel<<<(unsigned)blocks, 256, 0, st>>>(xs, M, ys, N, flags);
   return cudaGetLastError();
 }
 

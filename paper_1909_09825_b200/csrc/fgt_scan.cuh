@@ -22,7 +22,7 @@ constexpr int kSegWarps = FGT_SEG_WARPS;  // segments (warps) per CTA in K1 / K3
 constexpr int kThreads = 32 * kSegWarps;
 constexpr int kMaxMom = kMaxDeg;        // highest moment order of the expansions
 #ifndef FGT_PLAN_SEGS
-#define FGT_PLAN_SEGS 16
+#define FGT_PLAN_SEGS 15
 #endif
 constexpr int kPlanSegs = FGT_PLAN_SEGS;  // segments per plan tile
 constexpr int kPlanTile = kPlanSegs * kSeg;  // merged elements per plan tile
@@ -113,6 +113,10 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
                               const int64_t* tile_ib, int64_t ntiles, int64_t nseg,
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
                               uint32_t* seg_mask, double2* seg_gap, int* flags, cudaStream_t st);
+// Element-wise checks of unsorted input (flags[0..4] as launch_plan_tiles,
+// zeroed by the caller) over the arrays as given.
+cudaError_t launch_check_points(const double* xs, int64_t M, const double* ys, int64_t N,
+                                int* flags, cudaStream_t st);
 // Batched plans: per-transform offsets (B+1 each, concatenated arrays) and
 // the first global segment of each transform (B+1).  Partition at
 // kPlanTile granularity inside each transform, then the tile pass writes the

@@ -65,11 +65,11 @@ def test_cfg3_full_size(delta):
     y = np.sort(up(n, 0, 0))
     a = 2.0 * up(n, 0, 1) - 1.0
     u = run(x, y, a, delta, 6)
-    ref = None
-    if delta == 1e-3:
-        ref = oracle.transform(x, y, a, delta, ne=6, mode=0, threads=THREADS)
-        err = np.max(np.abs(u - ref)) / np.sum(np.abs(a))
-        assert err <= 1e-12, err
+    # the whole delta sweep of BASELINE cfg 3 against the oracle over all
+    # targets (the reference's own delta-sweep gate: acceptance.cpp:394-423)
+    ref = oracle.transform(x, y, a, delta, ne=6, mode=0, threads=THREADS)
+    err = np.max(np.abs(u - ref)) / np.sum(np.abs(a))
+    assert err <= 1e-12, err
     check_direct(x, y, a, delta, u, 6, 1e-10, ref)
 
 
@@ -100,3 +100,50 @@ def test_cfg4_clustered_full_size():
     err = np.max(np.abs(u - ref)) / np.sum(np.abs(a))
     assert err <= 1e-12, err
     check_direct(x, y, a, 1e-6, u, 5, 1e-8, ref)
+
+
+def test_cfg1_direct_on_1000_sampled_targets():
+    # BASELINE cfg 1 / SURVEY 8(d): N=M=1e5 presorted, delta 1e-2, tol 1e-10
+    # (n_e = 6); the reference CPU transform on all targets and the direct
+    # sum on 1000 targets drawn like fgt1d_cli.cpp:198-218 (stream 2)
+    n = 100_000
+    x = np.sort(up(n, 0, 3))
+    y = np.sort(up(n, 0, 0))
+    a = 2.0 * up(n, 0, 1) - 1.0
+    u = run(x, y, a, 1e-2, 6)
+    ref = oracle.ref_transform(x, y, a, 1e-2, ne=6, mode=0)[0] if oracle.ref_available() else \
+        oracle.transform(x, y, a, 1e-2, ne=6, mode=0)
+    assert np.max(np.abs(u - ref)) / np.sum(np.abs(a)) <= 1e-12
+    idx = np.minimum(n - 1, (up(1000, 0, 2) * n).astype(np.int64))
+    d = oracle.direct(x, y, a, 1e-2, idx)
+    keep = np.abs(d) >= 1e-3 * np.max(np.abs(d))
+    rel = np.max(np.abs(u[idx][keep] - d[keep]) / np.abs(d[keep]))
+    rel_ref = np.max(np.abs(ref[idx][keep] - d[keep]) / np.abs(d[keep]))
+    assert np.max(np.abs(u[idx] - d)) / np.sum(np.abs(a)) <= 1.05 * E_N[6]
+    assert rel <= max(1.1 * rel_ref, 1e-10), (rel, rel_ref)
+
+
+@pytest.mark.parametrize("tol", [1e-3, 1e-6, 1e-10])
+def test_cfg5_batched_full_shape(tol):
+    # BASELINE cfg 5: 4096 independent transforms of N=M=65536, transform b
+    # from seed b (targets stream 3, sources 0, alpha = 2u-1 stream 1),
+    # presorted, delta_b = 10^(-6+5u) (seed 0, stream 9); one batched plan.
+    # Oracle on 64 transforms incl. the smallest and largest delta, over all
+    # their targets (per-transform semantics: transform.cpp:249-253).
+    B, n = 4096, 65536
+    deltas = 10.0 ** (-6.0 + 5.0 * up(B, 0, 9))
+    xs = [np.sort(up(n, b, 3)) for b in range(B)]
+    ys = [np.sort(up(n, b, 0)) for b in range(B)]
+    al = [2.0 * up(n, b, 1) - 1.0 for b in range(B)]
+    soe = fgt.soe_for_tolerance(tol)
+    ne = len(soe)
+    out = fgt.batch_transform(xs, ys, al, deltas, soe)
+    pick = set(np.random.default_rng(int(ne)).choice(B, size=62, replace=False).tolist())
+    pick |= {int(np.argmin(deltas)), int(np.argmax(deltas))}
+    worst = 0.0
+    for b in sorted(pick):
+        ref = oracle.transform(xs[b], ys[b], al[b], deltas[b], ne=ne, mode=0)
+        err = np.max(np.abs(out[b] - ref)) / np.sum(np.abs(al[b]))
+        worst = max(worst, err)
+        assert err <= 1e-12, (b, deltas[b], err)
+    assert len(pick) >= 64

@@ -105,3 +105,17 @@ def test_rng_pins():
     assert L.oracle_counter_rand(42, 1, 7) == 0x8d3b7fd7abb430ae
     assert up(1, 0, 0)[0] == 0.65244848637403219
     assert abs(up(1, 123456789, 3, offset=1000000)[0] - 0.17446248443028345) < 1e-16
+
+
+def test_gap_table_and_rng_restatements_match_reference():
+    # precompute_gap_table (transform.cpp:221-237) and rng::uniform_points
+    # (rng.cpp:7-29) of the C restatement, bit for bit against the reference
+    if not oracle.ref_available():
+        pytest.skip("reference library not built")
+    from paper_1909_09825_b200.transform import uniform_points_array as up
+    x = np.sort(np.concatenate([up(700, 31, 3), up(700, 31, 3)[:40], [5.0, 90.0]]))
+    for delta, ne in ((0.8, 5), (1e-6, 6), (1e3, 3)):
+        assert np.array_equal(oracle.gap_table(x, delta, ne), oracle.ref_gap_table(x, delta, ne))
+    for seed, stream in ((0, 0), (42, 1), (123456789, 3)):
+        assert np.array_equal(oracle.ref_uniform_points(10_000, seed, stream), up(10_000, seed, stream))
+    assert oracle.ref_lib().fgt_ref_counter_rand(123456789, 3, 1000000) == 0x2ca992c901c93ced
