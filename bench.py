@@ -99,18 +99,46 @@ def cpu_info():
     return model
 
 
-def reference_sample(args, threads):
-    """Reference CPU path (oracle/_ref = the reference's own transform.cpp, or the
-    C restatement when the reference was not built) on a bounded presorted sample
-    of the same workload: plan -> precompute_gap_table -> apply_general, timed
-    like proj/tools/fgt1d_cli.cpp:240-251."""
+def ne_for_tolerance(tol):
+    """SURVEY 8(a13) / README.md:184-189: the fewest preset modes whose
+    documented transform error is <= tol (kept here so the reference arm
+    never loads the product library)."""
+    for ne, t in ((3, 1e-3), (4, 1e-6), (5, 1e-8), (6, 1e-10), (7, 1e-11)):
+        if tol >= t:
+            return ne
+    raise ValueError("tolerance below the reach of the CF tables")
+
+
+def workload_config(n, delta, tol):
+    """The workload both arms report (identical dicts: same_config)."""
+    ne = ne_for_tolerance(tol)
+    return {"workload": f"cfg3: N=M={n:.0e} presorted uniform [0,1], alpha=2u-1, "
+                        f"delta={delta:g}, tol={tol:g} (n_e={ne})",
+            "n_e": ne, "delta": delta, "M": n, "N": n,
+            "l2": "inputs (3.2 GB) >> 126 MB L2; no flush needed"}
+
+
+def reference_inputs(n, seed):
+    """cfg3 inputs from the reference library's own generator
+    (rng::uniform_points, rng.cpp:24-29): sorted targets (stream 3), sorted
+    sources (stream 0), alpha = 2u-1 index-aligned with the sorted sources
+    (stream 1), as run_bench_once with --presort (fgt1d_cli.cpp:228-239)."""
     import oracle
-    from paper_1909_09825_b200.transform import uniform_points_array
-    n = int(args.cpu_sample)
-    ne = mode_count(args.tol)
-    x = np.sort(uniform_points_array(n, args.seed, 3))
-    y = np.sort(uniform_points_array(n, args.seed, 0))
-    a = 2.0 * uniform_points_array(n, args.seed, 1) - 1.0
+    x = np.sort(oracle.ref_uniform_points(n, seed, 3))
+    y = np.sort(oracle.ref_uniform_points(n, seed, 0))
+    a = 2.0 * oracle.ref_uniform_points(n, seed, 1) - 1.0
+    return x, y, a
+
+
+def reference_sample(args, threads, n=None, data=None):
+    """One run of the reference's own CPU path (oracle/_ref = the reference's
+    transform.cpp compiled unmodified; the C restatement if it was not built):
+    plan -> precompute_gap_table -> apply_general, phases timed like
+    proj/tools/fgt1d_cli.cpp:240-251."""
+    import oracle
+    n = int(args.cpu_sample) if n is None else int(n)
+    ne = ne_for_tolerance(args.tol)
+    x, y, a = data if data is not None else reference_inputs(n, args.seed)
     if oracle.ref_available():
         t0 = time.perf_counter()
         _u, (t_sort, t_pre, t_rem) = oracle.ref_transform(x, y, a, args.delta, ne=ne, mode=0,
@@ -127,41 +155,50 @@ def reference_sample(args, threads):
                 kind=kind, n=n, ne=ne)
 
 
-def mode_count(tol):
-    from paper_1909_09825_b200.soe import mode_count_for_tolerance
-    return mode_count_for_tolerance(tol)
-
-
 def run_reference(args):
+    """--impl reference: the reference's CPU transform on the SAME workload as
+    our arm (N = M = args.n, default 1e8), rank 0 only.  Its only parallelism
+    is one thread per folded mode (transform.cpp:167-168), so threads =
+    min(n_e, nproc).  Warm-up runs use a 1e6-point sample of the workload
+    (they only page in code and allocator state; a full-size warm-up would
+    add ~30 s each); every timed step is the full workload."""
     rank, world, _ = env_rank()
     if rank != 0:
         return
-    threads = max(1, min(mode_count(args.tol), os.cpu_count() or 1))
-    res = None
+    ne = ne_for_tolerance(args.tol)
+    threads = max(1, min(ne, os.cpu_count() or 1))
+    n = int(args.n)
+    warm_n = min(n, 1_000_000)
+    warm = reference_inputs(warm_n, args.seed)
     for _ in range(args.warmup):
-        reference_sample(args, threads)
-    vals = []
+        reference_sample(args, threads, n=warm_n, data=warm)
+    del warm
+    data = reference_inputs(n, args.seed)
+    res, totals = None, []
+    phases = np.zeros(3)
     t_all = time.perf_counter()
     for _ in range(args.steps):
-        res = reference_sample(args, threads)
-        vals.append(res["t_total"])
+        res = reference_sample(args, threads, n=n, data=data)
+        totals.append(res["t_total"])
+        phases += np.array([res["t_sort"], res["t_pre"], res["t_rem"]])
     wall = time.perf_counter() - t_all
-    n = int(args.cpu_sample)
-    ms = 1e3 * float(np.mean(vals))
+    ms = 1e3 * float(np.mean(totals))
     value = 2.0 * n / (ms / 1e3)
-    sample = (f"N=M={n} presorted uniform (seed {args.seed}), delta={args.delta}, "
-              f"n_e={res['ne']}: plan + precompute_gap_table + apply_general, "
-              f"threads={threads} (mode parallelism, transform.cpp:167-168)")
+    ph = phases / max(args.steps, 1)
+    sample = (f"the whole workload every step: N=M={n} presorted uniform (seed {args.seed}), "
+              f"delta={args.delta}, n_e={ne}: plan + precompute_gap_table + apply_general, "
+              f"threads={threads} (mode parallelism, transform.cpp:167-168); "
+              f"warm-up runs on N=M={warm_n}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference counter RNG)",
-        "config": {"workload": f"cfg3 sample: N=M={n} presorted uniform, delta={args.delta}, tol={args.tol}",
-                   "n_e": res["ne"], "delta": args.delta},
+        "data": "synthetic (reference counter RNG rng::uniform_points)",
+        "config": workload_config(n, args.delta, args.tol),
+        "parallelism": f"reference CPU path, {threads} threads",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": res["kind"],
                          "sample": sample, "cpu": cpu_info(), "nproc": os.cpu_count(),
-                         "t_sort": res["t_sort"], "t_pre": res["t_pre"], "t_rem": res["t_rem"]},
+                         "t_sort": ph[0], "t_pre": ph[1], "t_rem": ph[2]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
@@ -652,12 +689,9 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference counter RNG, seed 0; sorted on device by our radix sort)",
-            "config": {"workload": f"cfg3: N=M={n:.0e} presorted uniform [0,1], alpha=2u-1, "
-                                   f"delta={args.delta:g}, tol={args.tol:g} (n_e={ne})",
-                       "n_e": ne, "delta": args.delta, "M": n, "N": n,
-                       "parallelism": (f"merged-stream chunks x{world}" if world > 1 else
-                                       "1 GPU (chunk path)" if args.chunk_path else "1 GPU"),
-                       "l2": "inputs (3.2 GB) >> 126 MB L2; no flush needed"},
+            "config": workload_config(n, args.delta, args.tol),
+            "parallelism": (f"merged-stream chunks x{world}" if world > 1 else
+                            "1 GPU (chunk path)" if args.chunk_path else "1 GPU"),
             # dominant kernel: K3 (main pass) -- reads x, y, alpha and writes u,
             # 16 B per merged point, timed by CUDA events on the launching stream
             "roofline": {"bound": "hbm", "achieved": achieved_k3, "peak": hbm_peak, "unit": "GB/s",

@@ -1,6 +1,7 @@
 """bench.py --impl reference (the reference arm: the reference's own CPU
-transform path on a bounded sample), single process and under torchrun
-(rank 0 alone prints; the other ranks exit 0).  CPU only."""
+transform path on our arm's workload), single process and under torchrun
+(rank 0 alone prints; the other ranks exit 0).  CPU only; a small --n keeps
+it quick (the driver runs the default N = M = 1e8)."""
 import json
 import os
 import socket
@@ -8,7 +9,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-ARGS = ["--impl", "reference", "--steps", "2", "--warmup", "1", "--cpu-sample", "20000"]
+ARGS = ["--impl", "reference", "--steps", "2", "--warmup", "1", "--size", "20000"]
 
 
 def _lines(out):
@@ -27,6 +28,24 @@ def test_reference_arm_line():
     assert cb["kind"] in ("reference", "port")
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
+    # same workload dict as our arm reports
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.workload_config(20000, 1e-3, 1e-10)
+
+
+def test_reference_arm_loads_no_product_code():
+    # the reference arm runs the reference's own transform (oracle/_ref) and
+    # nothing of the product: no package import, no libfgt1d_b200.so mapped
+    code = ("import sys, bench; sys.argv = ['bench.py'] + %r; bench.main(); "
+            "import sys; maps = open('/proc/self/maps').read(); "
+            "assert 'libfgt1d_b200' not in maps, 'product library mapped'; "
+            "assert not any(m.startswith('paper_1909_09825_b200') for m in sys.modules); "
+            "print('CLEAN')" % (ARGS,))
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "CLEAN" in out.stdout
 
 
 def test_reference_arm_under_torchrun_prints_once():

@@ -55,5 +55,5 @@ def test_bench_chunk_path_single_rank():
     out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
-    assert d["config"]["parallelism"] == "1 GPU (chunk path)"
+    assert d["parallelism"] == "1 GPU (chunk path)"
     assert d["multi_rank_check"]["pass"], d["multi_rank_check"]
