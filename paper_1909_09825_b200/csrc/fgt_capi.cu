@@ -220,7 +220,6 @@ struct fgt_plan_s {
   int64_t ntiles = 0;  // segments of kSeg merged elements
   int64_t* d_tile_ib = nullptr;
   double2* d_seg_z = nullptr;
-  double2* d_seg_gap = nullptr;  // per segment: largest inner gap, first coordinate
   int* d_seg_deg = nullptr;      // per segment: packed degrees (classify_kernel)
   uint32_t* d_seg_mask = nullptr;
   // batched plans (fgt_batch_create)
@@ -231,6 +230,8 @@ struct fgt_plan_s {
   ModeTable* d_mtb = nullptr;
   // segment classes (launch_classify): K1 / K3 wide-path segment counts
   int64_t nwide1 = -1, nwide3 = -1;
+  int dn_narrow = -1;  // highest collapsed degree of the K3-narrow segments
+  CollConsts cc{};     // collapsed-form constants of the plan (single plans)
   double zprev0 = 0.0;
   int* d_flag = nullptr;
   ChunkState cs;
@@ -421,10 +422,11 @@ unsigned char* pinned_scratch() {
   return s.p;
 }
 
-// d_flag: tile-pass check flags 0..4, two 64-bit segment-class counters at
-// ints 8..11, element-wise check flags (launch_check_points) at 12..16.
-constexpr int kFlagInts = 20;
-constexpr int kFullCheck = 12;
+// d_flag: tile-pass check flags 0..4, three 64-bit segment-class counters at
+// ints 8..13 (launch_classify), element-wise check flags
+// (launch_check_points) at 16..20.
+constexpr int kFlagInts = 24;
+constexpr int kFullCheck = 16;
 unsigned long long* class_counts(fgt_plan_s* p) {
   return reinterpret_cast<unsigned long long*>(p->d_flag + 8);
 }
@@ -434,6 +436,7 @@ StreamArgs stream_args(const fgt_plan_s* p, const double* bs) {
                 p->d_seg_z, p->d_seg_mask, p->d_seg_info, p->d_seg_jb, p->d_mtb};
   sa.nwide1 = p->nwide1;
   sa.nwide3 = p->nwide3;
+  sa.dn_narrow = p->dn_narrow;
   sa.seg_deg = p->d_seg_deg;
   return sa;
 }
@@ -444,19 +447,20 @@ void queue_classify(fgt_plan_s* p, unsigned long long* h, cudaStream_t st,
                     bool check_flags = false, bool zprev0_first = false) {
   StreamArgs sa = stream_args(p, nullptr);
   sa.zprev0_first = zprev0_first;
-  ck(launch_classify(sa, p->P, p->P.smax, p->d_seg_gap, p->d_seg_deg,
+  ck(launch_classify(sa, p->P, p->P.smax, p->d_seg_deg,
                      check_flags ? p->d_flag : nullptr, class_counts(p), st),
      "classify");
-  ck(cudaMemcpyAsync(h, class_counts(p), 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+  ck(cudaMemcpyAsync(h, class_counts(p), 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                      st),
      "class counts");
 }
 void take_classes(fgt_plan_s* p, const unsigned long long* h) {
   p->nwide1 = (int64_t)h[0];
   p->nwide3 = (int64_t)h[1];
+  p->dn_narrow = (int)h[2] - 1;
 }
 void classify_sync(fgt_plan_s* p, cudaStream_t st) {
-  unsigned long long hl[2] = {0, 0};
+  unsigned long long hl[3] = {0, 0, 0};
   unsigned char* pin = pinned_scratch();
   unsigned long long* h = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hl;
   queue_classify(p, h, st);
@@ -474,7 +478,7 @@ void plan_tiles(fgt_plan_s* p, const double* xd, const double* yd, bool check_so
   int64_t* tib = dmalloc<int64_t>(ntl + 1, st);
   ck(launch_partition(xd, p->M, yd, p->N, kPlanTile, ntl, tib, st), "partition");
   ck(launch_plan_tiles(xd, p->M, yd, p->N, tib, ntl, p->ntiles, check_sorted ? 1 : 0,
-                       p->d_tile_ib, p->d_seg_z, p->d_seg_mask, p->d_seg_gap, p->d_flag, st),
+                       p->d_tile_ib, p->d_seg_z, p->d_seg_mask, p->d_flag, st),
      "plan tiles");
   dfree(tib, st);
 }
@@ -484,6 +488,7 @@ void plan_tiles(fgt_plan_s* p, const double* xd, const double* yd, bool check_so
 void upload_modes(fgt_plan_s* p, cudaStream_t st) {
   ModeTable T;
   build_modes(p->soe, p->delta, p->P, T);
+  p->cc = coll_consts(T.gpoly);
   p->d_mt = dmalloc<ModeTable>(1, st);
   ck(launch_store_table(T, p->d_mt, st), "store mode table");
 }
@@ -524,7 +529,6 @@ void destroy_plan(fgt_plan_s* p) {
   dfree(p->d_sperm, st);
   dfree(p->d_tile_ib, st);
   dfree(p->d_seg_z, st);
-  dfree(p->d_seg_gap, st);
   dfree(p->d_seg_deg, st);
   dfree(p->d_seg_mask, st);
   dfree(p->d_seg_jb, st);
@@ -617,7 +621,7 @@ void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint3
     o.tperm = p->d_tperm;
     {
       ProfScope ps(2, st);
-      ck(launch_main(sa, p->P, p->d_mt, ts, o, st), "main pass");
+      ck(launch_main(sa, p->P, p->d_mt, ts, o, st, p->batch ? nullptr : &p->cc), "main pass");
     }
   }
   note_use(p, st);
@@ -711,7 +715,7 @@ void run_chunk_finish(fgt_plan_s* p, const double* strengths, const cplx* carry_
   o.tperm = p->d_tperm;
   {
     ProfScope ps(2, st);
-    ck(launch_main(sa, p->P, p->d_mt, ts, o, st), "main pass");
+    ck(launch_main(sa, p->P, p->d_mt, ts, o, st, p->batch ? nullptr : &p->cc), "main pass");
   }
   note_use(p, st);
   if (!dev) {
@@ -796,7 +800,6 @@ fgt_plan_s* pipe_chunk_plan(const double* dx, int64_t M, const double* dy, int64
     p->ntiles = (M + N + kSeg - 1) / kSeg;
     p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
     p->d_seg_z = dmalloc<double2>(p->ntiles, st);
-    p->d_seg_gap = dmalloc<double2>(p->ntiles, st);
     p->d_seg_deg = dmalloc<int>(p->ntiles, st);
     p->d_seg_mask = dmalloc<uint32_t>((size_t)p->ntiles * (kSeg / 32), st);
     p->d_xs = const_cast<double*>(dx);
@@ -806,9 +809,10 @@ fgt_plan_s* pipe_chunk_plan(const double* dx, int64_t M, const double* dy, int64
     plan_tiles(p, dx, dy, true, st);
     p->d_mt = dmalloc<ModeTable>(1, st);
     ck(launch_store_table(T, p->d_mt, st), "store mode table");
+    p->cc = coll_consts(T.gpoly);
     p->zprev0 = zprev;
     const StreamArgs sa = stream_args(p, nullptr);
-    ck(launch_classify(sa, p->P, p->P.smax, p->d_seg_gap, p->d_seg_deg, nullptr,
+    ck(launch_classify(sa, p->P, p->P.smax, p->d_seg_deg, nullptr,
                        class_counts(p), st),
        "classify");
     p->nwide1 = p->nwide3 = -1;
@@ -1080,7 +1084,7 @@ void transform_host(const double* x, int64_t M, const double* y, int64_t N, cons
       ck(launch_carry_scan(ts, p->ntiles, ne, d_car + g * 2 * ne, nullptr, st), "carry scan");
       OutArgs o;
       o.u = du + c.i0;
-      ck(launch_main(sa, P, p->d_mt, ts, o, st), "main pass");
+      ck(launch_main(sa, P, p->d_mt, ts, o, st, &p->cc), "main pass");
     }
     pipe_chunk_destroy(p);
     cudaEvent_t done = ps.event();
@@ -1211,8 +1215,7 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
       p->ntiles = (L + kSeg - 1) / kSeg;
       p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
       p->d_seg_z = dmalloc<double2>(p->ntiles, st);
-      p->d_seg_gap = dmalloc<double2>(p->ntiles, st);
-      p->d_seg_deg = dmalloc<int>(p->ntiles, st);
+        p->d_seg_deg = dmalloc<int>(p->ntiles, st);
       p->d_seg_mask = dmalloc<uint32_t>((size_t)p->ntiles * (kSeg / 32), st);
       // one read of both sets: checks + (speculative) segment metadata
       plan_tiles(p, xs.dptr, ys.dptr, !(flags & FGT_ASSUME_SORTED), st);
@@ -1223,7 +1226,7 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
       unsigned char* pin = pinned_scratch();
       int hfl[8] = {0};
       double xyl[2] = {0.0, 0.0};
-      unsigned long long hcl[2] = {0, 0};
+      unsigned long long hcl[3] = {0, 0, 0};
       int* hf = pin ? reinterpret_cast<int*>(pin) : hfl;
       double* xy0 = pin ? reinterpret_cast<double*>(pin + 32) : xyl;
       unsigned long long* hc = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hcl;
@@ -1629,7 +1632,6 @@ extern "C" int fgt_batch_create(int B, const double* targets, const int64_t* t_o
       p->d_seg_jb = dmalloc<int64_t>(nseg + 1, st);
       p->d_seg_info = dmalloc<int4>(nseg + 1, st);
       p->d_seg_z = dmalloc<double2>(nseg + 1, st);
-      p->d_seg_gap = dmalloc<double2>(nseg + 1, st);
       p->d_seg_deg = dmalloc<int>(nseg + 1, st);
       p->d_seg_mask = dmalloc<uint32_t>((size_t)(nseg + 1) * (kSeg / 32), st);
       Work w{st, {}};
@@ -1647,7 +1649,7 @@ extern "C" int fgt_batch_create(int B, const double* targets, const int64_t* t_o
         ck(cudaMemcpyAsync(d_ttid, tile_tid.data(), 4 * ntl, cudaMemcpyHostToDevice, st), "tile map");
       ck(launch_batch_plan(xs.dptr, ys.dptr, d_toff, d_soff, d_sbase, d_tbase, d_ttid, B, ntl,
                            d_tib, p->d_tile_ib, p->d_seg_jb, p->d_seg_info, p->d_seg_z,
-                           p->d_seg_mask, p->d_seg_gap, p->d_flag, st),
+                           p->d_seg_mask, p->d_flag, st),
          "batch plan");
       unsigned char* pin = pinned_scratch();
       int hfl[8] = {0};
@@ -1669,7 +1671,7 @@ extern "C" int fgt_batch_create(int B, const double* targets, const int64_t* t_o
       ck(launch_batch_modes(base, d_deltas, B, p->d_mtb, st), "mode tables");
       p->d_mt = dmalloc<ModeTable>(1, st);
       ck(launch_store_table(T0, p->d_mt, st), "mode table");
-      unsigned long long hcl[2] = {0, 0};
+      unsigned long long hcl[3] = {0, 0, 0};
       unsigned long long* hc = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hcl;
       queue_classify(p, hc, st, true);
       ck(cudaStreamSynchronize(st), "batch plan sync");

@@ -1087,6 +1087,16 @@ __device__ __forceinline__ double seg_smax(const StreamArgs& a, const SegGeom& g
   return a.mtb ? __ldg(&a.mtb[g.tid].smax) : smax;
 }
 
+// Taylor degree of a segment's gap factors from its lane runs (r.g = gaps,
+// the first one from the element before the run): the largest gap of the
+// segment including the one into its first element.  Warp-collective.
+__device__ __forceinline__ int run_gap_degree(const ModeParams& P, double smax, const LaneRun& r) {
+  double gm = r.g[0];
+#pragma unroll
+  for (int e = 1; e < kR; ++e) gm = fmax(gm, r.g[e]);
+  return pick_degree(P, smax, warp_max(gm));
+}
+
 // Wide segments: lane aggregates from the gap factors (degree-D Taylor,
 // exact for D < 0), reduced across the warp in lane order.
 __device__ __forceinline__ void seg_aggregate_wide(const ModeTable& mt, int ne, int D, int lane,
@@ -1277,7 +1287,7 @@ __global__ void __launch_bounds__(kThreads, FGT_K1_MINB)
 #pragma unroll
         for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
         r.g[0] -= zp;
-        seg_aggregate_wide(mx, ne, seg_deg_D(deg), lane, r, a.nseg, s, ts);
+        seg_aggregate_wide(mx, ne, run_gap_degree(P, mx.smax, r), lane, r, a.nseg, s, ts);
       }
     }
   }
@@ -1336,39 +1346,45 @@ __global__ void batch_modes_kernel(BatchModeBase base, const double* __restrict_
 }
 
 // Plan-time segment classes: counts[0] = K1 wide segments, counts[1] = K3.
-__global__ void classify_kernel(StreamArgs a, ModeParams P, double smax,
-                                const double2* __restrict__ seg_gap, int* __restrict__ seg_deg,
+__global__ void classify_kernel(StreamArgs a, ModeParams P, double smax, int* __restrict__ seg_deg,
                                 const int* __restrict__ skip_flags,
                                 unsigned long long* __restrict__ counts) {
   // metadata of a rejected batch (non-finite / unsorted) is not valid
   if (skip_flags && (skip_flags[0] | skip_flags[1] | skip_flags[3] | skip_flags[4])) return;
   const int lane = threadIdx.x & 31;
   unsigned long long c1 = 0, c3 = 0;
+  unsigned dn1 = 0;  // highest DN + 1 among this thread's K3-narrow segments
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t s0 = (int64_t)blockIdx.x * blockDim.x; s0 < a.nseg; s0 += stride) {
     const int64_t s = s0 + threadIdx.x;
     bool w1 = false, w3 = false;
     if (s < a.nseg) {
       SegGeom g = seg_geom(a, s);
-      const double2 gz = seg_gap[s];
-      if (s == 0 && a.zprev0_first) g.zprev = gz.y;
+      if (s == 0 && a.zprev0_first) {
+        // a stream without a predecessor: segment 0 starts at its own first
+        // element, the smaller of the first target / source
+        g.zprev = fmin(a.M > 0 ? __ldg(a.xs) : INFINITY, a.N > 0 ? __ldg(a.ys) : INFINITY);
+      }
       const double sm = seg_smax(a, g, smax);
       const int DM = seg_moment_degree(P, sm, seg_frame(g));
-      // the gap factors' degree: largest gap of the segment including the
-      // one from the element before it (as the kernels' lane runs see them)
-      const int D = pick_degree(P, sm, fmax(gz.x, gz.y - g.zprev));
+      // the gap factors' degree is chosen by the wide kernels from their own
+      // lane runs (run_gap_degree)
+      const int D = -1;
       const SegFrame f = seg_frame(g);
       const int DN = pick_degree(P, sm, f.h0 + f.h1);
       seg_deg[s] = (D + 1) | ((DM + 1) << 8) | ((DN + 1) << 16);
       w1 = !k1_narrow(DM);
       w3 = !k3_narrow(DM);
+      if (!w3 && DN + 1 > dn1) dn1 = DN + 1;
     }
     c1 += __popc(__ballot_sync(0xffffffffu, w1));
     c3 += __popc(__ballot_sync(0xffffffffu, w3));
   }
+  dn1 = __reduce_max_sync(0xffffffffu, dn1);
   if (lane == 0) {
     atomicAdd(counts, c1);
     atomicAdd(counts + 1, c3);
+    if (dn1 > 0) atomicMax(counts + 2, (unsigned long long)dn1);
   }
 }
 
@@ -1481,6 +1497,7 @@ __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParam
 #pragma unroll
     for (int e = kR - 1; e > 0; --e) r.g[e] -= r.g[e - 1];
     r.g[0] -= zp;
+    D = run_gap_degree(P, mx.smax, r);
     if constexpr (!WIDE) __syncwarp();
     double out[kR];
 #pragma unroll
@@ -1682,6 +1699,309 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
   }
 }
 
+// ------------------------------------------------------- K3 narrow (k3n)
+//
+// The collapsed narrow pass with a launch-uniform degree DN (the plan's
+// highest collapsed degree over its narrow segments; a higher degree than a
+// segment needs only adds terms below 2^-52).  Per segment, per warp:
+//   stage   : the next segment's x / y / beta by TMA bulk copies, its merge
+//             mask words and its collapsed carries E^c_q (one 64-byte bulk
+//             copy; written by collapse_carries_kernel after K2) land in the
+//             warp's shared-memory stage while this one is computed
+//   decode  : lane runs of kR merged elements from the mask (w = z - zc, b)
+//   moments : lane-run source moments, NM = DN + 1 warp scans -> exclusive
+//             lane prefix Pre_m and segment totals Tot_m
+//   evaluate: u(w) = sum_q w^q [E_q + sum_{m+q odd} H[m][q] Pre_m(w)],
+//             E_q = E^c_q + sum_m B[q][m] Tot_m  (collapsed_segment's form)
+//   store   : potentials staged in shared memory, written back by one TMA
+//             bulk store per segment (or scattered through the permutation)
+// No per-mode work and no branches on the element loop.
+constexpr int kK3nStageXY = kSeg + 16;
+constexpr int kK3nStageB = kSeg + 12;
+struct K3nStage {
+  double* xy;      // [kK3nStageXY]  x at slot ox, y at slot oy
+  double* bb;      // [kK3nStageB]   b at slot ob
+  double* su;      // [kSeg + 2]     staged potentials
+  double* ec;      // [kEcStride]    collapsed carries
+  uint32_t* mask;  // [kSeg / 32]
+  double* zero;    // one 0.0 (the strength slot of every target)
+  uint64_t* bar;
+};
+constexpr size_t kK3nWarpBytes =
+    sizeof(double) * (kK3nStageXY + kK3nStageB + (kSeg + 2) + kEcStride + 2) + 4 * (kSeg / 32) + 16;
+static_assert(kK3nWarpBytes % 16 == 0, "k3n stage alignment");
+__device__ __forceinline__ K3nStage k3n_stage(unsigned char* base) {
+  K3nStage p;
+  p.xy = reinterpret_cast<double*>(base);
+  p.bb = p.xy + kK3nStageXY;
+  p.su = p.bb + kK3nStageB;
+  p.ec = p.su + kSeg + 2;
+  p.zero = p.ec + kEcStride;
+  p.mask = reinterpret_cast<uint32_t*>(p.zero + 2);
+  p.bar = reinterpret_cast<uint64_t*>(p.mask + kSeg / 32);
+  return p;
+}
+
+__device__ __forceinline__ void bulk_s2g(double* dst, const double* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+// Lanes 0..2 bulk-copy the 16-byte aligned interiors of x / y / b, lane 3 the
+// mask words, lane 10 the collapsed carries, lanes 4..9 the unaligned head /
+// tail elements by 8-byte cp.async.
+__device__ __forceinline__ void k3n_issue(const StreamArgs& a, const double* ec, int64_t s,
+                                          const SegGeom& g, const K3nStage& sp, int lane) {
+  const StageSlots o = stage_slots(a, g);
+  if (lane == 0) {
+    fence_proxy_async();  // earlier generic reads of the stage before async writes
+    mbar_expect(sp.bar, stage_bulk_bytes(o, g) + 32u + 8u * kEcStride);
+  }
+  __syncwarp();
+  const int arr = lane < 3 ? lane : ((lane - 4) >> 1);  // 0 x, 1 y, 2 b (lanes < 10)
+  const double* src = arr == 0 ? a.xs + g.ib : (arr == 1 ? a.ys + g.jb : a.bs + g.jb);
+  const int n = arr == 0 ? g.nx : g.ny;
+  const int so = arr == 0 ? o.ox : (arr == 1 ? o.oy : o.ob);
+  double* buf = arr == 2 ? sp.bb : sp.xy;
+  const int h = so & 1;
+  int c = (n - h) & ~1;
+  if (c < 0) c = 0;
+  if (lane < 3) {
+    if (n > 0 && c > 0) bulk_g2s(buf + so + h, src + h, 8u * (unsigned)c, sp.bar);
+  } else if (lane == 3) {
+    bulk_g2s(sp.mask, a.seg_mask + s * (kSeg / 32), 32u, sp.bar);
+  } else if (lane < 10) {
+    const bool tail = (lane - 4) & 1;
+    const int e = tail ? n - 1 : 0;
+    if (n > 0 && (tail ? h + c < n : h != 0)) cp_async8(buf + so + e, src + e);
+  } else if (lane == 10) {
+    bulk_g2s(sp.ec, ec + s * kEcStride, 8u * kEcStride, sp.bar);
+  }
+  cp_async_commit();
+}
+
+#ifndef FGT_K3N_MINB
+#define FGT_K3N_MINB 5
+#endif
+template <int DN>
+__global__ void __launch_bounds__(kThreads, FGT_K3N_MINB)
+    k3n_kernel(StreamArgs a, const double* __restrict__ ec, const CollConsts cc, OutArgs o) {
+  constexpr int NM = DN + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const K3nStage sp = k3n_stage(smem_raw + (size_t)warp * kK3nWarpBytes);
+  if (lane == 0) {
+    mbar_init(sp.bar);
+    sp.zero[0] = 0.0;
+  }
+  __syncwarp();
+  const WarpWalk walk{(int64_t)blockIdx.x * kSegWarps + warp, (int64_t)gridDim.x * kSegWarps,
+                      a.nseg};
+  const int64_t S1 = a.nseg;
+  // next narrow segment at or after s (S1 if none): issues its staging
+  auto issue_next = [&](int64_t s, SegGeom& g) -> int64_t {
+    for (; s < S1; s = walk.next(s)) {
+      if (k3_narrow(seg_deg_DM(__ldg(a.seg_deg + s)))) {
+        g = seg_geom(a, s);
+        k3n_issue(a, ec, s, g, sp, lane);
+        return s;
+      }
+    }
+    return S1;
+  };
+  unsigned parity = 0;
+  SegGeom g;
+  int64_t s = issue_next(walk.first(), g);
+  while (s < S1) {
+    const SegGeom gc = g;
+    const SegFrame f = seg_frame(gc);
+    const StageSlots so = stage_slots(a, gc);
+    cp_async_wait_all();
+    mbar_wait(sp.bar, parity);
+    parity ^= 1u;
+    __syncwarp();
+    if (gc.len < kSeg) {
+      // partial (last) segment: lanes past the end decode as strength-0
+      // sources at the centre (their mask bits are 0)
+      for (int q = lane; q < kSeg - gc.len + 8; q += 32) {
+        sp.xy[so.oy + gc.ny + q] = f.zc;
+        sp.bb[so.ob + gc.ny + q] = 0.0;
+      }
+      __syncwarp();
+    }
+    // ---- decode this lane's run
+    const uint32_t word = sp.mask[lane >> 2];
+    const unsigned byte = (word >> ((lane & 3) * 8)) & 0xffu;
+    const int nt = __popc(byte);
+    int incl = nt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const int i0 = incl - nt;
+    const int j0 = lane * kR - i0;
+    const double* px = sp.xy + so.ox + i0;
+    const double* py = sp.xy + so.oy + j0;
+    const double* pb = sp.bb + so.ob + j0;
+    double w[kR], b[kR];
+#pragma unroll
+    for (int e = 0; e < kR; ++e) {
+      const bool tg = (byte >> e) & 1u;
+      w[e] = *(tg ? px : py) - f.zc;
+      b[e] = *(tg ? sp.zero : pb);
+      px += tg ? 1 : 0;
+      py += tg ? 0 : 1;
+      pb += tg ? 0 : 1;
+    }
+    double ecq[NM];
+#pragma unroll
+    for (int q = 0; q < NM; ++q) ecq[q] = sp.ec[q];
+    __syncwarp();  // stage free: the next segment's copies go in now
+    SegGeom gn;
+    const int64_t sn = issue_next(walk.next(s), gn);
+    // ---- lane-run moments, warp scans -> exclusive prefix and totals
+    double pre[NM], E[NM];
+    {
+      double M[NM];
+#pragma unroll
+      for (int m = 0; m < NM; ++m) M[m] = 0.0;
+#pragma unroll
+      for (int e = 0; e < kR; ++e) {
+        double p = b[e];
+        M[0] += p;
+#pragma unroll
+        for (int m = 1; m < NM; ++m) {
+          p *= w[e];
+          M[m] += p;
+        }
+      }
+      double tot[NM];
+#pragma unroll
+      for (int m = 0; m < NM; ++m) {
+        double v = M[m];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const double t = __shfl_up_sync(0xffffffffu, v, d);
+          if (lane >= d) v += t;
+        }
+        tot[m] = __shfl_sync(0xffffffffu, v, 31);
+        pre[m] = v - M[m];
+      }
+#pragma unroll
+      for (int q = 0; q < NM; ++q) {
+        double acc = ecq[q];
+#pragma unroll
+        for (int m = 0; m + q < NM; ++m) acc = fma(cc.B[q][m], tot[m], acc);
+        E[q] = acc;
+      }
+    }
+    // ---- evaluate every element (targets keep theirs)
+    const int64_t base = o.u_offset + gc.ib;
+    // su slot of target i: i + off, off = u's 8-byte phase within 16 bytes,
+    // so that the bulk store's shared and global addresses share alignment
+    const int off = (int)((reinterpret_cast<uintptr_t>(o.u + base) >> 3) & 1);
+    if (lane == 0) bulk_wait_read();  // the previous segment's store has read su
+    __syncwarp();
+    {
+      int tk = i0 + off;
+#pragma unroll
+      for (int e = 0; e < kR; ++e) {
+        double p = b[e];  // 0 for targets: the prefix is exclusive for them
+        pre[0] += p;
+#pragma unroll
+        for (int m = 1; m < NM; ++m) {
+          p *= w[e];
+          pre[m] += p;
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int q = DN; q >= 0; --q) {
+          double c = E[q];
+#pragma unroll
+          for (int m = 0; m + q < NM; ++m)
+            if ((m + q) & 1) c = fma(cc.H[m][q], pre[m], c);
+          acc = q == DN ? c : fma(acc, w[e], c);
+        }
+        const bool tg = (byte >> e) & 1u;
+        if (tg) sp.su[tk] = acc;
+        tk += tg ? 1 : 0;
+      }
+    }
+    __syncwarp();
+    // ---- write back
+    if (o.tperm) {
+      const int32_t* tp = o.tperm + base;
+      for (int i = lane; i < gc.nx; i += 32) o.u[tp[i]] = sp.su[i + off];
+      __syncwarp();
+    } else if (gc.nx > 0) {
+      // interior [off, off + c) by one bulk store (16-byte aligned on both
+      // sides), a misaligned head / odd tail element by plain stores
+      double* up = o.u + base;
+      const int c = (gc.nx - off) & ~1;
+      if (lane == 0) {
+        fence_proxy_async();  // the generic stores to su before the async read
+        if (c > 0) bulk_s2g(up + off, sp.su + 2 * off, 8u * (unsigned)c);
+      }
+      if (lane == 1 && off) up[0] = sp.su[1];
+      if (lane == 2 && off + c < gc.nx) up[gc.nx - 1] = sp.su[gc.nx - 1 + off];
+    }
+    s = sn;
+    g = gn;
+  }
+  if (lane == 0) bulk_wait_all();
+}
+
+// Collapsed carries of the narrow segments (after K2): per segment, the
+// segment carries at the frame centre Tf_k = e^{-s_k h0} Cf_k, Tb_k =
+// e^{-s_k h1} Cb_k folded into E^c_q = Re sum_k mw_k c_kq (Tf_k + (-1)^q Tb_k),
+// q <= DN (collapsed_segment's carry part, done once per segment here
+// instead of on a few lanes of every K3 warp).
+__global__ void collapse_carries_kernel(StreamArgs a, const ModeTable* __restrict__ mt,
+                                        int ne, TileState ts, int DN) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= a.nseg) return;
+  if (!k3_narrow(seg_deg_DM(__ldg(a.seg_deg + s)))) return;
+  const SegFrame f = seg_frame(seg_geom(a, s));
+  double E[kCollMax + 1];
+#pragma unroll
+  for (int q = 0; q <= kCollMax; ++q) E[q] = 0.0;
+  for (int k = 0; k < ne; ++k) {
+    const cplx* c = mt->coef[k];
+    // e^{-s h} by the degree-DN Taylor polynomial (|s h| <= rmax[DN] / 2)
+    cplx e0 = c[DN], e1 = c[DN];
+    for (int n = DN - 1; n >= 0; --n) {
+      const cplx cn = c[n];
+      e0 = {fma(e0.re, f.h0, cn.re), fma(e0.im, f.h0, cn.im)};
+      e1 = {fma(e1.re, f.h1, cn.re), fma(e1.im, f.h1, cn.im)};
+    }
+    const int64_t idx = (int64_t)k * a.nseg + s;
+    const cplx tf = cmul(e0, ts.Cf[idx]);
+    const cplx tb = cmul(e1, ts.Cb[idx]);
+#pragma unroll
+    for (int q = 0; q <= kCollMax; ++q) {
+      if (q <= DN) {
+        const cplx x = mt->mwc[k][q];
+        const double sg = (q & 1) ? -1.0 : 1.0;
+        E[q] = fma(x.re, fma(sg, tb.re, tf.re), fma(-x.im, fma(sg, tb.im, tf.im), E[q]));
+      }
+    }
+  }
+  double* out = ts.ec + s * kEcStride;
+#pragma unroll
+  for (int q = 0; q <= kCollMax; ++q) out[q] = q <= DN ? E[q] : 0.0;
+#pragma unroll
+  for (int q = kCollMax + 1; q < kEcStride; ++q) out[q] = 0.0;
+}
+
 // ------------------------------------------------------------------- K0
 
 __global__ void partition_kernel(const double* __restrict__ xs, int64_t M,
@@ -1765,6 +2085,45 @@ __device__ __forceinline__ int merge_path_smem(const double* x, int nx, const do
   return lo;
 }
 
+// Index-order checks of one staged set s[0..n) (16-byte aligned pairs from
+// s + head, see stage_plan): non-finite values and, when check_sorted, an
+// element below its predecessor (prev = the element before s[0], -inf if
+// none).  Pairs by 16-byte shared loads (conflict-free); the predecessor of
+// a pair comes from the neighbouring thread.
+__device__ __forceinline__ void check_staged(const double* sv, int n, int head, double prev,
+                                             int check_sorted, int t, int& fin, int& ord) {
+  if (n <= 0) return;
+  // element 0 when it is the unaligned head, then pairs (head + 2k, +1)
+  if (head && t == 0) {
+    fin |= !isfinite(sv[0]);
+    if (check_sorted) ord |= prev > sv[0];
+  }
+  const int npair = (n - head) >> 1;
+  const int lane = t & 31;
+  for (int k0 = 0; k0 < npair; k0 += blockDim.x) {  // block-uniform trip count
+    const int k = k0 + t;
+    const bool have = k < npair;
+    double2 v = make_double2(0.0, 0.0);
+    if (have) v = *reinterpret_cast<const double2*>(sv + head + 2 * k);
+    // predecessor: the previous thread's second element (lane 0: a load)
+    double pv = __shfl_up_sync(0xffffffffu, v.y, 1);
+    if (lane == 0 && have) {
+      const int i = head + 2 * k;
+      pv = i > 0 ? sv[i - 1] : prev;
+    }
+    if (have) {
+      fin |= !isfinite(v.x) | !isfinite(v.y);
+      if (check_sorted) ord |= (pv > v.x) | (v.x > v.y);
+    }
+  }
+  // odd tail element
+  if (((n - head) & 1) && t == 0) {
+    const double v = sv[n - 1];
+    fin |= !isfinite(v);
+    if (check_sorted) ord |= (n >= 2 ? sv[n - 2] : prev) > v;
+  }
+}
+
 template <bool BATCH>
 __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorted,
                                                int64_t nseg, int64_t* __restrict__ seg_ib,
@@ -1772,13 +2131,10 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
                                                int4* __restrict__ seg_info,
                                                double2* __restrict__ seg_z,
                                                uint32_t* __restrict__ seg_mask,
-                                               double2* __restrict__ seg_gap,
                                                int* __restrict__ flags) {
   extern __shared__ __align__(16) double tsm[];
   __shared__ int sib[kPlanSegs + 1];
   __shared__ uint32_t smask[kPlanWords];
-  __shared__ unsigned long long sgap[kPlanSegs];  // largest inner gap (bits of a double >= 0)
-  __shared__ double szf[kPlanSegs];               // first coordinate of each segment
   __shared__ int sflags;
   __shared__ __align__(8) uint64_t bar;
   const int64_t ib = c.ib, ie = c.ie;
@@ -1805,7 +2161,6 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
     mbar_init(&bar);
   }
   for (int w = t; w < kPlanWords; w += kPlanThreads) smask[w] = 0u;
-  if (t < kPlanSegs) sgap[t] = 0ull;
   __syncthreads();
   if (t == 0) {
     const unsigned bx = 8u * (unsigned)(stx.i1 - stx.i0), by = 8u * (unsigned)(sty.i1 - sty.i0);
@@ -1825,16 +2180,8 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
   mbar_wait(&bar, 0);
   __syncthreads();
   int f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0;
-  for (int i = t; i < nx; i += kPlanThreads) {
-    const double v = sx[i];
-    f0 |= !isfinite(v);
-    if (check_sorted) f3 |= (i > 0 ? sx[i - 1] : xprev) > v;
-  }
-  for (int j = t; j < ny; j += kPlanThreads) {
-    const double v = sy[j];
-    f1 |= !isfinite(v);
-    if (check_sorted) f4 |= (j > 0 ? sy[j - 1] : yprev) > v;
-  }
+  check_staged(sx, nx, stx.head, xprev, check_sorted, t, f0, f3);
+  check_staged(sy, ny, sty.head, yprev, check_sorted, t, f1, f4);
   // same-points needs x[i] == y[i] for every i; skip once any tile has seen
   // a mismatch (distinct point sets), otherwise compare against the staged
   // sources where the index ranges overlap (they do when x == y)
@@ -1852,10 +2199,8 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
   if (t < nsegs_tile) sib[t] = merge_path_smem(sx, nx, sy, ny, t * kSeg);
   if (t == 0) sib[nsegs_tile] = nx;
   __syncthreads();
-  // merge: thread t owns merged positions [kPlanPer t, kPlanPer (t + 1)); it
-  // sets their mask bits (1 = target) and tracks the largest gap between
-  // consecutive elements per segment (the gap into a segment's first
-  // element is left to classify_kernel, which knows zprev)
+  // merge: thread t owns merged positions [kPlanPer t, kPlanPer (t + 1)) and
+  // sets their mask bits (1 = target)
   const int d0 = t * kPlanPer;
   if (d0 < len) {
     const int k = d0 / kSeg, D0 = k * kSeg;
@@ -1881,47 +2226,30 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
     // run up to kPlanPer past it, into the buffer's padding
     double cx = sx[i];
     double cy = sy[j];
-    double zp = fmax(i > 0 ? sx[i - 1] : -INFINITY, j > 0 ? sy[j - 1] : -INFINITY);
-    const int kb = D0 + kSeg;  // first position of the next segment
     unsigned bits = 0u;
-    double ga = 0.0, gb = 0.0;
+    const int nwin = len - d0 < kPlanPer ? len - d0 : kPlanPer;
 #pragma unroll
     for (int e = 0; e < kPlanPer; ++e) {
-      const int p = d0 + e;
-      if (p < len) {
-        const bool tgt = !(cy <= cx);  // sources first on ties
-        const double z = tgt ? cx : cy;
-        if (p == D0 || p == kb) {
-          szf[p / kSeg] = z;  // tile-local segment index
-        } else if (p < kb) {
-          ga = fmax(ga, z - zp);
-        } else {
-          gb = fmax(gb, z - zp);
-        }
-        zp = z;
-        bits |= (unsigned)tgt << e;
-        if (tgt) {
-          ++i;
-          cx = sx[i];
-        } else {
-          ++j;
-          cy = sy[j];
-        }
+      const bool tgt = !(cy <= cx);  // sources first on ties
+      bits |= (unsigned)tgt << e;
+      if (tgt) {
+        ++i;
+        cx = sx[i];
+      } else {
+        ++j;
+        cy = sy[j];
       }
     }
+    bits &= (nwin >= 32 ? 0xffffffffu : ((1u << nwin) - 1u));
     const int sh = d0 & 31;
     atomicOr(&smask[d0 >> 5], bits << sh);
     if (sh + kPlanPer > 32) atomicOr(&smask[(d0 >> 5) + 1], bits >> (32 - sh));
-    atomicMax(&sgap[k], (unsigned long long)__double_as_longlong(ga));
-    if (d0 + kPlanPer > kb && k + 1 < kPlanSegs)
-      atomicMax(&sgap[k + 1], (unsigned long long)__double_as_longlong(gb));
   }
   __syncthreads();
   for (int w = t; w < nsegs_tile * (kSeg / 32); w += kPlanThreads)
     seg_mask[c.seg0 * (kSeg / 32) + w] = smask[w];
   if (t < nsegs_tile) {
     const int k = t;
-    seg_gap[c.seg0 + k] = make_double2(__longlong_as_double((long long)sgap[k]), szf[k]);
     const int i0 = sib[k], i1 = sib[k + 1];
     const int sd0 = k * kSeg;
     const int sd1 = (sd0 + kSeg < len) ? sd0 + kSeg : len;
@@ -1960,8 +2288,7 @@ __global__ void __launch_bounds__(kPlanThreads, FGT_PLAN_MINB)
     plan_tile_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
                      int64_t N, const int64_t* __restrict__ tile_ib, int64_t nseg,
                      int check_sorted, int64_t* __restrict__ seg_ib, double2* __restrict__ seg_z,
-                     uint32_t* __restrict__ seg_mask, double2* __restrict__ seg_gap,
-                     int* __restrict__ flags) {
+                     uint32_t* __restrict__ seg_mask, int* __restrict__ flags) {
   const int64_t t = blockIdx.x;
   const int64_t L = M + N;
   TileCtx c;
@@ -1976,8 +2303,7 @@ __global__ void __launch_bounds__(kPlanThreads, FGT_PLAN_MINB)
   c.seg0 = t * kPlanSegs;
   c.xoff = c.yoff = 0;
   c.tid = 0;
-  plan_tile_body<false>(c, check_sorted, nseg, seg_ib, nullptr, nullptr, seg_z, seg_mask, seg_gap,
-                        flags);
+  plan_tile_body<false>(c, check_sorted, nseg, seg_ib, nullptr, nullptr, seg_z, seg_mask, flags);
 }
 
 struct BatchArgs {
@@ -2023,10 +2349,9 @@ __global__ void __launch_bounds__(kPlanThreads, FGT_PLAN_MINB)
     batch_plan_tile_kernel(BatchArgs b, const int64_t* __restrict__ tile_ib,
                            int64_t* __restrict__ seg_ib, int64_t* __restrict__ seg_jb,
                            int4* __restrict__ seg_info, double2* __restrict__ seg_z,
-                           uint32_t* __restrict__ seg_mask, double2* __restrict__ seg_gap,
-                           int* __restrict__ flags) {
+                           uint32_t* __restrict__ seg_mask, int* __restrict__ flags) {
   const TileCtx c = batch_ctx(b, blockIdx.x, tile_ib);
-  plan_tile_body<true>(c, 1, 0, seg_ib, seg_jb, seg_info, seg_z, seg_mask, seg_gap, flags);
+  plan_tile_body<true>(c, 1, 0, seg_ib, seg_jb, seg_info, seg_z, seg_mask, flags);
 }
 
 // Element-wise checks of the input as given (no partition involved):
@@ -2289,12 +2614,36 @@ int64_t scan_blocks(int64_t nseg) { return (nseg + kScanBlock - 1) / kScanBlock;
 
 size_t tile_state_elems(int64_t nseg, int ne) {
   const size_t nt = (size_t)nseg * (size_t)ne;
-  return 5 * nt + (size_t)scan_blocks(nseg) * 2 * (size_t)ne * 3 + 8;
+  const size_t blk = (size_t)scan_blocks(nseg) * 2 * (size_t)ne * 3 + 8;
+  return 5 * nt + blk + (size_t)nseg * (kEcStride / 2) + 4;
 }
 
 TileState tile_state_carve(cplx* base, int64_t nseg, int ne) {
   const size_t nt = (size_t)nseg * (size_t)ne;
-  return TileState{base, base + nt, base + 2 * nt, base + 3 * nt, base + 4 * nt, base + 5 * nt};
+  const size_t blk = (size_t)scan_blocks(nseg) * 2 * (size_t)ne * 3 + 8;
+  // collapsed carries: 64-byte aligned rows (one bulk copy per segment)
+  uintptr_t ecp = reinterpret_cast<uintptr_t>(base + 5 * nt + blk);
+  ecp = (ecp + 63) & ~(uintptr_t)63;
+  return TileState{base,           base + nt,      base + 2 * nt,
+                   base + 3 * nt,  base + 4 * nt,  base + 5 * nt,
+                   reinterpret_cast<double*>(ecp)};
+}
+
+CollConsts coll_consts(const double* g) {
+  CollConsts c{};
+  auto binom = [](int n, int m) {
+    double r = 1.0;
+    for (int i = 1; i <= m; ++i) r = r * (n - m + i) / i;
+    return r;
+  };
+  for (int m = 0; m <= kCollMax; ++m)
+    for (int q = 0; q <= kCollMax; ++q) {
+      const int n = m + q;
+      if (n > kCollMax) continue;
+      if (n & 1) c.H[m][q] = ((m & 1) ? -2.0 : 2.0) * binom(n, m) * g[n];
+      c.B[q][m] = ((q & 1) ? -1.0 : 1.0) * binom(n, m) * g[n];
+    }
+  return c;
 }
 
 size_t seg_smem_bytes(int ne, bool batched, bool stream, bool lane_carries) {
@@ -2315,7 +2664,7 @@ cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int6
 cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int64_t N,
                               const int64_t* tile_ib, int64_t ntiles, int64_t nseg,
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
-                              uint32_t* seg_mask, double2* seg_gap, int* flags, cudaStream_t st) {
+                              uint32_t* seg_mask, int* flags, cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
   // both sets, heads, sentinels + padding for merge overruns on unsorted input
   const size_t smem = sizeof(double) * (kPlanTile + 8 + 2 * kPlanPer);
@@ -2324,7 +2673,7 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
   if (e != cudaSuccess) return e;
   note_launch();
   plan_tile_kernel<<<(unsigned)ntiles, kPlanThreads, smem, st>>>(xs, M, ys, N, tile_ib, nseg, check_sorted,
-                                                         seg_ib, seg_z, seg_mask, seg_gap, flags);
+                                                         seg_ib, seg_z, seg_mask, flags);
   return cudaGetLastError();
 }
 
@@ -2345,7 +2694,7 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
                               const int64_t* tile_base, const int32_t* tile_tid, int B,
                               int64_t ntiles, int64_t* tile_ib, int64_t* seg_ib, int64_t* seg_jb,
                               int4* seg_info, double2* seg_z, uint32_t* seg_mask,
-                              double2* seg_gap, int* flags, cudaStream_t st) {
+                              int* flags, cudaStream_t st) {
   (void)B;
   if (ntiles == 0) return cudaSuccess;
   const BatchArgs b{xs, ys, t_off, s_off, seg_base, tile_base, tile_tid};
@@ -2357,7 +2706,7 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
   cudaError_t e = ensure_dynamic_smem(batch_plan_tile_kernel, (int)smem, done);
   if (e != cudaSuccess) return e;
   batch_plan_tile_kernel<<<(unsigned)ntiles, kPlanThreads, smem, st>>>(b, tile_ib, seg_ib, seg_jb, seg_info,
-                                                              seg_z, seg_mask, seg_gap, flags);
+                                                              seg_z, seg_mask, flags);
   return cudaGetLastError();
 }
 
@@ -2400,14 +2749,14 @@ cudaError_t launch_batch_modes(const BatchModeBase& base, const double* deltas, 
 }
 
 cudaError_t launch_classify(const StreamArgs& a, const ModeParams& P, double smax,
-                            const double2* seg_gap, int* seg_deg, const int* skip_flags,
+                            int* seg_deg, const int* skip_flags,
                             unsigned long long* counts, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), st);
+  cudaError_t e = cudaMemsetAsync(counts, 0, 3 * sizeof(unsigned long long), st);
   if (e != cudaSuccess || a.nseg == 0) return e;
   const int64_t want = (a.nseg + 255) / 256;
   const int64_t cap = (int64_t)num_sms() * 8;
   note_launch();
-  classify_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(a, P, smax, seg_gap, seg_deg,
+  classify_kernel<<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(a, P, smax, seg_deg,
                                                                        skip_flags, counts);
   return cudaGetLastError();
 }
@@ -2481,9 +2830,46 @@ cudaError_t launch_chunk_carries(const cplx* aggs, int n_chunks, int ne, int ran
   return cudaGetLastError();
 }
 
+template <int DN>
+static cudaError_t launch_k3n_dn(const StreamArgs& a, const TileState& ts, const CollConsts& cc,
+                                 OutArgs o, cudaStream_t st) {
+  static std::atomic<unsigned long long> done{0};
+  const size_t smem = (size_t)kSegWarps * kK3nWarpBytes;
+  cudaError_t e = ensure_dynamic_smem(k3n_kernel<DN>, (int)smem, done);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3n_kernel<DN>, kThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t want = (a.nseg + kSegWarps - 1) / kSegWarps;
+  const int64_t cap = (int64_t)num_sms() * per_sm * FGT_K3N_WAVES;
+  note_launch();
+  k3n_kernel<DN><<<(unsigned)(want < cap ? want : cap), kThreads, smem, st>>>(a, ts.ec, cc, o);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
-                        TileState ts, OutArgs o, cudaStream_t st) {
-  return launch_seg_main<false>(a, P, mt, ts, o, st);
+                        TileState ts, OutArgs o, cudaStream_t st, const CollConsts* cc) {
+  if (!cc || a.mtb || a.nseg == 0) return launch_seg_main<false>(a, P, mt, ts, o, st);
+  // single plan: wide segments on the per-segment kernel, narrow ones on the
+  // collapsed kernel at the plan's highest narrow degree
+  if (a.nwide3 != 0) {
+    cudaError_t e = launch_seg_main_variant<false, true>(a, P, mt, ts, o, st);
+    if (e != cudaSuccess) return e;
+  }
+  if (a.nwide3 == a.nseg) return cudaSuccess;
+  const int DN = a.dn_narrow >= 0 ? (a.dn_narrow < kCollMax ? a.dn_narrow : kCollMax) : kCollMax;
+  note_launch();
+  collapse_carries_kernel<<<(unsigned)((a.nseg + 255) / 256), 256, 0, st>>>(a, mt, P.ne, ts, DN);
+  switch (DN) {
+    case 0: return launch_k3n_dn<0>(a, ts, *cc, o, st);
+    case 1: return launch_k3n_dn<1>(a, ts, *cc, o, st);
+    case 2: return launch_k3n_dn<2>(a, ts, *cc, o, st);
+    case 3: return launch_k3n_dn<3>(a, ts, *cc, o, st);
+    case 4: return launch_k3n_dn<4>(a, ts, *cc, o, st);
+    case 5: return launch_k3n_dn<5>(a, ts, *cc, o, st);
+    default: return launch_k3n_dn<6>(a, ts, *cc, o, st);
+  }
 }
 
 cudaError_t launch_mode_sums(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,

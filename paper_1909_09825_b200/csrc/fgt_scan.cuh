@@ -47,6 +47,20 @@ struct ModeTable {
 // tables are staged ahead of 16-byte aligned stages in shared memory
 static_assert(sizeof(ModeTable) % 16 == 0, "ModeTable size must be a multiple of 16 bytes");
 
+// Constants of the collapsed narrow K3 (k3n), derived from the collapsed
+// polynomial G(t) = sum_n g_n t^n of a plan (ModeTable::gpoly):
+//   H[m][q] = 2 (-1)^m C(m+q, m) g_{m+q}   (m + q odd)  prefix-moment terms
+//   B[q][m] = (-1)^q C(m+q, m) g_{m+q}                  total-moment terms
+// (fgt_scan.cu, collapsed form).  Passed as a kernel parameter: the FMAs read
+// them from the constant bank.
+constexpr int kCollMax = 6;   // highest collapsed degree of the narrow K3
+constexpr int kEcStride = 8;  // doubles per segment of the collapsed carries
+struct CollConsts {
+  double H[kCollMax + 1][kCollMax + 1];
+  double B[kCollMax + 1][kCollMax + 1];
+};
+CollConsts coll_consts(const double* gpoly);
+
 struct StreamArgs {
   const double* xs;  // sorted targets (this chunk)
   int64_t M;
@@ -75,6 +89,9 @@ struct StreamArgs {
   // classify_kernel only: segment 0's zprev is its own first element (a
   // plan without a predecessor, classified before zprev0 is known on the host)
   bool zprev0_first = false;
+  // plan-time highest collapsed degree DN over the narrow segments (-1:
+  // unknown -> the narrow K3 runs at kCollMax)
+  int dn_narrow = -1;
 };
 
 struct OutArgs {
@@ -93,6 +110,7 @@ struct TileState {
   cplx* Cf;
   cplx* Cb;
   cplx* blk;  // scan workspace: scan_blocks(nseg) * 2 * ne * 3 complex
+  double* ec;  // collapsed carries of the narrow segments, [nseg][kEcStride]
 };
 
 int64_t scan_blocks(int64_t nseg);
@@ -108,11 +126,10 @@ cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int6
 // x non-finite, y non-finite, x != y when M == N, x unsorted, y unsorted;
 // zeroed by the caller) and segment metadata seg_ib / seg_z / seg_mask.
 // tile_ib: launch_partition output at kPlanTile granularity.
-// seg_gap: per segment (largest gap between its elements, its first coordinate).
 cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int64_t N,
                               const int64_t* tile_ib, int64_t ntiles, int64_t nseg,
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
-                              uint32_t* seg_mask, double2* seg_gap, int* flags, cudaStream_t st);
+                              uint32_t* seg_mask, int* flags, cudaStream_t st);
 // Element-wise checks of unsorted input (flags[0..4] as launch_plan_tiles,
 // zeroed by the caller) over the arrays as given.
 cudaError_t launch_check_points(const double* xs, int64_t M, const double* ys, int64_t N,
@@ -128,7 +145,7 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
                               const int64_t* tile_base, const int32_t* tile_tid, int B,
                               int64_t ntiles, int64_t* tile_ib, int64_t* seg_ib, int64_t* seg_jb,
                               int4* seg_info, double2* seg_z, uint32_t* seg_mask,
-                              double2* seg_gap, int* flags, cudaStream_t st);
+                              int* flags, cudaStream_t st);
 // Per-transform mode tables of a batched plan, built on the device:
 // s_k = t_k / sqrt(delta_b), mw_k, Taylor coefficients of exp(-s g)
 // (c_0 = 1 and c_1 = -s exact), smax.  deltas: device array of B.
@@ -143,11 +160,12 @@ cudaError_t launch_store_table(const ModeTable& T, ModeTable* out, cudaStream_t 
 cudaError_t launch_batch_modes(const BatchModeBase& base, const double* deltas, int B,
                                ModeTable* out, cudaStream_t st);
 // Plan-time classification: counts[0] / counts[1] = segments that K1 / K3
-// process on their wide (per-element) path.  smax: the single plan's
+// process on their wide (per-element) path, counts[2] = the highest
+// collapsed degree DN among the K3-narrow segments.  smax: the single plan's
 // max |s_k| (batched plans read their tables).
 // Also writes seg_deg (see StreamArgs) from seg_gap and the segment frames.
 cudaError_t launch_classify(const StreamArgs& a, const ModeParams& P, double smax,
-                            const double2* seg_gap, int* seg_deg, const int* skip_flags,
+                            int* seg_deg, const int* skip_flags,
                             unsigned long long* counts, cudaStream_t st);
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, cudaStream_t st);
@@ -164,8 +182,10 @@ cudaError_t launch_carry_scan(const TileState& ts, int64_t nseg, int ne, const c
 // algebra of fgt_chunk_carries, one thread per mode).
 cudaError_t launch_chunk_carries(const cplx* aggs, int n_chunks, int ne, int rank, cplx* out,
                                  cudaStream_t st);
+// K3.  cc: the plan's collapsed-form constants (single plans); nullptr runs
+// the per-segment-degree narrow kernel (batched plans, per-transform tables).
 cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
-                        TileState ts, OutArgs o, cudaStream_t st);
+                        TileState ts, OutArgs o, cudaStream_t st, const CollConsts* cc = nullptr);
 cudaError_t launch_mode_sums(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, OutArgs o, cudaStream_t st);
 cudaError_t launch_gather(const double* alpha, const int32_t* perm, int64_t n, double* out,
