@@ -443,9 +443,14 @@ StreamArgs stream_args(const fgt_plan_s* p, const double* bs) {
 
 // Queue the segment classification; the counts land in h[0..1] once the
 // stream is synchronized (see take_classes).
+// xd / yd: the arrays the segments were cut from (the plan's own sorted
+// arrays when null).
 void queue_classify(fgt_plan_s* p, unsigned long long* h, cudaStream_t st,
-                    bool check_flags = false, bool zprev0_first = false) {
+                    bool check_flags = false, bool zprev0_first = false,
+                    const double* xd = nullptr, const double* yd = nullptr) {
   StreamArgs sa = stream_args(p, nullptr);
+  if (xd) sa.xs = xd;
+  if (yd) sa.ys = yd;
   sa.zprev0_first = zprev0_first;
   ck(launch_classify(sa, p->P, p->P.smax, p->d_seg_deg,
                      check_flags ? p->d_flag : nullptr, class_counts(p), st),
@@ -1232,7 +1237,7 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
       unsigned long long* hc = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hcl;
       xy0[0] = xy0[1] = 0.0;
       if (has_prev) p->zprev0 = z_prev;
-      queue_classify(p, hc, st, false, !has_prev);
+      queue_classify(p, hc, st, false, !has_prev, xs.dptr, ys.dptr);
       ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(int) * 8, cudaMemcpyDeviceToHost, st), "flags");
       if (M > 0) ck(cudaMemcpyAsync(xy0, xs.dptr, 8, cudaMemcpyDeviceToHost, st), "x0");
       if (N > 0) ck(cudaMemcpyAsync(xy0 + 1, ys.dptr, 8, cudaMemcpyDeviceToHost, st), "y0");

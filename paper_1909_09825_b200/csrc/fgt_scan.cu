@@ -1718,28 +1718,102 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
 // No per-mode work and no branches on the element loop.
 constexpr int kK3nStageXY = kSeg + 16;
 constexpr int kK3nStageB = kSeg + 12;
-struct K3nStage {
+constexpr int kK3nSu = kSeg + 4;  // staged potentials + a discard slot for non-targets
+// One TMA stage (double-buffered per warp): a segment's x / y (xy), b, merge
+// mask words, collapsed carries and the stage's mbarrier.
+struct K3nBuf {
   double* xy;      // [kK3nStageXY]  x at slot ox, y at slot oy
   double* bb;      // [kK3nStageB]   b at slot ob
-  double* su;      // [kSeg + 2]     staged potentials
   double* ec;      // [kEcStride]    collapsed carries
   uint32_t* mask;  // [kSeg / 32]
-  double* zero;    // one 0.0 (the strength slot of every target)
   uint64_t* bar;
 };
+constexpr size_t kK3nBufBytes =
+    sizeof(double) * (kK3nStageXY + kK3nStageB + kEcStride) + 4 * (kSeg / 32) + 16;
+static_assert(kK3nBufBytes % 16 == 0, "k3n stage alignment");
+struct K3nStage {
+  double* su;      // [kK3nSu]       staged potentials (slot kSeg + 2: discard)
+  double* scan;    // [kCollMax + 1][32] lane moments -> exclusive lane prefixes
+  double* tot;     // [kCollMax + 1 (+1)] segment totals
+  double* zero;    // one 0.0 (the strength slot of every target)
+};
 constexpr size_t kK3nWarpBytes =
-    sizeof(double) * (kK3nStageXY + kK3nStageB + (kSeg + 2) + kEcStride + 2) + 4 * (kSeg / 32) + 16;
+    2 * kK3nBufBytes + sizeof(double) * (kK3nSu + 32 * (kCollMax + 1) + (kCollMax + 1 + 1) + 2);
 static_assert(kK3nWarpBytes % 16 == 0, "k3n stage alignment");
-__device__ __forceinline__ K3nStage k3n_stage(unsigned char* base) {
-  K3nStage p;
+__device__ __forceinline__ K3nBuf k3n_buf(unsigned char* base) {
+  K3nBuf p;
   p.xy = reinterpret_cast<double*>(base);
   p.bb = p.xy + kK3nStageXY;
-  p.su = p.bb + kK3nStageB;
-  p.ec = p.su + kSeg + 2;
-  p.zero = p.ec + kEcStride;
-  p.mask = reinterpret_cast<uint32_t*>(p.zero + 2);
+  p.ec = p.bb + kK3nStageB;
+  p.mask = reinterpret_cast<uint32_t*>(p.ec + kEcStride);
   p.bar = reinterpret_cast<uint64_t*>(p.mask + kSeg / 32);
   return p;
+}
+__device__ __forceinline__ K3nStage k3n_stage(unsigned char* base) {
+  K3nStage p;
+  p.su = reinterpret_cast<double*>(base + 2 * kK3nBufBytes);
+  p.scan = p.su + kK3nSu;
+  p.tot = p.scan + 32 * (kCollMax + 1);
+  p.zero = p.tot + (kCollMax + 1 + 1);
+  return p;
+}
+
+// Exclusive warp prefix and total of NM per-lane values through shared
+// memory: lane q < 4 NM takes moment q / 4 over lanes 8 (q % 4) .. + 7 (a
+// sequential prefix of 8), then the 4 group sums of a moment are scanned by
+// two shuffles.  ~40 warp instructions for NM = 4 against ~180 for NM
+// Kogge-Stone shuffle scans of doubles.
+template <int NM>
+__device__ __forceinline__ void warp_moment_scan(const K3nStage& sp, int lane, const double (&M)[NM],
+                                                 double (&pre)[NM], double (&tot)[NM]) {
+  static_assert(NM <= 8, "moment scan width");
+#pragma unroll
+  for (int m = 0; m < NM; ++m) sp.scan[m * 32 + lane] = M[m];
+  __syncwarp();
+  constexpr unsigned kAct = NM * 4 >= 32 ? 0xffffffffu : ((1u << (NM * 4)) - 1u);
+  if (lane < NM * 4) {
+    const int m = lane >> 2, g = lane & 3;
+    double2* row = reinterpret_cast<double2*>(sp.scan + m * 32 + g * 8);
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double2 t = row[i];
+      v[2 * i] = t.x;
+      v[2 * i + 1] = t.y;
+    }
+    double run = 0.0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double t = v[i];
+      v[i] = run;
+      run += t;
+    }
+    double incl = run;
+#pragma unroll
+    for (int d = 1; d < 4; d <<= 1) {
+      const double t = __shfl_up_sync(kAct, incl, d, 4);
+      if (g >= d) incl += t;
+    }
+    const double excl = incl - run;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) row[i] = make_double2(v[2 * i] + excl, v[2 * i + 1] + excl);
+    if (g == 3) sp.tot[m] = incl;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int m = 0; m < NM; ++m) {
+    pre[m] = sp.scan[m * 32 + lane];
+    tot[m] = sp.tot[m];
+  }
+}
+
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts_f64(unsigned addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(addr), "d"(v));
 }
 
 __device__ __forceinline__ void bulk_s2g(double* dst, const double* src, unsigned bytes) {
@@ -1758,38 +1832,62 @@ __device__ __forceinline__ void bulk_wait_all() {
 // Lanes 0..2 bulk-copy the 16-byte aligned interiors of x / y / b, lane 3 the
 // mask words, lane 10 the collapsed carries, lanes 4..9 the unaligned head /
 // tail elements by 8-byte cp.async.
+// Stage slots of a segment in a K3nBuf: its targets at xy[xo ..), sources at
+// xy[yo ..), strengths at bb[bo ..).  Each set is copied as the 16-byte
+// blocks that enclose it (at most one extra element at either end, read
+// from the same 16-byte block as a valid element), so one bulk copy per
+// set and no unaligned head / tail copies.
+struct K3nSlots {
+  int xo, yo, bo;
+};
+__device__ __forceinline__ int phase8(const double* p) {
+  return (int)((reinterpret_cast<uintptr_t>(p) >> 3) & 1);
+}
+__device__ __forceinline__ K3nSlots k3n_slots(const StreamArgs& a, const SegGeom& g) {
+  K3nSlots o;
+  const int hx = phase8(a.xs + g.ib);
+  o.xo = hx;
+  const int ys = (hx + g.nx + 1) & ~1;  // 16-byte aligned start of the y blocks
+  o.yo = ys + phase8(a.ys + g.jb);
+  o.bo = phase8(a.bs + g.jb);
+  return o;
+}
+// Issue of one segment's stage by one lane: 3 enclosing-block copies (x, y,
+// b), the merge-mask words and the collapsed carries, on the buffer's
+// mbarrier.
 __device__ __forceinline__ void k3n_issue(const StreamArgs& a, const double* ec, int64_t s,
-                                          const SegGeom& g, const K3nStage& sp, int lane) {
-  const StageSlots o = stage_slots(a, g);
-  if (lane == 0) {
-    fence_proxy_async();  // earlier generic reads of the stage before async writes
-    mbar_expect(sp.bar, stage_bulk_bytes(o, g) + 32u + 8u * kEcStride);
-  }
-  __syncwarp();
-  const int arr = lane < 3 ? lane : ((lane - 4) >> 1);  // 0 x, 1 y, 2 b (lanes < 10)
-  const double* src = arr == 0 ? a.xs + g.ib : (arr == 1 ? a.ys + g.jb : a.bs + g.jb);
-  const int n = arr == 0 ? g.nx : g.ny;
-  const int so = arr == 0 ? o.ox : (arr == 1 ? o.oy : o.ob);
-  double* buf = arr == 2 ? sp.bb : sp.xy;
-  const int h = so & 1;
-  int c = (n - h) & ~1;
-  if (c < 0) c = 0;
-  if (lane < 3) {
-    if (n > 0 && c > 0) bulk_g2s(buf + so + h, src + h, 8u * (unsigned)c, sp.bar);
-  } else if (lane == 3) {
-    bulk_g2s(sp.mask, a.seg_mask + s * (kSeg / 32), 32u, sp.bar);
-  } else if (lane < 10) {
-    const bool tail = (lane - 4) & 1;
-    const int e = tail ? n - 1 : 0;
-    if (n > 0 && (tail ? h + c < n : h != 0)) cp_async8(buf + so + e, src + e);
-  } else if (lane == 10) {
-    bulk_g2s(sp.ec, ec + s * kEcStride, 8u * kEcStride, sp.bar);
-  }
-  cp_async_commit();
+                                          const SegGeom& g, const K3nBuf& sp, int lane) {
+  if (lane != 0) return;
+  auto blocks = [](const double* p, int n, const double*& src) -> unsigned {
+    const uintptr_t b0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+    const uintptr_t b1 = (reinterpret_cast<uintptr_t>(p + n) + 15) & ~(uintptr_t)15;
+    src = reinterpret_cast<const double*>(b0);
+    return n > 0 ? (unsigned)(b1 - b0) : 0u;
+  };
+  const double *sx, *sy, *sb;
+  const unsigned bx = blocks(a.xs + g.ib, g.nx, sx);
+  const unsigned by = blocks(a.ys + g.jb, g.ny, sy);
+  const unsigned bb = blocks(a.bs + g.jb, g.ny, sb);
+  const int ys = (phase8(a.xs + g.ib) + g.nx + 1) & ~1;
+  fence_proxy_async();  // earlier generic reads of the buffer before async writes
+  mbar_expect(sp.bar, bx + by + bb + 32u + 8u * kEcStride);
+  if (bx) bulk_g2s(sp.xy, sx, bx, sp.bar);
+  if (by) bulk_g2s(sp.xy + ys, sy, by, sp.bar);
+  if (bb) bulk_g2s(sp.bb, sb, bb, sp.bar);
+  bulk_g2s(sp.mask, a.seg_mask + s * (kSeg / 32), 32u, sp.bar);
+  bulk_g2s(sp.ec, ec + s * kEcStride, 8u * kEcStride, sp.bar);
+}
+
+// An opaque copy of a value: keeps a kernel-parameter constant in a register
+// for the whole kernel instead of re-reading the constant bank at each use.
+__device__ __forceinline__ double in_reg(double v) {
+  double r;
+  asm volatile("mov.b64 %0, %1;\n" : "=d"(r) : "d"(v));
+  return r;
 }
 
 #ifndef FGT_K3N_MINB
-#define FGT_K3N_MINB 5
+#define FGT_K3N_MINB 4
 #endif
 template <int DN>
 __global__ void __launch_bounds__(kThreads, FGT_K3N_MINB)
@@ -1797,48 +1895,68 @@ __global__ void __launch_bounds__(kThreads, FGT_K3N_MINB)
   constexpr int NM = DN + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const K3nStage sp = k3n_stage(smem_raw + (size_t)warp * kK3nWarpBytes);
+  unsigned char* const wbase = smem_raw + (size_t)warp * kK3nWarpBytes;
+  const K3nStage sp = k3n_stage(wbase);
   if (lane == 0) {
-    mbar_init(sp.bar);
+    mbar_init(k3n_buf(wbase).bar);
+    mbar_init(k3n_buf(wbase + kK3nBufBytes).bar);
     sp.zero[0] = 0.0;
   }
   __syncwarp();
   const WarpWalk walk{(int64_t)blockIdx.x * kSegWarps + warp, (int64_t)gridDim.x * kSegWarps,
                       a.nseg};
   const int64_t S1 = a.nseg;
-  // next narrow segment at or after s (S1 if none): issues its staging
-  auto issue_next = [&](int64_t s, SegGeom& g) -> int64_t {
-    for (; s < S1; s = walk.next(s)) {
-      if (k3_narrow(seg_deg_DM(__ldg(a.seg_deg + s)))) {
-        g = seg_geom(a, s);
-        k3n_issue(a, ec, s, g, sp, lane);
-        return s;
-      }
-    }
+  const bool all_narrow = a.nwide3 == 0;  // plan-time class counts: no lookups
+  auto next_narrow = [&](int64_t s) -> int64_t {
+    if (all_narrow) return s;
+    for (; s < S1; s = walk.next(s))
+      if (k3_narrow(seg_deg_DM(__ldg(a.seg_deg + s)))) return s;
     return S1;
   };
-  unsigned parity = 0;
+  unsigned parity = 0;  // bit k: phase of buffer k
+  int k = 0;
+  int64_t s = next_narrow(walk.first());
   SegGeom g;
-  int64_t s = issue_next(walk.first(), g);
+  if (s < S1) {
+    g = seg_geom(a, s);
+    k3n_issue(a, ec, s, g, k3n_buf(wbase), lane);
+  }
+  const unsigned az = smem_u32(sp.zero);
+  // the collapsed-form constants of this degree, held in registers
+  double Hr[NM][NM], Br[NM][NM];
+#pragma unroll
+  for (int m = 0; m < NM; ++m)
+#pragma unroll
+    for (int q = 0; q < NM; ++q) {
+      Hr[m][q] = (m + q < NM && ((m + q) & 1)) ? in_reg(cc.H[m][q]) : 0.0;
+      Br[q][m] = (m + q < NM) ? in_reg(cc.B[q][m]) : 0.0;
+    }
   while (s < S1) {
-    const SegGeom gc = g;
-    const SegFrame f = seg_frame(gc);
-    const StageSlots so = stage_slots(a, gc);
-    cp_async_wait_all();
-    mbar_wait(sp.bar, parity);
-    parity ^= 1u;
+    // prefetch: the next segment into the other buffer (consumed last round)
+    const int64_t sn = next_narrow(walk.next(s));
+    SegGeom gn;
+    if (sn < S1) {
+      gn = seg_geom(a, sn);
+      __syncwarp();
+      k3n_issue(a, ec, sn, gn, k3n_buf(wbase + (k ^ 1) * kK3nBufBytes), lane);
+    }
+    const K3nBuf bf = k3n_buf(wbase + k * kK3nBufBytes);
+    const SegFrame f = seg_frame(g);
+    const K3nSlots so = k3n_slots(a, g);
+    mbar_wait(bf.bar, (parity >> k) & 1u);
+    parity ^= 1u << k;
     __syncwarp();
-    if (gc.len < kSeg) {
+    if (g.len < kSeg) {
       // partial (last) segment: lanes past the end decode as strength-0
       // sources at the centre (their mask bits are 0)
-      for (int q = lane; q < kSeg - gc.len + 8; q += 32) {
-        sp.xy[so.oy + gc.ny + q] = f.zc;
-        sp.bb[so.ob + gc.ny + q] = 0.0;
+      for (int q = lane; q < kSeg - g.len + 8; q += 32) {
+        bf.xy[so.yo + g.ny + q] = f.zc;
+        bf.bb[so.bo + g.ny + q] = 0.0;
       }
       __syncwarp();
     }
-    // ---- decode this lane's run
-    const uint32_t word = sp.mask[lane >> 2];
+    // ---- this lane's run from the merge mask
+    const uint32_t word = bf.mask[lane >> 2];
     const unsigned byte = (word >> ((lane & 3) * 8)) & 0xffu;
     const int nt = __popc(byte);
     int incl = nt;
@@ -1849,113 +1967,107 @@ __global__ void __launch_bounds__(kThreads, FGT_K3N_MINB)
     }
     const int i0 = incl - nt;
     const int j0 = lane * kR - i0;
-    const double* px = sp.xy + so.ox + i0;
-    const double* py = sp.xy + so.oy + j0;
-    const double* pb = sp.bb + so.ob + j0;
-    double w[kR], b[kR];
+    // running 32-bit shared addresses of the next target / source / strength
+    unsigned ax = smem_u32(bf.xy + so.xo + i0);
+    unsigned ay = smem_u32(bf.xy + so.yo + j0);
+    unsigned ab = smem_u32(bf.bb + so.bo + j0);
+    // ---- one pass over the run: w = z - zc, local prefix moments lp_m of the
+    // run's sources up to and including the element (exclusive for a target,
+    // whose b is 0) and the run-local part of its potential
+    //   L = sum_q w^q sum_{m+q odd} H[m][q] lp_m
+    double w[kR], L[kR];
+    double lp[NM];
+#pragma unroll
+    for (int m = 0; m < NM; ++m) lp[m] = 0.0;
 #pragma unroll
     for (int e = 0; e < kR; ++e) {
-      const bool tg = (byte >> e) & 1u;
-      w[e] = *(tg ? px : py) - f.zc;
-      b[e] = *(tg ? sp.zero : pb);
-      px += tg ? 1 : 0;
-      py += tg ? 0 : 1;
-      pb += tg ? 0 : 1;
+      const unsigned tg = (byte >> e) & 1u;
+      const double we = lds_f64(tg ? ax : ay) - f.zc;
+      double p = lds_f64(tg ? az : ab);
+      ax += tg << 3;
+      ay += (tg ^ 1u) << 3;
+      ab += (tg ^ 1u) << 3;
+      lp[0] += p;
+#pragma unroll
+      for (int m = 1; m < NM; ++m) {
+        p *= we;
+        lp[m] += p;
+      }
+      double acc = 0.0;
+#pragma unroll
+      for (int q = DN; q >= 0; --q) {
+        double c = 0.0;
+        bool any = false;
+#pragma unroll
+        for (int m = 0; m + q < NM; ++m)
+          if ((m + q) & 1) {
+            c = any ? fma(Hr[m][q], lp[m], c) : Hr[m][q] * lp[m];
+            any = true;
+          }
+        acc = q == DN ? c : fma(acc, we, c);
+      }
+      w[e] = we;
+      L[e] = acc;
     }
     double ecq[NM];
 #pragma unroll
-    for (int q = 0; q < NM; ++q) ecq[q] = sp.ec[q];
-    __syncwarp();  // stage free: the next segment's copies go in now
-    SegGeom gn;
-    const int64_t sn = issue_next(walk.next(s), gn);
-    // ---- lane-run moments, warp scans -> exclusive prefix and totals
-    double pre[NM], E[NM];
-    {
-      double M[NM];
+    for (int q = 0; q < NM; ++q) ecq[q] = bf.ec[q];
+    // ---- run moments (the final lp) -> exclusive lane prefix and totals
+    double pre[NM], tot[NM];
+    warp_moment_scan<NM>(sp, lane, lp, pre, tot);
+    // lane-uniform coefficients: E_q + sum_{m+q odd} H[m][q] Pre_m with
+    // E_q = E^c_q + sum_m B[q][m] Tot_m
+    double cq[NM];
 #pragma unroll
-      for (int m = 0; m < NM; ++m) M[m] = 0.0;
+    for (int q = 0; q < NM; ++q) {
+      double acc = ecq[q];
 #pragma unroll
-      for (int e = 0; e < kR; ++e) {
-        double p = b[e];
-        M[0] += p;
+      for (int m = 0; m + q < NM; ++m) acc = fma(Br[q][m], tot[m], acc);
 #pragma unroll
-        for (int m = 1; m < NM; ++m) {
-          p *= w[e];
-          M[m] += p;
-        }
-      }
-      double tot[NM];
-#pragma unroll
-      for (int m = 0; m < NM; ++m) {
-        double v = M[m];
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const double t = __shfl_up_sync(0xffffffffu, v, d);
-          if (lane >= d) v += t;
-        }
-        tot[m] = __shfl_sync(0xffffffffu, v, 31);
-        pre[m] = v - M[m];
-      }
-#pragma unroll
-      for (int q = 0; q < NM; ++q) {
-        double acc = ecq[q];
-#pragma unroll
-        for (int m = 0; m + q < NM; ++m) acc = fma(cc.B[q][m], tot[m], acc);
-        E[q] = acc;
-      }
+      for (int m = 0; m + q < NM; ++m)
+        if ((m + q) & 1) acc = fma(Hr[m][q], pre[m], acc);
+      cq[q] = acc;
     }
-    // ---- evaluate every element (targets keep theirs)
-    const int64_t base = o.u_offset + gc.ib;
+    // ---- potentials: L + Horner of the lane coefficients; targets only
+    const int64_t base = o.u_offset + g.ib;
     // su slot of target i: i + off, off = u's 8-byte phase within 16 bytes,
     // so that the bulk store's shared and global addresses share alignment
     const int off = (int)((reinterpret_cast<uintptr_t>(o.u + base) >> 3) & 1);
     if (lane == 0) bulk_wait_read();  // the previous segment's store has read su
     __syncwarp();
     {
-      int tk = i0 + off;
+      unsigned at = smem_u32(sp.su + i0 + off);
+      const unsigned adis = smem_u32(sp.su + kSeg + 2);  // discard slot of non-targets
 #pragma unroll
       for (int e = 0; e < kR; ++e) {
-        double p = b[e];  // 0 for targets: the prefix is exclusive for them
-        pre[0] += p;
+        double acc = cq[DN];
 #pragma unroll
-        for (int m = 1; m < NM; ++m) {
-          p *= w[e];
-          pre[m] += p;
-        }
-        double acc = 0.0;
-#pragma unroll
-        for (int q = DN; q >= 0; --q) {
-          double c = E[q];
-#pragma unroll
-          for (int m = 0; m + q < NM; ++m)
-            if ((m + q) & 1) c = fma(cc.H[m][q], pre[m], c);
-          acc = q == DN ? c : fma(acc, w[e], c);
-        }
-        const bool tg = (byte >> e) & 1u;
-        if (tg) sp.su[tk] = acc;
-        tk += tg ? 1 : 0;
+        for (int q = DN - 1; q >= 0; --q) acc = fma(acc, w[e], cq[q]);
+        const unsigned tg = (byte >> e) & 1u;
+        sts_f64(tg ? at : adis, acc + L[e]);
+        at += tg << 3;
       }
     }
     __syncwarp();
     // ---- write back
     if (o.tperm) {
       const int32_t* tp = o.tperm + base;
-      for (int i = lane; i < gc.nx; i += 32) o.u[tp[i]] = sp.su[i + off];
-      __syncwarp();
-    } else if (gc.nx > 0) {
+      for (int i = lane; i < g.nx; i += 32) o.u[tp[i]] = sp.su[i + off];
+    } else if (g.nx > 0) {
       // interior [off, off + c) by one bulk store (16-byte aligned on both
       // sides), a misaligned head / odd tail element by plain stores
       double* up = o.u + base;
-      const int c = (gc.nx - off) & ~1;
+      const int c = (g.nx - off) & ~1;
       if (lane == 0) {
         fence_proxy_async();  // the generic stores to su before the async read
         if (c > 0) bulk_s2g(up + off, sp.su + 2 * off, 8u * (unsigned)c);
       }
       if (lane == 1 && off) up[0] = sp.su[1];
-      if (lane == 2 && off + c < gc.nx) up[gc.nx - 1] = sp.su[gc.nx - 1 + off];
+      if (lane == 2 && off + c < g.nx) up[g.nx - 1] = sp.su[g.nx - 1 + off];
     }
     s = sn;
     g = gn;
+    k ^= 1;
   }
   if (lane == 0) bulk_wait_all();
 }
