@@ -198,6 +198,7 @@ void build_modes(const Soe& folded, double delta, ModeParams& P, ModeTable& T) {
 
 // Per-chunk persistent state for the two-phase (multi-GPU) apply.
 struct ChunkState {
+  double* mom = nullptr;           // segment moments between the phases (moment path)
   double* bs = nullptr;            // strengths, sorted-source order (owned copy)
   const double* bs_dev = nullptr;  // or the caller's device strengths (already sorted order)
   cplx* tile = nullptr;            // 5 * ne * ntiles
@@ -231,6 +232,7 @@ struct fgt_plan_s {
   // segment classes (launch_classify): K1 / K3 wide-path segment counts
   int64_t nwide1 = -1, nwide3 = -1;
   int dn_narrow = -1;  // highest collapsed degree of the K3-narrow segments
+  int dm_narrow = -1;  // highest moment degree of the K1-narrow segments
   CollConsts cc{};     // collapsed-form constants of the plan (single plans)
   double zprev0 = 0.0;
   int* d_flag = nullptr;
@@ -437,6 +439,7 @@ StreamArgs stream_args(const fgt_plan_s* p, const double* bs) {
   sa.nwide1 = p->nwide1;
   sa.nwide3 = p->nwide3;
   sa.dn_narrow = p->dn_narrow;
+  sa.dm_narrow = p->dm_narrow;
   sa.seg_deg = p->d_seg_deg;
   return sa;
 }
@@ -455,7 +458,7 @@ void queue_classify(fgt_plan_s* p, unsigned long long* h, cudaStream_t st,
   ck(launch_classify(sa, p->P, p->P.smax, p->d_seg_deg,
                      check_flags ? p->d_flag : nullptr, class_counts(p), st),
      "classify");
-  ck(cudaMemcpyAsync(h, class_counts(p), 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+  ck(cudaMemcpyAsync(h, class_counts(p), 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                      st),
      "class counts");
 }
@@ -463,9 +466,10 @@ void take_classes(fgt_plan_s* p, const unsigned long long* h) {
   p->nwide1 = (int64_t)h[0];
   p->nwide3 = (int64_t)h[1];
   p->dn_narrow = (int)h[2] - 1;
+  p->dm_narrow = (int)h[3] - 1;
 }
 void classify_sync(fgt_plan_s* p, cudaStream_t st) {
-  unsigned long long hl[3] = {0, 0, 0};
+  unsigned long long hl[4] = {0, 0, 0, 0};
   unsigned char* pin = pinned_scratch();
   unsigned long long* h = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hl;
   queue_classify(p, h, st);
@@ -542,6 +546,7 @@ void destroy_plan(fgt_plan_s* p) {
   dfree(p->d_mt, st);
   dfree(p->d_flag, st);
   dfree(p->cs.bs, st);
+  dfree(p->cs.mom, st);
   dfree(p->cs.tile, st);
   cudaGetLastError();
   cudaSetDevice(cur);
@@ -613,20 +618,37 @@ void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint3
     const StreamArgs sa = stream_args(p, bs);
     const TileState ts = tile_state_carve(w.get<cplx>(tile_state_elems(p->ntiles, p->P.ne)),
                                           p->ntiles, p->P.ne);
-    {
-      ProfScope ps(0, st);
-      ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
-    }
-    {
-      ProfScope ps(1, st);
-      ck(launch_carry_scan(ts, p->ntiles, p->P.ne, nullptr, nullptr, st), "carry scan");
-    }
     OutArgs o;
     o.u = u;
     o.tperm = p->d_tperm;
-    {
-      ProfScope ps(2, st);
-      ck(launch_main(sa, p->P, p->d_mt, ts, o, st, p->batch ? nullptr : &p->cc), "main pass");
+    if (!p->batch) {
+      // moment path: K1m -> K2m (collapsed carries) -> K3
+      double* mom = w.get<double>((size_t)p->ntiles * k1m_moments(sa));
+      {
+        ProfScope ps(0, st);
+        ck(launch_moments(sa, p->P, p->d_mt, ts, mom, st), "segment moments");
+      }
+      {
+        ProfScope ps(1, st);
+        ck(launch_mom_scan(sa, p->P.ne, p->d_mt, ts, mom, nullptr, nullptr, st), "carry scan");
+      }
+      {
+        ProfScope ps(2, st);
+        ck(launch_main(sa, p->P, p->d_mt, ts, o, st, &p->cc, true), "main pass");
+      }
+    } else {
+      {
+        ProfScope ps(0, st);
+        ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
+      }
+      {
+        ProfScope ps(1, st);
+        ck(launch_carry_scan(ts, p->ntiles, p->P.ne, nullptr, nullptr, st), "carry scan");
+      }
+      {
+        ProfScope ps(2, st);
+        ck(launch_main(sa, p->P, p->d_mt, ts, o, st), "main pass");
+      }
     }
   }
   note_use(p, st);
@@ -670,15 +692,17 @@ void run_chunk_aggregate(fgt_plan_s* p, const double* strengths, cplx* totals_ou
   }
   const StreamArgs sa = stream_args(p, bs);
   const TileState ts = tile_state_carve(p->cs.tile, p->ntiles, ne);
+  if (!p->cs.mom) p->cs.mom = dmalloc<double>((size_t)p->ntiles * k1m_moments(sa), st);
   {
     ProfScope ps(0, st);
-    ck(launch_aggregate(sa, p->P, p->d_mt, ts, st), "tile aggregates");
+    ck(launch_moments(sa, p->P, p->d_mt, ts, p->cs.mom, st), "segment moments");
   }
   cplx* d_tot = dev_aggs ? totals_out : w.get<cplx>(3 * ne);
   {
     // block reduce + top level only: phase 2's down-sweep writes the carries
     ProfScope ps(1, st);
-    ck(launch_carry_scan(ts, p->ntiles, ne, nullptr, d_tot, st, true, false), "chunk totals");
+    ck(launch_mom_scan(sa, ne, p->d_mt, ts, p->cs.mom, nullptr, d_tot, st, true, false),
+       "chunk totals");
   }
   note_use(p, st);
   if (dev_aggs) return;  // stream-ordered: the caller gathers the device totals
@@ -713,14 +737,14 @@ void run_chunk_finish(fgt_plan_s* p, const double* strengths, const cplx* carry_
   {
     ProfScope ps(1, st);
     // phase 1's block aggregates are still in the tile state: top + down only
-    ck(launch_carry_scan(ts, p->ntiles, ne, d_cin, nullptr, st, false), "carry scan");
+    ck(launch_mom_scan(sa, ne, p->d_mt, ts, p->cs.mom, d_cin, nullptr, st, false), "carry scan");
   }
   OutArgs o;
   o.u = u;
   o.tperm = p->d_tperm;
   {
     ProfScope ps(2, st);
-    ck(launch_main(sa, p->P, p->d_mt, ts, o, st, p->batch ? nullptr : &p->cc), "main pass");
+    ck(launch_main(sa, p->P, p->d_mt, ts, o, st, &p->cc, true), "main pass");
   }
   note_use(p, st);
   if (!dev) {
@@ -1231,7 +1255,7 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
       unsigned char* pin = pinned_scratch();
       int hfl[8] = {0};
       double xyl[2] = {0.0, 0.0};
-      unsigned long long hcl[3] = {0, 0, 0};
+      unsigned long long hcl[4] = {0, 0, 0, 0};
       int* hf = pin ? reinterpret_cast<int*>(pin) : hfl;
       double* xy0 = pin ? reinterpret_cast<double*>(pin + 32) : xyl;
       unsigned long long* hc = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hcl;
@@ -1676,7 +1700,7 @@ extern "C" int fgt_batch_create(int B, const double* targets, const int64_t* t_o
       ck(launch_batch_modes(base, d_deltas, B, p->d_mtb, st), "mode tables");
       p->d_mt = dmalloc<ModeTable>(1, st);
       ck(launch_store_table(T0, p->d_mt, st), "mode table");
-      unsigned long long hcl[3] = {0, 0, 0};
+      unsigned long long hcl[4] = {0, 0, 0, 0};
       unsigned long long* hc = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hcl;
       queue_classify(p, hc, st, true);
       ck(cudaStreamSynchronize(st), "batch plan sync");

@@ -1354,6 +1354,7 @@ __global__ void classify_kernel(StreamArgs a, ModeParams P, double smax, int* __
   const int lane = threadIdx.x & 31;
   unsigned long long c1 = 0, c3 = 0;
   unsigned dn1 = 0;  // highest DN + 1 among this thread's K3-narrow segments
+  unsigned dm1 = 0;  // highest DM + 1 among its K1-narrow segments
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t s0 = (int64_t)blockIdx.x * blockDim.x; s0 < a.nseg; s0 += stride) {
     const int64_t s = s0 + threadIdx.x;
@@ -1376,15 +1377,18 @@ __global__ void classify_kernel(StreamArgs a, ModeParams P, double smax, int* __
       w1 = !k1_narrow(DM);
       w3 = !k3_narrow(DM);
       if (!w3 && DN + 1 > dn1) dn1 = DN + 1;
+      if (!w1 && DM + 1 > dm1) dm1 = DM + 1;
     }
     c1 += __popc(__ballot_sync(0xffffffffu, w1));
     c3 += __popc(__ballot_sync(0xffffffffu, w3));
   }
   dn1 = __reduce_max_sync(0xffffffffu, dn1);
+  dm1 = __reduce_max_sync(0xffffffffu, dm1);
   if (lane == 0) {
     atomicAdd(counts, c1);
     atomicAdd(counts + 1, c3);
     if (dn1 > 0) atomicMax(counts + 2, (unsigned long long)dn1);
+    if (dm1 > 0) atomicMax(counts + 3, (unsigned long long)dm1);
   }
 }
 
@@ -2681,6 +2685,409 @@ __global__ void __launch_bounds__(kScanThreads) scan_down_kernel(ScanArgs sa) {
   }
 }
 
+// ------------------------------------------- moment path: K1m and K2m
+//
+// Single plans carry the narrow segments' aggregates as their source
+// moments about the segment centre, Mom_n = sum b (y - zc)^n, n < NMk (the
+// plan's highest K1 moment degree + 1): 8 NMk bytes per segment instead of
+// 48 ne (A, F, G per mode).  The per-mode pairs are formed from them inside
+// the carry scan (K2m), whose down-sweep also folds every K3-narrow
+// segment's carries into its collapsed carries E^c (the collapse kernel's
+// job) so the per-mode carries of those segments never reach memory.
+
+constexpr int kMomMax = FGT_K1_MAXDM + 1;
+// Scan blocks of the moment path: kMomBlock consecutive segments per warp.
+constexpr int kMomBlock = 64;
+constexpr int kMomPerLane = kMomBlock / 32;
+static_assert(kMomPerLane == 2, "moment-path scan block layout");
+
+struct MomScanArgs {
+  StreamArgs a;
+  int ne;
+  double* mom;  // [nseg][nm]
+  int nm;       // K1 moments per segment (launch-uniform)
+  int dn;       // collapsed degree of the narrow K3 (E^c rows)
+  TileState ts;
+  int64_t nblk;
+  cplx* blkagg;    // [2ne][nblk] pairs (backward blocks stored right to left)
+  cplx* blkcarry;  // [2ne][nblk]
+};
+
+__device__ __forceinline__ bool mom_n1(const StreamArgs& a, int DM) {
+  return a.nwide1 == 0 || k1_narrow(DM);
+}
+__device__ __forceinline__ bool mom_n3(const StreamArgs& a, int DM) {
+  return a.nwide3 == 0 || k3_narrow(DM);
+}
+
+// Mode k of a segment from its moments about its centre (seg_aggregate_from's
+// algebra): A = e^{-s (h0 + h1)}, F = forward state after the segment, G =
+// backward state before it; E0 / E1 = e^{-s h0} / e^{-s h1} (degree NM-1
+// Taylor polynomials, |s h| <= rmax[DM]).
+template <int NM>
+__device__ __forceinline__ void mom_pairs(const ModeTable& mt, int k, const double (&M)[NM],
+                                          double h0, double h1, cplx& A, cplx& F, cplx& G,
+                                          cplx& E0, cplx& E1) {
+  const cplx* c = mt.coef[k];
+  cplx e0 = c[NM - 1], e1 = c[NM - 1];
+  cplx ev = {0.0, 0.0}, od = {0.0, 0.0};
+#pragma unroll
+  for (int n = NM - 1; n >= 0; --n) {
+    const cplx cn = c[n];
+    if (n < NM - 1) {
+      e0 = {fma(e0.re, h0, cn.re), fma(e0.im, h0, cn.im)};
+      e1 = {fma(e1.re, h1, cn.re), fma(e1.im, h1, cn.im)};
+    }
+    if (n & 1) {
+      od.re = fma(cn.re, M[n], od.re);
+      od.im = fma(cn.im, M[n], od.im);
+    } else {
+      ev.re = fma(cn.re, M[n], ev.re);
+      ev.im = fma(cn.im, M[n], ev.im);
+    }
+  }
+  E0 = e0;
+  E1 = e1;
+  A = cmul(e0, e1);
+  F = cmul(e1, cplx{ev.re - od.re, ev.im - od.im});
+  G = cmul(e0, cplx{ev.re + od.re, ev.im + od.im});
+}
+
+// K1b: one CTA per scan block of kMomCta = kSegWarps * kMomBlock segments,
+// kMomBlock consecutive segments per warp.  Phase 1 (per warp): every
+// segment's source moments about its centre from a ring of kK1Stages TMA
+// stages (each segment's y and beta as their enclosing 16-byte blocks; the
+// next kK1Stages - 1 segments stay in flight while one is reduced), stored
+// for the down-sweep.  Phase 2: lanes k < ne fold mode k forward (left to
+// right), lanes ne + k backward (right to left) over the warp's segments;
+// the CTA combines its warps' aggregates into the block aggregates of K2's
+// top level.  K1-wide segments take the (A, F, G) the wide K1 stored.
+constexpr int kMomCta = kSegWarps * kMomBlock;
+constexpr int kK1Stages = 3;
+constexpr int kK1StageD = kSeg + 4;  // doubles per set and stage
+struct K1Stage {
+  double* y;
+  double* b;
+  uint64_t* bar;
+};
+constexpr size_t kK1WarpBytes =
+    (sizeof(double) * 2 * kK1StageD * kK1Stages + 8 * kK1Stages + 15) & ~(size_t)15;
+__device__ __forceinline__ K1Stage k1_stage(unsigned char* wb, int i) {
+  K1Stage st;
+  st.y = reinterpret_cast<double*>(wb) + (size_t)i * 2 * kK1StageD;
+  st.b = st.y + kK1StageD;
+  st.bar = reinterpret_cast<uint64_t*>(wb + sizeof(double) * 2 * kK1StageD * kK1Stages) + i;
+  return st;
+}
+// One lane issues a segment's sources (y, beta) into a stage.
+__device__ __forceinline__ void k1_issue(const StreamArgs& a, const SegGeom& g, const K1Stage& st) {
+  auto blocks = [](const double* p, int n, const double*& src) -> unsigned {
+    const uintptr_t b0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+    const uintptr_t b1 = (reinterpret_cast<uintptr_t>(p + n) + 15) & ~(uintptr_t)15;
+    src = reinterpret_cast<const double*>(b0);
+    return n > 0 ? (unsigned)(b1 - b0) : 0u;
+  };
+  const double *sy, *sb;
+  const unsigned by = blocks(a.ys + g.jb, g.ny, sy);
+  const unsigned bb = blocks(a.bs + g.jb, g.ny, sb);
+  fence_proxy_async();
+  mbar_expect(st.bar, by + bb);
+  if (by) bulk_g2s(st.y, sy, by, st.bar);
+  if (bb) bulk_g2s(st.b, sb, bb, st.bar);
+}
+
+template <int NM>
+__global__ void __launch_bounds__(kThreads, 4) k1b_kernel(MomScanArgs q,
+                                                          const ModeTable* __restrict__ mtab) {
+  extern __shared__ __align__(16) unsigned char k1b_smem[];
+  __shared__ ModeTable mt;
+  __shared__ double smom[kSegWarps][kMomBlock][NM];
+  __shared__ Pair wagg[kSegWarps][2 * kMaxModes];
+  load_mode_table(mtab, mt);
+  const StreamArgs& a = q.a;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ne = q.ne;
+  const bool all1 = a.nwide1 == 0;
+  unsigned char* wb = k1b_smem + (size_t)warp * kK1WarpBytes;
+  if (lane == 0)
+    for (int i = 0; i < kK1Stages; ++i) mbar_init(k1_stage(wb, i).bar);
+  __syncthreads();
+  unsigned parity = 0;
+  for (int64_t b = blockIdx.x; b < q.nblk; b += gridDim.x) {
+    const int64_t s0 = b * kMomCta + (int64_t)warp * kMomBlock;
+    const int64_t s1 = s0 + kMomBlock < a.nseg ? s0 + kMomBlock : a.nseg;
+    // ---- phase 1: moments (stage ring)
+    if (lane == 0)
+      for (int i = 0; i < kK1Stages && s0 + i < s1; ++i)
+        k1_issue(a, seg_geom(a, s0 + i), k1_stage(wb, i));
+    for (int64_t s = s0; s < s1; ++s) {
+      const int i = (int)((s - s0) % kK1Stages);
+      const K1Stage st = k1_stage(wb, i);
+      const SegGeom g = seg_geom(a, s);
+      const double zc = seg_frame(g).zc;
+      const int oy = phase8(a.ys + g.jb), ob = phase8(a.bs + g.jb);
+      mbar_wait(st.bar, (parity >> i) & 1u);
+      parity ^= 1u << i;
+      double M[NM];
+#pragma unroll
+      for (int n = 0; n < NM; ++n) M[n] = 0.0;
+#pragma unroll
+      for (int u = 0; u < kK1Per; ++u) {
+        const int j = lane + 32 * u;
+        const bool live = j < g.ny;
+        const double d = live ? st.y[oy + j] - zc : 0.0;
+        double p = live ? st.b[ob + j] : 0.0;
+        M[0] += p;
+#pragma unroll
+        for (int n = 1; n < NM; ++n) {
+          p *= d;
+          M[n] += p;
+        }
+      }
+      __syncwarp();  // stage consumed: refill it with segment s + kK1Stages
+      if (lane == 0 && s + kK1Stages < s1) k1_issue(a, seg_geom(a, s + kK1Stages), st);
+#pragma unroll
+      for (int n = 0; n < NM; ++n) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) M[n] += __shfl_xor_sync(0xffffffffu, M[n], o);
+      }
+      if (lane == 0) {
+        double* out = q.mom + s * NM;
+#pragma unroll
+        for (int n = 0; n < NM; ++n) {
+          out[n] = M[n];
+          smom[warp][s - s0][n] = M[n];
+        }
+      }
+    }
+    __syncwarp();
+    // ---- phase 2: per-warp aggregates per mode, lane l holding segments
+    // s0 + 2l and s0 + 2l + 1; ordered warp reductions (forward: lower lanes
+    // first; backward: higher lanes first)
+    {
+      bool live[2], n1[2];
+      double h0[2], h1[2];
+      int64_t sg[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        sg[i] = s0 + 2 * lane + i;
+        live[i] = sg[i] < s1;
+        n1[i] = false;
+        h0[i] = h1[i] = 0.0;
+        if (live[i]) {
+          n1[i] = all1 || k1_narrow(seg_deg_DM(__ldg(a.seg_deg + sg[i])));
+          const SegFrame f = seg_frame(seg_geom(a, sg[i]));
+          h0[i] = f.h0;
+          h1[i] = f.h1;
+        }
+      }
+      for (int k = 0; k < ne; ++k) {
+        cplx A[2], F[2], G[2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (!live[i]) {
+            A[i] = {1.0, 0.0};
+            F[i] = G[i] = {0.0, 0.0};
+          } else if (n1[i]) {
+            double M[NM];
+#pragma unroll
+            for (int n = 0; n < NM; ++n) M[n] = smom[warp][2 * lane + i][n];
+            cplx E0, E1;
+            mom_pairs<NM>(mt, k, M, h0[i], h1[i], A[i], F[i], G[i], E0, E1);
+          } else {
+            const int64_t o = (int64_t)k * a.nseg + sg[i];
+            A[i] = q.ts.A[o];
+            F[i] = q.ts.F[o];
+            G[i] = q.ts.G[o];
+          }
+        }
+        Pair fw = combine(Pair{A[0], F[0]}, Pair{A[1], F[1]});
+        Pair bw = combine(Pair{A[1], G[1]}, Pair{A[0], G[0]});
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          Pair of, ob;
+          of.a.re = __shfl_xor_sync(0xffffffffu, fw.a.re, off);
+          of.a.im = __shfl_xor_sync(0xffffffffu, fw.a.im, off);
+          of.s.re = __shfl_xor_sync(0xffffffffu, fw.s.re, off);
+          of.s.im = __shfl_xor_sync(0xffffffffu, fw.s.im, off);
+          ob.a.re = __shfl_xor_sync(0xffffffffu, bw.a.re, off);
+          ob.a.im = __shfl_xor_sync(0xffffffffu, bw.a.im, off);
+          ob.s.re = __shfl_xor_sync(0xffffffffu, bw.s.re, off);
+          ob.s.im = __shfl_xor_sync(0xffffffffu, bw.s.im, off);
+          const bool lower = (lane & off) == 0;
+          fw = lower ? combine(fw, of) : combine(of, fw);
+          bw = lower ? combine(ob, bw) : combine(bw, ob);
+        }
+        if (lane == 0) {
+          wagg[warp][k] = fw;
+          wagg[warp][ne + k] = bw;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- the CTA's block aggregates: forward over warps 0.., backward over
+    // warps ..0 (warps past the end hold identities)
+    if (threadIdx.x < 2 * ne) {
+      const bool bwd = (int)threadIdx.x >= ne;
+      Pair acc{{1.0, 0.0}, {0.0, 0.0}};
+      for (int w = 0; w < kSegWarps; ++w) {
+        const int ww = bwd ? kSegWarps - 1 - w : w;
+        if (b * kMomCta + (int64_t)ww * kMomBlock < a.nseg) acc = combine(acc, wagg[ww][threadIdx.x]);
+      }
+      cplx* out = q.blkagg + ((int64_t)threadIdx.x * q.nblk + (bwd ? q.nblk - 1 - b : b)) * 2;
+      out[0] = acc.a;
+      out[1] = acc.s;
+    }
+    __syncthreads();
+  }
+}
+
+// K2m down-sweep, one CTA per scan block (kMomBlock segments per warp, two
+// per lane: s0 + 2l, s0 + 2l + 1).  Per mode: exclusive warp scans of the
+// lane pairs (forward by shfl_up, backward by shfl_down), the warps' totals
+// combined through shared memory into each warp's carry-in, seeded with the
+// block carries of the top level.  K3-narrow segments fold their carries
+// into the collapsed carries E^c, K3-wide ones store them.
+template <int NM>
+__global__ void __launch_bounds__(kThreads) k2m_down_kernel(MomScanArgs q,
+                                                            const ModeTable* __restrict__ mtab) {
+  __shared__ ModeTable mt;
+  __shared__ Pair wtot[kMaxModes][2][kSegWarps];
+  load_mode_table(mtab, mt);
+  __syncthreads();
+  const StreamArgs& a = q.a;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = blockIdx.x;
+  const int ne = q.ne;
+  bool live[2], n1[2], n3[2];
+  double h0[2], h1[2];
+  double M[2][NM];
+  int64_t sg[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    sg[i] = b * kMomCta + (int64_t)warp * kMomBlock + 2 * lane + i;
+    live[i] = sg[i] < a.nseg;
+    n1[i] = n3[i] = false;
+    h0[i] = h1[i] = 0.0;
+#pragma unroll
+    for (int n = 0; n < NM; ++n) M[i][n] = 0.0;
+    if (live[i]) {
+      const int DM = seg_deg_DM(__ldg(a.seg_deg + sg[i]));
+      n1[i] = mom_n1(a, DM);
+      n3[i] = mom_n3(a, DM);
+      const SegFrame f = seg_frame(seg_geom(a, sg[i]));
+      h0[i] = f.h0;
+      h1[i] = f.h1;
+      if (n1[i]) {
+        const double* m = q.mom + sg[i] * NM;
+#pragma unroll
+        for (int n = 0; n < NM; ++n) M[i][n] = __ldg(m + n);
+      }
+    }
+  }
+  double E[2][kCollMax + 1];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int n = 0; n <= kCollMax; ++n) E[i][n] = 0.0;
+  const Pair id{{1.0, 0.0}, {0.0, 0.0}};
+  for (int k = 0; k < ne; ++k) {
+    cplx A[2], F[2], G[2], E0[2], E1[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      if (!live[i]) {
+        A[i] = {1.0, 0.0};
+        F[i] = G[i] = E0[i] = E1[i] = {0.0, 0.0};
+      } else if (n1[i]) {
+        mom_pairs<NM>(mt, k, M[i], h0[i], h1[i], A[i], F[i], G[i], E0[i], E1[i]);
+      } else {
+        const int64_t o = (int64_t)k * a.nseg + sg[i];
+        A[i] = q.ts.A[o];
+        F[i] = q.ts.F[o];
+        G[i] = q.ts.G[o];
+        E0[i] = E1[i] = {0.0, 0.0};
+      }
+    }
+    // forward: lane aggregate (item 0 then 1), inclusive scan over lanes
+    Pair fincl = combine(Pair{A[0], F[0]}, Pair{A[1], F[1]});
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const Pair p = shfl_up_pair(fincl, off);
+      if (lane >= off) fincl = combine(p, fincl);
+    }
+    Pair fex = shfl_up_pair(fincl, 1);
+    if (lane == 0) fex = id;
+    // backward: lane aggregate in reverse order (item 1 then 0), inclusive
+    // scan from the right
+    Pair bincl = combine(Pair{A[1], G[1]}, Pair{A[0], G[0]});
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      Pair p;
+      p.a.re = __shfl_down_sync(0xffffffffu, bincl.a.re, off);
+      p.a.im = __shfl_down_sync(0xffffffffu, bincl.a.im, off);
+      p.s.re = __shfl_down_sync(0xffffffffu, bincl.s.re, off);
+      p.s.im = __shfl_down_sync(0xffffffffu, bincl.s.im, off);
+      if (lane + off < 32) bincl = combine(p, bincl);
+    }
+    Pair bex;
+    bex.a.re = __shfl_down_sync(0xffffffffu, bincl.a.re, 1);
+    bex.a.im = __shfl_down_sync(0xffffffffu, bincl.a.im, 1);
+    bex.s.re = __shfl_down_sync(0xffffffffu, bincl.s.re, 1);
+    bex.s.im = __shfl_down_sync(0xffffffffu, bincl.s.im, 1);
+    if (lane == 31) bex = id;
+    if (lane == 31) wtot[k][0][warp] = fincl;
+    if (lane == 0) wtot[k][1][warp] = bincl;
+    __syncthreads();
+    // this warp's carries in: the block's carry through the earlier warps
+    // (forward) / the later warps (backward)
+    cplx cinf = q.blkcarry[(int64_t)k * q.nblk + b];
+    cplx cinb = q.blkcarry[(int64_t)(ne + k) * q.nblk + (q.nblk - 1 - b)];
+    for (int w = 0; w < warp; ++w) {
+      const Pair t = wtot[k][0][w];
+      cinf = cmad(t.a, cinf, t.s);
+    }
+    for (int w = kSegWarps - 1; w > warp; --w) {
+      const Pair t = wtot[k][1][w];
+      cinb = cmad(t.a, cinb, t.s);
+    }
+    cplx cf[2], cb[2];
+    cf[0] = cmad(fex.a, cinf, fex.s);  // forward state before item 0
+    cf[1] = cmad(A[0], cf[0], F[0]);   // ... before item 1
+    cb[1] = cmad(bex.a, cinb, bex.s);  // backward state at item 1's last element
+    cb[0] = cmad(A[1], cb[1], G[1]);   // ... at item 0's last element
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      if (!live[i]) continue;
+      if (n3[i]) {
+        // collapsed carries: Re sum_k mw_k c_kq (e^{-s h0} Cf + (-1)^q e^{-s h1} Cb)
+        const cplx tf = cmul(E0[i], cf[i]), tb = cmul(E1[i], cb[i]);
+#pragma unroll
+        for (int n = 0; n <= kCollMax; ++n) {
+          if (n <= q.dn) {
+            const cplx x = mt.mwc[k][n];
+            const double sgn = (n & 1) ? -1.0 : 1.0;
+            E[i][n] = fma(x.re, fma(sgn, tb.re, tf.re), fma(-x.im, fma(sgn, tb.im, tf.im), E[i][n]));
+          }
+        }
+      } else {
+        const int64_t o = (int64_t)k * a.nseg + sg[i];
+        q.ts.Cf[o] = cf[i];
+        q.ts.Cb[o] = cb[i];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    if (live[i] && n3[i]) {
+      double* out = q.ts.ec + sg[i] * kEcStride;
+#pragma unroll
+      for (int n = 0; n <= kCollMax; ++n) out[n] = n <= q.dn ? E[i][n] : 0.0;
+#pragma unroll
+      for (int n = kCollMax + 1; n < kEcStride; ++n) out[n] = 0.0;
+    }
+  }
+}
+
 // out[i] = alpha[perm[i]]: random reads; kGatherILP independent gathers per
 // thread in flight (coalesced index loads first, then the data loads).
 constexpr int kGatherILP = 8;
@@ -2724,15 +3131,17 @@ static int num_sms() {
 
 int64_t scan_blocks(int64_t nseg) { return (nseg + kScanBlock - 1) / kScanBlock; }
 
+// the moment path's smaller scan blocks set the workspace size
+static int64_t ws_blocks(int64_t nseg) { return (nseg + 255) / 256; }
 size_t tile_state_elems(int64_t nseg, int ne) {
   const size_t nt = (size_t)nseg * (size_t)ne;
-  const size_t blk = (size_t)scan_blocks(nseg) * 2 * (size_t)ne * 3 + 8;
+  const size_t blk = (size_t)ws_blocks(nseg) * 2 * (size_t)ne * 3 + 8;
   return 5 * nt + blk + (size_t)nseg * (kEcStride / 2) + 4;
 }
 
 TileState tile_state_carve(cplx* base, int64_t nseg, int ne) {
   const size_t nt = (size_t)nseg * (size_t)ne;
-  const size_t blk = (size_t)scan_blocks(nseg) * 2 * (size_t)ne * 3 + 8;
+  const size_t blk = (size_t)ws_blocks(nseg) * 2 * (size_t)ne * 3 + 8;
   // collapsed carries: 64-byte aligned rows (one bulk copy per segment)
   uintptr_t ecp = reinterpret_cast<uintptr_t>(base + 5 * nt + blk);
   ecp = (ecp + 63) & ~(uintptr_t)63;
@@ -2863,7 +3272,7 @@ cudaError_t launch_batch_modes(const BatchModeBase& base, const double* deltas, 
 cudaError_t launch_classify(const StreamArgs& a, const ModeParams& P, double smax,
                             int* seg_deg, const int* skip_flags,
                             unsigned long long* counts, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(counts, 0, 3 * sizeof(unsigned long long), st);
+  cudaError_t e = cudaMemsetAsync(counts, 0, 4 * sizeof(unsigned long long), st);
   if (e != cudaSuccess || a.nseg == 0) return e;
   const int64_t want = (a.nseg + 255) / 256;
   const int64_t cap = (int64_t)num_sms() * 8;
@@ -2960,8 +3369,13 @@ static cudaError_t launch_k3n_dn(const StreamArgs& a, const TileState& ts, const
   return cudaGetLastError();
 }
 
+int k3n_degree(const StreamArgs& a) {
+  return a.dn_narrow >= 0 ? (a.dn_narrow < kCollMax ? a.dn_narrow : kCollMax) : kCollMax;
+}
+
 cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
-                        TileState ts, OutArgs o, cudaStream_t st, const CollConsts* cc) {
+                        TileState ts, OutArgs o, cudaStream_t st, const CollConsts* cc,
+                        bool ec_ready) {
   if (!cc || a.mtb || a.nseg == 0) return launch_seg_main<false>(a, P, mt, ts, o, st);
   // single plan: wide segments on the per-segment kernel, narrow ones on the
   // collapsed kernel at the plan's highest narrow degree
@@ -2970,9 +3384,11 @@ cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTabl
     if (e != cudaSuccess) return e;
   }
   if (a.nwide3 == a.nseg) return cudaSuccess;
-  const int DN = a.dn_narrow >= 0 ? (a.dn_narrow < kCollMax ? a.dn_narrow : kCollMax) : kCollMax;
-  note_launch();
-  collapse_carries_kernel<<<(unsigned)((a.nseg + 255) / 256), 256, 0, st>>>(a, mt, P.ne, ts, DN);
+  const int DN = k3n_degree(a);
+  if (!ec_ready) {
+    note_launch();
+    collapse_carries_kernel<<<(unsigned)((a.nseg + 255) / 256), 256, 0, st>>>(a, mt, P.ne, ts, DN);
+  }
   switch (DN) {
     case 0: return launch_k3n_dn<0>(a, ts, *cc, o, st);
     case 1: return launch_k3n_dn<1>(a, ts, *cc, o, st);
@@ -3010,6 +3426,73 @@ cudaError_t launch_gather(const double* alpha, const int32_t* perm, int64_t n, d
   if (blocks > 148 * 16) blocks = 148 * 16;
   note_launch();
   gather_kernel<<<blocks, 256, 0, st>>>(alpha, perm, n, out);
+  return cudaGetLastError();
+}
+
+// ---- moment path launchers
+
+int k1m_moments(const StreamArgs& a) {
+  return a.dm_narrow >= 0 ? a.dm_narrow + 1 : kMomMax;
+}
+
+int64_t mom_scan_blocks(int64_t nseg) { return (nseg + kMomCta - 1) / kMomCta; }
+
+cudaError_t launch_moments(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
+                           TileState ts, double* mom, cudaStream_t st) {
+  (void)mom;
+  if (a.nseg == 0 || a.nwide1 == 0) return cudaSuccess;
+  // K1-wide segments keep their per-mode (A, F, G) (wide K1); the narrow
+  // ones' moments are formed by K1b inside launch_mom_scan
+  const int64_t want = (a.nseg + kSegWarps - 1) / kSegWarps;
+  const int64_t cap = (int64_t)num_sms() * FGT_K1_GRID;
+  note_launch();
+  seg_aggregate_kernel<true><<<(unsigned)(want < cap ? want : cap), kThreads, sizeof(ModeTable),
+                               st>>>(a, P, mt, ts);
+  return cudaGetLastError();
+}
+
+template <int NM>
+static cudaError_t launch_mom_nm(const MomScanArgs& q, const ModeTable* mt, bool reduce, bool down,
+                                 const ScanArgs& sa, const cplx* carry_in, cplx* totals,
+                                 cudaStream_t st) {
+  const size_t smem = (size_t)kSegWarps * kK1WarpBytes;
+  static std::atomic<unsigned long long> done{0};
+  cudaError_t e = ensure_dynamic_smem(k1b_kernel<NM>, (int)smem, done);
+  if (e != cudaSuccess) return e;
+  const unsigned grid = (unsigned)q.nblk;
+  note_launch(1 + (reduce ? 1 : 0) + (down ? 1 : 0));
+  if (reduce) k1b_kernel<NM><<<grid, kThreads, smem, st>>>(q, mt);
+  scan_top_kernel<<<2 * q.ne, 1024, 0, st>>>(sa, carry_in, totals);
+  if (down) k2m_down_kernel<NM><<<grid, kThreads, 0, st>>>(q, mt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mom_scan(const StreamArgs& a, int ne, const ModeTable* mt, const TileState& ts,
+                            double* mom, const cplx* carry_in, cplx* totals, cudaStream_t st,
+                            bool reduce, bool down) {
+  if (a.nseg == 0) return cudaSuccess;
+  const int64_t nblk = mom_scan_blocks(a.nseg);
+  MomScanArgs q;
+  q.a = a;
+  q.ne = ne;
+  q.mom = mom;
+  q.nm = k1m_moments(a);
+  q.dn = k3n_degree(a);
+  q.ts = ts;
+  q.nblk = nblk;
+  q.blkagg = ts.blk;
+  q.blkcarry = ts.blk + (size_t)nblk * 2 * ne * 2;
+  const ScanArgs sa{ts.A, ts.F, ts.G, ts.Cf, ts.Cb, a.nseg, ne, nblk, q.blkagg, q.blkcarry};
+  switch (q.nm) {
+#define FGT_MNM(n)                                                 \
+  case n:                                                          \
+    return launch_mom_nm<n>(q, mt, reduce, down, sa, carry_in, totals, st);
+    FGT_MNM(1) FGT_MNM(2) FGT_MNM(3) FGT_MNM(4) FGT_MNM(5) FGT_MNM(6) FGT_MNM(7) FGT_MNM(8)
+    FGT_MNM(9) FGT_MNM(10) FGT_MNM(11) FGT_MNM(12) FGT_MNM(13)
+#undef FGT_MNM
+    default:
+      return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

@@ -92,6 +92,9 @@ struct StreamArgs {
   // plan-time highest collapsed degree DN over the narrow segments (-1:
   // unknown -> the narrow K3 runs at kCollMax)
   int dn_narrow = -1;
+  // plan-time highest moment degree DM over the K1-narrow segments (-1:
+  // unknown -> kMomMax moments)
+  int dm_narrow = -1;
 };
 
 struct OutArgs {
@@ -185,7 +188,21 @@ cudaError_t launch_chunk_carries(const cplx* aggs, int n_chunks, int ne, int ran
 // K3.  cc: the plan's collapsed-form constants (single plans); nullptr runs
 // the per-segment-degree narrow kernel (batched plans, per-transform tables).
 cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
-                        TileState ts, OutArgs o, cudaStream_t st, const CollConsts* cc = nullptr);
+                        TileState ts, OutArgs o, cudaStream_t st, const CollConsts* cc = nullptr,
+                        bool ec_ready = false);
+// Moment path (single plans): K1m writes the narrow segments' source
+// moments (k1m_moments(a) per segment, mom[nseg][..]) and the wide K1 the
+// others' (A, F, G); K2m scans them per mode and direction and writes the
+// K3-narrow segments' collapsed carries (ts.ec, launch_main(..., ec_ready))
+// and the K3-wide segments' carries (ts.Cf / Cb).  carry_in / totals /
+// reduce / down as launch_carry_scan.
+int k1m_moments(const StreamArgs& a);
+int k3n_degree(const StreamArgs& a);
+cudaError_t launch_moments(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
+                           TileState ts, double* mom, cudaStream_t st);
+cudaError_t launch_mom_scan(const StreamArgs& a, int ne, const ModeTable* mt, const TileState& ts,
+                            double* mom, const cplx* carry_in, cplx* totals,
+                            cudaStream_t st, bool reduce = true, bool down = true);
 cudaError_t launch_mode_sums(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, OutArgs o, cudaStream_t st);
 cudaError_t launch_gather(const double* alpha, const int32_t* perm, int64_t n, double* out,
