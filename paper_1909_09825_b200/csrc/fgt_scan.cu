@@ -2201,45 +2201,6 @@ __device__ __forceinline__ int merge_path_smem(const double* x, int nx, const do
   return lo;
 }
 
-// Index-order checks of one staged set s[0..n) (16-byte aligned pairs from
-// s + head, see stage_plan): non-finite values and, when check_sorted, an
-// element below its predecessor (prev = the element before s[0], -inf if
-// none).  Pairs by 16-byte shared loads (conflict-free); the predecessor of
-// a pair comes from the neighbouring thread.
-__device__ __forceinline__ void check_staged(const double* sv, int n, int head, double prev,
-                                             int check_sorted, int t, int& fin, int& ord) {
-  if (n <= 0) return;
-  // element 0 when it is the unaligned head, then pairs (head + 2k, +1)
-  if (head && t == 0) {
-    fin |= !isfinite(sv[0]);
-    if (check_sorted) ord |= prev > sv[0];
-  }
-  const int npair = (n - head) >> 1;
-  const int lane = t & 31;
-  for (int k0 = 0; k0 < npair; k0 += blockDim.x) {  // block-uniform trip count
-    const int k = k0 + t;
-    const bool have = k < npair;
-    double2 v = make_double2(0.0, 0.0);
-    if (have) v = *reinterpret_cast<const double2*>(sv + head + 2 * k);
-    // predecessor: the previous thread's second element (lane 0: a load)
-    double pv = __shfl_up_sync(0xffffffffu, v.y, 1);
-    if (lane == 0 && have) {
-      const int i = head + 2 * k;
-      pv = i > 0 ? sv[i - 1] : prev;
-    }
-    if (have) {
-      fin |= !isfinite(v.x) | !isfinite(v.y);
-      if (check_sorted) ord |= (pv > v.x) | (v.x > v.y);
-    }
-  }
-  // odd tail element
-  if (((n - head) & 1) && t == 0) {
-    const double v = sv[n - 1];
-    fin |= !isfinite(v);
-    if (check_sorted) ord |= (n >= 2 ? sv[n - 2] : prev) > v;
-  }
-}
-
 template <bool BATCH>
 __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorted,
                                                int64_t nseg, int64_t* __restrict__ seg_ib,
@@ -2250,6 +2211,7 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
                                                int* __restrict__ flags) {
   extern __shared__ __align__(16) double tsm[];
   __shared__ int sib[kPlanSegs + 1];
+  __shared__ int swin[kPlanThreads];
   __shared__ uint32_t smask[kPlanWords];
   __shared__ int sflags;
   __shared__ __align__(8) uint64_t bar;
@@ -2296,19 +2258,6 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
   mbar_wait(&bar, 0);
   __syncthreads();
   int f0 = 0, f1 = 0, f2 = 0, f3 = 0, f4 = 0;
-  check_staged(sx, nx, stx.head, xprev, check_sorted, t, f0, f3);
-  check_staged(sy, ny, sty.head, yprev, check_sorted, t, f1, f4);
-  // same-points needs x[i] == y[i] for every i; skip once any tile has seen
-  // a mismatch (distinct point sets), otherwise compare against the staged
-  // sources where the index ranges overlap (they do when x == y)
-  if (!BATCH && (c.M == c.N) && *(volatile int*)(flags + 2) == 0) {
-    for (int i = t; i < nx; i += kPlanThreads) {
-      const int64_t gi = ib + i;
-      const int64_t jl = gi - jb;
-      const double yv = (jl >= 0 && jl < ny) ? sy[jl] : __ldg(c.y + gi);
-      f2 |= !(sx[i] == yv);
-    }
-  }
   // merge-path splits in two levels: the segment starts over the whole tile,
   // then every thread's window inside its segment's split range
   const int nsegs_tile = (len + kSeg - 1) / kSeg;
@@ -2316,8 +2265,16 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
   if (t == 0) sib[nsegs_tile] = nx;
   __syncthreads();
   // merge: thread t owns merged positions [kPlanPer t, kPlanPer (t + 1)) and
-  // sets their mask bits (1 = target)
+  // sets their mask bits (1 = target).  The checks ride on the walk: every
+  // consumed value is tested for finiteness and against the previous value
+  // of its set, and (M == N) the stream must alternate source, equal target
+  // (x == y elementwise for sorted sets, transform.cpp:214-216).  The walk
+  // visits every element of the tile exactly once when the windows chain
+  // (each ends where the next starts), which is checked too; a broken chain
+  // reports "unsorted", and the host then re-checks the input element-wise.
   const int d0 = t * kPlanPer;
+  const bool same_chk = !BATCH && c.M == c.N && *(volatile int*)(flags + 2) == 0;
+  int iend = -1, istart = -1;
   if (d0 < len) {
     const int k = d0 / kSeg, D0 = k * kSeg;
     int i;
@@ -2336,30 +2293,55 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
       }
       i = lo;
     }
+    istart = i;
     int j = d0 - i;
     // no index clamps: on sorted input the merge never reads past a set's
     // sentinel; on unsorted input (flagged, redone after the sort) it can
     // run up to kPlanPer past it, into the buffer's padding
     double cx = sx[i];
     double cy = sy[j];
+    double lx = i > 0 ? sx[i - 1] : (t == 0 ? xprev : -INFINITY);
+    double ly = j > 0 ? sy[j - 1] : (t == 0 ? yprev : -INFINITY);
+    double zp = fmax(lx, ly);
     unsigned bits = 0u;
     const int nwin = len - d0 < kPlanPer ? len - d0 : kPlanPer;
 #pragma unroll
     for (int e = 0; e < kPlanPer; ++e) {
-      const bool tgt = !(cy <= cx);  // sources first on ties
-      bits |= (unsigned)tgt << e;
-      if (tgt) {
-        ++i;
-        cx = sx[i];
-      } else {
-        ++j;
-        cy = sy[j];
+      if (e < nwin) {
+        const bool tgt = !(cy <= cx);  // sources first on ties
+        const double z = tgt ? cx : cy;
+        const bool fin = isfinite(z);
+        if (tgt) {
+          f0 |= !fin;
+          f3 |= z < lx;
+          lx = z;
+          ++i;
+          cx = sx[i];
+        } else {
+          f1 |= !fin;
+          f4 |= z < ly;
+          ly = z;
+          ++j;
+          cy = sy[j];
+        }
+        if (same_chk) f2 |= (tgt != ((e + d0) & 1)) | (tgt && z != zp);
+        zp = z;
+        bits |= (unsigned)tgt << e;
       }
     }
-    bits &= (nwin >= 32 ? 0xffffffffu : ((1u << nwin) - 1u));
+    if (!check_sorted) f3 = f4 = 0;
+    iend = i;
     const int sh = d0 & 31;
     atomicOr(&smask[d0 >> 5], bits << sh);
     if (sh + kPlanPer > 32) atomicOr(&smask[(d0 >> 5) + 1], bits >> (32 - sh));
+  }
+  // chain check: every window starts where the previous one ended, and the
+  // last one ends at the tile's end (then the walk covered every element)
+  swin[t] = istart;
+  __syncthreads();
+  if (d0 < len) {
+    const bool last = d0 + kPlanPer >= len;
+    if (last ? iend != nx : iend != swin[t + 1]) f3 = 1;
   }
   __syncthreads();
   for (int w = t; w < nsegs_tile * (kSeg / 32); w += kPlanThreads)
