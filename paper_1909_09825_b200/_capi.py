@@ -69,6 +69,9 @@ SIGNATURES = {
     "fgt_direct": (_I, [_PD, _I64, _PD, _I64, _PD, _D, _PI64, _I64, _PD]),
     "fgt_uniform_points_device": (_I, [_VP, _I64, _U64, _U64, _U64, _VP]),
     "fgt_sort_device": (_I, [_VP, _I64, _VP, _VP, _VP]),
+    "fgt_gather_device": (_I, [_VP, _VP, _I64, _VP, _VP]),
+    "fgt_scatter_device": (_I, [_VP, _VP, _I64, _VP, _VP]),
+    "fgt_merge_runs_device": (_I, [_VP, _PI64, _I, _VP, _VP, _VP]),
     "fgt_batch_create": (_I, [_I, _PD, _PI64, _PD, _PI64, _PD, _PD, _PD, _PD, _PD, _PU8, _I, _I,
                               _U32, _I, _VP, _PVP]),
     "fgt_launch_counter": (ctypes.c_longlong, []),

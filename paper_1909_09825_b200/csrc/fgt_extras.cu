@@ -6,12 +6,14 @@
 //   fgt_sort_device       <- sort_with_perm (transform.cpp:27-39)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <string>
 #include <vector>
 
 #include "../../include/fgt1d_b200.h"
 #include "fgt_device.cuh"
+#include "fgt_scan.cuh"
 #include "fgt_sort.cuh"
 
 using namespace fgt_b200;
@@ -158,6 +160,56 @@ __global__ void uniform_kernel(double* __restrict__ out, int64_t n, uint64_t see
   }
 }
 
+// out[perm[i]] = src[i] (the inverse of launch_gather's out[i] = src[perm[i]]).
+__global__ void scatter_kernel(const double* __restrict__ src, const int32_t* __restrict__ perm,
+                               int64_t n, double* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[__ldg(perm + i)] = __ldg(src + i);
+}
+
+// Stable merge of two sorted runs A (na) and B (nb) with int32 payloads:
+// out[d] for d in [0, na + nb); A's element precedes B's at equal values
+// (A is the earlier run).  Thread t writes kMergePer consecutive outputs
+// from its merge-path split.
+constexpr int kMergePer = 16;
+__global__ void merge2_kernel(const double* __restrict__ av, const int32_t* __restrict__ ai,
+                              int64_t na, const double* __restrict__ bv,
+                              const int32_t* __restrict__ bi, int64_t nb,
+                              double* __restrict__ ov, int32_t* __restrict__ oi) {
+  const int64_t n = na + nb;
+  const int64_t d0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kMergePer;
+  if (d0 >= n) return;
+  int64_t lo = d0 - nb > 0 ? d0 - nb : 0, hi = d0 < na ? d0 : na;
+  while (lo < hi) {  // i = number of A elements among the first d0 outputs
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (av[mid - 1] <= bv[d0 - mid])
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  int64_t i = lo, j = d0 - lo;
+  const int64_t d1 = d0 + kMergePer < n ? d0 + kMergePer : n;
+  for (int64_t d = d0; d < d1; ++d) {
+    const bool takea = j >= nb || (i < na && av[i] <= bv[j]);
+    if (takea) {
+      ov[d] = av[i];
+      oi[d] = ai[i];
+      ++i;
+    } else {
+      ov[d] = bv[j];
+      oi[d] = bi[j];
+      ++j;
+    }
+  }
+}
+
+__global__ void iota_kernel(int32_t* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)i;
+}
+
 // FP64 pipe probe: 8 independent DFMA chains per thread, fully unrolled.
 __global__ void __launch_bounds__(256) fp64_probe_kernel(double* out, int iters, double a, double b) {
   double x0 = threadIdx.x * 1e-9, x1 = x0 + 1e-9, x2 = x0 + 2e-9, x3 = x0 + 3e-9;
@@ -302,6 +354,76 @@ int fgt_uniform_points_device(double* out_device, int64_t count, uint64_t seed, 
   uniform_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)cuda_stream>>>(out_device, count, seed,
                                                                          stream, offset);
   CKR(cudaGetLastError(), "uniform kernel");
+  return FGT_OK;
+}
+
+int fgt_gather_device(const double* src, const int32_t* perm, int64_t n, double* out,
+                      void* stream) {
+  if (n <= 0) return FGT_OK;
+  CKR(launch_gather(src, perm, n, out, (cudaStream_t)stream), "gather");
+  return FGT_OK;
+}
+
+int fgt_scatter_device(const double* src, const int32_t* perm, int64_t n, double* out,
+                       void* stream) {
+  if (n <= 0) return FGT_OK;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  note_launch();
+  scatter_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(src, perm, n, out);
+  CKR(cudaGetLastError(), "scatter");
+  return FGT_OK;
+}
+
+// Stable merge of G sorted runs v[off[r] .. off[r+1]) (host offsets) by a
+// tree of pairwise merge-path merges: merged values and the permutation
+// (merged[i] == v[perm[i]]), ties in run order -- the order a stable sort of
+// the concatenation gives.
+int fgt_merge_runs_device(const double* v, const int64_t* off, int G, double* merged,
+                          int32_t* perm, void* stream) {
+  if (G < 1) {
+    g_err = std::string("merge needs at least one run");
+    return FGT_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = off[G];
+  if (n <= 0) return FGT_OK;
+  std::vector<int64_t> o(off, off + G + 1);
+  double* bufv[2] = {nullptr, nullptr};
+  int32_t* bufi[2] = {nullptr, nullptr};
+  for (int b = 0; b < 2; ++b) {
+    CKR(cudaMallocAsync(reinterpret_cast<void**>(&bufv[b]), sizeof(double) * n, st), "merge ws");
+    CKR(cudaMallocAsync(reinterpret_cast<void**>(&bufi[b]), sizeof(int32_t) * n, st), "merge ws");
+  }
+  CKR(cudaMemcpyAsync(bufv[0], v, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
+  note_launch();
+  iota_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(bufi[0], n);
+  int cur = 0;
+  while (o.size() > 2) {
+    std::vector<int64_t> no{0};
+    for (size_t r = 0; r + 1 < o.size(); r += 2) {
+      const int64_t a0 = o[r], a1 = o[r + 1];
+      const int64_t b1 = r + 2 < o.size() ? o[r + 2] : a1;
+      const int64_t tot = b1 - a0;
+      if (tot > 0) {
+        const int64_t threads = (tot + kMergePer - 1) / kMergePer;
+        note_launch();
+        merge2_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, st>>>(
+            bufv[cur] + a0, bufi[cur] + a0, a1 - a0, bufv[cur] + a1, bufi[cur] + a1, b1 - a1,
+            bufv[cur ^ 1] + a0, bufi[cur ^ 1] + a0);
+      }
+      no.push_back(b1);
+    }
+    o.swap(no);
+    cur ^= 1;
+  }
+  CKR(cudaMemcpyAsync(merged, bufv[cur], sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "copy");
+  CKR(cudaMemcpyAsync(perm, bufi[cur], sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st), "copy");
+  for (int b = 0; b < 2; ++b) {
+    cudaFreeAsync(bufv[b], st);
+    cudaFreeAsync(bufi[b], st);
+  }
+  CKR(cudaGetLastError(), "merge");
   return FGT_OK;
 }
 

@@ -59,3 +59,55 @@ def test_sharded_transform_on_device(world):
     u = np.concatenate([res[r] for r in range(world)])
     ref = oracle.transform(x, y, a, delta, ne=ne, mode=0)
     assert np.max(np.abs(u - ref)) <= 1e-12 * np.sum(np.abs(a))
+
+
+def test_device_permutation_helpers():
+    # fgt_gather_device / fgt_scatter_device / fgt_merge_runs_device (the
+    # sharded path's device data movement) against numpy
+    from paper_1909_09825_b200.sharded import DeviceOps
+    from paper_1909_09825_b200.transform import uniform_points_array as up
+    ops = DeviceOps("cuda:0")
+    rng = np.random.default_rng(4)
+    v = up(100_003, 31, 0)
+    perm = rng.permutation(v.size).astype(np.int32)
+    vd, pd = torch.from_numpy(v).cuda(), torch.from_numpy(perm).cuda()
+    assert np.array_equal(ops.gather(vd, pd).cpu().numpy(), v[perm])
+    sc = np.empty_like(v)
+    sc[perm] = v
+    assert np.array_equal(ops.scatter(vd, pd).cpu().numpy(), sc)
+    for counts in ([5, 0, 17, 100_000], [100_003], [0, 0, 3, 0, 100_000], [1] * 7 + [99_996]):
+        runs, o = [], 0
+        for c in counts:
+            r = np.sort(rng.choice(np.round(v[:2000], 3), size=c)) if c else np.empty(0)
+            runs.append(r)
+            o += c
+        cat = np.concatenate(runs)
+        m, p = ops.merge_runs(torch.from_numpy(cat).cuda(), counts)
+        ref_p = np.argsort(cat, kind="stable")  # ties in run order
+        assert np.array_equal(p.cpu().numpy(), ref_p)
+        assert np.array_equal(m.cpu().numpy(), cat[ref_p])
+
+
+@pytest.mark.parametrize("world", [3])
+def test_sharded_transform_unsorted_ragged_three_ranks(world):
+    from paper_1909_09825_b200.transform import uniform_points_array as up
+    n, m, delta, ne = 120001, 90001, 1e-5, 5
+    x, y = up(n, 22, 3), up(m, 22, 0)
+    a = up(m, 22, 1)
+    cuts_x, cuts_y = [1000, 100000], [0, 89000]  # ragged; rank 0 holds no sources
+    shards = [(s_x, s_y, s_a) for s_x, s_y, s_a in
+              zip(np.split(x, cuts_x), np.split(y, cuts_y), np.split(a, cuts_y))]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=worker, args=(r, world, port, shards, delta, ne, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    u = np.concatenate([res[r] for r in range(world)])
+    ref = oracle.transform(x, y, a, delta, ne=ne, mode=0)
+    assert np.max(np.abs(u - ref)) <= 1e-12 * np.sum(np.abs(a))

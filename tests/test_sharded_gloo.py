@@ -28,7 +28,19 @@ class EmulatedOps:
     def sort(self, v):
         vn = v.numpy()
         p = np.argsort(vn, kind="stable")
-        return torch.from_numpy(vn[p].copy()), torch.from_numpy(p.astype(np.int64))
+        return torch.from_numpy(vn[p].copy()), torch.from_numpy(p.astype(np.int32))
+
+    def gather(self, src, perm):
+        return src[perm.long()]
+
+    def scatter(self, src, perm):
+        out = torch.empty(perm.numel(), dtype=torch.float64)
+        out[perm.long()] = src
+        return out
+
+    def merge_runs(self, v, counts):
+        # a stable sort of the concatenated sorted runs is their stable merge
+        return self.sort(v)
 
     def chunk(self, xs, ys, bs, z_prev, has_prev, delta, soe_args, ne, gather_aggs):
         t, mw = oracle.folded_table(2 * ne)
@@ -38,13 +50,14 @@ class EmulatedOps:
         agg = np.zeros(3 * ne, complex)
         for k in range(ne):
             agg[k], agg[ne + k], agg[2 * ne + k] = chunk_aggregate(z, b, zp, s_all[k])
-        flat = np.empty(6 * ne)
-        flat[0::2], flat[1::2] = agg.real, agg.imag
-        allagg, rank = gather_aggs(flat)
+        flat = np.zeros(6 * ne + 1)
+        flat[0:6 * ne:2], flat[1:6 * ne:2] = agg.real, agg.imag
+        allagg, rank = gather_aggs(torch.from_numpy(flat))
+        allagg = np.ascontiguousarray(allagg.numpy()[:, :6 * ne])
+        assert allagg.shape[0] >= 1
         from paper_1909_09825_b200 import _capi
         import ctypes
         PD = ctypes.POINTER(ctypes.c_double)
-        allagg = np.ascontiguousarray(allagg)
         world = allagg.shape[0]
         carries = np.empty(world * 4 * ne)
         _capi.check(_capi.lib().fgt_chunk_carries(allagg.ctypes.data_as(PD), world, ne,
@@ -121,3 +134,39 @@ def test_splitters_are_monotone_and_balanced():
     assert np.allclose(c, [0.25, 0.5, 0.75], atol=2e-3)
     # zero-weight padding is ignored; all-empty gives +inf (everything on rank 0..)
     assert np.all(np.isinf(splitters(np.zeros(8), np.zeros(8), 3)))
+
+
+def nan_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1909_09825_b200 import cf_soe, fold
+    from paper_1909_09825_b200.sharded import sharded_transform
+    from paper_1909_09825_b200.transform import uniform_points_array as up
+    x = torch.from_numpy(up(50, rank, 3))
+    y = torch.from_numpy(up(40, rank, 0))
+    a = torch.from_numpy(up(40, rank, 1))
+    if rank == world - 1:
+        y[7] = float("nan")  # one bad source on one rank only
+    try:
+        sharded_transform(x, y, a, 1e-3, fold(cf_soe(8)), ops=EmulatedOps())
+        q.put((rank, "no error"))
+    except ValueError as e:
+        q.put((rank, str(e)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_non_finite_on_one_rank_raises_on_all(world):
+    # a domain error on one rank must not leave the others
+    # waiting in a collective
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=nan_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=180) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all("source coordinates must be finite" in res[r] for r in range(world)), res
