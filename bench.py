@@ -70,6 +70,10 @@ def parse():
                     help="N=1: run the multi-GPU chunk path (plan_create_chunk, device "
                          "aggregate exchange, finish) instead of one plan: the per-rank "
                          "step of a multi-GPU run at this per-rank size")
+    ap.add_argument("--config", type=int, default=3, choices=[2, 3, 4, 5],
+                    help="BASELINE.json config: 3 (default, the headline line) or the "
+                         "single-GPU runs of cfg 2 (unsorted: sort-bound), 4 (clustered, "
+                         "unsorted) and 5 (4096 batched transforms, one line per tol)")
     ap.add_argument("--check", action="store_true",
                     help="N>1 (or --chunk-path): rank 0 also runs the whole transform as one "
                          "plan and reports max|u_ranks - u_single| / sum|alpha| "
@@ -351,10 +355,41 @@ def merge_split(x, y, diag):
     return lo
 
 
+def run_other_config(args):
+    """--config 2 / 4 / 5: the other BASELINE configs on one GPU with the same
+    timing rules (device-resident inputs > L2, W warm-ups, K timed steps
+    between CUDA events on the launching stream).  One line per config (per
+    tolerance for cfg 5) with the bench keys plus plan / apply breakdown:
+    for the unsorted configs the plan time is the device sort."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import bench_configs as bc
+
+    def emit(txt):
+        d = json.loads(txt)
+        line = {"metric": METRIC, "value": d["value"], "unit": UNIT, "n_gpus": 1,
+                "steps": d["steps"], "warmup": d["warmup"], "ms_per_step": d["ms_per_step"],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (reference counter RNG)",
+                "config": {k: d[k] for k in d if k not in ("value", "steps", "warmup",
+                                                             "ms_per_step", "metric")},
+                "plan_ms": d["plan_ms"], "apply_ms": d["apply_ms"]}
+        print(json.dumps(line), flush=True)
+    bc.EMIT = emit
+    if args.config == 2:
+        bc.cfg2(args.steps, args.warmup)
+    elif args.config == 4:
+        bc.cfg4(args.steps, args.warmup)
+    else:
+        bc.cfg5(args.steps, args.warmup)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.config != 3:
+        run_other_config(args)
         return
     import torch
     import torch.distributed as dist
