@@ -2745,7 +2745,16 @@ __device__ __forceinline__ void mom_pairs(const ModeTable& mt, int k, const doub
 // the CTA combines its warps' aggregates into the block aggregates of K2's
 // top level.  K1-wide segments take the (A, F, G) the wide K1 stored.
 constexpr int kMomCta = kSegWarps * kMomBlock;
-constexpr int kK1Stages = 3;
+#ifndef FGT_K1_STAGES
+#define FGT_K1_STAGES 2
+#endif
+#ifndef FGT_K1B_MINB
+#define FGT_K1B_MINB 5
+#endif
+#ifndef FGT_K1_SMEMRED
+#define FGT_K1_SMEMRED 1
+#endif
+constexpr int kK1Stages = FGT_K1_STAGES;
 constexpr int kK1StageD = kSeg + 4;  // doubles per set and stage
 struct K1Stage {
   double* y;
@@ -2779,12 +2788,13 @@ __device__ __forceinline__ void k1_issue(const StreamArgs& a, const SegGeom& g, 
 }
 
 template <int NM>
-__global__ void __launch_bounds__(kThreads, 4) k1b_kernel(MomScanArgs q,
+__global__ void __launch_bounds__(kThreads, FGT_K1B_MINB) k1b_kernel(MomScanArgs q,
                                                           const ModeTable* __restrict__ mtab) {
   extern __shared__ __align__(16) unsigned char k1b_smem[];
   __shared__ ModeTable mt;
   __shared__ double smom[kSegWarps][kMomBlock][NM];
   __shared__ Pair wagg[kSegWarps][2 * kMaxModes];
+  __shared__ __align__(16) double kred[FGT_K1_SMEMRED ? kSegWarps : 1][32 * 4];
   load_mode_table(mtab, mt);
   const StreamArgs& a = q.a;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -2828,17 +2838,40 @@ __global__ void __launch_bounds__(kThreads, 4) k1b_kernel(MomScanArgs q,
       }
       __syncwarp();  // stage consumed: refill it with segment s + kK1Stages
       if (lane == 0 && s + kK1Stages < s1) k1_issue(a, seg_geom(a, s + kK1Stages), st);
+      if constexpr (FGT_K1_SMEMRED != 0 && NM <= 4) {
+        // transposed reduction: lanes park their partial moments, lane 8n + g
+        // sums lanes 4g .. 4g + 3 of moment n, three shuffles finish the rows
+        double* red = kred[warp];
 #pragma unroll
-      for (int n = 0; n < NM; ++n) {
+        for (int n = 0; n < NM; ++n) red[n * 32 + lane] = M[n];
+        __syncwarp();
+        const int n = lane >> 3, g = lane & 7;
+        double v = 0.0;
+        if (n < NM) {
+          const double2 a0 = *reinterpret_cast<const double2*>(red + n * 32 + 4 * g);
+          const double2 a1 = *reinterpret_cast<const double2*>(red + n * 32 + 4 * g + 2);
+          v = (a0.x + a0.y) + (a1.x + a1.y);
+        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) M[n] += __shfl_xor_sync(0xffffffffu, M[n], o);
-      }
-      if (lane == 0) {
-        double* out = q.mom + s * NM;
+        for (int o = 4; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (n < NM && g == 0) {
+          q.mom[s * NM + n] = v;
+          smom[warp][s - s0][n] = v;
+        }
+        __syncwarp();
+      } else {
 #pragma unroll
         for (int n = 0; n < NM; ++n) {
-          out[n] = M[n];
-          smom[warp][s - s0][n] = M[n];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) M[n] += __shfl_xor_sync(0xffffffffu, M[n], o);
+        }
+        if (lane == 0) {
+          double* out = q.mom + s * NM;
+#pragma unroll
+          for (int n = 0; n < NM; ++n) {
+            out[n] = M[n];
+            smom[warp][s - s0][n] = M[n];
+          }
         }
       }
     }
