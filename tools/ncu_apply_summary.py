@@ -1,13 +1,14 @@
 #!/usr/bin/env python3
-"""Summarise an ncu --set full capture of one apply (tools/profile_round.sh)
-into profiles/r01_apply_ncu.json and profiles/traffic.json (the DRAM traffic
-bench.py reports as roofline.traffic)."""
+"""Summarise an ncu --set full capture of one whole cfg3 step (plan + apply,
+tools/profile_round.sh) into profiles/r02_step_ncu.json and
+profiles/traffic.json (the DRAM traffic bench.py reports as roofline.traffic
+and roofline_step.traffic)."""
 import csv
 import json
 import subprocess
 import sys
 
-rep = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/prof/apply_full.ncu-rep"
+rep = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/prof/step_full.ncu-rep"
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
@@ -34,16 +35,21 @@ for r in rows[2:]:
     d["dram_bytes"] = float(r[ir]) * scale[units[ir]] + float(r[iw]) * scale[units[iw]]
     tot += d["dram_bytes"]
     kern.append(d)
-json.dump({"source": "ncu --set full --clock-control none (tools/profile_round.sh) of one cfg3 apply: "
-                     "N=M=1e8 presorted, delta=1e-3, n_e=6; the launches of K1 narrow, K2 "
-                     "(reduce/top/down), K3 narrow",
-           "kernels": kern, "dram_bytes_per_apply": tot, "algorithmic_bytes_per_apply": 16 * 2e8},
-          open("profiles/r01_apply_ncu.json", "w"), indent=1)
-k3 = [k for k in kern if "seg_main_kernel" in k["kernel"]]
-json.dump({"kernel": "apply = K1 + K2 + K3 (cfg3, N=M=1e8, n_e=6)", "dram_bytes_per_apply": tot,
+apply = [k for k in kern if any(t in k["kernel"] for t in ("k1b", "scan_top", "k2m_down", "k3n"))]
+json.dump({"source": "ncu --set full --clock-control none (tools/profile_round.sh) of one cfg3 step: "
+                     "N=M=1e8 presorted, delta=1e-3, n_e=6; plan (partition, tile pass, mode table) "
+                     "and apply (K1b moments + block aggregates, K2 top, K2m down-sweep with the "
+                     "collapsed carries, K3n collapsed main pass)",
+           "kernels": kern, "dram_bytes_per_step": tot,
+           "dram_bytes_per_apply": sum(k["dram_bytes"] for k in apply),
+           "algorithmic_bytes_per_apply": 16 * 2e8},
+          open("profiles/r02_step_ncu.json", "w"), indent=1)
+k3 = [k for k in kern if "k3n" in k["kernel"]]
+json.dump({"kernel": "cfg3 step (N=M=1e8, n_e=6): plan + apply", "dram_bytes_per_step": tot,
+           "dram_bytes_per_apply": sum(k["dram_bytes"] for k in apply),
            "k3_dram_bytes_per_launch": k3[0]["dram_bytes"] if k3 else None,
-           "source": "profiles/r01_apply_ncu.json (ncu --set full, dram__bytes_read.sum + "
-                     "dram__bytes_write.sum over the apply's launches)"},
+           "source": "profiles/r02_step_ncu.json (ncu --set full, dram__bytes_read.sum + "
+                     "dram__bytes_write.sum over the step's launches)"},
           open("profiles/traffic.json", "w"), indent=1)
 print("traffic GB", tot / 1e9)
 for k in kern:

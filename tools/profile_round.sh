@@ -1,17 +1,19 @@
 #!/usr/bin/env bash
 # Round-end measurement bundle (run on the GPU box; results in gpurun_out/prof):
-#   bench.json      -- bench.py line (cfg 3, 1 GPU)
-#   configs.jsonl   -- cfg 2 / 4 / 5 lines (tools/bench_configs.py)
+#   bench.json      -- bench.py line (cfg 3, 1 GPU), the driver's command
+#   configs.jsonl   -- cfg 2 / 4 / 5 lines (bench.py --config)
 #   launches.csv    -- ncu launch list (gpu__time_duration, --clock-control none) of bench.py
-#   apply_full.ncu-rep -- ncu --set full of one apply (K1, K2, K3) for the summaries / traffic
+#   step_full.ncu-rep -- ncu --set full of one whole cfg3 step (plan + apply kernels)
 set -u
 OUT=gpurun_out/prof
 mkdir -p $OUT
-python bench.py --steps 10 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err
-python tools/bench_configs.py --configs 2,4,5 --steps 10 --warmup 3 > $OUT/configs.jsonl 2> $OUT/configs.err
+python bench.py --gpus 1 --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/bench.err
+for c in 2 4 5; do python bench.py --config $c --steps 10 --warmup 3 >> $OUT/configs.jsonl 2>> $OUT/configs.err; done
+python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-sweep > $OUT/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-sweep > $OUT/ncu_launches.log 2>&1
-ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
-    -k 'regex:ScanArgs|seg_main_kernel|seg_aggregate_kernel' -c 5 -o $OUT/apply_full \
-    python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e --no-sweep > $OUT/ncu_full.log 2>&1
+python tools/prof_driver.py --n 1e8 --reps 1 > $OUT/plain2.log 2>&1 && \
+ncu --set full --import-source on --clock-control none \
+    -k 'regex:partition|plan_tile|store_table|k1b|scan_top|k2m_down|k3n' -c 8 -o $OUT/step_full \
+    python tools/prof_driver.py --n 1e8 --reps 1 > $OUT/ncu_full.log 2>&1
 echo done
