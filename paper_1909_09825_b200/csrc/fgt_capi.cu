@@ -830,7 +830,7 @@ fgt_plan_s* pipe_chunk_plan(const double* dx, int64_t M, const double* dy, int64
     p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
     p->d_seg_z = dmalloc<double2>(p->ntiles, st);
     p->d_seg_deg = dmalloc<int>(p->ntiles, st);
-    p->d_seg_mask = dmalloc<uint32_t>((size_t)p->ntiles * (kSeg / 32), st);
+    p->d_seg_mask = dmalloc<uint32_t>(seg_mask_words(p->ntiles), st);
     p->d_xs = const_cast<double*>(dx);
     p->d_ys = const_cast<double*>(dy);
     p->own_xs = p->own_ys = false;
@@ -1245,7 +1245,7 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
       p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
       p->d_seg_z = dmalloc<double2>(p->ntiles, st);
         p->d_seg_deg = dmalloc<int>(p->ntiles, st);
-      p->d_seg_mask = dmalloc<uint32_t>((size_t)p->ntiles * (kSeg / 32), st);
+      p->d_seg_mask = dmalloc<uint32_t>(seg_mask_words(p->ntiles), st);
       // one read of both sets: checks + (speculative) segment metadata
       plan_tiles(p, xs.dptr, ys.dptr, !(flags & FGT_ASSUME_SORTED), st);
       upload_modes(p, st);

@@ -2076,6 +2076,392 @@ __global__ void __launch_bounds__(kThreads, FGT_K3N_MINB)
   if (lane == 0) bulk_wait_all();
 }
 
+// ------------------------------------------- K3 narrow, CTA chunks (k3c)
+//
+// k3n's arithmetic with the staging lifted from the warp to the CTA.  A CTA
+// of kCW warps takes a chunk of kCW consecutive segments (warp w: segment
+// s0 + w); the chunk's targets, sources and strengths are three contiguous
+// ranges, and so are its merge-mask words, collapsed carries, segment starts
+// and frames, so one thread stages the whole chunk with seven bulk copies
+// (two stages, the chunk after next in flight while one is computed) and
+// writes the chunk's potentials back with one bulk store.  k3n issued five
+// copies and one store per segment through uniform-register waterfalls (a
+// quarter of its instructions); here that is per kCW segments.
+constexpr int kCW = 8;
+constexpr int kCThreads = 32 * kCW;
+constexpr int kChunk = kCW * kSeg;
+constexpr int kCStageXY = kChunk + 16;
+constexpr int kCStageB = kChunk + 12;
+constexpr int kCSu = kChunk + 4;
+// stage header, written by the issuing thread before the copies
+struct K3cHdr {
+  long long ib0, jb0;  // first target / source of the chunk
+  int xo, yo, bo;      // stage slots of x[ib0] (xy), y[jb0] (xy), b[jb0] (bb)
+  int io;              // slot of seg_ib[s0] in the stage's seg_ib copy
+  int nx;              // targets of the chunk
+  int pad[3];
+};
+static_assert(sizeof(K3cHdr) == 48, "k3c header");
+struct K3cStage {
+  double* xy;        // [kCStageXY]
+  double* bb;        // [kCStageB]
+  double* ec;        // [kCW * kEcStride]
+  double2* sz;       // [kCW] (zprev, zlast)
+  long long* ib;     // [kCW + 3] seg_ib[s0 .. s1] as enclosing 16-byte blocks
+  uint32_t* mask;    // [kCW * kSeg / 32]
+  uint2* pre;        // [kCW] per-word target prefix counts (seg_mask_prefix)
+  K3cHdr* hdr;
+  uint64_t* bar;
+};
+constexpr size_t kCStageBytes = sizeof(double) * (kCStageXY + kCStageB + kCW * kEcStride) +
+                                16 * kCW + 8 * (kCW + 4) + 4 * (kCW * kSeg / 32) + 8 * kCW +
+                                sizeof(K3cHdr) + 16;
+static_assert(kCStageBytes % 16 == 0, "k3c stage alignment");
+__device__ __forceinline__ K3cStage k3c_stage(unsigned char* base) {
+  K3cStage p;
+  p.xy = reinterpret_cast<double*>(base);
+  p.bb = p.xy + kCStageXY;
+  p.ec = p.bb + kCStageB;
+  p.sz = reinterpret_cast<double2*>(p.ec + kCW * kEcStride);
+  p.ib = reinterpret_cast<long long*>(p.sz + kCW);
+  p.mask = reinterpret_cast<uint32_t*>(p.ib + kCW + 4);
+  p.pre = reinterpret_cast<uint2*>(p.mask + kCW * kSeg / 32);
+  p.hdr = reinterpret_cast<K3cHdr*>(p.pre + kCW);
+  p.bar = reinterpret_cast<uint64_t*>(p.hdr + 1);
+  return p;
+}
+// per-warp scratch of the moment scan: [NM][32] lane values + NM totals
+template <int NM>
+constexpr size_t k3c_scratch_doubles() {
+  return ((size_t)NM * 32 + NM + 2 + 1) & ~(size_t)1;
+}
+// staged potentials: two chunk buffers when two CTAs still fit an SM
+template <int NM>
+constexpr int k3c_nsu() {
+  return 2 * (2 * kCStageBytes + 2 * sizeof(double) * kCSu +
+              sizeof(double) * kCW * k3c_scratch_doubles<NM>() + 64) <= 225 * 1024
+             ? 2
+             : 1;
+}
+template <int NM>
+constexpr size_t k3c_smem_bytes() {
+  return 2 * kCStageBytes + sizeof(double) * kCSu * k3c_nsu<NM>() +
+         sizeof(double) * kCW * k3c_scratch_doubles<NM>() + 64;
+}
+
+__device__ __forceinline__ void mbar_init_n(uint64_t* bar, unsigned n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Issue of chunk c (segments s0 .. s1) into a stage by one thread; ib0 / ib1
+// = seg_ib[s0] / seg_ib[s1] (prefetched by the caller).
+__device__ __forceinline__ void k3c_issue(const StreamArgs& a, const double* ec, int64_t c,
+                                          int64_t ib0, int64_t ib1, const K3cStage& st) {
+  auto blocks = [](const void* p, size_t nbytes, const void*& src) -> unsigned {
+    const uintptr_t b0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+    const uintptr_t b1 = (reinterpret_cast<uintptr_t>(p) + nbytes + 15) & ~(uintptr_t)15;
+    src = reinterpret_cast<const void*>(b0);
+    return nbytes > 0 ? (unsigned)(b1 - b0) : 0u;
+  };
+  const int64_t s0 = c * kCW;
+  const int64_t s1 = s0 + kCW < a.nseg ? s0 + kCW : a.nseg;
+  const int64_t L = a.M + a.N;
+  const int64_t d0 = s0 * kSeg, d1 = s1 * kSeg < L ? s1 * kSeg : L;
+  const int64_t jb0 = d0 - ib0, jb1 = d1 - ib1;
+  const int nx = (int)(ib1 - ib0), ny = (int)(jb1 - jb0);
+  const void *sx, *sy, *sb, *si;
+  const unsigned bx = blocks(a.xs + ib0, 8u * nx, sx);
+  const unsigned by = blocks(a.ys + jb0, 8u * ny, sy);
+  const unsigned bb = blocks(a.bs + jb0, 8u * ny, sb);
+  const unsigned bi = blocks(a.seg_ib + s0, 8u * (unsigned)(s1 - s0 + 1), si);
+  const unsigned ns = (unsigned)(s1 - s0);
+  K3cHdr h;
+  h.ib0 = ib0;
+  h.jb0 = jb0;
+  h.xo = phase8(a.xs + ib0);
+  const int ys = (h.xo + nx + 1) & ~1;
+  h.yo = ys + phase8(a.ys + jb0);
+  h.bo = phase8(a.bs + jb0);
+  h.io = (int)((reinterpret_cast<uintptr_t>(a.seg_ib + s0) >> 3) & 1);
+  h.nx = nx;
+  *st.hdr = h;
+  fence_proxy_async();  // generic accesses of the stage before the async writes
+  const unsigned bp = (8u * ns + 15u) & ~15u;
+  mbar_expect(st.bar, bx + by + bb + bi + bp + ns * (8u * kEcStride + 16u + 32u));
+  if (bx) bulk_g2s(st.xy, sx, bx, st.bar);
+  if (by) bulk_g2s(st.xy + ys, sy, by, st.bar);
+  if (bb) bulk_g2s(st.bb, sb, bb, st.bar);
+  bulk_g2s(st.ib, si, bi, st.bar);
+  bulk_g2s(st.mask, a.seg_mask + s0 * (kSeg / 32), 32u * ns, st.bar);
+  bulk_g2s(st.ec, ec + s0 * kEcStride, 8u * kEcStride * ns, st.bar);
+  bulk_g2s(st.sz, a.seg_z + s0, 16u * ns, st.bar);
+  bulk_g2s(st.pre, seg_mask_prefix(a.seg_mask, a.nseg) + s0, bp, st.bar);
+}
+
+// CTA layout: kCW compute warps (warp w: segment s0 + w of each chunk) and
+// one producer warp whose elected lane stages the chunks and stores their
+// potentials.  Hand-offs by mbarriers, no CTA-wide barrier in the loop:
+//   full[k]  : chunk data landed in stage k (TMA transaction bytes)
+//   empty[k] : all compute warps are done reading stage k (kCW arrivals)
+//   sfull[j] : all compute warps staged their potentials in su[j]
+//   sfree[j] : the bulk store of su[j] has read it (producer arrival)
+// With a permutation or wide segments in the plan each warp writes its own
+// targets back from a private region of su instead.
+#ifndef FGT_K3C_MINB
+#define FGT_K3C_MINB 2
+#endif
+template <int DN>
+__global__ void __launch_bounds__(kCThreads + 32, FGT_K3C_MINB)
+    k3c_kernel(StreamArgs a, const double* __restrict__ ec, const CollConsts cc, OutArgs o) {
+  constexpr int NM = DN + 1;
+  constexpr int NSU = k3c_nsu<NM>();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* const su0 = reinterpret_cast<double*>(smem_raw + 2 * kCStageBytes);
+  double* const scr0 = su0 + (size_t)kCSu * NSU;
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(scr0 + (size_t)kCW * k3c_scratch_doubles<NM>());
+  uint64_t* const empty = bars;        // [2]
+  uint64_t* const sfull = bars + 2;    // [NSU]
+  uint64_t* const sfree = bars + 4;    // [NSU]
+  double* const zero = reinterpret_cast<double*>(bars + 6);
+  const int64_t nchunk = (a.nseg + kCW - 1) / kCW;
+  const int64_t L = a.M + a.N;
+  const bool all_narrow = a.nwide3 == 0;
+  const bool bulk_out = all_narrow && !o.tperm;
+  if (threadIdx.x == 0) {
+    mbar_init(k3c_stage(smem_raw).bar);
+    mbar_init(k3c_stage(smem_raw + kCStageBytes).bar);
+    for (int i = 0; i < 2; ++i) mbar_init_n(empty + i, kCW);
+    for (int j = 0; j < NSU; ++j) {
+      mbar_init_n(sfull + j, kCW);
+      mbar_init_n(sfree + j, 1);
+    }
+    zero[0] = 0.0;
+  }
+  __syncthreads();
+  if (warp == kCW) {
+    // ---------------- producer
+    if (lane != 0) return;
+    auto chunk_ib = [&](int64_t c, int64_t& i0, int64_t& i1) {
+      const int64_t s0 = c * kCW;
+      const int64_t s1 = s0 + kCW < a.nseg ? s0 + kCW : a.nseg;
+      i0 = __ldg(a.seg_ib + s0);
+      i1 = __ldg(a.seg_ib + s1);
+    };
+    // (first target, target count) of the chunk in each stage
+    int64_t gib[2] = {0, 0};
+    int gnx[2] = {0, 0};
+    for (int i = 0; i < 2; ++i) {
+      const int64_t c = blockIdx.x + (int64_t)i * gridDim.x;
+      if (c < nchunk) {
+        int64_t i0, i1;
+        chunk_ib(c, i0, i1);
+        k3c_issue(a, ec, c, i0, i1, k3c_stage(smem_raw + i * kCStageBytes));
+        gib[i] = i0;
+        gnx[i] = (int)(i1 - i0);
+      }
+    }
+    int64_t nib0 = 0, nib1 = 0;
+    if (blockIdx.x + 2 * (int64_t)gridDim.x < nchunk)
+      chunk_ib(blockIdx.x + 2 * (int64_t)gridDim.x, nib0, nib1);
+    int it = 0;
+    for (int64_t c = blockIdx.x; c < nchunk; c += gridDim.x, ++it) {
+      const int k = it & 1;
+      const int64_t ib0 = k ? gib[1] : gib[0];
+      const int nx = k ? gnx[1] : gnx[0];
+      const int64_t c2 = c + 2 * (int64_t)gridDim.x;
+      if (c2 < nchunk) {
+        mbar_wait(empty + k, (unsigned)(it >> 1) & 1u);
+        k3c_issue(a, ec, c2, nib0, nib1, k3c_stage(smem_raw + k * kCStageBytes));
+        if (k) {
+          gib[1] = nib0;
+          gnx[1] = (int)(nib1 - nib0);
+        } else {
+          gib[0] = nib0;
+          gnx[0] = (int)(nib1 - nib0);
+        }
+        if (c2 + gridDim.x < nchunk) chunk_ib(c2 + gridDim.x, nib0, nib1);
+      }
+      if (bulk_out) {
+        const int j = NSU == 2 ? k : 0;
+        double* const su = su0 + (size_t)j * kCSu;
+        mbar_wait(sfull + j, (unsigned)(it / NSU) & 1u);
+        double* const up = o.u + o.u_offset + ib0;
+        const int uoff = (int)((reinterpret_cast<uintptr_t>(up) >> 3) & 1);
+        const int cnt = (nx - uoff) & ~1;
+        fence_proxy_async();  // the compute warps' stores to su before the async read
+        if (cnt > 0) bulk_s2g(up + uoff, su + 2 * uoff, 8u * (unsigned)cnt);
+        if (uoff && nx > 0) up[0] = su[1];
+        if (uoff + cnt < nx) up[nx - 1] = su[nx - 1 + uoff];
+        bulk_wait_read();
+        mbar_arrive(sfree + j);
+      }
+    }
+    bulk_wait_all();
+    return;
+  }
+  // ---------------- compute warps
+  K3nStage sp;  // the moment scan's scratch (k3n layout)
+  sp.su = nullptr;
+  sp.scan = scr0 + (size_t)warp * k3c_scratch_doubles<NM>();
+  sp.tot = sp.scan + NM * 32;
+  sp.zero = zero;
+  const unsigned az = smem_u32(zero);
+  double Hr[NM][NM], Br[NM][NM];
+#pragma unroll
+  for (int m = 0; m < NM; ++m)
+#pragma unroll
+    for (int q = 0; q < NM; ++q) {
+      Hr[m][q] = (m + q < NM && ((m + q) & 1)) ? in_reg(cc.H[m][q]) : 0.0;
+      Br[q][m] = (m + q < NM) ? in_reg(cc.B[q][m]) : 0.0;
+    }
+  int it = 0;
+  for (int64_t c = blockIdx.x; c < nchunk; c += gridDim.x, ++it) {
+    const int k = it & 1;
+    const K3cStage st = k3c_stage(smem_raw + k * kCStageBytes);
+    mbar_wait(st.bar, (unsigned)(it >> 1) & 1u);
+    const K3cHdr h = *st.hdr;
+    const int64_t s = c * kCW + warp;
+    // this warp's segment from the staged starts and frames
+    bool live = s < a.nseg;
+    int nx = 0, ny = 0, len = 0, lx = 0, ly = 0;
+    double zc = 0.0;
+    if (live) {
+      const int64_t ib = st.ib[h.io + warp], ie = st.ib[h.io + warp + 1];
+      const int64_t d0 = s * kSeg;
+      len = (int)(d0 + kSeg < L ? kSeg : L - d0);
+      nx = (int)(ie - ib);
+      ny = len - nx;
+      lx = (int)(ib - h.ib0);
+      ly = (int)(d0 - ib - h.jb0);
+      const double2 z = st.sz[warp];
+      SegGeom g;
+      g.zprev = s == 0 ? a.zprev0 : z.x;
+      g.zlast = z.y;
+      zc = seg_frame(g).zc;
+      if (!all_narrow) live = k3_narrow(seg_deg_DM(__ldg(a.seg_deg + s)));
+    }
+    double w[kR], L8[kR], cq[NM];
+    unsigned byte = 0;
+    int i0 = 0;
+    if (live) {
+      const int xo = h.xo + lx, yo = h.yo + ly, bo = h.bo + ly;
+      if (len < kSeg) {
+        // partial (last) segment: lanes past the end decode as strength-0
+        // sources at the centre (their mask bits are 0)
+        for (int q = lane; q < kSeg - len + 8; q += 32) {
+          st.xy[yo + ny + q] = zc;
+          st.bb[bo + ny + q] = 0.0;
+        }
+        fence_proxy_async();  // before the stage is refilled by the async proxy
+        __syncwarp();
+      }
+      const uint32_t word = st.mask[warp * (kSeg / 32) + (lane >> 2)];
+      const unsigned sh = (lane & 3) * 8;
+      byte = (word >> sh) & 0xffu;
+      // targets before this lane's run: the word prefix (plan-time) + the
+      // lower bytes of its own word
+      const uint2 pw = st.pre[warp];
+      const unsigned pq = lane & 16 ? pw.y : pw.x;
+      i0 = (int)((pq >> ((lane & 12) * 2)) & 0xffu) + __popc(word & ((1u << sh) - 1u));
+      const int j0 = lane * kR - i0;
+      unsigned ax = smem_u32(st.xy + xo + i0);
+      unsigned ay = smem_u32(st.xy + yo + j0);
+      unsigned ab = smem_u32(st.bb + bo + j0);
+      double lp[NM];
+#pragma unroll
+      for (int m = 0; m < NM; ++m) lp[m] = 0.0;
+#pragma unroll
+      for (int e = 0; e < kR; ++e) {
+        const unsigned tg = (byte >> e) & 1u;
+        const double we = lds_f64(tg ? ax : ay) - zc;
+        double p = lds_f64(tg ? az : ab);
+        ax += tg << 3;
+        ay += (tg ^ 1u) << 3;
+        ab += (tg ^ 1u) << 3;
+        lp[0] += p;
+#pragma unroll
+        for (int m = 1; m < NM; ++m) {
+          p *= we;
+          lp[m] += p;
+        }
+        double acc = 0.0;
+#pragma unroll
+        for (int q = DN; q >= 0; --q) {
+          double c2 = 0.0;
+          bool any = false;
+#pragma unroll
+          for (int m = 0; m + q < NM; ++m)
+            if ((m + q) & 1) {
+              c2 = any ? fma(Hr[m][q], lp[m], c2) : Hr[m][q] * lp[m];
+              any = true;
+            }
+          acc = q == DN ? c2 : fma(acc, we, c2);
+        }
+        w[e] = we;
+        L8[e] = acc;
+      }
+      double ecq[NM];
+#pragma unroll
+      for (int q = 0; q < NM; ++q) ecq[q] = st.ec[warp * kEcStride + q];
+      double pre[NM], tot[NM];
+      warp_moment_scan<NM>(sp, lane, lp, pre, tot);
+#pragma unroll
+      for (int q = 0; q < NM; ++q) {
+        double acc = ecq[q];
+#pragma unroll
+        for (int m = 0; m + q < NM; ++m) acc = fma(Br[q][m], tot[m], acc);
+#pragma unroll
+        for (int m = 0; m + q < NM; ++m)
+          if ((m + q) & 1) acc = fma(Hr[m][q], pre[m], acc);
+        cq[q] = acc;
+      }
+    }
+    // the stage is consumed
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + k);
+    const int j = NSU == 2 ? k : 0;
+    double* const su = su0 + (size_t)j * kCSu;
+    int base;
+    if (bulk_out) {
+      // chunk slots (aligned like u); wait for the store that last read su[j]
+      if (it >= NSU) mbar_wait(sfree + j, (unsigned)(it / NSU - 1) & 1u);
+      base = (int)((reinterpret_cast<uintptr_t>(o.u + o.u_offset + h.ib0) >> 3) & 1) + lx;
+    } else {
+      base = warp * kSeg;  // private region
+    }
+    if (live) {
+      unsigned at = smem_u32(su + base + i0);
+      const unsigned adis = smem_u32(su + kChunk + 2);  // discard slot of non-targets
+#pragma unroll
+      for (int e = 0; e < kR; ++e) {
+        double acc = cq[DN];
+#pragma unroll
+        for (int q = DN - 1; q >= 0; --q) acc = fma(acc, w[e], cq[q]);
+        const unsigned tg = (byte >> e) & 1u;
+        sts_f64(tg ? at : adis, acc + L8[e]);
+        at += tg << 3;
+      }
+    }
+    __syncwarp();
+    if (bulk_out) {
+      if (lane == 0) mbar_arrive(sfull + j);
+    } else if (live) {
+      const int64_t t0 = o.u_offset + h.ib0 + lx;
+      if (o.tperm) {
+        const int32_t* tp = o.tperm + t0;
+        for (int i = lane; i < nx; i += 32) o.u[tp[i]] = su[base + i];
+      } else {
+        for (int i = lane; i < nx; i += 32) o.u[t0 + i] = su[base + i];
+      }
+      __syncwarp();
+    }
+  }
+}
+
 // Collapsed carries of the narrow segments (after K2): per segment, the
 // segment carries at the frame centre Tf_k = e^{-s_k h0} Cf_k, Tb_k =
 // e^{-s_k h1} Cb_k folded into E^c_q = Re sum_k mw_k c_kq (Tf_k + (-1)^q Tb_k),
@@ -2346,6 +2732,20 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
   __syncthreads();
   for (int w = t; w < nsegs_tile * (kSeg / 32); w += kPlanThreads)
     seg_mask[c.seg0 * (kSeg / 32) + w] = smask[w];
+  if (!BATCH && t < nsegs_tile) {
+    // per-word target prefix counts of the segment (byte q: targets in
+    // words 0 .. q-1), read by k3c in place of a warp scan
+    unsigned pre = 0, lo = 0, hi = 0;
+#pragma unroll
+    for (int q = 0; q < kSeg / 32; ++q) {
+      if (q < 4)
+        lo |= pre << (8 * q);
+      else
+        hi |= pre << (8 * (q - 4));
+      pre += __popc(smask[t * (kSeg / 32) + q]);
+    }
+    seg_mask_prefix(seg_mask, nseg)[c.seg0 + t] = make_uint2(lo, hi);
+  }
   if (t < nsegs_tile) {
     const int k = t;
     const int i0 = sib[k], i1 = sib[k + 1];
@@ -3366,9 +3766,31 @@ cudaError_t launch_chunk_carries(const cplx* aggs, int n_chunks, int ne, int ran
   return cudaGetLastError();
 }
 
+#ifndef FGT_K3_CHUNKED
+#define FGT_K3_CHUNKED 1
+#endif
+template <int DN>
+static cudaError_t launch_k3c_dn(const StreamArgs& a, const TileState& ts, const CollConsts& cc,
+                                 OutArgs o, cudaStream_t st) {
+  static std::atomic<unsigned long long> done{0};
+  const size_t smem = k3c_smem_bytes<DN + 1>();
+  cudaError_t e = ensure_dynamic_smem(k3c_kernel<DN>, (int)smem, done);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3c_kernel<DN>, kCThreads + 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t want = (a.nseg + kCW - 1) / kCW;
+  const int64_t cap = (int64_t)num_sms() * per_sm;
+  note_launch();
+  k3c_kernel<DN><<<(unsigned)(want < cap ? want : cap), kCThreads + 32, smem, st>>>(a, ts.ec, cc, o);
+  return cudaGetLastError();
+}
+
 template <int DN>
 static cudaError_t launch_k3n_dn(const StreamArgs& a, const TileState& ts, const CollConsts& cc,
                                  OutArgs o, cudaStream_t st) {
+  if (FGT_K3_CHUNKED) return launch_k3c_dn<DN>(a, ts, cc, o, st);
   static std::atomic<unsigned long long> done{0};
   const size_t smem = (size_t)kSegWarps * kK3nWarpBytes;
   cudaError_t e = ensure_dynamic_smem(k3n_kernel<DN>, (int)smem, done);

@@ -71,7 +71,8 @@ struct StreamArgs {
   int64_t nseg;
   double zprev0;  // coordinate of the element before this chunk (or its first)
   // plan-time segment metadata (seg_meta): (zprev, zlast) per segment and
-  // the merged order as one bit per element (1 = target), 8 words/segment
+  // the merged order as one bit per element (1 = target), 8 words/segment;
+  // single plans append per-segment word prefix counts (seg_mask_prefix)
   const double2* seg_z;
   const uint32_t* seg_mask;
   // batched transforms (nullptr for a single stream): per segment
@@ -96,6 +97,20 @@ struct StreamArgs {
   // unknown -> kMomMax moments)
   int dm_narrow = -1;
 };
+
+// Single plans: seg_mask holds kSeg / 32 words per segment followed by one
+// uint2 per segment whose byte q counts the targets in words 0 .. q-1 (plan
+// tile pass); seg_mask_words sizes that allocation (+ one padding entry).
+constexpr int kSegMaskWords = kSeg / 32;
+__host__ __device__ inline size_t seg_mask_words(int64_t nseg) {
+  return (size_t)nseg * kSegMaskWords + 2 * (size_t)nseg + 4;
+}
+__host__ __device__ inline uint2* seg_mask_prefix(uint32_t* seg_mask, int64_t nseg) {
+  return reinterpret_cast<uint2*>(seg_mask + (size_t)nseg * kSegMaskWords);
+}
+__host__ __device__ inline const uint2* seg_mask_prefix(const uint32_t* seg_mask, int64_t nseg) {
+  return reinterpret_cast<const uint2*>(seg_mask + (size_t)nseg * kSegMaskWords);
+}
 
 struct OutArgs {
   double* u = nullptr;             // potentials (original target order if tperm)
