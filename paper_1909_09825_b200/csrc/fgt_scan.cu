@@ -3357,6 +3357,307 @@ __global__ void __launch_bounds__(kThreads, FGT_K1B_MINB) k1b_kernel(MomScanArgs
   }
 }
 
+// K1c: K1b with CTA-level staging (k3c's scheme).  A CTA takes scan blocks of
+// kMomCta segments; each block is walked in chunks of kCW consecutive
+// segments (compute warp w: segment s0 + w), whose sources and strengths are
+// one contiguous range each: a producer warp stages a chunk (y, beta,
+// segment starts and frames: four bulk copies) into one of two stages while
+// the compute warps reduce the previous one to segment moments.  A warp's
+// element loop runs only over its segment's sources (warp-uniform trip
+// count), not over all kSeg merged slots.  Phase 2 (per-mode block
+// aggregates from the moments, one segment per lane) is K1b's.
+constexpr int kK1cStageD = kChunk + 8;  // doubles per set and stage
+struct K1cHdr {
+  long long jb0;
+  int yo, bo, io;
+  int pad[3];
+};
+struct K1cStage {
+  double* y;
+  double* b;
+  double2* sz;
+  long long* ib;
+  K1cHdr* hdr;
+  uint64_t* bar;
+};
+constexpr size_t kK1cStageBytes =
+    sizeof(double) * 2 * kK1cStageD + 16 * kCW + 8 * (kCW + 4) + sizeof(K1cHdr) + 16;
+static_assert(kK1cStageBytes % 16 == 0, "k1c stage alignment");
+static_assert(kMomCta % kCW == 0, "k1c: scan blocks are whole chunks");
+__device__ __forceinline__ K1cStage k1c_stage(unsigned char* base) {
+  K1cStage p;
+  p.y = reinterpret_cast<double*>(base);
+  p.b = p.y + kK1cStageD;
+  p.sz = reinterpret_cast<double2*>(p.b + kK1cStageD);
+  p.ib = reinterpret_cast<long long*>(p.sz + kCW);
+  p.hdr = reinterpret_cast<K1cHdr*>(p.ib + kCW + 4);
+  p.bar = reinterpret_cast<uint64_t*>(p.hdr + 1);
+  return p;
+}
+template <int NM>
+constexpr size_t k1c_smem_bytes() {
+  return 2 * kK1cStageBytes + 64;
+}
+
+__device__ __forceinline__ void k1c_issue(const StreamArgs& a, int64_t c, int64_t ib0, int64_t ib1,
+                                          const K1cStage& st) {
+  auto blocks = [](const void* p, size_t nbytes, const void*& src) -> unsigned {
+    const uintptr_t b0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+    const uintptr_t b1 = (reinterpret_cast<uintptr_t>(p) + nbytes + 15) & ~(uintptr_t)15;
+    src = reinterpret_cast<const void*>(b0);
+    return nbytes > 0 ? (unsigned)(b1 - b0) : 0u;
+  };
+  const int64_t s0 = c * kCW;
+  const int64_t s1 = s0 + kCW < a.nseg ? s0 + kCW : a.nseg;
+  const int64_t L = a.M + a.N;
+  const int64_t d0 = s0 * kSeg, d1 = s1 * kSeg < L ? s1 * kSeg : L;
+  const int64_t jb0 = d0 - ib0, jb1 = d1 - ib1;
+  const int ny = (int)(jb1 - jb0);
+  const void *sy, *sb, *si;
+  const unsigned by = blocks(a.ys + jb0, 8u * ny, sy);
+  const unsigned bb = blocks(a.bs + jb0, 8u * ny, sb);
+  const unsigned bi = blocks(a.seg_ib + s0, 8u * (unsigned)(s1 - s0 + 1), si);
+  const unsigned ns = (unsigned)(s1 - s0);
+  K1cHdr h;
+  h.jb0 = jb0;
+  h.yo = phase8(a.ys + jb0);
+  h.bo = phase8(a.bs + jb0);
+  h.io = (int)((reinterpret_cast<uintptr_t>(a.seg_ib + s0) >> 3) & 1);
+  *st.hdr = h;
+  fence_proxy_async();
+  mbar_expect(st.bar, by + bb + bi + 16u * ns);
+  if (by) bulk_g2s(st.y, sy, by, st.bar);
+  if (bb) bulk_g2s(st.b, sb, bb, st.bar);
+  bulk_g2s(st.ib, si, bi, st.bar);
+  bulk_g2s(st.sz, a.seg_z + s0, 16u * ns, st.bar);
+}
+
+__device__ __forceinline__ void bar_compute(unsigned nthreads) {
+  asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
+}
+
+template <int NM>
+__global__ void __launch_bounds__(kCThreads + 32, 2) k1c_kernel(MomScanArgs q,
+                                                          const ModeTable* __restrict__ mtab) {
+  extern __shared__ __align__(16) unsigned char k1c_smem[];
+  __shared__ ModeTable mt;
+  __shared__ double smom[kMomCta][NM];
+  __shared__ double2 sh01[kMomCta];  // (h0, h1) of the block's segments
+  __shared__ Pair wagg[kCW][2 * kMaxModes];
+  __shared__ __align__(16) double kred[kCW][32 * 4];
+  load_mode_table(mtab, mt);
+  const StreamArgs& a = q.a;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ne = q.ne;
+  constexpr int64_t kCPB = kMomCta / kCW;  // chunks per scan block
+  uint64_t* const empty = reinterpret_cast<uint64_t*>(k1c_smem + 2 * kK1cStageBytes);
+  if (threadIdx.x == 0) {
+    mbar_init(k1c_stage(k1c_smem).bar);
+    mbar_init(k1c_stage(k1c_smem + kK1cStageBytes).bar);
+    mbar_init_n(empty, kCW);
+    mbar_init_n(empty + 1, kCW);
+  }
+  __syncthreads();
+  const int64_t nchunk = (a.nseg + kCW - 1) / kCW;
+  // the CTA's chunk sequence: blocks blockIdx.x, + gridDim.x, ..., kCPB
+  // chunks each, up to the last chunk of the stream
+  auto chunk_of = [&](int64_t it) -> int64_t {
+    const int64_t b = blockIdx.x + (it / kCPB) * (int64_t)gridDim.x;
+    return b * kCPB + it % kCPB;
+  };
+  if (warp == kCW) {
+    if (lane != 0) return;
+    auto chunk_ib = [&](int64_t c, int64_t& i0, int64_t& i1) {
+      const int64_t s0 = c * kCW;
+      const int64_t s1 = s0 + kCW < a.nseg ? s0 + kCW : a.nseg;
+      i0 = __ldg(a.seg_ib + s0);
+      i1 = __ldg(a.seg_ib + s1);
+    };
+    for (int i = 0; i < 2; ++i) {
+      const int64_t c = chunk_of(i);
+      if (c < nchunk) {
+        int64_t i0, i1;
+        chunk_ib(c, i0, i1);
+        k1c_issue(a, c, i0, i1, k1c_stage(k1c_smem + i * kK1cStageBytes));
+      }
+    }
+    int64_t nib0 = 0, nib1 = 0;
+    if (chunk_of(2) < nchunk) chunk_ib(chunk_of(2), nib0, nib1);
+    for (int64_t it = 0;; ++it) {
+      const int64_t c2 = chunk_of(it + 2);
+      if (c2 >= nchunk) break;
+      const int k = (int)(it & 1);
+      mbar_wait(empty + k, (unsigned)(it >> 1) & 1u);
+      k1c_issue(a, c2, nib0, nib1, k1c_stage(k1c_smem + k * kK1cStageBytes));
+      const int64_t c3 = chunk_of(it + 3);
+      if (c3 < nchunk) chunk_ib(c3, nib0, nib1);
+    }
+    return;
+  }
+  const bool all1 = a.nwide1 == 0;
+  const int64_t L = a.M + a.N;
+  int64_t it = 0;
+  for (int64_t b = blockIdx.x; b < q.nblk; b += gridDim.x) {
+    // ---- phase 1: moments of the block's segments, chunk by chunk
+    for (int64_t ci = 0; ci < kCPB; ++ci, ++it) {
+      const int64_t c = b * kCPB + ci;
+      if (c >= nchunk) break;  // only at the end of the stream
+      const int k = (int)(it & 1);
+      const K1cStage st = k1c_stage(k1c_smem + k * kK1cStageBytes);
+      mbar_wait(st.bar, (unsigned)(it >> 1) & 1u);
+      const int64_t s = c * kCW + warp;
+      double M[NM];
+#pragma unroll
+      for (int n = 0; n < NM; ++n) M[n] = 0.0;
+      const bool live = s < a.nseg;
+      if (live) {
+        const K1cHdr h = *st.hdr;
+        const int64_t ib = st.ib[h.io + warp], ie = st.ib[h.io + warp + 1];
+        const int64_t d0 = s * kSeg;
+        const int len = (int)(d0 + kSeg < L ? kSeg : L - d0);
+        const int ny = len - (int)(ie - ib);
+        const int ly = (int)(d0 - ib - h.jb0);
+        const double2 z = st.sz[warp];
+        SegGeom g;
+        g.zprev = s == 0 ? a.zprev0 : z.x;
+        g.zlast = z.y;
+        const SegFrame f = seg_frame(g);
+        const double zc = f.zc;
+        if (lane == 0) sh01[s - b * kMomCta] = make_double2(f.h0, f.h1);
+        const double* yy = st.y + h.yo + ly;
+        const double* bb = st.b + h.bo + ly;
+        // two warp-uniform halves of kSeg / 64 source slots per lane (a
+        // segment holds about kSeg / 2 sources); no branch inside a half
+        auto half = [&](int u0) {
+          double d[kSeg / 64], p[kSeg / 64];
+#pragma unroll
+          for (int u = 0; u < kSeg / 64; ++u) {
+            const int j = lane + 32 * (u0 + u);
+            const bool in = j < ny;
+            d[u] = in ? yy[j] - zc : 0.0;
+            p[u] = in ? bb[j] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < kSeg / 64; ++u) {
+            double q = p[u];
+            M[0] += q;
+#pragma unroll
+            for (int n = 1; n < NM; ++n) {
+              q *= d[u];
+              M[n] += q;
+            }
+          }
+        };
+        half(0);
+        if (ny > kSeg / 2) half(kSeg / 64);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + k);  // stage consumed
+      const int sl = (int)(s - b * kMomCta);  // slot in the block
+      if constexpr (NM <= 4) {
+        double* red = kred[warp];
+#pragma unroll
+        for (int n = 0; n < NM; ++n) red[n * 32 + lane] = M[n];
+        __syncwarp();
+        const int n = lane >> 3, g = lane & 7;
+        double v = 0.0;
+        if (n < NM) {
+          const double2 a0 = *reinterpret_cast<const double2*>(red + n * 32 + 4 * g);
+          const double2 a1 = *reinterpret_cast<const double2*>(red + n * 32 + 4 * g + 2);
+          v = (a0.x + a0.y) + (a1.x + a1.y);
+        }
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (live && n < NM && g == 0) {
+          q.mom[s * NM + n] = v;
+          smom[sl][n] = v;
+        }
+        __syncwarp();
+      } else {
+#pragma unroll
+        for (int n = 0; n < NM; ++n) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) M[n] += __shfl_xor_sync(0xffffffffu, M[n], o);
+        }
+        if (live && lane < NM) {
+          double v = M[0];
+#pragma unroll
+          for (int n = 1; n < NM; ++n)
+            if (lane == n) v = M[n];
+          q.mom[s * NM + lane] = v;
+          smom[sl][lane] = v;
+        }
+      }
+    }
+    bar_compute(kCThreads);
+    // ---- phase 2: per-warp aggregates per mode, lane l holding segment
+    // b kMomCta + 32 w + l; ordered warp reductions
+    {
+      const int64_t sg = b * kMomCta + 32 * warp + lane;
+      const bool lv = sg < a.nseg;
+      bool n1 = false;
+      double h0 = 0.0, h1 = 0.0;
+      if (lv) {
+        n1 = all1 || k1_narrow(seg_deg_DM(__ldg(a.seg_deg + sg)));
+        const double2 hh = sh01[32 * warp + lane];
+        h0 = hh.x;
+        h1 = hh.y;
+      }
+      double Mm[NM];
+#pragma unroll
+      for (int n = 0; n < NM; ++n) Mm[n] = lv ? smom[32 * warp + lane][n] : 0.0;
+      for (int k = 0; k < ne; ++k) {
+        cplx A, F, G;
+        if (!lv) {
+          A = {1.0, 0.0};
+          F = G = {0.0, 0.0};
+        } else if (n1) {
+          cplx E0, E1;
+          mom_pairs<NM>(mt, k, Mm, h0, h1, A, F, G, E0, E1);
+        } else {
+          const int64_t o = (int64_t)k * a.nseg + sg;
+          A = q.ts.A[o];
+          F = q.ts.F[o];
+          G = q.ts.G[o];
+        }
+        Pair fw{A, F}, bw{A, G};
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          Pair of, ob;
+          of.a.re = __shfl_xor_sync(0xffffffffu, fw.a.re, off);
+          of.a.im = __shfl_xor_sync(0xffffffffu, fw.a.im, off);
+          of.s.re = __shfl_xor_sync(0xffffffffu, fw.s.re, off);
+          of.s.im = __shfl_xor_sync(0xffffffffu, fw.s.im, off);
+          ob.a.re = __shfl_xor_sync(0xffffffffu, bw.a.re, off);
+          ob.a.im = __shfl_xor_sync(0xffffffffu, bw.a.im, off);
+          ob.s.re = __shfl_xor_sync(0xffffffffu, bw.s.re, off);
+          ob.s.im = __shfl_xor_sync(0xffffffffu, bw.s.im, off);
+          const bool lower = (lane & off) == 0;
+          fw = lower ? combine(fw, of) : combine(of, fw);
+          bw = lower ? combine(ob, bw) : combine(bw, ob);
+        }
+        if (lane == 0) {
+          wagg[warp][k] = fw;
+          wagg[warp][ne + k] = bw;
+        }
+      }
+    }
+    bar_compute(kCThreads);
+    if (threadIdx.x < 2 * ne) {
+      const bool bwd = (int)threadIdx.x >= ne;
+      Pair acc{{1.0, 0.0}, {0.0, 0.0}};
+      for (int w = 0; w < kCW; ++w) {
+        const int ww = bwd ? kCW - 1 - w : w;
+        if (b * kMomCta + (int64_t)ww * 32 < a.nseg) acc = combine(acc, wagg[ww][threadIdx.x]);
+      }
+      cplx* out = q.blkagg + ((int64_t)threadIdx.x * q.nblk + (bwd ? q.nblk - 1 - b : b)) * 2;
+      out[0] = acc.a;
+      out[1] = acc.s;
+    }
+    bar_compute(kCThreads);
+  }
+}
+
 // K2m down-sweep, one CTA per scan block (kMomBlock segments per warp, two
 // per lane: s0 + 2l, s0 + 2l + 1).  Per mode: exclusive warp scans of the
 // lane pairs (forward by shfl_up, backward by shfl_down), the warps' totals
@@ -3769,6 +4070,9 @@ cudaError_t launch_chunk_carries(const cplx* aggs, int n_chunks, int ne, int ran
 #ifndef FGT_K3_CHUNKED
 #define FGT_K3_CHUNKED 1
 #endif
+#ifndef FGT_K1_CHUNKED
+#define FGT_K1_CHUNKED 1
+#endif
 template <int DN>
 static cudaError_t launch_k3c_dn(const StreamArgs& a, const TileState& ts, const CollConsts& cc,
                                  OutArgs o, cudaStream_t st) {
@@ -3892,13 +4196,26 @@ template <int NM>
 static cudaError_t launch_mom_nm(const MomScanArgs& q, const ModeTable* mt, bool reduce, bool down,
                                  const ScanArgs& sa, const cplx* carry_in, cplx* totals,
                                  cudaStream_t st) {
-  const size_t smem = (size_t)kSegWarps * kK1WarpBytes;
-  static std::atomic<unsigned long long> done{0};
-  cudaError_t e = ensure_dynamic_smem(k1b_kernel<NM>, (int)smem, done);
-  if (e != cudaSuccess) return e;
   const unsigned grid = (unsigned)q.nblk;
   note_launch(1 + (reduce ? 1 : 0) + (down ? 1 : 0));
-  if (reduce) k1b_kernel<NM><<<grid, kThreads, smem, st>>>(q, mt);
+  if (reduce && FGT_K1_CHUNKED) {
+    const size_t smem = k1c_smem_bytes<NM>();
+    static std::atomic<unsigned long long> done{0};
+    cudaError_t e = ensure_dynamic_smem(k1c_kernel<NM>, (int)smem, done);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1c_kernel<NM>, kCThreads + 32, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    const int64_t cap = (int64_t)num_sms() * per_sm;
+    k1c_kernel<NM><<<(unsigned)(q.nblk < cap ? q.nblk : cap), kCThreads + 32, smem, st>>>(q, mt);
+  } else if (reduce) {
+    const size_t smem = (size_t)kSegWarps * kK1WarpBytes;
+    static std::atomic<unsigned long long> done{0};
+    cudaError_t e = ensure_dynamic_smem(k1b_kernel<NM>, (int)smem, done);
+    if (e != cudaSuccess) return e;
+    k1b_kernel<NM><<<grid, kThreads, smem, st>>>(q, mt);
+  }
   scan_top_kernel<<<2 * q.ne, 1024, 0, st>>>(sa, carry_in, totals);
   if (down) k2m_down_kernel<NM><<<grid, kThreads, 0, st>>>(q, mt);
   return cudaGetLastError();
