@@ -74,6 +74,11 @@ def parse():
                     help="BASELINE.json config: 3 (default, the headline line) or the "
                          "single-GPU runs of cfg 2 (unsorted: sort-bound), 4 (clustered, "
                          "unsorted) and 5 (4096 batched transforms, one line per tol)")
+    ap.add_argument("--cfg5-transforms", type=int, default=4096,
+                    help="--config 5: number of transforms B (BASELINE: 4096)")
+    ap.add_argument("--cfg5-size", type=int, default=65536,
+                    help="--config 5: targets = sources per transform (BASELINE: 65536)")
+    ap.add_argument("--tols", default="1e-3,1e-6,1e-10", help="--config 5 tolerances")
     ap.add_argument("--check", action="store_true",
                     help="N>1 (or --chunk-path): rank 0 also runs the whole transform as one "
                          "plan and reports max|u_ranks - u_single| / sum|alpha| "
@@ -366,13 +371,16 @@ def run_other_config(args):
 
     def emit(txt):
         d = json.loads(txt)
-        line = {"metric": METRIC, "value": d["value"], "unit": UNIT, "n_gpus": 1,
+        line = {"metric": METRIC, "value": d["value"], "unit": UNIT, "n_gpus": d.get("n_gpus", 1),
                 "steps": d["steps"], "warmup": d["warmup"], "ms_per_step": d["ms_per_step"],
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (reference counter RNG)",
                 "config": {k: d[k] for k in d if k not in ("value", "steps", "warmup",
-                                                             "ms_per_step", "metric")},
+                                                             "ms_per_step", "metric", "n_gpus",
+                                                             "multi_rank_check")},
                 "plan_ms": d["plan_ms"], "apply_ms": d["apply_ms"]}
+        if "multi_rank_check" in d:
+            line["multi_rank_check"] = d["multi_rank_check"]
         print(json.dumps(line), flush=True)
     bc.EMIT = emit
     if args.config == 2:
@@ -380,7 +388,8 @@ def run_other_config(args):
     elif args.config == 4:
         bc.cfg4(args.steps, args.warmup)
     else:
-        bc.cfg5(args.steps, args.warmup)
+        bc.cfg5(args.steps, args.warmup, B=args.cfg5_transforms, n=args.cfg5_size,
+                tols=tuple(float(t) for t in args.tols.split(",")), check=args.check)
 
 
 def main():

@@ -57,3 +57,25 @@ def test_bench_chunk_path_single_rank():
     d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
     assert d["parallelism"] == "1 GPU (chunk path)"
     assert d["multi_rank_check"]["pass"], d["multi_rank_check"]
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_bench_cfg5_transforms_split_over_ranks(world):
+    """--config 5 under torchrun: the batched transforms split over the ranks
+    (no exchange), every rank's potentials checked against one batched plan
+    over all transforms on rank 0."""
+    if _capi.lib().fgt_device_count() < 1:
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+    env = dict(os.environ, FGT_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={world}", "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           "bench.py", "--config", "5", "--gpus", str(world), "--steps", "2", "--warmup", "1",
+           "--cfg5-transforms", "12", "--cfg5-size", "5000", "--tols", "1e-6", "--check"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == world
+    assert d["config"]["transforms"] == 12
+    assert d["multi_rank_check"]["pass"], d["multi_rank_check"]

@@ -11,7 +11,8 @@ partition, segment metadata) + apply + destroy.
         unsorted, alpha ~ U[0,1), delta=1e-6, tol 1e-8 -> n_e=5  (1 GPU; the
         8-GPU partition needs 8 GPUs)
   cfg5: 4096 transforms of N=M=65536, presorted uniform, alpha=2u-1,
-        delta_b log-uniform in [1e-6, 1e-1] (stream 9), tol in {1e-3, 1e-6, 1e-10}
+        delta_b log-uniform in [1e-6, 1e-1] (stream 9), tol in {1e-3, 1e-6, 1e-10};
+        under torchrun the transforms are split over the ranks
 
 Prints one JSON line per config.
 """
@@ -34,7 +35,8 @@ from paper_1909_09825_b200.transform import uniform_points_array as up  # noqa: 
 PD = ctypes.POINTER(ctypes.c_double)
 PI64 = ctypes.POINTER(ctypes.c_int64)
 L = _capi.lib()
-dev = torch.device("cuda", 0)
+dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count()))
+torch.cuda.set_device(dev)
 stream = torch.cuda.current_stream()
 sh = ctypes.c_void_p(stream.cuda_stream)
 
@@ -143,39 +145,92 @@ def cfg4(steps, warmup):
                   {"data": "16-component mixture sigma 1e-3, unsorted, alpha U[0,1)"})
 
 
-def cfg5(steps, warmup, B=4096, n=65536, fixed_delta=None, tols=(1e-3, 1e-6, 1e-10)):
+class Ranks:
+    """Process group of a multi-GPU cfg 5 run (torchrun): ranks take equal
+    contiguous ranges of the B transforms (independent problems, no exchange),
+    timed between a barrier and CUDA events, max over ranks."""
+
+    def __init__(self):
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.dist = None
+        self.backend = os.environ.get("FGT_BENCH_BACKEND", "nccl")
+        if self.world > 1:
+            import torch.distributed as dist
+            if not dist.is_initialized():
+                if self.backend == "nccl":
+                    dist.init_process_group("nccl", device_id=dev)
+                else:
+                    dist.init_process_group(self.backend)
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist is not None:
+            if self.backend == "nccl":
+                self.dist.barrier(device_ids=[dev.index])
+            else:
+                self.dist.barrier()
+
+    def max(self, v):
+        if self.dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64,
+                         device=dev if self.backend == "nccl" else "cpu")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather(self, t):
+        """all_gather of equal-size device tensors -> list on rank 0 (cpu)."""
+        if self.dist is None:
+            return [t.cpu()]
+        src = t if self.backend == "nccl" else t.cpu()
+        parts = [torch.empty_like(src) for _ in range(self.world)]
+        self.dist.all_gather(parts, src)
+        return [p.cpu() for p in parts]
+
+
+def cfg5(steps, warmup, B=4096, n=65536, fixed_delta=None, tols=(1e-3, 1e-6, 1e-10),
+         check=False):
+    """BASELINE cfg 5: B transforms of N = M = n.  Under torchrun the
+    transforms are split over the ranks (rank r: transforms
+    [r B / G, (r + 1) B / G), the same data as on one GPU)."""
+    rk = Ranks()
+    b0, b1 = B * rk.rank // rk.world, B * (rk.rank + 1) // rk.world
+    Bl = b1 - b0
     # per transform b: seed b, sorted uniform targets / sources, alpha = 2u-1
-    x = torch.empty(B, n, dtype=torch.float64, device=dev)
-    y = torch.empty(B, n, dtype=torch.float64, device=dev)
-    a = torch.empty(B, n, dtype=torch.float64, device=dev)
-    for b in range(B):
-        _capi.check(L.fgt_uniform_points_device(x[b].data_ptr(), n, b, 3, 0, sh))
-        _capi.check(L.fgt_uniform_points_device(y[b].data_ptr(), n, b, 0, 0, sh))
-        _capi.check(L.fgt_uniform_points_device(a[b].data_ptr(), n, b, 1, 0, sh))
+    x = torch.empty(Bl, n, dtype=torch.float64, device=dev)
+    y = torch.empty(Bl, n, dtype=torch.float64, device=dev)
+    a = torch.empty(Bl, n, dtype=torch.float64, device=dev)
+    for i in range(Bl):
+        b = b0 + i
+        _capi.check(L.fgt_uniform_points_device(x[i].data_ptr(), n, b, 3, 0, sh))
+        _capi.check(L.fgt_uniform_points_device(y[i].data_ptr(), n, b, 0, 0, sh))
+        _capi.check(L.fgt_uniform_points_device(a[i].data_ptr(), n, b, 1, 0, sh))
     x = torch.sort(x, dim=1).values.contiguous()
     y = torch.sort(y, dim=1).values.contiguous()
     a.mul_(2.0).sub_(1.0)
-    deltas = 10.0 ** (-6.0 + 5.0 * up(B, 0, 9))
+    deltas_all = 10.0 ** (-6.0 + 5.0 * up(B, 0, 9))
     dlabel = "log-uniform [1e-6, 1e-1] (stream 9)"
     if fixed_delta is not None:
-        deltas = np.full(B, fixed_delta)
+        deltas_all = np.full(B, fixed_delta)
         dlabel = "all %g" % fixed_delta
-    off = np.arange(B + 1, dtype=np.int64) * n
-    u = torch.empty(B * n, dtype=torch.float64, device=dev)
+    deltas = np.ascontiguousarray(deltas_all[b0:b1])
+    off = np.arange(Bl + 1, dtype=np.int64) * n
+    u = torch.empty(Bl * n, dtype=torch.float64, device=dev)
     fl = _capi.FGT_DEVICE_PTRS | _capi.FGT_BORROW
     for tol in tols:
         keep, sp = soe_args(tol)
 
         def plan():
             hh = ctypes.c_void_p()
-            _capi.check(L.fgt_batch_create(B, ctypes.cast(x.data_ptr(), PD), off.ctypes.data_as(PI64),
+            _capi.check(L.fgt_batch_create(Bl, ctypes.cast(x.data_ptr(), PD), off.ctypes.data_as(PI64),
                                            ctypes.cast(y.data_ptr(), PD), off.ctypes.data_as(PI64),
-                                           deltas.ctypes.data_as(PD), *sp, fl, 0, sh,
+                                           deltas.ctypes.data_as(PD), *sp, fl, dev.index, sh,
                                            ctypes.byref(hh)))
             return hh
 
         def apply(hh):
-            _capi.check(L.fgt_apply_general(hh, ctypes.cast(a.data_ptr(), PD), B * n,
+            _capi.check(L.fgt_apply_general(hh, ctypes.cast(a.data_ptr(), PD), Bl * n,
                                             ctypes.cast(u.data_ptr(), PD), 1, fl, sh))
 
         def step():
@@ -183,18 +238,66 @@ def cfg5(steps, warmup, B=4096, n=65536, fixed_delta=None, tols=(1e-3, 1e-6, 1e-
             apply(hh)
             L.fgt_plan_destroy(hh)
 
-        ms = timed(step, steps, warmup)
+        def ranked(fn):
+            for _ in range(warmup):
+                fn()
+            torch.cuda.synchronize()
+            rk.barrier()
+            ms = timed(fn, steps, 0)
+            rk.barrier()
+            return rk.max(ms)
+
+        ms = ranked(step)
         hh = plan()
-        ms_apply = timed(lambda: apply(hh), steps, warmup)
+        ms_apply = ranked(lambda: apply(hh))
         kms = kernel_ms(lambda: apply(hh))
         L.fgt_plan_destroy(hh)
+        extra = {}
+        if check:
+            # every rank's potentials vs one plan over all B transforms (rank 0)
+            step()
+            torch.cuda.synchronize()
+            parts = rk.gather(u)
+            if rk.rank == 0:
+                xs = torch.empty(B, n, dtype=torch.float64, device=dev)
+                ys = torch.empty(B, n, dtype=torch.float64, device=dev)
+                al = torch.empty(B, n, dtype=torch.float64, device=dev)
+                for b in range(B):
+                    _capi.check(L.fgt_uniform_points_device(xs[b].data_ptr(), n, b, 3, 0, sh))
+                    _capi.check(L.fgt_uniform_points_device(ys[b].data_ptr(), n, b, 0, 0, sh))
+                    _capi.check(L.fgt_uniform_points_device(al[b].data_ptr(), n, b, 1, 0, sh))
+                xs = torch.sort(xs, dim=1).values.contiguous()
+                ys = torch.sort(ys, dim=1).values.contiguous()
+                al.mul_(2.0).sub_(1.0)
+                offa = np.arange(B + 1, dtype=np.int64) * n
+                ua = torch.empty(B * n, dtype=torch.float64, device=dev)
+                hh = ctypes.c_void_p()
+                _capi.check(L.fgt_batch_create(B, ctypes.cast(xs.data_ptr(), PD),
+                                               offa.ctypes.data_as(PI64),
+                                               ctypes.cast(ys.data_ptr(), PD),
+                                               offa.ctypes.data_as(PI64),
+                                               deltas_all.ctypes.data_as(PD), *sp, fl, dev.index,
+                                               sh, ctypes.byref(hh)))
+                _capi.check(L.fgt_apply_general(hh, ctypes.cast(al.data_ptr(), PD), B * n,
+                                                ctypes.cast(ua.data_ptr(), PD), 1, fl, sh))
+                L.fgt_plan_destroy(hh)
+                torch.cuda.synchronize()
+                ur = torch.cat(parts)
+                err = float((ur - ua.cpu()).abs().max() / al.abs().sum(dim=1).max().cpu())
+                extra["multi_rank_check"] = {
+                    "max_abs_diff_over_sum_abs_alpha_b": err, "pass": err <= 1e-12,
+                    "reference": "one batched plan over all B transforms on rank 0's GPU"}
         pts = 2.0 * B * n
-        EMIT(json.dumps({"config": "cfg5", "metric": "(M+N) points/s", "value": pts / (ms / 1e3),
-                          "ms_per_step": ms, "apply_ms": ms_apply,
-                          "apply_value": pts / (ms_apply / 1e3), "plan_ms": ms - ms_apply,
-                          "transforms": B, "M_each": n, "N_each": n, "tol": tol,
-                          "n_e": len(keep[0]), "kernels_ms": kms, "deltas": dlabel,
-                          "steps": steps, "warmup": warmup}))
+        if rk.rank == 0:
+            EMIT(json.dumps({"config": "cfg5", "metric": "(M+N) points/s", "value": pts / (ms / 1e3),
+                              "ms_per_step": ms, "apply_ms": ms_apply,
+                              "apply_value": pts / (ms_apply / 1e3), "plan_ms": ms - ms_apply,
+                              "transforms": B, "M_each": n, "N_each": n, "tol": tol,
+                              "n_e": len(keep[0]), "kernels_ms": kms, "deltas": dlabel,
+                              "n_gpus": rk.world,
+                              "parallelism": (f"transforms split over {rk.world} GPUs"
+                                              if rk.world > 1 else "1 GPU"),
+                              "steps": steps, "warmup": warmup, **extra}))
 
 
 if __name__ == "__main__":
