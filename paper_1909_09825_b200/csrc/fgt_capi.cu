@@ -630,11 +630,12 @@ void run_apply(fgt_plan_s* p, const double* strengths, double* potentials, uint3
       }
       {
         ProfScope ps(1, st);
-        ck(launch_mom_scan(sa, p->P.ne, p->d_mt, ts, mom, nullptr, nullptr, st), "carry scan");
+        ck(launch_mom_scan(sa, p->P.ne, p->d_mt, ts, mom, nullptr, nullptr, st, true, true, &p->cc),
+           "carry scan");
       }
       {
         ProfScope ps(2, st);
-        ck(launch_main(sa, p->P, p->d_mt, ts, o, st, &p->cc, true), "main pass");
+        ck(launch_main(sa, p->P, p->d_mt, ts, o, st, &p->cc, true, k3_folds(sa)), "main pass");
       }
     } else {
       {
@@ -737,14 +738,15 @@ void run_chunk_finish(fgt_plan_s* p, const double* strengths, const cplx* carry_
   {
     ProfScope ps(1, st);
     // phase 1's block aggregates are still in the tile state: top + down only
-    ck(launch_mom_scan(sa, ne, p->d_mt, ts, p->cs.mom, d_cin, nullptr, st, false), "carry scan");
+    ck(launch_mom_scan(sa, ne, p->d_mt, ts, p->cs.mom, d_cin, nullptr, st, false, true, &p->cc),
+       "carry scan");
   }
   OutArgs o;
   o.u = u;
   o.tperm = p->d_tperm;
   {
     ProfScope ps(2, st);
-    ck(launch_main(sa, p->P, p->d_mt, ts, o, st, &p->cc, true), "main pass");
+    ck(launch_main(sa, p->P, p->d_mt, ts, o, st, &p->cc, true, k3_folds(sa)), "main pass");
   }
   note_use(p, st);
   if (!dev) {

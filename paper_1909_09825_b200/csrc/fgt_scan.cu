@@ -2213,7 +2213,7 @@ __device__ __forceinline__ void k3c_issue(const StreamArgs& a, const double* ec,
 #ifndef FGT_K3C_MINB
 #define FGT_K3C_MINB 2
 #endif
-template <int DN>
+template <int DN, bool FOLD>
 __global__ void __launch_bounds__(kCThreads + 32, FGT_K3C_MINB)
     k3c_kernel(StreamArgs a, const double* __restrict__ ec, const CollConsts cc, OutArgs o) {
   constexpr int NM = DN + 1;
@@ -2316,7 +2316,7 @@ __global__ void __launch_bounds__(kCThreads + 32, FGT_K3C_MINB)
 #pragma unroll
     for (int q = 0; q < NM; ++q) {
       Hr[m][q] = (m + q < NM && ((m + q) & 1)) ? in_reg(cc.H[m][q]) : 0.0;
-      Br[q][m] = (m + q < NM) ? in_reg(cc.B[q][m]) : 0.0;
+      Br[q][m] = (!FOLD && m + q < NM) ? in_reg(cc.B[q][m]) : 0.0;
     }
   int it = 0;
   for (int64_t c = blockIdx.x; c < nchunk; c += gridDim.x, ++it) {
@@ -2412,8 +2412,10 @@ __global__ void __launch_bounds__(kCThreads + 32, FGT_K3C_MINB)
 #pragma unroll
       for (int q = 0; q < NM; ++q) {
         double acc = ecq[q];
+        if constexpr (!FOLD) {
 #pragma unroll
-        for (int m = 0; m + q < NM; ++m) acc = fma(Br[q][m], tot[m], acc);
+          for (int m = 0; m + q < NM; ++m) acc = fma(Br[q][m], tot[m], acc);
+        }
 #pragma unroll
         for (int m = 0; m + q < NM; ++m)
           if ((m + q) & 1) acc = fma(Hr[m][q], pre[m], acc);
@@ -3093,6 +3095,10 @@ struct MomScanArgs {
   int64_t nblk;
   cplx* blkagg;    // [2ne][nblk] pairs (backward blocks stored right to left)
   cplx* blkcarry;  // [2ne][nblk]
+  // K2m also folds the segment-total terms sum_m B[q][m] Tot_m of the
+  // collapsed form into E^c (k3_folds: the moments reach degree dn)
+  int fold = 0;
+  CollConsts cc;
 };
 
 __device__ __forceinline__ bool mom_n1(const StreamArgs& a, int DM) {
@@ -3688,10 +3694,14 @@ __global__ void __launch_bounds__(kThreads) k2m_down_kernel(MomScanArgs q,
 #pragma unroll
     for (int n = 0; n < NM; ++n) M[i][n] = 0.0;
     if (live[i]) {
-      const int DM = seg_deg_DM(__ldg(a.seg_deg + sg[i]));
+      const int DM = a.nwide1 == 0 && a.nwide3 == 0 ? 0 : seg_deg_DM(__ldg(a.seg_deg + sg[i]));
       n1[i] = mom_n1(a, DM);
       n3[i] = mom_n3(a, DM);
-      const SegFrame f = seg_frame(seg_geom(a, sg[i]));
+      const double2 z = __ldg(a.seg_z + sg[i]);
+      SegGeom g;
+      g.zprev = sg[i] == 0 ? a.zprev0 : z.x;
+      g.zlast = z.y;
+      const SegFrame f = seg_frame(g);
       h0[i] = f.h0;
       h1[i] = f.h1;
       if (n1[i]) {
@@ -3791,6 +3801,16 @@ __global__ void __launch_bounds__(kThreads) k2m_down_kernel(MomScanArgs q,
         q.ts.Cb[o] = cb[i];
       }
     }
+  }
+  if (q.fold) {
+    // E_q += sum_m B[q][m] Tot_m (Tot = the segment's source moments)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int n = 0; n <= kCollMax; ++n)
+#pragma unroll
+        for (int m = 0; m < NM; ++m)
+          if (n + m <= kCollMax && n + m <= q.dn) E[i][n] = fma(q.cc.B[n][m], M[i][m], E[i][n]);
   }
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
@@ -4073,28 +4093,36 @@ cudaError_t launch_chunk_carries(const cplx* aggs, int n_chunks, int ne, int ran
 #ifndef FGT_K1_CHUNKED
 #define FGT_K1_CHUNKED 1
 #endif
-template <int DN>
-static cudaError_t launch_k3c_dn(const StreamArgs& a, const TileState& ts, const CollConsts& cc,
-                                 OutArgs o, cudaStream_t st) {
+template <int DN, bool FOLD>
+static cudaError_t launch_k3c_dnf(const StreamArgs& a, const TileState& ts, const CollConsts& cc,
+                                  OutArgs o, cudaStream_t st) {
   static std::atomic<unsigned long long> done{0};
   const size_t smem = k3c_smem_bytes<DN + 1>();
-  cudaError_t e = ensure_dynamic_smem(k3c_kernel<DN>, (int)smem, done);
+  cudaError_t e = ensure_dynamic_smem(k3c_kernel<DN, FOLD>, (int)smem, done);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3c_kernel<DN>, kCThreads + 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3c_kernel<DN, FOLD>, kCThreads + 32,
+                                                    smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const int64_t want = (a.nseg + kCW - 1) / kCW;
   const int64_t cap = (int64_t)num_sms() * per_sm;
   note_launch();
-  k3c_kernel<DN><<<(unsigned)(want < cap ? want : cap), kCThreads + 32, smem, st>>>(a, ts.ec, cc, o);
+  k3c_kernel<DN, FOLD><<<(unsigned)(want < cap ? want : cap), kCThreads + 32, smem, st>>>(a, ts.ec,
+                                                                                         cc, o);
   return cudaGetLastError();
+}
+template <int DN>
+static cudaError_t launch_k3c_dn(const StreamArgs& a, const TileState& ts, const CollConsts& cc,
+                                 OutArgs o, cudaStream_t st, bool folded) {
+  return folded ? launch_k3c_dnf<DN, true>(a, ts, cc, o, st)
+                : launch_k3c_dnf<DN, false>(a, ts, cc, o, st);
 }
 
 template <int DN>
 static cudaError_t launch_k3n_dn(const StreamArgs& a, const TileState& ts, const CollConsts& cc,
-                                 OutArgs o, cudaStream_t st) {
-  if (FGT_K3_CHUNKED) return launch_k3c_dn<DN>(a, ts, cc, o, st);
+                                 OutArgs o, cudaStream_t st, bool folded) {
+  if (FGT_K3_CHUNKED || folded) return launch_k3c_dn<DN>(a, ts, cc, o, st, folded);
   static std::atomic<unsigned long long> done{0};
   const size_t smem = (size_t)kSegWarps * kK3nWarpBytes;
   cudaError_t e = ensure_dynamic_smem(k3n_kernel<DN>, (int)smem, done);
@@ -4114,9 +4142,11 @@ int k3n_degree(const StreamArgs& a) {
   return a.dn_narrow >= 0 ? (a.dn_narrow < kCollMax ? a.dn_narrow : kCollMax) : kCollMax;
 }
 
+bool k3_folds(const StreamArgs& a) { return k3n_degree(a) + 1 <= k1m_moments(a); }
+
 cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                         TileState ts, OutArgs o, cudaStream_t st, const CollConsts* cc,
-                        bool ec_ready) {
+                        bool ec_ready, bool folded) {
   if (!cc || a.mtb || a.nseg == 0) return launch_seg_main<false>(a, P, mt, ts, o, st);
   // single plan: wide segments on the per-segment kernel, narrow ones on the
   // collapsed kernel at the plan's highest narrow degree
@@ -4131,13 +4161,13 @@ cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTabl
     collapse_carries_kernel<<<(unsigned)((a.nseg + 255) / 256), 256, 0, st>>>(a, mt, P.ne, ts, DN);
   }
   switch (DN) {
-    case 0: return launch_k3n_dn<0>(a, ts, *cc, o, st);
-    case 1: return launch_k3n_dn<1>(a, ts, *cc, o, st);
-    case 2: return launch_k3n_dn<2>(a, ts, *cc, o, st);
-    case 3: return launch_k3n_dn<3>(a, ts, *cc, o, st);
-    case 4: return launch_k3n_dn<4>(a, ts, *cc, o, st);
-    case 5: return launch_k3n_dn<5>(a, ts, *cc, o, st);
-    default: return launch_k3n_dn<6>(a, ts, *cc, o, st);
+    case 0: return launch_k3n_dn<0>(a, ts, *cc, o, st, folded);
+    case 1: return launch_k3n_dn<1>(a, ts, *cc, o, st, folded);
+    case 2: return launch_k3n_dn<2>(a, ts, *cc, o, st, folded);
+    case 3: return launch_k3n_dn<3>(a, ts, *cc, o, st, folded);
+    case 4: return launch_k3n_dn<4>(a, ts, *cc, o, st, folded);
+    case 5: return launch_k3n_dn<5>(a, ts, *cc, o, st, folded);
+    default: return launch_k3n_dn<6>(a, ts, *cc, o, st, folded);
   }
 }
 
@@ -4223,7 +4253,7 @@ static cudaError_t launch_mom_nm(const MomScanArgs& q, const ModeTable* mt, bool
 
 cudaError_t launch_mom_scan(const StreamArgs& a, int ne, const ModeTable* mt, const TileState& ts,
                             double* mom, const cplx* carry_in, cplx* totals, cudaStream_t st,
-                            bool reduce, bool down) {
+                            bool reduce, bool down, const CollConsts* cc) {
   if (a.nseg == 0) return cudaSuccess;
   const int64_t nblk = mom_scan_blocks(a.nseg);
   MomScanArgs q;
@@ -4236,6 +4266,10 @@ cudaError_t launch_mom_scan(const StreamArgs& a, int ne, const ModeTable* mt, co
   q.nblk = nblk;
   q.blkagg = ts.blk;
   q.blkcarry = ts.blk + (size_t)nblk * 2 * ne * 2;
+  if (cc && k3_folds(a)) {
+    q.fold = 1;
+    q.cc = *cc;
+  }
   const ScanArgs sa{ts.A, ts.F, ts.G, ts.Cf, ts.Cb, a.nseg, ne, nblk, q.blkagg, q.blkcarry};
   switch (q.nm) {
 #define FGT_MNM(n)                                                 \

@@ -202,9 +202,11 @@ cudaError_t launch_chunk_carries(const cplx* aggs, int n_chunks, int ne, int ran
                                  cudaStream_t st);
 // K3.  cc: the plan's collapsed-form constants (single plans); nullptr runs
 // the per-segment-degree narrow kernel (batched plans, per-transform tables).
+// folded: ts.ec already holds the segment-total terms (launch_mom_scan with
+// cc and k3_folds(a)).
 cudaError_t launch_main(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                         TileState ts, OutArgs o, cudaStream_t st, const CollConsts* cc = nullptr,
-                        bool ec_ready = false);
+                        bool ec_ready = false, bool folded = false);
 // Moment path (single plans): K1m writes the narrow segments' source
 // moments (k1m_moments(a) per segment, mom[nseg][..]) and the wide K1 the
 // others' (A, F, G); K2m scans them per mode and direction and writes the
@@ -215,9 +217,13 @@ int k1m_moments(const StreamArgs& a);
 int k3n_degree(const StreamArgs& a);
 cudaError_t launch_moments(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                            TileState ts, double* mom, cudaStream_t st);
+// cc: fold the collapsed form's segment-total terms into E^c when
+// k3_folds(a) (the K1 moments reach the collapsed degree).
+bool k3_folds(const StreamArgs& a);
 cudaError_t launch_mom_scan(const StreamArgs& a, int ne, const ModeTable* mt, const TileState& ts,
                             double* mom, const cplx* carry_in, cplx* totals,
-                            cudaStream_t st, bool reduce = true, bool down = true);
+                            cudaStream_t st, bool reduce = true, bool down = true,
+                            const CollConsts* cc = nullptr);
 cudaError_t launch_mode_sums(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
                              TileState ts, OutArgs o, cudaStream_t st);
 cudaError_t launch_gather(const double* alpha, const int32_t* perm, int64_t n, double* out,
