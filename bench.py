@@ -743,13 +743,13 @@ def main():
                          "traffic": traffic.get("k3_dram_bytes_per_launch"),
                          "traffic_source": "profiles/traffic.json (ncu --set full of K3: "
                                            "dram__bytes_read.sum + dram__bytes_write.sum)",
-                         "kernel": "K3n k3n_kernel (collapsed narrow main pass): one launch per apply",
+                         "kernel": "K3c k3c_kernel (collapsed narrow main pass, CTA-chunked): one launch per apply",
                          "bytes_per_launch": 16.0 * pts_rank, "bytes_per_point": 16,
                          "launch_ms": kavg[2], "peak_source": hbm_src},
             "roofline_apply": {"bound": "hbm", "achieved": achieved_hbm, "peak": hbm_peak,
                                "unit": "GB/s", "frac": achieved_hbm / hbm_peak if achieved_hbm else None,
                                "bytes_per_point": 16,
-                               "kernel": "apply = K1b (moments) + K2 (top, down) + K3n",
+                               "kernel": "apply = K1c (moments) + K2 (top, down) + K3c",
                                "traffic": traffic.get("dram_bytes_per_apply"),
                                "peak_source": hbm_src},
             # the whole step (plan included): 16 B per point over the step time
@@ -769,8 +769,8 @@ def main():
                                      "work": f"SURVEY 8(d) W = n_e(48 + 4M/(M+N)) = {W:.0f} "
                                              "fp64-pipe instr/pt, counted as FMA-2 flops",
                                      "peak_source": "measured on this GPU (fgt_fp64_peak DFMA probe)"},
-            # kind 0: wide-segment K1 (none on cfg 3); kind 1: K1b moments + block
-            # aggregates, K2 top, K2m down-sweep; kind 2: K3n (+ wide K3)
+            # kind 0: wide-segment K1 (none on cfg 3); kind 1: K1c moments + block
+            # aggregates, K2 top, K2m down-sweep; kind 2: K3c (+ wide K3)
             "kernels_ms": {"K1_wide": kavg[0], "K1b_K2_moment_scan": kavg[1], "K3_main": kavg[2],
                            "apply_total": apply_ms, "plan_and_other": ms - apply_ms},
             "apply_value": 2.0 * n / (apply_ms / 1e3) if apply_ms > 0 else None,

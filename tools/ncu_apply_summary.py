@@ -35,16 +35,16 @@ for r in rows[2:]:
     d["dram_bytes"] = float(r[ir]) * scale[units[ir]] + float(r[iw]) * scale[units[iw]]
     tot += d["dram_bytes"]
     kern.append(d)
-apply = [k for k in kern if any(t in k["kernel"] for t in ("k1b", "scan_top", "k2m_down", "k3n"))]
+apply = [k for k in kern if any(t in k["kernel"] for t in ("k1c", "k1b", "scan_top", "k2m_down", "k3c", "k3n"))]
 json.dump({"source": "ncu --set full --clock-control none (tools/profile_round.sh) of one cfg3 step: "
                      "N=M=1e8 presorted, delta=1e-3, n_e=6; plan (partition, tile pass, mode table) "
-                     "and apply (K1b moments + block aggregates, K2 top, K2m down-sweep with the "
-                     "collapsed carries, K3n collapsed main pass)",
+                     "and apply (K1c moments + block aggregates, K2 top, K2m down-sweep with the "
+                     "collapsed carries, K3c collapsed main pass)",
            "kernels": kern, "dram_bytes_per_step": tot,
            "dram_bytes_per_apply": sum(k["dram_bytes"] for k in apply),
            "algorithmic_bytes_per_apply": 16 * 2e8},
           open("profiles/r02_step_ncu.json", "w"), indent=1)
-k3 = [k for k in kern if "k3n" in k["kernel"]]
+k3 = [k for k in kern if "k3c" in k["kernel"] or "k3n" in k["kernel"]]
 json.dump({"kernel": "cfg3 step (N=M=1e8, n_e=6): plan + apply", "dram_bytes_per_step": tot,
            "dram_bytes_per_apply": sum(k["dram_bytes"] for k in apply),
            "k3_dram_bytes_per_launch": k3[0]["dram_bytes"] if k3 else None,
