@@ -128,12 +128,38 @@ __device__ __forceinline__ void gap_factors_rt(const ModeTable& mt, int k, int D
     return;
   }
   const cplx* cf = mt.coef[k];
-  const cplx top = cf[D];
+  if (D == 0) {
 #pragma unroll
-  for (int i = 0; i < kR; ++i) d[i] = top;
+    for (int i = 0; i < kR; ++i) d[i] = cf[0];
+    return;
+  }
+  // first step folded into the initialisation (no register copies), then
+  // two degrees per iteration (half the loop overhead), odd remainder last
+  {
+    const cplx top = cf[D], c = cf[D - 1];
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      d[i].re = fma(top.re, g[i], c.re);
+      d[i].im = fma(top.im, g[i], c.im);
+    }
+  }
+  int n = D - 2;
 #pragma unroll 1
-  for (int n = D - 1; n >= 0; --n) {
-    const cplx c = cf[n];
+  for (; n >= 1; n -= 2) {
+    const cplx c1 = cf[n], c0 = cf[n - 1];
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      d[i].re = fma(d[i].re, g[i], c1.re);
+      d[i].im = fma(d[i].im, g[i], c1.im);
+    }
+#pragma unroll
+    for (int i = 0; i < kR; ++i) {
+      d[i].re = fma(d[i].re, g[i], c0.re);
+      d[i].im = fma(d[i].im, g[i], c0.im);
+    }
+  }
+  if (n == 0) {
+    const cplx c = cf[0];
 #pragma unroll
     for (int i = 0; i < kR; ++i) {
       d[i].re = fma(d[i].re, g[i], c.re);
