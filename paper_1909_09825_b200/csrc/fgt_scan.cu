@@ -3024,29 +3024,40 @@ __global__ void __launch_bounds__(kScanThreads) scan_reduce_kernel(ScanArgs sa) 
 
 __global__ void __launch_bounds__(1024)
     scan_top_kernel(ScanArgs sa, const cplx* __restrict__ carry_in, cplx* __restrict__ totals) {
+  // thread aggregates of contiguous runs, then an inclusive scan over the
+  // 1024 threads: warp shuffles, the 32 warp totals by warp 0 (two barriers
+  // instead of a 10-step Hillis-Steele over shared memory)
   __shared__ Pair sp[1024];
+  __shared__ Pair wsp[32];
   const int q = blockIdx.x;
   const int ne = sa.ne;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t per = (sa.nblk + 1023) / 1024;
   const int64_t r0 = (int64_t)threadIdx.x * per;
   const int64_t r1 = r0 + per < sa.nblk ? r0 + per : sa.nblk;
   const cplx* ag = sa.blkagg + (int64_t)q * sa.nblk * 2;
   Pair acc{{1.0, 0.0}, {0.0, 0.0}};
   for (int64_t r = r0; r < r1; ++r) acc = combine(acc, Pair{ag[2 * r], ag[2 * r + 1]});
-  // Hillis-Steele over 1024 thread aggregates (tiny)
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const Pair p = shfl_up_pair(acc, off);
+    if (lane >= off) acc = combine(p, acc);
+  }
+  if (lane == 31) wsp[warp] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    Pair w = wsp[lane];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const Pair p = shfl_up_pair(w, off);
+      if (lane >= off) w = combine(p, w);
+    }
+    wsp[lane] = w;
+  }
+  __syncthreads();
+  if (warp > 0) acc = combine(wsp[warp - 1], acc);
   sp[threadIdx.x] = acc;
   __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {
-    Pair p{{1.0, 0.0}, {0.0, 0.0}};
-    const bool has = threadIdx.x >= off;
-    if (has) p = sp[threadIdx.x - off];
-    __syncthreads();
-    if (has) {
-      acc = combine(p, acc);
-      sp[threadIdx.x] = acc;
-    }
-    __syncthreads();
-  }
   Pair ex{{1.0, 0.0}, {0.0, 0.0}};
   if (threadIdx.x > 0) ex = sp[threadIdx.x - 1];
   const cplx cin = carry_in ? carry_in[q] : cplx{0.0, 0.0};
