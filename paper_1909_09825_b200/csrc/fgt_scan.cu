@@ -3479,20 +3479,17 @@ __device__ __forceinline__ void bar_compute(unsigned nthreads) {
   asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
 }
 
+#ifndef FGT_K1C_MINB
+#define FGT_K1C_MINB 3
+#endif
 template <int NM>
-__global__ void __launch_bounds__(kCThreads + 32, 2) k1c_kernel(MomScanArgs q,
+__global__ void __launch_bounds__(kCThreads + 32, FGT_K1C_MINB) k1c_kernel(MomScanArgs q,
                                                           const ModeTable* __restrict__ mtab) {
+  (void)mtab;
   extern __shared__ __align__(16) unsigned char k1c_smem[];
-  __shared__ ModeTable mt;
-  __shared__ double smom[kMomCta][NM];
-  __shared__ double2 sh01[kMomCta];  // (h0, h1) of the block's segments
-  __shared__ Pair wagg[kCW][2 * kMaxModes];
   __shared__ __align__(16) double kred[kCW][32 * 4];
-  load_mode_table(mtab, mt);
   const StreamArgs& a = q.a;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ne = q.ne;
-  constexpr int64_t kCPB = kMomCta / kCW;  // chunks per scan block
   uint64_t* const empty = reinterpret_cast<uint64_t*>(k1c_smem + 2 * kK1cStageBytes);
   if (threadIdx.x == 0) {
     mbar_init(k1c_stage(k1c_smem).bar);
@@ -3502,12 +3499,10 @@ __global__ void __launch_bounds__(kCThreads + 32, 2) k1c_kernel(MomScanArgs q,
   }
   __syncthreads();
   const int64_t nchunk = (a.nseg + kCW - 1) / kCW;
-  // the CTA's chunk sequence: blocks blockIdx.x, + gridDim.x, ..., kCPB
-  // chunks each, up to the last chunk of the stream
-  auto chunk_of = [&](int64_t it) -> int64_t {
-    const int64_t b = blockIdx.x + (it / kCPB) * (int64_t)gridDim.x;
-    return b * kCPB + it % kCPB;
-  };
+  // the CTA's chunks: an equal contiguous range (balanced to one chunk; the
+  // block aggregates are formed afterwards by k1agg_kernel)
+  const int64_t cbeg = nchunk * blockIdx.x / gridDim.x;
+  const int64_t cend = nchunk * (blockIdx.x + 1) / gridDim.x;
   if (warp == kCW) {
     if (lane != 0) return;
     auto chunk_ib = [&](int64_t c, int64_t& i0, int64_t& i1) {
@@ -3517,34 +3512,28 @@ __global__ void __launch_bounds__(kCThreads + 32, 2) k1c_kernel(MomScanArgs q,
       i1 = __ldg(a.seg_ib + s1);
     };
     for (int i = 0; i < 2; ++i) {
-      const int64_t c = chunk_of(i);
-      if (c < nchunk) {
+      const int64_t c = cbeg + i;
+      if (c < cend) {
         int64_t i0, i1;
         chunk_ib(c, i0, i1);
         k1c_issue(a, c, i0, i1, k1c_stage(k1c_smem + i * kK1cStageBytes));
       }
     }
     int64_t nib0 = 0, nib1 = 0;
-    if (chunk_of(2) < nchunk) chunk_ib(chunk_of(2), nib0, nib1);
+    if (cbeg + 2 < cend) chunk_ib(cbeg + 2, nib0, nib1);
     for (int64_t it = 0;; ++it) {
-      const int64_t c2 = chunk_of(it + 2);
-      if (c2 >= nchunk) break;
+      const int64_t c2 = cbeg + it + 2;
+      if (c2 >= cend) break;
       const int k = (int)(it & 1);
       mbar_wait(empty + k, (unsigned)(it >> 1) & 1u);
       k1c_issue(a, c2, nib0, nib1, k1c_stage(k1c_smem + k * kK1cStageBytes));
-      const int64_t c3 = chunk_of(it + 3);
-      if (c3 < nchunk) chunk_ib(c3, nib0, nib1);
+      if (c2 + 1 < cend) chunk_ib(c2 + 1, nib0, nib1);
     }
     return;
   }
-  const bool all1 = a.nwide1 == 0;
   const int64_t L = a.M + a.N;
   int64_t it = 0;
-  for (int64_t b = blockIdx.x; b < q.nblk; b += gridDim.x) {
-    // ---- phase 1: moments of the block's segments, chunk by chunk
-    for (int64_t ci = 0; ci < kCPB; ++ci, ++it) {
-      const int64_t c = b * kCPB + ci;
-      if (c >= nchunk) break;  // only at the end of the stream
+  for (int64_t c = cbeg; c < cend; ++c, ++it) {
       const int k = (int)(it & 1);
       const K1cStage st = k1c_stage(k1c_smem + k * kK1cStageBytes);
       mbar_wait(st.bar, (unsigned)(it >> 1) & 1u);
@@ -3566,7 +3555,6 @@ __global__ void __launch_bounds__(kCThreads + 32, 2) k1c_kernel(MomScanArgs q,
         g.zlast = z.y;
         const SegFrame f = seg_frame(g);
         const double zc = f.zc;
-        if (lane == 0) sh01[s - b * kMomCta] = make_double2(f.h0, f.h1);
         const double* yy = st.y + h.yo + ly;
         const double* bb = st.b + h.bo + ly;
         // two warp-uniform halves of kSeg / 64 source slots per lane (a
@@ -3596,7 +3584,6 @@ __global__ void __launch_bounds__(kCThreads + 32, 2) k1c_kernel(MomScanArgs q,
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + k);  // stage consumed
-      const int sl = (int)(s - b * kMomCta);  // slot in the block
       if constexpr (NM <= 4) {
         double* red = kred[warp];
 #pragma unroll
@@ -3613,7 +3600,6 @@ __global__ void __launch_bounds__(kCThreads + 32, 2) k1c_kernel(MomScanArgs q,
         for (int o = 4; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (live && n < NM && g == 0) {
           q.mom[s * NM + n] = v;
-          smom[sl][n] = v;
         }
         __syncwarp();
       } else {
@@ -3628,76 +3614,114 @@ __global__ void __launch_bounds__(kCThreads + 32, 2) k1c_kernel(MomScanArgs q,
           for (int n = 1; n < NM; ++n)
             if (lane == n) v = M[n];
           q.mom[s * NM + lane] = v;
-          smom[sl][lane] = v;
         }
+      }
+  }
+}
+
+// Block aggregates of the moment path (K1c's second half): two warps per
+// scan block of kMomCta segments, lane l of a warp holding kAggPer
+// consecutive segments (their moments and frames loaded once, before the
+// mode loop).  Per mode: each segment's (A, F) / (A, G) pairs from its
+// moments, combined in order in registers (forward: earlier first;
+// backward: later first), one ordered warp reduction, the two warps'
+// results combined in order -- under half the FP64 work of a warp reduction
+// over single segments.
+constexpr int kAggPer = 4;                       // segments per lane
+constexpr int kAggWarps = kMomCta / (32 * kAggPer);  // warps per scan block
+static_assert(kAggWarps == 2 && kCW % kAggWarps == 0, "k1agg layout");
+template <int NM>
+__global__ void __launch_bounds__(kCThreads) k1agg_kernel(MomScanArgs q,
+                                                         const ModeTable* __restrict__ mtab) {
+  __shared__ ModeTable mt;
+  __shared__ Pair wagg[kCW][2 * kMaxModes];
+  load_mode_table(mtab, mt);
+  const StreamArgs& a = q.a;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ne = q.ne;
+  const bool all1 = a.nwide1 == 0;
+  const int64_t b = (int64_t)blockIdx.x * (kCW / kAggWarps) + warp / kAggWarps;
+  const int64_t s0 = b * kMomCta + (int64_t)(warp % kAggWarps) * 32 * kAggPer +
+                     (int64_t)lane * kAggPer;
+  double Mm[kAggPer][NM];
+  double h0[kAggPer], h1[kAggPer];
+  bool lv[kAggPer], n1[kAggPer];
+#pragma unroll
+  for (int i = 0; i < kAggPer; ++i) {
+    const int64_t sg = s0 + i;
+    lv[i] = b < q.nblk && sg < a.nseg;
+    n1[i] = false;
+    h0[i] = h1[i] = 0.0;
+#pragma unroll
+    for (int n = 0; n < NM; ++n) Mm[i][n] = 0.0;
+    if (lv[i]) {
+      n1[i] = all1 || k1_narrow(seg_deg_DM(__ldg(a.seg_deg + sg)));
+      const double2 z = __ldg(a.seg_z + sg);
+      SegGeom g;
+      g.zprev = sg == 0 ? a.zprev0 : z.x;
+      g.zlast = z.y;
+      const SegFrame f = seg_frame(g);
+      h0[i] = f.h0;
+      h1[i] = f.h1;
+      if (n1[i]) {
+#pragma unroll
+        for (int n = 0; n < NM; ++n) Mm[i][n] = __ldg(q.mom + sg * NM + n);
       }
     }
-    bar_compute(kCThreads);
-    // ---- phase 2: per-warp aggregates per mode, lane l holding segment
-    // b kMomCta + 32 w + l; ordered warp reductions
-    {
-      const int64_t sg = b * kMomCta + 32 * warp + lane;
-      const bool lv = sg < a.nseg;
-      bool n1 = false;
-      double h0 = 0.0, h1 = 0.0;
-      if (lv) {
-        n1 = all1 || k1_narrow(seg_deg_DM(__ldg(a.seg_deg + sg)));
-        const double2 hh = sh01[32 * warp + lane];
-        h0 = hh.x;
-        h1 = hh.y;
-      }
-      double Mm[NM];
+  }
+  __syncthreads();  // the mode table
+  for (int k = 0; k < ne; ++k) {
+    Pair fw{{1.0, 0.0}, {0.0, 0.0}}, bw{{1.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-      for (int n = 0; n < NM; ++n) Mm[n] = lv ? smom[32 * warp + lane][n] : 0.0;
-      for (int k = 0; k < ne; ++k) {
-        cplx A, F, G;
-        if (!lv) {
-          A = {1.0, 0.0};
-          F = G = {0.0, 0.0};
-        } else if (n1) {
-          cplx E0, E1;
-          mom_pairs<NM>(mt, k, Mm, h0, h1, A, F, G, E0, E1);
-        } else {
-          const int64_t o = (int64_t)k * a.nseg + sg;
-          A = q.ts.A[o];
-          F = q.ts.F[o];
-          G = q.ts.G[o];
-        }
-        Pair fw{A, F}, bw{A, G};
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          Pair of, ob;
-          of.a.re = __shfl_xor_sync(0xffffffffu, fw.a.re, off);
-          of.a.im = __shfl_xor_sync(0xffffffffu, fw.a.im, off);
-          of.s.re = __shfl_xor_sync(0xffffffffu, fw.s.re, off);
-          of.s.im = __shfl_xor_sync(0xffffffffu, fw.s.im, off);
-          ob.a.re = __shfl_xor_sync(0xffffffffu, bw.a.re, off);
-          ob.a.im = __shfl_xor_sync(0xffffffffu, bw.a.im, off);
-          ob.s.re = __shfl_xor_sync(0xffffffffu, bw.s.re, off);
-          ob.s.im = __shfl_xor_sync(0xffffffffu, bw.s.im, off);
-          const bool lower = (lane & off) == 0;
-          fw = lower ? combine(fw, of) : combine(of, fw);
-          bw = lower ? combine(ob, bw) : combine(bw, ob);
-        }
-        if (lane == 0) {
-          wagg[warp][k] = fw;
-          wagg[warp][ne + k] = bw;
-        }
+    for (int i = 0; i < kAggPer; ++i) {
+      if (!lv[i]) continue;
+      cplx A, F, G;
+      if (n1[i]) {
+        cplx E0, E1;
+        mom_pairs<NM>(mt, k, Mm[i], h0[i], h1[i], A, F, G, E0, E1);
+      } else {
+        const int64_t o = (int64_t)k * a.nseg + s0 + i;
+        A = q.ts.A[o];
+        F = q.ts.F[o];
+        G = q.ts.G[o];
       }
+      fw = combine(fw, Pair{A, F});
+      bw = combine(Pair{A, G}, bw);
     }
-    bar_compute(kCThreads);
-    if (threadIdx.x < 2 * ne) {
-      const bool bwd = (int)threadIdx.x >= ne;
-      Pair acc{{1.0, 0.0}, {0.0, 0.0}};
-      for (int w = 0; w < kCW; ++w) {
-        const int ww = bwd ? kCW - 1 - w : w;
-        if (b * kMomCta + (int64_t)ww * 32 < a.nseg) acc = combine(acc, wagg[ww][threadIdx.x]);
-      }
-      cplx* out = q.blkagg + ((int64_t)threadIdx.x * q.nblk + (bwd ? q.nblk - 1 - b : b)) * 2;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      Pair of, ob;
+      of.a.re = __shfl_xor_sync(0xffffffffu, fw.a.re, off);
+      of.a.im = __shfl_xor_sync(0xffffffffu, fw.a.im, off);
+      of.s.re = __shfl_xor_sync(0xffffffffu, fw.s.re, off);
+      of.s.im = __shfl_xor_sync(0xffffffffu, fw.s.im, off);
+      ob.a.re = __shfl_xor_sync(0xffffffffu, bw.a.re, off);
+      ob.a.im = __shfl_xor_sync(0xffffffffu, bw.a.im, off);
+      ob.s.re = __shfl_xor_sync(0xffffffffu, bw.s.re, off);
+      ob.s.im = __shfl_xor_sync(0xffffffffu, bw.s.im, off);
+      const bool lower = (lane & off) == 0;
+      fw = lower ? combine(fw, of) : combine(of, fw);
+      bw = lower ? combine(ob, bw) : combine(bw, ob);
+    }
+    if (lane == 0) {
+      wagg[warp][k] = fw;
+      wagg[warp][ne + k] = bw;
+    }
+  }
+  __syncthreads();
+  // the scan blocks of this CTA: thread t < (kCW / kAggWarps) 2 ne
+  const int per = 2 * ne;
+  if ((int)threadIdx.x < (kCW / kAggWarps) * per) {
+    const int bl = threadIdx.x / per, q2 = threadIdx.x % per;
+    const int64_t bb = (int64_t)blockIdx.x * (kCW / kAggWarps) + bl;
+    if (bb < q.nblk) {
+      const bool bwd = q2 >= ne;
+      const Pair p0 = wagg[bl * kAggWarps][q2], p1 = wagg[bl * kAggWarps + 1][q2];
+      const Pair acc = bwd ? combine(p1, p0) : combine(p0, p1);
+      cplx* out = q.blkagg + ((int64_t)q2 * q.nblk + (bwd ? q.nblk - 1 - bb : bb)) * 2;
       out[0] = acc.a;
       out[1] = acc.s;
     }
-    bar_compute(kCThreads);
   }
 }
 
@@ -4264,7 +4288,7 @@ static cudaError_t launch_mom_nm(const MomScanArgs& q, const ModeTable* mt, bool
                                  const ScanArgs& sa, const cplx* carry_in, cplx* totals,
                                  cudaStream_t st) {
   const unsigned grid = (unsigned)q.nblk;
-  note_launch(1 + (reduce ? 1 : 0) + (down ? 1 : 0));
+  note_launch(1 + (reduce ? (FGT_K1_CHUNKED ? 2 : 1) : 0) + (down ? 1 : 0));
   if (reduce && FGT_K1_CHUNKED) {
     const size_t smem = k1c_smem_bytes<NM>();
     static std::atomic<unsigned long long> done{0};
@@ -4274,8 +4298,11 @@ static cudaError_t launch_mom_nm(const MomScanArgs& q, const ModeTable* mt, bool
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1c_kernel<NM>, kCThreads + 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
+    const int64_t nchunk = (q.a.nseg + kCW - 1) / kCW;
     const int64_t cap = (int64_t)num_sms() * per_sm;
-    k1c_kernel<NM><<<(unsigned)(q.nblk < cap ? q.nblk : cap), kCThreads + 32, smem, st>>>(q, mt);
+    k1c_kernel<NM><<<(unsigned)(nchunk < cap ? nchunk : cap), kCThreads + 32, smem, st>>>(q, mt);
+    k1agg_kernel<NM><<<(unsigned)((q.nblk + kCW / kAggWarps - 1) / (kCW / kAggWarps)), kCThreads, 0,
+                       st>>>(q, mt);
   } else if (reduce) {
     const size_t smem = (size_t)kSegWarps * kK1WarpBytes;
     static std::atomic<unsigned long long> done{0};
