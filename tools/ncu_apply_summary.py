@@ -35,7 +35,7 @@ for r in rows[2:]:
     d["dram_bytes"] = float(r[ir]) * scale[units[ir]] + float(r[iw]) * scale[units[iw]]
     tot += d["dram_bytes"]
     kern.append(d)
-apply = [k for k in kern if any(t in k["kernel"] for t in ("k1c", "k1b", "scan_top", "k2m_down", "k3c", "k3n"))]
+apply = [k for k in kern if any(t in k["kernel"] for t in ("k1c", "k1agg", "k1b", "scan_top", "k2m_down", "k3c", "k3n"))]
 json.dump({"source": "ncu --set full --clock-control none (tools/profile_round.sh) of one cfg3 step: "
                      "N=M=1e8 presorted, delta=1e-3, n_e=6; plan (partition, tile pass, mode table) "
                      "and apply (K1c moments + block aggregates, K2 top, K2m down-sweep with the "

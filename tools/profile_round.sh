@@ -17,6 +17,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/
 python tools/summarize_launches.py $OUT/launches.csv > $OUT/launches_summary.txt 2>&1
 python tools/prof_driver.py --n 1e8 --reps 1 > $OUT/plain2.log 2>&1 && \
 ncu --set full --import-source on --clock-control none \
-    -k 'regex:partition|plan_tile|store_table|classify|k1c|scan_top|k2m_down|k3c' -c 8 -o $OUT/step_full \
+    -k 'regex:partition|plan_tile|store_table|classify|k1c|k1agg|scan_top|k2m_down|k3c' -c 9 -o $OUT/step_full \
     python tools/prof_driver.py --n 1e8 --reps 1 > $OUT/ncu_full.log 2>&1
 echo done
