@@ -223,6 +223,7 @@ struct fgt_plan_s {
   double2* d_seg_z = nullptr;
   int* d_seg_deg = nullptr;      // per segment: packed degrees (classify_kernel)
   uint32_t* d_seg_mask = nullptr;
+  unsigned long long* d_cls = nullptr;  // slotted class counts of the fused classification
   // batched plans (fgt_batch_create)
   bool batch = false;
   int nbatch = 0;
@@ -415,7 +416,7 @@ unsigned char* pinned_scratch() {
   thread_local PinnedScratch s;
   if (!s.p) {
     void* q = nullptr;
-    if (cudaMallocHost(&q, 256) == cudaSuccess) {
+    if (cudaMallocHost(&q, 2048) == cudaSuccess) {
       s.p = static_cast<unsigned char*>(q);
     } else {
       cudaGetLastError();
@@ -468,28 +469,56 @@ void take_classes(fgt_plan_s* p, const unsigned long long* h) {
   p->dn_narrow = (int)h[2] - 1;
   p->dm_narrow = (int)h[3] - 1;
 }
-void classify_sync(fgt_plan_s* p, cudaStream_t st) {
-  unsigned long long hl[4] = {0, 0, 0, 0};
-  unsigned char* pin = pinned_scratch();
-  unsigned long long* h = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hl;
-  queue_classify(p, h, st);
-  ck(cudaStreamSynchronize(st), "classify sync");
-  take_classes(p, h);
-}
 
 // Partition + speculative tile pass (checks and segment metadata) on the
 // arrays as given; valid metadata whenever they turn out to be sorted.
+// classify: also write the segment degrees and the slotted class counts
+// (p->d_cls; p->P must be set), read back by read_classes.
 void plan_tiles(fgt_plan_s* p, const double* xd, const double* yd, bool check_sorted,
-                cudaStream_t st) {
+                cudaStream_t st, bool classify = false, bool has_prev = false,
+                double z_prev = 0.0) {
   const int64_t L = p->M + p->N;
   const int64_t ntl = (L + kPlanTile - 1) / kPlanTile;
   if (ntl == 0) return;
   int64_t* tib = dmalloc<int64_t>(ntl + 1, st);
   ck(launch_partition(xd, p->M, yd, p->N, kPlanTile, ntl, tib, st), "partition");
+  PlanClassify cls;
+  if (classify) {
+    if (!p->d_cls) p->d_cls = dmalloc<unsigned long long>(4 * kClassSlots, st);
+    cls.enabled = 1;
+    cls.P = p->P;
+    cls.smax = p->P.smax;
+    cls.seg_deg = p->d_seg_deg;
+    cls.counts = p->d_cls;
+    cls.has_prev = has_prev ? 1 : 0;
+    cls.z_prev = z_prev;
+  }
   ck(launch_plan_tiles(xd, p->M, yd, p->N, tib, ntl, p->ntiles, check_sorted ? 1 : 0,
-                       p->d_tile_ib, p->d_seg_z, p->d_seg_mask, p->d_flag, st),
+                       p->d_tile_ib, p->d_seg_z, p->d_seg_mask, p->d_flag, st, &cls),
      "plan tiles");
   dfree(tib, st);
+}
+
+// The fused classification's slotted counts -> host (h: 4 kClassSlots u64,
+// pinned), reduced by take_slotted_classes once the stream is synchronized.
+void queue_slotted_classes(fgt_plan_s* p, unsigned long long* h, cudaStream_t st) {
+  if (!p->d_cls) {  // no tiles (empty sets)
+    for (int q = 0; q < 4 * kClassSlots; ++q) h[q] = 0;
+    return;
+  }
+  ck(cudaMemcpyAsync(h, p->d_cls, sizeof(unsigned long long) * 4 * kClassSlots,
+                     cudaMemcpyDeviceToHost, st),
+     "class counts");
+}
+void take_slotted_classes(fgt_plan_s* p, const unsigned long long* h) {
+  unsigned long long r[4] = {0, 0, 0, 0};
+  for (int q = 0; q < kClassSlots; ++q) {
+    r[0] += h[4 * q];
+    r[1] += h[4 * q + 1];
+    r[2] = h[4 * q + 2] > r[2] ? h[4 * q + 2] : r[2];
+    r[3] = h[4 * q + 3] > r[3] ? h[4 * q + 3] : r[3];
+  }
+  take_classes(p, r);
 }
 
 // Mode table of a single plan: built on the host, stored by a kernel
@@ -540,6 +569,7 @@ void destroy_plan(fgt_plan_s* p) {
   dfree(p->d_seg_z, st);
   dfree(p->d_seg_deg, st);
   dfree(p->d_seg_mask, st);
+  dfree(p->d_cls, st);
   dfree(p->d_seg_jb, st);
   dfree(p->d_seg_info, st);
   dfree(p->d_mtb, st);
@@ -1248,22 +1278,22 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
       p->d_seg_z = dmalloc<double2>(p->ntiles, st);
         p->d_seg_deg = dmalloc<int>(p->ntiles, st);
       p->d_seg_mask = dmalloc<uint32_t>(seg_mask_words(p->ntiles), st);
-      // one read of both sets: checks + (speculative) segment metadata
-      plan_tiles(p, xs.dptr, ys.dptr, !(flags & FGT_ASSUME_SORTED), st);
       upload_modes(p, st);
-      // speculative classification (valid when both sets are sorted: segment
-      // 0 starts at its own first element), flags, first coordinates and
-      // class counts in one round trip (pinned scratch)
+      // one read of both sets: checks + (speculative) segment metadata and
+      // classification (valid when both sets are sorted: segment 0 starts at
+      // its own first element, or after z_prev); flags, first coordinates
+      // and class counts in one round trip (pinned scratch)
+      plan_tiles(p, xs.dptr, ys.dptr, !(flags & FGT_ASSUME_SORTED), st, true, has_prev, z_prev);
       unsigned char* pin = pinned_scratch();
       int hfl[8] = {0};
       double xyl[2] = {0.0, 0.0};
-      unsigned long long hcl[4] = {0, 0, 0, 0};
+      std::vector<unsigned long long> hcl(4 * kClassSlots, 0);
       int* hf = pin ? reinterpret_cast<int*>(pin) : hfl;
       double* xy0 = pin ? reinterpret_cast<double*>(pin + 32) : xyl;
-      unsigned long long* hc = pin ? reinterpret_cast<unsigned long long*>(pin + 64) : hcl;
+      unsigned long long* hc = pin ? reinterpret_cast<unsigned long long*>(pin + 128) : hcl.data();
       xy0[0] = xy0[1] = 0.0;
       if (has_prev) p->zprev0 = z_prev;
-      queue_classify(p, hc, st, false, !has_prev, xs.dptr, ys.dptr);
+      queue_slotted_classes(p, hc, st);
       ck(cudaMemcpyAsync(hf, p->d_flag, sizeof(int) * 8, cudaMemcpyDeviceToHost, st), "flags");
       if (M > 0) ck(cudaMemcpyAsync(xy0, xs.dptr, 8, cudaMemcpyDeviceToHost, st), "x0");
       if (N > 0) ck(cudaMemcpyAsync(xy0 + 1, ys.dptr, 8, cudaMemcpyDeviceToHost, st), "y0");
@@ -1294,8 +1324,10 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
         adopt_set(ys, N, p->s_sorted, flags, st, &p->d_ys, &p->own_ys, &p->d_sperm);
       }
       if (!p->t_sorted || !p->s_sorted || tile_flagged) {
-        // metadata of the sorted stream; first coordinates after sorting
-        plan_tiles(p, p->d_xs, p->d_ys, false, st);
+        // metadata and classes of the sorted stream; first coordinates after
+        // sorting
+        plan_tiles(p, p->d_xs, p->d_ys, false, st, true, has_prev, z_prev);
+        queue_slotted_classes(p, hc, st);
         if (M > 0) ck(cudaMemcpyAsync(xy0, p->d_xs, 8, cudaMemcpyDeviceToHost, st), "x0");
         if (N > 0) ck(cudaMemcpyAsync(xy0 + 1, p->d_ys, 8, cudaMemcpyDeviceToHost, st), "y0");
         ck(cudaStreamSynchronize(st), "sorted sync");
@@ -1303,10 +1335,7 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
       // coordinate before the first merged element: the element itself
       const double x0 = xy0[0], y0 = xy0[1];
       p->zprev0 = has_prev ? z_prev : (M > 0 && N > 0) ? std::fmin(x0, y0) : (M > 0 ? x0 : y0);
-      if (!p->t_sorted || !p->s_sorted || tile_flagged)
-        classify_sync(p, st);
-      else
-        take_classes(p, hc);
+      take_slotted_classes(p, hc);
     } catch (...) {
       for (void* t : temps) cudaFreeAsync(t, st);
       destroy_plan(p);

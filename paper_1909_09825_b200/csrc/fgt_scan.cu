@@ -2622,7 +2622,8 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
                                                int4* __restrict__ seg_info,
                                                double2* __restrict__ seg_z,
                                                uint32_t* __restrict__ seg_mask,
-                                               int* __restrict__ flags) {
+                                               int* __restrict__ flags,
+                                               const PlanClassify* cls = nullptr) {
   extern __shared__ __align__(16) double tsm[];
   __shared__ int sib[kPlanSegs + 1];
   __shared__ int swin[kPlanThreads];
@@ -2774,6 +2775,8 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
     }
     seg_mask_prefix(seg_mask, nseg)[c.seg0 + t] = make_uint2(lo, hi);
   }
+  bool cw1 = false, cw3 = false;
+  int cdn = 0, cdm = 0;
   if (t < nsegs_tile) {
     const int k = t;
     const int i0 = sib[k], i1 = sib[k + 1];
@@ -2799,6 +2802,38 @@ __device__ __forceinline__ void plan_tile_body(const TileCtx& c, int check_sorte
     const double ly = j1 > j0 ? sy[j1 - 1] : -INFINITY;
     seg_z[sg] = make_double2(fmax(px, py), fmax(lx, ly));
     if (!BATCH && sg + 1 == nseg) seg_ib[nseg] = c.M;
+    if (!BATCH && cls && cls->enabled) {
+      // classify_kernel's degrees, from this segment's frame
+      double zp = fmax(px, py);
+      if (sg == 0)
+        zp = cls->has_prev ? cls->z_prev
+                           : fmin(nx > 0 ? sx[0] : INFINITY, ny > 0 ? sy[0] : INFINITY);
+      SegGeom g;
+      g.zprev = zp;
+      g.zlast = fmax(lx, ly);
+      const SegFrame f = seg_frame(g);
+      const int DM = seg_moment_degree(cls->P, cls->smax, f);
+      const int DN = pick_degree(cls->P, cls->smax, f.h0 + f.h1);
+      cls->seg_deg[sg] = 0 | ((DM + 1) << 8) | ((DN + 1) << 16);
+      cw1 = !k1_narrow(DM);
+      cw3 = !k3_narrow(DM);
+      cdn = !cw3 ? DN + 1 : 0;
+      cdm = !cw1 ? DM + 1 : 0;
+    }
+  }
+  if (!BATCH && cls && cls->enabled && t < 32) {
+    // the tile's segments are all in warp 0: one slot update per CTA
+    const unsigned n1 = __popc(__ballot_sync(0xffffffffu, cw1));
+    const unsigned n3 = __popc(__ballot_sync(0xffffffffu, cw3));
+    const unsigned mdn = __reduce_max_sync(0xffffffffu, (unsigned)cdn);
+    const unsigned mdm = __reduce_max_sync(0xffffffffu, (unsigned)cdm);
+    if (t == 0) {
+      unsigned long long* slot = cls->counts + 4 * (blockIdx.x % kClassSlots);
+      if (n1) atomicAdd(slot, (unsigned long long)n1);
+      if (n3) atomicAdd(slot + 1, (unsigned long long)n3);
+      if (mdn) atomicMax(slot + 2, (unsigned long long)mdn);
+      if (mdm) atomicMax(slot + 3, (unsigned long long)mdm);
+    }
   }
   int fl = (f0 ? 1 : 0) | (f1 ? 2 : 0) | (f2 ? 4 : 0) | (f3 ? 8 : 0) | (f4 ? 16 : 0);
   fl = __reduce_or_sync(0xffffffffu, fl);
@@ -2814,7 +2849,8 @@ __global__ void __launch_bounds__(kPlanThreads, FGT_PLAN_MINB)
     plan_tile_kernel(const double* __restrict__ xs, int64_t M, const double* __restrict__ ys,
                      int64_t N, const int64_t* __restrict__ tile_ib, int64_t nseg,
                      int check_sorted, int64_t* __restrict__ seg_ib, double2* __restrict__ seg_z,
-                     uint32_t* __restrict__ seg_mask, int* __restrict__ flags) {
+                     uint32_t* __restrict__ seg_mask, int* __restrict__ flags,
+                     const __grid_constant__ PlanClassify cls) {
   const int64_t t = blockIdx.x;
   const int64_t L = M + N;
   TileCtx c;
@@ -2829,7 +2865,8 @@ __global__ void __launch_bounds__(kPlanThreads, FGT_PLAN_MINB)
   c.seg0 = t * kPlanSegs;
   c.xoff = c.yoff = 0;
   c.tid = 0;
-  plan_tile_body<false>(c, check_sorted, nseg, seg_ib, nullptr, nullptr, seg_z, seg_mask, flags);
+  plan_tile_body<false>(c, check_sorted, nseg, seg_ib, nullptr, nullptr, seg_z, seg_mask, flags,
+                        &cls);
 }
 
 struct BatchArgs {
@@ -3475,9 +3512,6 @@ __device__ __forceinline__ void k1c_issue(const StreamArgs& a, int64_t c, int64_
   bulk_g2s(st.sz, a.seg_z + s0, 16u * ns, st.bar);
 }
 
-__device__ __forceinline__ void bar_compute(unsigned nthreads) {
-  asm volatile("bar.sync 1, %0;\n" ::"r"(nthreads) : "memory");
-}
 
 #ifndef FGT_K1C_MINB
 #define FGT_K1C_MINB 3
@@ -3982,8 +4016,15 @@ cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int6
 cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int64_t N,
                               const int64_t* tile_ib, int64_t ntiles, int64_t nseg,
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
-                              uint32_t* seg_mask, int* flags, cudaStream_t st) {
+                              uint32_t* seg_mask, int* flags, cudaStream_t st,
+                              const PlanClassify* cls) {
   if (ntiles == 0) return cudaSuccess;
+  PlanClassify cl;
+  if (cls && cls->enabled) {
+    cl = *cls;
+    cudaError_t e0 = cudaMemsetAsync(cl.counts, 0, sizeof(unsigned long long) * 4 * kClassSlots, st);
+    if (e0 != cudaSuccess) return e0;
+  }
   // both sets, heads, sentinels + padding for merge overruns on unsorted input
   const size_t smem = sizeof(double) * (kPlanTile + 8 + 2 * kPlanPer);
   static std::atomic<unsigned long long> done{0};
@@ -3991,7 +4032,7 @@ cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int
   if (e != cudaSuccess) return e;
   note_launch();
   plan_tile_kernel<<<(unsigned)ntiles, kPlanThreads, smem, st>>>(xs, M, ys, N, tile_ib, nseg, check_sorted,
-                                                         seg_ib, seg_z, seg_mask, flags);
+                                                         seg_ib, seg_z, seg_mask, flags, cl);
   return cudaGetLastError();
 }
 

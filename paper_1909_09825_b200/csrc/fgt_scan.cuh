@@ -144,10 +144,26 @@ cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int6
 // x non-finite, y non-finite, x != y when M == N, x unsorted, y unsorted;
 // zeroed by the caller) and segment metadata seg_ib / seg_z / seg_mask.
 // tile_ib: launch_partition output at kPlanTile granularity.
+// Segment classification folded into the tile pass (single plans): the
+// degrees classify_kernel would write (seg_deg) and the class counts, summed
+// per CTA into kClassSlots slots of 4 u64 each (wide-K1 count, wide-K3 count,
+// max DN + 1, max DM + 1), which the host reduces.  z_prev: the coordinate
+// before segment 0 when has_prev (chunk plans), else its own first element.
+constexpr int kClassSlots = 32;
+struct PlanClassify {
+  int enabled = 0;
+  ModeParams P;
+  double smax = 0.0;
+  int* seg_deg = nullptr;
+  unsigned long long* counts = nullptr;  // [kClassSlots][4]
+  int has_prev = 0;
+  double z_prev = 0.0;
+};
 cudaError_t launch_plan_tiles(const double* xs, int64_t M, const double* ys, int64_t N,
                               const int64_t* tile_ib, int64_t ntiles, int64_t nseg,
                               int check_sorted, int64_t* seg_ib, double2* seg_z,
-                              uint32_t* seg_mask, int* flags, cudaStream_t st);
+                              uint32_t* seg_mask, int* flags, cudaStream_t st,
+                              const PlanClassify* cls = nullptr);
 // Element-wise checks of unsorted input (flags[0..4] as launch_plan_tiles,
 // zeroed by the caller) over the arrays as given.
 cudaError_t launch_check_points(const double* xs, int64_t M, const double* ys, int64_t N,
