@@ -3034,6 +3034,7 @@ struct ScanArgs {
   int64_t nblk;
   cplx* blkagg;    // [2ne][nblk] (a, s) pairs as 2 complex
   cplx* blkcarry;  // [2ne][nblk]
+  cplx* blka = nullptr;  // [2ne][nblk] exclusive products of the block A's (moment path)
 };
 
 __device__ __forceinline__ Pair load_item(const ScanArgs& sa, int q, int64_t r) {
@@ -3100,9 +3101,22 @@ __global__ void __launch_bounds__(1024)
   const cplx cin = carry_in ? carry_in[q] : cplx{0.0, 0.0};
   cplx c = cmad(ex.a, cin, ex.s);
   cplx* bc = sa.blkcarry + (int64_t)q * sa.nblk;
-  for (int64_t r = r0; r < r1; ++r) {
-    bc[r] = c;
-    c = cmad(ag[2 * r], c, ag[2 * r + 1]);
+  if (sa.blka) {
+    // also the exclusive A products, so that a later carry-in applies
+    // without another top-level pass (chunk phase 2: c = A cin + carry)
+    cplx* ba = sa.blka + (int64_t)q * sa.nblk;
+    cplx ar = ex.a;
+    for (int64_t r = r0; r < r1; ++r) {
+      bc[r] = c;
+      ba[r] = ar;
+      c = cmad(ag[2 * r], c, ag[2 * r + 1]);
+      ar = cmul(ag[2 * r], ar);
+    }
+  } else {
+    for (int64_t r = r0; r < r1; ++r) {
+      bc[r] = c;
+      c = cmad(ag[2 * r], c, ag[2 * r + 1]);
+    }
   }
   if (totals && threadIdx.x == 1023) {
     const Pair t = sp[1023];
@@ -3169,6 +3183,9 @@ struct MomScanArgs {
   int64_t nblk;
   cplx* blkagg;    // [2ne][nblk] pairs (backward blocks stored right to left)
   cplx* blkcarry;  // [2ne][nblk]
+  cplx* blka;      // [2ne][nblk] exclusive block A products (top level)
+  // chunk phase 2: carries = blka * carry_in + blkcarry (no second top pass)
+  const cplx* carry_in = nullptr;
   // K2m also folds the segment-total terms sum_m B[q][m] Tot_m of the
   // collapsed form into E^c (k3_folds: the moments reach degree dn)
   int fold = 0;
@@ -3861,8 +3878,13 @@ __global__ void __launch_bounds__(kThreads) k2m_down_kernel(MomScanArgs q,
     __syncthreads();
     // this warp's carries in: the block's carry through the earlier warps
     // (forward) / the later warps (backward)
-    cplx cinf = q.blkcarry[(int64_t)k * q.nblk + b];
-    cplx cinb = q.blkcarry[(int64_t)(ne + k) * q.nblk + (q.nblk - 1 - b)];
+    const int64_t of = (int64_t)k * q.nblk + b, ob = (int64_t)(ne + k) * q.nblk + (q.nblk - 1 - b);
+    cplx cinf = q.blkcarry[of];
+    cplx cinb = q.blkcarry[ob];
+    if (q.carry_in) {
+      cinf = cmad(q.blka[of], q.carry_in[k], cinf);
+      cinb = cmad(q.blka[ob], q.carry_in[ne + k], cinb);
+    }
     for (int w = 0; w < warp; ++w) {
       const Pair t = wtot[k][0][w];
       cinf = cmad(t.a, cinf, t.s);
@@ -3966,13 +3988,13 @@ int64_t scan_blocks(int64_t nseg) { return (nseg + kScanBlock - 1) / kScanBlock;
 static int64_t ws_blocks(int64_t nseg) { return (nseg + 255) / 256; }
 size_t tile_state_elems(int64_t nseg, int ne) {
   const size_t nt = (size_t)nseg * (size_t)ne;
-  const size_t blk = (size_t)ws_blocks(nseg) * 2 * (size_t)ne * 3 + 8;
+  const size_t blk = (size_t)ws_blocks(nseg) * 2 * (size_t)ne * 4 + 8;
   return 5 * nt + blk + (size_t)nseg * (kEcStride / 2) + 4;
 }
 
 TileState tile_state_carve(cplx* base, int64_t nseg, int ne) {
   const size_t nt = (size_t)nseg * (size_t)ne;
-  const size_t blk = (size_t)ws_blocks(nseg) * 2 * (size_t)ne * 3 + 8;
+  const size_t blk = (size_t)ws_blocks(nseg) * 2 * (size_t)ne * 4 + 8;
   // collapsed carries: 64-byte aligned rows (one bulk copy per segment)
   uintptr_t ecp = reinterpret_cast<uintptr_t>(base + 5 * nt + blk);
   ecp = (ecp + 63) & ~(uintptr_t)63;
@@ -4329,7 +4351,8 @@ static cudaError_t launch_mom_nm(const MomScanArgs& q, const ModeTable* mt, bool
                                  const ScanArgs& sa, const cplx* carry_in, cplx* totals,
                                  cudaStream_t st) {
   const unsigned grid = (unsigned)q.nblk;
-  note_launch(1 + (reduce ? (FGT_K1_CHUNKED ? 2 : 1) : 0) + (down ? 1 : 0));
+  const bool top = reduce || !down || !carry_in;
+  note_launch((top ? 1 : 0) + (reduce ? (FGT_K1_CHUNKED ? 2 : 1) : 0) + (down ? 1 : 0));
   if (reduce && FGT_K1_CHUNKED) {
     const size_t smem = k1c_smem_bytes<NM>();
     static std::atomic<unsigned long long> done{0};
@@ -4351,7 +4374,7 @@ static cudaError_t launch_mom_nm(const MomScanArgs& q, const ModeTable* mt, bool
     if (e != cudaSuccess) return e;
     k1b_kernel<NM><<<grid, kThreads, smem, st>>>(q, mt);
   }
-  scan_top_kernel<<<2 * q.ne, 1024, 0, st>>>(sa, carry_in, totals);
+  if (top) scan_top_kernel<<<2 * q.ne, 1024, 0, st>>>(sa, carry_in, totals);
   if (down) k2m_down_kernel<NM><<<grid, kThreads, 0, st>>>(q, mt);
   return cudaGetLastError();
 }
@@ -4371,11 +4394,18 @@ cudaError_t launch_mom_scan(const StreamArgs& a, int ne, const ModeTable* mt, co
   q.nblk = nblk;
   q.blkagg = ts.blk;
   q.blkcarry = ts.blk + (size_t)nblk * 2 * ne * 2;
+  q.blka = ts.blk + (size_t)nblk * 2 * ne * 3;
   if (cc && k3_folds(a)) {
     q.fold = 1;
     q.cc = *cc;
   }
-  const ScanArgs sa{ts.A, ts.F, ts.G, ts.Cf, ts.Cb, a.nseg, ne, nblk, q.blkagg, q.blkcarry};
+  ScanArgs sa{ts.A, ts.F, ts.G, ts.Cf, ts.Cb, a.nseg, ne, nblk, q.blkagg, q.blkcarry};
+  sa.blka = q.blka;
+  if (!reduce && down) {
+    // chunk phase 2: phase 1's top level left the block carries without a
+    // carry-in and the exclusive A products; K2m applies carry_in itself
+    q.carry_in = carry_in;
+  }
   switch (q.nm) {
 #define FGT_MNM(n)                                                 \
   case n:                                                          \
