@@ -1729,65 +1729,16 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
   }
 }
 
-// ------------------------------------------------------- K3 narrow (k3n)
+// ------------------------------------------------ collapsed-form helpers
 //
-// The collapsed narrow pass with a launch-uniform degree DN (the plan's
-// highest collapsed degree over its narrow segments; a higher degree than a
-// segment needs only adds terms below 2^-52).  Per segment, per warp:
-//   stage   : the next segment's x / y / beta by TMA bulk copies, its merge
-//             mask words and its collapsed carries E^c_q (one 64-byte bulk
-//             copy; written by collapse_carries_kernel after K2) land in the
-//             warp's shared-memory stage while this one is computed
-//   decode  : lane runs of kR merged elements from the mask (w = z - zc, b)
-//   moments : lane-run source moments, NM = DN + 1 warp scans -> exclusive
-//             lane prefix Pre_m and segment totals Tot_m
-//   evaluate: u(w) = sum_q w^q [E_q + sum_{m+q odd} H[m][q] Pre_m(w)],
-//             E_q = E^c_q + sum_m B[q][m] Tot_m  (collapsed_segment's form)
-//   store   : potentials staged in shared memory, written back by one TMA
-//             bulk store per segment (or scattered through the permutation)
-// No per-mode work and no branches on the element loop.
-constexpr int kK3nStageXY = kSeg + 16;
-constexpr int kK3nStageB = kSeg + 12;
-constexpr int kK3nSu = kSeg + 4;  // staged potentials + a discard slot for non-targets
-// One TMA stage (double-buffered per warp): a segment's x / y (xy), b, merge
-// mask words, collapsed carries and the stage's mbarrier.
-struct K3nBuf {
-  double* xy;      // [kK3nStageXY]  x at slot ox, y at slot oy
-  double* bb;      // [kK3nStageB]   b at slot ob
-  double* ec;      // [kEcStride]    collapsed carries
-  uint32_t* mask;  // [kSeg / 32]
-  uint64_t* bar;
-};
-constexpr size_t kK3nBufBytes =
-    sizeof(double) * (kK3nStageXY + kK3nStageB + kEcStride) + 4 * (kSeg / 32) + 16;
-static_assert(kK3nBufBytes % 16 == 0, "k3n stage alignment");
+// Per-warp scratch of the collapsed pass's moment scan (k3c): lane moments
+// -> exclusive lane prefixes, segment totals.
 struct K3nStage {
-  double* su;      // [kK3nSu]       staged potentials (slot kSeg + 2: discard)
+  double* su;      // unused (k3c stages its potentials per chunk)
   double* scan;    // [kCollMax + 1][32] lane moments -> exclusive lane prefixes
   double* tot;     // [kCollMax + 1 (+1)] segment totals
   double* zero;    // one 0.0 (the strength slot of every target)
 };
-constexpr size_t kK3nWarpBytes =
-    2 * kK3nBufBytes + sizeof(double) * (kK3nSu + 32 * (kCollMax + 1) + (kCollMax + 1 + 1) + 2);
-static_assert(kK3nWarpBytes % 16 == 0, "k3n stage alignment");
-__device__ __forceinline__ K3nBuf k3n_buf(unsigned char* base) {
-  K3nBuf p;
-  p.xy = reinterpret_cast<double*>(base);
-  p.bb = p.xy + kK3nStageXY;
-  p.ec = p.bb + kK3nStageB;
-  p.mask = reinterpret_cast<uint32_t*>(p.ec + kEcStride);
-  p.bar = reinterpret_cast<uint64_t*>(p.mask + kSeg / 32);
-  return p;
-}
-__device__ __forceinline__ K3nStage k3n_stage(unsigned char* base) {
-  K3nStage p;
-  p.su = reinterpret_cast<double*>(base + 2 * kK3nBufBytes);
-  p.scan = p.su + kK3nSu;
-  p.tot = p.scan + 32 * (kCollMax + 1);
-  p.zero = p.tot + (kCollMax + 1 + 1);
-  return p;
-}
-
 // Exclusive warp prefix and total of NM per-lane values through shared
 // memory: lane q < 4 NM takes moment q / 4 over lanes 8 (q % 4) .. + 7 (a
 // sequential prefix of 8), then the 4 group sums of a moment are scanned by
@@ -1859,53 +1810,9 @@ __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
-// Lanes 0..2 bulk-copy the 16-byte aligned interiors of x / y / b, lane 3 the
-// mask words, lane 10 the collapsed carries, lanes 4..9 the unaligned head /
-// tail elements by 8-byte cp.async.
-// Stage slots of a segment in a K3nBuf: its targets at xy[xo ..), sources at
-// xy[yo ..), strengths at bb[bo ..).  Each set is copied as the 16-byte
-// blocks that enclose it (at most one extra element at either end, read
-// from the same 16-byte block as a valid element), so one bulk copy per
-// set and no unaligned head / tail copies.
-struct K3nSlots {
-  int xo, yo, bo;
-};
+// 8-byte phase of a pointer within its 16-byte block (0 or 1)
 __device__ __forceinline__ int phase8(const double* p) {
   return (int)((reinterpret_cast<uintptr_t>(p) >> 3) & 1);
-}
-__device__ __forceinline__ K3nSlots k3n_slots(const StreamArgs& a, const SegGeom& g) {
-  K3nSlots o;
-  const int hx = phase8(a.xs + g.ib);
-  o.xo = hx;
-  const int ys = (hx + g.nx + 1) & ~1;  // 16-byte aligned start of the y blocks
-  o.yo = ys + phase8(a.ys + g.jb);
-  o.bo = phase8(a.bs + g.jb);
-  return o;
-}
-// Issue of one segment's stage by one lane: 3 enclosing-block copies (x, y,
-// b), the merge-mask words and the collapsed carries, on the buffer's
-// mbarrier.
-__device__ __forceinline__ void k3n_issue(const StreamArgs& a, const double* ec, int64_t s,
-                                          const SegGeom& g, const K3nBuf& sp, int lane) {
-  if (lane != 0) return;
-  auto blocks = [](const double* p, int n, const double*& src) -> unsigned {
-    const uintptr_t b0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
-    const uintptr_t b1 = (reinterpret_cast<uintptr_t>(p + n) + 15) & ~(uintptr_t)15;
-    src = reinterpret_cast<const double*>(b0);
-    return n > 0 ? (unsigned)(b1 - b0) : 0u;
-  };
-  const double *sx, *sy, *sb;
-  const unsigned bx = blocks(a.xs + g.ib, g.nx, sx);
-  const unsigned by = blocks(a.ys + g.jb, g.ny, sy);
-  const unsigned bb = blocks(a.bs + g.jb, g.ny, sb);
-  const int ys = (phase8(a.xs + g.ib) + g.nx + 1) & ~1;
-  fence_proxy_async();  // earlier generic reads of the buffer before async writes
-  mbar_expect(sp.bar, bx + by + bb + 32u + 8u * kEcStride);
-  if (bx) bulk_g2s(sp.xy, sx, bx, sp.bar);
-  if (by) bulk_g2s(sp.xy + ys, sy, by, sp.bar);
-  if (bb) bulk_g2s(sp.bb, sb, bb, sp.bar);
-  bulk_g2s(sp.mask, a.seg_mask + s * (kSeg / 32), 32u, sp.bar);
-  bulk_g2s(sp.ec, ec + s * kEcStride, 8u * kEcStride, sp.bar);
 }
 
 // An opaque copy of a value: keeps a kernel-parameter constant in a register
@@ -1916,203 +1823,25 @@ __device__ __forceinline__ double in_reg(double v) {
   return r;
 }
 
-#ifndef FGT_K3N_MINB
-#define FGT_K3N_MINB 4
-#endif
-template <int DN>
-__global__ void __launch_bounds__(kThreads, FGT_K3N_MINB)
-    k3n_kernel(StreamArgs a, const double* __restrict__ ec, const CollConsts cc, OutArgs o) {
-  constexpr int NM = DN + 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* const wbase = smem_raw + (size_t)warp * kK3nWarpBytes;
-  const K3nStage sp = k3n_stage(wbase);
-  if (lane == 0) {
-    mbar_init(k3n_buf(wbase).bar);
-    mbar_init(k3n_buf(wbase + kK3nBufBytes).bar);
-    sp.zero[0] = 0.0;
-  }
-  __syncwarp();
-  const WarpWalk walk{(int64_t)blockIdx.x * kSegWarps + warp, (int64_t)gridDim.x * kSegWarps,
-                      a.nseg};
-  const int64_t S1 = a.nseg;
-  const bool all_narrow = a.nwide3 == 0;  // plan-time class counts: no lookups
-  auto next_narrow = [&](int64_t s) -> int64_t {
-    if (all_narrow) return s;
-    for (; s < S1; s = walk.next(s))
-      if (k3_narrow(seg_deg_DM(__ldg(a.seg_deg + s)))) return s;
-    return S1;
-  };
-  unsigned parity = 0;  // bit k: phase of buffer k
-  int k = 0;
-  int64_t s = next_narrow(walk.first());
-  SegGeom g;
-  if (s < S1) {
-    g = seg_geom(a, s);
-    k3n_issue(a, ec, s, g, k3n_buf(wbase), lane);
-  }
-  const unsigned az = smem_u32(sp.zero);
-  // the collapsed-form constants of this degree, held in registers
-  double Hr[NM][NM], Br[NM][NM];
-#pragma unroll
-  for (int m = 0; m < NM; ++m)
-#pragma unroll
-    for (int q = 0; q < NM; ++q) {
-      Hr[m][q] = (m + q < NM && ((m + q) & 1)) ? in_reg(cc.H[m][q]) : 0.0;
-      Br[q][m] = (m + q < NM) ? in_reg(cc.B[q][m]) : 0.0;
-    }
-  while (s < S1) {
-    // prefetch: the next segment into the other buffer (consumed last round)
-    const int64_t sn = next_narrow(walk.next(s));
-    SegGeom gn;
-    if (sn < S1) {
-      gn = seg_geom(a, sn);
-      __syncwarp();
-      k3n_issue(a, ec, sn, gn, k3n_buf(wbase + (k ^ 1) * kK3nBufBytes), lane);
-    }
-    const K3nBuf bf = k3n_buf(wbase + k * kK3nBufBytes);
-    const SegFrame f = seg_frame(g);
-    const K3nSlots so = k3n_slots(a, g);
-    mbar_wait(bf.bar, (parity >> k) & 1u);
-    parity ^= 1u << k;
-    __syncwarp();
-    if (g.len < kSeg) {
-      // partial (last) segment: lanes past the end decode as strength-0
-      // sources at the centre (their mask bits are 0)
-      for (int q = lane; q < kSeg - g.len + 8; q += 32) {
-        bf.xy[so.yo + g.ny + q] = f.zc;
-        bf.bb[so.bo + g.ny + q] = 0.0;
-      }
-      __syncwarp();
-    }
-    // ---- this lane's run from the merge mask
-    const uint32_t word = bf.mask[lane >> 2];
-    const unsigned byte = (word >> ((lane & 3) * 8)) & 0xffu;
-    const int nt = __popc(byte);
-    int incl = nt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += v;
-    }
-    const int i0 = incl - nt;
-    const int j0 = lane * kR - i0;
-    // running 32-bit shared addresses of the next target / source / strength
-    unsigned ax = smem_u32(bf.xy + so.xo + i0);
-    unsigned ay = smem_u32(bf.xy + so.yo + j0);
-    unsigned ab = smem_u32(bf.bb + so.bo + j0);
-    // ---- one pass over the run: w = z - zc, local prefix moments lp_m of the
-    // run's sources up to and including the element (exclusive for a target,
-    // whose b is 0) and the run-local part of its potential
-    //   L = sum_q w^q sum_{m+q odd} H[m][q] lp_m
-    double w[kR], L[kR];
-    double lp[NM];
-#pragma unroll
-    for (int m = 0; m < NM; ++m) lp[m] = 0.0;
-#pragma unroll
-    for (int e = 0; e < kR; ++e) {
-      const unsigned tg = (byte >> e) & 1u;
-      const double we = lds_f64(tg ? ax : ay) - f.zc;
-      double p = lds_f64(tg ? az : ab);
-      ax += tg << 3;
-      ay += (tg ^ 1u) << 3;
-      ab += (tg ^ 1u) << 3;
-      lp[0] += p;
-#pragma unroll
-      for (int m = 1; m < NM; ++m) {
-        p *= we;
-        lp[m] += p;
-      }
-      double acc = 0.0;
-#pragma unroll
-      for (int q = DN; q >= 0; --q) {
-        double c = 0.0;
-        bool any = false;
-#pragma unroll
-        for (int m = 0; m + q < NM; ++m)
-          if ((m + q) & 1) {
-            c = any ? fma(Hr[m][q], lp[m], c) : Hr[m][q] * lp[m];
-            any = true;
-          }
-        acc = q == DN ? c : fma(acc, we, c);
-      }
-      w[e] = we;
-      L[e] = acc;
-    }
-    double ecq[NM];
-#pragma unroll
-    for (int q = 0; q < NM; ++q) ecq[q] = bf.ec[q];
-    // ---- run moments (the final lp) -> exclusive lane prefix and totals
-    double pre[NM], tot[NM];
-    warp_moment_scan<NM>(sp, lane, lp, pre, tot);
-    // lane-uniform coefficients: E_q + sum_{m+q odd} H[m][q] Pre_m with
-    // E_q = E^c_q + sum_m B[q][m] Tot_m
-    double cq[NM];
-#pragma unroll
-    for (int q = 0; q < NM; ++q) {
-      double acc = ecq[q];
-#pragma unroll
-      for (int m = 0; m + q < NM; ++m) acc = fma(Br[q][m], tot[m], acc);
-#pragma unroll
-      for (int m = 0; m + q < NM; ++m)
-        if ((m + q) & 1) acc = fma(Hr[m][q], pre[m], acc);
-      cq[q] = acc;
-    }
-    // ---- potentials: L + Horner of the lane coefficients; targets only
-    const int64_t base = o.u_offset + g.ib;
-    // su slot of target i: i + off, off = u's 8-byte phase within 16 bytes,
-    // so that the bulk store's shared and global addresses share alignment
-    const int off = (int)((reinterpret_cast<uintptr_t>(o.u + base) >> 3) & 1);
-    if (lane == 0) bulk_wait_read();  // the previous segment's store has read su
-    __syncwarp();
-    {
-      unsigned at = smem_u32(sp.su + i0 + off);
-      const unsigned adis = smem_u32(sp.su + kSeg + 2);  // discard slot of non-targets
-#pragma unroll
-      for (int e = 0; e < kR; ++e) {
-        double acc = cq[DN];
-#pragma unroll
-        for (int q = DN - 1; q >= 0; --q) acc = fma(acc, w[e], cq[q]);
-        const unsigned tg = (byte >> e) & 1u;
-        sts_f64(tg ? at : adis, acc + L[e]);
-        at += tg << 3;
-      }
-    }
-    __syncwarp();
-    // ---- write back
-    if (o.tperm) {
-      const int32_t* tp = o.tperm + base;
-      for (int i = lane; i < g.nx; i += 32) o.u[tp[i]] = sp.su[i + off];
-    } else if (g.nx > 0) {
-      // interior [off, off + c) by one bulk store (16-byte aligned on both
-      // sides), a misaligned head / odd tail element by plain stores
-      double* up = o.u + base;
-      const int c = (g.nx - off) & ~1;
-      if (lane == 0) {
-        fence_proxy_async();  // the generic stores to su before the async read
-        if (c > 0) bulk_s2g(up + off, sp.su + 2 * off, 8u * (unsigned)c);
-      }
-      if (lane == 1 && off) up[0] = sp.su[1];
-      if (lane == 2 && off + c < g.nx) up[g.nx - 1] = sp.su[g.nx - 1 + off];
-    }
-    s = sn;
-    g = gn;
-    k ^= 1;
-  }
-  if (lane == 0) bulk_wait_all();
-}
-
 // ------------------------------------------- K3 narrow, CTA chunks (k3c)
 //
-// k3n's arithmetic with the staging lifted from the warp to the CTA.  A CTA
-// of kCW warps takes a chunk of kCW consecutive segments (warp w: segment
-// s0 + w); the chunk's targets, sources and strengths are three contiguous
-// ranges, and so are its merge-mask words, collapsed carries, segment starts
-// and frames, so one thread stages the whole chunk with seven bulk copies
-// (two stages, the chunk after next in flight while one is computed) and
-// writes the chunk's potentials back with one bulk store.  k3n issued five
-// copies and one store per segment through uniform-register waterfalls (a
-// quarter of its instructions); here that is per kCW segments.
+// The collapsed narrow pass with a launch-uniform degree DN (the plan's
+// highest collapsed degree over its narrow segments; a higher degree than a
+// segment needs only adds terms below 2^-52).  A CTA of kCW compute warps
+// takes a chunk of kCW consecutive segments (warp w: segment s0 + w); the
+// chunk's targets, sources and strengths are three contiguous ranges, and so
+// are its merge-mask words, collapsed carries, segment starts and frames, so
+// one thread stages the whole chunk with seven bulk copies (two stages, the
+// chunk after next in flight while one is computed) and writes the chunk's
+// potentials back with one bulk store.  Per segment, per warp:
+//   decode  : lane runs of kR merged elements from the mask and the plan's
+//             per-word target prefix counts (w = z - zc, b)
+//   moments : lane-run source moments, NM = DN + 1 -> exclusive lane prefix
+//             Pre_m and segment totals Tot_m (transposed shared-memory scan)
+//   evaluate: u(w) = sum_q w^q [E_q + sum_{m+q odd} H[m][q] Pre_m(w)],
+//             E_q = E^c_q + sum_m B[q][m] Tot_m (the B terms folded into E^c
+//             by K2m when FOLD)
+// No per-mode work and no branches on the element loop.
 constexpr int kCW = 8;
 constexpr int kCThreads = 32 * kCW;
 constexpr int kChunk = kCW * kSeg;
@@ -2330,7 +2059,7 @@ __global__ void __launch_bounds__(kCThreads + 32, FGT_K3C_MINB)
     return;
   }
   // ---------------- compute warps
-  K3nStage sp;  // the moment scan's scratch (k3n layout)
+  K3nStage sp;  // the moment scan's scratch
   sp.su = nullptr;
   sp.scan = scr0 + (size_t)warp * k3c_scratch_doubles<NM>();
   sp.tot = sp.scan + NM * 32;
@@ -3232,237 +2961,18 @@ __device__ __forceinline__ void mom_pairs(const ModeTable& mt, int k, const doub
   G = cmul(e0, cplx{ev.re + od.re, ev.im + od.im});
 }
 
-// K1b: one CTA per scan block of kMomCta = kSegWarps * kMomBlock segments,
-// kMomBlock consecutive segments per warp.  Phase 1 (per warp): every
-// segment's source moments about its centre from a ring of kK1Stages TMA
-// stages (each segment's y and beta as their enclosing 16-byte blocks; the
-// next kK1Stages - 1 segments stay in flight while one is reduced), stored
-// for the down-sweep.  Phase 2: lanes k < ne fold mode k forward (left to
-// right), lanes ne + k backward (right to left) over the warp's segments;
-// the CTA combines its warps' aggregates into the block aggregates of K2's
-// top level.  K1-wide segments take the (A, F, G) the wide K1 stored.
+// Scan blocks of the moment path: kMomCta consecutive segments (K1agg's block
+// aggregates, K2's top level, K2m's down-sweep CTAs).
 constexpr int kMomCta = kSegWarps * kMomBlock;
-#ifndef FGT_K1_STAGES
-#define FGT_K1_STAGES 2
-#endif
-#ifndef FGT_K1B_MINB
-#define FGT_K1B_MINB 5
-#endif
-#ifndef FGT_K1_SMEMRED
-#define FGT_K1_SMEMRED 1
-#endif
-constexpr int kK1Stages = FGT_K1_STAGES;
-constexpr int kK1StageD = kSeg + 4;  // doubles per set and stage
-struct K1Stage {
-  double* y;
-  double* b;
-  uint64_t* bar;
-};
-constexpr size_t kK1WarpBytes =
-    (sizeof(double) * 2 * kK1StageD * kK1Stages + 8 * kK1Stages + 15) & ~(size_t)15;
-__device__ __forceinline__ K1Stage k1_stage(unsigned char* wb, int i) {
-  K1Stage st;
-  st.y = reinterpret_cast<double*>(wb) + (size_t)i * 2 * kK1StageD;
-  st.b = st.y + kK1StageD;
-  st.bar = reinterpret_cast<uint64_t*>(wb + sizeof(double) * 2 * kK1StageD * kK1Stages) + i;
-  return st;
-}
-// One lane issues a segment's sources (y, beta) into a stage.
-__device__ __forceinline__ void k1_issue(const StreamArgs& a, const SegGeom& g, const K1Stage& st) {
-  auto blocks = [](const double* p, int n, const double*& src) -> unsigned {
-    const uintptr_t b0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
-    const uintptr_t b1 = (reinterpret_cast<uintptr_t>(p + n) + 15) & ~(uintptr_t)15;
-    src = reinterpret_cast<const double*>(b0);
-    return n > 0 ? (unsigned)(b1 - b0) : 0u;
-  };
-  const double *sy, *sb;
-  const unsigned by = blocks(a.ys + g.jb, g.ny, sy);
-  const unsigned bb = blocks(a.bs + g.jb, g.ny, sb);
-  fence_proxy_async();
-  mbar_expect(st.bar, by + bb);
-  if (by) bulk_g2s(st.y, sy, by, st.bar);
-  if (bb) bulk_g2s(st.b, sb, bb, st.bar);
-}
 
-template <int NM>
-__global__ void __launch_bounds__(kThreads, FGT_K1B_MINB) k1b_kernel(MomScanArgs q,
-                                                          const ModeTable* __restrict__ mtab) {
-  extern __shared__ __align__(16) unsigned char k1b_smem[];
-  __shared__ ModeTable mt;
-  __shared__ double smom[kSegWarps][kMomBlock][NM];
-  __shared__ Pair wagg[kSegWarps][2 * kMaxModes];
-  __shared__ __align__(16) double kred[FGT_K1_SMEMRED ? kSegWarps : 1][32 * 4];
-  load_mode_table(mtab, mt);
-  const StreamArgs& a = q.a;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ne = q.ne;
-  const bool all1 = a.nwide1 == 0;
-  unsigned char* wb = k1b_smem + (size_t)warp * kK1WarpBytes;
-  if (lane == 0)
-    for (int i = 0; i < kK1Stages; ++i) mbar_init(k1_stage(wb, i).bar);
-  __syncthreads();
-  unsigned parity = 0;
-  for (int64_t b = blockIdx.x; b < q.nblk; b += gridDim.x) {
-    const int64_t s0 = b * kMomCta + (int64_t)warp * kMomBlock;
-    const int64_t s1 = s0 + kMomBlock < a.nseg ? s0 + kMomBlock : a.nseg;
-    // ---- phase 1: moments (stage ring)
-    if (lane == 0)
-      for (int i = 0; i < kK1Stages && s0 + i < s1; ++i)
-        k1_issue(a, seg_geom(a, s0 + i), k1_stage(wb, i));
-    for (int64_t s = s0; s < s1; ++s) {
-      const int i = (int)((s - s0) % kK1Stages);
-      const K1Stage st = k1_stage(wb, i);
-      const SegGeom g = seg_geom(a, s);
-      const double zc = seg_frame(g).zc;
-      const int oy = phase8(a.ys + g.jb), ob = phase8(a.bs + g.jb);
-      mbar_wait(st.bar, (parity >> i) & 1u);
-      parity ^= 1u << i;
-      double M[NM];
-#pragma unroll
-      for (int n = 0; n < NM; ++n) M[n] = 0.0;
-#pragma unroll
-      for (int u = 0; u < kK1Per; ++u) {
-        const int j = lane + 32 * u;
-        const bool live = j < g.ny;
-        const double d = live ? st.y[oy + j] - zc : 0.0;
-        double p = live ? st.b[ob + j] : 0.0;
-        M[0] += p;
-#pragma unroll
-        for (int n = 1; n < NM; ++n) {
-          p *= d;
-          M[n] += p;
-        }
-      }
-      __syncwarp();  // stage consumed: refill it with segment s + kK1Stages
-      if (lane == 0 && s + kK1Stages < s1) k1_issue(a, seg_geom(a, s + kK1Stages), st);
-      if constexpr (FGT_K1_SMEMRED != 0 && NM <= 4) {
-        // transposed reduction: lanes park their partial moments, lane 8n + g
-        // sums lanes 4g .. 4g + 3 of moment n, three shuffles finish the rows
-        double* red = kred[warp];
-#pragma unroll
-        for (int n = 0; n < NM; ++n) red[n * 32 + lane] = M[n];
-        __syncwarp();
-        const int n = lane >> 3, g = lane & 7;
-        double v = 0.0;
-        if (n < NM) {
-          const double2 a0 = *reinterpret_cast<const double2*>(red + n * 32 + 4 * g);
-          const double2 a1 = *reinterpret_cast<const double2*>(red + n * 32 + 4 * g + 2);
-          v = (a0.x + a0.y) + (a1.x + a1.y);
-        }
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (n < NM && g == 0) {
-          q.mom[s * NM + n] = v;
-          smom[warp][s - s0][n] = v;
-        }
-        __syncwarp();
-      } else {
-#pragma unroll
-        for (int n = 0; n < NM; ++n) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) M[n] += __shfl_xor_sync(0xffffffffu, M[n], o);
-        }
-        if (lane == 0) {
-          double* out = q.mom + s * NM;
-#pragma unroll
-          for (int n = 0; n < NM; ++n) {
-            out[n] = M[n];
-            smom[warp][s - s0][n] = M[n];
-          }
-        }
-      }
-    }
-    __syncwarp();
-    // ---- phase 2: per-warp aggregates per mode, lane l holding segments
-    // s0 + 2l and s0 + 2l + 1; ordered warp reductions (forward: lower lanes
-    // first; backward: higher lanes first)
-    {
-      bool live[2], n1[2];
-      double h0[2], h1[2];
-      int64_t sg[2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        sg[i] = s0 + 2 * lane + i;
-        live[i] = sg[i] < s1;
-        n1[i] = false;
-        h0[i] = h1[i] = 0.0;
-        if (live[i]) {
-          n1[i] = all1 || k1_narrow(seg_deg_DM(__ldg(a.seg_deg + sg[i])));
-          const SegFrame f = seg_frame(seg_geom(a, sg[i]));
-          h0[i] = f.h0;
-          h1[i] = f.h1;
-        }
-      }
-      for (int k = 0; k < ne; ++k) {
-        cplx A[2], F[2], G[2];
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          if (!live[i]) {
-            A[i] = {1.0, 0.0};
-            F[i] = G[i] = {0.0, 0.0};
-          } else if (n1[i]) {
-            double M[NM];
-#pragma unroll
-            for (int n = 0; n < NM; ++n) M[n] = smom[warp][2 * lane + i][n];
-            cplx E0, E1;
-            mom_pairs<NM>(mt, k, M, h0[i], h1[i], A[i], F[i], G[i], E0, E1);
-          } else {
-            const int64_t o = (int64_t)k * a.nseg + sg[i];
-            A[i] = q.ts.A[o];
-            F[i] = q.ts.F[o];
-            G[i] = q.ts.G[o];
-          }
-        }
-        Pair fw = combine(Pair{A[0], F[0]}, Pair{A[1], F[1]});
-        Pair bw = combine(Pair{A[1], G[1]}, Pair{A[0], G[0]});
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          Pair of, ob;
-          of.a.re = __shfl_xor_sync(0xffffffffu, fw.a.re, off);
-          of.a.im = __shfl_xor_sync(0xffffffffu, fw.a.im, off);
-          of.s.re = __shfl_xor_sync(0xffffffffu, fw.s.re, off);
-          of.s.im = __shfl_xor_sync(0xffffffffu, fw.s.im, off);
-          ob.a.re = __shfl_xor_sync(0xffffffffu, bw.a.re, off);
-          ob.a.im = __shfl_xor_sync(0xffffffffu, bw.a.im, off);
-          ob.s.re = __shfl_xor_sync(0xffffffffu, bw.s.re, off);
-          ob.s.im = __shfl_xor_sync(0xffffffffu, bw.s.im, off);
-          const bool lower = (lane & off) == 0;
-          fw = lower ? combine(fw, of) : combine(of, fw);
-          bw = lower ? combine(ob, bw) : combine(bw, ob);
-        }
-        if (lane == 0) {
-          wagg[warp][k] = fw;
-          wagg[warp][ne + k] = bw;
-        }
-      }
-    }
-    __syncthreads();
-    // ---- the CTA's block aggregates: forward over warps 0.., backward over
-    // warps ..0 (warps past the end hold identities)
-    if (threadIdx.x < 2 * ne) {
-      const bool bwd = (int)threadIdx.x >= ne;
-      Pair acc{{1.0, 0.0}, {0.0, 0.0}};
-      for (int w = 0; w < kSegWarps; ++w) {
-        const int ww = bwd ? kSegWarps - 1 - w : w;
-        if (b * kMomCta + (int64_t)ww * kMomBlock < a.nseg) acc = combine(acc, wagg[ww][threadIdx.x]);
-      }
-      cplx* out = q.blkagg + ((int64_t)threadIdx.x * q.nblk + (bwd ? q.nblk - 1 - b : b)) * 2;
-      out[0] = acc.a;
-      out[1] = acc.s;
-    }
-    __syncthreads();
-  }
-}
-
-// K1c: K1b with CTA-level staging (k3c's scheme).  A CTA takes scan blocks of
-// kMomCta segments; each block is walked in chunks of kCW consecutive
+// K1c: the segment source moments with CTA-level staging (k3c's scheme).
+// Each CTA takes an equal contiguous range of chunks of kCW consecutive
 // segments (compute warp w: segment s0 + w), whose sources and strengths are
-// one contiguous range each: a producer warp stages a chunk (y, beta,
-// segment starts and frames: four bulk copies) into one of two stages while
-// the compute warps reduce the previous one to segment moments.  A warp's
-// element loop runs only over its segment's sources (warp-uniform trip
-// count), not over all kSeg merged slots.  Phase 2 (per-mode block
-// aggregates from the moments, one segment per lane) is K1b's.
+// one contiguous range each: a producer warp stages a chunk (y, beta, segment
+// starts and frames: four bulk copies) into one of two stages while the
+// compute warps reduce the previous one to segment moments.  A warp's element
+// loop runs only over its segment's sources (warp-uniform trip count), not
+// over all kSeg merged slots.  The scan blocks' aggregates follow in K1agg.
 constexpr int kK1cStageD = kChunk + 8;  // doubles per set and stage
 struct K1cHdr {
   long long jb0;
@@ -4211,12 +3721,6 @@ cudaError_t launch_chunk_carries(const cplx* aggs, int n_chunks, int ne, int ran
   return cudaGetLastError();
 }
 
-#ifndef FGT_K3_CHUNKED
-#define FGT_K3_CHUNKED 1
-#endif
-#ifndef FGT_K1_CHUNKED
-#define FGT_K1_CHUNKED 1
-#endif
 template <int DN, bool FOLD>
 static cudaError_t launch_k3c_dnf(const StreamArgs& a, const TileState& ts, const CollConsts& cc,
                                   OutArgs o, cudaStream_t st) {
@@ -4246,20 +3750,7 @@ static cudaError_t launch_k3c_dn(const StreamArgs& a, const TileState& ts, const
 template <int DN>
 static cudaError_t launch_k3n_dn(const StreamArgs& a, const TileState& ts, const CollConsts& cc,
                                  OutArgs o, cudaStream_t st, bool folded) {
-  if (FGT_K3_CHUNKED || folded) return launch_k3c_dn<DN>(a, ts, cc, o, st, folded);
-  static std::atomic<unsigned long long> done{0};
-  const size_t smem = (size_t)kSegWarps * kK3nWarpBytes;
-  cudaError_t e = ensure_dynamic_smem(k3n_kernel<DN>, (int)smem, done);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3n_kernel<DN>, kThreads, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  const int64_t want = (a.nseg + kSegWarps - 1) / kSegWarps;
-  const int64_t cap = (int64_t)num_sms() * per_sm * FGT_K3N_WAVES;
-  note_launch();
-  k3n_kernel<DN><<<(unsigned)(want < cap ? want : cap), kThreads, smem, st>>>(a, ts.ec, cc, o);
-  return cudaGetLastError();
+  return launch_k3c_dn<DN>(a, ts, cc, o, st, folded);
 }
 
 int k3n_degree(const StreamArgs& a) {
@@ -4337,7 +3828,7 @@ cudaError_t launch_moments(const StreamArgs& a, const ModeParams& P, const ModeT
   (void)mom;
   if (a.nseg == 0 || a.nwide1 == 0) return cudaSuccess;
   // K1-wide segments keep their per-mode (A, F, G) (wide K1); the narrow
-  // ones' moments are formed by K1b inside launch_mom_scan
+  // ones' moments are formed by K1c inside launch_mom_scan
   const int64_t want = (a.nseg + kSegWarps - 1) / kSegWarps;
   const int64_t cap = (int64_t)num_sms() * FGT_K1_GRID;
   note_launch();
@@ -4352,8 +3843,8 @@ static cudaError_t launch_mom_nm(const MomScanArgs& q, const ModeTable* mt, bool
                                  cudaStream_t st) {
   const unsigned grid = (unsigned)q.nblk;
   const bool top = reduce || !down || !carry_in;
-  note_launch((top ? 1 : 0) + (reduce ? (FGT_K1_CHUNKED ? 2 : 1) : 0) + (down ? 1 : 0));
-  if (reduce && FGT_K1_CHUNKED) {
+  note_launch((top ? 1 : 0) + (reduce ? 2 : 0) + (down ? 1 : 0));
+  if (reduce) {
     const size_t smem = k1c_smem_bytes<NM>();
     static std::atomic<unsigned long long> done{0};
     cudaError_t e = ensure_dynamic_smem(k1c_kernel<NM>, (int)smem, done);
@@ -4367,12 +3858,6 @@ static cudaError_t launch_mom_nm(const MomScanArgs& q, const ModeTable* mt, bool
     k1c_kernel<NM><<<(unsigned)(nchunk < cap ? nchunk : cap), kCThreads + 32, smem, st>>>(q, mt);
     k1agg_kernel<NM><<<(unsigned)((q.nblk + kCW / kAggWarps - 1) / (kCW / kAggWarps)), kCThreads, 0,
                        st>>>(q, mt);
-  } else if (reduce) {
-    const size_t smem = (size_t)kSegWarps * kK1WarpBytes;
-    static std::atomic<unsigned long long> done{0};
-    cudaError_t e = ensure_dynamic_smem(k1b_kernel<NM>, (int)smem, done);
-    if (e != cudaSuccess) return e;
-    k1b_kernel<NM><<<grid, kThreads, smem, st>>>(q, mt);
   }
   if (top) scan_top_kernel<<<2 * q.ne, 1024, 0, st>>>(sa, carry_in, totals);
   if (down) k2m_down_kernel<NM><<<grid, kThreads, 0, st>>>(q, mt);
