@@ -164,6 +164,7 @@ void build_modes(const Soe& folded, double delta, ModeParams& P, ModeTable& T) {
   const double isq = 1.0 / std::sqrt(delta);
   double smax = 0.0;
   long double gpoly[kCollDeg + 1] = {};
+  long double gl[kMaxDeg + 1] = {};
   for (int k = 0; k < ne; ++k) {
     const double sre = folded.nodes[k].real() * isq;
     const double sim = folded.nodes[k].imag() * isq;
@@ -180,6 +181,7 @@ void build_modes(const Soe& folded, double delta, ModeParams& P, ModeTable& T) {
     const std::complex<long double> lmw((long double)mw.real(), (long double)mw.imag());
     for (int n = 0; n <= kMaxDeg; ++n) {
       T.coef[k][n] = {(double)c.real(), (double)c.imag()};
+      gl[n] += (lmw * c).real();
       if (n <= kCollDeg) {
         const std::complex<long double> x = lmw * c;
         T.mwc[k][n] = {(double)x.real(), (double)x.imag()};
@@ -189,6 +191,7 @@ void build_modes(const Soe& folded, double delta, ModeParams& P, ModeTable& T) {
     }
   }
   for (int n = 0; n <= kCollDeg; ++n) T.gpoly[n] = (double)gpoly[n];
+  for (int n = 0; n <= kMaxDeg; ++n) T.gl[n] = (double)gl[n];
   P.smax = smax;
   T.smax = smax;
   fill_rmax(P);
@@ -432,6 +435,14 @@ constexpr int kFlagInts = 24;
 constexpr int kFullCheck = 16;
 unsigned long long* class_counts(fgt_plan_s* p) {
   return reinterpret_cast<unsigned long long*>(p->d_flag + 8);
+}
+
+// Packed segment degrees plus, behind them, the plan's count of segments the
+// lane-collapsed K3 flagged for the per-mode kernel (seg_fallback_count).
+int* alloc_seg_deg(int64_t nseg, cudaStream_t st) {
+  int* d = dmalloc<int>(nseg + 2, st);
+  ck(cudaMemsetAsync(d + nseg, 0, 2 * sizeof(int), st), "seg_deg tail");
+  return d;
 }
 
 StreamArgs stream_args(const fgt_plan_s* p, const double* bs) {
@@ -861,7 +872,7 @@ fgt_plan_s* pipe_chunk_plan(const double* dx, int64_t M, const double* dy, int64
     p->ntiles = (M + N + kSeg - 1) / kSeg;
     p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
     p->d_seg_z = dmalloc<double2>(p->ntiles, st);
-    p->d_seg_deg = dmalloc<int>(p->ntiles, st);
+    p->d_seg_deg = alloc_seg_deg(p->ntiles, st);
     p->d_seg_mask = dmalloc<uint32_t>(seg_mask_words(p->ntiles), st);
     p->d_xs = const_cast<double*>(dx);
     p->d_ys = const_cast<double*>(dy);
@@ -1276,7 +1287,7 @@ int plan_create_impl(const double* targets, int64_t M, const double* sources, in
       p->ntiles = (L + kSeg - 1) / kSeg;
       p->d_tile_ib = dmalloc<int64_t>(p->ntiles + 1, st);
       p->d_seg_z = dmalloc<double2>(p->ntiles, st);
-        p->d_seg_deg = dmalloc<int>(p->ntiles, st);
+        p->d_seg_deg = alloc_seg_deg(p->ntiles, st);
       p->d_seg_mask = dmalloc<uint32_t>(seg_mask_words(p->ntiles), st);
       upload_modes(p, st);
       // one read of both sets: checks + (speculative) segment metadata and
@@ -1692,7 +1703,7 @@ extern "C" int fgt_batch_create(int B, const double* targets, const int64_t* t_o
       p->d_seg_jb = dmalloc<int64_t>(nseg + 1, st);
       p->d_seg_info = dmalloc<int4>(nseg + 1, st);
       p->d_seg_z = dmalloc<double2>(nseg + 1, st);
-      p->d_seg_deg = dmalloc<int>(nseg + 1, st);
+      p->d_seg_deg = alloc_seg_deg(nseg, st);
       p->d_seg_mask = dmalloc<uint32_t>((size_t)(nseg + 1) * (kSeg / 32), st);
       Work w{st, {}};
       int64_t* d_toff = w.get<int64_t>(B + 1);

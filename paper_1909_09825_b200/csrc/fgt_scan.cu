@@ -183,8 +183,9 @@ __device__ __forceinline__ void load_mode_table(const ModeTable* g, ModeTable& s
 
 // One warp copies a transform's mode table (the rows of its ne modes) into
 // its shared-memory slot (batched plans).
-// COLL: also the collapsed-form rows (narrow K3 only).
-template <bool COLL = false>
+// EXTRA: 1 also the collapsed-form rows (narrow K3), 2 the lane-collapsed
+// polynomial gl, 3 both.
+template <int EXTRA = 0>
 __device__ __forceinline__ void warp_load_table(const ModeTable* g, ModeTable& s, int ne,
                                                 int lane) {
   __syncwarp();
@@ -195,17 +196,24 @@ __device__ __forceinline__ void warp_load_table(const ModeTable* g, ModeTable& s
   const int n = kHead + kRow * ne;
   for (int i = lane; i < n; i += 32) dst[i] = __ldg(src + i);
   if (lane == 0) s.smax = __ldg(&g->smax);
-  if constexpr (COLL) {
-  // collapsed-form rows and polynomial
-  constexpr int kOff = offsetof(ModeTable, mwc) / sizeof(double);
-  constexpr int kCRow = 2 * (kCollDeg + 1);
-  const int nc = kCRow * ne;
-  for (int i = lane; i < nc; i += 32) dst[kOff + i] = __ldg(src + kOff + i);
-  constexpr int kOffG = offsetof(ModeTable, gpoly) / sizeof(double);
-  if (lane <= kCollDeg) dst[kOffG + lane] = __ldg(src + kOffG + lane);
+  if constexpr ((EXTRA & 2) != 0) {
+    constexpr int kOffL = offsetof(ModeTable, gl) / sizeof(double);
+    if (lane <= kMaxDeg) dst[kOffL + lane] = __ldg(src + kOffL + lane);
+  }
+  if constexpr ((EXTRA & 1) != 0) {
+    // collapsed-form rows and polynomial
+    constexpr int kOff = offsetof(ModeTable, mwc) / sizeof(double);
+    constexpr int kCRow = 2 * (kCollDeg + 1);
+    const int nc = kCRow * ne;
+    for (int i = lane; i < nc; i += 32) dst[kOff + i] = __ldg(src + kOff + i);
+    constexpr int kOffG = offsetof(ModeTable, gpoly) / sizeof(double);
+    if (lane <= kCollDeg) dst[kOffG + lane] = __ldg(src + kOffG + lane);
   }
   __syncwarp();
 }
+// the lane-collapsed kernel's table slots end before the collapsed-form rows
+constexpr size_t kLaneTableBytes = offsetof(ModeTable, mwc);
+static_assert(kLaneTableBytes % 16 == 0, "lane table slot alignment");
 static_assert(offsetof(ModeTable, coef) == sizeof(double) * 4 * kMaxModes, "table layout");
 
 // Consecutive segments a warp walks in batched plans before striding.
@@ -957,15 +965,260 @@ __device__ __forceinline__ void wide_modes(const ModeTable& mt, int ne, int D, c
   }
 }
 
+
+// ------------------------------------------ lane-collapsed wide segments
+//
+// Wide segments (no segment moment form) whose LANE RUNS are narrow: with W =
+// zl - zp the width of a lane's run (the element before it to its last
+// element) and |s| W <= rmax[DL] for every lane of the warp, every exponential
+// inside a run is a degree-DL polynomial, so per run
+//   * the lane aggregates follow from the run's source moments about its last
+//     element, M_n = sum b v^n (v = zl - y >= 0, mode independent):
+//       A = e^{-s W},  F = sum_n c_n M_n,  G = A sum_n (-1)^n c_n M_n
+//     (c_n = (-s)^n / n!, the table's Taylor row): one Horner and 2 (DL + 1)
+//     multiply-adds per mode instead of a gap factor per element;
+//   * the lane carries come from a sequential scan of the 32 lane aggregates
+//     by lanes k (forward, mode k) and ne + k (backward) through shared memory
+//     (32 multiply-adds per lane) instead of 2 x 5 shuffle steps per mode;
+//   * the carries' part of a target's potential is one real polynomial in its
+//     own v,  sum_q v^q E_q,  E_q = Re sum_k c_kq mw_k (cb_k + (-1)^q A_k cf_k);
+//   * the sources of the run itself contribute b G(|z_i - z_j|) with the
+//     mode-folded polynomial G(t) = Re sum_k mw_k e^{-s_k t} = sum_n g_n t^n
+//     (ModeTable::gl): symmetric, so the 28 element pairs of a run are
+//     evaluated once each, branch-free.
+// No per-element exponentials, no per-mode chains.  Each term is bounded by
+// sum|mw| (|s| W)^n / n! |b| like the per-mode recurrences.
+// Slots of one warp: A / F / G of lane l and mode k at [l * SK + k], SK odd
+// (conflict-free both lane-wise and mode-wise).
+__host__ __device__ __forceinline__ int lane_slot_stride(int ne) { return ne | 1; }
+__host__ __device__ __forceinline__ size_t lane_slot_bytes(int ne) {
+  return sizeof(cplx) * 3 * 32 * (size_t)lane_slot_stride(ne);
+}
+
+// Lanes k < ne: forward carries of mode k (exclusive, seeded with the segment
+// carry) written over F; lanes ne + k: backward carries over G.
+__device__ __noinline__ void lane_slot_scan(cplx* slots, int ne, int lane, cplx seed) {
+  const int SK = lane_slot_stride(ne);
+  const bool fwd = lane < ne;
+  const int k = fwd ? lane : lane - ne;
+  const cplx* sA = slots + k;
+  cplx* sS = slots + (fwd ? 32 : 64) * SK + k;
+  const int step = fwd ? SK : -SK;
+  int at = fwd ? 0 : 31 * SK;
+  cplx S = seed;
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i) {
+    const cplx a = sA[at];
+    const cplx f = sS[at];
+    sS[at] = S;
+    S = cmad(a, S, f);
+    at += step;
+  }
+}
+
+// Runtime degree DL <= kMaxDeg (one body for every degree: the unrolled
+// loops leave at n > DL, the descending Horner is entered at DL).
+// Offsets v_e = zl - z_e of a run's elements (r.g holds coordinates; padding
+// sits on zl: v = 0, b = 0) and its source moments M_n = sum b v^n, n <= DL.
+__device__ __forceinline__ void lane_moments(const LaneRun& r, double zl, int DL,
+                                             double (&v)[kR], double (&M)[kMaxDeg + 1]) {
+  double pw[kR];
+  M[0] = 0.0;
+#pragma unroll
+  for (int e = 0; e < kR; ++e) {
+    v[e] = zl - r.g[e];
+    pw[e] = r.b[e];
+    M[0] += pw[e];
+  }
+#pragma unroll
+  for (int n = 1; n <= kMaxDeg; ++n) {
+    M[n] = 0.0;
+    if (n > DL) break;
+#pragma unroll
+    for (int e = 0; e < kR; ++e) {
+      pw[e] *= v[e];
+      M[n] += pw[e];
+    }
+  }
+}
+
+// One mode's lane aggregates from the moments: A = e^{-s W},
+// F = sum_n c_n M_n, G = A sum_n (-1)^n c_n M_n  (cf = the mode's Taylor row).
+__device__ __forceinline__ void lane_mode_aggregate(const cplx* cf, int DL,
+                                                    const double (&M)[kMaxDeg + 1], double W,
+                                                    cplx& A, cplx& F, cplx& G) {
+  A = cf[0];
+  cplx ev = {A.re * M[0], A.im * M[0]}, od = {0.0, 0.0};
+  double Wn = 1.0;
+#pragma unroll
+  for (int n = 1; n <= kMaxDeg; ++n) {
+    if (n > DL) break;
+    const cplx cn = cf[n];
+    Wn *= W;
+    A.re = fma(cn.re, Wn, A.re);
+    A.im = fma(cn.im, Wn, A.im);
+    if (n & 1) {
+      od.re = fma(cn.re, M[n], od.re);
+      od.im = fma(cn.im, M[n], od.im);
+    } else {
+      ev.re = fma(cn.re, M[n], ev.re);
+      ev.im = fma(cn.im, M[n], ev.im);
+    }
+  }
+  F = cplx{ev.re + od.re, ev.im + od.im};
+  G = cmul(A, cplx{ev.re - od.re, ev.im - od.im});
+}
+
+__device__ __forceinline__ void lane_collapsed(const ModeTable& mt, int ne, int DL,
+                                               const LaneRun& r, double zp, double zl, int lane,
+                                               const cplx* terms, bool noprev, cplx* slots,
+                                               double* su) {
+  const int SK = lane_slot_stride(ne);
+  cplx* sA = slots + lane * SK;
+  cplx* sF = sA + 32 * SK;
+  cplx* sG = sA + 64 * SK;
+  const double W = zl - zp;
+  double v[kR];
+  {
+    double M[kMaxDeg + 1];
+    lane_moments(r, zl, DL, v, M);
+    for (int k = 0; k < ne; ++k) {
+      cplx A, F, G;
+      lane_mode_aggregate(mt.coef[k], DL, M, W, A, F, G);
+      sA[k] = A;
+      sF[k] = F;
+      sG[k] = G;
+    }
+  }
+  // the run's own sources: pairs (i, j), i < j, t = z_j - z_i = v_i - v_j >= 0
+  double out[kR];
+#pragma unroll
+  for (int e = 0; e < kR; ++e) out[e] = 0.0;
+  const double gtop = mt.gl[DL];
+#pragma unroll
+  for (int grp = 0; grp < kR / 2; ++grp) {
+    // rows grp and kR - 1 - grp: kR - 1 pairs per group
+    double t[kR - 1], acc[kR - 1];
+    {
+      int q = 0;
+#pragma unroll
+      for (int j = grp + 1; j < kR; ++j) t[q++] = v[grp] - v[j];
+#pragma unroll
+      for (int j = kR - grp; j < kR; ++j) t[q++] = v[kR - 1 - grp] - v[j];
+    }
+#pragma unroll
+    for (int q = 0; q < kR - 1; ++q) acc[q] = gtop;
+#pragma unroll 2
+    for (int n = DL - 1; n >= 0; --n) {
+      const double gn = mt.gl[n];
+#pragma unroll
+      for (int q = 0; q < kR - 1; ++q) acc[q] = fma(acc[q], t[q], gn);
+    }
+    {
+      int q = 0;
+#pragma unroll
+      for (int j = grp + 1; j < kR; ++j, ++q) {
+        out[grp] = fma(r.b[j], acc[q], out[grp]);
+        out[j] = fma(r.b[grp], acc[q], out[j]);
+      }
+#pragma unroll
+      for (int j = kR - grp; j < kR; ++j, ++q) {
+        out[kR - 1 - grp] = fma(r.b[j], acc[q], out[kR - 1 - grp]);
+        out[j] = fma(r.b[kR - 1 - grp], acc[q], out[j]);
+      }
+    }
+  }
+  __syncwarp();
+  if (lane < 2 * ne)
+    lane_slot_scan(slots, ne, lane, (noprev && lane < ne) ? cplx{0.0, 0.0} : terms[lane]);
+  __syncwarp();
+  // carries: E_q on every lane, then one Horner per element
+  {
+    double E[kMaxDeg + 1];
+#pragma unroll
+    for (int q = 0; q <= kMaxDeg; ++q) E[q] = 0.0;
+    for (int k = 0; k < ne; ++k) {
+      const cplx mw = mt.mw[k];
+      const cplx ta = cmul(mw, cmul(sA[k], sF[k]));
+      const cplx tb = cmul(mw, sG[k]);
+      const cplx tp = {tb.re + ta.re, tb.im + ta.im};
+      const cplx tm = {tb.re - ta.re, tb.im - ta.im};
+      const cplx* cf = mt.coef[k];
+#pragma unroll
+      for (int q = 0; q <= kMaxDeg; ++q) {
+        if (q > DL) break;
+        const cplx cq = cf[q];
+        const cplx x = (q & 1) ? tm : tp;
+        E[q] = fma(cq.re, x.re, fma(-cq.im, x.im, E[q]));
+      }
+    }
+    double acc[kR];
+#pragma unroll
+    for (int e = 0; e < kR; ++e) acc[e] = 0.0;
+    switch (DL) {
+#define FGT_LH(q)                                                  \
+  case q:                                                          \
+    _Pragma("unroll") for (int e = 0; e < kR; ++e) acc[e] = fma(acc[e], v[e], E[q]); \
+    [[fallthrough]];
+      FGT_LH(16) FGT_LH(15) FGT_LH(14) FGT_LH(13) FGT_LH(12) FGT_LH(11) FGT_LH(10) FGT_LH(9)
+      FGT_LH(8) FGT_LH(7) FGT_LH(6) FGT_LH(5) FGT_LH(4) FGT_LH(3) FGT_LH(2) FGT_LH(1)
+#undef FGT_LH
+      default:
+#pragma unroll
+        for (int e = 0; e < kR; ++e) acc[e] = fma(acc[e], v[e], E[0]);
+        break;
+    }
+#pragma unroll
+    for (int e = 0; e < kR; ++e) out[e] += acc[e];
+  }
+  __syncwarp();  // every lane has read its slots: su may alias them
+  int tk = r.tfirst;
+#pragma unroll
+  for (int e = 0; e < kR; ++e)
+    if (r.tmask & (1u << e)) su[tk++] = out[e];
+}
+static_assert(kMaxDeg == 16, "lane_collapsed: Horner entry points");
+
+// false: the runs are too wide for the lane-collapsed form.
+#ifndef FGT_LANE_COLL
+#define FGT_LANE_COLL 1
+#endif
+__device__ __forceinline__ bool lane_collapsed_dispatch(const ModeParams& P, const ModeTable& mt,
+                                                        int ne, const LaneRun& r, double zp,
+                                                        double zl, int lane, const cplx* terms,
+                                                        cplx* slots, double* su) {
+  // (the shuffle keeps the degree one opaque integer: the unrolled loops of
+  // lane_collapsed then test it with one compare each)
+  // A run without a predecessor (zp = -inf: the first segment of a batched
+  // transform) starts at its own first element: nothing precedes it, so its
+  // forward carry is 0 and its A / G reach no one.
+  const bool noprev = __shfl_sync(0xffffffffu, zp == -INFINITY ? 1 : 0, 0) != 0;
+  if (zp == -INFINITY) zp = r.g[0];
+  const int DL = __shfl_sync(0xffffffffu, pick_degree(P, mt.smax, warp_max(zl - zp)), 0);
+  if (DL < 0) return false;
+  lane_collapsed(mt, ne, DL, r, zp, zl, lane, terms, noprev, slots, su);
+  return true;
+}
+
 // -------------------------------------------------------- shared memory
 
 // Per-warp region of K3: lane carries, then the output staging.
 // lane_carries: false for the collapsed narrow path (potentials only),
 // which keeps no per-lane carries in shared memory.
-__host__ __device__ __forceinline__ size_t warp_region_bytes(int ne, bool lane_carries = true) {
+// region: 0 none (collapsed narrow path), 1 lane carries (mode sums / wide),
+// 3 the lane-collapsed kernel: the lane-aggregate slots, which the output
+// staging aliases, then the segment-carry terms.
+__host__ __device__ __forceinline__ size_t warp_lead_bytes(int ne, int region) {
+  return region == 1 ? sizeof(Carry) * 32 * (size_t)ne : 0;
+}
+__host__ __device__ __forceinline__ size_t lane_region_lead(int ne) {
+  const size_t sl = lane_slot_bytes(ne), so = sizeof(double) * kSeg;
+  return sl > so ? sl : so;
+}
+__host__ __device__ __forceinline__ size_t warp_region_bytes(int ne, int region) {
+  if (region == 3) return lane_region_lead(ne) + sizeof(cplx) * 2 * kMaxModes;
   // lane carries, output staging, segment-carry terms
-  return (lane_carries ? sizeof(Carry) * 32 * (size_t)ne : 0) + sizeof(double) * kSeg +
-         sizeof(cplx) * 2 * kMaxModes;
+  return warp_lead_bytes(ne, region) + sizeof(double) * kSeg + sizeof(cplx) * 2 * kMaxModes;
 }
 
 // ------------------------------------------------------------------- K1
@@ -1202,6 +1455,81 @@ __device__ __forceinline__ void seg_aggregate_lanes(const ModeTable& mt, int ne,
   }
 }
 
+// Wide segments whose lane runs are narrow (K1): the lane aggregates of
+// lane_collapsed (one-sided moment form, runtime degree) folded across the
+// warp through shared memory, kK1Pass modes at a time: 4 sub-chains of 8
+// lanes per mode and direction (all 32 lanes fold), combined by shuffles --
+// instead of a 5-step shuffle reduction of (A, F, G) per mode.
+constexpr int kK1Pass = 4;
+constexpr int kK1SlotStride = kK1Pass | 1;
+constexpr size_t kK1SlotBytes = sizeof(cplx) * 3 * 32 * kK1SlotStride;
+__device__ __forceinline__ void seg_aggregate_slots(const ModeTable& mt, int ne, int DL, int lane,
+                                                    const LaneRun& r, double zp, double zl,
+                                                    bool noprev, cplx* slots, int64_t nseg,
+                                                    int64_t s, TileState ts) {
+  constexpr int SK = kK1SlotStride;
+  cplx* sA = slots + lane * SK;
+  cplx* sF = sA + 32 * SK;
+  cplx* sG = sA + 64 * SK;
+  const double W = zl - zp;
+  double v[kR], M[kMaxDeg + 1];
+  lane_moments(r, zl, DL, v, M);
+  const int sub = lane >> 3, dir = (lane >> 2) & 1, kk = lane & 3;
+  for (int k0 = 0; k0 < ne; k0 += kK1Pass) {
+    const int np = ne - k0 < kK1Pass ? ne - k0 : kK1Pass;
+    for (int q = 0; q < np; ++q) {
+      cplx A, F, G;
+      lane_mode_aggregate(mt.coef[k0 + q], DL, M, W, A, F, G);
+      if (noprev) {  // nothing precedes this run: its gap is infinite
+        A = cplx{0.0, 0.0};
+        G = cplx{0.0, 0.0};
+      }
+      sA[q] = A;
+      sF[q] = F;
+      sG[q] = G;
+    }
+    __syncwarp();
+    // fold this thread's 8 lanes (forward: ascending, F; backward: descending, G)
+    cplx Pr = {1.0, 0.0}, S = {0.0, 0.0};
+    if (kk < np) {
+      const cplx* pa = slots + kk;
+      const cplx* px = slots + (dir ? 64 : 32) * SK + kk;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int l = 8 * sub + (dir ? 7 - i : i);
+        const cplx a = pa[l * SK];
+        const cplx x = px[l * SK];
+        S = cmad(a, S, x);
+        Pr = cmul(Pr, a);
+      }
+    }
+    // chain the 4 sub-chains in fold order (held by sub 0 forward, sub 3 backward)
+#pragma unroll
+    for (int c = 1; c < 4; ++c) {
+      const int src = (dir ? 3 - c : c) * 8 + (lane & 7);
+      cplx Pc, Sc;
+      Pc.re = __shfl_sync(0xffffffffu, Pr.re, src);
+      Pc.im = __shfl_sync(0xffffffffu, Pr.im, src);
+      Sc.re = __shfl_sync(0xffffffffu, S.re, src);
+      Sc.im = __shfl_sync(0xffffffffu, S.im, src);
+      if (sub == (dir ? 3 : 0)) {
+        S = cmad(Pc, S, Sc);
+        Pr = cmul(Pr, Pc);
+      }
+    }
+    if (kk < np && sub == (dir ? 3 : 0)) {
+      const int64_t o = (int64_t)(k0 + kk) * nseg + s;
+      if (dir == 0) {
+        ts.A[o] = Pr;
+        ts.F[o] = S;
+      } else {
+        ts.G[o] = S;
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // K1: warps loop over segments (grid-stride; groups of kBatchGroup for
 // batched plans).  Two variants with their own register allocation: the
 // moment path for narrow segments (WIDE = false) and per-element lane
@@ -1225,6 +1553,10 @@ __global__ void __launch_bounds__(kThreads, FGT_K1_MINB)
   ModeTable& mx = batched ? tabs[warp] : tabs[0];
   int cached_tid = -1;
   const int ne = P.ne;
+  // wide variant: per-warp lane-aggregate slots behind the tables
+  cplx* slots = reinterpret_cast<cplx*>(k1_smem + sizeof(ModeTable) * (batched ? kSegWarps : 1) +
+                                        (WIDE ? kK1SlotBytes * warp : 0));
+  (void)slots;
   if constexpr (!WIDE) {
     // contiguous range per warp (metadata from L1); the next narrow
     // segment's sources are loaded into registers before this one is reduced
@@ -1299,6 +1631,18 @@ __global__ void __launch_bounds__(kThreads, FGT_K1_MINB)
         LaneRun r;
         double zp, zl;
         lane_load(a, g, s, lane, r, zp, zl);
+#if FGT_LANE_COLL
+        {
+          // lane-run moment form when every run is narrow enough
+          const bool noprev = zp == -INFINITY;  // first segment of a transform (lane 0)
+          const double zq = noprev ? r.g[0] : zp;
+          const int DLs = __shfl_sync(0xffffffffu, pick_degree(P, mx.smax, warp_max(zl - zq)), 0);
+          if (DLs >= 0) {
+            seg_aggregate_slots(mx, ne, DLs, lane, r, zq, zl, noprev, slots, a.nseg, s, ts);
+            continue;
+          }
+        }
+#endif
         // lane-run moments when the runs are narrow enough (a few degrees)
         const int DL = pick_degree(P, mx.smax, warp_max(0.5 * (zl - zp)));
         if (DL >= 0 && DL <= kLaneMomMax) {
@@ -1369,6 +1713,12 @@ __global__ void batch_modes_kernel(BatchModeBase base, const double* __restrict_
     T.gpoly[n] = gn;
   }
   T.pad2 = 0.0;
+  for (int n = 0; n <= kMaxDeg; ++n) {
+    double gn = 0.0;
+    for (int k = 0; k < kMaxModes; ++k) gn += cmul(T.mw[k], T.coef[k][n]).re;
+    T.gl[n] = gn;
+  }
+  T.pad3 = 0.0;
 }
 
 // Plan-time segment classes: counts[0] = K1 wide segments, counts[1] = K3.
@@ -1426,6 +1776,28 @@ __global__ void classify_kernel(StreamArgs a, ModeParams P, double smax, int* __
 // One segment of K3 once its lane runs are in registers (r.g = coordinates):
 // segment carries, lane carries (moment form for narrow segments, warp scans
 // for wide ones), both chains of every mode, staged write of u.
+// The segment's staged potentials (su, sorted order) to global memory.
+__device__ __forceinline__ void store_segment(const OutArgs& o, const SegGeom& g,
+                                              const double* su, int lane) {
+  __syncwarp();
+  const int64_t base = o.u_offset + g.ib;
+  if (o.tperm) {
+    const int32_t* tp = o.tperm + base;
+#pragma unroll
+    for (int q = 0; q < kSeg / 32; ++q) {
+      const int i = lane + 32 * q;
+      if (i < g.nx) o.u[tp[i]] = su[i];
+    }
+  } else {
+    double* up = o.u + base;
+#pragma unroll
+    for (int q = 0; q < kSeg / 32; ++q) {
+      const int i = lane + 32 * q;
+      if (i < g.nx) up[i] = su[i];
+    }
+  }
+}
+
 template <bool MS, bool WIDE>
 __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParams& P,
                                             const ModeTable& mx, const OutArgs& o,
@@ -1550,25 +1922,7 @@ __device__ __forceinline__ void seg_compute(const StreamArgs& a, const ModeParam
     }
     }
   }
-  if constexpr (!MS) {
-    __syncwarp();
-    const int64_t base = o.u_offset + g.ib;
-    if (o.tperm) {
-      const int32_t* tp = o.tperm + base;
-#pragma unroll
-      for (int q = 0; q < kSeg / 32; ++q) {
-        const int i = lane + 32 * q;
-        if (i < g.nx) o.u[tp[i]] = su[i];
-      }
-    } else {
-      double* up = o.u + base;
-#pragma unroll
-      for (int q = 0; q < kSeg / 32; ++q) {
-        const int i = lane + 32 * q;
-        if (i < g.nx) up[i] = su[i];
-      }
-    }
-  }
+  if constexpr (!MS) store_segment(o, g, su, lane);
   __syncwarp();
 }
 
@@ -1604,26 +1958,39 @@ __host__ __device__ constexpr bool k3_stream() {
 // bulk copies while the current one is computed.  Wide variant: grid-stride
 // (groups of kBatchGroup for batched plans) with direct loads.  Each skips
 // the other's segments.
-template <bool MS, bool WIDE>
+// LANE (wide, potentials only): the lane-collapsed form; segments whose lane
+// runs are too wide for it are flagged in seg_deg (kSegFallbackBit: a
+// property of the plan's geometry, so the flag is set once and stays) and
+// left to the wide kernel, launched behind it with a.fallback_only.
+template <bool MS, bool WIDE, bool LANE = false>
 __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
     seg_main_kernel(StreamArgs a, ModeParams P, const ModeTable* __restrict__ mtab,
                     TileState ts, OutArgs o) {
+  static_assert(!LANE || (WIDE && !MS && k3_stream<true>()), "lane-collapsed: wide, streamed");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // mode tables (slot 0 shared by the CTA for single plans, one per warp for
   // batched plans), then the per-warp regions (+ the stage when streaming)
-  ModeTable* tabs = reinterpret_cast<ModeTable*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ne = P.ne;
   const bool batched = a.mtb != nullptr;
   constexpr bool STREAM = k3_stream<WIDE>();
-  constexpr bool LC = WIDE || MS;  // lane carries kept in shared memory
+  if constexpr (WIDE && !LANE) {
+    // behind the lane-collapsed kernel: nothing flagged, nothing to do
+    if (a.fallback_only && *seg_fallback_count(a.seg_deg, a.nseg) == 0) return;
+  }
+  // lead region: lane carries (mode sums of narrow segments), none otherwise
+  constexpr int LC = LANE ? 3 : ((MS && !WIDE) ? 1 : 0);
+  constexpr size_t kTab = LANE ? kLaneTableBytes : sizeof(ModeTable);
   const size_t wbytes = warp_region_bytes(ne, LC) + (STREAM ? kStageBytes : 0);
-  unsigned char* wreg =
-      smem_raw + sizeof(ModeTable) * (batched ? kSegWarps : 1) + (size_t)warp * wbytes;
+  unsigned char* wreg = smem_raw + kTab * (batched ? kSegWarps : 1) + (size_t)warp * wbytes;
   Carry* carries = reinterpret_cast<Carry*>(wreg);
-  double* su = reinterpret_cast<double*>(wreg + (LC ? sizeof(Carry) * 32 * (size_t)ne : 0));
-  if (!batched) load_mode_table(mtab, tabs[0]);
-  ModeTable& mx = batched ? tabs[warp] : tabs[0];
+  double* su = reinterpret_cast<double*>(wreg + warp_lead_bytes(ne, LC));
+  if (!batched) {
+    const double* src = reinterpret_cast<const double*>(mtab);
+    double* dst = reinterpret_cast<double*>(smem_raw);
+    for (int i = threadIdx.x; i < (int)(kTab / sizeof(double)); i += blockDim.x) dst[i] = src[i];
+  }
+  ModeTable& mx = *reinterpret_cast<ModeTable*>(smem_raw + (batched ? kTab * warp : 0));
   int cached_tid = -1;
   if constexpr (STREAM) {
     const StagePtrs sp = stage_ptrs(wreg + warp_region_bytes(ne, LC));
@@ -1632,11 +1999,16 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
     const WarpWalk walk{(int64_t)blockIdx.x * kSegWarps + warp, (int64_t)gridDim.x * kSegWarps,
                         a.nseg};
     const int64_t S1 = a.nseg;
-    // next narrow segment at or after s (S1 if none); issues its staging
+    const int fb_only = a.fallback_only;
+    // next segment of this variant at or after s (S1 if none); issues its staging
     auto issue_next = [&](int64_t s) -> int64_t {
       for (; s < S1; s = walk.next(s)) {
-        const SegGeom g = seg_geom(a, s);
-        if (k3_narrow(seg_deg_DM(__ldg(a.seg_deg + s))) != WIDE) {
+        const int deg = __ldg(a.seg_deg + s);
+        bool mine = k3_narrow(seg_deg_DM(deg)) != WIDE;
+        if constexpr (LANE) mine = mine && !(deg & kSegFallbackBit);
+        if constexpr (WIDE && !LANE) mine = mine && (!fb_only || (deg & kSegFallbackBit));
+        if (mine) {
+          const SegGeom g = seg_geom(a, s);
           stage_issue(a, ts, ne, s, g, sp, lane);
           return s;
         }
@@ -1651,7 +2023,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
       const int deg = __ldg(a.seg_deg + s);
       const int D = seg_deg_D(deg), DM = seg_deg_DM(deg);
       if (batched && g.tid != cached_tid) {
-        warp_load_table<!MS>(a.mtb + g.tid, mx, ne, lane);
+        warp_load_table<(LANE ? 2 : (MS ? 0 : 1))>(a.mtb + g.tid, mx, ne, lane);
         cached_tid = g.tid;
       }
       cp_async_wait_all();
@@ -1664,7 +2036,27 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
       const cplx seg_c = lane < 2 * ne ? sp.car[lane] : cplx{0.0, 0.0};
       __syncwarp();  // stage free: the next segment's copies go in now
       const int64_t sn = issue_next(walk.next(s));
-      seg_compute<MS, WIDE>(a, P, mx, o, g, f, D, DM, seg_deg_DN(deg), seg_c, r, zp, zl, lane, carries, su);
+      if constexpr (LANE) {
+        (void)f;
+        (void)D;
+        (void)DM;
+        (void)carries;
+        // slots (aliased by su), then the segment-carry terms
+        cplx* slots = reinterpret_cast<cplx*>(wreg);
+        cplx* terms = reinterpret_cast<cplx*>(wreg + lane_region_lead(ne));
+        if (lane < 2 * ne) terms[lane] = seg_c;
+        __syncwarp();
+        if (lane_collapsed_dispatch(P, mx, ne, r, zp, zl, lane, terms, slots, su)) {
+          store_segment(o, g, su, lane);
+        } else if (lane == 0) {
+          const_cast<int*>(a.seg_deg)[s] = deg | kSegFallbackBit;
+          atomicAdd(seg_fallback_count(a.seg_deg, a.nseg), 1);
+        }
+        __syncwarp();
+      } else {
+        seg_compute<MS, WIDE>(a, P, mx, o, g, f, D, DM, seg_deg_DN(deg), seg_c, r, zp, zl, lane,
+                              carries, su);
+      }
       s = sn;
     }
   } else if constexpr (!WIDE) {
@@ -1689,7 +2081,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
         const SegGeom g = seg_geom(a, s);
         const SegFrame f = seg_frame(g);
         if (batched && g.tid != cached_tid) {
-          warp_load_table<!MS>(a.mtb + g.tid, mx, ne, lane);
+          warp_load_table<(MS ? 0 : 1)>(a.mtb + g.tid, mx, ne, lane);
           cached_tid = g.tid;
         }
         LaneRun r;
@@ -1716,7 +2108,7 @@ __global__ void __launch_bounds__(kThreads, WIDE ? FGT_K3W_MINB : FGT_K3_MINB)
         const SegGeom g = seg_geom(a, s);
         const SegFrame f = seg_frame(g);
         if (batched && g.tid != cached_tid) {
-          warp_load_table<!MS>(a.mtb + g.tid, mx, ne, lane);
+          warp_load_table<(MS ? 0 : 1)>(a.mtb + g.tid, mx, ne, lane);
           cached_tid = g.tid;
         }
         const cplx seg_c = load_seg_carry(ts, a.nseg, s, ne, lane);
@@ -3530,9 +3922,9 @@ CollConsts coll_consts(const double* g) {
   return c;
 }
 
-size_t seg_smem_bytes(int ne, bool batched, bool stream, bool lane_carries) {
-  return sizeof(ModeTable) * (batched ? kSegWarps : 1) +
-         (size_t)kSegWarps * (warp_region_bytes(ne, lane_carries) + (stream ? kStageBytes : 0));
+size_t seg_smem_bytes(int ne, bool batched, bool stream, int region) {
+  return (region == 3 ? kLaneTableBytes : sizeof(ModeTable)) * (batched ? kSegWarps : 1) +
+         (size_t)kSegWarps * (warp_region_bytes(ne, region) + (stream ? kStageBytes : 0));
 }
 
 cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int64_t N,
@@ -3602,8 +3994,8 @@ cudaError_t launch_batch_plan(const double* xs, const double* ys, const int64_t*
 }
 
 template <class K>
-static cudaError_t set_smem(K kernel, std::atomic<unsigned long long>& done) {
-  return ensure_dynamic_smem(kernel, (int)seg_smem_bytes(kMaxModes, true, true, true), done);
+static cudaError_t set_smem(K kernel, std::atomic<unsigned long long>& done, int region) {
+  return ensure_dynamic_smem(kernel, (int)seg_smem_bytes(kMaxModes, true, true, region), done);
 }
 
 cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const ModeTable* mt,
@@ -3616,7 +4008,8 @@ cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const Mod
   const size_t smem = sizeof(ModeTable) * (a.mtb ? kSegWarps : 1);
   if (a.nwide1 != 0) {
     note_launch();
-    seg_aggregate_kernel<true><<<grid, kThreads, smem, st>>>(a, P, mt, ts);
+    seg_aggregate_kernel<true><<<grid, kThreads, smem + kK1SlotBytes * kSegWarps, st>>>(a, P, mt,
+                                                                                        ts);
   }
   if (a.nwide1 != a.nseg) {
     note_launch();
@@ -3652,14 +4045,25 @@ cudaError_t launch_classify(const StreamArgs& a, const ModeParams& P, double sma
   return cudaGetLastError();
 }
 
-template <bool MS, bool WIDE>
+template <bool MS, bool WIDE, bool LANE = false>
 static cudaError_t launch_seg_main_variant(const StreamArgs& a, const ModeParams& P,
                                            const ModeTable* mt, TileState ts, OutArgs o,
                                            cudaStream_t st) {
+  if constexpr (WIDE && !MS && !LANE && FGT_LANE_COLL && k3_stream<true>()) {
+    // lane-collapsed kernel first; what it flags goes to the per-mode kernel
+    if (!a.fallback_only) {
+      cudaError_t e = launch_seg_main_variant<MS, WIDE, true>(a, P, mt, ts, o, st);
+      if (e != cudaSuccess) return e;
+      StreamArgs fb = a;
+      fb.fallback_only = 1;
+      return launch_seg_main_variant<MS, WIDE, false>(fb, P, mt, ts, o, st);
+    }
+  }
+  constexpr int region = LANE ? 3 : ((MS && !WIDE) ? 1 : 0);
   static std::atomic<unsigned long long> done{0};
-  cudaError_t e = set_smem(seg_main_kernel<MS, WIDE>, done);
+  cudaError_t e = set_smem(seg_main_kernel<MS, WIDE, LANE>, done, region);
   if (e != cudaSuccess) return e;
-  const size_t smem = seg_smem_bytes(P.ne, a.mtb != nullptr, k3_stream<WIDE>(), WIDE || MS);
+  const size_t smem = seg_smem_bytes(P.ne, a.mtb != nullptr, k3_stream<WIDE>(), region);
   int64_t want, cap;
   if constexpr (!k3_stream<WIDE>()) {
     const int64_t per_cta = (int64_t)kSegWarps * (a.mtb ? kBatchGroup : 1);
@@ -3668,8 +4072,8 @@ static cudaError_t launch_seg_main_variant(const StreamArgs& a, const ModeParams
   } else {
     // streaming: one resident wave, contiguous segment ranges per warp
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg_main_kernel<MS, WIDE>, kThreads,
-                                                      smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seg_main_kernel<MS, WIDE, LANE>,
+                                                      kThreads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     want = (a.nseg + kSegWarps - 1) / kSegWarps;
@@ -3677,7 +4081,7 @@ static cudaError_t launch_seg_main_variant(const StreamArgs& a, const ModeParams
   }
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   note_launch();
-  seg_main_kernel<MS, WIDE><<<grid, kThreads, smem, st>>>(a, P, mt, ts, o);
+  seg_main_kernel<MS, WIDE, LANE><<<grid, kThreads, smem, st>>>(a, P, mt, ts, o);
   return cudaGetLastError();
 }
 
@@ -3832,8 +4236,8 @@ cudaError_t launch_moments(const StreamArgs& a, const ModeParams& P, const ModeT
   const int64_t want = (a.nseg + kSegWarps - 1) / kSegWarps;
   const int64_t cap = (int64_t)num_sms() * FGT_K1_GRID;
   note_launch();
-  seg_aggregate_kernel<true><<<(unsigned)(want < cap ? want : cap), kThreads, sizeof(ModeTable),
-                               st>>>(a, P, mt, ts);
+  seg_aggregate_kernel<true><<<(unsigned)(want < cap ? want : cap), kThreads,
+                               sizeof(ModeTable) + kK1SlotBytes * kSegWarps, st>>>(a, P, mt, ts);
   return cudaGetLastError();
 }
 

@@ -38,12 +38,18 @@ struct ModeTable {
   cplx coef[kMaxModes][kMaxDeg + 1];
   double smax;  // max_k |s_k| (degree selection)
   double pad;
+  // lane-collapsed wide segments (fgt_scan.cu lane_collapsed): the mode-folded
+  // polynomial up to the highest Taylor degree, gl[n] = Re sum_k mw_k coef[k][n]
+  double gl[kMaxDeg + 1];
+  double pad3;
   // collapsed form of narrow segments (fgt_scan.cu collapsed_segment):
   // mwc[k][n] = mw_k coef[k][n], gpoly[n] = Re sum_k mwc[k][n]
+  // (the lane-collapsed kernel stages only the fields before mwc)
   cplx mwc[kMaxModes][kCollDeg + 1];
   double gpoly[kCollDeg + 1];
   double pad2;
 };
+static_assert(sizeof(ModeTable) <= 4096, "ModeTable is passed as a kernel parameter");
 // tables are staged ahead of 16-byte aligned stages in shared memory
 static_assert(sizeof(ModeTable) % 16 == 0, "ModeTable size must be a multiple of 16 bytes");
 
@@ -53,6 +59,13 @@ static_assert(sizeof(ModeTable) % 16 == 0, "ModeTable size must be a multiple of
 //   B[q][m] = (-1)^q C(m+q, m) g_{m+q}                  total-moment terms
 // (fgt_scan.cu, collapsed form).  Passed as a kernel parameter: the FMAs read
 // them from the constant bank.
+constexpr int kSegFallbackBit = 1 << 30;  // seg_deg: not lane-collapsible (set by K3)
+// seg_deg is allocated with two trailing ints; the second counts the flagged
+// segments of the plan (the per-mode kernel behind the lane-collapsed one
+// leaves at once while it is 0).
+__host__ __device__ inline int* seg_fallback_count(const int* seg_deg, int64_t nseg) {
+  return const_cast<int*>(seg_deg) + nseg + 1;
+}
 constexpr int kCollMax = 6;   // highest collapsed degree of the narrow K3
 constexpr int kEcStride = 8;  // doubles per segment of the collapsed carries
 struct CollConsts {
@@ -87,6 +100,9 @@ struct StreamArgs {
   // plan-time degrees per segment: (D + 1) | (DM + 1) << 8 with D the Taylor
   // degree of its gap factors and DM its moment degree (-1 = none)
   const int* seg_deg = nullptr;
+  // wide K3 after the lane-collapsed kernel: only the segments that kernel
+  // flagged (kSegFallbackBit of seg_deg: lane runs too wide for it)
+  int fallback_only = 0;
   // classify_kernel only: segment 0's zprev is its own first element (a
   // plan without a predecessor, classified before zprev0 is known on the host)
   bool zprev0_first = false;
@@ -136,7 +152,7 @@ int64_t scan_blocks(int64_t nseg);
 size_t tile_state_elems(int64_t nseg, int ne);
 TileState tile_state_carve(cplx* base, int64_t nseg, int ne);
 
-size_t seg_smem_bytes(int ne, bool batched, bool stream, bool lane_carries = true);
+size_t seg_smem_bytes(int ne, bool batched, bool stream, int region = 1);
 
 cudaError_t launch_partition(const double* xs, int64_t M, const double* ys, int64_t N,
                              int64_t seg, int64_t nseg, int64_t* seg_ib, cudaStream_t st);
