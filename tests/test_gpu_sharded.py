@@ -18,9 +18,14 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-def worker(rank, world, port, shards, delta, ne, q):
+def worker(rank, world, port, shards, delta, ne, q, backend="gloo"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1909_09825_b200 import cf_soe, fold
     from paper_1909_09825_b200.sharded import sharded_transform
     x, y, a = (torch.from_numpy(v).cuda() for v in shards[rank])
@@ -36,8 +41,10 @@ def free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world", [1, 2])
-def test_sharded_transform_on_device(world):
+@pytest.mark.parametrize("world,backend", [(1, "gloo"), (2, "gloo"), (1, "nccl")])
+def test_sharded_transform_on_device(world, backend):
+    """(1, "nccl"): the NCCL data plane itself -- all_gather / all_to_all_single /
+    all_reduce on device tensors, no host copies -- on the one GPU of the box."""
     from paper_1909_09825_b200.transform import uniform_points_array as up
     n, m, delta, ne = 200003, 150001, 1e-4, 6
     x, y = up(n, 21, 3), up(m, 21, 0)
@@ -48,7 +55,7 @@ def test_sharded_transform_on_device(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, world, port, shards, delta, ne, q))
+    procs = [ctx.Process(target=worker, args=(r, world, port, shards, delta, ne, q, backend))
              for r in range(world)]
     for p in procs:
         p.start()
