@@ -1016,12 +1016,13 @@ __device__ __noinline__ void lane_slot_scan(cplx* slots, int ne, int lane, cplx 
   }
 }
 
-// Runtime degree DL <= kMaxDeg (one body for every degree: the unrolled
-// loops leave at n > DL, the descending Horner is entered at DL).
+// Compile-time degree DL <= kMaxDeg (lane_degree_bucket: the runtime degree
+// rounded up to the next instantiated one; every loop is straight-line code).
 // Offsets v_e = zl - z_e of a run's elements (r.g holds coordinates; padding
 // sits on zl: v = 0, b = 0) and its source moments M_n = sum b v^n, n <= DL.
-__device__ __forceinline__ void lane_moments(const LaneRun& r, double zl, int DL,
-                                             double (&v)[kR], double (&M)[kMaxDeg + 1]) {
+template <int DL>
+__device__ __forceinline__ void lane_moments(const LaneRun& r, double zl, double (&v)[kR],
+                                             double (&M)[DL + 1]) {
   double pw[kR];
   M[0] = 0.0;
 #pragma unroll
@@ -1031,9 +1032,8 @@ __device__ __forceinline__ void lane_moments(const LaneRun& r, double zl, int DL
     M[0] += pw[e];
   }
 #pragma unroll
-  for (int n = 1; n <= kMaxDeg; ++n) {
+  for (int n = 1; n <= DL; ++n) {
     M[n] = 0.0;
-    if (n > DL) break;
 #pragma unroll
     for (int e = 0; e < kR; ++e) {
       pw[e] *= v[e];
@@ -1044,19 +1044,18 @@ __device__ __forceinline__ void lane_moments(const LaneRun& r, double zl, int DL
 
 // One mode's lane aggregates from the moments: A = e^{-s W},
 // F = sum_n c_n M_n, G = A sum_n (-1)^n c_n M_n  (cf = the mode's Taylor row).
-__device__ __forceinline__ void lane_mode_aggregate(const cplx* cf, int DL,
-                                                    const double (&M)[kMaxDeg + 1], double W,
-                                                    cplx& A, cplx& F, cplx& G) {
-  A = cf[0];
-  cplx ev = {A.re * M[0], A.im * M[0]}, od = {0.0, 0.0};
-  double Wn = 1.0;
+template <int DL>
+__device__ __forceinline__ void lane_mode_aggregate(const cplx* cf, const double (&M)[DL + 1],
+                                                    double W, cplx& A, cplx& F, cplx& G) {
+  const cplx c0 = cf[0];
+  A = cf[DL];
+  cplx ev = {c0.re * M[0], c0.im * M[0]}, od = {0.0, 0.0};
 #pragma unroll
-  for (int n = 1; n <= kMaxDeg; ++n) {
-    if (n > DL) break;
+  for (int n = DL; n >= 1; --n) {
     const cplx cn = cf[n];
-    Wn *= W;
-    A.re = fma(cn.re, Wn, A.re);
-    A.im = fma(cn.im, Wn, A.im);
+    const cplx lo = cf[n - 1];
+    A.re = fma(A.re, W, lo.re);
+    A.im = fma(A.im, W, lo.im);
     if (n & 1) {
       od.re = fma(cn.re, M[n], od.re);
       od.im = fma(cn.im, M[n], od.im);
@@ -1069,6 +1068,63 @@ __device__ __forceinline__ void lane_mode_aggregate(const cplx* cf, int DL,
   G = cmul(A, cplx{ev.re - od.re, ev.im - od.im});
 }
 
+// The instantiated degrees: a runtime degree runs at the next one at or above
+// it (a higher Taylor degree only lowers the truncation error).
+#define FGT_LANE_DEGREES(X) X(4) X(6) X(8) X(10) X(12) X(14) X(16)
+static_assert(kMaxDeg == 16, "lane-collapsed degree buckets");
+__device__ __forceinline__ int lane_degree_bucket(int DL) { return DL <= 4 ? 4 : ((DL + 1) & ~1); }
+
+// Phase A of lane_collapsed: the run's moments and every mode's aggregates
+// into the slots.
+template <int DL>
+__device__ __forceinline__ void lane_phase_aggregates(const ModeTable& mt, int ne,
+                                                      const LaneRun& r, double zl, double W,
+                                                      cplx* sA, cplx* sF, cplx* sG) {
+  double v[kR], M[DL + 1];
+  lane_moments<DL>(r, zl, v, M);
+  for (int k = 0; k < ne; ++k) {
+    cplx A, F, G;
+    lane_mode_aggregate<DL>(mt.coef[k], M, W, A, F, G);
+    sA[k] = A;
+    sF[k] = F;
+    sG[k] = G;
+  }
+}
+
+// Phase C: the carries' polynomial E_q (every lane its own), one Horner per
+// element, added to out.
+template <int DL>
+__device__ __forceinline__ void lane_phase_carries(const ModeTable& mt, int ne,
+                                                   const double (&v)[kR], const cplx* sA,
+                                                   const cplx* sF, const cplx* sG,
+                                                   double (&out)[kR]) {
+  double E[DL + 1];
+#pragma unroll
+  for (int q = 0; q <= DL; ++q) E[q] = 0.0;
+  for (int k = 0; k < ne; ++k) {
+    const cplx mw = mt.mw[k];
+    const cplx ta = cmul(mw, cmul(sA[k], sF[k]));
+    const cplx tb = cmul(mw, sG[k]);
+    const cplx tp = {tb.re + ta.re, tb.im + ta.im};
+    const cplx tm = {tb.re - ta.re, tb.im - ta.im};
+    const cplx* cf = mt.coef[k];
+#pragma unroll
+    for (int q = 0; q <= DL; ++q) {
+      const cplx cq = cf[q];
+      const cplx x = (q & 1) ? tm : tp;
+      E[q] = fma(cq.re, x.re, fma(-cq.im, x.im, E[q]));
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < kR; ++e) {
+    double acc = E[DL];
+#pragma unroll
+    for (int q = DL - 1; q >= 0; --q) acc = fma(acc, v[e], E[q]);
+    out[e] += acc;
+  }
+}
+
+// DL: a degree of FGT_LANE_DEGREES (warp uniform).
 __device__ __forceinline__ void lane_collapsed(const ModeTable& mt, int ne, int DL,
                                                const LaneRun& r, double zp, double zl, int lane,
                                                const cplx* terms, bool noprev, cplx* slots,
@@ -1078,19 +1134,20 @@ __device__ __forceinline__ void lane_collapsed(const ModeTable& mt, int ne, int 
   cplx* sF = sA + 32 * SK;
   cplx* sG = sA + 64 * SK;
   const double W = zl - zp;
-  double v[kR];
-  {
-    double M[kMaxDeg + 1];
-    lane_moments(r, zl, DL, v, M);
-    for (int k = 0; k < ne; ++k) {
-      cplx A, F, G;
-      lane_mode_aggregate(mt.coef[k], DL, M, W, A, F, G);
-      sA[k] = A;
-      sF[k] = F;
-      sG[k] = G;
-    }
+  switch (DL) {
+#define FGT_LC_CASE(d)                                              \
+  case d:                                                           \
+    lane_phase_aggregates<d>(mt, ne, r, zl, W, sA, sF, sG);        \
+    break;
+    FGT_LANE_DEGREES(FGT_LC_CASE)
+#undef FGT_LC_CASE
   }
+  double v[kR];
+#pragma unroll
+  for (int e = 0; e < kR; ++e) v[e] = zl - r.g[e];
   // the run's own sources: pairs (i, j), i < j, t = z_j - z_i = v_i - v_j >= 0
+  // (one loop for every degree: the polynomial's coefficients come from
+  // shared memory)
   double out[kR];
 #pragma unroll
   for (int e = 0; e < kR; ++e) out[e] = 0.0;
@@ -1132,44 +1189,13 @@ __device__ __forceinline__ void lane_collapsed(const ModeTable& mt, int ne, int 
   if (lane < 2 * ne)
     lane_slot_scan(slots, ne, lane, (noprev && lane < ne) ? cplx{0.0, 0.0} : terms[lane]);
   __syncwarp();
-  // carries: E_q on every lane, then one Horner per element
-  {
-    double E[kMaxDeg + 1];
-#pragma unroll
-    for (int q = 0; q <= kMaxDeg; ++q) E[q] = 0.0;
-    for (int k = 0; k < ne; ++k) {
-      const cplx mw = mt.mw[k];
-      const cplx ta = cmul(mw, cmul(sA[k], sF[k]));
-      const cplx tb = cmul(mw, sG[k]);
-      const cplx tp = {tb.re + ta.re, tb.im + ta.im};
-      const cplx tm = {tb.re - ta.re, tb.im - ta.im};
-      const cplx* cf = mt.coef[k];
-#pragma unroll
-      for (int q = 0; q <= kMaxDeg; ++q) {
-        if (q > DL) break;
-        const cplx cq = cf[q];
-        const cplx x = (q & 1) ? tm : tp;
-        E[q] = fma(cq.re, x.re, fma(-cq.im, x.im, E[q]));
-      }
-    }
-    double acc[kR];
-#pragma unroll
-    for (int e = 0; e < kR; ++e) acc[e] = 0.0;
-    switch (DL) {
-#define FGT_LH(q)                                                  \
-  case q:                                                          \
-    _Pragma("unroll") for (int e = 0; e < kR; ++e) acc[e] = fma(acc[e], v[e], E[q]); \
-    [[fallthrough]];
-      FGT_LH(16) FGT_LH(15) FGT_LH(14) FGT_LH(13) FGT_LH(12) FGT_LH(11) FGT_LH(10) FGT_LH(9)
-      FGT_LH(8) FGT_LH(7) FGT_LH(6) FGT_LH(5) FGT_LH(4) FGT_LH(3) FGT_LH(2) FGT_LH(1)
-#undef FGT_LH
-      default:
-#pragma unroll
-        for (int e = 0; e < kR; ++e) acc[e] = fma(acc[e], v[e], E[0]);
-        break;
-    }
-#pragma unroll
-    for (int e = 0; e < kR; ++e) out[e] += acc[e];
+  switch (DL) {
+#define FGT_LC_CASE(d)                                              \
+  case d:                                                           \
+    lane_phase_carries<d>(mt, ne, v, sA, sF, sG, out);             \
+    break;
+    FGT_LANE_DEGREES(FGT_LC_CASE)
+#undef FGT_LC_CASE
   }
   __syncwarp();  // every lane has read its slots: su may alias them
   int tk = r.tfirst;
@@ -1177,7 +1203,6 @@ __device__ __forceinline__ void lane_collapsed(const ModeTable& mt, int ne, int 
   for (int e = 0; e < kR; ++e)
     if (r.tmask & (1u << e)) su[tk++] = out[e];
 }
-static_assert(kMaxDeg == 16, "lane_collapsed: Horner entry points");
 
 // false: the runs are too wide for the lane-collapsed form.
 #ifndef FGT_LANE_COLL
@@ -1196,7 +1221,7 @@ __device__ __forceinline__ bool lane_collapsed_dispatch(const ModeParams& P, con
   if (zp == -INFINITY) zp = r.g[0];
   const int DL = __shfl_sync(0xffffffffu, pick_degree(P, mt.smax, warp_max(zl - zp)), 0);
   if (DL < 0) return false;
-  lane_collapsed(mt, ne, DL, r, zp, zl, lane, terms, noprev, slots, su);
+  lane_collapsed(mt, ne, lane_degree_bucket(DL), r, zp, zl, lane, terms, noprev, slots, su);
   return true;
 }
 
@@ -1456,30 +1481,31 @@ __device__ __forceinline__ void seg_aggregate_lanes(const ModeTable& mt, int ne,
 }
 
 // Wide segments whose lane runs are narrow (K1): the lane aggregates of
-// lane_collapsed (one-sided moment form, runtime degree) folded across the
+// lane_collapsed (one-sided moment form, degree buckets) folded across the
 // warp through shared memory, kK1Pass modes at a time: 4 sub-chains of 8
 // lanes per mode and direction (all 32 lanes fold), combined by shuffles --
 // instead of a 5-step shuffle reduction of (A, F, G) per mode.
 constexpr int kK1Pass = 4;
 constexpr int kK1SlotStride = kK1Pass | 1;
 constexpr size_t kK1SlotBytes = sizeof(cplx) * 3 * 32 * kK1SlotStride;
-__device__ __forceinline__ void seg_aggregate_slots(const ModeTable& mt, int ne, int DL, int lane,
-                                                    const LaneRun& r, double zp, double zl,
-                                                    bool noprev, cplx* slots, int64_t nseg,
-                                                    int64_t s, TileState ts) {
+template <int DL>
+__device__ __forceinline__ void seg_aggregate_slots(const ModeTable& mt, int ne, int lane,
+                                                 const LaneRun& r, double zp, double zl,
+                                                 bool noprev, cplx* slots, int64_t nseg, int64_t s,
+                                                 TileState ts) {
   constexpr int SK = kK1SlotStride;
   cplx* sA = slots + lane * SK;
   cplx* sF = sA + 32 * SK;
   cplx* sG = sA + 64 * SK;
   const double W = zl - zp;
-  double v[kR], M[kMaxDeg + 1];
-  lane_moments(r, zl, DL, v, M);
+  double v[kR], M[DL + 1];
+  lane_moments<DL>(r, zl, v, M);
   const int sub = lane >> 3, dir = (lane >> 2) & 1, kk = lane & 3;
   for (int k0 = 0; k0 < ne; k0 += kK1Pass) {
     const int np = ne - k0 < kK1Pass ? ne - k0 : kK1Pass;
     for (int q = 0; q < np; ++q) {
       cplx A, F, G;
-      lane_mode_aggregate(mt.coef[k0 + q], DL, M, W, A, F, G);
+      lane_mode_aggregate<DL>(mt.coef[k0 + q], M, W, A, F, G);
       if (noprev) {  // nothing precedes this run: its gap is infinite
         A = cplx{0.0, 0.0};
         G = cplx{0.0, 0.0};
@@ -1638,7 +1664,14 @@ __global__ void __launch_bounds__(kThreads, FGT_K1_MINB)
           const double zq = noprev ? r.g[0] : zp;
           const int DLs = __shfl_sync(0xffffffffu, pick_degree(P, mx.smax, warp_max(zl - zq)), 0);
           if (DLs >= 0) {
-            seg_aggregate_slots(mx, ne, DLs, lane, r, zq, zl, noprev, slots, a.nseg, s, ts);
+            switch (lane_degree_bucket(DLs)) {
+#define FGT_LC_CASE(d)                                                                 \
+  case d:                                                                              \
+    seg_aggregate_slots<d>(mx, ne, lane, r, zq, zl, noprev, slots, a.nseg, s, ts);    \
+    break;
+              FGT_LANE_DEGREES(FGT_LC_CASE)
+#undef FGT_LC_CASE
+            }
             continue;
           }
         }
