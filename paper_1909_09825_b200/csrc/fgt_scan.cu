@@ -1091,38 +1091,59 @@ __device__ __forceinline__ void lane_phase_aggregates(const ModeTable& mt, int n
   }
 }
 
-// Phase C: the carries' polynomial E_q (every lane its own), one Horner per
-// element, added to out.
-template <int DL>
-__device__ __forceinline__ void lane_phase_carries(const ModeTable& mt, int ne,
+// Phase C: the carries' polynomial sum_q v^q E_q,
+// E_q = Re sum_k c_kq mw_k (cb_k + (-1)^q A_k cf_k), one Horner per element
+// with E_q formed on the way down (tp / tm = mw (cb +- A cf) of every mode in
+// registers; NE = the launch's mode count).  The loop over the degree is
+// rolled (DL even): one body for every degree.
+template <int NE>
+__device__ __forceinline__ void lane_phase_carries(const ModeTable& mt, int DL,
                                                    const double (&v)[kR], const cplx* sA,
                                                    const cplx* sF, const cplx* sG,
                                                    double (&out)[kR]) {
-  double E[DL + 1];
+  cplx tp[NE], tm[NE];
 #pragma unroll
-  for (int q = 0; q <= DL; ++q) E[q] = 0.0;
-  for (int k = 0; k < ne; ++k) {
+  for (int k = 0; k < NE; ++k) {
     const cplx mw = mt.mw[k];
     const cplx ta = cmul(mw, cmul(sA[k], sF[k]));
     const cplx tb = cmul(mw, sG[k]);
-    const cplx tp = {tb.re + ta.re, tb.im + ta.im};
-    const cplx tm = {tb.re - ta.re, tb.im - ta.im};
-    const cplx* cf = mt.coef[k];
+    tp[k] = cplx{tb.re + ta.re, tb.im + ta.im};
+    tm[k] = cplx{tb.re - ta.re, tb.im - ta.im};
+  }
+  double acc[kR];
+  {
+    double Er = 0.0, Ei = 0.0;  // q = DL (even)
 #pragma unroll
-    for (int q = 0; q <= DL; ++q) {
-      const cplx cq = cf[q];
-      const cplx x = (q & 1) ? tm : tp;
-      E[q] = fma(cq.re, x.re, fma(-cq.im, x.im, E[q]));
+    for (int k = 0; k < NE; ++k) {
+      const cplx c = mt.coef[k][DL];
+      Er = fma(c.re, tp[k].re, Er);
+      Ei = fma(c.im, tp[k].im, Ei);
     }
+#pragma unroll
+    for (int e = 0; e < kR; ++e) acc[e] = Er - Ei;
+  }
+#pragma unroll 1
+  for (int q = DL - 1; q > 0; q -= 2) {
+    double Eor = 0.0, Eoi = 0.0, Eer = 0.0, Eei = 0.0;  // q odd, q - 1 even
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+      const cplx co = mt.coef[k][q];
+      const cplx ce = mt.coef[k][q - 1];
+      Eor = fma(co.re, tm[k].re, Eor);
+      Eoi = fma(co.im, tm[k].im, Eoi);
+      Eer = fma(ce.re, tp[k].re, Eer);
+      Eei = fma(ce.im, tp[k].im, Eei);
+    }
+    const double Eo = Eor - Eoi, Ee = Eer - Eei;
+#pragma unroll
+    for (int e = 0; e < kR; ++e) acc[e] = fma(fma(acc[e], v[e], Eo), v[e], Ee);
   }
 #pragma unroll
-  for (int e = 0; e < kR; ++e) {
-    double acc = E[DL];
-#pragma unroll
-    for (int q = DL - 1; q >= 0; --q) acc = fma(acc, v[e], E[q]);
-    out[e] += acc;
-  }
+  for (int e = 0; e < kR; ++e) out[e] += acc[e];
 }
+// the mode counts the carries phase is instantiated for
+#define FGT_LANE_MODES(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)
+static_assert(kMaxModes == 8 && kMaxDeg % 2 == 0, "lane-collapsed form");
 
 // DL: a degree of FGT_LANE_DEGREES (warp uniform).
 __device__ __forceinline__ void lane_collapsed(const ModeTable& mt, int ne, int DL,
@@ -1189,12 +1210,12 @@ __device__ __forceinline__ void lane_collapsed(const ModeTable& mt, int ne, int 
   if (lane < 2 * ne)
     lane_slot_scan(slots, ne, lane, (noprev && lane < ne) ? cplx{0.0, 0.0} : terms[lane]);
   __syncwarp();
-  switch (DL) {
-#define FGT_LC_CASE(d)                                              \
-  case d:                                                           \
-    lane_phase_carries<d>(mt, ne, v, sA, sF, sG, out);             \
+  switch (ne) {
+#define FGT_LC_CASE(m)                                              \
+  case m:                                                           \
+    lane_phase_carries<m>(mt, DL, v, sA, sF, sG, out);             \
     break;
-    FGT_LANE_DEGREES(FGT_LC_CASE)
+    FGT_LANE_MODES(FGT_LC_CASE)
 #undef FGT_LC_CASE
   }
   __syncwarp();  // every lane has read its slots: su may alias them
