@@ -1173,36 +1173,46 @@ __device__ __forceinline__ void lane_collapsed(const ModeTable& mt, int ne, int 
 #pragma unroll
   for (int e = 0; e < kR; ++e) out[e] = 0.0;
   const double gtop = mt.gl[DL];
+  static_assert(kR % 4 == 0, "pair groups are evaluated two at a time");
 #pragma unroll
-  for (int grp = 0; grp < kR / 2; ++grp) {
-    // rows grp and kR - 1 - grp: kR - 1 pairs per group
-    double t[kR - 1], acc[kR - 1];
+  for (int grp = 0; grp < kR / 2; grp += 2) {
+    // rows grp and kR - 1 - grp, rows grp + 1 and kR - 2 - grp: kR - 1 pairs
+    // each, 2 (kR - 1) independent Horner chains per loop pass
+    constexpr int NP = 2 * (kR - 1);
+    double t[NP], acc[NP];
     {
       int q = 0;
 #pragma unroll
-      for (int j = grp + 1; j < kR; ++j) t[q++] = v[grp] - v[j];
+      for (int h = 0; h < 2; ++h) {
 #pragma unroll
-      for (int j = kR - grp; j < kR; ++j) t[q++] = v[kR - 1 - grp] - v[j];
+        for (int j = grp + h + 1; j < kR; ++j) t[q++] = v[grp + h] - v[j];
+#pragma unroll
+        for (int j = kR - grp - h; j < kR; ++j) t[q++] = v[kR - 1 - grp - h] - v[j];
+      }
     }
 #pragma unroll
-    for (int q = 0; q < kR - 1; ++q) acc[q] = gtop;
-#pragma unroll 2
+    for (int q = 0; q < NP; ++q) acc[q] = gtop;
+#pragma unroll 1
     for (int n = DL - 1; n >= 0; --n) {
       const double gn = mt.gl[n];
 #pragma unroll
-      for (int q = 0; q < kR - 1; ++q) acc[q] = fma(acc[q], t[q], gn);
+      for (int q = 0; q < NP; ++q) acc[q] = fma(acc[q], t[q], gn);
     }
     {
       int q = 0;
 #pragma unroll
-      for (int j = grp + 1; j < kR; ++j, ++q) {
-        out[grp] = fma(r.b[j], acc[q], out[grp]);
-        out[j] = fma(r.b[grp], acc[q], out[j]);
-      }
+      for (int h = 0; h < 2; ++h) {
+        const int lo = grp + h, hi = kR - 1 - grp - h;
 #pragma unroll
-      for (int j = kR - grp; j < kR; ++j, ++q) {
-        out[kR - 1 - grp] = fma(r.b[j], acc[q], out[kR - 1 - grp]);
-        out[j] = fma(r.b[kR - 1 - grp], acc[q], out[j]);
+        for (int j = lo + 1; j < kR; ++j, ++q) {
+          out[lo] = fma(r.b[j], acc[q], out[lo]);
+          out[j] = fma(r.b[lo], acc[q], out[j]);
+        }
+#pragma unroll
+        for (int j = hi + 1; j < kR; ++j, ++q) {
+          out[hi] = fma(r.b[j], acc[q], out[hi]);
+          out[j] = fma(r.b[hi], acc[q], out[j]);
+        }
       }
     }
   }
