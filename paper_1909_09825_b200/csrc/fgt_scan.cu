@@ -1082,6 +1082,7 @@ __device__ __forceinline__ void lane_phase_aggregates(const ModeTable& mt, int n
                                                       cplx* sA, cplx* sF, cplx* sG) {
   double v[kR], M[DL + 1];
   lane_moments<DL>(r, zl, v, M);
+#pragma unroll 2
   for (int k = 0; k < ne; ++k) {
     cplx A, F, G;
     lane_mode_aggregate<DL>(mt.coef[k], M, W, A, F, G);
