@@ -1073,6 +1073,9 @@ __device__ __forceinline__ void lane_mode_aggregate(const cplx* cf, const double
 #define FGT_LANE_DEGREES(X) X(4) X(6) X(8) X(10) X(12) X(14) X(16)
 static_assert(kMaxDeg == 16, "lane-collapsed degree buckets");
 __device__ __forceinline__ int lane_degree_bucket(int DL) { return DL <= 4 ? 4 : ((DL + 1) & ~1); }
+// K1 runs only the moments / aggregates phase: multiples of 4 (fewer bodies in
+// flight; measured cfg 5 K1 4.26 -> 4.08 ms, while K3 loses at these: 10.75 -> 10.91 ms)
+__device__ __forceinline__ int lane_degree_bucket4(int DL) { return (DL + 3) & ~3; }
 
 // Phase A of lane_collapsed: the run's moments and every mode's aggregates
 // into the slots.
@@ -1649,15 +1652,18 @@ __global__ void __launch_bounds__(kThreads, FGT_K1_MINB)
         warp_load_table(a.mtb + g.tid, mx, ne, lane);
         cached_tid = g.tid;
       }
-      switch (DM) {
+      // even moment degrees only (an odd one runs at the next even one: a
+      // higher degree only lowers the truncation error, and half the bodies
+      // keep the kernel within the instruction cache)
+      static_assert(FGT_K1_MAXDM % 2 == 0, "K1 moment degree buckets");
+      switch ((DM + 1) & ~1) {
 #define FGT_K1(n)                                                     \
   case n:                                                             \
     if constexpr (n <= FGT_K1_MAXDM)                                  \
       seg_aggregate_from<n>(f, mx, ne, lane, a.nseg, s, ts, yv, bv);  \
     break;
-        FGT_K1(0) FGT_K1(1) FGT_K1(2) FGT_K1(3) FGT_K1(4) FGT_K1(5) FGT_K1(6) FGT_K1(7)
-        FGT_K1(8) FGT_K1(9) FGT_K1(10) FGT_K1(11) FGT_K1(12) FGT_K1(13) FGT_K1(14)
-        FGT_K1(15) FGT_K1(16)
+        FGT_K1(0) FGT_K1(2) FGT_K1(4) FGT_K1(6) FGT_K1(8) FGT_K1(10) FGT_K1(12) FGT_K1(14)
+        FGT_K1(16)
 #undef FGT_K1
         default:
           break;
@@ -1696,7 +1702,7 @@ __global__ void __launch_bounds__(kThreads, FGT_K1_MINB)
           const double zq = noprev ? r.g[0] : zp;
           const int DLs = __shfl_sync(0xffffffffu, pick_degree(P, mx.smax, warp_max(zl - zq)), 0);
           if (DLs >= 0) {
-            switch (lane_degree_bucket(DLs)) {
+            switch (DLs <= 4 ? 4 : lane_degree_bucket4(DLs)) {
 #define FGT_LC_CASE(d)                                                                 \
   case d:                                                                              \
     seg_aggregate_slots<d>(mx, ne, lane, r, zq, zl, noprev, slots, a.nseg, s, ts);    \

@@ -1,15 +1,15 @@
 #!/usr/bin/env bash
 # cfg 5 (batched transforms) check + profile, run on the GPU box:
-#   1. the parity tests that cover the wide / batched kernels,
+#   1. the parity tests that cover the wide / batched kernels (skipped with QUICK=1),
 #   2. bench.py --config 5 (one line per tolerance; kernels_ms = K1 / K2 / K3),
 #   3. with NCU=1: ncu --set full of the wide kernels on 512 transforms at tol 1e-10
 #      (gpurun_out/cfg5/wide.ncu-rep; read with tools/ncu_kstat.py, tools/ncu_lines.py).
 set -u
 OUT=gpurun_out/cfg5
 mkdir -p $OUT
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_random.py tests/test_gpu_large.py -m gpu -x -q \
+[ "${QUICK:-0}" = "1" ] || python -m pytest tests/test_gpu_parity.py tests/test_gpu_random.py tests/test_gpu_large.py -m gpu -x -q \
     -k "batch or cfg5 or wide or random or mode_sums or cfg4" > $OUT/pytest.log 2>&1
-tail -3 $OUT/pytest.log
+[ "${QUICK:-0}" = "1" ] || tail -3 $OUT/pytest.log
 python bench.py --config 5 --steps 10 --warmup 3 --tols ${TOLS:-1e-3,1e-6,1e-10} > $OUT/cfg5.jsonl 2> $OUT/cfg5.err
 python - <<'PY'
 import json
