@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(kSortThreads)
   }
 }
 
-// ---- generic exclusive scan of uint32 (values fit: counts <= 2^32) --------
+// ---- block-wide exclusive scan of uint32 (values fit: counts <= 2^32) -----
 constexpr int kScanBlock = 1024;
 constexpr int kScanItems = 8;
 constexpr int kScanChunk = kScanBlock * kScanItems;
@@ -232,67 +232,38 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* total)
   return r;
 }
 
+// The scatter offsets of one pass in one launch: CTA d scans the tile counts
+// of digit d (cnt is digit-major) on top of the digit's base, the number of
+// keys with a smaller digit (from the global histogram of the pass).
 __global__ void __launch_bounds__(kScanBlock)
-    sort_scan_reduce_kernel(const uint32_t* __restrict__ in, int64_t n, uint32_t* __restrict__ sums) {
+    digit_scan_kernel(const uint32_t* __restrict__ cnt, int64_t ntiles,
+                      const unsigned long long* __restrict__ hist, uint32_t* __restrict__ offs) {
   __shared__ unsigned tot;
-  const int64_t base = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kScanItems;
-  unsigned s = 0;
+  const int d = blockIdx.x;
+  const unsigned hb = (int)threadIdx.x < d ? (unsigned)hist[threadIdx.x] : 0u;
+  block_excl_scan(hb, &tot);
+  unsigned run = tot;
+  const uint32_t* in = cnt + (int64_t)d * ntiles;
+  uint32_t* out = offs + (int64_t)d * ntiles;
+  for (int64_t c0 = 0; c0 < ntiles; c0 += kScanChunk) {
+    const int64_t base = c0 + (int64_t)threadIdx.x * kScanItems;
+    unsigned v[kScanItems];
+    unsigned s = 0;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i)
-    if (base + i < n) s += in[base + i];
-  block_excl_scan(s, &tot);
-  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(kScanBlock)
-    sort_scan_apply_kernel(const uint32_t* __restrict__ in, int64_t n,
-                      const uint32_t* __restrict__ block_off, uint32_t* __restrict__ out) {
-  __shared__ unsigned tot;
-  const int64_t base = (int64_t)blockIdx.x * kScanChunk + (int64_t)threadIdx.x * kScanItems;
-  unsigned v[kScanItems];
-  unsigned s = 0;
+    for (int i = 0; i < kScanItems; ++i) {
+      v[i] = base + i < ntiles ? in[base + i] : 0u;
+      s += v[i];
+    }
+    unsigned r = run + block_excl_scan(s, &tot);
+    run += tot;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    v[i] = base + i < n ? in[base + i] : 0u;
-    s += v[i];
-  }
-  unsigned run = block_excl_scan(s, &tot) + (block_off ? block_off[blockIdx.x] : 0u);
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    if (base + i < n) out[base + i] = run;
-    run += v[i];
+    for (int i = 0; i < kScanItems; ++i) {
+      if (base + i < ntiles) out[base + i] = r;
+      r += v[i];
+    }
   }
 }
-
-// Exclusive scan, recursive over chunk sums.  tmp must hold scan_tmp_elems(n).
-cudaError_t excl_scan_u32(const uint32_t* in, int64_t n, uint32_t* out, uint32_t* tmp,
-                          cudaStream_t st) {
-  if (n <= 0) return cudaSuccess;
-  const int64_t nb = (n + kScanChunk - 1) / kScanChunk;
-  note_launch(nb == 1 ? 1 : 2);
-  if (nb == 1) {
-    sort_scan_apply_kernel<<<1, kScanBlock, 0, st>>>(in, n, nullptr, out);
-    return cudaGetLastError();
-  }
-  uint32_t* sums = tmp;
-  uint32_t* sums_scanned = tmp + nb;
-  sort_scan_reduce_kernel<<<(unsigned)nb, kScanBlock, 0, st>>>(in, n, sums);
-  cudaError_t e = excl_scan_u32(sums, nb, sums_scanned, tmp + 2 * nb, st);
-  if (e != cudaSuccess) return e;
-  sort_scan_apply_kernel<<<(unsigned)nb, kScanBlock, 0, st>>>(in, n, sums_scanned, out);
-  return cudaGetLastError();
-}
-
-int64_t scan_tmp_elems(int64_t n) {
-  int64_t total = 0;
-  while (true) {
-    const int64_t nb = (n + kScanChunk - 1) / kScanChunk;
-    if (nb <= 1) break;
-    total += 2 * nb;
-    n = nb;
-  }
-  return total + 16;
-}
+static_assert(kScanBlock >= kRadix, "digit_scan_kernel: one thread per smaller digit");
 
 inline unsigned grid_for(int64_t n, int bs) {
   int64_t g = (n + bs - 1) / bs;
@@ -309,7 +280,6 @@ size_t radix_sort_workspace_bytes(int64_t n) {
   b += 2 * sizeof(uint64_t) * (size_t)n;                 // keys x2
   b += 2 * sizeof(uint32_t) * (size_t)n;                 // vals x2
   b += 2 * sizeof(uint32_t) * (size_t)(ntiles * kRadix); // cnt + offs
-  b += sizeof(uint32_t) * (size_t)scan_tmp_elems(ntiles * kRadix);
   b += sizeof(unsigned long long) * 8 * kRadix;
   return b + 16 * 256;  // 8 regions, each re-aligned to 256 B
 }
@@ -321,7 +291,7 @@ static inline char* align_up(char* p) {
 // Workspace layout of one sort.
 struct SortWs {
   uint64_t *k0, *k1;
-  uint32_t *v0, *v1, *cnt, *offs, *stmp;
+  uint32_t *v0, *v1, *cnt, *offs;
   unsigned long long* hist8;
 };
 static SortWs sort_ws(void* workspace, int64_t n) {
@@ -334,7 +304,6 @@ static SortWs sort_ws(void* workspace, int64_t n) {
   w.v1 = (uint32_t*)p; p = align_up(p + sizeof(uint32_t) * n);
   w.cnt = (uint32_t*)p; p = align_up(p + sizeof(uint32_t) * ntiles * kRadix);
   w.offs = (uint32_t*)p; p = align_up(p + sizeof(uint32_t) * ntiles * kRadix);
-  w.stmp = (uint32_t*)p; p = align_up(p + sizeof(uint32_t) * scan_tmp_elems(ntiles * kRadix));
   w.hist8 = (unsigned long long*)p;
   return w;
 }
@@ -399,8 +368,9 @@ cudaError_t radix_sort_end(const double* x, int64_t n, double* sorted, int32_t* 
     else
       tile_hist_kernel<false><<<(unsigned)ntiles, kSortThreads, 0, st>>>(kin, nullptr, n, shift,
                                                                          w.cnt, ntiles);
-    e = excl_scan_u32(w.cnt, ntiles * kRadix, w.offs, w.stmp, st);
-    if (e != cudaSuccess) return e;
+    note_launch();
+    digit_scan_kernel<<<kRadix, kScanBlock, 0, st>>>(w.cnt, ntiles, w.hist8 + passes[q] * kRadix,
+                                                     w.offs);
     if (first && last)
       e = scatter_pass<true, true>(nullptr, nullptr, x, n, shift, w.offs, ntiles, nullptr, nullptr,
                                    sorted, perm, st);
