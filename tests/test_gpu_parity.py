@@ -563,6 +563,34 @@ def test_batched_mixed_segment_classes():
         check(out[b], oracle.transform(xs[b], ys[b], al[b], d, ne=len(soe), mode=0), al[b])
 
 
+@pytest.mark.parametrize("nmodes", [1, 2, 5, 7, 8])
+def test_custom_mode_counts_all_segment_classes(nmodes):
+    """Folded SOEs with 1..8 modes (kMaxModes = 8; the presets have 3..7): every
+    instantiated mode count of the lane-collapsed wide kernels, on deltas that
+    put segments in the narrow (moment), lane-collapsed and per-mode classes,
+    as single plans and as one batched plan.  The modes are the folded modes of
+    the n = 14 and n = 12 tables (no longer a Gaussian approximation: parity
+    with the oracle on the same modes is the bar)."""
+    t7, w7 = oracle.folded_table(14)
+    t6, w6 = oracle.folded_table(12)
+    t = np.concatenate([t7, t6[:1]])[:nmodes]
+    mw = np.concatenate([w7, w6[:1]])[:nmodes]
+    # mw carries the fold multiplier 2 of a conjugate pair (halving is exact)
+    soe = fgt.SoeApprox(list(t), list(0.5 * mw), fgt.SoeForm.FOLDED, [0] * nmodes)
+    n = 20000
+    deltas = [1.0, 1e-3, 1e-5, 3e-7, 1e-9, 1e-12]
+    xs = [np.sort(up(n, 700 + b, 3)) for b in range(len(deltas))]
+    ys = [np.sort(up(n + 37, 700 + b, 0)) for b in range(len(deltas))]
+    al = [2.0 * up(n + 37, 700 + b, 1) - 1.0 for b in range(len(deltas))]
+    refs = [oracle.transform(xs[b], ys[b], al[b], d, mode=0, soe=(t, mw))
+            for b, d in enumerate(deltas)]
+    for b, d in enumerate(deltas):
+        check(gpu_transform(xs[b], ys[b], al[b], d, None, mode=0, soe=soe), refs[b], al[b])
+    out = fgt.batch_transform(xs, ys, al, deltas, soe)
+    for b in range(len(deltas)):
+        check(out[b], refs[b], al[b])
+
+
 def test_batched_rejects_unsorted_and_reuses_plan():
     soe = fgt.fold(fgt.cf_soe(8))
     with pytest.raises(ValueError):
