@@ -3158,8 +3158,11 @@ constexpr int kScanThreads = FGT_SCAN_THREADS;
 #ifndef FGT_K3N_WAVES
 #define FGT_K3N_WAVES 32
 #endif
+// (wide: segment costs differ by the lane-run degree, 4 .. 16, so smaller
+// ranges per CTA balance better: cfg 5 K3 10.75 ms at 32 waves, 10.41 at 128,
+// 10.43 at 256, 10.62 at 512, 11.2 at 8)
 #ifndef FGT_K3W_WAVES
-#define FGT_K3W_WAVES 32
+#define FGT_K3W_WAVES 128
 #endif
 #ifndef FGT_K1_GRID
 #define FGT_K1_GRID 64
