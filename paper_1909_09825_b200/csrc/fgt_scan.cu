@@ -3158,14 +3158,22 @@ constexpr int kScanThreads = FGT_SCAN_THREADS;
 #ifndef FGT_K3N_WAVES
 #define FGT_K3N_WAVES 32
 #endif
-// (wide: segment costs differ by the lane-run degree, 4 .. 16, so smaller
-// ranges per CTA balance better: cfg 5 K3 10.75 ms at 32 waves, 10.41 at 128,
-// 10.43 at 256, 10.62 at 512, 11.2 at 8)
 #ifndef FGT_K3W_WAVES
-#define FGT_K3W_WAVES 128
+#define FGT_K3W_WAVES 32
+#endif
+// (batched plans: segment costs differ by the lane-run degree, 4 .. 16, so
+// smaller ranges per CTA balance better: cfg 5 K3 10.75 ms at 32 waves, 10.41
+// at 128, 10.43 at 256, 10.62 at 512, 11.2 at 8)
+#ifndef FGT_K3W_WAVES_BATCH
+#define FGT_K3W_WAVES_BATCH 128
 #endif
 #ifndef FGT_K1_GRID
 #define FGT_K1_GRID 64
+#endif
+// batched plans: segment costs vary from transform to transform (their own
+// delta), so the grids are finer (cfg 5 K1: 4.09 ms at 64, 4.00 at 256)
+#ifndef FGT_K1_GRID_BATCH
+#define FGT_K1_GRID_BATCH 256
 #endif
 #ifndef FGT_K3_GRID
 #define FGT_K3_GRID 64
@@ -4077,7 +4085,7 @@ cudaError_t launch_aggregate(const StreamArgs& a, const ModeParams& P, const Mod
   if (a.nseg == 0) return cudaSuccess;
   const int64_t per_cta = (int64_t)kSegWarps * (a.mtb ? kBatchGroup : 1);
   int64_t want = (a.nseg + per_cta - 1) / per_cta;
-  const int64_t cap = (int64_t)num_sms() * FGT_K1_GRID;
+  const int64_t cap = (int64_t)num_sms() * (a.mtb ? FGT_K1_GRID_BATCH : FGT_K1_GRID);
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   const size_t smem = sizeof(ModeTable) * (a.mtb ? kSegWarps : 1);
   if (a.nwide1 != 0) {
@@ -4151,7 +4159,8 @@ static cudaError_t launch_seg_main_variant(const StreamArgs& a, const ModeParams
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     want = (a.nseg + kSegWarps - 1) / kSegWarps;
-    cap = (int64_t)num_sms() * per_sm * (WIDE ? FGT_K3W_WAVES : FGT_K3N_WAVES);
+    cap = (int64_t)num_sms() * per_sm *
+          (WIDE ? (a.mtb ? FGT_K3W_WAVES_BATCH : FGT_K3W_WAVES) : FGT_K3N_WAVES);
   }
   const unsigned grid = (unsigned)(want < cap ? want : cap);
   note_launch();
