@@ -413,7 +413,10 @@ def main():
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # a process group also at world 1 when FGT_BENCH_FORCE_PG is set (test hook:
+    # the collectives of the multi-rank path then run over NCCL on one GPU)
+    pg = world > 1 or bool(os.environ.get("FGT_BENCH_FORCE_PG"))
+    if pg:
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
@@ -485,7 +488,7 @@ def main():
 
     def gather_dev(t, out):
         """all_gather of this rank's device aggregates into `out` (device)."""
-        if world == 1:
+        if not pg:
             out.copy_(t)
         elif backend == "nccl":
             dist.all_gather_into_tensor(out, t)
@@ -522,7 +525,7 @@ def main():
         L.fgt_plan_destroy(h)
 
     def barrier():
-        if world > 1:
+        if pg:
             if backend == "nccl":
                 dist.barrier(device_ids=[local])
             else:
@@ -540,7 +543,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ms = e0.elapsed_time(e1) / steps
-        if world > 1:
+        if pg:
             ms = reduce_max(ms)
         return ms
 
@@ -569,7 +572,7 @@ def main():
     if args.check and (world > 1 or args.chunk_path):
         def allgather_cpu(t):
             """all_gather of equal-size CPU tensors over either backend."""
-            if world == 1:
+            if not pg:
                 return [t]
             src = t.to(dev) if backend == "nccl" else t
             parts = [torch.zeros_like(src) for _ in range(world)]
@@ -783,7 +786,7 @@ def main():
         if mr_check is not None:
             line["multi_rank_check"] = mr_check
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if pg:
         dist.destroy_process_group()
 
 

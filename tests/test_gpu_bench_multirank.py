@@ -59,6 +59,25 @@ def test_bench_chunk_path_single_rank():
     assert d["multi_rank_check"]["pass"], d["multi_rank_check"]
 
 
+def test_bench_chunk_path_over_nccl_world_one():
+    """The multi-rank step with its collectives over the real backend: torchrun
+    with one rank, a forced NCCL process group (FGT_BENCH_FORCE_PG), so the
+    aggregate all_gather_into_tensor, the device-id barrier, the max-over-ranks
+    all_reduce and the check's all_gather run through NCCL on the box's GPU."""
+    if _capi.lib().fgt_device_count() < 1:
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+    env = dict(os.environ, FGT_BENCH_FORCE_PG="1")
+    env.pop("FGT_BENCH_BACKEND", None)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", "bench.py", "--gpus", "1",
+           "--steps", "2", "--warmup", "1", "--size", "400000", "--no-cpu-baseline",
+           "--no-sweep", "--no-e2e", "--chunk-path", "--check"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert d["multi_rank_check"]["pass"], d["multi_rank_check"]
+
+
 @pytest.mark.parametrize("world", [1, 2])
 def test_bench_cfg5_transforms_split_over_ranks(world):
     """--config 5 under torchrun: the batched transforms split over the ranks
