@@ -1196,7 +1196,7 @@ __device__ __forceinline__ void lane_collapsed(const ModeTable& mt, int ne, int 
     }
 #pragma unroll
     for (int q = 0; q < NP; ++q) acc[q] = gtop;
-#pragma unroll 1
+#pragma unroll 4
     for (int n = DL - 1; n >= 0; --n) {
       const double gn = mt.gl[n];
 #pragma unroll
