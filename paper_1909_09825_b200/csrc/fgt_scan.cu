@@ -1006,7 +1006,7 @@ __device__ __noinline__ void lane_slot_scan(cplx* slots, int ne, int lane, cplx 
   const int step = fwd ? SK : -SK;
   int at = fwd ? 0 : 31 * SK;
   cplx S = seed;
-#pragma unroll 8
+#pragma unroll 4
   for (int i = 0; i < 32; ++i) {
     const cplx a = sA[at];
     const cplx f = sS[at];
