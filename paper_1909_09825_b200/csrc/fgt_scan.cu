@@ -2764,10 +2764,10 @@ struct TileCtx {
 #define FGT_PLAN_MINB 6
 #endif
 // Merged positions per thread: one per segment of the tile, so a tile of
-// kPlanSegs segments has kSeg threads.  An odd window (15) spreads the
+// kPlanSegs segments has kSeg threads.  An odd window spreads the
 // threads' merge reads over the shared-memory banks (the window starts are
-// ~7.5 doubles apart in each set; an even window of 16 put them 8 doubles =
-// 64 bytes apart, i.e. on the same banks).
+// about kPlanPer / 2 doubles apart in each set; an even window of 16 put
+// them 8 doubles = 64 bytes apart, i.e. on the same banks).
 constexpr int kPlanPer = kPlanSegs;
 constexpr int kPlanThreads = kSeg;
 constexpr int kPlanWords = kPlanTile / 32;  // merge-mask words per tile

@@ -21,8 +21,10 @@ constexpr int kSeg = 32 * kR;           // merged elements per segment (one warp
 constexpr int kSegWarps = FGT_SEG_WARPS;  // segments (warps) per CTA in K1 / K3
 constexpr int kThreads = 32 * kSegWarps;
 constexpr int kMaxMom = kMaxDeg;        // highest moment order of the expansions
+// (21: the largest odd tile that keeps 5 CTAs per SM in the tile pass; cfg 3
+// plan + other 0.563 ms at 15, 0.545 at 19, 0.52-0.53 at 21, 0.556 at 23, 0.537 at 25)
 #ifndef FGT_PLAN_SEGS
-#define FGT_PLAN_SEGS 15
+#define FGT_PLAN_SEGS 21
 #endif
 constexpr int kPlanSegs = FGT_PLAN_SEGS;  // segments per plan tile
 constexpr int kPlanTile = kPlanSegs * kSeg;  // merged elements per plan tile

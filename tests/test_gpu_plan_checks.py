@@ -21,7 +21,7 @@ from paper_1909_09825_b200.transform import uniform_points_array as up
 
 pytestmark = pytest.mark.gpu
 PD = ctypes.POINTER(ctypes.c_double)
-N_BIG = 200_003  # ~52 plan tiles of 3840 merged elements
+N_BIG = 200_003  # ~37 plan tiles of 5376 merged elements (21 segments)
 
 
 @pytest.fixture(scope="module")
