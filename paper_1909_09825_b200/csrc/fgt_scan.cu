@@ -53,6 +53,60 @@ __device__ __forceinline__ int64_t merge_path(Ptr x, int64_t nx, Ptr y, int64_t 
   return lo;
 }
 
+// The same split from a proportional guess (diag nx / (nx + ny): exact for
+// evenly interleaved sets, within ~sqrt(diag) for random ones): gallop from
+// the guess in doubling steps to bracket the answer, then bisect the bracket
+// -- about 17 dependent loads instead of 27 at 2e8 elements, and at most
+// kGallop + 1 more than the bisection's on any data.  The predicate is the
+// bisection's, so on sorted input the result is identical.
+template <class Ptr>
+__device__ __forceinline__ int64_t merge_path_guess(Ptr x, int64_t nx, Ptr y, int64_t ny,
+                                                    int64_t diag) {
+  int64_t lo = diag - ny > 0 ? diag - ny : 0;
+  int64_t hi = diag < nx ? diag : nx;
+  if (lo >= hi) return lo;
+  // pred(mid), lo < mid <= hi: the split is at or above mid
+  auto pred = [&](int64_t mid) { return x[mid - 1] < y[diag - mid]; };
+  int64_t g = (int64_t)((double)diag * ((double)nx / (double)(nx + ny)));
+  g = g < lo ? lo : (g > hi ? hi : g);
+  int64_t step = 1024;
+  // (at most kGallop doubling steps: beyond 1024 * 2^kGallop elements from the
+  // guess the remaining range is bisected as it is)
+  constexpr int kGallop = 6;
+  if (g > lo && pred(g)) {
+    lo = g;
+    for (int k = 0; k < kGallop && lo < hi; ++k) {
+      const int64_t p = lo + step < hi ? lo + step : hi;
+      if (pred(p)) {
+        lo = p;
+        step <<= 1;
+      } else {
+        hi = p - 1;
+        break;
+      }
+    }
+  } else {
+    if (g > lo) hi = g - 1;
+    for (int k = 0; k < kGallop && lo < hi; ++k) {
+      const int64_t p = hi - step + 1 > lo + 1 ? hi - step + 1 : lo + 1;
+      if (pred(p)) {
+        lo = p;
+        break;
+      }
+      hi = p - 1;
+      step <<= 1;
+    }
+  }
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (pred(mid))
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
 // Coefficients of one mode: held in registers up to degree kRegDeg, read
 // from shared memory (broadcast) above it to bound register pressure.
 constexpr int kRegDeg = 8;
@@ -2733,7 +2787,7 @@ __global__ void partition_kernel(const double* __restrict__ xs, int64_t M,
   if (t > nseg) return;
   int64_t diag = t * seg;
   if (diag > M + N) diag = M + N;
-  seg_ib[t] = merge_path(xs, M, ys, N, diag);
+  seg_ib[t] = merge_path_guess(xs, M, ys, N, diag);
 }
 
 // Plan-time tile pass (one CTA per tile of kPlanTile merged elements,
